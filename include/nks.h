@@ -1,0 +1,203 @@
+/*
+ * nks.h -- C ABI of the B200 (sm_100a) Newton-Krylov-Schwarz time step of arXiv 2209.08001.
+ *
+ * The library solves, once per time step, the nonlinear system F(X^{n+1}; X^n, dt) = 0 of the
+ * discrete-variational-derivative scheme NSOA-1 (Eq. NSOA-1) for the
+ * reduced Ni-alloy phase-field model: composition c, one long-range order parameter eta and the
+ * quasi-static displacement u_1..u_d.  Method (Sec. 4):
+ * inexact Newton with line search, restarted right-preconditioned GMRES, restricted additive
+ * Schwarz (left-RAS, Cai-Sarkis) with point-block ILU(0) subdomain solves, adaptive dt (Eq.
+ * sencondt).  All arithmetic is fp64 on the device; the host only steers.
+ *
+ * Conventions
+ *   - Field layout at the ABI: field-major arrays (c, then eta, then u_1..u_d), each field in C
+ *     order over (z, y, x) with x fastest, no halo, n[0]*n[1]*n[2] points per field.  u_I is the
+ *     displacement component along axis I (I = 1 is x).
+ *   - "on_device" = 1: the pointer is a CUDA device pointer on the state's device; 0: host memory.
+ *   - Every call returns nks_status (NKS_OK = 0); no C++ exception crosses the ABI; the per-state
+ *     message of the last failure is returned by nks_last_error().
+ *   - Ownership: the caller owns every array, info struct and the workspace, which must outlive
+ *     the state; the library keeps no caller pointer past return except the workspace.  The
+ *     library owns the events/plans it creates and destroys them in nks_destroy().
+ *   - Threading: one state per stream; no global mutable state.  Calls on one state must not
+ *     overlap.
+ *   - Determinism: every reduction is a fixed-order two-stage tree; results are bitwise
+ *     reproducible for a given grid, params and launch configuration.
+ */
+#ifndef NKS_H
+#define NKS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define NKS_API __attribute__((visibility("default")))
+#else
+#define NKS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  NKS_OK = 0,
+  NKS_E_INVALID = 1,   /* bad argument: grid/params out of range, NULL pointer, size mismatch   */
+  NKS_E_DOMAIN = 2,    /* state inadmissible: c, p = c*eta or q = c*(4-3*eta) not in (0,1), NaN */
+  NKS_E_DIVERGED = 3,  /* Newton max-its, line-search failure or GMRES max-its (reading R24)     */
+  NKS_E_CUDA = 4,      /* CUDA / cuFFT runtime error (message in nks_last_error)                */
+  NKS_E_NCCL = 5,      /* reserved for the multi-GPU communicator                               */
+  NKS_E_OOM = 6,       /* workspace too small                                                   */
+  NKS_E_STATE = 7      /* call order violated (e.g. nks_step before nks_set_fields)            */
+} nks_status;
+
+/* Divergence reasons reported in nks_step_info.reason. */
+enum { NKS_REASON_NONE = 0, NKS_REASON_NEWTON_MAXIT = 1, NKS_REASON_LINE_SEARCH = 2,
+       NKS_REASON_GMRES_MAXIT = 3, NKS_REASON_DOMAIN = 4, NKS_REASON_DT_FLOOR = 5 };
+
+/* Preconditioner types. */
+enum { NKS_PC_NONE = 0, NKS_PC_RAS_BILU0 = 2 };
+
+typedef struct {
+  int32_t dim;       /* 2 or 3                                                          */
+  int32_t n[3];      /* grid points per axis, n[0] = x (fastest); n[2] = 1 when dim == 2.       */
+                     /* Periodic.  Each n[j] >= 5 (stencil radius 2 must not alias).    */
+  double h;          /* uniform mesh size (0.25)                                         */
+  int32_t nsub[3];   /* RAS subdomain boxes per axis (1 <= nsub[j] <= n[j]); nsub[2]=1 in 2D     */
+  int32_t overlap;   /* delta: cells added on each side of every box (0..8)      */
+} nks_grid;
+
+typedef struct {
+  /* ---- model, dimensionless (App. A/B).  CALPHAD-style coefficients in units of
+   *      V_m*dE; the library derives M0..M6 of App. B from them.              */
+  double theta;      /* theta of E_G                                                 */
+  double gamma_c;    /* gradient coefficient of c                                       */
+  double gamma_eta;  /* gradient coefficient of eta (enters as 3*gamma_eta)              */
+  double kappa;      /* mobility scale, M = kappa c(1-c)                       */
+  double eps0;       /* eigenstrain coefficient                                 */
+  double C11, C12, C44;   /* cubic Hooke tensor                                  */
+  double Lscale;     /* multiplier of the Hooke tensor, script-L of P:634                      */
+  double w_c;        /* weight of theta*Psi(c) in E_G: 1 = main text P:66 (reading R2)         */
+  double L0, L1, L2, L3, U1, U4;   /* App. A/B coefficients / (V_m dE)                          */
+  double dE0;        /* (E0_Al - E0_Ni)/(V_m dE): M0 = dE0 + L0 - L1 + L2 - L3         */
+  int32_t S;         /* Taylor order of Psi_S (10); 1..16                    */
+  /* ---- Newton / GMRES (readings R16-R18, R24) */
+  double newton_rtol, newton_atol;   /* stop when ||F|| <= max(rtol*||F0||, atol) */
+  double gmres_rtol, gmres_atol;     /* ||J S + F|| <= max(rtol*||F||, atol) */
+  int32_t newton_maxit;              /* > this many Newton iterations -> DIVERGED             */
+  int32_t gmres_restart;             /* GMRES(m) restart length, 1..64                        */
+  int32_t gmres_maxit;               /* total GMRES iterations per Newton solve -> DIVERGED    */
+  int32_t pc_type;                   /* NKS_PC_NONE or NKS_PC_RAS_BILU0                       */
+  int32_t pc_reuse;                  /* 0: refactor every Newton iterate; 1: once per step;    */
+                                     /* 2: keep factors across steps while dt is unchanged     */
+  double ls_alpha;                   /* sufficient decrease ||F(X+lS)|| <= (1-alpha l)||F||    */
+  int32_t ls_max_halvings;           /* lambda = 1, 1/2, ... 2^-max before line-search failure */
+  /* ---- adaptive controller (Eq. sencondt; readings R23/R24) */
+  double zeta, dt_min, dt_max, dt_init;
+  double dt_floor_factor;            /* abort when the retried dt < dt_min * factor            */
+  int32_t xd_norm;                   /* ||X^n - X^{n-1}||: 0 RMS, 1 Euclidean, 2 (c,eta) Eucl. */
+} nks_params;
+
+typedef struct {
+  int32_t converged;        /* 1 if the step was accepted                                      */
+  int32_t reason;           /* NKS_REASON_* of the last failure                               */
+  int32_t newton_its;       /* Newton iterations of the accepted attempt                       */
+  int32_t gmres_its;        /* GMRES iterations summed over those Newton iterations            */
+  int32_t retries;          /* dt halvings by sqrt(2) before acceptance (nks_run_adaptive)     */
+  int32_t ls_halvings;      /* line-search halvings summed over the Newton iterations          */
+  int32_t pc_setups;        /* preconditioner (re)factorisations in this step                  */
+  int32_t pad_;
+  double dt;                /* accepted dt                                                     */
+  double time;              /* t_{n+1}                                                         */
+  double energy;            /* discrete free energy E~^{n+1}, cell volume h^d      */
+  double energy_parts[4];   /* E~1..E~4                                                        */
+  double mass;              /* h^d sum c                                               */
+  double fnorm0, fnorm;     /* ||F(X_0)||, ||F(X_final)||                                      */
+  double zeta;              /* controller zeta after the step (doubles on every retry)  */
+  double xd;                /* X'_d used to predict this step's dt (0 for the first step)      */
+} nks_step_info;
+
+typedef struct nks_state nks_state;
+
+/* Bytes of device workspace nks_create needs for this grid/params (0 on invalid input). */
+NKS_API size_t nks_workspace_bytes(const nks_grid* grid, const nks_params* params);
+
+/* Create a single-GPU state on the current CUDA device.
+ *   workspace: device buffer of >= nks_workspace_bytes() bytes, 256-byte aligned, caller-owned
+ *              (PyTorch allocates it); must outlive the state.
+ *   cuda_stream: cudaStream_t on which every kernel of this state is launched (NULL = legacy).
+ * Errors: NKS_E_INVALID (grid/params), NKS_E_OOM (workspace too small), NKS_E_CUDA. */
+NKS_API nks_status nks_create(const nks_grid* grid, const nks_params* params, void* workspace,
+                      size_t workspace_bytes, void* cuda_stream, nks_state** out);
+
+/* Set X^n.  c, eta: N doubles each; u: d*N doubles (u_1 block first) or NULL, in which case
+ * u^0 solves the discrete mechanical equilibrium [D^ sigma^el]^0 = 0 (reading R13)
+ * by an fp64 FFT.  Sets cbar0 = mean(c) and projects u onto the canonical gauge
+ * (zero mean per component and parity sub-lattice, reading R14).  Resets time, step history,
+ * zeta and cached factors.  NKS_E_DOMAIN if the state is inadmissible. */
+NKS_API nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, const double* u,
+                          int32_t on_device);
+
+/* Copy X^n out (same layout as nks_set_fields; u must hold d*N doubles). */
+NKS_API nks_status nks_get_fields(const nks_state* st, double* c, double* eta, double* u, int32_t on_device);
+
+/* One NKS time step X^n -> X^{n+1} with the given dt.
+ * Transactional: on failure X^n is unchanged, status NKS_E_DIVERGED / NKS_E_DOMAIN and
+ * info->reason tell why.  info may be NULL. */
+NKS_API nks_status nks_step(nks_state* st, double dt, nks_step_info* info);
+
+/* Adaptive time stepping (Eq. sencondt): up to max_steps accepted steps, stopping
+ * early once time >= t_end (t_end <= 0: no time limit).  Step 0 uses dt_init; a diverged
+ * attempt retries with dt/sqrt(2) and zeta*2; aborts with NKS_E_DIVERGED when dt would drop
+ * below dt_min*dt_floor_factor.  per_step: array of max_steps records (or NULL); *done receives
+ * the number of accepted steps. */
+NKS_API nks_status nks_run_adaptive(nks_state* st, int32_t max_steps, double t_end,
+                            nks_step_info* per_step, int32_t* done);
+
+/* Discrete energy parts E~1..E~4 and mass of X^n. */
+NKS_API nks_status nks_energy(nks_state* st, double parts[4], double* mass);
+
+/* ---- test / benchmark hooks on the current X^n (level a) --------------------------------- */
+
+/* F(x_b) of Eq. NSOA-1 for level a = X^n: x_b and F hold (2+d)*N doubles. */
+NKS_API nks_status nks_eval_residual(nks_state* st, double dt, const double* x_b, double* F, int32_t on_device);
+
+/* J(x_b) v (matrix-free analytic Jacobian). */
+NKS_API nks_status nks_eval_jv(nks_state* st, double dt, const double* x_b, const double* v, double* Jv,
+                       int32_t on_device);
+
+/* Assemble and factor the RAS/BILU(0) preconditioner at x_b, then z = M^{-1} r. */
+NKS_API nks_status nks_pc_setup(nks_state* st, double dt, const double* x_b, int32_t on_device);
+NKS_API nks_status nks_pc_apply(nks_state* st, const double* r, double* z, int32_t on_device);
+
+/* Solve J(x_b) s = rhs by the library's right-preconditioned GMRES (after nks_pc_setup when
+ * pc_type != NONE) to ||J s - rhs|| <= max(gmres_rtol ||rhs||, gmres_atol).  *its receives the
+ * iteration count.  NKS_E_DIVERGED at gmres_maxit. */
+NKS_API nks_status nks_gmres_solve(nks_state* st, double dt, const double* x_b, const double* rhs, double* s,
+                           int32_t on_device, int32_t* its);
+
+/* Launch counters of this state since creation (kernels issued by the library). */
+NKS_API nks_status nks_counters(const nks_state* st, int64_t* kernel_launches, int64_t* host_syncs);
+
+/* Phase profiling with CUDA events recorded on the state's stream around every launch of a
+ * phase: [0] residual F, [1] J.v, [2] RAS apply, [3] assembly, [4] BILU(0) factorisation,
+ * [5] GMRES vector ops, [6] reductions (norms, energy, gauge), [7] other.
+ * nks_set_profiling(st, 1) enables recording (it costs two event records per launch);
+ * nks_phase_times synchronises the stream and returns accumulated ms and launch counts;
+ * reset = 1 clears the accumulators afterwards. */
+NKS_API nks_status nks_set_profiling(nks_state* st, int32_t enable);
+NKS_API nks_status nks_phase_times(nks_state* st, double ms[8], int64_t counts[8], int32_t reset);
+
+NKS_API nks_status nks_destroy(nks_state* st);
+
+/* Message of the last failure on this state ("" if none); valid until the next call. */
+NKS_API const char* nks_last_error(const nks_state* st);
+
+/* Library version string. */
+NKS_API const char* nks_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NKS_H */

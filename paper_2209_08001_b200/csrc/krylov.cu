@@ -1,0 +1,185 @@
+// GMRES vector kernels (K7): fused multi-dot, fused update + re-orthogonalisation dots, fused
+// update + normalise, linear combination, axpy.  Classical Gram-Schmidt with one
+// re-orthogonalisation (CGS2), all dot products of one Arnoldi step reduced in fixed order
+// (deterministic) and read by the host once per iteration.
+#include "nks_internal.cuh"
+
+namespace nks {
+
+struct Coefs {
+  double c[64];
+};
+
+template <int NV>
+__device__ __forceinline__ void block_reduce_k(double (&vals)[NV]) {
+  __shared__ double sred[NV][kRedThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double v = vals[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sred[k][wid] = v;
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double v = lane < (int)(blockDim.x >> 5) ? sred[k][lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      vals[k] = v;
+    }
+  }
+  __syncthreads();
+}
+
+// part[b][k] = sum_i V_k[i] w[i] (k < nk), part[b][nk] = sum_i w[i]^2.
+template <int NK>
+__global__ void __launch_bounds__(kRedThreads) k_mdot(long long n, int nk, const double* __restrict__ V, long long ld,
+                                                      const double* __restrict__ w, double* __restrict__ part) {
+  double acc[NK + 1];
+#pragma unroll
+  for (int k = 0; k <= NK; ++k) acc[k] = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double wi = w[i];
+#pragma unroll
+    for (int k = 0; k < NK; ++k)
+      if (k < nk) acc[k] = fma(__ldg(V + k * ld + i), wi, acc[k]);
+    acc[NK] = fma(wi, wi, acc[NK]);
+  }
+  block_reduce_k<NK + 1>(acc);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < nk; ++k) part[blockIdx.x * (nk + 1) + k] = acc[k];
+    part[blockIdx.x * (nk + 1) + nk] = acc[NK];
+  }
+}
+
+// w -= sum_k h[k] V_k (h on device), then part = [V^T w_new, |w_new|^2].
+template <int NK>
+__global__ void __launch_bounds__(kRedThreads) k_update_dot(long long n, int nk, const double* __restrict__ V, long long ld,
+                                                            const double* __restrict__ h, double* __restrict__ w,
+                                                            double* __restrict__ part) {
+  __shared__ double sh[NK];
+  if (threadIdx.x < nk) sh[threadIdx.x] = h[threadIdx.x];
+  __syncthreads();
+  double acc[NK + 1];
+#pragma unroll
+  for (int k = 0; k <= NK; ++k) acc[k] = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double vk[NK];
+    double wi = w[i];
+#pragma unroll
+    for (int k = 0; k < NK; ++k)
+      if (k < nk) { vk[k] = __ldg(V + k * ld + i); wi = fma(-sh[k], vk[k], wi); }
+    w[i] = wi;
+#pragma unroll
+    for (int k = 0; k < NK; ++k)
+      if (k < nk) acc[k] = fma(vk[k], wi, acc[k]);
+    acc[NK] = fma(wi, wi, acc[NK]);
+  }
+  block_reduce_k<NK + 1>(acc);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < nk; ++k) part[blockIdx.x * (nk + 1) + k] = acc[k];
+    part[blockIdx.x * (nk + 1) + nk] = acc[NK];
+  }
+}
+
+// w = (w - sum_k h[k] V_k) * scale
+template <int NK>
+__global__ void k_update_scale(long long n, int nk, const double* __restrict__ V, long long ld,
+                               const double* __restrict__ h, double scale, double* __restrict__ w) {
+  __shared__ double sh[NK];
+  if (threadIdx.x < nk) sh[threadIdx.x] = h[threadIdx.x];
+  __syncthreads();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double wi = w[i];
+#pragma unroll
+    for (int k = 0; k < NK; ++k)
+      if (k < nk) wi = fma(-sh[k], __ldg(V + k * ld + i), wi);
+    w[i] = wi * scale;
+  }
+}
+
+// out = sum_k y[k] V_k
+__global__ void k_lincomb(long long n, int nk, const double* __restrict__ V, long long ld, Coefs y,
+                          double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < nk; ++k) s = fma(y.c[k], __ldg(V + k * ld + i), s);
+    out[i] = s;
+  }
+}
+
+// y = a x + b y
+__global__ void k_axpby(long long n, double a, const double* x, double b, double* y) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = b == 0.0 ? a * x[i] : fma(a, x[i], b * y[i]);
+}
+
+// z = x + a y
+__global__ void k_xpay(long long n, const double* __restrict__ x, double a, const double* __restrict__ y,
+                       double* __restrict__ z) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    z[i] = fma(a, y[i], x[i]);
+}
+
+__global__ void k_reduce_final2(const double* __restrict__ part, int nb, int nv, double* __restrict__ out) {
+  __shared__ double s[kRedThreads];
+  for (int k = 0; k < nv; ++k) {
+    double acc = 0.0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) acc += part[(long long)b * nv + k];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      if ((int)threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[k] = s[0];
+    __syncthreads();
+  }
+}
+
+static int vec_blocks(long long n) { return (int)std::min<long long>((n + 255) / 256, 148 * 8); }
+
+#define NK_DISPATCH(nk, KERNEL, ...)                           \
+  do {                                                         \
+    if ((nk) <= 8) KERNEL<8>__VA_ARGS__;                       \
+    else if ((nk) <= 16) KERNEL<16>__VA_ARGS__;                \
+    else if ((nk) <= 32) KERNEL<32>__VA_ARGS__;                \
+    else KERNEL<64>__VA_ARGS__;                                \
+  } while (0)
+
+// h[0..nk) = V^T w, h[nk] = w.w  -> out (device)
+void launch_mdot(long long n, int nk, const double* V, long long ld, const double* w, double* part, double* out,
+                 cudaStream_t s) {
+  NK_DISPATCH(nk, k_mdot, <<<kRedBlocks, kRedThreads, 0, s>>>(n, nk, V, ld, w, part));
+  k_reduce_final2<<<1, kRedThreads, 0, s>>>(part, kRedBlocks, nk + 1, out);
+}
+
+void launch_update_dot(long long n, int nk, const double* V, long long ld, const double* h, double* w, double* part,
+                       double* out, cudaStream_t s) {
+  NK_DISPATCH(nk, k_update_dot, <<<kRedBlocks, kRedThreads, 0, s>>>(n, nk, V, ld, h, w, part));
+  k_reduce_final2<<<1, kRedThreads, 0, s>>>(part, kRedBlocks, nk + 1, out);
+}
+
+void launch_update_scale(long long n, int nk, const double* V, long long ld, const double* h, double scale, double* w,
+                         cudaStream_t s) {
+  NK_DISPATCH(nk, k_update_scale, <<<vec_blocks(n), 256, 0, s>>>(n, nk, V, ld, h, scale, w));
+}
+
+void launch_lincomb(long long n, int nk, const double* V, long long ld, const double* y, double* out, cudaStream_t s) {
+  Coefs c;
+  for (int k = 0; k < nk && k < 64; ++k) c.c[k] = y[k];
+  k_lincomb<<<vec_blocks(n), 256, 0, s>>>(n, nk, V, ld, c, out);
+}
+
+void launch_axpby(long long n, double a, const double* x, double b, double* y, cudaStream_t s) {
+  k_axpby<<<vec_blocks(n), 256, 0, s>>>(n, a, x, b, y);
+}
+
+void launch_xpay(long long n, const double* x, double a, const double* y, double* z, cudaStream_t s) {
+  k_xpay<<<vec_blocks(n), 256, 0, s>>>(n, x, a, y, z);
+}
+
+}  // namespace nks

@@ -1,0 +1,904 @@
+// Host controller and C ABI of the B200 NKS library (include/nks.h).
+//
+// Newton with the line search of reading R17, restarted right-preconditioned
+// GMRES (reading R18) with CGS2 and one host read of <= 2(m+1)+1 doubles per
+// iteration, left-RAS/BILU(0) preconditioner, the adaptive controller of
+// Eq. (sencondt).  Every arithmetic step runs in the device kernels of stencil.cu,
+// krylov.cu, precond.cu and init_fft.cu; this file only sequences them and does O(m^2) Givens
+// arithmetic on the <= 64 Hessenberg entries.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "nks_internal.cuh"
+
+namespace nks {
+// stencil.cu
+void launch_level_prep(const DevParams& P, const double* X, double* T, cudaStream_t s);
+void launch_residual(const DevParams& P, const double* Xa, const double* Xb, const double* Ta, double* F, cudaStream_t s);
+void launch_pointwise_jac(const DevParams& P, const double* Xa, const double* Xb, double* jac4, cudaStream_t s);
+void launch_jv(const DevParams& P, const double* Xa, const double* jac4, const double* v, double* out, cudaStream_t s);
+void launch_norm_admissible(long long N, int nf, const double* F, const double* X, double* part, double* out, cudaStream_t s);
+void launch_energy(const DevParams& P, const double* X, double* part, double* out, cudaStream_t s);
+void launch_gauge(const DevParams& P, double* X, double* part, double* out, cudaStream_t s);
+// krylov.cu
+void launch_mdot(long long n, int nk, const double* V, long long ld, const double* w, double* part, double* out, cudaStream_t s);
+void launch_update_dot(long long n, int nk, const double* V, long long ld, const double* h, double* w, double* part,
+                       double* out, cudaStream_t s);
+void launch_update_scale(long long n, int nk, const double* V, long long ld, const double* h, double scale, double* w,
+                         cudaStream_t s);
+void launch_lincomb(long long n, int nk, const double* V, long long ld, const double* y, double* out, cudaStream_t s);
+void launch_axpby(long long n, double a, const double* x, double b, double* y, cudaStream_t s);
+void launch_xpay(long long n, const double* x, double a, const double* y, double* z, cudaStream_t s);
+// precond.cu
+void build_slot_tables(int dim, BoxSet& B);
+long long box_positions(const nks_grid& g);
+HostBoxes build_boxes_host(const nks_grid& g, const BoxSet& B);
+void launch_assemble(const DevParams& P, const BoxSet& B, int nf, const double* Xa, const double* jac4, double* fac,
+                     cudaStream_t s);
+void launch_factor(const BoxSet& B, int nf, double* fac, cudaStream_t s);
+void launch_ras_apply(const BoxSet& B, int nf, long long N, const double* fac, const double* r, double* y, double* z,
+                      cudaStream_t s);
+// init_fft.cu
+int init_displacement_fft(const DevParams& P, const double* c, double* u, void* scratch, cudaStream_t s, std::string& err);
+}  // namespace nks
+
+using namespace nks;
+
+namespace {
+
+enum Phase { PH_F = 0, PH_JV = 1, PH_RAS = 2, PH_ASM = 3, PH_FACT = 4, PH_VEC = 5, PH_RED = 6, PH_OTHER = 7 };
+
+struct CudaError {
+  cudaError_t e;
+};
+
+#define CK(call)                                   \
+  do {                                             \
+    cudaError_t _e = (call);                       \
+    if (_e != cudaSuccess) throw CudaError{_e};    \
+  } while (0)
+
+struct Layout {
+  size_t off_X[7];
+  size_t off_Ta, off_jac4, off_V, off_Z, off_W2, off_part, off_out;
+  size_t off_fac, off_ybox, off_gidx, off_nbr, off_levoff, off_levptr, off_posoff;
+  size_t total;
+  long long P;
+  int nslots, nbox, nlevptr;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+const char* validate(const nks_grid* g, const nks_params* p) {
+  if (!g || !p) return "NULL grid or params";
+  if (g->dim != 2 && g->dim != 3) return "dim must be 2 or 3";
+  for (int j = 0; j < g->dim; ++j)
+    if (g->n[j] < 5) return "every n[j] must be >= 5";
+  if (g->dim == 2 && g->n[2] != 1) return "n[2] must be 1 in 2D";
+  if (!(g->h > 0)) return "h must be > 0";
+  if (p->S < 1 || p->S > kMaxS) return "S must be in 1..16";
+  if (p->gmres_restart < 1 || p->gmres_restart > 60) return "gmres_restart must be in 1..60";
+  if (p->newton_maxit < 0 || p->gmres_maxit < 1) return "bad iteration limits";
+  if (p->pc_type != NKS_PC_NONE && p->pc_type != NKS_PC_RAS_BILU0) return "unknown pc_type";
+  if (p->pc_type == NKS_PC_RAS_BILU0) {
+    for (int j = 0; j < 3; ++j)
+      if (g->nsub[j] < 1 || g->nsub[j] > g->n[j]) return "nsub[j] must be in 1..n[j]";
+    if (g->dim == 2 && g->nsub[2] != 1) return "nsub[2] must be 1 in 2D";
+    if (g->overlap < 0 || g->overlap > 8) return "overlap must be in 0..8";
+  }
+  if (!(p->kappa > 0) || !(p->theta >= 0)) return "kappa must be > 0, theta >= 0";
+  return nullptr;
+}
+
+Layout make_layout(const nks_grid& g, const nks_params& p) {
+  Layout L{};
+  const int d = g.dim, nf = 2 + d;
+  const long long N = (long long)g.n[0] * g.n[1] * g.n[2];
+  const size_t vec = (size_t)nf * N * sizeof(double);
+  size_t o = 0;
+  for (int k = 0; k < 7; ++k) { L.off_X[k] = o; o = align256(o + vec); }
+  L.off_Ta = o; o = align256(o + N * sizeof(double));
+  L.off_jac4 = o; o = align256(o + 4 * N * sizeof(double));
+  L.off_V = o; o = align256(o + (size_t)(p.gmres_restart + 1) * vec);
+  L.off_Z = o; o = align256(o + vec);
+  L.off_W2 = o; o = align256(o + vec);
+  L.off_part = o; o = align256(o + (size_t)kRedBlocks * 80 * sizeof(double));
+  L.off_out = o; o = align256(o + 256 * sizeof(double));
+  L.P = 0;
+  if (p.pc_type == NKS_PC_RAS_BILU0) {
+    const int nslots = d == 2 ? 13 : 25;
+    L.nslots = nslots;
+    L.nbox = g.nsub[0] * g.nsub[1] * g.nsub[2];
+    L.P = box_positions(g);
+    // upper bound of level pointers: sum over boxes of (nlev + 1)
+    long long nl = 0;
+    {
+      // every box has at most (e0-1)+2(e1-1)+3(e2-1)+2 entries
+      const int ez = d == 3 ? g.overlap * 2 : 0;
+      const int e0 = g.n[0] / g.nsub[0] + 1 + 2 * g.overlap, e1 = g.n[1] / g.nsub[1] + 1 + 2 * g.overlap,
+                e2 = g.n[2] / g.nsub[2] + 1 + ez;
+      nl = (long long)L.nbox * ((e0 - 1) + 2 * (e1 - 1) + 3 * (e2 - 1) + 2);
+    }
+    L.nlevptr = (int)nl;
+    L.off_fac = o; o = align256(o + (size_t)nslots * nf * nf * L.P * sizeof(double));
+    L.off_ybox = o; o = align256(o + (size_t)nf * L.P * sizeof(double));
+    L.off_gidx = o; o = align256(o + (size_t)L.P * sizeof(int));
+    L.off_nbr = o; o = align256(o + (size_t)nslots * L.P * sizeof(int));
+    L.off_levoff = o; o = align256(o + (size_t)(L.nbox + 1) * sizeof(int));
+    L.off_levptr = o; o = align256(o + (size_t)nl * sizeof(int));
+    L.off_posoff = o; o = align256(o + (size_t)(L.nbox + 1) * sizeof(int));
+  }
+  L.total = o;
+  return L;
+}
+
+DevParams make_devparams(const nks_grid& g, const nks_params& p) {
+  DevParams P{};
+  P.dim = g.dim;
+  P.nx = g.n[0]; P.ny = g.n[1]; P.nz = g.n[2];
+  P.N = (long long)g.n[0] * g.n[1] * g.n[2];
+  P.h = g.h;
+  P.inv_h2 = 1.0 / (g.h * g.h);
+  P.inv_2h = 0.5 / g.h;
+  P.inv_4h2 = 0.25 / (g.h * g.h);
+  P.dt = 1.0; P.inv_dt = 1.0;
+  P.theta = p.theta; P.gamma_c = p.gamma_c; P.gamma_eta = p.gamma_eta; P.kappa = p.kappa; P.eps0 = p.eps0;
+  P.C11 = p.C11; P.C12 = p.C12; P.C44 = p.C44; P.Ls = p.Lscale; P.w_c = p.w_c;
+  // App. B, P:1113-1121 (coefficients already divided by V_m dE)
+  P.M0 = p.dE0 + (p.L0 - p.L1 + p.L2 - p.L3);
+  P.m1a = -(2.0 * p.L0 - 6.0 * p.L1 + 10.0 * p.L2 - 14.0 * p.L3);
+  P.m1b = 24.0 * p.U1 + 72.0 * p.U4;
+  P.m2a = -(6.0 * p.L1 - 24.0 * p.L2 + 54.0 * p.L3);
+  P.m2b = -216.0 * p.U4;
+  P.m2c = -144.0 * p.U4;
+  P.M3 = -(16.0 * p.L2 - 80.0 * p.L3);
+  P.M4 = -40.0 * p.L3;
+  P.m5a = -(24.0 * p.U1 + 72.0 * p.U4);   // M5(c) = -(24 U1 c^2 + 72 U4 (1-2c) c^2)
+  P.m5b = 144.0 * p.U4;
+  P.m6 = 144.0 * p.U4;                     // M6(c) = 144 U4 c^3
+  P.S = p.S;
+  for (int k = 1; k < kMaxS + 1; ++k) P.pcoef[k - 1] = (k <= p.S - 1) ? 1.0 / (2.0 * k * (2.0 * k + 1.0)) : 0.0;
+  P.K = p.Lscale * (p.C11 + (g.dim - 1) * p.C12);
+  P.cbar0 = 0.0;
+  return P;
+}
+
+// ---- phase profiling ---------------------------------------------------------------------------
+cudaEvent_t take_event(nks_state* st) {
+  if (st->ev_pool.empty()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+  cudaEvent_t e = st->ev_pool.back();
+  st->ev_pool.pop_back();
+  return e;
+}
+
+void ph_begin(nks_state* st, int ph) {
+  if (!st->profile) return;
+  cudaEvent_t e = take_event(st);
+  CK(cudaEventRecord(e, st->stream));
+  st->cur_phase = ph;
+  st->cur_ev = e;
+}
+
+void ph_end(nks_state* st) {
+  if (!st->profile || st->cur_phase < 0) return;
+  cudaEvent_t e = take_event(st);
+  CK(cudaEventRecord(e, st->stream));
+  st->pend_phase.push_back(st->cur_phase);
+  st->pend_ev.push_back(st->cur_ev);
+  st->pend_ev.push_back(e);
+  st->cur_phase = -1;
+  if (st->pend_phase.size() > 20000) {   // drain to bound the pool
+    CK(cudaStreamSynchronize(st->stream));
+    for (size_t k = 0; k < st->pend_phase.size(); ++k) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, st->pend_ev[2 * k], st->pend_ev[2 * k + 1]));
+      st->phase_ms[st->pend_phase[k]] += ms;
+      st->phase_cnt[st->pend_phase[k]] += 1;
+      st->ev_pool.push_back(st->pend_ev[2 * k]);
+      st->ev_pool.push_back(st->pend_ev[2 * k + 1]);
+    }
+    st->pend_phase.clear();
+    st->pend_ev.clear();
+  }
+}
+
+struct PhaseScope {
+  nks_state* st;
+  PhaseScope(nks_state* s, int ph) : st(s) { ph_begin(st, ph); }
+  ~PhaseScope() { ph_end(st); }
+};
+
+// ---- building blocks -------------------------------------------------------------------------------
+void sync(nks_state* st) {
+  CK(cudaStreamSynchronize(st->stream));
+  st->syncs++;
+}
+
+void residual(nks_state* st, const double* Xb, double* F) {
+  PhaseScope ps(st, PH_F);
+  launch_residual(st->dp, st->Xn, Xb, st->Ta, F, st->stream);
+  st->launches += 1;
+}
+
+// (||F||, #inadmissible points of X) -- host sync
+void norm_adm(nks_state* st, const double* F, const double* X, double& nrm, double& bad) {
+  {
+    PhaseScope ps(st, PH_RED);
+    launch_norm_admissible(st->N, st->nf, F, X, st->red_part, st->red_out, st->stream);
+    st->launches += 2;
+  }
+  CK(cudaMemcpyAsync(st->h_red, st->red_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
+  sync(st);
+  nrm = std::sqrt(st->h_red[0]);
+  bad = st->h_red[1];
+}
+
+void gauge(nks_state* st, double* X) {
+  PhaseScope ps(st, PH_RED);
+  launch_gauge(st->dp, X, st->red_part, st->red_out + 128, st->stream);
+  st->launches += 3;
+}
+
+void jv(nks_state* st, const double* v, double* out) {
+  PhaseScope ps(st, PH_JV);
+  launch_jv(st->dp, st->Xn, st->jac4, v, out, st->stream);
+  st->launches += 1;
+}
+
+void pc_apply(nks_state* st, const double* r, double* z) {
+  if (st->prm.pc_type == NKS_PC_NONE) {
+    CK(cudaMemcpyAsync(z, r, st->nvec * sizeof(double), cudaMemcpyDeviceToDevice, st->stream));
+    return;
+  }
+  PhaseScope ps(st, PH_RAS);
+  launch_ras_apply(st->boxes, st->nf, st->N, st->fac, r, st->ybox, z, st->stream);
+  st->launches += 1;
+}
+
+void pc_setup(nks_state* st, const double* Xb) {
+  if (st->prm.pc_type == NKS_PC_NONE) return;
+  {
+    PhaseScope ps(st, PH_ASM);
+    launch_assemble(st->dp, st->boxes, st->nf, st->Xn, st->jac4, st->fac, st->stream);
+    st->launches += 1;
+  }
+  {
+    PhaseScope ps(st, PH_FACT);
+    launch_factor(st->boxes, st->nf, st->fac, st->stream);
+    st->launches += 1;
+  }
+  (void)Xb;
+  st->pc_valid = true;
+  st->pc_dt = st->dp.dt;
+}
+
+void set_dt(nks_state* st, double dt) {
+  st->dp.dt = dt;
+  st->dp.inv_dt = 1.0 / dt;
+}
+
+// Right-preconditioned restarted GMRES: J s = b with s0 = 0.  Returns 0 converged, 1 maxit.
+int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, int& its) {
+  const int m = st->prm.gmres_restart;
+  const long long n = st->nvec;
+  double* V = st->V;
+  std::vector<double> H((m + 1) * m, 0.0), cs(m, 0.0), sn(m, 0.0), g(m + 1, 0.0), y(m, 0.0);
+  CK(cudaMemsetAsync(s, 0, n * sizeof(double), st->stream));
+  its = 0;
+  double beta = bnorm;
+  bool first = true;
+  while (true) {
+    if (beta <= tol) return 0;
+    {
+      PhaseScope ps(st, PH_VEC);
+      launch_axpby(n, 1.0 / beta, first ? b : V, 0.0, V, st->stream);
+      st->launches += 1;
+    }
+    first = false;
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int j = 0;
+    double resid = beta;
+    bool done = false;
+    for (j = 0; j < m; ++j) {
+      double* vj = V + (long long)j * n;
+      double* w = V + (long long)(j + 1) * n;
+      pc_apply(st, vj, st->Z);
+      jv(st, st->Z, w);
+      {
+        PhaseScope ps(st, PH_VEC);
+        launch_mdot(n, j + 1, V, n, w, st->red_part, st->red_out, st->stream);
+        launch_update_dot(n, j + 1, V, n, st->red_out, w, st->red_part, st->red_out + 64, st->stream);
+        st->launches += 4;
+      }
+      CK(cudaMemcpyAsync(st->h_red, st->red_out, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
+      CK(cudaMemcpyAsync(st->h_red + 64, st->red_out + 64, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
+      sync(st);
+      double h2sq = 0.0;
+      for (int k = 0; k <= j; ++k) {
+        H[k * m + j] = st->h_red[k] + st->h_red[64 + k];
+        h2sq += st->h_red[64 + k] * st->h_red[64 + k];
+      }
+      const double ww1 = st->h_red[64 + j + 1];
+      const double nrm = std::sqrt(std::max(ww1 - h2sq, 0.0));
+      H[(j + 1) * m + j] = nrm;
+      ++its;
+      const bool breakdown = !(nrm > 1e-300);
+      {
+        PhaseScope ps(st, PH_VEC);
+        launch_update_scale(n, j + 1, V, n, st->red_out + 64, breakdown ? 0.0 : 1.0 / nrm, w, st->stream);
+        st->launches += 1;
+      }
+      // Givens
+      for (int k = 0; k < j; ++k) {
+        const double a = H[k * m + j], bb = H[(k + 1) * m + j];
+        H[k * m + j] = cs[k] * a + sn[k] * bb;
+        H[(k + 1) * m + j] = -sn[k] * a + cs[k] * bb;
+      }
+      {
+        const double a = H[j * m + j], bb = H[(j + 1) * m + j];
+        const double r = std::hypot(a, bb);
+        cs[j] = r > 0 ? a / r : 1.0;
+        sn[j] = r > 0 ? bb / r : 0.0;
+        H[j * m + j] = r;
+        H[(j + 1) * m + j] = 0.0;
+        g[j + 1] = -sn[j] * g[j];
+        g[j] = cs[j] * g[j];
+      }
+      resid = std::fabs(g[j + 1]);
+      if (resid <= tol || breakdown || its >= st->prm.gmres_maxit) {
+        ++j;
+        done = true;
+        break;
+      }
+    }
+    // y = H^{-1} g (upper triangular j x j)
+    for (int k = j - 1; k >= 0; --k) {
+      double acc = g[k];
+      for (int l = k + 1; l < j; ++l) acc -= H[k * m + l] * y[l];
+      y[k] = acc / H[k * m + k];
+    }
+    {
+      PhaseScope ps(st, PH_VEC);
+      launch_lincomb(n, j, V, n, y.data(), st->W2, st->stream);
+      st->launches += 1;
+    }
+    pc_apply(st, st->W2, st->Z);
+    {
+      PhaseScope ps(st, PH_VEC);
+      launch_axpby(n, 1.0, st->Z, 1.0, s, st->stream);
+      st->launches += 1;
+    }
+    if (resid <= tol) return 0;
+    if (its >= st->prm.gmres_maxit) return 1;
+    (void)done;
+    // restart: r = b - J s  -> V[0]
+    jv(st, s, st->W2);
+    {
+      PhaseScope ps(st, PH_VEC);
+      launch_xpay(n, b, -1.0, st->W2, V, st->stream);
+      st->launches += 1;
+    }
+    {
+      PhaseScope ps(st, PH_RED);
+      launch_norm_admissible(n / st->nf, st->nf, V, nullptr, st->red_part, st->red_out, st->stream);
+      st->launches += 2;
+    }
+    CK(cudaMemcpyAsync(st->h_red, st->red_out, sizeof(double), cudaMemcpyDeviceToHost, st->stream));
+    sync(st);
+    beta = std::sqrt(st->h_red[0]);
+    // V already holds r; scale below uses V as source (first == false)
+  }
+}
+
+void energy(nks_state* st, const double* X, double parts[4], double& mass) {
+  {
+    PhaseScope ps(st, PH_RED);
+    launch_energy(st->dp, X, st->red_part, st->red_out, st->stream);
+    st->launches += 2;
+  }
+  CK(cudaMemcpyAsync(st->h_red, st->red_out, 5 * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
+  sync(st);
+  const double vol = std::pow(st->grid.h, st->d);
+  for (int k = 0; k < 4; ++k) parts[k] = st->h_red[k] * vol;
+  mass = st->h_red[4] * vol;
+}
+
+void level_prep(nks_state* st) {
+  PhaseScope ps(st, PH_OTHER);
+  launch_level_prep(st->dp, st->Xn, st->Ta, st->stream);
+  st->launches += 1;
+}
+
+// One NKS step (transactional).
+nks_status step_impl(nks_state* st, double dt, nks_step_info* info) {
+  nks_step_info loc{};
+  nks_step_info& I = info ? *info : loc;
+  std::memset(&I, 0, sizeof(I));
+  I.dt = dt;
+  if (!(dt > 0)) { st->err = "dt must be > 0"; return NKS_E_INVALID; }
+  set_dt(st, dt);
+  const long long nbytes = st->nvec * sizeof(double);
+  CK(cudaMemcpyAsync(st->Xb, st->Xn, nbytes, cudaMemcpyDeviceToDevice, st->stream));
+  residual(st, st->Xb, st->F);
+  double f, bad;
+  norm_adm(st, st->F, st->Xb, f, bad);
+  if (bad > 0 || !std::isfinite(f)) {
+    I.reason = NKS_REASON_DOMAIN;
+    st->err = "X^n inadmissible";
+    return NKS_E_DOMAIN;
+  }
+  const double f0 = f;
+  I.fnorm0 = f0;
+  const nks_params& p = st->prm;
+  int it = 0;
+  for (;; ++it) {
+    if (f <= std::max(p.newton_rtol * f0, p.newton_atol)) break;
+    if (it == p.newton_maxit) {
+      I.reason = NKS_REASON_NEWTON_MAXIT;
+      I.fnorm = f;
+      st->err = "Newton did not converge in newton_maxit iterations";
+      return NKS_E_DIVERGED;
+    }
+    {
+      PhaseScope ps(st, PH_OTHER);
+      launch_pointwise_jac(st->dp, st->Xn, st->Xb, st->jac4, st->stream);
+      st->launches += 1;
+    }
+    if (p.pc_type != NKS_PC_NONE) {
+      bool refactor = p.pc_reuse == 0 || (p.pc_reuse == 1 && it == 0) ||
+                      (p.pc_reuse == 2 && (!st->pc_valid || st->pc_dt != dt));
+      if (refactor) {
+        pc_setup(st, st->Xb);
+        I.pc_setups++;
+      }
+    }
+    // b = -F (into Ft), solve J S = b
+    {
+      PhaseScope ps(st, PH_VEC);
+      launch_axpby(st->nvec, -1.0, st->F, 0.0, st->Ft, st->stream);
+      st->launches += 1;
+    }
+    int gits = 0;
+    const double tol = std::max(p.gmres_rtol * f, p.gmres_atol);
+    const int grc = gmres(st, st->Ft, f, st->S, tol, gits);
+    I.gmres_its += gits;
+    if (grc != 0) {
+      I.reason = NKS_REASON_GMRES_MAXIT;
+      I.fnorm = f;
+      st->err = "GMRES reached gmres_maxit";
+      return NKS_E_DIVERGED;
+    }
+    // line search (reading R17)
+    double lam = 1.0, ft = 0.0;
+    bool accepted = false;
+    for (int hv = 0; hv <= p.ls_max_halvings; ++hv) {
+      {
+        PhaseScope ps(st, PH_VEC);
+        launch_xpay(st->nvec, st->Xb, lam, st->S, st->Xt, st->stream);
+        st->launches += 1;
+      }
+      residual(st, st->Xt, st->Ft);
+      norm_adm(st, st->Ft, st->Xt, ft, bad);
+      if (bad == 0 && std::isfinite(ft) && ft <= (1.0 - p.ls_alpha * lam) * f) {
+        accepted = true;
+        break;
+      }
+      lam *= 0.5;
+      I.ls_halvings++;
+    }
+    if (!accepted) {
+      I.reason = NKS_REASON_LINE_SEARCH;
+      I.fnorm = f;
+      st->err = "line search failed";
+      return NKS_E_DIVERGED;
+    }
+    std::swap(st->Xb, st->Xt);
+    std::swap(st->F, st->Ft);
+    f = ft;
+    gauge(st, st->Xb);
+  }
+  I.newton_its = it;
+  I.fnorm = f;
+  I.converged = 1;
+  // accept: X^{n-1} <- X^n, X^n <- X^b
+  double* old = st->Xprev;
+  st->Xprev = st->Xn;
+  st->Xn = st->Xb;
+  st->Xb = old;
+  st->have_prev = true;
+  st->dt_prev = dt;
+  st->time += dt;
+  level_prep(st);
+  energy(st, st->Xn, I.energy_parts, I.mass);
+  I.energy = I.energy_parts[0] + I.energy_parts[1] + I.energy_parts[2] + I.energy_parts[3];
+  I.time = st->time;
+  I.zeta = st->zeta;
+  return NKS_OK;
+}
+
+double change_rate(nks_state* st) {
+  const nks_params& p = st->prm;
+  const long long n = p.xd_norm == 2 ? 2 * st->N : st->nvec;
+  {
+    PhaseScope ps(st, PH_VEC);
+    launch_xpay(n, st->Xn, -1.0, st->Xprev, st->W2, st->stream);
+    st->launches += 1;
+  }
+  {
+    PhaseScope ps(st, PH_RED);
+    launch_norm_admissible(n, 1, st->W2, nullptr, st->red_part, st->red_out, st->stream);
+    st->launches += 2;
+  }
+  CK(cudaMemcpyAsync(st->h_red, st->red_out, sizeof(double), cudaMemcpyDeviceToHost, st->stream));
+  sync(st);
+  double nrm = std::sqrt(st->h_red[0]);
+  if (p.xd_norm == 0) nrm /= std::sqrt((double)st->nvec);
+  return nrm / st->dt_prev;
+}
+
+template <typename F>
+nks_status guarded(nks_state* st, F&& fn) {
+  try {
+    return fn();
+  } catch (const CudaError& e) {
+    if (st) st->err = std::string("CUDA error: ") + cudaGetErrorString(e.e);
+    return NKS_E_CUDA;
+  } catch (const std::exception& e) {
+    if (st) st->err = e.what();
+    return NKS_E_CUDA;
+  }
+}
+
+cudaMemcpyKind kind_in(int on_device) { return on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice; }
+cudaMemcpyKind kind_out(int on_device) { return on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost; }
+
+}  // namespace
+
+// =====================================================================================================
+extern "C" {
+
+const char* nks_version(void) { return "nks-b200 0.1 (sm_100a, fp64)"; }
+
+size_t nks_workspace_bytes(const nks_grid* grid, const nks_params* params) {
+  if (validate(grid, params)) return 0;
+  return make_layout(*grid, *params).total;
+}
+
+nks_status nks_create(const nks_grid* grid, const nks_params* params, void* workspace, size_t workspace_bytes,
+                      void* cuda_stream, nks_state** out) {
+  if (!out) return NKS_E_INVALID;
+  *out = nullptr;
+  if (validate(grid, params)) return NKS_E_INVALID;
+  if (!workspace) return NKS_E_INVALID;
+  const Layout L = make_layout(*grid, *params);
+  if (workspace_bytes < L.total) return NKS_E_OOM;
+  nks_state* st = new nks_state();
+  st->grid = *grid;
+  st->prm = *params;
+  st->stream = (cudaStream_t)cuda_stream;
+  st->d = grid->dim;
+  st->nf = 2 + grid->dim;
+  st->N = (long long)grid->n[0] * grid->n[1] * grid->n[2];
+  st->nvec = st->nf * st->N;
+  st->dp = make_devparams(*grid, *params);
+  st->ws = (char*)workspace;
+  st->ws_bytes = workspace_bytes;
+  st->zeta = params->zeta;
+  const nks_status rc = guarded(st, [&]() -> nks_status {
+    char* w = st->ws;
+    double** Xs[7] = {&st->Xn, &st->Xprev, &st->Xb, &st->Xt, &st->S, &st->F, &st->Ft};
+    for (int k = 0; k < 7; ++k) *Xs[k] = (double*)(w + L.off_X[k]);
+    st->Ta = (double*)(w + L.off_Ta);
+    st->jac4 = (double*)(w + L.off_jac4);
+    st->V = (double*)(w + L.off_V);
+    st->Z = (double*)(w + L.off_Z);
+    st->W2 = (double*)(w + L.off_W2);
+    st->red_part = (double*)(w + L.off_part);
+    st->red_out = (double*)(w + L.off_out);
+    CK(cudaMallocHost(&st->h_red, 256 * sizeof(double)));
+    if (params->pc_type == NKS_PC_RAS_BILU0) {
+      BoxSet& B = st->boxes;
+      build_slot_tables(grid->dim, B);
+      HostBoxes H = build_boxes_host(*grid, B);
+      B.nbox = L.nbox;
+      B.P = H.P;
+      B.max_levels = H.max_levels;
+      B.max_level_width = H.max_width;
+      if ((long long)H.lev_ptr.size() > L.nlevptr) throw std::runtime_error("level table overflow");
+      st->fac = (double*)(w + L.off_fac);
+      st->ybox = (double*)(w + L.off_ybox);
+      B.gidx = (int*)(w + L.off_gidx);
+      B.nbr = (int*)(w + L.off_nbr);
+      B.box_lev_off = (int*)(w + L.off_levoff);
+      B.lev_ptr = (int*)(w + L.off_levptr);
+      B.box_pos_off = (int*)(w + L.off_posoff);
+      B.h_box_lev_off = H.box_lev_off;
+      B.h_box_pos_off = H.box_pos_off;
+      CK(cudaMemcpyAsync(B.gidx, H.gidx.data(), H.gidx.size() * sizeof(int), cudaMemcpyHostToDevice, st->stream));
+      CK(cudaMemcpyAsync(B.nbr, H.nbr.data(), H.nbr.size() * sizeof(int), cudaMemcpyHostToDevice, st->stream));
+      CK(cudaMemcpyAsync(B.box_lev_off, H.box_lev_off.data(), H.box_lev_off.size() * sizeof(int), cudaMemcpyHostToDevice,
+                         st->stream));
+      CK(cudaMemcpyAsync(B.lev_ptr, H.lev_ptr.data(), H.lev_ptr.size() * sizeof(int), cudaMemcpyHostToDevice, st->stream));
+      CK(cudaMemcpyAsync(B.box_pos_off, H.box_pos_off.data(), H.box_pos_off.size() * sizeof(int), cudaMemcpyHostToDevice,
+                         st->stream));
+      CK(cudaStreamSynchronize(st->stream));
+    }
+    return NKS_OK;
+  });
+  if (rc != NKS_OK) {
+    if (st->h_red) cudaFreeHost(st->h_red);
+    delete st;
+    return rc;
+  }
+  *out = st;
+  return NKS_OK;
+}
+
+nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, const double* u, int32_t on_device) {
+  if (!st || !c || !eta) return NKS_E_INVALID;
+  return guarded(st, [&]() -> nks_status {
+    const long long N = st->N;
+    CK(cudaMemcpyAsync(st->Xn, c, N * sizeof(double), kind_in(on_device), st->stream));
+    CK(cudaMemcpyAsync(st->Xn + N, eta, N * sizeof(double), kind_in(on_device), st->stream));
+    // cbar0 = mean(c): the energy kernel's 5th sum is sum c
+    {
+      PhaseScope ps(st, PH_RED);
+      launch_energy(st->dp, st->Xn, st->red_part, st->red_out, st->stream);  // u garbage only affects E3 here
+      st->launches += 2;
+    }
+    CK(cudaMemcpyAsync(st->h_red, st->red_out, 5 * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
+    sync(st);
+    st->dp.cbar0 = st->h_red[4] / (double)N;
+    if (u) {
+      CK(cudaMemcpyAsync(st->Xn + 2 * N, u, st->d * N * sizeof(double), kind_in(on_device), st->stream));
+    } else {
+      std::string e;
+      if (init_displacement_fft(st->dp, st->Xn, st->Xn + 2 * N, st->V, st->stream, e) != 0) {
+        st->err = e;
+        return NKS_E_CUDA;
+      }
+      st->launches += 3 + st->d;
+    }
+    gauge(st, st->Xn);
+    level_prep(st);
+    double nrm, bad;
+    CK(cudaMemsetAsync(st->F, 0, st->nvec * sizeof(double), st->stream));
+    norm_adm(st, st->F, st->Xn, nrm, bad);
+    st->time = 0.0;
+    st->have_prev = false;
+    st->have_fields = true;
+    st->pc_valid = false;
+    st->zeta = st->prm.zeta;
+    if (bad > 0) {
+      st->err = "initial state inadmissible";
+      return NKS_E_DOMAIN;
+    }
+    return NKS_OK;
+  });
+}
+
+nks_status nks_get_fields(const nks_state* cst, double* c, double* eta, double* u, int32_t on_device) {
+  nks_state* st = const_cast<nks_state*>(cst);
+  if (!st || !c || !eta || !u) return NKS_E_INVALID;
+  if (!st->have_fields) return NKS_E_STATE;
+  return guarded(st, [&]() -> nks_status {
+    const long long N = st->N;
+    CK(cudaMemcpyAsync(c, st->Xn, N * sizeof(double), kind_out(on_device), st->stream));
+    CK(cudaMemcpyAsync(eta, st->Xn + N, N * sizeof(double), kind_out(on_device), st->stream));
+    CK(cudaMemcpyAsync(u, st->Xn + 2 * N, st->d * N * sizeof(double), kind_out(on_device), st->stream));
+    sync(st);
+    return NKS_OK;
+  });
+}
+
+nks_status nks_step(nks_state* st, double dt, nks_step_info* info) {
+  if (!st) return NKS_E_INVALID;
+  if (!st->have_fields) return NKS_E_STATE;
+  return guarded(st, [&]() { return step_impl(st, dt, info); });
+}
+
+nks_status nks_run_adaptive(nks_state* st, int32_t max_steps, double t_end, nks_step_info* per_step, int32_t* done) {
+  if (!st || max_steps < 0) return NKS_E_INVALID;
+  if (!st->have_fields) return NKS_E_STATE;
+  if (done) *done = 0;
+  return guarded(st, [&]() -> nks_status {
+    const nks_params& p = st->prm;
+    for (int n = 0; n < max_steps; ++n) {
+      if (t_end > 0 && st->time >= t_end) break;
+      double dt, xd = 0.0;
+      if (!st->have_prev) {
+        dt = p.dt_init;
+      } else {
+        xd = change_rate(st);
+        dt = std::max(p.dt_min, p.dt_max / std::sqrt(1.0 + st->zeta * xd * xd));   // Eq. (sencondt)
+      }
+      int retries = 0;
+      nks_step_info info{};
+      while (true) {
+        const nks_status rc = step_impl(st, dt, &info);
+        if (rc == NKS_OK) break;
+        if (rc != NKS_E_DIVERGED) return rc;
+        dt /= std::sqrt(2.0);
+        st->zeta *= 2.0;
+        ++retries;
+        if (dt < p.dt_min * p.dt_floor_factor) {
+          info.reason = NKS_REASON_DT_FLOOR;
+          if (per_step) per_step[n] = info;
+          st->err = "adaptive controller: dt fell below dt_min * dt_floor_factor";
+          return NKS_E_DIVERGED;
+        }
+      }
+      info.retries = retries;
+      info.xd = xd;
+      info.zeta = st->zeta;
+      if (per_step) per_step[n] = info;
+      if (done) *done = n + 1;
+    }
+    return NKS_OK;
+  });
+}
+
+nks_status nks_energy(nks_state* st, double parts[4], double* mass) {
+  if (!st || !parts || !mass) return NKS_E_INVALID;
+  if (!st->have_fields) return NKS_E_STATE;
+  return guarded(st, [&]() -> nks_status {
+    energy(st, st->Xn, parts, *mass);
+    return NKS_OK;
+  });
+}
+
+nks_status nks_eval_residual(nks_state* st, double dt, const double* x_b, double* F, int32_t on_device) {
+  if (!st || !x_b || !F || !(dt > 0)) return NKS_E_INVALID;
+  if (!st->have_fields) return NKS_E_STATE;
+  return guarded(st, [&]() -> nks_status {
+    set_dt(st, dt);
+    const size_t nb = st->nvec * sizeof(double);
+    CK(cudaMemcpyAsync(st->Xt, x_b, nb, kind_in(on_device), st->stream));
+    residual(st, st->Xt, st->Ft);
+    CK(cudaMemcpyAsync(F, st->Ft, nb, kind_out(on_device), st->stream));
+    sync(st);
+    return NKS_OK;
+  });
+}
+
+nks_status nks_eval_jv(nks_state* st, double dt, const double* x_b, const double* v, double* Jv, int32_t on_device) {
+  if (!st || !x_b || !v || !Jv || !(dt > 0)) return NKS_E_INVALID;
+  if (!st->have_fields) return NKS_E_STATE;
+  return guarded(st, [&]() -> nks_status {
+    set_dt(st, dt);
+    const size_t nb = st->nvec * sizeof(double);
+    CK(cudaMemcpyAsync(st->Xt, x_b, nb, kind_in(on_device), st->stream));
+    CK(cudaMemcpyAsync(st->W2, v, nb, kind_in(on_device), st->stream));
+    {
+      PhaseScope ps(st, PH_OTHER);
+      launch_pointwise_jac(st->dp, st->Xn, st->Xt, st->jac4, st->stream);
+      st->launches += 1;
+    }
+    jv(st, st->W2, st->Ft);
+    CK(cudaMemcpyAsync(Jv, st->Ft, nb, kind_out(on_device), st->stream));
+    sync(st);
+    return NKS_OK;
+  });
+}
+
+nks_status nks_pc_setup(nks_state* st, double dt, const double* x_b, int32_t on_device) {
+  if (!st || !x_b || !(dt > 0)) return NKS_E_INVALID;
+  if (!st->have_fields) return NKS_E_STATE;
+  return guarded(st, [&]() -> nks_status {
+    set_dt(st, dt);
+    CK(cudaMemcpyAsync(st->Xb, x_b, st->nvec * sizeof(double), kind_in(on_device), st->stream));
+    {
+      PhaseScope ps(st, PH_OTHER);
+      launch_pointwise_jac(st->dp, st->Xn, st->Xb, st->jac4, st->stream);
+      st->launches += 1;
+    }
+    pc_setup(st, st->Xb);
+    sync(st);
+    return NKS_OK;
+  });
+}
+
+nks_status nks_pc_apply(nks_state* st, const double* r, double* z, int32_t on_device) {
+  if (!st || !r || !z) return NKS_E_INVALID;
+  if (st->prm.pc_type != NKS_PC_NONE && !st->pc_valid) return NKS_E_STATE;
+  return guarded(st, [&]() -> nks_status {
+    const size_t nb = st->nvec * sizeof(double);
+    CK(cudaMemcpyAsync(st->W2, r, nb, kind_in(on_device), st->stream));
+    pc_apply(st, st->W2, st->Z);
+    CK(cudaMemcpyAsync(z, st->Z, nb, kind_out(on_device), st->stream));
+    sync(st);
+    return NKS_OK;
+  });
+}
+
+nks_status nks_gmres_solve(nks_state* st, double dt, const double* x_b, const double* rhs, double* s, int32_t on_device,
+                           int32_t* its) {
+  if (!st || !x_b || !rhs || !s || !(dt > 0)) return NKS_E_INVALID;
+  if (!st->have_fields) return NKS_E_STATE;
+  return guarded(st, [&]() -> nks_status {
+    set_dt(st, dt);
+    const size_t nb = st->nvec * sizeof(double);
+    CK(cudaMemcpyAsync(st->Xb, x_b, nb, kind_in(on_device), st->stream));
+    CK(cudaMemcpyAsync(st->Ft, rhs, nb, kind_in(on_device), st->stream));
+    {
+      PhaseScope ps(st, PH_OTHER);
+      launch_pointwise_jac(st->dp, st->Xn, st->Xb, st->jac4, st->stream);
+      st->launches += 1;
+    }
+    if (st->prm.pc_type != NKS_PC_NONE) pc_setup(st, st->Xb);
+    double bn, bad;
+    norm_adm(st, st->Ft, nullptr, bn, bad);
+    int it = 0;
+    const double tol = std::max(st->prm.gmres_rtol * bn, st->prm.gmres_atol);
+    const int rc = gmres(st, st->Ft, bn, st->S, tol, it);
+    if (its) *its = it;
+    CK(cudaMemcpyAsync(s, st->S, nb, kind_out(on_device), st->stream));
+    sync(st);
+    if (rc != 0) {
+      st->err = "GMRES reached gmres_maxit";
+      return NKS_E_DIVERGED;
+    }
+    return NKS_OK;
+  });
+}
+
+nks_status nks_counters(const nks_state* st, int64_t* kernel_launches, int64_t* host_syncs) {
+  if (!st) return NKS_E_INVALID;
+  if (kernel_launches) *kernel_launches = st->launches;
+  if (host_syncs) *host_syncs = st->syncs;
+  return NKS_OK;
+}
+
+nks_status nks_set_profiling(nks_state* st, int32_t enable) {
+  if (!st) return NKS_E_INVALID;
+  st->profile = enable != 0;
+  return NKS_OK;
+}
+
+nks_status nks_phase_times(nks_state* st, double ms[8], int64_t counts[8], int32_t reset) {
+  if (!st) return NKS_E_INVALID;
+  return guarded(st, [&]() -> nks_status {
+    CK(cudaStreamSynchronize(st->stream));
+    for (size_t k = 0; k < st->pend_phase.size(); ++k) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, st->pend_ev[2 * k], st->pend_ev[2 * k + 1]));
+      st->phase_ms[st->pend_phase[k]] += t;
+      st->phase_cnt[st->pend_phase[k]] += 1;
+      st->ev_pool.push_back(st->pend_ev[2 * k]);
+      st->ev_pool.push_back(st->pend_ev[2 * k + 1]);
+    }
+    st->pend_phase.clear();
+    st->pend_ev.clear();
+    for (int k = 0; k < 8; ++k) {
+      if (ms) ms[k] = st->phase_ms[k];
+      if (counts) counts[k] = st->phase_cnt[k];
+      if (reset) { st->phase_ms[k] = 0; st->phase_cnt[k] = 0; }
+    }
+    return NKS_OK;
+  });
+}
+
+nks_status nks_destroy(nks_state* st) {
+  if (!st) return NKS_E_INVALID;
+  cudaStreamSynchronize(st->stream);
+  for (auto e : st->ev_pool) cudaEventDestroy(e);
+  for (auto e : st->pend_ev) cudaEventDestroy(e);
+  if (st->h_red) cudaFreeHost(st->h_red);
+  delete st;
+  return NKS_OK;
+}
+
+const char* nks_last_error(const nks_state* st) { return st ? st->err.c_str() : "NULL state"; }
+
+}  // extern "C"

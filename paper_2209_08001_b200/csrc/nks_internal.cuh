@@ -1,0 +1,135 @@
+// Internal declarations of the B200 NKS library (not part of the ABI; see include/nks.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/nks.h"
+
+namespace nks {
+
+constexpr int kMaxDim = 3;
+constexpr int kMaxNf = 5;          // 2 + d
+constexpr int kMaxSlots = 25;      // |o|_1 <= 2 block footprint in 3D
+constexpr int kMaxS = 16;
+constexpr int kRedBlocks = 592;    // 4 x 148 SMs: blocks of every reduction first stage
+constexpr int kRedThreads = 256;
+
+// Parameters passed by value to every kernel (fp64 model constants derived on the host).
+struct DevParams {
+  int dim, nx, ny, nz;
+  long long N;          // points
+  double h, inv_h2, inv_2h, inv_4h2;
+  double dt, inv_dt;
+  double theta, gamma_c, gamma_eta, kappa, eps0, C11, C12, C44, Ls, w_c;
+  // App. B, derived from L0..L3, U1, U4, dE0:
+  // M1(phi) = m1a + m1b phi^2, M2(phi) = m2a + m2b phi^2 + m2c phi^3, M5(c) = m5a c^2 + m5b c^3,
+  // M6(c) = m6 c^3.
+  double M0, m1a, m1b, m2a, m2b, m2c, M3, M4, m5a, m5b, m6;
+  int S;
+  double pcoef[kMaxS];  // pcoef[k-1] = 1/(2k(2k+1)), k = 1..S-1 (odd-order Taylor terms)
+  double K;             // Ls*(C11 + (d-1) C12): T = K (sum_J D^_J u_J - d eps0 (c - cbar0))
+  double cbar0;
+};
+
+// Geometry of the RAS boxes (host-built, device-resident).
+struct BoxSet {
+  int nbox = 0;
+  int nslots = 0;            // 13 or 25
+  long long P = 0;           // total box positions over all boxes
+  int max_levels = 0;
+  int max_level_width = 0;
+  // device arrays
+  int* gidx = nullptr;       // [P] global point index, negative-1-encoded when not owned: ~gidx
+  int* nbr = nullptr;        // [nslots][P] neighbour position or -1
+  int* box_lev_off = nullptr;   // [nbox+1] offset into lev_ptr
+  int* lev_ptr = nullptr;       // concatenated per-box level pointers (absolute positions)
+  int* box_pos_off = nullptr;   // [nbox+1]
+  // host copies
+  std::vector<int> h_box_lev_off, h_box_pos_off;
+  // slot tables (host, copied into kernel params)
+  int off[kMaxSlots][3];
+  int lower[kMaxSlots];   int nlower = 0;   // lower slots in ascending natural order
+  int upper[kMaxSlots];   int nupper = 0;   // strictly upper slots
+  int diag = 0;
+  // update pairs for the IKJ factorisation: for lower slot index a: pairs (sb, st)
+  int npairs[kMaxSlots];
+  int pair_b[kMaxSlots][kMaxSlots];
+  int pair_t[kMaxSlots][kMaxSlots];
+};
+
+// Slot tables passed by value to the factor / solve kernels.
+struct SlotTables {
+  int nslots, nf, diag, nlower, nupper;
+  int off[kMaxSlots][3];
+  int lower[kMaxSlots];
+  int upper[kMaxSlots];
+  int npairs[kMaxSlots];
+  int pair_b[kMaxSlots][kMaxSlots];
+  int pair_t[kMaxSlots][kMaxSlots];
+};
+
+// Host-side box tables before upload (precond.cu).
+struct HostBoxes {
+  std::vector<int> gidx, nbr, box_lev_off, lev_ptr, box_pos_off;
+  long long P = 0;
+  int max_levels = 0, max_width = 0;
+};
+
+}  // namespace nks
+
+struct nks_state {
+  nks_grid grid;
+  nks_params prm;
+  nks::DevParams dp;
+  cudaStream_t stream = nullptr;
+  int d = 2, nf = 4;
+  long long N = 0;          // points
+  long long nvec = 0;       // nf * N
+  // workspace carve
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  double* Xn = nullptr;     // X^n
+  double* Xprev = nullptr;  // X^{n-1}
+  double* Xb = nullptr;     // Newton iterate
+  double* Xt = nullptr;     // line-search trial
+  double* S = nullptr;      // Newton direction
+  double* F = nullptr;
+  double* Ft = nullptr;
+  double* Ta = nullptr;     // T^n = tr sigma^el(u^n, c^n)
+  double* jac4 = nullptr;   // a11, a12, a21, a22 pointwise partials (4N)
+  double* V = nullptr;      // Krylov basis (m+1) * nvec
+  double* Z = nullptr;      // preconditioned vector / scratch (nvec)
+  double* W2 = nullptr;     // scratch (nvec)
+  double* red_part = nullptr;   // reduction partials [kRedBlocks * 64]
+  double* red_out = nullptr;    // reduction results [64]
+  double* h_red = nullptr;      // pinned host mirror [64]
+  // preconditioner
+  nks::BoxSet boxes;
+  double* fac = nullptr;    // [nslots][nf][nf][P]
+  double* ybox = nullptr;   // [nf][P]
+  bool pc_valid = false;
+  double pc_dt = 0.0;
+  // history / controller
+  double time = 0.0;
+  double dt_prev = 0.0;
+  double zeta = 0.0;
+  bool have_fields = false;
+  bool have_prev = false;
+  // counters
+  long long launches = 0;
+  long long syncs = 0;
+  // phase profiling (CUDA events on this stream)
+  bool profile = false;
+  double phase_ms[8] = {0};
+  long long phase_cnt[8] = {0};
+  std::vector<cudaEvent_t> ev_pool;          // free events
+  std::vector<int> pend_phase;                // pending (phase, start, end)
+  std::vector<cudaEvent_t> pend_ev;
+  int cur_phase = -1;
+  cudaEvent_t cur_ev = nullptr;
+  std::string err;
+};

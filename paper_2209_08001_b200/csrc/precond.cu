@@ -1,0 +1,498 @@
+// Restricted additive Schwarz preconditioner with point-block ILU(0) subdomain solves (P:581-586,
+// P:789-797): box geometry (host), analytic point-block Jacobian assembly (K4), level-scheduled
+// BILU(0) factorisation (K5) and the RAS apply with forward/backward wavefront sweeps (K6).
+//
+// Boxes (R19/R20): nsub_j boxes per axis, the first n_j mod nsub_j one cell longer,
+// each extended by delta cells per side into a NON-periodic local grid (an axis with one box
+// self-overlaps across the periodic seam).  Local natural order (x fastest); level of a local
+// point l = lx + 2 ly + 3 lz (the exact dependency depth of the |o|_1 <= 2 block pattern, R21;
+// i+j+k would violate the (1,-1,0)/(1,0,-1)/(0,1,-1) couplings).  Box-local arrays are stored in
+// level order ("positions") so one level is a contiguous, coalesced range.
+#include <algorithm>
+#include <numeric>
+
+#include "nks_internal.cuh"
+
+namespace nks {
+
+// ------------------------------------------------------------------------------------------ host geometry
+static long long nat_key(const int o[3]) { return ((long long)o[2] * 64 + o[1]) * 64 + o[0]; }
+
+void build_slot_tables(int dim, BoxSet& B) {
+  int cnt = 0;
+  int offs[kMaxSlots][3];
+  for (int oz = (dim == 3 ? -2 : 0); oz <= (dim == 3 ? 2 : 0); ++oz)
+    for (int oy = -2; oy <= 2; ++oy)
+      for (int ox = -2; ox <= 2; ++ox)
+        if (std::abs(ox) + std::abs(oy) + std::abs(oz) <= 2) {
+          offs[cnt][0] = ox; offs[cnt][1] = oy; offs[cnt][2] = oz; ++cnt;
+        }
+  // sort by natural order key
+  int idx[kMaxSlots];
+  std::iota(idx, idx + cnt, 0);
+  std::sort(idx, idx + cnt, [&](int a, int b) { return nat_key(offs[a]) < nat_key(offs[b]); });
+  B.nslots = cnt;
+  B.nlower = B.nupper = 0;
+  for (int s = 0; s < cnt; ++s) {
+    for (int k = 0; k < 3; ++k) B.off[s][k] = offs[idx[s]][k];
+    const long long key = nat_key(B.off[s]);
+    if (key < 0) B.lower[B.nlower++] = s;
+    else if (key > 0) B.upper[B.nupper++] = s;
+    else B.diag = s;
+  }
+  auto find = [&](int ox, int oy, int oz) {
+    for (int s = 0; s < cnt; ++s)
+      if (B.off[s][0] == ox && B.off[s][1] == oy && B.off[s][2] == oz) return s;
+    return -1;
+  };
+  for (int ia = 0; ia < B.nlower; ++ia) {
+    const int sa = B.lower[ia];
+    B.npairs[ia] = 0;
+    for (int ib = 0; ib < B.nupper; ++ib) {
+      const int sb = B.upper[ib];
+      const int t = find(B.off[sa][0] + B.off[sb][0], B.off[sa][1] + B.off[sb][1], B.off[sa][2] + B.off[sb][2]);
+      if (t < 0) continue;
+      B.pair_b[ia][B.npairs[ia]] = sb;
+      B.pair_t[ia][B.npairs[ia]] = t;
+      ++B.npairs[ia];
+    }
+  }
+}
+
+
+static void split_axis(int n, int nsub, std::vector<int>& start, std::vector<int>& len) {
+  const int base = n / nsub, rem = n % nsub;
+  int s = 0;
+  for (int b = 0; b < nsub; ++b) {
+    const int l = base + (b < rem ? 1 : 0);
+    start.push_back(s);
+    len.push_back(l);
+    s += l;
+  }
+}
+
+long long box_positions(const nks_grid& g) {
+  std::vector<int> st[3], ln[3];
+  long long P = 0;
+  for (int j = 0; j < 3; ++j) split_axis(g.n[j], g.nsub[j], st[j], ln[j]);
+  const int dz = g.dim == 3 ? g.overlap : 0;
+  for (int bz = 0; bz < g.nsub[2]; ++bz)
+    for (int by = 0; by < g.nsub[1]; ++by)
+      for (int bx = 0; bx < g.nsub[0]; ++bx)
+        P += (long long)(ln[0][bx] + 2 * g.overlap) * (ln[1][by] + 2 * g.overlap) * (ln[2][bz] + 2 * dz);
+  return P;
+}
+
+HostBoxes build_boxes_host(const nks_grid& g, const BoxSet& B) {
+  HostBoxes H;
+  std::vector<int> st[3], ln[3];
+  for (int j = 0; j < 3; ++j) split_axis(g.n[j], g.nsub[j], st[j], ln[j]);
+  const int delta = g.overlap;
+  const int dz = g.dim == 3 ? delta : 0;
+  H.P = box_positions(g);
+  H.gidx.assign(H.P, 0);
+  H.nbr.assign((size_t)B.nslots * H.P, -1);
+  H.box_pos_off.push_back(0);
+  H.box_lev_off.push_back(0);
+  long long base = 0;
+  for (int bz = 0; bz < g.nsub[2]; ++bz)
+    for (int by = 0; by < g.nsub[1]; ++by)
+      for (int bx = 0; bx < g.nsub[0]; ++bx) {
+        const int e[3] = {ln[0][bx] + 2 * delta, ln[1][by] + 2 * delta, ln[2][bz] + 2 * dz};
+        const int s0[3] = {st[0][bx] - delta, st[1][by] - delta, st[2][bz] - dz};
+        const int own[3] = {ln[0][bx], ln[1][by], ln[2][bz]};
+        const int d0[3] = {delta, delta, dz};
+        const long long np = (long long)e[0] * e[1] * e[2];
+        const int nlev = (e[0] - 1) + 2 * (e[1] - 1) + 3 * (e[2] - 1) + 1;
+        // counting sort by level, natural order within a level
+        std::vector<int> count(nlev + 1, 0);
+        for (int lz = 0; lz < e[2]; ++lz)
+          for (int ly = 0; ly < e[1]; ++ly)
+            for (int lx = 0; lx < e[0]; ++lx) count[lx + 2 * ly + 3 * lz + 1]++;
+        for (int l = 0; l < nlev; ++l) count[l + 1] += count[l];
+        std::vector<int> lvstart(count.begin(), count.end());
+        for (int l = 0; l < nlev; ++l) H.max_width = std::max(H.max_width, count[l + 1] - count[l]);
+        H.max_levels = std::max(H.max_levels, nlev);
+        std::vector<int> posof(np);
+        std::vector<int> fill(count.begin(), count.end() - 1);
+        for (int lz = 0; lz < e[2]; ++lz)
+          for (int ly = 0; ly < e[1]; ++ly)
+            for (int lx = 0; lx < e[0]; ++lx) {
+              const int lin = (lz * e[1] + ly) * e[0] + lx;
+              posof[lin] = fill[lx + 2 * ly + 3 * lz]++;
+            }
+        for (int lz = 0; lz < e[2]; ++lz)
+          for (int ly = 0; ly < e[1]; ++ly)
+            for (int lx = 0; lx < e[0]; ++lx) {
+              const int lin = (lz * e[1] + ly) * e[0] + lx;
+              const long long pos = base + posof[lin];
+              const int l[3] = {lx, ly, lz};
+              int gc[3];
+              bool owned = true;
+              for (int j = 0; j < 3; ++j) {
+                int v = (s0[j] + l[j]) % g.n[j];
+                if (v < 0) v += g.n[j];
+                gc[j] = v;
+                if (l[j] < d0[j] || l[j] >= d0[j] + own[j]) owned = false;
+              }
+              const int gi = (gc[2] * g.n[1] + gc[1]) * g.n[0] + gc[0];
+              H.gidx[pos] = owned ? gi : ~gi;
+              for (int s = 0; s < B.nslots; ++s) {
+                const int q[3] = {lx + B.off[s][0], ly + B.off[s][1], lz + B.off[s][2]};
+                if (q[0] < 0 || q[0] >= e[0] || q[1] < 0 || q[1] >= e[1] || q[2] < 0 || q[2] >= e[2]) continue;
+                const int qlin = (q[2] * e[1] + q[1]) * e[0] + q[0];
+                H.nbr[(size_t)s * H.P + pos] = (int)(base + posof[qlin]);
+              }
+            }
+        for (int l = 0; l <= nlev; ++l) H.lev_ptr.push_back((int)(base + lvstart[l]));
+        H.box_lev_off.push_back((int)H.lev_ptr.size());
+        base += np;
+        H.box_pos_off.push_back((int)base);
+      }
+  return H;
+}
+
+// ------------------------------------------------------------------------------------------ K4 assembly
+__device__ __forceinline__ int wrapi(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
+
+// Block (nf x nf) of J at grid point (x,y,z), column point (x,y,z)+o.  Rows/cols: c, eta, u_1..u_d.
+__device__ void jac_block(const DevParams& P, const double* __restrict__ Xa, const double* __restrict__ jac4,
+                          int x, int y, int z, const int o[3], double* blk, int nf) {
+  const int d = P.dim;
+  const long long N = P.N;
+  auto gid = [&](int dx, int dy, int dz) -> long long {
+    return ((long long)wrapi(z + dz, P.nz) * P.ny + wrapi(y + dy, P.ny)) * P.nx + wrapi(x + dx, P.nx);
+  };
+  for (int k = 0; k < nf * nf; ++k) blk[k] = 0.0;
+  const int l1 = abs(o[0]) + abs(o[1]) + abs(o[2]);
+  const double ih2 = P.inv_h2;
+  // ---- c row: -sum_a W_{i,i+a} dG_c(i+a)/dX(i+o)  (+ 1/dt on the diagonal)
+  {
+    const double cai = Xa[gid(0, 0, 0)];
+    const double mi = cai * (1.0 - cai);
+    const double beta_nb = -0.5 * P.gamma_c * ih2;                 // dG4_c(k)/dc(k +- e_L)
+    const double cT = 0.5 * P.K * d * P.eps0 * P.eps0 + P.gamma_c * d * ih2;   // diag extra of dG_c/dc
+    // a in {0, +-e_J}
+    for (int ia = 0; ia < 2 * d + 1; ++ia) {
+      int a[3] = {0, 0, 0};
+      double wa;
+      if (ia == 0) {
+        double s = 0.0;
+        for (int J = 0; J < d; ++J) {
+          int e1[3] = {0, 0, 0};
+          e1[J] = 1;
+          const double cp = Xa[gid(e1[0], e1[1], e1[2])], cm = Xa[gid(-e1[0], -e1[1], -e1[2])];
+          s += (mi + cp * (1.0 - cp)) + (mi + cm * (1.0 - cm));
+        }
+        wa = 0.5 * P.kappa * s * ih2;           // -W_ii
+      } else {
+        const int J = (ia - 1) / 2, sg = ((ia - 1) % 2 == 0) ? 1 : -1;
+        a[J] = sg;
+        const double cn = Xa[gid(a[0], a[1], a[2])];
+        wa = -0.5 * P.kappa * (mi + cn * (1.0 - cn)) * ih2;   // -W_{i,i+a}
+      }
+      const int b[3] = {o[0] - a[0], o[1] - a[1], o[2] - a[2]};
+      const int bl1 = abs(b[0]) + abs(b[1]) + abs(b[2]);
+      if (bl1 > 1) continue;
+      const long long k = gid(a[0], a[1], a[2]);
+      if (bl1 == 0) {
+        blk[0 * nf + 0] += wa * (jac4[k] + cT);
+        blk[0 * nf + 1] += wa * jac4[N + k];
+      } else {
+        int L = b[0] != 0 ? 0 : (b[1] != 0 ? 1 : 2);
+        const int s = b[L];
+        blk[0 * nf + 0] += wa * beta_nb;
+        blk[0 * nf + 2 + L] += wa * (-P.eps0 * P.K * s * 0.25 / P.h);
+      }
+    }
+    if (l1 == 0) blk[0] += P.inv_dt;
+  }
+  // ---- eta row
+  {
+    const long long i = gid(0, 0, 0);
+    if (l1 == 0) {
+      blk[1 * nf + 0] = jac4[2 * N + i];
+      blk[1 * nf + 1] = P.inv_dt + jac4[3 * N + i] + 3.0 * P.gamma_eta * d * ih2;
+    } else if (l1 == 1) {
+      blk[1 * nf + 1] = -1.5 * P.gamma_eta * ih2;
+    }
+  }
+  // ---- u rows
+  const double e4 = P.Ls * P.inv_4h2;
+  for (int I = 0; I < d; ++I) {
+    double* row = blk + (2 + I) * nf;
+    if (l1 == 0) {
+      row[2 + I] = e4 * (-2.0 * P.C11 - 2.0 * P.C44 * (d - 1));
+    } else if (l1 == 2) {
+      // +-2 e_J ?
+      int nz = 0, J = -1;
+      for (int k = 0; k < 3; ++k)
+        if (o[k] != 0) { ++nz; J = k; }
+      if (nz == 1) {
+        row[2 + I] = e4 * (J == I ? P.C11 : P.C44);
+      } else {
+        // o = s e_I + t e_M (M != I)
+        if (o[I] != 0) {
+          for (int M = 0; M < d; ++M)
+            if (M != I && o[M] != 0) row[2 + M] = e4 * (P.C12 + P.C44) * o[I] * o[M];
+        }
+      }
+    } else if (l1 == 1) {
+      if (o[I] != 0) row[0] = -P.K * P.eps0 * o[I] * P.inv_2h;
+    }
+  }
+}
+
+__global__ void k_assemble(DevParams P, SlotTables T, const double* __restrict__ Xa, const double* __restrict__ jac4,
+                           const int* __restrict__ gidx, const int* __restrict__ nbr, long long Ptot,
+                           double* __restrict__ fac) {
+  const int nf = T.nf;
+  const long long total = Ptot * T.nslots;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const long long pos = t % Ptot;
+    const int s = (int)(t / Ptot);
+    double blk[kMaxNf * kMaxNf];
+    if (nbr[(long long)s * Ptot + pos] < 0) {
+      for (int k = 0; k < nf * nf; ++k) blk[k] = 0.0;
+    } else {
+      int gi = gidx[pos];
+      if (gi < 0) gi = ~gi;
+      const int x = gi % P.nx, y = (gi / P.nx) % P.ny, z = gi / (P.nx * P.ny);
+      jac_block(P, Xa, jac4, x, y, z, T.off[s], blk, nf);
+    }
+    for (int k = 0; k < nf * nf; ++k) fac[((long long)s * nf * nf + k) * Ptot + pos] = blk[k];
+  }
+}
+
+// ------------------------------------------------------------------------------------------ K5 factorisation
+template <int NF>
+__device__ __forceinline__ void load_blk(const double* fac, int s, long long pos, long long Ptot, double (&b)[NF][NF]) {
+#pragma unroll
+  for (int r = 0; r < NF; ++r)
+#pragma unroll
+    for (int c = 0; c < NF; ++c) b[r][c] = fac[((long long)(s * NF + r) * NF + c) * Ptot + pos];
+}
+template <int NF>
+__device__ __forceinline__ void store_blk(double* fac, int s, long long pos, long long Ptot, const double (&b)[NF][NF]) {
+#pragma unroll
+  for (int r = 0; r < NF; ++r)
+#pragma unroll
+    for (int c = 0; c < NF; ++c) fac[((long long)(s * NF + r) * NF + c) * Ptot + pos] = b[r][c];
+}
+
+// In-register Gauss-Jordan inverse with partial pivoting.
+template <int NF>
+__device__ __forceinline__ void invert(double (&a)[NF][NF]) {
+  double inv[NF][NF];
+#pragma unroll
+  for (int r = 0; r < NF; ++r)
+#pragma unroll
+    for (int c = 0; c < NF; ++c) inv[r][c] = r == c ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = 0; k < NF; ++k) {
+    int piv = k;
+    double best = fabs(a[k][k]);
+#pragma unroll
+    for (int r = k + 1; r < NF; ++r)
+      if (fabs(a[r][k]) > best) { best = fabs(a[r][k]); piv = r; }
+    if (piv != k) {
+#pragma unroll
+      for (int r = k + 1; r < NF; ++r)
+        if (r == piv) {
+#pragma unroll
+          for (int c = 0; c < NF; ++c) {
+            double t = a[k][c]; a[k][c] = a[r][c]; a[r][c] = t;
+            t = inv[k][c]; inv[k][c] = inv[r][c]; inv[r][c] = t;
+          }
+        }
+    }
+    const double ip = 1.0 / a[k][k];
+#pragma unroll
+    for (int c = 0; c < NF; ++c) { a[k][c] *= ip; inv[k][c] *= ip; }
+#pragma unroll
+    for (int r = 0; r < NF; ++r) {
+      if (r == k) continue;
+      const double f = a[r][k];
+#pragma unroll
+      for (int c = 0; c < NF; ++c) { a[r][c] -= f * a[k][c]; inv[r][c] -= f * inv[k][c]; }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < NF; ++r)
+#pragma unroll
+    for (int c = 0; c < NF; ++c) a[r][c] = inv[r][c];
+}
+
+template <int NF>
+__global__ void k_bilu0(SlotTables T, const int* __restrict__ nbr, const int* __restrict__ box_lev_off,
+                        const int* __restrict__ lev_ptr, long long Ptot, double* fac) {
+  const int b = blockIdx.x;
+  const int l0 = box_lev_off[b], l1 = box_lev_off[b + 1] - 1;     // levels l0 .. l1-1
+  for (int l = l0; l < l1; ++l) {
+    const int p0 = lev_ptr[l], p1 = lev_ptr[l + 1];
+    for (int pos = p0 + threadIdx.x; pos < p1; pos += blockDim.x) {
+      for (int ia = 0; ia < T.nlower; ++ia) {
+        const int sa = T.lower[ia];
+        const int k = nbr[(long long)sa * Ptot + pos];
+        if (k < 0) continue;
+        double A[NF][NF], D[NF][NF], Lk[NF][NF];
+        load_blk<NF>(fac, sa, pos, Ptot, A);
+        load_blk<NF>(fac, T.diag, k, Ptot, D);       // U_kk^{-1}
+#pragma unroll
+        for (int r = 0; r < NF; ++r)
+#pragma unroll
+          for (int c = 0; c < NF; ++c) {
+            double s = 0.0;
+#pragma unroll
+            for (int m = 0; m < NF; ++m) s = fma(A[r][m], D[m][c], s);
+            Lk[r][c] = s;
+          }
+        store_blk<NF>(fac, sa, pos, Ptot, Lk);
+        for (int ip = 0; ip < T.npairs[ia]; ++ip) {
+          const int sb = T.pair_b[ia][ip], st = T.pair_t[ia][ip];
+          if (nbr[(long long)st * Ptot + pos] < 0) continue;
+          double U[NF][NF], Tt[NF][NF];
+          load_blk<NF>(fac, sb, k, Ptot, U);
+          load_blk<NF>(fac, st, pos, Ptot, Tt);
+#pragma unroll
+          for (int r = 0; r < NF; ++r)
+#pragma unroll
+            for (int c = 0; c < NF; ++c) {
+              double s = Tt[r][c];
+#pragma unroll
+              for (int m = 0; m < NF; ++m) s = fma(-Lk[r][m], U[m][c], s);
+              Tt[r][c] = s;
+            }
+          store_blk<NF>(fac, st, pos, Ptot, Tt);
+        }
+      }
+      double Dg[NF][NF];
+      load_blk<NF>(fac, T.diag, pos, Ptot, Dg);
+      invert<NF>(Dg);
+      store_blk<NF>(fac, T.diag, pos, Ptot, Dg);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------------------ K6 RAS apply
+template <int NF>
+__global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const int* __restrict__ nbr,
+                            const int* __restrict__ box_lev_off, const int* __restrict__ lev_ptr,
+                            const int* __restrict__ box_pos_off, long long Ptot, long long N,
+                            const double* __restrict__ fac, const double* __restrict__ r, double* y,
+                            double* __restrict__ z) {
+  const int b = blockIdx.x;
+  const int q0 = box_pos_off[b], q1 = box_pos_off[b + 1];
+  // R_i^delta r
+  for (int pos = q0 + threadIdx.x; pos < q1; pos += blockDim.x) {
+    int gi = gidx[pos];
+    if (gi < 0) gi = ~gi;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) y[f * Ptot + pos] = r[f * N + gi];
+  }
+  __syncthreads();
+  const int l0 = box_lev_off[b], l1 = box_lev_off[b + 1] - 1;
+  // forward: y_i -= sum_{k<i} L_ik y_k
+  for (int l = l0; l < l1; ++l) {
+    const int p0 = lev_ptr[l], p1 = lev_ptr[l + 1];
+    for (int pos = p0 + threadIdx.x; pos < p1; pos += blockDim.x) {
+      double acc[NF];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) acc[f] = y[f * Ptot + pos];
+      for (int ia = 0; ia < T.nlower; ++ia) {
+        const int sa = T.lower[ia];
+        const int k = nbr[(long long)sa * Ptot + pos];
+        if (k < 0) continue;
+        double yk[NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) yk[f] = y[f * Ptot + k];
+#pragma unroll
+        for (int rr = 0; rr < NF; ++rr)
+#pragma unroll
+          for (int c = 0; c < NF; ++c) acc[rr] = fma(-fac[((long long)(sa * NF + rr) * NF + c) * Ptot + pos], yk[c], acc[rr]);
+      }
+#pragma unroll
+      for (int f = 0; f < NF; ++f) y[f * Ptot + pos] = acc[f];
+    }
+    __syncthreads();
+  }
+  // backward: x_i = U_ii^{-1} (y_i - sum_{j>i} U_ij x_j)
+  for (int l = l1 - 1; l >= l0; --l) {
+    const int p0 = lev_ptr[l], p1 = lev_ptr[l + 1];
+    for (int pos = p0 + threadIdx.x; pos < p1; pos += blockDim.x) {
+      double acc[NF];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) acc[f] = y[f * Ptot + pos];
+      for (int iu = 0; iu < T.nupper; ++iu) {
+        const int su = T.upper[iu];
+        const int j = nbr[(long long)su * Ptot + pos];
+        if (j < 0) continue;
+        double xj[NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) xj[f] = y[f * Ptot + j];
+#pragma unroll
+        for (int rr = 0; rr < NF; ++rr)
+#pragma unroll
+          for (int c = 0; c < NF; ++c) acc[rr] = fma(-fac[((long long)(su * NF + rr) * NF + c) * Ptot + pos], xj[c], acc[rr]);
+      }
+      double xo[NF];
+#pragma unroll
+      for (int rr = 0; rr < NF; ++rr) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < NF; ++c) s = fma(fac[((long long)(T.diag * NF + rr) * NF + c) * Ptot + pos], acc[c], s);
+        xo[rr] = s;
+      }
+#pragma unroll
+      for (int f = 0; f < NF; ++f) y[f * Ptot + pos] = xo[f];
+    }
+    __syncthreads();
+  }
+  // R_i^{0T}: owned points only
+  for (int pos = q0 + threadIdx.x; pos < q1; pos += blockDim.x) {
+    const int gi = gidx[pos];
+    if (gi < 0) continue;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) z[f * N + gi] = y[f * Ptot + pos];
+  }
+}
+
+// ------------------------------------------------------------------------------------------ host launchers
+SlotTables make_tables(const BoxSet& B, int nf) {
+  SlotTables T;
+  T.nslots = B.nslots; T.nf = nf; T.diag = B.diag; T.nlower = B.nlower; T.nupper = B.nupper;
+  for (int s = 0; s < kMaxSlots; ++s) {
+    for (int k = 0; k < 3; ++k) T.off[s][k] = B.off[s][k];
+    T.lower[s] = B.lower[s]; T.upper[s] = B.upper[s]; T.npairs[s] = B.npairs[s];
+    for (int p = 0; p < kMaxSlots; ++p) { T.pair_b[s][p] = B.pair_b[s][p]; T.pair_t[s][p] = B.pair_t[s][p]; }
+  }
+  return T;
+}
+
+void launch_assemble(const DevParams& P, const BoxSet& B, int nf, const double* Xa, const double* jac4, double* fac,
+                     cudaStream_t s) {
+  const SlotTables T = make_tables(B, nf);
+  const long long total = B.P * B.nslots;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 32);
+  k_assemble<<<blocks, 256, 0, s>>>(P, T, Xa, jac4, B.gidx, B.nbr, B.P, fac);
+}
+
+void launch_factor(const BoxSet& B, int nf, double* fac, cudaStream_t s) {
+  const SlotTables T = make_tables(B, nf);
+  const int threads = std::min(256, std::max(32, ((B.max_level_width + 31) / 32) * 32));
+  if (nf == 4) k_bilu0<4><<<B.nbox, threads, 0, s>>>(T, B.nbr, B.box_lev_off, B.lev_ptr, B.P, fac);
+  else k_bilu0<5><<<B.nbox, threads, 0, s>>>(T, B.nbr, B.box_lev_off, B.lev_ptr, B.P, fac);
+}
+
+void launch_ras_apply(const BoxSet& B, int nf, long long N, const double* fac, const double* r, double* y, double* z,
+                      cudaStream_t s) {
+  const SlotTables T = make_tables(B, nf);
+  const int threads = std::min(256, std::max(32, ((B.max_level_width + 31) / 32) * 32));
+  if (nf == 4)
+    k_ras_apply<4><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, N, fac, r, y, z);
+  else
+    k_ras_apply<5><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, N, fac, r, y, z);
+}
+
+}  // namespace nks

@@ -1,0 +1,108 @@
+"""C-ABI checks that need no GPU: the library builds for sm_100a, loads, exports every symbol
+include/nks.h declares, and its struct layouts match the Python binding byte for byte."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+import nks_inputs as ni
+from paper_2209_08001_b200 import build, nks
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "nks.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build.build()
+    return nks.load_library()
+
+
+def declared_functions():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"NKS_API\s+[\w\s\*]+?\b(nks_\w+)\s*\(", txt)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ["nks_create", "nks_step", "nks_run_adaptive", "nks_set_fields", "nks_get_fields",
+                 "nks_eval_residual", "nks_eval_jv", "nks_pc_setup", "nks_pc_apply", "nks_gmres_solve",
+                 "nks_energy", "nks_destroy", "nks_workspace_bytes"]:
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", nks.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\sT\s(nks_\w+)", out))
+    for name in declared_functions():
+        assert name in exported, name
+        assert hasattr(lib, name)
+    # and nothing else leaks out of the .so under the nks_ prefix
+    assert exported == set(declared_functions())
+
+
+def test_binding_signatures_cover_header(lib):
+    assert set(nks._SIGS) == set(declared_functions())
+
+
+def test_struct_layout_matches_c(tmp_path):
+    src = tmp_path / "probe.c"
+    src.write_text(r'''
+#include <stdio.h>
+#include <stddef.h>
+#include "nks.h"
+#define F(T, m) printf("%s.%s %zu\n", #T, #m, offsetof(T, m));
+int main(void) {
+  printf("nks_grid %zu\n", sizeof(nks_grid));
+  printf("nks_params %zu\n", sizeof(nks_params));
+  printf("nks_step_info %zu\n", sizeof(nks_step_info));
+  F(nks_grid, h) F(nks_grid, nsub) F(nks_grid, overlap)
+  F(nks_params, S) F(nks_params, newton_rtol) F(nks_params, pc_reuse) F(nks_params, ls_alpha)
+  F(nks_params, zeta) F(nks_params, xd_norm)
+  F(nks_step_info, dt) F(nks_step_info, energy_parts) F(nks_step_info, mass) F(nks_step_info, xd)
+  return 0;
+}
+''')
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
+    assert int(got["nks_grid"]) == C.sizeof(nks.Grid)
+    assert int(got["nks_params"]) == C.sizeof(nks.Params)
+    assert int(got["nks_step_info"]) == C.sizeof(nks.StepInfo)
+    for key, val in got.items():
+        if "." in key:
+            t, m = key.split(".")
+            cls = {"nks_grid": nks.Grid, "nks_params": nks.Params, "nks_step_info": nks.StepInfo}[t]
+            assert getattr(cls, m).offset == int(val), key
+
+
+def test_workspace_bytes_validates(lib):
+    p = nks.make_params(ni.model_default(), ni.solver_default())
+    g = nks.make_grid((64, 64), 0.25, (1, 1), 2)
+    nb = lib.nks_workspace_bytes(C.byref(g), C.byref(p))
+    assert nb > 64 * 64 * 4 * 8 * 30
+    bad = nks.make_grid((4, 64), 0.25, (1, 1), 2)        # n < 5 would alias the radius-2 stencil
+    assert lib.nks_workspace_bytes(C.byref(bad), C.byref(p)) == 0
+    p2 = nks.make_params(ni.model_default(), ni.solver_default())
+    p2.S = 0
+    assert lib.nks_workspace_bytes(C.byref(g), C.byref(p2)) == 0
+    g3 = nks.make_grid((16, 16, 16), 0.25, (2, 2, 2), 2)
+    assert lib.nks_workspace_bytes(C.byref(g3), C.byref(p)) > 0
+
+
+def test_null_arguments_rejected_without_device(lib):
+    assert lib.nks_create(None, None, None, 0, None, None) == nks.NKS_E_INVALID
+    assert lib.nks_step(None, C.c_double(0.01), None) == nks.NKS_E_INVALID
+    assert lib.nks_destroy(None) == nks.NKS_E_INVALID
+    assert b"nks-b200" in lib.nks_version()
+
+
+def test_no_cpu_fallback_in_product():
+    """The product package never imports the oracle."""
+    pkg = os.path.join(ROOT, "paper_2209_08001_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            txt = open(os.path.join(pkg, fn)).read()
+            assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", txt, flags=re.M), fn

@@ -1,0 +1,287 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Tolerances: pointwise operators (F, J.v, energy) are the same fp64
+arithmetic in a different order -> 1e-12 relative to the field's max magnitude; solves are
+compared at BASELINE.json's bar (fields rel. L2 <= 1e-8, energy rel. <= 1e-10, mass drift
+<= 1e-12).
+"""
+import numpy as np
+import pytest
+
+import nks_inputs as ni
+from oracle import jacobian, pc, scheme, solver
+
+pytestmark = pytest.mark.gpu
+
+MODEL = ni.model_default()
+SOL = ni.solver_default()
+
+
+def gpu_solver(shape, nsub=None, overlap=2, pc_type=2, **kw):
+    from paper_2209_08001_b200 import Solver
+    sol = dict(SOL)
+    sol.update(kw.pop("sol", {}))
+    return Solver(shape, MODEL, sol, h=0.25, nsub=nsub or (1,) * len(shape), overlap=overlap, pc_type=pc_type, **kw)
+
+
+def oracle_model(d):
+    return scheme.Model.from_dict(d, 0.25, MODEL)
+
+
+def states(shape, seed=0, amp=2e-3):
+    d = len(shape)
+    ca, ea = ni.initial_fields(shape, seed)
+    ua = ni.random_displacement(d, shape, seed + 2, 1e-3)
+    Xa = np.concatenate([ca[None], ea[None], ua])
+    cb, eb = ni.perturbed_state(ca, ea, seed + 1, amp)
+    Xb = np.concatenate([cb[None], eb[None], ua + ni.random_displacement(d, shape, seed + 3, 1e-4)])
+    return Xa, Xb
+
+
+def field_rel_err(a, b):
+    """max |a-b| / max |b| per field."""
+    return [float(np.abs(a[f] - b[f]).max() / max(np.abs(b[f]).max(), 1e-300)) for f in range(a.shape[0])]
+
+
+SHAPES = [(40, 36), (12, 20, 36), (64, 64), (9, 7, 11)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_residual_parity(shape):
+    d = len(shape)
+    Xa, Xb = states(shape)
+    g = gpu_solver(shape)
+    g.set_fields(Xa[0], Xa[1], Xa[2:])
+    cbar = Xa[0].mean()
+    for dt in (0.01, 1.7):
+        Fg = g.eval_residual(Xb, dt).cpu().numpy()
+        Fo = scheme.residual(oracle_model(d), Xa, Xb, dt, cbar)
+        errs = field_rel_err(Fg, Fo)
+        assert max(errs) < 1e-12, errs
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_jv_parity(shape):
+    d = len(shape)
+    Xa, Xb = states(shape)
+    v = ni.random_direction(2 + d, shape, 7)
+    g = gpu_solver(shape)
+    g.set_fields(Xa[0], Xa[1], Xa[2:])
+    for dt in (0.01, 2.0):
+        Jg = g.eval_jv(Xb, v, dt).cpu().numpy()
+        Jo = jacobian.jv(oracle_model(d), Xa, Xb, dt, v)
+        errs = field_rel_err(Jg, Jo)
+        assert max(errs) < 1e-12, errs
+
+
+@pytest.mark.parametrize("shape", [(40, 36), (12, 20, 36)])
+def test_energy_and_mass_parity(shape):
+    d = len(shape)
+    Xa, _ = states(shape)
+    g = gpu_solver(shape)
+    g.set_fields(Xa[0], Xa[1], Xa[2:])
+    parts, mass = g.energy()
+    # the library projects u onto the canonical gauge; E3 is gauge invariant
+    ref = scheme.energy_parts(oracle_model(d), Xa, Xa[0].mean())
+    for a, b in zip(parts, ref):
+        assert a == pytest.approx(b, rel=1e-12, abs=1e-12)
+    assert mass == pytest.approx(scheme.mass(oracle_model(d), Xa), rel=1e-14)
+
+
+@pytest.mark.parametrize("shape", [(64, 64), (36, 40), (8, 12, 10), (7, 9)])
+def test_initial_displacement_and_gauge(shape):
+    d = len(shape)
+    c, eta = ni.initial_fields(shape, 3)
+    g = gpu_solver(shape)
+    g.set_fields(c, eta, None)
+    X = g.get_state()
+    uo = solver.init_displacement(oracle_model(d), c, c.mean())
+    scale = np.abs(uo).max()
+    assert np.abs(X[2:] - uo).max() <= 1e-10 * scale
+    np.testing.assert_array_equal(X[0], c)
+
+
+def test_set_fields_host_path_and_errors():
+    from paper_2209_08001_b200 import NKSError
+    shape = (16, 16)
+    c, eta = ni.initial_fields(shape, 0)
+    g = gpu_solver(shape)
+    g.set_fields_host(c, eta)
+    X = g.get_state()
+    np.testing.assert_array_equal(X[1], eta)
+    bad = eta.copy()
+    bad[3, 4] = -0.2          # p = c*eta < 0: outside the domain of Psi
+    with pytest.raises(NKSError):
+        g.set_fields(c, bad)
+
+
+# ---------------------------------------------------------------------------------------- preconditioner
+
+PC_CASES = [((16, 16), (2, 2), 2), ((12, 14), (1, 1), 2), ((10, 13), (3, 2), 1), ((6, 7, 6), (1, 1, 2), 1),
+            ((16, 16), (4, 4), 0)]
+
+
+@pytest.mark.parametrize("shape,nsub,delta", PC_CASES)
+def test_ras_bilu0_apply_parity(shape, nsub, delta):
+    d = len(shape)
+    nf = 2 + d
+    Xa, Xb = states(shape)
+    dt = 0.3
+    g = gpu_solver(shape, nsub=nsub, overlap=delta)
+    g.set_fields(Xa[0], Xa[1], Xa[2:])
+    g.pc_setup(Xb, dt)
+    r = ni.random_direction(nf, shape, 11)
+    zg = g.pc_apply(r).cpu().numpy()
+    J = jacobian.assemble(oracle_model(d), Xa, Xb, dt)
+    ras = pc.RAS(J, shape, nf, tuple(reversed(nsub)), delta)
+    zo = ras.apply(r)
+    errs = field_rel_err(zg, zo)
+    assert max(errs) < 1e-10, errs
+
+
+@pytest.mark.parametrize("shape,nsub", [((24, 24), (2, 2)), ((8, 8, 8), (2, 1, 1))])
+def test_gmres_solves_the_newton_system(shape, nsub):
+    d = len(shape)
+    Xa, Xb = states(shape)
+    dt = 0.5
+    m = oracle_model(d)
+    Fo = scheme.residual(m, Xa, Xb, dt, Xa[0].mean())
+    g = gpu_solver(shape, nsub=nsub, sol={"gmres_rtol": 1e-12})
+    g.set_fields(Xa[0], Xa[1], Xa[2:])
+    s, its = g.gmres_solve(Xb, -Fo, dt)
+    s = s.cpu().numpy()
+    J = jacobian.assemble(m, Xa, Xb, dt)
+    res = J @ s.ravel() + Fo.ravel()
+    assert np.linalg.norm(res) <= 1e-11 * np.linalg.norm(Fo)
+    # the same Newton direction as the oracle's pinned direct solve (up to the gauge null space)
+    import scipy.sparse.linalg as spla
+    A, b = solver.pin(J, -Fo.ravel(), solver.pinned_rows(shape, d))
+    so = spla.spsolve(A, b).reshape(s.shape)
+    sg = solver.gauge_project(s)
+    so = solver.gauge_project(so)
+    for f in range(2 + d):
+        assert np.linalg.norm(sg[f] - so[f]) <= 1e-8 * np.linalg.norm(so[f]) + 1e-14
+    assert its < 200
+
+
+# ---------------------------------------------------------------------------------------- time steps
+
+def _run_parity(shape, dts, nsub, delta, seed=0, pc_type=2):
+    d = len(shape)
+    m = oracle_model(d)
+    c, eta = ni.initial_fields(shape, seed)
+    cbar = c.mean()
+    u0 = solver.init_displacement(m, c, cbar)
+    Xo = np.concatenate([c[None], eta[None], u0])
+    g = gpu_solver(shape, nsub=nsub, overlap=delta, pc_type=pc_type)
+    g.set_fields(c, eta, None)          # the library solves its own u^0 (FFT)
+    mass0 = scheme.mass(m, Xo)
+    out = []
+    for dt in dts:
+        Xo, info_o = solver.newton_step(m, Xo, dt, cbar, SOL)
+        assert info_o["converged"]
+        info_g = g.step(dt)
+        Xg = g.get_state()
+        rel = [float(np.linalg.norm(Xg[f] - Xo[f]) / np.linalg.norm(Xo[f])) for f in range(2 + d)]
+        e_o = scheme.energy(m, Xo, cbar)
+        assert max(rel) <= 1e-8, (dt, rel)
+        assert info_g["energy"] == pytest.approx(e_o, rel=1e-10)
+        assert abs(info_g["mass"] - mass0) <= 1e-12 * abs(mass0)
+        out.append((info_g, info_o, rel))
+    return out
+
+
+def test_step_parity_config1():
+    """BASELINE config 1: 2D 64x64, fixed dt = 0.01, 10 steps, one self-overlapping subdomain, delta = 2."""
+    cfg = ni.CONFIGS[1]
+    out = _run_parity(cfg["shape"], [cfg["dt"]] * cfg["steps"], cfg["nsub"], cfg["overlap"])
+    e = [o[0]["energy"] for o in out]
+    assert all(e[k + 1] <= e[k] + 1e-10 for k in range(len(e) - 1))
+
+
+@pytest.mark.parametrize("dt", [0.5, 2.0])
+def test_step_parity_large_dt(dt):
+    _run_parity((32, 32), [dt, dt], (2, 2), 2)
+
+
+def test_step_parity_3d():
+    _run_parity((10, 12, 12), [0.01, 0.3], (1, 2, 2), 2)
+
+
+def test_step_parity_no_preconditioner():
+    _run_parity((16, 16), [0.01], (1, 1), 0, pc_type=0)
+
+
+def test_adaptive_run_parity():
+    """nks_run_adaptive vs the oracle controller on a 2D 32x32 grid."""
+    shape = (32, 32)
+    d = 2
+    m = oracle_model(d)
+    c, eta = ni.initial_fields(shape, 1)
+    cbar = c.mean()
+    Xo = np.concatenate([c[None], eta[None], solver.init_displacement(m, c, cbar)])
+    Xo, recs_o = solver.run_adaptive(m, Xo, cbar, SOL, 6)
+    g = gpu_solver(shape, nsub=(2, 2))
+    g.set_fields(c, eta, None)
+    recs_g = g.run_adaptive(6)
+    assert len(recs_g) == 6
+    for rg, ro in zip(recs_g, recs_o):
+        assert rg["dt"] == pytest.approx(ro["dt"], rel=1e-9)
+        assert rg["energy"] == pytest.approx(ro["energy"], rel=1e-10)
+        assert rg["retries"] == ro["retries"]
+    Xg = g.get_state()
+    for f in range(4):
+        assert np.linalg.norm(Xg[f] - Xo[f]) <= 1e-8 * np.linalg.norm(Xo[f])
+
+
+def test_step_failure_is_transactional():
+    """A step that cannot converge (newton_maxit = 0) leaves X^n unchanged and reports DIVERGED."""
+    shape = (16, 16)
+    c, eta = ni.initial_fields(shape, 0)
+    g = gpu_solver(shape, sol={"newton_maxit": 0})
+    g.set_fields(c, eta, None)
+    X0 = g.get_state()
+    info = g.step(0.5, raise_on_fail=False)
+    assert info["status"] == "DIVERGED" and info["reason"] == "newton_maxit"
+    np.testing.assert_array_equal(g.get_state(), X0)
+
+
+# ---------------------------------------------------------------------------------------- full-size sampled parity
+
+def _window(X, centre, r):
+    """Periodic window of radius r around centre (C-order index tuple), shape (nf, 2r+1, ...)."""
+    idx = [np.arange(c - r, c + r + 1) % n for c, n in zip(centre, X.shape[1:])]
+    return X[(slice(None),) + np.ix_(*idx)]
+
+
+@pytest.mark.parametrize("cfg_id", [2, 3])
+def test_full_size_sampled_residual_and_jv(cfg_id):
+    """At BASELINE sizes: F and J.v are radius-2 stencils, so the oracle evaluated on a periodic
+    9^d window reproduces the exact value at the window centre; compare 64 sampled points."""
+    shape = ni.CONFIGS[cfg_id]["shape"]
+    d = len(shape)
+    m = oracle_model(d)
+    c, eta = ni.initial_fields(shape, 0)
+    cbar = c.mean()
+    u0 = solver.init_displacement_fft(m, c, cbar)          # oracle-side u^0 (inputs never come from the GPU)
+    Xa = np.concatenate([c[None], eta[None], u0])
+    g = gpu_solver(shape, pc_type=0)
+    g.set_fields(c, eta, u0)
+    cb, eb = ni.perturbed_state(c, eta, 1, 1e-3)
+    Xb = Xa.copy()
+    Xb[0], Xb[1] = cb, eb
+    v = ni.random_direction(2 + d, shape, 5)
+    dt = 0.01
+    F = g.eval_residual(Xb, dt).cpu().numpy()
+    Jv = g.eval_jv(Xb, v, dt).cpu().numpy()
+    rng = np.random.default_rng(9)
+    r = 4
+    for _ in range(64):
+        ctr = tuple(int(rng.integers(0, n)) for n in shape)
+        wa, wb, wv = _window(Xa, ctr, r), _window(Xb, ctr, r), _window(v, ctr, r)
+        Fo = scheme.residual(m, wa, wb, dt, cbar)[(slice(None),) + (r,) * d]
+        Jo = jacobian.jv(m, wa, wb, dt, wv)[(slice(None),) + (r,) * d]
+        Fg = F[(slice(None),) + ctr]
+        Jg = Jv[(slice(None),) + ctr]
+        np.testing.assert_allclose(Fg, Fo, rtol=1e-11, atol=1e-11 * np.abs(F).max(axis=tuple(range(1, d + 1))).max())
+        np.testing.assert_allclose(Jg, Jo, rtol=1e-11, atol=1e-11 * np.abs(Jv).max())
