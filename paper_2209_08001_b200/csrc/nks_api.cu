@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -379,6 +380,7 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
       launch_axpby(n, 1.0, st->Z, 1.0, s, st->stream);
       st->launches += 1;
     }
+    if (st->debug) std::fprintf(stderr, "[nks] gmres cycle its=%d beta=%.3e resid_est=%.3e tol=%.3e\n", its, beta, resid, tol);
     if (resid <= tol) return 0;
     if (its >= st->prm.gmres_maxit) return 1;
     (void)done;
@@ -469,6 +471,12 @@ nks_status step_impl(nks_state* st, double dt, nks_step_info* info) {
       launch_axpby(st->nvec, -1.0, st->F, 0.0, st->Ft, st->stream);
       st->launches += 1;
     }
+    // Project b onto range(J): the left null space of J is spanned by the indicators of the u_I rows
+    // on each parity sub-lattice (sub-lattice sums of D^(.) vanish identically, reading R14), so
+    // the u-rows of F carry only an inconsistent roundoff component there.  Removing it (the same
+    // sub-lattice-mean projection as the gauge) keeps GMRES from chasing an unreachable residual;
+    // the oracle's pinned-row direct solve drops the same component.
+    gauge(st, st->Ft);
     int gits = 0;
     const double tol = std::max(p.gmres_rtol * f, p.gmres_atol);
     const int grc = gmres(st, st->Ft, f, st->S, tol, gits);
@@ -595,6 +603,7 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
   st->ws = (char*)workspace;
   st->ws_bytes = workspace_bytes;
   st->zeta = params->zeta;
+  st->debug = std::getenv("NKS_DEBUG") != nullptr;
   const nks_status rc = guarded(st, [&]() -> nks_status {
     char* w = st->ws;
     double** Xs[7] = {&st->Xn, &st->Xprev, &st->Xb, &st->Xt, &st->S, &st->F, &st->Ft};

@@ -119,6 +119,7 @@ struct nks_state {
   double zeta = 0.0;
   bool have_fields = false;
   bool have_prev = false;
+  bool debug = false;          // NKS_DEBUG set: per-cycle GMRES trace on stderr
   // counters
   long long launches = 0;
   long long syncs = 0;
