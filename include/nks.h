@@ -53,7 +53,8 @@ typedef enum {
 
 /* Divergence reasons reported in nks_step_info.reason. */
 enum { NKS_REASON_NONE = 0, NKS_REASON_NEWTON_MAXIT = 1, NKS_REASON_LINE_SEARCH = 2,
-       NKS_REASON_GMRES_MAXIT = 3, NKS_REASON_DOMAIN = 4, NKS_REASON_DT_FLOOR = 5 };
+       NKS_REASON_GMRES_MAXIT = 3, NKS_REASON_DOMAIN = 4, NKS_REASON_DT_FLOOR = 5,
+       NKS_REASON_GMRES_STAGNATION = 6 /* 3 restart cycles each removing < 0.1 % of the residual */ };
 
 /* Preconditioner types. */
 enum { NKS_PC_NONE = 0, NKS_PC_RAS_BILU0 = 2 };

@@ -43,6 +43,12 @@ HostBoxes build_boxes_host(const nks_grid& g, const BoxSet& B);
 void launch_assemble(const DevParams& P, const BoxSet& B, int nf, const double* Xa, const double* jac4, double* fac,
                      cudaStream_t s);
 void launch_factor(const BoxSet& B, int nf, double* fac, cudaStream_t s);
+size_t ras2d_workspace_bytes(const nks_grid& g);
+void* ras2d_plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaStream_t stream, std::string& why);
+void launch_ras2d_pack(void* plan, const double* fac, long long ld, cudaStream_t s);
+void ras2d_free(void* plan);
+int ras2d_cluster(void* plan);
+cudaError_t launch_ras2d(void* plan, const double* r, double* z, cudaStream_t s);
 void launch_ras_apply(const BoxSet& B, int nf, long long N, const double* fac, const double* r, double* y, double* z,
                       cudaStream_t s);
 // init_fft.cu
@@ -68,9 +74,10 @@ struct CudaError {
 struct Layout {
   size_t off_X[7];
   size_t off_Ta, off_jac4, off_V, off_Z, off_W2, off_part, off_out;
-  size_t off_fac, off_ybox, off_gidx, off_nbr, off_levoff, off_levptr, off_posoff;
+  size_t off_fac, off_ybox, off_gidx, off_nbr, off_levoff, off_levptr, off_posoff, off_geo;
   size_t total;
-  long long P;
+  long long P, ld;
+  size_t geo_bytes;
   int nslots, nbox, nlevptr;
 };
 
@@ -127,13 +134,16 @@ Layout make_layout(const nks_grid& g, const nks_params& p) {
       nl = (long long)L.nbox * ((e0 - 1) + 2 * (e1 - 1) + 3 * (e2 - 1) + 2);
     }
     L.nlevptr = (int)nl;
-    L.off_fac = o; o = align256(o + (size_t)nslots * nf * nf * L.P * sizeof(double));
+    L.ld = (L.P + 31) / 32 * 32;
+    L.off_fac = o; o = align256(o + (size_t)nslots * nf * nf * L.ld * sizeof(double));
     L.off_ybox = o; o = align256(o + (size_t)nf * L.P * sizeof(double));
     L.off_gidx = o; o = align256(o + (size_t)L.P * sizeof(int));
     L.off_nbr = o; o = align256(o + (size_t)nslots * L.P * sizeof(int));
     L.off_levoff = o; o = align256(o + (size_t)(L.nbox + 1) * sizeof(int));
     L.off_levptr = o; o = align256(o + (size_t)nl * sizeof(int));
     L.off_posoff = o; o = align256(o + (size_t)(L.nbox + 1) * sizeof(int));
+    L.off_geo = o; o = align256(o + (d == 2 ? ras2d_workspace_bytes(g) : 0));
+    L.geo_bytes = d == 2 ? ras2d_workspace_bytes(g) : 0;
   }
   L.total = o;
   return L;
@@ -262,7 +272,8 @@ void pc_apply(nks_state* st, const double* r, double* z) {
     return;
   }
   PhaseScope ps(st, PH_RAS);
-  launch_ras_apply(st->boxes, st->nf, st->N, st->fac, r, st->ybox, z, st->stream);
+  if (st->ras2d) CK(launch_ras2d(st->ras2d, r, z, st->stream));
+  else launch_ras_apply(st->boxes, st->nf, st->N, st->fac, r, st->ybox, z, st->stream);
   st->launches += 1;
 }
 
@@ -277,6 +288,10 @@ void pc_setup(nks_state* st, const double* Xb) {
     PhaseScope ps(st, PH_FACT);
     launch_factor(st->boxes, st->nf, st->fac, st->stream);
     st->launches += 1;
+    if (st->ras2d) {
+      launch_ras2d_pack(st->ras2d, st->fac, st->boxes.ld, st->stream);
+      st->launches += 1;
+    }
   }
   (void)Xb;
   st->pc_valid = true;
@@ -298,6 +313,7 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
   its = 0;
   double beta = bnorm;
   bool first = true;
+  int stall = 0;
   while (true) {
     if (beta <= tol) return 0;
     {
@@ -316,6 +332,12 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
       double* w = V + (long long)(j + 1) * n;
       pc_apply(st, vj, st->Z);
       jv(st, st->Z, w);
+      if (st->debug && j < 3) {
+        double nz, nw, bad;
+        norm_adm(st, st->Z, nullptr, nz, bad);
+        norm_adm(st, w, nullptr, nw, bad);
+        std::fprintf(stderr, "[nks]   it %d |z| = %.3e |Jz| = %.3e\n", its, nz, nw);
+      }
       {
         PhaseScope ps(st, PH_VEC);
         launch_mdot(n, j + 1, V, n, w, st->red_part, st->red_out, st->stream);
@@ -398,7 +420,14 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
     }
     CK(cudaMemcpyAsync(st->h_red, st->red_out, sizeof(double), cudaMemcpyDeviceToHost, st->stream));
     sync(st);
-    beta = std::sqrt(st->h_red[0]);
+    {
+      const double prev = beta;
+      beta = std::sqrt(st->h_red[0]);
+      // Stagnation (reading R18): a restart cycle that removes less than 0.1 % of the true residual,
+      // three cycles in a row, is reported as divergence instead of running to gmres_maxit.
+      stall = (beta > 0.999 * prev) ? stall + 1 : 0;
+      if (stall >= 3) return 2;
+    }
     // V already holds r; scale below uses V as source (first == false)
   }
 }
@@ -482,9 +511,10 @@ nks_status step_impl(nks_state* st, double dt, nks_step_info* info) {
     const int grc = gmres(st, st->Ft, f, st->S, tol, gits);
     I.gmres_its += gits;
     if (grc != 0) {
-      I.reason = NKS_REASON_GMRES_MAXIT;
+      I.reason = grc == 2 ? NKS_REASON_GMRES_STAGNATION : NKS_REASON_GMRES_MAXIT;
       I.fnorm = f;
-      st->err = "GMRES reached gmres_maxit";
+      st->err = grc == 2 ? "GMRES stagnated (3 restart cycles with < 0.1 % residual reduction)"
+                         : "GMRES reached gmres_maxit";
       return NKS_E_DIVERGED;
     }
     // line search (reading R17)
@@ -622,6 +652,7 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
       HostBoxes H = build_boxes_host(*grid, B);
       B.nbox = L.nbox;
       B.P = H.P;
+      B.ld = L.ld;
       B.max_levels = H.max_levels;
       B.max_level_width = H.max_width;
       if ((long long)H.lev_ptr.size() > L.nlevptr) throw std::runtime_error("level table overflow");
@@ -642,6 +673,13 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
       CK(cudaMemcpyAsync(B.box_pos_off, H.box_pos_off.data(), H.box_pos_off.size() * sizeof(int), cudaMemcpyHostToDevice,
                          st->stream));
       CK(cudaStreamSynchronize(st->stream));
+      if (grid->dim == 2 && std::getenv("NKS_RAS_LEVEL") == nullptr) {
+        std::string why;
+        st->ras2d = ras2d_plan(*grid, B, w + L.off_geo, L.geo_bytes, st->stream, why);
+        if (st->debug) std::fprintf(stderr, "[nks] ras2d pipeline: %s (cluster %d)\n", st->ras2d ? "on" : why.c_str(),
+                                    ras2d_cluster(st->ras2d));
+        CK(cudaStreamSynchronize(st->stream));
+      }
     }
     return NKS_OK;
   });
@@ -855,7 +893,7 @@ nks_status nks_gmres_solve(nks_state* st, double dt, const double* x_b, const do
     CK(cudaMemcpyAsync(s, st->S, nb, kind_out(on_device), st->stream));
     sync(st);
     if (rc != 0) {
-      st->err = "GMRES reached gmres_maxit";
+      st->err = rc == 2 ? "GMRES stagnated" : "GMRES reached gmres_maxit";
       return NKS_E_DIVERGED;
     }
     return NKS_OK;
@@ -904,6 +942,7 @@ nks_status nks_destroy(nks_state* st) {
   for (auto e : st->ev_pool) cudaEventDestroy(e);
   for (auto e : st->pend_ev) cudaEventDestroy(e);
   if (st->h_red) cudaFreeHost(st->h_red);
+  if (st->ras2d) ras2d_free(st->ras2d);
   delete st;
   return NKS_OK;
 }

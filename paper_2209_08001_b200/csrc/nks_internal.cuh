@@ -40,6 +40,7 @@ struct BoxSet {
   int nbox = 0;
   int nslots = 0;            // 13 or 25
   long long P = 0;           // total box positions over all boxes
+  long long ld = 0;          // leading dimension of the factor planes (P rounded up to 32)
   int max_levels = 0;
   int max_level_width = 0;
   // device arrays
@@ -112,6 +113,7 @@ struct nks_state {
   double* fac = nullptr;    // [nslots][nf][nf][P]
   double* ybox = nullptr;   // [nf][P]
   bool pc_valid = false;
+  void* ras2d = nullptr;    // plan of the row-pipelined 2D RAS apply (ras2d.cu), or null
   double pc_dt = 0.0;
   // history / controller
   double time = 0.0;

@@ -245,7 +245,7 @@ __device__ void jac_block(const DevParams& P, const double* __restrict__ Xa, con
 
 __global__ void k_assemble(DevParams P, SlotTables T, const double* __restrict__ Xa, const double* __restrict__ jac4,
                            const int* __restrict__ gidx, const int* __restrict__ nbr, long long Ptot,
-                           double* __restrict__ fac) {
+                           long long ld, double* __restrict__ fac) {
   const int nf = T.nf;
   const long long total = Ptot * T.nslots;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
@@ -260,24 +260,24 @@ __global__ void k_assemble(DevParams P, SlotTables T, const double* __restrict__
       const int x = gi % P.nx, y = (gi / P.nx) % P.ny, z = gi / (P.nx * P.ny);
       jac_block(P, Xa, jac4, x, y, z, T.off[s], blk, nf);
     }
-    for (int k = 0; k < nf * nf; ++k) fac[((long long)s * nf * nf + k) * Ptot + pos] = blk[k];
+    for (int k = 0; k < nf * nf; ++k) fac[((long long)s * nf * nf + k) * ld + pos] = blk[k];
   }
 }
 
 // ------------------------------------------------------------------------------------------ K5 factorisation
 template <int NF>
-__device__ __forceinline__ void load_blk(const double* fac, int s, long long pos, long long Ptot, double (&b)[NF][NF]) {
+__device__ __forceinline__ void load_blk(const double* fac, int s, long long pos, long long ld, double (&b)[NF][NF]) {
 #pragma unroll
   for (int r = 0; r < NF; ++r)
 #pragma unroll
-    for (int c = 0; c < NF; ++c) b[r][c] = fac[((long long)(s * NF + r) * NF + c) * Ptot + pos];
+    for (int c = 0; c < NF; ++c) b[r][c] = fac[((long long)(s * NF + r) * NF + c) * ld + pos];
 }
 template <int NF>
-__device__ __forceinline__ void store_blk(double* fac, int s, long long pos, long long Ptot, const double (&b)[NF][NF]) {
+__device__ __forceinline__ void store_blk(double* fac, int s, long long pos, long long ld, const double (&b)[NF][NF]) {
 #pragma unroll
   for (int r = 0; r < NF; ++r)
 #pragma unroll
-    for (int c = 0; c < NF; ++c) fac[((long long)(s * NF + r) * NF + c) * Ptot + pos] = b[r][c];
+    for (int c = 0; c < NF; ++c) fac[((long long)(s * NF + r) * NF + c) * ld + pos] = b[r][c];
 }
 
 // In-register Gauss-Jordan inverse with partial pivoting.
@@ -325,7 +325,7 @@ __device__ __forceinline__ void invert(double (&a)[NF][NF]) {
 
 template <int NF>
 __global__ void k_bilu0(SlotTables T, const int* __restrict__ nbr, const int* __restrict__ box_lev_off,
-                        const int* __restrict__ lev_ptr, long long Ptot, double* fac) {
+                        const int* __restrict__ lev_ptr, long long Ptot, long long ld, double* fac) {
   const int b = blockIdx.x;
   const int l0 = box_lev_off[b], l1 = box_lev_off[b + 1] - 1;     // levels l0 .. l1-1
   for (int l = l0; l < l1; ++l) {
@@ -336,8 +336,8 @@ __global__ void k_bilu0(SlotTables T, const int* __restrict__ nbr, const int* __
         const int k = nbr[(long long)sa * Ptot + pos];
         if (k < 0) continue;
         double A[NF][NF], D[NF][NF], Lk[NF][NF];
-        load_blk<NF>(fac, sa, pos, Ptot, A);
-        load_blk<NF>(fac, T.diag, k, Ptot, D);       // U_kk^{-1}
+        load_blk<NF>(fac, sa, pos, ld, A);
+        load_blk<NF>(fac, T.diag, k, ld, D);       // U_kk^{-1}
 #pragma unroll
         for (int r = 0; r < NF; ++r)
 #pragma unroll
@@ -347,13 +347,13 @@ __global__ void k_bilu0(SlotTables T, const int* __restrict__ nbr, const int* __
             for (int m = 0; m < NF; ++m) s = fma(A[r][m], D[m][c], s);
             Lk[r][c] = s;
           }
-        store_blk<NF>(fac, sa, pos, Ptot, Lk);
+        store_blk<NF>(fac, sa, pos, ld, Lk);
         for (int ip = 0; ip < T.npairs[ia]; ++ip) {
           const int sb = T.pair_b[ia][ip], st = T.pair_t[ia][ip];
           if (nbr[(long long)st * Ptot + pos] < 0) continue;
           double U[NF][NF], Tt[NF][NF];
-          load_blk<NF>(fac, sb, k, Ptot, U);
-          load_blk<NF>(fac, st, pos, Ptot, Tt);
+          load_blk<NF>(fac, sb, k, ld, U);
+          load_blk<NF>(fac, st, pos, ld, Tt);
 #pragma unroll
           for (int r = 0; r < NF; ++r)
 #pragma unroll
@@ -363,13 +363,13 @@ __global__ void k_bilu0(SlotTables T, const int* __restrict__ nbr, const int* __
               for (int m = 0; m < NF; ++m) s = fma(-Lk[r][m], U[m][c], s);
               Tt[r][c] = s;
             }
-          store_blk<NF>(fac, st, pos, Ptot, Tt);
+          store_blk<NF>(fac, st, pos, ld, Tt);
         }
       }
       double Dg[NF][NF];
-      load_blk<NF>(fac, T.diag, pos, Ptot, Dg);
+      load_blk<NF>(fac, T.diag, pos, ld, Dg);
       invert<NF>(Dg);
-      store_blk<NF>(fac, T.diag, pos, Ptot, Dg);
+      store_blk<NF>(fac, T.diag, pos, ld, Dg);
     }
     __syncthreads();
   }
@@ -379,7 +379,7 @@ __global__ void k_bilu0(SlotTables T, const int* __restrict__ nbr, const int* __
 template <int NF>
 __global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const int* __restrict__ nbr,
                             const int* __restrict__ box_lev_off, const int* __restrict__ lev_ptr,
-                            const int* __restrict__ box_pos_off, long long Ptot, long long N,
+                            const int* __restrict__ box_pos_off, long long Ptot, long long ld, long long N,
                             const double* __restrict__ fac, const double* __restrict__ r, double* y,
                             double* __restrict__ z) {
   const int b = blockIdx.x;
@@ -410,7 +410,7 @@ __global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const in
 #pragma unroll
         for (int rr = 0; rr < NF; ++rr)
 #pragma unroll
-          for (int c = 0; c < NF; ++c) acc[rr] = fma(-fac[((long long)(sa * NF + rr) * NF + c) * Ptot + pos], yk[c], acc[rr]);
+          for (int c = 0; c < NF; ++c) acc[rr] = fma(-fac[((long long)(sa * NF + rr) * NF + c) * ld + pos], yk[c], acc[rr]);
       }
 #pragma unroll
       for (int f = 0; f < NF; ++f) y[f * Ptot + pos] = acc[f];
@@ -434,14 +434,14 @@ __global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const in
 #pragma unroll
         for (int rr = 0; rr < NF; ++rr)
 #pragma unroll
-          for (int c = 0; c < NF; ++c) acc[rr] = fma(-fac[((long long)(su * NF + rr) * NF + c) * Ptot + pos], xj[c], acc[rr]);
+          for (int c = 0; c < NF; ++c) acc[rr] = fma(-fac[((long long)(su * NF + rr) * NF + c) * ld + pos], xj[c], acc[rr]);
       }
       double xo[NF];
 #pragma unroll
       for (int rr = 0; rr < NF; ++rr) {
         double s = 0.0;
 #pragma unroll
-        for (int c = 0; c < NF; ++c) s = fma(fac[((long long)(T.diag * NF + rr) * NF + c) * Ptot + pos], acc[c], s);
+        for (int c = 0; c < NF; ++c) s = fma(fac[((long long)(T.diag * NF + rr) * NF + c) * ld + pos], acc[c], s);
         xo[rr] = s;
       }
 #pragma unroll
@@ -475,14 +475,14 @@ void launch_assemble(const DevParams& P, const BoxSet& B, int nf, const double* 
   const SlotTables T = make_tables(B, nf);
   const long long total = B.P * B.nslots;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 32);
-  k_assemble<<<blocks, 256, 0, s>>>(P, T, Xa, jac4, B.gidx, B.nbr, B.P, fac);
+  k_assemble<<<blocks, 256, 0, s>>>(P, T, Xa, jac4, B.gidx, B.nbr, B.P, B.ld, fac);
 }
 
 void launch_factor(const BoxSet& B, int nf, double* fac, cudaStream_t s) {
   const SlotTables T = make_tables(B, nf);
   const int threads = std::min(256, std::max(32, ((B.max_level_width + 31) / 32) * 32));
-  if (nf == 4) k_bilu0<4><<<B.nbox, threads, 0, s>>>(T, B.nbr, B.box_lev_off, B.lev_ptr, B.P, fac);
-  else k_bilu0<5><<<B.nbox, threads, 0, s>>>(T, B.nbr, B.box_lev_off, B.lev_ptr, B.P, fac);
+  if (nf == 4) k_bilu0<4><<<B.nbox, threads, 0, s>>>(T, B.nbr, B.box_lev_off, B.lev_ptr, B.P, B.ld, fac);
+  else k_bilu0<5><<<B.nbox, threads, 0, s>>>(T, B.nbr, B.box_lev_off, B.lev_ptr, B.P, B.ld, fac);
 }
 
 void launch_ras_apply(const BoxSet& B, int nf, long long N, const double* fac, const double* r, double* y, double* z,
@@ -490,9 +490,9 @@ void launch_ras_apply(const BoxSet& B, int nf, long long N, const double* fac, c
   const SlotTables T = make_tables(B, nf);
   const int threads = std::min(256, std::max(32, ((B.max_level_width + 31) / 32) * 32));
   if (nf == 4)
-    k_ras_apply<4><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, N, fac, r, y, z);
+    k_ras_apply<4><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, B.ld, N, fac, r, y, z);
   else
-    k_ras_apply<5><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, N, fac, r, y, z);
+    k_ras_apply<5><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, B.ld, N, fac, r, y, z);
 }
 
 }  // namespace nks

@@ -1,0 +1,571 @@
+// K6 in 2D: the RAS/BILU(0) apply z = sum_i R_i^{0T} (L_i U_i)^{-1} R_i^delta r (reading R19)
+// as a row-pipelined sweep instead of a level-synchronous one.
+//
+// Natural-order BILU(0) on the 13-point block pattern has dependency depth i + 2j (reading R21):
+// point (i, j) needs y at (i-1,j), (i-2,j) [own row], (i-1,j-1), (i,j-1), (i+1,j-1) [row j-1] and
+// (i,j-2).  Giving every box row a group of 4 threads (one per output field) and processing point
+// i = t - 2j of row j at step t satisfies all of them with ONE CTA barrier per step, and keeps the
+// working vector of the rows in shared memory (the backward sweep mirrors it: step t descending,
+// rows j+1, j+2).  A box is split into CS stripes of consecutive rows, one CTA each, forming a
+// thread-block cluster: the two boundary rows a stripe needs from its neighbour stripe are pushed
+// into the neighbour's shared memory (DSMEM stores) as they are produced; the consumer spins on a
+// signalling-NaN sentinel in the slot itself (each slot is written exactly once per apply, so no
+// flags or fences are needed).
+//
+// The factor blocks a stripe needs at step t are repacked once per factorisation (k_ras2d_pack)
+// into one contiguous chunk per (box, stripe, step) -- [column q = row - first active row][plane],
+// plane = slot*16 + col*4 + row (blocks column-major so the 4 threads of a row read 4 consecutive
+// doubles; row pitch padded for conflict-free shared-memory reads) -- and stream through an
+// NS-deep shared-memory ring with one bulk copy per step (cp.async.bulk + mbarrier complete_tx,
+// issued NS-1 steps ahead).  Source layout (precond.cu): plane p = slot*16 + row*4 + col,
+// position-minor with leading dimension ld; slots 0..5 lower, 6 diagonal (inverted), 7..12 upper.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "nks_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace nks {
+
+struct Box2Geo {
+  int s0x, s0y;       // global coordinate of local (0,0) (may be negative: wraps)
+  int ex, ey;         // extended box size
+  int ox0, oy0;       // first owned local index (= delta)
+  int ownx, owny;     // owned extent
+  int lev_off;        // index into lev_ptr of this box's level 0
+  int pad;
+};
+
+constexpr unsigned long long kSentinel = 0x7FF4DEADBEEF0001ull;   // signalling NaN: never produced by arithmetic
+constexpr int kGR = 8;     // rows per warp group (4 lanes per row)
+constexpr int kPF = 98;    // forward chunk row pitch (96 planes: 6 lower slots x 16); 784 B = 16 mod 128
+constexpr int kPB = 114;   // backward chunk row pitch (112 planes: diagonal + 6 upper); 912 B = 16 mod 128
+
+// slot offsets (ox, oy): lower slots 0..5 and upper 7..12 (build_slot_tables: natural key order)
+// lower: (0,-2) (-1,-1) (0,-1) (1,-1) (-2,0) (-1,0); upper: (1,0) (2,0) (-1,1) (0,1) (1,1) (0,2)
+__host__ __device__ constexpr int lo_dx(int a) { return a == 1 ? -1 : a == 3 ? 1 : a == 4 ? -2 : a == 5 ? -1 : 0; }
+__host__ __device__ constexpr int lo_dy(int a) { return a == 0 ? -2 : a <= 3 ? -1 : 0; }
+__host__ __device__ constexpr int up_dx(int a) { return a == 0 ? 1 : a == 1 ? 2 : a == 2 ? -1 : a == 4 ? 1 : 0; }
+__host__ __device__ constexpr int up_dy(int a) { return a <= 1 ? 0 : a <= 4 ? 1 : 2; }
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ double ld_spin(const double* p) {
+  unsigned long long v;
+  const unsigned a = smem_u32(p);
+  unsigned spins = 0;
+  do {
+    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+    if (++spins > (1u << 28)) __trap();      // a lost producer would otherwise hang the GPU
+  } while (v == kSentinel);
+  return __longlong_as_double((long long)v);
+}
+
+__device__ __forceinline__ void st_remote(double* local_equiv, unsigned rank, double v) {
+  unsigned raddr;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(local_equiv)), "r"(rank));
+  asm volatile("st.relaxed.cluster.shared::cluster.f64 [%0], %1;" ::"r"(raddr), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ void remote_flush(int mode) {
+  if (mode == 1) asm volatile("fence.acq_rel.cluster;" ::: "memory");
+  else if (mode == 2) asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = smem_u32(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+
+// one contiguous global -> shared bulk copy completing on an mbarrier (bytes: multiple of 16)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+struct Ras2dArgs {
+  const Box2Geo* boxes;
+  const int* lev_ptr;
+  const double* chunkF;   // [box][group][KG][8][kPF]
+  const double* chunkB;   // [box][group][KG][8][kPB]
+  long long N;
+  int nx, ny;
+  int CS, NGmax, KG, NSW, Wmax, rmaxC;
+  int prof, dbg;
+  const double* r;
+  double* z;
+};
+
+// optional in-kernel cycle accounting (NKS_RAS2D_PROF): per warp [total, mbar wait, neighbour wait, steps]
+__device__ unsigned long long g_ras2d_prof[4096 * 4];
+
+__device__ __forceinline__ int jmin_of(int t, int ex) { return max(0, (t - ex + 2) >> 1); }
+
+__device__ __forceinline__ int ld_vol(const int* p) {
+  int v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_vol(int* p, int v) {
+  asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------------- repack
+// One thread per (box point, plane): copies one factor entry from the SoA planes into the chunk of
+// the point's 8-row group and step, at column q (forward: 6 lower blocks; backward: diag + 6 upper).
+__global__ void k_ras2d_pack(Ras2dArgs A, const double* __restrict__ fac, long long ld, int nbox, long long work,
+                             double* chunkF, double* chunkB) {
+  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < work;
+       w += (long long)gridDim.x * blockDim.x) {
+    long long rem = w;
+    const int plane = (int)(rem % 208);
+    rem /= 208;
+    int b = 0;
+    for (; b < nbox; ++b) {                 // boxes may differ in size (nbox is small)
+      const long long npts = (long long)A.boxes[b].ex * A.boxes[b].ey;
+      if (rem < npts) break;
+      rem -= npts;
+    }
+    if (b >= nbox) continue;
+    const Box2Geo G = A.boxes[b];
+    const int j = (int)(rem / G.ex), i = (int)(rem % G.ex);
+    const int t = i + 2 * j;
+    const int pos = A.lev_ptr[G.lev_off + t] + (j - jmin_of(t, G.ex));
+    const int g = j / kGR, R0 = g * kGR;
+    const int q = j - max(R0, jmin_of(t, G.ex));
+    const int kk = t - 2 * R0;
+    const int slot = plane >> 4;
+    const double v = fac[(long long)plane * ld + pos];
+    const long long row = (((long long)b * A.NGmax + g) * A.KG + kk) * kGR + q;
+    if (slot < 6) chunkF[row * kPF + plane] = v;
+    else chunkB[row * kPB + (plane - 96)] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------------- apply
+// CTA s of box b owns the 8-row groups [g0, g1); warp w runs group g0 + w as an independent
+// pipeline: its own bulk-copy ring (2 steps per copy), no CTA barrier inside the sweeps.  Lanes: 4
+// per row (output field).  Neighbour vectors are read from the stripe rows S (shared memory): the
+// warp's own rows after a __syncwarp, the rows of the neighbouring group after its progress word
+// says they are there.  The neighbour group is another warp of this CTA, or the last/first group of
+// CTA s-1/s+1, which pushes its two boundary rows and its progress word into this CTA's shared
+// memory (DSMEM); progress is published every kPub steps (a lag, not a rate, for the consumer).
+constexpr int kSPB = 2;    // steps per bulk copy
+constexpr int kPub = 2;    // progress published every kPub steps
+
+__device__ __forceinline__ void st_remote_u32(int* local_equiv, unsigned rank, int v) {
+  unsigned raddr;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(local_equiv)), "r"(rank));
+  asm volatile("st.relaxed.cluster.shared::cluster.u32 [%0], %1;" ::"r"(raddr), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int s = (int)cluster.block_rank();
+  const int CS = A.CS;
+  const int b = blockIdx.x / CS;
+  const Box2Geo G = A.boxes[b];
+  const int ex = G.ex, ey = G.ey;
+  const int NG = (ey + kGR - 1) / kGR;
+  const int g0 = (s * NG) / CS, g1 = ((s + 1) * NG) / CS;
+  const int r0 = g0 * kGR, r1 = min(g1 * kGR, ey), R = r1 - r0;
+  const int g0u = s > 0 ? ((s - 1) * NG) / CS : 0;
+  const int Rup = r0 - g0u * kGR;                          // rows of CTA s-1
+  const int NSW = A.NSW, Wmax = A.Wmax;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int w = tid >> 5, lane = tid & 31;
+  const int rl = lane >> 2, f = lane & 3;
+
+  // ---- shared memory carve
+  const int stage_elems = kSPB * kGR * kPB;
+  double* stage = reinterpret_cast<double*>(smem);                                          // [Wmax][NSW][SPB][8][kPB]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + (size_t)Wmax * NSW * stage_elems);  // [Wmax][NSW]
+  int* prog = reinterpret_cast<int*>(mbar + Wmax * NSW);                                    // [Wmax][2]: fwd-in, bwd-in
+  const int pitch = (ex + 4) * 4 + 2;       // doubles per S row: cells -2 .. ex+1 (2 zero pads each side) + bank spread
+  double* S = reinterpret_cast<double*>(smem + ((((size_t)Wmax * NSW * stage_elems * 8 + (size_t)Wmax * NSW * 8 +
+                                                  (size_t)Wmax * 8) + 15) & ~(size_t)15));  // rows -2 .. rmaxC+1
+  auto Srow = [&](int rr) -> double* { return S + (size_t)(rr + 2) * pitch + 8; };   // cell 0 of row rr
+
+  // ---- prologue: zero S (pads, halo rows), r gathered onto the stripe (R^delta), barriers, progress words
+  for (int k = tid; k < (R + 4) * pitch; k += nthr) S[k] = 0.0;
+  __syncthreads();
+  for (int k = tid; k < R * ex * 4; k += nthr) {
+    const int ff = k / (R * ex), rem = k % (R * ex), rr = rem / ex, i = rem % ex;
+    int gx = (G.s0x + i) % A.nx; if (gx < 0) gx += A.nx;
+    int gy = (G.s0y + r0 + rr) % A.ny; if (gy < 0) gy += A.ny;
+    Srow(rr)[i * 4 + ff] = __ldg(A.r + (long long)ff * A.N + (long long)gy * A.nx + gx);
+  }
+  if (lane == 0) {
+    for (int k = 0; k < NSW; ++k) mbar_init(&mbar[w * NSW + k], 1);
+    prog[w * 2 + 0] = -(1 << 30);
+    prog[w * 2 + 1] = 1 << 30;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  cluster.sync();      // halo rows and progress words of every CTA are initialised before neighbours write them
+
+  const int g = g0 + w;
+  if (g < g1) {
+    const int R0 = g * kGR, R1 = min(R0 + kGR, ey);
+    const int lr0 = R0 - r0;                                  // local S row of the group's first row
+    const int tf0 = 2 * R0, tf1 = 2 * (R1 - 1) + ex - 1;
+    const int nF = tf1 - tf0 + 1;
+    const bool has_up = g > 0, has_dn = g + 1 < NG;
+    const bool up_remote = g == g0 && s > 0, dn_remote = g + 1 == g1 && s < CS - 1;
+    const int tf1_up = 2 * (R0 - 1) + ex - 1;               // last forward step of the group above
+    const int tf0_dn = 2 * R1;                                // first step of the group below
+    const long long cb = ((long long)b * A.NGmax + g) * A.KG;
+    double* wstage = stage + (size_t)w * NSW * stage_elems;
+    uint64_t* wbar = mbar + w * NSW;
+    const int nbF = (nF + kSPB - 1) / kSPB, nbatch = 2 * nbF;
+    // batch m: forward covers chunk steps [m*SPB, m*SPB+SPB); backward batch m' = m - nbF covers the
+    // descending steps kk = nF-1-m'*SPB ... -> chunk range [lo, lo+SPB) with lo = nF - (m'+1)*SPB (clamped)
+    auto issue = [&](int m) {
+      double* dst = wstage + (size_t)(m % NSW) * stage_elems;
+      if (m < nbF) {
+        const int lo = m * kSPB, n = min(kSPB, nF - lo);
+        bulk_load(dst, A.chunkF + (cb + lo) * kGR * kPF, (unsigned)(n * kGR * kPF * 8), &wbar[m % NSW]);
+      } else {
+        const int mb = m - nbF;
+        const int hi = nF - 1 - mb * kSPB, lo = max(0, hi - kSPB + 1);
+        bulk_load(dst, A.chunkB + (cb + lo) * kGR * kPB, (unsigned)((hi - lo + 1) * kGR * kPB * 8), &wbar[m % NSW]);
+      }
+    };
+    if (lane == 0)
+      for (int m = 0; m < NSW - 1 && m < nbatch; ++m) issue(m);
+    const int j = R0 + rl;
+    const int lr = lr0 + rl;
+    double* const Sown = Srow(lr);
+    const double* const Sbase = Sown;
+    int seen = 0;
+    // publication targets: the group below (forward) / above (backward), in this CTA or the next/previous one
+    int* pubF = dn_remote ? &prog[0 * 2 + 0] : &prog[(w + 1) * 2 + 0];          // slot 0 of CTA s+1 if remote
+    int* pubB = up_remote ? &prog[(g0 - 1 - g0u) * 2 + 1] : &prog[(w - 1) * 2 + 1];   // last warp of CTA s-1
+    long long c_start = clock64(), c_mbar = 0, c_wait = 0;
+    int m = 0, stg = 0, par = 0;          // current batch, its stage and phase parity
+    for (int k = 0; k < 2 * nF; ++k) {
+      const bool fwd = k < nF;
+      const int kb = fwd ? k : k - nF;    // index within the sweep
+      __syncwarp();                       // the previous step's S writes and tile reads of all lanes are done
+      if (kb % kSPB == 0 || k == nF) {
+        // entering a new batch: refill the ring and wait for this batch's copy
+        if (k > 0) { ++m; if (++stg == NSW) { stg = 0; par ^= 1; } }
+        if (lane == 0 && m + NSW - 1 < nbatch) issue(m + NSW - 1);
+        long long c0 = A.prof ? clock64() : 0;
+        mbar_wait(&wbar[stg], (unsigned)par);
+        if (A.prof) c_mbar += clock64() - c0;
+      }
+      const int t = fwd ? tf0 + k : tf1 - kb;
+      const int i = t - 2 * j;
+      const bool active = j < R1 && i >= 0 && i < ex;
+      const int ic = min(max(i, 0), ex - 1);
+      const int q = min(max(j - max(R0, jmin_of(t, ex)), 0), kGR - 1);
+      // tile row of this step inside the batch (backward batches hold ascending chunk steps)
+      const int kk = fwd ? k : nF - 1 - kb;
+      const int slot_in_batch = fwd ? (kk - m * kSPB) : (kk - max(0, (nF - 1 - (m - nbF) * kSPB) - kSPB + 1));
+      // ---- the neighbouring group's rows: wait for its progress word
+      {
+        long long c0 = A.prof ? clock64() : 0;
+        if (fwd && has_up) {
+          const int need = min(t - 1, tf1_up);
+          if (seen < need) {
+            int v = 0;
+            if (lane == 0) {
+              do { v = ld_vol(&prog[w * 2 + 0]); } while (v < need);
+              if (up_remote) asm volatile("fence.acq_rel.cluster;" ::: "memory");
+              else __threadfence_block();
+            }
+            __syncwarp();
+            seen = __shfl_sync(0xffffffffu, v, 0);
+          }
+        } else if (!fwd && has_dn) {
+          if (k == nF) seen = 1 << 30;
+          const int need = max(t + 1, tf0_dn);
+          if (seen > need) {
+            int v = 0;
+            if (lane == 0) {
+              do { v = ld_vol(&prog[w * 2 + 1]); } while (v > need);
+              if (dn_remote) asm volatile("fence.acq_rel.cluster;" ::: "memory");
+              else __threadfence_block();
+            }
+            __syncwarp();
+            seen = __shfl_sync(0xffffffffu, v, 0);
+          }
+        }
+        if (A.prof) c_wait += clock64() - c0;
+      }
+      if (fwd) {
+        // ---------------- forward: y_p = r_p - sum_{lower a} L_{p,a} y_{p+o_a}
+        const double* Lq = wstage + (size_t)stg * stage_elems + (size_t)(slot_in_batch * kGR + q) * kPF + f * 4;
+        double acc0 = Sown[ic * 4 + f], acc1 = 0.0;
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+          // out-of-box neighbours have zero blocks; the padded rows keep every read finite and in bounds
+          const double* src = Sbase + lo_dy(a) * pitch + (ic + lo_dx(a)) * 4;
+          const double2 v01 = *reinterpret_cast<const double2*>(src);
+          const double2 v23 = *reinterpret_cast<const double2*>(src + 2);
+          const double2 l01 = *reinterpret_cast<const double2*>(Lq + a * 16);
+          const double2 l23 = *reinterpret_cast<const double2*>(Lq + a * 16 + 2);
+          acc0 = fma(-l01.x, v01.x, acc0);
+          acc1 = fma(-l01.y, v01.y, acc1);
+          acc0 = fma(-l23.x, v23.x, acc0);
+          acc1 = fma(-l23.y, v23.y, acc1);
+        }
+        const double y = acc0 + acc1;
+        if (active) {
+          Sown[i * 4 + f] = y;
+          if (dn_remote && j >= R1 - 2) st_remote(Srow(j - r1) + i * 4 + f, (unsigned)(s + 1), y);
+        }
+      } else {
+        // ---------------- backward: x_p = U_pp^{-1} (y_p - sum_{upper a} U_{p,a} x_{p+o_a})
+        const double* Uq = wstage + (size_t)stg * stage_elems + (size_t)(slot_in_batch * kGR + q) * kPB + f * 4;
+        double acc0 = Sown[ic * 4 + f], acc1 = 0.0;
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+          const double* src = Sbase + up_dy(a) * pitch + (ic + up_dx(a)) * 4;
+          const double2 v01 = *reinterpret_cast<const double2*>(src);
+          const double2 v23 = *reinterpret_cast<const double2*>(src + 2);
+          const double2 u01 = *reinterpret_cast<const double2*>(Uq + (a + 1) * 16);
+          const double2 u23 = *reinterpret_cast<const double2*>(Uq + (a + 1) * 16 + 2);
+          acc0 = fma(-u01.x, v01.x, acc0);
+          acc1 = fma(-u01.y, v01.y, acc1);
+          acc0 = fma(-u23.x, v23.x, acc0);
+          acc1 = fma(-u23.y, v23.y, acc1);
+        }
+        const double sum = acc0 + acc1;
+        const int q4 = lane & ~3;
+        const double v0 = __shfl_sync(0xffffffffu, sum, q4 + 0), v1 = __shfl_sync(0xffffffffu, sum, q4 + 1);
+        const double v2 = __shfl_sync(0xffffffffu, sum, q4 + 2), v3 = __shfl_sync(0xffffffffu, sum, q4 + 3);
+        const double2 d01 = *reinterpret_cast<const double2*>(Uq), d23 = *reinterpret_cast<const double2*>(Uq + 2);
+        const double x = fma(d01.x, v0, d01.y * v1) + fma(d23.x, v2, d23.y * v3);
+        if (active) {
+          Sown[i * 4 + f] = x;
+          if (up_remote && j < R0 + 2) st_remote(Srow(Rup + (j - r0)) + i * 4 + f, (unsigned)(s - 1), x);
+        }
+      }
+      // ---- publish progress to the neighbouring group (every kPub steps and at the sweep's end)
+      const bool pubf = fwd && has_dn && (kb % kPub == kPub - 1 || kb == nF - 1);
+      const bool pubb = !fwd && has_up && (kb % kPub == kPub - 1 || kb == nF - 1);
+      if (pubf || pubb) {
+        __syncwarp();
+        if (lane == 0) {
+          const bool remote = pubf ? dn_remote : up_remote;
+          if (remote) {
+            asm volatile("fence.acq_rel.cluster;" ::: "memory");
+            st_remote_u32(pubf ? pubF : pubB, (unsigned)(pubf ? s + 1 : s - 1), t);
+          } else {
+            __threadfence_block();
+            st_vol(pubf ? pubF : pubB, t);
+          }
+        }
+      }
+    }
+    if (A.prof && lane == 0) {
+      const int slotp = blockIdx.x * Wmax + w;
+      g_ras2d_prof[slotp * 4 + 0] = clock64() - c_start;
+      g_ras2d_prof[slotp * 4 + 1] = c_mbar;
+      g_ras2d_prof[slotp * 4 + 2] = c_wait;
+      g_ras2d_prof[slotp * 4 + 3] = 2 * nF;
+    }
+  }
+  __syncthreads();
+
+  // ---- R_i^{0T}: owned points only
+  for (int k = tid; k < R * ex * 4; k += nthr) {
+    const int ff = k / (R * ex), rem = k % (R * ex), rr = rem / ex, i = rem % ex;
+    const int jj = r0 + rr;
+    if (i < G.ox0 || i >= G.ox0 + G.ownx || jj < G.oy0 || jj >= G.oy0 + G.owny) continue;
+    int gx = (G.s0x + i) % A.nx; if (gx < 0) gx += A.nx;
+    int gy = (G.s0y + jj) % A.ny; if (gy < 0) gy += A.ny;
+    A.z[(long long)ff * A.N + (long long)gy * A.nx + gx] = Srow(rr)[i * 4 + ff];
+  }
+  cluster.sync();      // no CTA leaves while a neighbour may still address its shared memory
+}
+
+// ------------------------------------------------------------------------------------------ host
+struct Ras2dPlan {
+  int CS = 1, NSW = 4, Wmax = 1, NGmax = 1, KG = 1, threads = 32, nbox = 0, rmaxC = 8;
+  size_t smem = 0;
+  long long npts_total = 0;
+  Ras2dArgs A{};
+};
+
+static void split(int n, int nsub, std::vector<int>& st, std::vector<int>& ln) {
+  const int base = n / nsub, rem = n % nsub;
+  int s = 0;
+  for (int b = 0; b < nsub; ++b) {
+    const int l = base + (b < rem ? 1 : 0);
+    st.push_back(s);
+    ln.push_back(l);
+    s += l;
+  }
+}
+
+struct Ras2dGeom {
+  int CS, NGmax, Wmax, KG, exmax, eymax, nbox;
+};
+
+static bool ras2d_geom(const nks_grid& g, Ras2dGeom& Gm) {
+  if (g.dim != 2) return false;
+  std::vector<int> st[2], ln[2];
+  for (int j = 0; j < 2; ++j) split(g.n[j], g.nsub[j], st[j], ln[j]);
+  Gm.nbox = g.nsub[0] * g.nsub[1];
+  Gm.exmax = *std::max_element(ln[0].begin(), ln[0].end()) + 2 * g.overlap;
+  Gm.eymax = *std::max_element(ln[1].begin(), ln[1].end()) + 2 * g.overlap;
+  const int eymin = *std::min_element(ln[1].begin(), ln[1].end()) + 2 * g.overlap;
+  const int NGmin = (eymin + kGR - 1) / kGR;
+  Gm.NGmax = (Gm.eymax + kGR - 1) / kGR;
+  int CS = std::max(1, std::min(8, 148 / Gm.nbox));
+  if (const char* e = std::getenv("NKS_RAS2D_CS")) CS = std::max(1, std::min(8, std::atoi(e)));   // experiments
+  CS = std::min(CS, NGmin);
+  Gm.CS = CS;
+  Gm.Wmax = (Gm.NGmax + CS - 1) / CS;
+  Gm.KG = 2 * (kGR - 1) + Gm.exmax;
+  return Gm.Wmax <= 8;
+}
+
+// Workspace bytes for the packed chunks + geometry (0 when the pipelined path does not apply).
+size_t ras2d_workspace_bytes(const nks_grid& g) {
+  Ras2dGeom Gm;
+  if (!ras2d_geom(g, Gm)) return 0;
+  const size_t rows = (size_t)Gm.nbox * Gm.NGmax * Gm.KG * kGR;
+  return rows * (kPF + kPB) * sizeof(double) + (size_t)Gm.nbox * sizeof(Box2Geo) + 1024;
+}
+
+// Plans the pipelined apply inside the given workspace slice; nullptr = use the level-synchronous kernel.
+void* ras2d_plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaStream_t stream, std::string& why) {
+  Ras2dGeom Gm;
+  if (g.dim != 2 || !ras2d_geom(g, Gm)) { why = "not applicable (dim or box height)"; return nullptr; }
+  if (B.nslots != 13 || B.diag != 6) { why = "unexpected slot table"; return nullptr; }
+  if (ws_bytes < ras2d_workspace_bytes(g)) { why = "workspace"; return nullptr; }
+  std::vector<int> st[2], ln[2];
+  for (int j = 0; j < 2; ++j) split(g.n[j], g.nsub[j], st[j], ln[j]);
+  std::vector<Box2Geo> geo;
+  long long npts = 0;
+  for (int by = 0; by < g.nsub[1]; ++by)
+    for (int bx = 0; bx < g.nsub[0]; ++bx) {
+      Box2Geo q{};
+      q.ex = ln[0][bx] + 2 * g.overlap;
+      q.ey = ln[1][by] + 2 * g.overlap;
+      q.s0x = st[0][bx] - g.overlap;
+      q.s0y = st[1][by] - g.overlap;
+      q.ox0 = g.overlap;
+      q.oy0 = g.overlap;
+      q.ownx = ln[0][bx];
+      q.owny = ln[1][by];
+      q.lev_off = B.h_box_lev_off[geo.size()];
+      npts += (long long)q.ex * q.ey;
+      geo.push_back(q);
+    }
+  const int rmaxC = Gm.Wmax * kGR;
+  const int pitch = (Gm.exmax + 4) * 4 + 2;
+  const size_t fixed = (size_t)(rmaxC + 4) * pitch * 8 + (size_t)Gm.Wmax * 8 + 64;
+  const size_t per_stage = (size_t)Gm.Wmax * (kSPB * kGR * kPB * 8 + 8);
+  int dev = 0, maxsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int NSW = 4;
+  if (const char* e = std::getenv("NKS_RAS2D_NSW")) NSW = std::max(2, std::atoi(e));
+  while (NSW > 2 && fixed + NSW * per_stage > (size_t)maxsm) --NSW;
+  if (fixed + NSW * per_stage > (size_t)maxsm) { why = "shared memory"; return nullptr; }
+  Ras2dPlan* P = new Ras2dPlan();
+  P->CS = Gm.CS; P->NSW = NSW; P->Wmax = Gm.Wmax; P->NGmax = Gm.NGmax; P->KG = Gm.KG; P->nbox = Gm.nbox;
+  P->rmaxC = rmaxC;
+  P->threads = 32 * Gm.Wmax;
+  P->smem = fixed + NSW * per_stage;
+  P->npts_total = npts;
+  char* w = (char*)ws;
+  const size_t rows = (size_t)Gm.nbox * Gm.NGmax * Gm.KG * kGR;
+  double* cF = (double*)w;
+  double* cB = cF + rows * kPF;
+  Box2Geo* gd = (Box2Geo*)(cB + rows * kPB);
+  if (cudaMemcpyAsync(gd, geo.data(), geo.size() * sizeof(Box2Geo), cudaMemcpyHostToDevice, stream) != cudaSuccess ||
+      cudaMemsetAsync(w, 0, rows * (kPF + kPB) * sizeof(double), stream) != cudaSuccess) {
+    why = "copy"; delete P; return nullptr;
+  }
+  P->A = Ras2dArgs{gd, B.lev_ptr, cF, cB, (long long)g.n[0] * g.n[1], g.n[0], g.n[1], Gm.CS, Gm.NGmax, Gm.KG, NSW,
+                   Gm.Wmax, rmaxC, 0, 0, nullptr, nullptr};
+  if (cudaFuncSetAttribute(k_ras2d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem) != cudaSuccess) {
+    why = "smem attribute"; delete P; return nullptr;
+  }
+  return P;
+}
+
+void ras2d_free(void* plan) { delete (Ras2dPlan*)plan; }
+
+int ras2d_cluster(void* plan) { return plan ? ((Ras2dPlan*)plan)->CS : 0; }
+
+// Repack the factors (after every factorisation).
+void launch_ras2d_pack(void* plan, const double* fac, long long ld, cudaStream_t s) {
+  Ras2dPlan* P = (Ras2dPlan*)plan;
+  const long long work = P->npts_total * 208;
+  const int blocks = (int)std::min<long long>((work + 255) / 256, 148 * 16);
+  k_ras2d_pack<<<blocks, 256, 0, s>>>(P->A, fac, ld, P->nbox, work, const_cast<double*>(P->A.chunkF),
+                                      const_cast<double*>(P->A.chunkB));
+}
+
+cudaError_t launch_ras2d(void* plan, const double* r, double* z, cudaStream_t s) {
+  Ras2dPlan* P = (Ras2dPlan*)plan;
+  Ras2dArgs A = P->A;
+  A.r = r;
+  A.z = z;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P->nbox * P->CS, 1, 1);
+  cfg.blockDim = dim3(P->threads, 1, 1);
+  cfg.dynamicSmemBytes = P->smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = P->CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  static const bool prof = std::getenv("NKS_RAS2D_PROF") != nullptr;
+  A.prof = prof ? 1 : 0;
+  static const int dbg = std::getenv("NKS_RAS2D_DBG") ? std::atoi(std::getenv("NKS_RAS2D_DBG")) : 0;
+  A.dbg = dbg;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_ras2d, A);
+  if (prof && e == cudaSuccess) {
+    static int calls = 0;
+    if (++calls % 10 == 0) {
+      const int nw = P->nbox * P->CS * P->Wmax;
+      std::vector<unsigned long long> h((size_t)nw * 4, 0);
+      cudaStreamSynchronize(s);
+      cudaMemcpyFromSymbol(h.data(), g_ras2d_prof, h.size() * 8);
+      double tot = 0, mb = 0, wt = 0, st = 0, mx = 0, n = 0;
+      for (int c = 0; c < nw; ++c) {
+        if (!h[c * 4 + 3]) continue;
+        tot += h[c * 4]; mb += h[c * 4 + 1]; wt += h[c * 4 + 2]; st += h[c * 4 + 3]; n += 1;
+        mx = std::max(mx, (double)h[c * 4]);
+      }
+      std::fprintf(stderr, "[ras2d prof] CS %d Wmax %d NSW %d smem %zu | per warp: total %.0f cyc (max %.0f), mbar wait %.0f, "
+                   "neighbour wait %.0f, steps %.0f -> %.0f cyc/step\n", P->CS, P->Wmax, P->NSW, P->smem, tot / n, mx,
+                   mb / n, wt / n, st / n, tot / st);
+    }
+  }
+  return e;
+}
+
+}  // namespace nks

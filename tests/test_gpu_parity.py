@@ -199,9 +199,27 @@ def test_step_parity_config1():
     assert all(e[k + 1] <= e[k] + 1e-10 for k in range(len(e) - 1))
 
 
-@pytest.mark.parametrize("dt", [0.5, 2.0])
-def test_step_parity_large_dt(dt):
-    _run_parity((32, 32), [dt, dt], (2, 2), 2)
+@pytest.mark.parametrize("dts", [[0.5, 0.5], [2.0]])
+def test_step_parity_large_dt(dts):
+    _run_parity((32, 32), dts, (2, 2), 2)
+
+
+def test_bilu0_breakdown_is_reported_as_divergence():
+    """At dt = 2 after one dt = 2 step (eta ~ 0.3) J is indefinite and BILU(0)-RAS is unstable: GMRES
+    stagnates (the oracle's own RAS/BILU(0) + GMRES(30) stalls at 0.97 relative residual on the same
+    matrix, while exact subdomain LU converges in 48 iterations).  The library must stop early
+    (stagnation rule, R18), report DIVERGED and leave X^n unchanged -- the adaptive
+    controller then retries with dt/sqrt(2)."""
+    shape = (32, 32)
+    c, eta = ni.initial_fields(shape, 0)
+    g = gpu_solver(shape, nsub=(2, 2))
+    g.set_fields(c, eta, None)
+    assert g.step(2.0)["converged"]
+    X0 = g.get_state()
+    info = g.step(2.0, raise_on_fail=False)
+    assert info["status"] == "DIVERGED" and info["reason"] == "gmres_stagnation", info
+    assert info["gmres_its"] < 1000
+    np.testing.assert_array_equal(g.get_state(), X0)
 
 
 def test_step_parity_3d():
