@@ -101,6 +101,32 @@ __global__ void k_update_scale(long long n, int nk, const double* __restrict__ V
   }
 }
 
+// w = (w - sum_k h2[k] V_k) / nrm with nrm = sqrt(max(ww - sum_k h2[k]^2, 0)) computed on the device from
+// the re-orthogonalisation dots (h2 = hv[0..nk), ww = hv[nk]) in the same order as the host's copy, so
+// the host (one iteration behind) and the device agree on the value and on breakdown (nrm <= 1e-300).
+template <int NK>
+__global__ void k_update_scale_dev(long long n, int nk, const double* __restrict__ V, long long ld,
+                                   const double* __restrict__ hv, double* __restrict__ w) {
+  __shared__ double sh[NK];
+  __shared__ double s_scale;
+  if (threadIdx.x < nk) sh[threadIdx.x] = hv[threadIdx.x];
+  if (threadIdx.x == 0) {
+    double h2sq = 0.0;
+    for (int k = 0; k < nk; ++k) h2sq += hv[k] * hv[k];
+    const double nrm = sqrt(fmax(hv[nk] - h2sq, 0.0));
+    s_scale = nrm > 1e-300 ? 1.0 / nrm : 0.0;
+  }
+  __syncthreads();
+  const double scale = s_scale;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double wi = w[i];
+#pragma unroll
+    for (int k = 0; k < NK; ++k)
+      if (k < nk) wi = fma(-sh[k], __ldg(V + k * ld + i), wi);
+    w[i] = wi * scale;
+  }
+}
+
 // out = sum_k y[k] V_k
 __global__ void k_lincomb(long long n, int nk, const double* __restrict__ V, long long ld, Coefs y,
                           double* __restrict__ out) {
@@ -166,6 +192,11 @@ void launch_update_dot(long long n, int nk, const double* V, long long ld, const
 void launch_update_scale(long long n, int nk, const double* V, long long ld, const double* h, double scale, double* w,
                          cudaStream_t s) {
   NK_DISPATCH(nk, k_update_scale, <<<vec_blocks(n), 256, 0, s>>>(n, nk, V, ld, h, scale, w));
+}
+
+void launch_update_scale_dev(long long n, int nk, const double* V, long long ld, const double* hv, double* w,
+                             cudaStream_t s) {
+  NK_DISPATCH(nk, k_update_scale_dev, <<<vec_blocks(n), 256, 0, s>>>(n, nk, V, ld, hv, w));
 }
 
 void launch_lincomb(long long n, int nk, const double* V, long long ld, const double* y, double* out, cudaStream_t s) {

@@ -34,6 +34,8 @@ void launch_update_dot(long long n, int nk, const double* V, long long ld, const
 void launch_update_scale(long long n, int nk, const double* V, long long ld, const double* h, double scale, double* w,
                          cudaStream_t s);
 void launch_lincomb(long long n, int nk, const double* V, long long ld, const double* y, double* out, cudaStream_t s);
+void launch_update_scale_dev(long long n, int nk, const double* V, long long ld, const double* hv, double* w,
+                             cudaStream_t s);
 void launch_axpby(long long n, double a, const double* x, double b, double* y, cudaStream_t s);
 void launch_xpay(long long n, const double* x, double a, const double* y, double* z, cudaStream_t s);
 // precond.cu
@@ -327,41 +329,41 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
     int j = 0;
     double resid = beta;
     bool done = false;
-    for (j = 0; j < m; ++j) {
-      double* vj = V + (long long)j * n;
-      double* w = V + (long long)(j + 1) * n;
+    // Arnoldi with one iteration of look-ahead: iteration j+1 is queued before the host waits for
+    // iteration j's dot products, so the device never idles on the host's Givens/convergence test.
+    // Every quantity the device needs (projection coefficients, norm, breakdown) is computed on the
+    // device; the host replays the same doubles from a pinned copy (ring of 4 slots).
+    auto launch_iter = [&](int jj) {
+      double* vj = V + (long long)jj * n;
+      double* w = V + (long long)(jj + 1) * n;
       pc_apply(st, vj, st->Z);
       jv(st, st->Z, w);
-      if (st->debug && j < 3) {
-        double nz, nw, bad;
-        norm_adm(st, st->Z, nullptr, nz, bad);
-        norm_adm(st, w, nullptr, nw, bad);
-        std::fprintf(stderr, "[nks]   it %d |z| = %.3e |Jz| = %.3e\n", its, nz, nw);
-      }
       {
         PhaseScope ps(st, PH_VEC);
-        launch_mdot(n, j + 1, V, n, w, st->red_part, st->red_out, st->stream);
-        launch_update_dot(n, j + 1, V, n, st->red_out, w, st->red_part, st->red_out + 64, st->stream);
-        st->launches += 4;
+        launch_mdot(n, jj + 1, V, n, w, st->red_part, st->red_out, st->stream);
+        launch_update_dot(n, jj + 1, V, n, st->red_out, w, st->red_part, st->red_out + 64, st->stream);
+        launch_update_scale_dev(n, jj + 1, V, n, st->red_out + 64, w, st->stream);
+        st->launches += 5;
       }
-      CK(cudaMemcpyAsync(st->h_red, st->red_out, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
-      CK(cudaMemcpyAsync(st->h_red + 64, st->red_out + 64, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
-      sync(st);
+      double* slot = st->h_ring + (jj % 4) * 128;
+      CK(cudaMemcpyAsync(slot, st->red_out, (64 + jj + 2) * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
+      CK(cudaEventRecord(st->gm_ev[jj % 4], st->stream));
+    };
+    launch_iter(0);
+    for (j = 0; j < m; ++j) {
+      if (j + 1 < m && its + 1 < st->prm.gmres_maxit) launch_iter(j + 1);
+      CK(cudaEventSynchronize(st->gm_ev[j % 4]));
+      st->syncs++;
+      const double* hv = st->h_ring + (j % 4) * 128;
       double h2sq = 0.0;
       for (int k = 0; k <= j; ++k) {
-        H[k * m + j] = st->h_red[k] + st->h_red[64 + k];
-        h2sq += st->h_red[64 + k] * st->h_red[64 + k];
+        H[k * m + j] = hv[k] + hv[64 + k];
+        h2sq += hv[64 + k] * hv[64 + k];
       }
-      const double ww1 = st->h_red[64 + j + 1];
-      const double nrm = std::sqrt(std::max(ww1 - h2sq, 0.0));
+      const double nrm = std::sqrt(std::max(hv[64 + j + 1] - h2sq, 0.0));
       H[(j + 1) * m + j] = nrm;
       ++its;
       const bool breakdown = !(nrm > 1e-300);
-      {
-        PhaseScope ps(st, PH_VEC);
-        launch_update_scale(n, j + 1, V, n, st->red_out + 64, breakdown ? 0.0 : 1.0 / nrm, w, st->stream);
-        st->launches += 1;
-      }
       // Givens
       for (int k = 0; k < j; ++k) {
         const double a = H[k * m + j], bb = H[(k + 1) * m + j];
@@ -646,6 +648,8 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
     st->red_part = (double*)(w + L.off_part);
     st->red_out = (double*)(w + L.off_out);
     CK(cudaMallocHost(&st->h_red, 256 * sizeof(double)));
+    CK(cudaMallocHost(&st->h_ring, 4 * 128 * sizeof(double)));
+    for (int k = 0; k < 4; ++k) CK(cudaEventCreateWithFlags(&st->gm_ev[k], cudaEventDisableTiming));
     if (params->pc_type == NKS_PC_RAS_BILU0) {
       BoxSet& B = st->boxes;
       build_slot_tables(grid->dim, B);
@@ -685,6 +689,9 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
   });
   if (rc != NKS_OK) {
     if (st->h_red) cudaFreeHost(st->h_red);
+    if (st->h_ring) cudaFreeHost(st->h_ring);
+    for (int k = 0; k < 4; ++k)
+      if (st->gm_ev[k]) cudaEventDestroy(st->gm_ev[k]);
     delete st;
     return rc;
   }
@@ -942,6 +949,9 @@ nks_status nks_destroy(nks_state* st) {
   for (auto e : st->ev_pool) cudaEventDestroy(e);
   for (auto e : st->pend_ev) cudaEventDestroy(e);
   if (st->h_red) cudaFreeHost(st->h_red);
+  if (st->h_ring) cudaFreeHost(st->h_ring);
+  for (int k = 0; k < 4; ++k)
+    if (st->gm_ev[k]) cudaEventDestroy(st->gm_ev[k]);
   if (st->ras2d) ras2d_free(st->ras2d);
   delete st;
   return NKS_OK;

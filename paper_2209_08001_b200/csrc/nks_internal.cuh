@@ -108,6 +108,8 @@ struct nks_state {
   double* red_part = nullptr;   // reduction partials [kRedBlocks * 64]
   double* red_out = nullptr;    // reduction results [64]
   double* h_red = nullptr;      // pinned host mirror [64]
+  double* h_ring = nullptr;     // pinned [4][128]: GMRES dot products, one slot per in-flight iteration
+  cudaEvent_t gm_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // preconditioner
   nks::BoxSet boxes;
   double* fac = nullptr;    // [nslots][nf][nf][P]

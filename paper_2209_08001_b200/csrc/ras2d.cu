@@ -152,7 +152,7 @@ __global__ void k_ras2d_pack(Ras2dArgs A, const double* __restrict__ fac, long l
     const int t = i + 2 * j;
     const int pos = A.lev_ptr[G.lev_off + t] + (j - jmin_of(t, G.ex));
     const int g = j / kGR, R0 = g * kGR;
-    const int q = j - max(R0, jmin_of(t, G.ex));
+    const int q = j - R0;                  // chunk row = row within the 8-row group
     const int kk = t - 2 * R0;
     const int slot = plane >> 4;
     const double v = fac[(long long)plane * ld + pos];
@@ -164,19 +164,39 @@ __global__ void k_ras2d_pack(Ras2dArgs A, const double* __restrict__ fac, long l
 
 // ---------------------------------------------------------------------------------- apply
 // CTA s of box b owns the 8-row groups [g0, g1); warp w runs group g0 + w as an independent
-// pipeline: its own bulk-copy ring (2 steps per copy), no CTA barrier inside the sweeps.  Lanes: 4
-// per row (output field).  Neighbour vectors are read from the stripe rows S (shared memory): the
-// warp's own rows after a __syncwarp, the rows of the neighbouring group after its progress word
-// says they are there.  The neighbour group is another warp of this CTA, or the last/first group of
-// CTA s-1/s+1, which pushes its two boundary rows and its progress word into this CTA's shared
-// memory (DSMEM); progress is published every kPub steps (a lag, not a rate, for the consumer).
-constexpr int kSPB = 2;    // steps per bulk copy
+// pipeline: its own bulk-copy ring (one step per stage, L2 prefetch further ahead), no CTA barrier
+// inside the sweeps.  Lanes: 4 per row (output field f).
+//
+// Per step only the lag-1 neighbours (own row at t-1, row above at t-1) are on the loop-carried
+// critical path; they arrive by warp shuffles of the previous step's outputs.  Older neighbours are
+// register history (the vectors shuffled at earlier steps) -- the row two above comes from the row
+// above's history -- so a step costs 12 f64 shuffles and 24 DFMA.  The first two rows of a group
+// read the rows above from the stripe rows S (shared memory) after the group above has published
+// its progress; that group is another warp of the CTA, or the last group of CTA s-1, which pushes
+// its two boundary rows and its progress word into this CTA's shared memory (DSMEM).  The backward
+// sweep mirrors all of it (rows below, descending steps).
 constexpr int kPub = 2;    // progress published every kPub steps
+constexpr int kDL2 = 12;   // L2 prefetch distance (steps)
 
 __device__ __forceinline__ void st_remote_u32(int* local_equiv, unsigned rank, int v) {
   unsigned raddr;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(local_equiv)), "r"(rank));
   asm volatile("st.relaxed.cluster.shared::cluster.u32 [%0], %1;" ::"r"(raddr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+
+// acc -= B(row f) . v   (B row = 4 consecutive doubles at p)
+__device__ __forceinline__ void fms4(const double* p, const double (&v)[4], double& a0, double& a1) {
+  const double2 b01 = lds2(p), b23 = lds2(p + 2);
+  a0 = fma(-b01.x, v[0], a0);
+  a1 = fma(-b01.y, v[1], a1);
+  a0 = fma(-b23.x, v[2], a0);
+  a1 = fma(-b23.y, v[3], a1);
 }
 
 __global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
@@ -198,8 +218,8 @@ __global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
   const int rl = lane >> 2, f = lane & 3;
 
   // ---- shared memory carve
-  const int stage_elems = kSPB * kGR * kPB;
-  double* stage = reinterpret_cast<double*>(smem);                                          // [Wmax][NSW][SPB][8][kPB]
+  const int stage_elems = kGR * kPB;
+  double* stage = reinterpret_cast<double*>(smem);                                          // [Wmax][NSW][8][kPB]
   uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + (size_t)Wmax * NSW * stage_elems);  // [Wmax][NSW]
   int* prog = reinterpret_cast<int*>(mbar + Wmax * NSW);                                    // [Wmax][2]: fwd-in, bwd-in
   const int pitch = (ex + 4) * 4 + 2;       // doubles per S row: cells -2 .. ex+1 (2 zero pads each side) + bank spread
@@ -236,60 +256,70 @@ __global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
     const int tf1_up = 2 * (R0 - 1) + ex - 1;               // last forward step of the group above
     const int tf0_dn = 2 * R1;                                // first step of the group below
     const long long cb = ((long long)b * A.NGmax + g) * A.KG;
+    const double* chF = A.chunkF + cb * kGR * kPF;
+    const double* chB = A.chunkB + cb * kGR * kPB;
     double* wstage = stage + (size_t)w * NSW * stage_elems;
     uint64_t* wbar = mbar + w * NSW;
-    const int nbF = (nF + kSPB - 1) / kSPB, nbatch = 2 * nbF;
-    // batch m: forward covers chunk steps [m*SPB, m*SPB+SPB); backward batch m' = m - nbF covers the
-    // descending steps kk = nF-1-m'*SPB ... -> chunk range [lo, lo+SPB) with lo = nF - (m'+1)*SPB (clamped)
-    auto issue = [&](int m) {
-      double* dst = wstage + (size_t)(m % NSW) * stage_elems;
-      if (m < nbF) {
-        const int lo = m * kSPB, n = min(kSPB, nF - lo);
-        bulk_load(dst, A.chunkF + (cb + lo) * kGR * kPF, (unsigned)(n * kGR * kPF * 8), &wbar[m % NSW]);
-      } else {
-        const int mb = m - nbF;
-        const int hi = nF - 1 - mb * kSPB, lo = max(0, hi - kSPB + 1);
-        bulk_load(dst, A.chunkB + (cb + lo) * kGR * kPB, (unsigned)((hi - lo + 1) * kGR * kPB * 8), &wbar[m % NSW]);
-      }
+    // sequence index k in [0, 2nF): forward chunk k, then backward chunk nF-1-(k-nF)
+    auto chunk_ptr = [&](int k) -> const double* {
+      return k < nF ? chF + (size_t)k * kGR * kPF : chB + (size_t)(2 * nF - 1 - k) * kGR * kPB;
     };
-    if (lane == 0)
-      for (int m = 0; m < NSW - 1 && m < nbatch; ++m) issue(m);
+    auto chunk_bytes = [&](int k) -> unsigned { return (unsigned)(kGR * (k < nF ? kPF : kPB) * 8); };
+    auto issue = [&](int k) {
+      bulk_load(wstage + (size_t)(k % NSW) * stage_elems, chunk_ptr(k), chunk_bytes(k), &wbar[k % NSW]);
+    };
+    if (lane == 0) {
+      for (int k = 0; k < kDL2 && k < 2 * nF; ++k) l2_prefetch(chunk_ptr(k), chunk_bytes(k));
+      for (int k = 0; k < NSW - 1 && k < 2 * nF; ++k) issue(k);
+    }
     const int j = R0 + rl;
     const int lr = lr0 + rl;
     double* const Sown = Srow(lr);
-    const double* const Sbase = Sown;
-    int seen = 0;
-    // publication targets: the group below (forward) / above (backward), in this CTA or the next/previous one
-    int* pubF = dn_remote ? &prog[0 * 2 + 0] : &prog[(w + 1) * 2 + 0];          // slot 0 of CTA s+1 if remote
+    const double* const Sup1 = Srow(lr - 1);
+    const double* const Sup2 = Srow(lr - 2);
+    const double* const Sdn1 = Srow(lr + 1);
+    const double* const Sdn2 = Srow(lr + 2);
+    const int q4 = lane & ~3;                       // own quad
+    const int qa = (lane - 4) & 31, qb = (lane + 4) & 31;     // same field, row above / below
+    const int qa4 = qa & ~3, qb4 = qb & ~3;
+    int* pubF = dn_remote ? &prog[0 * 2 + 0] : &prog[(w + 1) * 2 + 0];                 // warp 0 of CTA s+1 if remote
     int* pubB = up_remote ? &prog[(g0 - 1 - g0u) * 2 + 1] : &prog[(w - 1) * 2 + 1];   // last warp of CTA s-1
     long long c_start = clock64(), c_mbar = 0, c_wait = 0;
-    int m = 0, stg = 0, par = 0;          // current batch, its stage and phase parity
-    for (int k = 0; k < 2 * nF; ++k) {
-      const bool fwd = k < nF;
-      const int kb = fwd ? k : k - nF;    // index within the sweep
-      __syncwarp();                       // the previous step's S writes and tile reads of all lanes are done
-      if (kb % kSPB == 0 || k == nF) {
-        // entering a new batch: refill the ring and wait for this batch's copy
-        if (k > 0) { ++m; if (++stg == NSW) { stg = 0; par ^= 1; } }
-        if (lane == 0 && m + NSW - 1 < nbatch) issue(m + NSW - 1);
-        long long c0 = A.prof ? clock64() : 0;
-        mbar_wait(&wbar[stg], (unsigned)par);
-        if (A.prof) c_mbar += clock64() - c0;
-      }
-      const int t = fwd ? tf0 + k : tf1 - kb;
-      const int i = t - 2 * j;
-      const bool active = j < R1 && i >= 0 && i < ex;
-      const int ic = min(max(i, 0), ex - 1);
-      const int q = min(max(j - max(R0, jmin_of(t, ex)), 0), kGR - 1);
-      // tile row of this step inside the batch (backward batches hold ascending chunk steps)
-      const int kk = fwd ? k : nF - 1 - kb;
-      const int slot_in_batch = fwd ? (kk - m * kSPB) : (kk - max(0, (nF - 1 - (m - nbF) * kSPB) - kSPB + 1));
-      // ---- the neighbouring group's rows: wait for its progress word
-      {
-        long long c0 = A.prof ? clock64() : 0;
-        if (fwd && has_up) {
+    int stg = 0;
+    unsigned par = 0;
+    int seen = -(1 << 30);
+
+    // ================================================================ forward sweep
+    {
+      double h0 = 0.0;                                    // this lane's output at t-1
+      double Yo1[4] = {0, 0, 0, 0}, Yo2[4] = {0, 0, 0, 0};                 // own row at t-1, t-2
+      double Ya1[4] = {0, 0, 0, 0}, Ya2[4] = {0, 0, 0, 0}, Ya3[4] = {0, 0, 0, 0};   // row above at t-1..t-3
+      for (int k = 0; k < nF; ++k) {
+        const int t = tf0 + k;
+        const int i = t - 2 * j;
+        const bool active = j < R1 && i >= 0 && i < ex;
+        const int ic = min(max(i, 0), ex - 1);
+        __syncwarp();
+        if (lane == 0) {
+          if (k + kDL2 < 2 * nF) l2_prefetch(chunk_ptr(k + kDL2), chunk_bytes(k + kDL2));
+          if (k + NSW - 1 < 2 * nF) issue(k + NSW - 1);
+        }
+        // row two above at t-4 = the row above's Ya3 (before it shifts)
+        double Yaa4[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) Yaa4[c] = __shfl_sync(0xffffffffu, Ya3[c], qa);
+        // lag-1 vectors: own row and row above at t-1
+        double n_o1[4], n_a1[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          n_o1[c] = __shfl_sync(0xffffffffu, h0, q4 + c);
+          n_a1[c] = __shfl_sync(0xffffffffu, h0, qa4 + c);
+        }
+        // rows above the group: S (after the group above has published step t-1)
+        if (has_up) {
           const int need = min(t - 1, tf1_up);
           if (seen < need) {
+            long long c0 = A.prof ? clock64() : 0;
             int v = 0;
             if (lane == 0) {
               do { v = ld_vol(&prog[w * 2 + 0]); } while (v < need);
@@ -298,11 +328,88 @@ __global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
             }
             __syncwarp();
             seen = __shfl_sync(0xffffffffu, v, 0);
+            if (A.prof) c_wait += clock64() - c0;
           }
-        } else if (!fwd && has_dn) {
-          if (k == nF) seen = 1 << 30;
+        }
+        if (rl == 0) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) { n_a1[c] = Sup1[(ic + 1) * 4 + c]; Yaa4[c] = Sup2[ic * 4 + c]; }
+        } else if (rl == 1) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) Yaa4[c] = Sup2[ic * 4 + c];
+        }
+        // shift histories: Ya2 -> Ya3, Ya1 -> Ya2, new -> Ya1; Yo1 -> Yo2, new -> Yo1
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          Ya3[c] = Ya2[c]; Ya2[c] = Ya1[c]; Ya1[c] = n_a1[c];
+          Yo2[c] = Yo1[c]; Yo1[c] = n_o1[c];
+        }
+        {
+          long long c0 = A.prof ? clock64() : 0;
+          if (k == 0 || (k >= 1 && true)) mbar_wait(&wbar[stg], par);
+          if (A.prof) c_mbar += clock64() - c0;
+        }
+        const double* L = wstage + (size_t)stg * stage_elems + rl * kPF + f * 4;
+        // lag >= 2 terms: (0,-2) Yaa4, (-1,-1) Ya3, (0,-1) Ya2, (-2,0) Yo2
+        double a0 = Sown[ic * 4 + f], a1 = 0.0;
+        fms4(L + 0 * 16, Yaa4, a0, a1);
+        fms4(L + 1 * 16, Ya3, a0, a1);
+        fms4(L + 2 * 16, Ya2, a0, a1);
+        fms4(L + 4 * 16, Yo2, a0, a1);
+        // lag-1 terms: (1,-1) Ya1, (-1,0) Yo1
+        fms4(L + 3 * 16, Ya1, a0, a1);
+        fms4(L + 5 * 16, Yo1, a0, a1);
+        const double y = active ? a0 + a1 : 0.0;
+        h0 = y;
+        if (active) {
+          Sown[i * 4 + f] = y;
+          if (dn_remote && j >= R1 - 2) st_remote(Srow(j - r1) + i * 4 + f, (unsigned)(s + 1), y);
+        }
+        if (++stg == NSW) { stg = 0; par ^= 1u; }
+        if (has_dn && (k % kPub == kPub - 1 || k == nF - 1)) {
+          __syncwarp();
+          if (lane == 0) {
+            if (dn_remote) {
+              asm volatile("fence.acq_rel.cluster;" ::: "memory");
+              st_remote_u32(pubF, (unsigned)(s + 1), t);
+            } else {
+              __threadfence_block();
+              st_vol(pubF, t);
+            }
+          }
+        }
+      }
+    }
+    // ================================================================ backward sweep
+    seen = 1 << 30;
+    {
+      double h0 = 0.0;
+      double Xo1[4] = {0, 0, 0, 0}, Xo2[4] = {0, 0, 0, 0};                 // own row at t+1, t+2 (i+1, i+2)
+      double Xb1[4] = {0, 0, 0, 0}, Xb2[4] = {0, 0, 0, 0}, Xb3[4] = {0, 0, 0, 0};   // row below at t+1..t+3 (i-1, i, i+1)
+      for (int kb = 0; kb < nF; ++kb) {
+        const int k = nF + kb;
+        const int t = tf1 - kb;
+        const int i = t - 2 * j;
+        const bool active = j < R1 && i >= 0 && i < ex;
+        const int ic = min(max(i, 0), ex - 1);
+        __syncwarp();
+        if (lane == 0) {
+          if (k + kDL2 < 2 * nF) l2_prefetch(chunk_ptr(k + kDL2), chunk_bytes(k + kDL2));
+          if (k + NSW - 1 < 2 * nF) issue(k + NSW - 1);
+        }
+        double Xbb4[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) Xbb4[c] = __shfl_sync(0xffffffffu, Xb3[c], qb);
+        double n_o1[4], n_b1[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          n_o1[c] = __shfl_sync(0xffffffffu, h0, q4 + c);
+          n_b1[c] = __shfl_sync(0xffffffffu, h0, qb4 + c);
+        }
+        if (has_dn) {
           const int need = max(t + 1, tf0_dn);
           if (seen > need) {
+            long long c0 = A.prof ? clock64() : 0;
             int v = 0;
             if (lane == 0) {
               do { v = ld_vol(&prog[w * 2 + 1]); } while (v > need);
@@ -311,72 +418,57 @@ __global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
             }
             __syncwarp();
             seen = __shfl_sync(0xffffffffu, v, 0);
+            if (A.prof) c_wait += clock64() - c0;
           }
         }
-        if (A.prof) c_wait += clock64() - c0;
-      }
-      if (fwd) {
-        // ---------------- forward: y_p = r_p - sum_{lower a} L_{p,a} y_{p+o_a}
-        const double* Lq = wstage + (size_t)stg * stage_elems + (size_t)(slot_in_batch * kGR + q) * kPF + f * 4;
-        double acc0 = Sown[ic * 4 + f], acc1 = 0.0;
+        if (j < R1 && (rl == kGR - 1 || j == R1 - 1)) {
 #pragma unroll
-        for (int a = 0; a < 6; ++a) {
-          // out-of-box neighbours have zero blocks; the padded rows keep every read finite and in bounds
-          const double* src = Sbase + lo_dy(a) * pitch + (ic + lo_dx(a)) * 4;
-          const double2 v01 = *reinterpret_cast<const double2*>(src);
-          const double2 v23 = *reinterpret_cast<const double2*>(src + 2);
-          const double2 l01 = *reinterpret_cast<const double2*>(Lq + a * 16);
-          const double2 l23 = *reinterpret_cast<const double2*>(Lq + a * 16 + 2);
-          acc0 = fma(-l01.x, v01.x, acc0);
-          acc1 = fma(-l01.y, v01.y, acc1);
-          acc0 = fma(-l23.x, v23.x, acc0);
-          acc1 = fma(-l23.y, v23.y, acc1);
-        }
-        const double y = acc0 + acc1;
-        if (active) {
-          Sown[i * 4 + f] = y;
-          if (dn_remote && j >= R1 - 2) st_remote(Srow(j - r1) + i * 4 + f, (unsigned)(s + 1), y);
-        }
-      } else {
-        // ---------------- backward: x_p = U_pp^{-1} (y_p - sum_{upper a} U_{p,a} x_{p+o_a})
-        const double* Uq = wstage + (size_t)stg * stage_elems + (size_t)(slot_in_batch * kGR + q) * kPB + f * 4;
-        double acc0 = Sown[ic * 4 + f], acc1 = 0.0;
+          for (int c = 0; c < 4; ++c) { n_b1[c] = Sdn1[(ic - 1) * 4 + c]; Xbb4[c] = Sdn2[ic * 4 + c]; }
+        } else if (j < R1 && (rl == kGR - 2 || j == R1 - 2)) {
 #pragma unroll
-        for (int a = 0; a < 6; ++a) {
-          const double* src = Sbase + up_dy(a) * pitch + (ic + up_dx(a)) * 4;
-          const double2 v01 = *reinterpret_cast<const double2*>(src);
-          const double2 v23 = *reinterpret_cast<const double2*>(src + 2);
-          const double2 u01 = *reinterpret_cast<const double2*>(Uq + (a + 1) * 16);
-          const double2 u23 = *reinterpret_cast<const double2*>(Uq + (a + 1) * 16 + 2);
-          acc0 = fma(-u01.x, v01.x, acc0);
-          acc1 = fma(-u01.y, v01.y, acc1);
-          acc0 = fma(-u23.x, v23.x, acc0);
-          acc1 = fma(-u23.y, v23.y, acc1);
+          for (int c = 0; c < 4; ++c) Xbb4[c] = Sdn2[ic * 4 + c];
         }
-        const double sum = acc0 + acc1;
-        const int q4 = lane & ~3;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          Xb3[c] = Xb2[c]; Xb2[c] = Xb1[c]; Xb1[c] = n_b1[c];
+          Xo2[c] = Xo1[c]; Xo1[c] = n_o1[c];
+        }
+        {
+          long long c0 = A.prof ? clock64() : 0;
+          mbar_wait(&wbar[stg], par);
+          if (A.prof) c_mbar += clock64() - c0;
+        }
+        const double* U = wstage + (size_t)stg * stage_elems + rl * kPB + f * 4;
+        // upper slots (block index in the tile: 1 + slot order): (1,0)=1 (2,0)=2 (-1,1)=3 (0,1)=4 (1,1)=5 (0,2)=6
+        double a0 = Sown[ic * 4 + f], a1 = 0.0;
+        fms4(U + 6 * 16, Xbb4, a0, a1);
+        fms4(U + 5 * 16, Xb3, a0, a1);
+        fms4(U + 4 * 16, Xb2, a0, a1);
+        fms4(U + 2 * 16, Xo2, a0, a1);
+        fms4(U + 3 * 16, Xb1, a0, a1);
+        fms4(U + 1 * 16, Xo1, a0, a1);
+        const double sum = a0 + a1;
         const double v0 = __shfl_sync(0xffffffffu, sum, q4 + 0), v1 = __shfl_sync(0xffffffffu, sum, q4 + 1);
         const double v2 = __shfl_sync(0xffffffffu, sum, q4 + 2), v3 = __shfl_sync(0xffffffffu, sum, q4 + 3);
-        const double2 d01 = *reinterpret_cast<const double2*>(Uq), d23 = *reinterpret_cast<const double2*>(Uq + 2);
-        const double x = fma(d01.x, v0, d01.y * v1) + fma(d23.x, v2, d23.y * v3);
+        const double2 d01 = lds2(U), d23 = lds2(U + 2);
+        const double xr = fma(d01.x, v0, d01.y * v1) + fma(d23.x, v2, d23.y * v3);
+        const double x = active ? xr : 0.0;
+        h0 = x;
         if (active) {
           Sown[i * 4 + f] = x;
           if (up_remote && j < R0 + 2) st_remote(Srow(Rup + (j - r0)) + i * 4 + f, (unsigned)(s - 1), x);
         }
-      }
-      // ---- publish progress to the neighbouring group (every kPub steps and at the sweep's end)
-      const bool pubf = fwd && has_dn && (kb % kPub == kPub - 1 || kb == nF - 1);
-      const bool pubb = !fwd && has_up && (kb % kPub == kPub - 1 || kb == nF - 1);
-      if (pubf || pubb) {
-        __syncwarp();
-        if (lane == 0) {
-          const bool remote = pubf ? dn_remote : up_remote;
-          if (remote) {
-            asm volatile("fence.acq_rel.cluster;" ::: "memory");
-            st_remote_u32(pubf ? pubF : pubB, (unsigned)(pubf ? s + 1 : s - 1), t);
-          } else {
-            __threadfence_block();
-            st_vol(pubf ? pubF : pubB, t);
+        if (++stg == NSW) { stg = 0; par ^= 1u; }
+        if (has_up && (kb % kPub == kPub - 1 || kb == nF - 1)) {
+          __syncwarp();
+          if (lane == 0) {
+            if (up_remote) {
+              asm volatile("fence.acq_rel.cluster;" ::: "memory");
+              st_remote_u32(pubB, (unsigned)(s - 1), t);
+            } else {
+              __threadfence_block();
+              st_vol(pubB, t);
+            }
           }
         }
       }
@@ -481,11 +573,11 @@ void* ras2d_plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, 
   const int rmaxC = Gm.Wmax * kGR;
   const int pitch = (Gm.exmax + 4) * 4 + 2;
   const size_t fixed = (size_t)(rmaxC + 4) * pitch * 8 + (size_t)Gm.Wmax * 8 + 64;
-  const size_t per_stage = (size_t)Gm.Wmax * (kSPB * kGR * kPB * 8 + 8);
+  const size_t per_stage = (size_t)Gm.Wmax * (kGR * kPB * 8 + 8);
   int dev = 0, maxsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  int NSW = 4;
+  int NSW = 6;
   if (const char* e = std::getenv("NKS_RAS2D_NSW")) NSW = std::max(2, std::atoi(e));
   while (NSW > 2 && fixed + NSW * per_stage > (size_t)maxsm) --NSW;
   if (fixed + NSW * per_stage > (size_t)maxsm) { why = "shared memory"; return nullptr; }
