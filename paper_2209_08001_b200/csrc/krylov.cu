@@ -127,6 +127,117 @@ __global__ void k_update_scale_dev(long long n, int nk, const double* __restrict
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Register-resident CGS2 passes for nk + 1 <= 32 columns (restart <= 31).  A thread streams rows of
+// the basis (grid-stride), keeps the 32 column values of its row and 32 dot accumulators in registers,
+// and the warp reduces its 32 accumulators with a butterfly reduce-scatter (31 f64 shuffles: lane l
+// ends with the warp sum of column l).  Block partials [block][32]; the last block to finish sums them
+// in block order (deterministic) into out[0..32).
+template <int OFF>
+__device__ __forceinline__ void rs_round(double (&v)[32], int lane) {
+  const bool up = (lane & OFF) != 0;
+#pragma unroll
+  for (int i = 0; i < OFF; ++i) {
+    const double lo = v[i], hi = v[i + OFF];
+    const double send = up ? lo : hi;
+    const double keep = up ? hi : lo;
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, OFF);
+  }
+}
+
+__device__ __forceinline__ double warp_reduce_scatter32(double (&v)[32], int lane) {
+  rs_round<16>(v, lane);
+  rs_round<8>(v, lane);
+  rs_round<4>(v, lane);
+  rs_round<2>(v, lane);
+  rs_round<1>(v, lane);
+  return v[0];
+}
+
+__device__ __forceinline__ void block_partials_32(double (&acc)[32], double* __restrict__ part,
+                                                  double* __restrict__ out, unsigned* __restrict__ counter) {
+  __shared__ double sw[kRedThreads / 32][32];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const double ws = warp_reduce_scatter32(acc, lane);
+  sw[wid][lane] = ws;
+  __syncthreads();
+  if (wid == 0) {
+    double b = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) b += sw[k][lane];
+    part[blockIdx.x * 32 + lane] = b;
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // last block: column = lane, block range split over warps, then warps combined in order
+  double a = 0.0;
+  for (int blk = wid; blk < (int)gridDim.x; blk += blockDim.x >> 5) a += part[blk * 32 + lane];
+  sw[wid][lane] = a;
+  __syncthreads();
+  if (wid == 0) {
+    double t = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sw[k][lane];
+    out[lane] = t;
+    if (lane == 0) *counter = 0u;
+  }
+}
+
+// out[k] = V_k . w (k < nk), out[nk] = w . w, out[nk+1..31] = 0
+__global__ void __launch_bounds__(kRedThreads) k_cgs_dot(long long n, int nk, const double* __restrict__ V, long long ld,
+                                                       const double* __restrict__ w, double* __restrict__ part,
+                                                       double* __restrict__ out, unsigned* __restrict__ counter) {
+  double acc[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) acc[k] = 0.0;
+  double ww = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double wi = w[i];
+#pragma unroll
+    for (int k = 0; k < 31; ++k) {
+      const double vk = k < nk ? __ldg(V + k * ld + i) : 0.0;
+      acc[k] = fma(vk, wi, acc[k]);
+    }
+    ww = fma(wi, wi, ww);
+  }
+#pragma unroll
+  for (int k = 0; k < 32; ++k) acc[k] = k == nk ? ww : acc[k];
+  block_partials_32(acc, part, out, counter);
+}
+
+// w <- w - sum_k h[k] V_k ; out[k] = V_k . w_new (k < nk), out[nk] = w_new . w_new
+__global__ void __launch_bounds__(kRedThreads) k_cgs_update_dot(long long n, int nk, const double* __restrict__ V,
+                                                              long long ld, const double* __restrict__ h,
+                                                              double* __restrict__ w, double* __restrict__ part,
+                                                              double* __restrict__ out, unsigned* __restrict__ counter) {
+  __shared__ double sh[32];
+  if (threadIdx.x < 32) sh[threadIdx.x] = threadIdx.x < nk ? h[threadIdx.x] : 0.0;
+  __syncthreads();
+  double acc[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) acc[k] = 0.0;
+  double ww = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double vk[31];
+    double wi = w[i];
+#pragma unroll
+    for (int k = 0; k < 31; ++k) {
+      vk[k] = k < nk ? __ldg(V + k * ld + i) : 0.0;
+      wi = fma(-sh[k], vk[k], wi);
+    }
+    w[i] = wi;
+#pragma unroll
+    for (int k = 0; k < 31; ++k) acc[k] = fma(vk[k], wi, acc[k]);
+    ww = fma(wi, wi, ww);
+  }
+#pragma unroll
+  for (int k = 0; k < 32; ++k) acc[k] = k == nk ? ww : acc[k];
+  block_partials_32(acc, part, out, counter);
+}
+
 // out = sum_k y[k] V_k
 __global__ void k_lincomb(long long n, int nk, const double* __restrict__ V, long long ld, Coefs y,
                           double* __restrict__ out) {
@@ -192,6 +303,18 @@ void launch_update_dot(long long n, int nk, const double* V, long long ld, const
 void launch_update_scale(long long n, int nk, const double* V, long long ld, const double* h, double scale, double* w,
                          cudaStream_t s) {
   NK_DISPATCH(nk, k_update_scale, <<<vec_blocks(n), 256, 0, s>>>(n, nk, V, ld, h, scale, w));
+}
+
+static int cgs_blocks(long long n) { return (int)std::min<long long>((n + kRedThreads - 1) / kRedThreads, 148); }
+
+void launch_cgs_dot(long long n, int nk, const double* V, long long ld, const double* w, double* part, double* out,
+                    unsigned* counter, cudaStream_t s) {
+  k_cgs_dot<<<cgs_blocks(n), kRedThreads, 0, s>>>(n, nk, V, ld, w, part, out, counter);
+}
+
+void launch_cgs_update_dot(long long n, int nk, const double* V, long long ld, const double* h, double* w, double* part,
+                           double* out, unsigned* counter, cudaStream_t s) {
+  k_cgs_update_dot<<<cgs_blocks(n), kRedThreads, 0, s>>>(n, nk, V, ld, h, w, part, out, counter);
 }
 
 void launch_update_scale_dev(long long n, int nk, const double* V, long long ld, const double* hv, double* w,

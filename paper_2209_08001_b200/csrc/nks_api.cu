@@ -34,6 +34,10 @@ void launch_update_dot(long long n, int nk, const double* V, long long ld, const
 void launch_update_scale(long long n, int nk, const double* V, long long ld, const double* h, double scale, double* w,
                          cudaStream_t s);
 void launch_lincomb(long long n, int nk, const double* V, long long ld, const double* y, double* out, cudaStream_t s);
+void launch_cgs_dot(long long n, int nk, const double* V, long long ld, const double* w, double* part, double* out,
+                    unsigned* counter, cudaStream_t s);
+void launch_cgs_update_dot(long long n, int nk, const double* V, long long ld, const double* h, double* w, double* part,
+                           double* out, unsigned* counter, cudaStream_t s);
 void launch_update_scale_dev(long long n, int nk, const double* V, long long ld, const double* hv, double* w,
                              cudaStream_t s);
 void launch_axpby(long long n, double a, const double* x, double b, double* y, cudaStream_t s);
@@ -340,10 +344,17 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
       jv(st, st->Z, w);
       {
         PhaseScope ps(st, PH_VEC);
-        launch_mdot(n, jj + 1, V, n, w, st->red_part, st->red_out, st->stream);
-        launch_update_dot(n, jj + 1, V, n, st->red_out, w, st->red_part, st->red_out + 64, st->stream);
+        if (jj + 2 <= 32) {      // register-resident CGS2 passes with last-block reductions
+          launch_cgs_dot(n, jj + 1, V, n, w, st->red_part, st->red_out, st->red_cnt, st->stream);
+          launch_cgs_update_dot(n, jj + 1, V, n, st->red_out, w, st->red_part, st->red_out + 64, st->red_cnt, st->stream);
+          st->launches += 2;
+        } else {
+          launch_mdot(n, jj + 1, V, n, w, st->red_part, st->red_out, st->stream);
+          launch_update_dot(n, jj + 1, V, n, st->red_out, w, st->red_part, st->red_out + 64, st->stream);
+          st->launches += 4;
+        }
         launch_update_scale_dev(n, jj + 1, V, n, st->red_out + 64, w, st->stream);
-        st->launches += 5;
+        st->launches += 1;
       }
       double* slot = st->h_ring + (jj % 4) * 128;
       CK(cudaMemcpyAsync(slot, st->red_out, (64 + jj + 2) * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
@@ -647,6 +658,8 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
     st->W2 = (double*)(w + L.off_W2);
     st->red_part = (double*)(w + L.off_part);
     st->red_out = (double*)(w + L.off_out);
+    st->red_cnt = (unsigned*)(st->red_out + 255);
+    CK(cudaMemsetAsync(st->red_cnt, 0, sizeof(unsigned), st->stream));
     CK(cudaMallocHost(&st->h_red, 256 * sizeof(double)));
     CK(cudaMallocHost(&st->h_ring, 4 * 128 * sizeof(double)));
     for (int k = 0; k < 4; ++k) CK(cudaEventCreateWithFlags(&st->gm_ev[k], cudaEventDisableTiming));

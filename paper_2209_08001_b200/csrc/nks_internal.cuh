@@ -107,6 +107,7 @@ struct nks_state {
   double* W2 = nullptr;     // scratch (nvec)
   double* red_part = nullptr;   // reduction partials [kRedBlocks * 64]
   double* red_out = nullptr;    // reduction results [64]
+  unsigned* red_cnt = nullptr;  // last-block-done counter of the CGS2 reductions (inside red_out's tail)
   double* h_red = nullptr;      // pinned host mirror [64]
   double* h_ring = nullptr;     // pinned [4][128]: GMRES dot products, one slot per in-flight iteration
   cudaEvent_t gm_ev[4] = {nullptr, nullptr, nullptr, nullptr};

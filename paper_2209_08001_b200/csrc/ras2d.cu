@@ -118,6 +118,7 @@ struct Ras2dArgs {
 
 // optional in-kernel cycle accounting (NKS_RAS2D_PROF): per warp [total, mbar wait, neighbour wait, steps]
 __device__ unsigned long long g_ras2d_prof[4096 * 4];
+__device__ long long g_ras2d_cta[2048 * 4];   // per CTA: start, after prologue, after sweeps, end (globaltimer ns)
 
 __device__ __forceinline__ int jmin_of(int t, int ex) { return max(0, (t - ex + 2) >> 1); }
 
@@ -125,6 +126,19 @@ __device__ __forceinline__ int ld_vol(const int* p) {
   int v;
   asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
   return v;
+}
+__device__ __forceinline__ int ld_acq_cluster(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cluster.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_rel_remote(int* local_equiv, unsigned rank, int v) {
+  unsigned raddr;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(local_equiv)), "r"(rank));
+  asm volatile("st.release.cluster.shared::cluster.u32 [%0], %1;" ::"r"(raddr), "r"(v) : "memory");
 }
 __device__ __forceinline__ void st_vol(int* p, int v) {
   asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
@@ -176,7 +190,7 @@ __global__ void k_ras2d_pack(Ras2dArgs A, const double* __restrict__ fac, long l
 // its two boundary rows and its progress word into this CTA's shared memory (DSMEM).  The backward
 // sweep mirrors all of it (rows below, descending steps).
 constexpr int kPub = 2;    // progress published every kPub steps
-constexpr int kDL2 = 12;   // L2 prefetch distance (steps)
+constexpr int kDL2 = 12;   // L2 prefetch distance (steps); off by default (NKS_RAS2D_DBG bit 8 clear = off)
 
 __device__ __forceinline__ void st_remote_u32(int* local_equiv, unsigned rank, int v) {
   unsigned raddr;
@@ -199,8 +213,10 @@ __device__ __forceinline__ void fms4(const double* p, const double (&v)[4], doub
   a1 = fma(-b23.y, v[3], a1);
 }
 
-__global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
+__global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
   extern __shared__ __align__(128) unsigned char smem[];
+  long long T0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(T0));
   cg::cluster_group cluster = cg::this_cluster();
   const int s = (int)cluster.block_rank();
   const int CS = A.CS;
@@ -244,13 +260,15 @@ __global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
   }
   __syncthreads();
   cluster.sync();      // halo rows and progress words of every CTA are initialised before neighbours write them
+  long long T1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(T1));
 
   const int g = g0 + w;
   if (g < g1) {
     const int R0 = g * kGR, R1 = min(R0 + kGR, ey);
     const int lr0 = R0 - r0;                                  // local S row of the group's first row
     const int tf0 = 2 * R0, tf1 = 2 * (R1 - 1) + ex - 1;
-    const int nF = tf1 - tf0 + 1;
+    const int nF = tf1 - tf0 + 1, ntot = 2 * nF;
     const bool has_up = g > 0, has_dn = g + 1 < NG;
     const bool up_remote = g == g0 && s > 0, dn_remote = g + 1 == g1 && s < CS - 1;
     const int tf1_up = 2 * (R0 - 1) + ex - 1;               // last forward step of the group above
@@ -259,21 +277,40 @@ __global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
     const double* chF = A.chunkF + cb * kGR * kPF;
     const double* chB = A.chunkB + cb * kGR * kPB;
     double* wstage = stage + (size_t)w * NSW * stage_elems;
-    uint64_t* wbar = mbar + w * NSW;
-    // sequence index k in [0, 2nF): forward chunk k, then backward chunk nF-1-(k-nF)
-    auto chunk_ptr = [&](int k) -> const double* {
-      return k < nF ? chF + (size_t)k * kGR * kPF : chB + (size_t)(2 * nF - 1 - k) * kGR * kPB;
+    // 32-bit shared addresses, computed once (the loops never convert generic pointers)
+    const unsigned stage_sa = smem_u32(wstage), bar_sa = smem_u32(mbar + w * NSW);
+    const unsigned stage_bytes = (unsigned)(stage_elems * 8);
+    const unsigned fbytes = (unsigned)(kGR * kPF * 8), bbytes = (unsigned)(kGR * kPB * 8);
+    // producer state (lane 0): next sequence index to copy / to prefetch into L2, and its stage
+    int kiss = 0, siss = 0, kpf = 0;
+    auto seq_src = [&](int k) -> const double* {
+      return k < nF ? chF + (size_t)k * kGR * kPF : chB + (size_t)(ntot - 1 - k) * kGR * kPB;
     };
-    auto chunk_bytes = [&](int k) -> unsigned { return (unsigned)(kGR * (k < nF ? kPF : kPB) * 8); };
-    auto issue = [&](int k) {
-      bulk_load(wstage + (size_t)(k % NSW) * stage_elems, chunk_ptr(k), chunk_bytes(k), &wbar[k % NSW]);
+    auto produce = [&]() {      // lane 0 only: keep NSW-1 copies and kDL2 prefetches in flight
+      if (A.dbg & 8)
+        for (; kpf < ntot && kpf < kiss + kDL2; ++kpf) l2_prefetch(seq_src(kpf), kpf < nF ? fbytes : bbytes);
+      const unsigned nb = kiss < nF ? fbytes : bbytes;
+      const unsigned bar = bar_sa + siss * 8;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nb) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       stage_sa + siss * stage_bytes),
+                   "l"(seq_src(kiss)), "r"(nb), "r"(bar)
+                   : "memory");
+      ++kiss;
+      if (++siss == NSW) siss = 0;
     };
-    if (lane == 0) {
-      for (int k = 0; k < kDL2 && k < 2 * nF; ++k) l2_prefetch(chunk_ptr(k), chunk_bytes(k));
-      for (int k = 0; k < NSW - 1 && k < 2 * nF; ++k) issue(k);
-    }
+    if (lane == 0)
+      for (int k = 0; k < NSW - 1 && k < ntot; ++k) produce();
+    auto wait_stage = [&](int stg, unsigned par) {
+      const unsigned a = bar_sa + stg * 8;
+      unsigned done = 0;
+      while (!done)
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(done) : "r"(a), "r"(par) : "memory");
+    };
     const int j = R0 + rl;
     const int lr = lr0 + rl;
+    const bool row_ok = j < R1;
     double* const Sown = Srow(lr);
     const double* const Sup1 = Srow(lr - 1);
     const double* const Sup2 = Srow(lr - 2);
@@ -282,9 +319,13 @@ __global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
     const int q4 = lane & ~3;                       // own quad
     const int qa = (lane - 4) & 31, qb = (lane + 4) & 31;     // same field, row above / below
     const int qa4 = qa & ~3, qb4 = qb & ~3;
-    int* pubF = dn_remote ? &prog[0 * 2 + 0] : &prog[(w + 1) * 2 + 0];                 // warp 0 of CTA s+1 if remote
-    int* pubB = up_remote ? &prog[(g0 - 1 - g0u) * 2 + 1] : &prog[(w - 1) * 2 + 1];   // last warp of CTA s-1
-    long long c_start = clock64(), c_mbar = 0, c_wait = 0;
+    int* const pubF = dn_remote ? &prog[0 * 2 + 0] : &prog[(w + 1) * 2 + 0];                 // warp 0 of CTA s+1 if remote
+    int* const pubB = up_remote ? &prog[(g0 - 1 - g0u) * 2 + 1] : &prog[(w - 1) * 2 + 1];   // last warp of CTA s-1
+    const int* const myF = &prog[w * 2 + 0];
+    const int* const myB = &prog[w * 2 + 1];
+    const double* const tile0 = wstage + rl * kPF + f * 4;     // forward tile row of this lane in stage 0
+    const double* const utile0 = wstage + rl * kPB + f * 4;    // backward
+    long long c_start = A.prof ? clock64() : 0;
     int stg = 0;
     unsigned par = 0;
     int seen = -(1 << 30);
@@ -294,71 +335,61 @@ __global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
       double h0 = 0.0;                                    // this lane's output at t-1
       double Yo1[4] = {0, 0, 0, 0}, Yo2[4] = {0, 0, 0, 0};                 // own row at t-1, t-2
       double Ya1[4] = {0, 0, 0, 0}, Ya2[4] = {0, 0, 0, 0}, Ya3[4] = {0, 0, 0, 0};   // row above at t-1..t-3
-      for (int k = 0; k < nF; ++k) {
+      int i = tf0 - 2 * j;
+      for (int k = 0; k < nF; ++k, ++i) {
         const int t = tf0 + k;
-        const int i = t - 2 * j;
-        const bool active = j < R1 && i >= 0 && i < ex;
+        const bool active = row_ok && i >= 0 && i < ex;
         const int ic = min(max(i, 0), ex - 1);
         __syncwarp();
-        if (lane == 0) {
-          if (k + kDL2 < 2 * nF) l2_prefetch(chunk_ptr(k + kDL2), chunk_bytes(k + kDL2));
-          if (k + NSW - 1 < 2 * nF) issue(k + NSW - 1);
-        }
-        // row two above at t-4 = the row above's Ya3 (before it shifts)
-        double Yaa4[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) Yaa4[c] = __shfl_sync(0xffffffffu, Ya3[c], qa);
-        // lag-1 vectors: own row and row above at t-1
-        double n_o1[4], n_a1[4];
+        if (lane == 0 && kiss < ntot) produce();
+        // row two above at t-4 = the row above's Ya3 (before it shifts); lag-1 vectors at t-1
+        double Yaa4[4], n_o1[4], n_a1[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
+          Yaa4[c] = __shfl_sync(0xffffffffu, Ya3[c], qa);
           n_o1[c] = __shfl_sync(0xffffffffu, h0, q4 + c);
           n_a1[c] = __shfl_sync(0xffffffffu, h0, qa4 + c);
         }
-        // rows above the group: S (after the group above has published step t-1)
         if (has_up) {
           const int need = min(t - 1, tf1_up);
           if (seen < need) {
-            long long c0 = A.prof ? clock64() : 0;
             int v = 0;
             if (lane == 0) {
-              do { v = ld_vol(&prog[w * 2 + 0]); } while (v < need);
-              if (up_remote) asm volatile("fence.acq_rel.cluster;" ::: "memory");
-              else __threadfence_block();
+              do { v = ld_acq_cluster(myF); } while (v < need);
             }
             __syncwarp();
             seen = __shfl_sync(0xffffffffu, v, 0);
-            if (A.prof) c_wait += clock64() - c0;
           }
         }
-        if (rl == 0) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) { n_a1[c] = Sup1[(ic + 1) * 4 + c]; Yaa4[c] = Sup2[ic * 4 + c]; }
-        } else if (rl == 1) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) Yaa4[c] = Sup2[ic * 4 + c];
-        }
-        // shift histories: Ya2 -> Ya3, Ya1 -> Ya2, new -> Ya1; Yo1 -> Yo2, new -> Yo1
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           Ya3[c] = Ya2[c]; Ya2[c] = Ya1[c]; Ya1[c] = n_a1[c];
           Yo2[c] = Yo1[c]; Yo1[c] = n_o1[c];
         }
-        {
-          long long c0 = A.prof ? clock64() : 0;
-          if (k == 0 || (k >= 1 && true)) mbar_wait(&wbar[stg], par);
-          if (A.prof) c_mbar += clock64() - c0;
+        // the group's first rows take the rows above straight from S (the group above ran steps this
+        // warp never executed, so there is no history to shift)
+        if (rl == 0) {
+          const double2 p1 = lds2(Sup1 + (ic + 1) * 4), p2 = lds2(Sup1 + (ic + 1) * 4 + 2);
+          const double2 q1 = lds2(Sup1 + ic * 4), q2 = lds2(Sup1 + ic * 4 + 2);
+          const double2 r1 = lds2(Sup1 + (ic - 1) * 4), r2 = lds2(Sup1 + (ic - 1) * 4 + 2);
+          const double2 s1 = lds2(Sup2 + ic * 4), s2 = lds2(Sup2 + ic * 4 + 2);
+          Ya1[0] = p1.x; Ya1[1] = p1.y; Ya1[2] = p2.x; Ya1[3] = p2.y;
+          Ya2[0] = q1.x; Ya2[1] = q1.y; Ya2[2] = q2.x; Ya2[3] = q2.y;
+          Ya3[0] = r1.x; Ya3[1] = r1.y; Ya3[2] = r2.x; Ya3[3] = r2.y;
+          Yaa4[0] = s1.x; Yaa4[1] = s1.y; Yaa4[2] = s2.x; Yaa4[3] = s2.y;
+        } else if (rl == 1) {
+          const double2 s1 = lds2(Sup2 + ic * 4), s2 = lds2(Sup2 + ic * 4 + 2);
+          Yaa4[0] = s1.x; Yaa4[1] = s1.y; Yaa4[2] = s2.x; Yaa4[3] = s2.y;
         }
-        const double* L = wstage + (size_t)stg * stage_elems + rl * kPF + f * 4;
-        // lag >= 2 terms: (0,-2) Yaa4, (-1,-1) Ya3, (0,-1) Ya2, (-2,0) Yo2
+        wait_stage(stg, par);
+        const double* L = tile0 + (size_t)stg * stage_elems;
         double a0 = Sown[ic * 4 + f], a1 = 0.0;
-        fms4(L + 0 * 16, Yaa4, a0, a1);
-        fms4(L + 1 * 16, Ya3, a0, a1);
-        fms4(L + 2 * 16, Ya2, a0, a1);
-        fms4(L + 4 * 16, Yo2, a0, a1);
-        // lag-1 terms: (1,-1) Ya1, (-1,0) Yo1
-        fms4(L + 3 * 16, Ya1, a0, a1);
-        fms4(L + 5 * 16, Yo1, a0, a1);
+        fms4(L + 0 * 16, Yaa4, a0, a1);      // (0,-2)
+        fms4(L + 1 * 16, Ya3, a0, a1);       // (-1,-1)
+        fms4(L + 2 * 16, Ya2, a0, a1);       // (0,-1)
+        fms4(L + 4 * 16, Yo2, a0, a1);       // (-2,0)
+        fms4(L + 3 * 16, Ya1, a0, a1);       // (1,-1)  lag 1
+        fms4(L + 5 * 16, Yo1, a0, a1);       // (-1,0)  lag 1
         const double y = active ? a0 + a1 : 0.0;
         h0 = y;
         if (active) {
@@ -366,16 +397,11 @@ __global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
           if (dn_remote && j >= R1 - 2) st_remote(Srow(j - r1) + i * 4 + f, (unsigned)(s + 1), y);
         }
         if (++stg == NSW) { stg = 0; par ^= 1u; }
-        if (has_dn && (k % kPub == kPub - 1 || k == nF - 1)) {
+        if (has_dn && ((k & (kPub - 1)) == kPub - 1 || k == nF - 1)) {
           __syncwarp();
           if (lane == 0) {
-            if (dn_remote) {
-              asm volatile("fence.acq_rel.cluster;" ::: "memory");
-              st_remote_u32(pubF, (unsigned)(s + 1), t);
-            } else {
-              __threadfence_block();
-              st_vol(pubF, t);
-            }
+            if (dn_remote) st_rel_remote(pubF, (unsigned)(s + 1), t);   // release: cumulative over the warp's
+            else st_rel_cta(pubF, t);                                   // stores ordered by __syncwarp
           }
         }
       }
@@ -386,67 +412,58 @@ __global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
       double h0 = 0.0;
       double Xo1[4] = {0, 0, 0, 0}, Xo2[4] = {0, 0, 0, 0};                 // own row at t+1, t+2 (i+1, i+2)
       double Xb1[4] = {0, 0, 0, 0}, Xb2[4] = {0, 0, 0, 0}, Xb3[4] = {0, 0, 0, 0};   // row below at t+1..t+3 (i-1, i, i+1)
-      for (int kb = 0; kb < nF; ++kb) {
-        const int k = nF + kb;
+      int i = tf1 - 2 * j;
+      for (int kb = 0; kb < nF; ++kb, --i) {
         const int t = tf1 - kb;
-        const int i = t - 2 * j;
-        const bool active = j < R1 && i >= 0 && i < ex;
+        const bool active = row_ok && i >= 0 && i < ex;
         const int ic = min(max(i, 0), ex - 1);
         __syncwarp();
-        if (lane == 0) {
-          if (k + kDL2 < 2 * nF) l2_prefetch(chunk_ptr(k + kDL2), chunk_bytes(k + kDL2));
-          if (k + NSW - 1 < 2 * nF) issue(k + NSW - 1);
-        }
-        double Xbb4[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) Xbb4[c] = __shfl_sync(0xffffffffu, Xb3[c], qb);
-        double n_o1[4], n_b1[4];
+        if (lane == 0 && kiss < ntot) produce();
+        double Xbb4[4], n_o1[4], n_b1[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
+          Xbb4[c] = __shfl_sync(0xffffffffu, Xb3[c], qb);
           n_o1[c] = __shfl_sync(0xffffffffu, h0, q4 + c);
           n_b1[c] = __shfl_sync(0xffffffffu, h0, qb4 + c);
         }
         if (has_dn) {
           const int need = max(t + 1, tf0_dn);
           if (seen > need) {
-            long long c0 = A.prof ? clock64() : 0;
             int v = 0;
             if (lane == 0) {
-              do { v = ld_vol(&prog[w * 2 + 1]); } while (v > need);
-              if (dn_remote) asm volatile("fence.acq_rel.cluster;" ::: "memory");
-              else __threadfence_block();
+              do { v = ld_acq_cluster(myB); } while (v > need);
             }
             __syncwarp();
             seen = __shfl_sync(0xffffffffu, v, 0);
-            if (A.prof) c_wait += clock64() - c0;
           }
-        }
-        if (j < R1 && (rl == kGR - 1 || j == R1 - 1)) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) { n_b1[c] = Sdn1[(ic - 1) * 4 + c]; Xbb4[c] = Sdn2[ic * 4 + c]; }
-        } else if (j < R1 && (rl == kGR - 2 || j == R1 - 2)) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) Xbb4[c] = Sdn2[ic * 4 + c];
         }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           Xb3[c] = Xb2[c]; Xb2[c] = Xb1[c]; Xb1[c] = n_b1[c];
           Xo2[c] = Xo1[c]; Xo1[c] = n_o1[c];
         }
-        {
-          long long c0 = A.prof ? clock64() : 0;
-          mbar_wait(&wbar[stg], par);
-          if (A.prof) c_mbar += clock64() - c0;
+        if (row_ok && (rl == kGR - 1 || j == R1 - 1)) {
+          const double2 p1 = lds2(Sdn1 + (ic - 1) * 4), p2 = lds2(Sdn1 + (ic - 1) * 4 + 2);
+          const double2 q1 = lds2(Sdn1 + ic * 4), q2 = lds2(Sdn1 + ic * 4 + 2);
+          const double2 r1 = lds2(Sdn1 + (ic + 1) * 4), r2 = lds2(Sdn1 + (ic + 1) * 4 + 2);
+          const double2 s1 = lds2(Sdn2 + ic * 4), s2 = lds2(Sdn2 + ic * 4 + 2);
+          Xb1[0] = p1.x; Xb1[1] = p1.y; Xb1[2] = p2.x; Xb1[3] = p2.y;
+          Xb2[0] = q1.x; Xb2[1] = q1.y; Xb2[2] = q2.x; Xb2[3] = q2.y;
+          Xb3[0] = r1.x; Xb3[1] = r1.y; Xb3[2] = r2.x; Xb3[3] = r2.y;
+          Xbb4[0] = s1.x; Xbb4[1] = s1.y; Xbb4[2] = s2.x; Xbb4[3] = s2.y;
+        } else if (row_ok && (rl == kGR - 2 || j == R1 - 2)) {
+          const double2 s1 = lds2(Sdn2 + ic * 4), s2 = lds2(Sdn2 + ic * 4 + 2);
+          Xbb4[0] = s1.x; Xbb4[1] = s1.y; Xbb4[2] = s2.x; Xbb4[3] = s2.y;
         }
-        const double* U = wstage + (size_t)stg * stage_elems + rl * kPB + f * 4;
-        // upper slots (block index in the tile: 1 + slot order): (1,0)=1 (2,0)=2 (-1,1)=3 (0,1)=4 (1,1)=5 (0,2)=6
+        wait_stage(stg, par);
+        const double* U = utile0 + (size_t)stg * stage_elems;
         double a0 = Sown[ic * 4 + f], a1 = 0.0;
-        fms4(U + 6 * 16, Xbb4, a0, a1);
-        fms4(U + 5 * 16, Xb3, a0, a1);
-        fms4(U + 4 * 16, Xb2, a0, a1);
-        fms4(U + 2 * 16, Xo2, a0, a1);
-        fms4(U + 3 * 16, Xb1, a0, a1);
-        fms4(U + 1 * 16, Xo1, a0, a1);
+        fms4(U + 6 * 16, Xbb4, a0, a1);      // (0,2)
+        fms4(U + 5 * 16, Xb3, a0, a1);       // (1,1)
+        fms4(U + 4 * 16, Xb2, a0, a1);       // (0,1)
+        fms4(U + 2 * 16, Xo2, a0, a1);       // (2,0)
+        fms4(U + 3 * 16, Xb1, a0, a1);       // (-1,1) lag 1
+        fms4(U + 1 * 16, Xo1, a0, a1);       // (1,0)  lag 1
         const double sum = a0 + a1;
         const double v0 = __shfl_sync(0xffffffffu, sum, q4 + 0), v1 = __shfl_sync(0xffffffffu, sum, q4 + 1);
         const double v2 = __shfl_sync(0xffffffffu, sum, q4 + 2), v3 = __shfl_sync(0xffffffffu, sum, q4 + 3);
@@ -459,16 +476,11 @@ __global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
           if (up_remote && j < R0 + 2) st_remote(Srow(Rup + (j - r0)) + i * 4 + f, (unsigned)(s - 1), x);
         }
         if (++stg == NSW) { stg = 0; par ^= 1u; }
-        if (has_up && (kb % kPub == kPub - 1 || kb == nF - 1)) {
+        if (has_up && ((kb & (kPub - 1)) == kPub - 1 || kb == nF - 1)) {
           __syncwarp();
           if (lane == 0) {
-            if (up_remote) {
-              asm volatile("fence.acq_rel.cluster;" ::: "memory");
-              st_remote_u32(pubB, (unsigned)(s - 1), t);
-            } else {
-              __threadfence_block();
-              st_vol(pubB, t);
-            }
+            if (up_remote) st_rel_remote(pubB, (unsigned)(s - 1), t);
+            else st_rel_cta(pubB, t);
           }
         }
       }
@@ -476,12 +488,14 @@ __global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
     if (A.prof && lane == 0) {
       const int slotp = blockIdx.x * Wmax + w;
       g_ras2d_prof[slotp * 4 + 0] = clock64() - c_start;
-      g_ras2d_prof[slotp * 4 + 1] = c_mbar;
-      g_ras2d_prof[slotp * 4 + 2] = c_wait;
+      g_ras2d_prof[slotp * 4 + 1] = 0;
+      g_ras2d_prof[slotp * 4 + 2] = 0;
       g_ras2d_prof[slotp * 4 + 3] = 2 * nF;
     }
   }
   __syncthreads();
+  long long T2;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(T2));
 
   // ---- R_i^{0T}: owned points only
   for (int k = tid; k < R * ex * 4; k += nthr) {
@@ -493,11 +507,17 @@ __global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
     A.z[(long long)ff * A.N + (long long)gy * A.nx + gx] = Srow(rr)[i * 4 + ff];
   }
   cluster.sync();      // no CTA leaves while a neighbour may still address its shared memory
+  if (A.prof && threadIdx.x == 0) {
+    long long T3;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(T3));
+    g_ras2d_cta[blockIdx.x * 4 + 0] = T0; g_ras2d_cta[blockIdx.x * 4 + 1] = T1;
+    g_ras2d_cta[blockIdx.x * 4 + 2] = T2; g_ras2d_cta[blockIdx.x * 4 + 3] = T3;
+  }
 }
 
 // ------------------------------------------------------------------------------------------ host
 struct Ras2dPlan {
-  int CS = 1, NSW = 4, Wmax = 1, NGmax = 1, KG = 1, threads = 32, nbox = 0, rmaxC = 8;
+  int CS = 1, NSW = 4, Wmax = 1, NGmax = 1, KG = 1, threads = 32, nbox = 0, rmaxC = 8, max_clusters = 0;
   size_t smem = 0;
   long long npts_total = 0;
   Ras2dArgs A{};
@@ -518,7 +538,7 @@ struct Ras2dGeom {
   int CS, NGmax, Wmax, KG, exmax, eymax, nbox;
 };
 
-static bool ras2d_geom(const nks_grid& g, Ras2dGeom& Gm) {
+static bool ras2d_geom(const nks_grid& g, Ras2dGeom& Gm, int cs_try = 0) {
   if (g.dim != 2) return false;
   std::vector<int> st[2], ln[2];
   for (int j = 0; j < 2; ++j) split(g.n[j], g.nsub[j], st[j], ln[j]);
@@ -528,13 +548,13 @@ static bool ras2d_geom(const nks_grid& g, Ras2dGeom& Gm) {
   const int eymin = *std::min_element(ln[1].begin(), ln[1].end()) + 2 * g.overlap;
   const int NGmin = (eymin + kGR - 1) / kGR;
   Gm.NGmax = (Gm.eymax + kGR - 1) / kGR;
-  int CS = std::max(1, std::min(8, 148 / Gm.nbox));
+  int CS = cs_try > 0 ? cs_try : std::max(1, std::min(8, 148 / Gm.nbox));
   if (const char* e = std::getenv("NKS_RAS2D_CS")) CS = std::max(1, std::min(8, std::atoi(e)));   // experiments
   CS = std::min(CS, NGmin);
   Gm.CS = CS;
   Gm.Wmax = (Gm.NGmax + CS - 1) / CS;
   Gm.KG = 2 * (kGR - 1) + Gm.exmax;
-  return Gm.Wmax <= 8;
+  return Gm.Wmax <= 16;
 }
 
 // Workspace bytes for the packed chunks + geometry (0 when the pipelined path does not apply).
@@ -546,11 +566,56 @@ size_t ras2d_workspace_bytes(const nks_grid& g) {
 }
 
 // Plans the pipelined apply inside the given workspace slice; nullptr = use the level-synchronous kernel.
+// Shared memory and co-residency of one launch configuration: returns NSW (0 = does not fit) and the
+// number of clusters that can be resident at once.
+static int ras2d_fit(const Ras2dGeom& Gm, size_t& smem, int& max_clusters) {
+  const int rmaxC = Gm.Wmax * kGR;
+  const int pitch = (Gm.exmax + 4) * 4 + 2;
+  const size_t fixed = (size_t)(rmaxC + 4) * pitch * 8 + (size_t)Gm.Wmax * 8 + 64;
+  const size_t per_stage = (size_t)Gm.Wmax * (kGR * kPB * 8 + 8);
+  int dev = 0, maxsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int NSW = 6;
+  if (const char* e = std::getenv("NKS_RAS2D_NSW")) NSW = std::max(2, std::atoi(e));
+  while (NSW > 3 && fixed + NSW * per_stage > (size_t)maxsm) --NSW;
+  if (fixed + NSW * per_stage > (size_t)maxsm) return 0;
+  smem = fixed + NSW * per_stage;
+  if (cudaFuncSetAttribute(k_ras2d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(Gm.nbox * Gm.CS, 1, 1);
+  cfg.blockDim = dim3(32 * Gm.Wmax, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = Gm.CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at; cfg.numAttrs = 1;
+  max_clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&max_clusters, k_ras2d, &cfg) != cudaSuccess) max_clusters = 0;
+  cudaGetLastError();
+  return NSW;
+}
+
+// Plans the pipelined apply inside the given workspace slice; nullptr = use the level-synchronous kernel.
+// The cluster size is the largest <= 8 whose clusters are all co-resident (one wave).
 void* ras2d_plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaStream_t stream, std::string& why) {
   Ras2dGeom Gm;
   if (g.dim != 2 || !ras2d_geom(g, Gm)) { why = "not applicable (dim or box height)"; return nullptr; }
   if (B.nslots != 13 || B.diag != 6) { why = "unexpected slot table"; return nullptr; }
   if (ws_bytes < ras2d_workspace_bytes(g)) { why = "workspace"; return nullptr; }
+  int NSW = 0, ncl = 0;
+  size_t smem = 0;
+  for (int cs = Gm.CS; cs >= 1; --cs) {
+    Ras2dGeom T;
+    if (!ras2d_geom(g, T, cs)) continue;
+    size_t sm = 0;
+    int mc = 0;
+    const int nsw = ras2d_fit(T, sm, mc);
+    if (nsw == 0) continue;
+    if (NSW == 0 || mc >= T.nbox) { Gm = T; NSW = nsw; smem = sm; ncl = mc; }
+    if (mc >= T.nbox) break;
+  }
+  if (NSW == 0) { why = "shared memory"; return nullptr; }
   std::vector<int> st[2], ln[2];
   for (int j = 0; j < 2; ++j) split(g.n[j], g.nsub[j], st[j], ln[j]);
   std::vector<Box2Geo> geo;
@@ -570,23 +635,13 @@ void* ras2d_plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, 
       npts += (long long)q.ex * q.ey;
       geo.push_back(q);
     }
-  const int rmaxC = Gm.Wmax * kGR;
-  const int pitch = (Gm.exmax + 4) * 4 + 2;
-  const size_t fixed = (size_t)(rmaxC + 4) * pitch * 8 + (size_t)Gm.Wmax * 8 + 64;
-  const size_t per_stage = (size_t)Gm.Wmax * (kGR * kPB * 8 + 8);
-  int dev = 0, maxsm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  int NSW = 6;
-  if (const char* e = std::getenv("NKS_RAS2D_NSW")) NSW = std::max(2, std::atoi(e));
-  while (NSW > 2 && fixed + NSW * per_stage > (size_t)maxsm) --NSW;
-  if (fixed + NSW * per_stage > (size_t)maxsm) { why = "shared memory"; return nullptr; }
   Ras2dPlan* P = new Ras2dPlan();
   P->CS = Gm.CS; P->NSW = NSW; P->Wmax = Gm.Wmax; P->NGmax = Gm.NGmax; P->KG = Gm.KG; P->nbox = Gm.nbox;
-  P->rmaxC = rmaxC;
+  P->rmaxC = Gm.Wmax * kGR;
   P->threads = 32 * Gm.Wmax;
-  P->smem = fixed + NSW * per_stage;
+  P->smem = smem;
   P->npts_total = npts;
+  P->max_clusters = ncl;
   char* w = (char*)ws;
   const size_t rows = (size_t)Gm.nbox * Gm.NGmax * Gm.KG * kGR;
   double* cF = (double*)w;
@@ -597,10 +652,13 @@ void* ras2d_plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, 
     why = "copy"; delete P; return nullptr;
   }
   P->A = Ras2dArgs{gd, B.lev_ptr, cF, cB, (long long)g.n[0] * g.n[1], g.n[0], g.n[1], Gm.CS, Gm.NGmax, Gm.KG, NSW,
-                   Gm.Wmax, rmaxC, 0, 0, nullptr, nullptr};
+                   Gm.Wmax, P->rmaxC, 0, 0, nullptr, nullptr};
   if (cudaFuncSetAttribute(k_ras2d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem) != cudaSuccess) {
     why = "smem attribute"; delete P; return nullptr;
   }
+  if (std::getenv("NKS_DEBUG"))
+    std::fprintf(stderr, "[nks] ras2d: %d boxes, cluster %d, %d warps/CTA, NSW %d, smem %zu B, max active clusters %d\n",
+                 P->nbox, P->CS, P->Wmax, P->NSW, P->smem, ncl);
   return P;
 }
 
@@ -652,6 +710,17 @@ cudaError_t launch_ras2d(void* plan, const double* r, double* z, cudaStream_t s)
         tot += h[c * 4]; mb += h[c * 4 + 1]; wt += h[c * 4 + 2]; st += h[c * 4 + 3]; n += 1;
         mx = std::max(mx, (double)h[c * 4]);
       }
+      std::vector<long long> hc((size_t)P->nbox * P->CS * 4);
+      cudaMemcpyFromSymbol(hc.data(), g_ras2d_cta, hc.size() * 8);
+      long long t0 = hc[0], t3 = 0;
+      double pro = 0, swp = 0, epi = 0;
+      for (int c = 0; c < P->nbox * P->CS; ++c) {
+        t0 = std::min(t0, hc[c * 4]); t3 = std::max(t3, hc[c * 4 + 3]);
+        pro += hc[c * 4 + 1] - hc[c * 4]; swp += hc[c * 4 + 2] - hc[c * 4 + 1]; epi += hc[c * 4 + 3] - hc[c * 4 + 2];
+      }
+      const double nc = P->nbox * P->CS;
+      std::fprintf(stderr, "[ras2d prof] CTA avg ns: prologue %.0f sweeps %.0f epilogue %.0f | first start->last end %lld ns\n",
+                   pro / nc, swp / nc, epi / nc, t3 - t0);
       std::fprintf(stderr, "[ras2d prof] CS %d Wmax %d NSW %d smem %zu | per warp: total %.0f cyc (max %.0f), mbar wait %.0f, "
                    "neighbour wait %.0f, steps %.0f -> %.0f cyc/step\n", P->CS, P->Wmax, P->NSW, P->smem, tot / n, mx,
                    mb / n, wt / n, st / n, tot / st);
