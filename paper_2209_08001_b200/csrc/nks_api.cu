@@ -22,8 +22,12 @@ namespace nks {
 // stencil.cu
 void launch_level_prep(const DevParams& P, const double* X, double* T, cudaStream_t s);
 void launch_residual(const DevParams& P, const double* Xa, const double* Xb, const double* Ta, double* F, cudaStream_t s);
+void launch_residual_tiled(const DevParams& P, const double* Xa, const double* Xb, const double* Ta, double* F,
+                           cudaStream_t s);
 void launch_pointwise_jac(const DevParams& P, const double* Xa, const double* Xb, double* jac4, cudaStream_t s);
 void launch_jv(const DevParams& P, const double* Xa, const double* jac4, const double* v, double* out, cudaStream_t s);
+void launch_jv_tiled(const DevParams& P, const double* Xa, const double* jac4, const double* v, double* out,
+                     cudaStream_t s);
 void launch_norm_admissible(long long N, int nf, const double* F, const double* X, double* part, double* out, cudaStream_t s);
 void launch_energy(const DevParams& P, const double* X, double* part, double* out, cudaStream_t s);
 void launch_gauge(const DevParams& P, double* X, double* part, double* out, cudaStream_t s);
@@ -243,7 +247,9 @@ void sync(nks_state* st) {
 
 void residual(nks_state* st, const double* Xb, double* F) {
   PhaseScope ps(st, PH_F);
-  launch_residual(st->dp, st->Xn, Xb, st->Ta, F, st->stream);
+  static const bool old_f = std::getenv("NKS_F_OLD") != nullptr;
+  if (old_f) launch_residual(st->dp, st->Xn, Xb, st->Ta, F, st->stream);
+  else launch_residual_tiled(st->dp, st->Xn, Xb, st->Ta, F, st->stream);
   st->launches += 1;
 }
 
@@ -268,7 +274,9 @@ void gauge(nks_state* st, double* X) {
 
 void jv(nks_state* st, const double* v, double* out) {
   PhaseScope ps(st, PH_JV);
-  launch_jv(st->dp, st->Xn, st->jac4, v, out, st->stream);
+  static const bool old_jv = std::getenv("NKS_JV_OLD") != nullptr;
+  if (old_jv) launch_jv(st->dp, st->Xn, st->jac4, v, out, st->stream);
+  else launch_jv_tiled(st->dp, st->Xn, st->jac4, v, out, st->stream);
   st->launches += 1;
 }
 
