@@ -47,12 +47,13 @@ UNIT = "steps/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="nks", choices=["nks", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-micro", action="store_true")
     return ap.parse_args()
 
 
@@ -218,6 +219,49 @@ def ras_bytes(solver_obj, cfg):
     return 8 * (nslots * nf * nf * P + nf * P + nf * N), P
 
 
+def micro_kernels(shape, reps=10):
+    """F (K1) and J.v (K2) alone on one grid (SURVEY 8(d) config 5 recipe): X^n = common init (u = 0),
+    X^b = X^n + U(-1e-3, 1e-3) on c and eta, v ~ U(-1, 1), dt = 0.01; library CUDA events around each
+    launch (nks_phase_times), mean over `reps` launches after warm-up.  Algorithmic bytes per point:
+    F = 8 (2 nf + 3) (X^b, c^a, eta^a, T^n in; F out); J.v = 8 (2 nf + 5) (v, 4 partials, c^a in; out)."""
+    import torch
+    from paper_2209_08001_b200 import PC_NONE, Solver
+    d = len(shape)
+    nf = 2 + d
+    N = int(np.prod(shape))
+    sol = dict(ni.solver_default())
+    sol["gmres_restart"] = 1                      # no Krylov basis needed here
+    g = Solver(shape, ni.model_default(), sol, pc_type=PC_NONE)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    c = 0.1622 + (torch.rand(shape, device="cuda", dtype=torch.float64, generator=gen) - 0.5) * 0.01
+    eta = 0.1 + (torch.rand(shape, device="cuda", dtype=torch.float64, generator=gen) - 0.5) * 0.02
+    u = torch.zeros((d,) + tuple(shape), device="cuda", dtype=torch.float64)
+    g.set_fields(c, eta, u)
+    xb = torch.cat([c[None], eta[None], u]).contiguous()
+    xb[0] += (torch.rand(shape, device="cuda", dtype=torch.float64, generator=gen) - 0.5) * 2e-3
+    xb[1] += (torch.rand(shape, device="cuda", dtype=torch.float64, generator=gen) - 0.5) * 2e-3
+    v = (torch.rand((nf,) + tuple(shape), device="cuda", dtype=torch.float64, generator=gen) - 0.5) * 2
+    del c, eta, u
+    for _ in range(2):
+        g.eval_residual(xb, 0.01)
+        g.eval_jv(xb, v, 0.01)
+    torch.cuda.synchronize()
+    g.set_profiling(True)
+    g.phase_times(reset=True)
+    for _ in range(reps):
+        g.eval_residual(xb, 0.01)
+        g.eval_jv(xb, v, 0.01)
+    ph = g.phase_times(reset=True)
+    out = {}
+    for key, per_pt in (("residual", 2 * nf + 3), ("jv", 2 * nf + 5)):
+        ms = ph[key]["ms"] / ph[key]["count"]
+        out[key] = {"ms": ms, "GDOF_s": nf * N / (ms * 1e-3) / 1e9, "alg_bytes": per_pt * 8 * N,
+                    "GB_s": per_pt * 8 * N / (ms * 1e-3) / 1e9}
+    del g, xb, v
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_gpu(args, world, rank, local, pg):
     import torch
     from paper_2209_08001_b200 import Solver
@@ -237,7 +281,6 @@ def run_gpu(args, world, rank, local, pg):
     for _ in range(args.warmup):
         recs += g.run_adaptive(1)
     torch.cuda.synchronize()
-    X_start = g.get_state()
     clk = ClockSampler(local)
     clk.start()
     g.set_profiling(True)
@@ -296,45 +339,74 @@ def run_gpu(args, world, rank, local, pg):
         roof = {"kernel": dom, "bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
                 "traffic": None, "peak_source": peak_src}
 
-    # ---- end to end through the C ABI with host buffers (dt-forced replay of the timed steps)
+    # ---- end to end through the C ABI with host buffers: every step uploads X^n from pinned host memory
+    # (nks_set_state, on_device = 0: keeps the controller's history), advances one adaptive step
+    # (nks_run_adaptive, retries included, exactly the device leg's work) and downloads X^{n+1}
     e2e = None
     if not args.no_e2e:
-        dts = [r["dt"] for r in timed]
-        ch = torch.from_numpy(np.ascontiguousarray(X_start[0])).pin_memory()
-        eh = torch.from_numpy(np.ascontiguousarray(X_start[1])).pin_memory()
-        uh = torch.from_numpy(np.ascontiguousarray(X_start[2:])).pin_memory()
-        outh = torch.empty((nf,) + tuple(shape), dtype=torch.float64).pin_memory()
-        g2 = Solver(shape, model, sol, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"], pc_reuse=1)
         import ctypes as C
+        from paper_2209_08001_b200.nks import StepInfo
+        g2 = Solver(shape, model, sol, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"], pc_reuse=1)
+        g2.set_fields(c, eta, None)
+        for _ in range(args.warmup):
+            g2.run_adaptive(1)
+        Xh = torch.from_numpy(g2.get_state()).pin_memory()
         lib = g2.lib
+        rec = (StepInfo * 1)()
+        done = C.c_int32(0)
         barrier(pg)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(g2.stream)
-        for k, dt in enumerate(dts):
-            src = (ch, eh, uh) if k == 0 else (outh[0], outh[1], outh[2:])
-            rc = lib.nks_set_fields(g2.st, C.c_void_p(src[0].data_ptr()), C.c_void_p(src[1].data_ptr()),
-                                    C.c_void_p(src[2].data_ptr()), 0)
+        for _ in range(args.steps):
+            rc = lib.nks_set_state(g2.st, C.c_void_p(Xh[0].data_ptr()), C.c_void_p(Xh[1].data_ptr()),
+                                   C.c_void_p(Xh[2].data_ptr()), 0)
             assert rc == 0, rc
-            info = g2.step(dt)
-            rc = lib.nks_get_fields(g2.st, C.c_void_p(outh[0].data_ptr()), C.c_void_p(outh[1].data_ptr()),
-                                    C.c_void_p(outh[2].data_ptr()), 0)
+            rc = lib.nks_run_adaptive(g2.st, 1, C.c_double(0.0), rec, C.byref(done))
+            assert rc == 0 and done.value == 1, rc
+            rc = lib.nks_get_fields(g2.st, C.c_void_p(Xh[0].data_ptr()), C.c_void_p(Xh[1].data_ptr()),
+                                    C.c_void_p(Xh[2].data_ptr()), 0)
             assert rc == 0, rc
         e1.record(g2.stream)
         torch.cuda.synchronize()
         t_e2e = max_over_ranks(pg, e0.elapsed_time(e1))
-        del info
-        e2e = {"value": world * len(dts) / (t_e2e / 1e3), "unit": UNIT,
+        del g2
+        e2e = {"value": world * args.steps / (t_e2e / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": nf * N * 8, "d2h_bytes_per_step": nf * N * 8,
                "wall_s": time.perf_counter() - t0,
-               "note": "dt-forced replay of the timed steps through nks_set_fields/nks_step/nks_get_fields "
-                       "with pinned host buffers (on_device = 0)"}
+               "note": "per step: nks_set_state (pinned host X^n, on_device=0) + nks_run_adaptive(1) + "
+                       "nks_get_fields (pinned host); same trajectory and warm-up as the device leg"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = oracle_sample(cfg)
+
+    micro = {}
+    if not args.no_micro:
+        del g
+        torch.cuda.empty_cache()
+        for name, shp in (("2d512", (512, 512)), ("3d256", (256, 256, 256)), ("3d512", (512, 512, 512))):
+            try:
+                r = micro_kernels(shp)
+            except Exception as e:           # e.g. out of memory on a smaller part
+                micro[name] = {"error": str(e)[:200]}
+                continue
+            for k in r:
+                r[k]["frac_hbm"] = r[k]["GB_s"] / hbm
+            micro[name] = r
+
+    # DRAM traffic of the roofline kernel from the committed ncu --set full capture (per launch), if any
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        if roof.get("kernel") in tr and tuple(tr[roof["kernel"]].get("grid", [])) == tuple(shape):
+            traffic = tr[roof["kernel"]]["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    roof["traffic"] = traffic
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -342,7 +414,7 @@ def run_gpu(args, world, rank, local, pg):
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config_dict(cfg, world), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks,
-                "kernels": kern,
+                "kernels": kern, "kernels_micro": micro,
                 "phases_ms": {k: round(v["ms"], 3) for k, v in phases.items()},
                 "solver": {"newton_its": [r["newton_its"] for r in timed], "gmres_its": [r["gmres_its"] for r in timed],
                            "dt": [r["dt"] for r in timed], "retries": [r["retries"] for r in timed],

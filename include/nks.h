@@ -139,6 +139,13 @@ NKS_API nks_status nks_create(const nks_grid* grid, const nks_params* params, vo
 NKS_API nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, const double* u,
                           int32_t on_device);
 
+/* Replace X^n by (c, eta, u) -- u required -- WITHOUT restarting the run: time, the X^{n-1} history of
+ * the controller (Eq. sencondt), zeta and cbar0 are kept; u is projected onto the
+ * canonical gauge (reading R14) and T^n is recomputed.  This is how a caller streams the state
+ * through host memory between steps (bench.py's end-to-end leg).  NKS_E_DOMAIN if inadmissible,
+ * NKS_E_STATE before nks_set_fields. */
+NKS_API nks_status nks_set_state(nks_state* st, const double* c, const double* eta, const double* u, int32_t on_device);
+
 /* Copy X^n out (same layout as nks_set_fields; u must hold d*N doubles). */
 NKS_API nks_status nks_get_fields(const nks_state* st, double* c, double* eta, double* u, int32_t on_device);
 

@@ -763,6 +763,28 @@ nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, con
   });
 }
 
+nks_status nks_set_state(nks_state* st, const double* c, const double* eta, const double* u, int32_t on_device) {
+  if (!st || !c || !eta || !u) return NKS_E_INVALID;
+  if (!st->have_fields) return NKS_E_STATE;
+  return guarded(st, [&]() -> nks_status {
+    const long long N = st->N;
+    CK(cudaMemcpyAsync(st->Xn, c, N * sizeof(double), kind_in(on_device), st->stream));
+    CK(cudaMemcpyAsync(st->Xn + N, eta, N * sizeof(double), kind_in(on_device), st->stream));
+    CK(cudaMemcpyAsync(st->Xn + 2 * N, u, st->d * N * sizeof(double), kind_in(on_device), st->stream));
+    gauge(st, st->Xn);
+    level_prep(st);
+    double nrm, bad;
+    CK(cudaMemsetAsync(st->F, 0, st->nvec * sizeof(double), st->stream));
+    norm_adm(st, st->F, st->Xn, nrm, bad);
+    st->pc_valid = false;
+    if (bad > 0) {
+      st->err = "state inadmissible";
+      return NKS_E_DOMAIN;
+    }
+    return NKS_OK;
+  });
+}
+
 nks_status nks_get_fields(const nks_state* cst, double* c, double* eta, double* u, int32_t on_device) {
   nks_state* st = const_cast<nks_state*>(cst);
   if (!st || !c || !eta || !u) return NKS_E_INVALID;

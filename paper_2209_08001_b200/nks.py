@@ -67,6 +67,7 @@ _SIGS = {
     "nks_create": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), _P, C.c_size_t, _P, C.POINTER(_P)]),
     "nks_set_fields": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
     "nks_get_fields": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
+    "nks_set_state": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
     "nks_step": (C.c_int, [_P, C.c_double, C.POINTER(StepInfo)]),
     "nks_run_adaptive": (C.c_int, [_P, C.c_int32, C.c_double, C.POINTER(StepInfo), C.POINTER(C.c_int32)]),
     "nks_energy": (C.c_int, [_P, _D, _D]),
@@ -214,6 +215,13 @@ class Solver:
         rc = self.lib.nks_set_fields(self.st, c.ctypes.data_as(C.c_void_p), eta.ctypes.data_as(C.c_void_p),
                                      uu.ctypes.data_as(C.c_void_p) if uu is not None else None, 0)
         self._check(rc, "nks_set_fields")
+
+    def set_state(self, c, eta, u):
+        """Replace X^n without restarting the run (nks_set_state): controller history, time, zeta kept."""
+        tc, te, tu = self._dev(c, self.N), self._dev(eta, self.N), self._dev(u, self.d * self.N)
+        rc = self.lib.nks_set_state(self.st, C.c_void_p(tc.data_ptr()), C.c_void_p(te.data_ptr()),
+                                    C.c_void_p(tu.data_ptr()), 1)
+        self._check(rc, "nks_set_state")
 
     def get_state(self):
         """X^n as a (2+d, *shape) float64 numpy array."""
