@@ -376,7 +376,11 @@ __global__ void k_bilu0(SlotTables T, const int* __restrict__ nbr, const int* __
 }
 
 // ------------------------------------------------------------------------------------------ K6 RAS apply
-template <int NF>
+// Level-synchronous sweeps (one CTA per box; 3D, and 2D cases the pipelined k_ras2d does not cover).
+// NL = number of lower (= upper) slots: 6 in 2D, 12 in 3D; the slot loops are unrolled so that every
+// neighbour index and neighbour vector of a point is requested before the first one is used (two
+// dependent memory latencies per wavefront level instead of 2*NL).
+template <int NF, int NL>
 __global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const int* __restrict__ nbr,
                             const int* __restrict__ box_lev_off, const int* __restrict__ lev_ptr,
                             const int* __restrict__ box_pos_off, long long Ptot, long long ld, long long N,
@@ -397,20 +401,24 @@ __global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const in
   for (int l = l0; l < l1; ++l) {
     const int p0 = lev_ptr[l], p1 = lev_ptr[l + 1];
     for (int pos = p0 + threadIdx.x; pos < p1; pos += blockDim.x) {
+      int kk[NL];
+#pragma unroll
+      for (int a = 0; a < NL; ++a) kk[a] = __ldg(nbr + (long long)T.lower[a] * Ptot + pos);
+      double yk[NL][NF];
+#pragma unroll
+      for (int a = 0; a < NL; ++a)
+#pragma unroll
+        for (int f = 0; f < NF; ++f) yk[a][f] = kk[a] >= 0 ? y[f * Ptot + kk[a]] : 0.0;
       double acc[NF];
 #pragma unroll
       for (int f = 0; f < NF; ++f) acc[f] = y[f * Ptot + pos];
-      for (int ia = 0; ia < T.nlower; ++ia) {
-        const int sa = T.lower[ia];
-        const int k = nbr[(long long)sa * Ptot + pos];
-        if (k < 0) continue;
-        double yk[NF];
 #pragma unroll
-        for (int f = 0; f < NF; ++f) yk[f] = y[f * Ptot + k];
+      for (int a = 0; a < NL; ++a) {
+        const double* L = fac + (long long)(T.lower[a] * NF * NF) * ld + pos;
 #pragma unroll
         for (int rr = 0; rr < NF; ++rr)
 #pragma unroll
-          for (int c = 0; c < NF; ++c) acc[rr] = fma(-fac[((long long)(sa * NF + rr) * NF + c) * ld + pos], yk[c], acc[rr]);
+          for (int c = 0; c < NF; ++c) acc[rr] = fma(-__ldg(L + (long long)(rr * NF + c) * ld), yk[a][c], acc[rr]);
       }
 #pragma unroll
       for (int f = 0; f < NF; ++f) y[f * Ptot + pos] = acc[f];
@@ -421,27 +429,32 @@ __global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const in
   for (int l = l1 - 1; l >= l0; --l) {
     const int p0 = lev_ptr[l], p1 = lev_ptr[l + 1];
     for (int pos = p0 + threadIdx.x; pos < p1; pos += blockDim.x) {
+      int kk[NL];
+#pragma unroll
+      for (int a = 0; a < NL; ++a) kk[a] = __ldg(nbr + (long long)T.upper[a] * Ptot + pos);
+      double xk[NL][NF];
+#pragma unroll
+      for (int a = 0; a < NL; ++a)
+#pragma unroll
+        for (int f = 0; f < NF; ++f) xk[a][f] = kk[a] >= 0 ? y[f * Ptot + kk[a]] : 0.0;
       double acc[NF];
 #pragma unroll
       for (int f = 0; f < NF; ++f) acc[f] = y[f * Ptot + pos];
-      for (int iu = 0; iu < T.nupper; ++iu) {
-        const int su = T.upper[iu];
-        const int j = nbr[(long long)su * Ptot + pos];
-        if (j < 0) continue;
-        double xj[NF];
 #pragma unroll
-        for (int f = 0; f < NF; ++f) xj[f] = y[f * Ptot + j];
+      for (int a = 0; a < NL; ++a) {
+        const double* U = fac + (long long)(T.upper[a] * NF * NF) * ld + pos;
 #pragma unroll
         for (int rr = 0; rr < NF; ++rr)
 #pragma unroll
-          for (int c = 0; c < NF; ++c) acc[rr] = fma(-fac[((long long)(su * NF + rr) * NF + c) * ld + pos], xj[c], acc[rr]);
+          for (int c = 0; c < NF; ++c) acc[rr] = fma(-__ldg(U + (long long)(rr * NF + c) * ld), xk[a][c], acc[rr]);
       }
+      const double* D = fac + (long long)(T.diag * NF * NF) * ld + pos;
       double xo[NF];
 #pragma unroll
       for (int rr = 0; rr < NF; ++rr) {
         double s = 0.0;
 #pragma unroll
-        for (int c = 0; c < NF; ++c) s = fma(fac[((long long)(T.diag * NF + rr) * NF + c) * ld + pos], acc[c], s);
+        for (int c = 0; c < NF; ++c) s = fma(__ldg(D + (long long)(rr * NF + c) * ld), acc[c], s);
         xo[rr] = s;
       }
 #pragma unroll
@@ -490,9 +503,9 @@ void launch_ras_apply(const BoxSet& B, int nf, long long N, const double* fac, c
   const SlotTables T = make_tables(B, nf);
   const int threads = std::min(256, std::max(32, ((B.max_level_width + 31) / 32) * 32));
   if (nf == 4)
-    k_ras_apply<4><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, B.ld, N, fac, r, y, z);
+    k_ras_apply<4, 6><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, B.ld, N, fac, r, y, z);
   else
-    k_ras_apply<5><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, B.ld, N, fac, r, y, z);
+    k_ras_apply<5, 12><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, B.ld, N, fac, r, y, z);
 }
 
 }  // namespace nks
