@@ -189,7 +189,7 @@ __global__ void k_ras2d_pack(Ras2dArgs A, const double* __restrict__ fac, long l
 // its progress; that group is another warp of the CTA, or the last group of CTA s-1, which pushes
 // its two boundary rows and its progress word into this CTA's shared memory (DSMEM).  The backward
 // sweep mirrors all of it (rows below, descending steps).
-constexpr int kPub = 2;    // progress published every kPub steps
+constexpr int kPub = 4;    // progress published every kPub steps
 constexpr int kDL2 = 12;   // L2 prefetch distance (steps); off by default (NKS_RAS2D_DBG bit 8 clear = off)
 
 __device__ __forceinline__ void st_remote_u32(int* local_equiv, unsigned rank, int v) {
@@ -236,10 +236,11 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
   // ---- shared memory carve
   const int stage_elems = kGR * kPB;
   double* stage = reinterpret_cast<double*>(smem);                                          // [Wmax][NSW][8][kPB]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + (size_t)Wmax * NSW * stage_elems);  // [Wmax][NSW]
-  int* prog = reinterpret_cast<int*>(mbar + Wmax * NSW);                                    // [Wmax][2]: fwd-in, bwd-in
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + (size_t)Wmax * NSW * stage_elems);  // [Wmax][NSW] full
+  uint64_t* ebar = mbar + Wmax * NSW;                                                       // [Wmax][NSW] empty
+  int* prog = reinterpret_cast<int*>(ebar + Wmax * NSW);                                    // [Wmax][2]: fwd-in, bwd-in
   const int pitch = (ex + 4) * 4 + 2;       // doubles per S row: cells -2 .. ex+1 (2 zero pads each side) + bank spread
-  double* S = reinterpret_cast<double*>(smem + ((((size_t)Wmax * NSW * stage_elems * 8 + (size_t)Wmax * NSW * 8 +
+  double* S = reinterpret_cast<double*>(smem + ((((size_t)Wmax * NSW * stage_elems * 8 + (size_t)Wmax * NSW * 16 +
                                                   (size_t)Wmax * 8) + 15) & ~(size_t)15));  // rows -2 .. rmaxC+1
   auto Srow = [&](int rr) -> double* { return S + (size_t)(rr + 2) * pitch + 8; };   // cell 0 of row rr
 
@@ -252,8 +253,11 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
     int gy = (G.s0y + r0 + rr) % A.ny; if (gy < 0) gy += A.ny;
     Srow(rr)[i * 4 + ff] = __ldg(A.r + (long long)ff * A.N + (long long)gy * A.nx + gx);
   }
-  if (lane == 0) {
-    for (int k = 0; k < NSW; ++k) mbar_init(&mbar[w * NSW + k], 1);
+  if (lane == 0 && w < Wmax) {
+    for (int k = 0; k < NSW; ++k) {
+      mbar_init(&mbar[w * NSW + k], 1);
+      mbar_init(&ebar[w * NSW + k], 1);
+    }
     prog[w * 2 + 0] = -(1 << 30);
     prog[w * 2 + 1] = 1 << 30;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -263,8 +267,60 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
   long long T1;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(T1));
 
+  // ---- producer warp (warp Wmax): streams every group's factor chunks into its stage ring, one bulk
+  // copy per (group, step), as far ahead as the group's consumer has released stages (empty barriers)
+  if (w == Wmax) {
+    if (lane == 0) {
+      int kiss[16];
+      int ntot_w[16];
+      const double* chF_w[16];
+      const double* chB_w[16];
+      const int ng = g1 - g0;
+      for (int q = 0; q < ng; ++q) {
+        const int gq = g0 + q;
+        const int R0q = gq * kGR, R1q = min(R0q + kGR, ey);
+        ntot_w[q] = 2 * (2 * (R1q - 1) + ex - 1 - 2 * R0q + 1);
+        const long long cbq = ((long long)b * A.NGmax + gq) * A.KG;
+        chF_w[q] = A.chunkF + cbq * kGR * kPF;
+        chB_w[q] = A.chunkB + cbq * kGR * kPB;
+        kiss[q] = 0;
+      }
+      const unsigned stage_sa0 = smem_u32(stage), bar_sa0 = smem_u32(mbar), ebar_sa0 = smem_u32(ebar);
+      const unsigned fbytes = (unsigned)(kGR * kPF * 8), bbytes = (unsigned)(kGR * kPB * 8);
+      int remaining = ng;
+      while (remaining > 0) {
+        bool issued = false;
+        for (int q = 0; q < ng; ++q) {
+          const int k = kiss[q];
+          if (k >= ntot_w[q]) continue;
+          const int st = k % NSW, use = k / NSW;
+          if (use > 0) {      // the consumer must have released use-1 of this stage
+            unsigned ok;
+            asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                         : "=r"(ok) : "r"(ebar_sa0 + (q * NSW + st) * 8), "r"((unsigned)((use - 1) & 1)) : "memory");
+            if (!ok) continue;
+          }
+          const int nF = ntot_w[q] / 2;
+          const bool fw = k < nF;
+          const double* src = fw ? chF_w[q] + (size_t)k * kGR * kPF : chB_w[q] + (size_t)(2 * nF - 1 - k) * kGR * kPB;
+          const unsigned nb = fw ? fbytes : bbytes;
+          const unsigned bar = bar_sa0 + (q * NSW + st) * 8;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nb) : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           stage_sa0 + (unsigned)((q * NSW + st) * stage_elems * 8)),
+                       "l"(src), "r"(nb), "r"(bar)
+                       : "memory");
+          kiss[q] = k + 1;
+          if (k + 1 >= ntot_w[q]) --remaining;
+          issued = true;
+        }
+        if (!issued) __nanosleep(32);
+      }
+    }
+  }
+
   const int g = g0 + w;
-  if (g < g1) {
+  if (w < Wmax && g < g1) {
     const int R0 = g * kGR, R1 = min(R0 + kGR, ey);
     const int lr0 = R0 - r0;                                  // local S row of the group's first row
     const int tf0 = 2 * R0, tf1 = 2 * (R1 - 1) + ex - 1;
@@ -278,29 +334,9 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
     const double* chB = A.chunkB + cb * kGR * kPB;
     double* wstage = stage + (size_t)w * NSW * stage_elems;
     // 32-bit shared addresses, computed once (the loops never convert generic pointers)
-    const unsigned stage_sa = smem_u32(wstage), bar_sa = smem_u32(mbar + w * NSW);
+    const unsigned bar_sa = smem_u32(mbar + w * NSW), ebar_sa = smem_u32(ebar + w * NSW);
     const unsigned stage_bytes = (unsigned)(stage_elems * 8);
     const unsigned fbytes = (unsigned)(kGR * kPF * 8), bbytes = (unsigned)(kGR * kPB * 8);
-    // producer state (lane 0): next sequence index to copy / to prefetch into L2, and its stage
-    int kiss = 0, siss = 0, kpf = 0;
-    auto seq_src = [&](int k) -> const double* {
-      return k < nF ? chF + (size_t)k * kGR * kPF : chB + (size_t)(ntot - 1 - k) * kGR * kPB;
-    };
-    auto produce = [&]() {      // lane 0 only: keep NSW-1 copies and kDL2 prefetches in flight
-      if (A.dbg & 8)
-        for (; kpf < ntot && kpf < kiss + kDL2; ++kpf) l2_prefetch(seq_src(kpf), kpf < nF ? fbytes : bbytes);
-      const unsigned nb = kiss < nF ? fbytes : bbytes;
-      const unsigned bar = bar_sa + siss * 8;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nb) : "memory");
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       stage_sa + siss * stage_bytes),
-                   "l"(seq_src(kiss)), "r"(nb), "r"(bar)
-                   : "memory");
-      ++kiss;
-      if (++siss == NSW) siss = 0;
-    };
-    if (lane == 0)
-      for (int k = 0; k < NSW - 1 && k < ntot; ++k) produce();
     auto wait_stage = [&](int stg, unsigned par) {
       const unsigned a = bar_sa + stg * 8;
       unsigned done = 0;
@@ -336,12 +372,12 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
       double Yo1[4] = {0, 0, 0, 0}, Yo2[4] = {0, 0, 0, 0};                 // own row at t-1, t-2
       double Ya1[4] = {0, 0, 0, 0}, Ya2[4] = {0, 0, 0, 0}, Ya3[4] = {0, 0, 0, 0};   // row above at t-1..t-3
       int i = tf0 - 2 * j;
+#pragma unroll 6
       for (int k = 0; k < nF; ++k, ++i) {
         const int t = tf0 + k;
         const bool active = row_ok && i >= 0 && i < ex;
         const int ic = min(max(i, 0), ex - 1);
         __syncwarp();
-        if (lane == 0 && kiss < ntot) produce();
         // row two above at t-4 = the row above's Ya3 (before it shifts); lag-1 vectors at t-1
         double Yaa4[4], n_o1[4], n_a1[4];
 #pragma unroll
@@ -396,6 +432,8 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
           Sown[i * 4 + f] = y;
           if (dn_remote && j >= R1 - 2) st_remote(Srow(j - r1) + i * 4 + f, (unsigned)(s + 1), y);
         }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ebar_sa + stg * 8) : "memory");
         if (++stg == NSW) { stg = 0; par ^= 1u; }
         if (has_dn && ((k & (kPub - 1)) == kPub - 1 || k == nF - 1)) {
           __syncwarp();
@@ -413,12 +451,12 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
       double Xo1[4] = {0, 0, 0, 0}, Xo2[4] = {0, 0, 0, 0};                 // own row at t+1, t+2 (i+1, i+2)
       double Xb1[4] = {0, 0, 0, 0}, Xb2[4] = {0, 0, 0, 0}, Xb3[4] = {0, 0, 0, 0};   // row below at t+1..t+3 (i-1, i, i+1)
       int i = tf1 - 2 * j;
+#pragma unroll 6
       for (int kb = 0; kb < nF; ++kb, --i) {
         const int t = tf1 - kb;
         const bool active = row_ok && i >= 0 && i < ex;
         const int ic = min(max(i, 0), ex - 1);
         __syncwarp();
-        if (lane == 0 && kiss < ntot) produce();
         double Xbb4[4], n_o1[4], n_b1[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -475,6 +513,8 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
           Sown[i * 4 + f] = x;
           if (up_remote && j < R0 + 2) st_remote(Srow(Rup + (j - r0)) + i * 4 + f, (unsigned)(s - 1), x);
         }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ebar_sa + stg * 8) : "memory");
         if (++stg == NSW) { stg = 0; par ^= 1u; }
         if (has_up && ((kb & (kPub - 1)) == kPub - 1 || kb == nF - 1)) {
           __syncwarp();
@@ -554,7 +594,7 @@ static bool ras2d_geom(const nks_grid& g, Ras2dGeom& Gm, int cs_try = 0) {
   Gm.CS = CS;
   Gm.Wmax = (Gm.NGmax + CS - 1) / CS;
   Gm.KG = 2 * (kGR - 1) + Gm.exmax;
-  return Gm.Wmax <= 16;
+  return Gm.Wmax <= 15;
 }
 
 // Workspace bytes for the packed chunks + geometry (0 when the pipelined path does not apply).
@@ -572,7 +612,7 @@ static int ras2d_fit(const Ras2dGeom& Gm, size_t& smem, int& max_clusters) {
   const int rmaxC = Gm.Wmax * kGR;
   const int pitch = (Gm.exmax + 4) * 4 + 2;
   const size_t fixed = (size_t)(rmaxC + 4) * pitch * 8 + (size_t)Gm.Wmax * 8 + 64;
-  const size_t per_stage = (size_t)Gm.Wmax * (kGR * kPB * 8 + 8);
+  const size_t per_stage = (size_t)Gm.Wmax * (kGR * kPB * 8 + 16);
   int dev = 0, maxsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -584,7 +624,7 @@ static int ras2d_fit(const Ras2dGeom& Gm, size_t& smem, int& max_clusters) {
   if (cudaFuncSetAttribute(k_ras2d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(Gm.nbox * Gm.CS, 1, 1);
-  cfg.blockDim = dim3(32 * Gm.Wmax, 1, 1);
+  cfg.blockDim = dim3(32 * (Gm.Wmax + 1), 1, 1);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -638,7 +678,7 @@ void* ras2d_plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, 
   Ras2dPlan* P = new Ras2dPlan();
   P->CS = Gm.CS; P->NSW = NSW; P->Wmax = Gm.Wmax; P->NGmax = Gm.NGmax; P->KG = Gm.KG; P->nbox = Gm.nbox;
   P->rmaxC = Gm.Wmax * kGR;
-  P->threads = 32 * Gm.Wmax;
+  P->threads = 32 * (Gm.Wmax + 1);      // + the producer warp
   P->smem = smem;
   P->npts_total = npts;
   P->max_clusters = ncl;
