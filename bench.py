@@ -262,6 +262,49 @@ def micro_kernels(shape, reps=10):
     return out
 
 
+def micro_sharded(shape, pg, reps=10):
+    """Config 5: F and J.v of a z-sharded 3D grid (each rank one slab, 2 ghost planes per side), the
+    NCCL halo exchange of every input included in the timed operator; time = max over ranks."""
+    import torch
+    from paper_2209_08001_b200.shard import SlabOperators
+    ops = SlabOperators(shape, ni.model_default(), ni.solver_default())
+    d = 3
+    nf = 2 + d
+    ls = ops.local_shape
+    gen = torch.Generator(device="cuda").manual_seed(1234 + ops.lo)
+    Xa = torch.empty((nf,) + ls, device="cuda", dtype=torch.float64)
+    Xa[0] = 0.1622 + (torch.rand(ls, device="cuda", dtype=torch.float64, generator=gen) - 0.5) * 0.01
+    Xa[1] = 0.1 + (torch.rand(ls, device="cuda", dtype=torch.float64, generator=gen) - 0.5) * 0.02
+    Xa[2:] = 0.0
+    ops.set_level_n(Xa, 0.1622)
+    Xb = Xa.clone()
+    Xb[:2] += (torch.rand((2,) + ls, device="cuda", dtype=torch.float64, generator=gen) - 0.5) * 2e-3
+    v = (torch.rand((nf,) + ls, device="cuda", dtype=torch.float64, generator=gen) - 0.5) * 2
+    del Xa
+    for _ in range(2):
+        ops.residual(Xb, 0.01)
+        ops.jv(Xb, v, 0.01)
+    res = {}
+    for key in ("residual", "jv"):
+        barrier(pg)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            if key == "residual":
+                ops.residual(Xb, 0.01)
+            else:
+                ops.jv(Xb, v, 0.01)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = max_over_ranks(pg, e0.elapsed_time(e1) / reps)
+        Ng = int(np.prod(shape))
+        res[key] = {"ms_incl_halo_exchange": ms, "GDOF_s": nf * Ng / (ms * 1e-3) / 1e9}
+    del ops, Xb, v
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_gpu(args, world, rank, local, pg):
     import torch
     from paper_2209_08001_b200 import Solver
@@ -383,8 +426,17 @@ def run_gpu(args, world, rank, local, pg):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = oracle_sample(cfg)
 
+    sharded = None
+    if world > 1 and not args.no_micro:
+        del g
+        torch.cuda.empty_cache()
+        try:
+            sharded = {"grid": [512, 512, 512], "sharding": f"z-slabs x {world}", **micro_sharded((512, 512, 512), pg)}
+        except Exception as e:
+            sharded = {"error": str(e)[:200]}
+        g = None
     micro = {}
-    if not args.no_micro:
+    if not args.no_micro and world == 1:
         del g
         torch.cuda.empty_cache()
         for name, shp in (("2d512", (512, 512)), ("3d256", (256, 256, 256)), ("3d512", (512, 512, 512))):
@@ -414,7 +466,7 @@ def run_gpu(args, world, rank, local, pg):
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config_dict(cfg, world), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks,
-                "kernels": kern, "kernels_micro": micro,
+                "kernels": kern, "kernels_micro": micro, "kernels_micro_sharded": sharded,
                 "phases_ms": {k: round(v["ms"], 3) for k, v in phases.items()},
                 "solver": {"newton_its": [r["newton_its"] for r in timed], "gmres_its": [r["gmres_its"] for r in timed],
                            "dt": [r["dt"] for r in timed], "retries": [r["retries"] for r in timed],

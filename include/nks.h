@@ -66,6 +66,11 @@ typedef struct {
   double h;          /* uniform mesh size (0.25)                                         */
   int32_t nsub[3];   /* RAS subdomain boxes per axis (1 <= nsub[j] <= n[j]); nsub[2]=1 in 2D     */
   int32_t overlap;   /* delta: cells added on each side of every box (0..8)      */
+  int32_t zghost;    /* 0: periodic grid.  2: this state is one z-slab of a z-sharded 3D grid --  */
+                     /* n[2] counts 2 ghost planes per side that the caller fills (halo exchange, */
+                     /* paper_2209_08001_b200/shard.py); F and J.v are evaluated on the own       */
+                     /* planes only, with no z wrap.  Slab states serve nks_eval_residual /       */
+                     /* nks_eval_jv; pc_type must be NKS_PC_NONE.        */
 } nks_grid;
 
 typedef struct {
@@ -145,6 +150,10 @@ NKS_API nks_status nks_set_fields(nks_state* st, const double* c, const double* 
  * through host memory between steps (bench.py's end-to-end leg).  NKS_E_DOMAIN if inadmissible,
  * NKS_E_STATE before nks_set_fields. */
 NKS_API nks_status nks_set_state(nks_state* st, const double* c, const double* eta, const double* u, int32_t on_device);
+
+/* Set cbar0, the mean composition of the eigenstrain, explicitly -- used by z-slab states,
+ * whose local mean is not the grid's.  Recomputes T^n. */
+NKS_API nks_status nks_set_cbar0(nks_state* st, double cbar0);
 
 /* Copy X^n out (same layout as nks_set_fields; u must hold d*N doubles). */
 NKS_API nks_status nks_get_fields(const nks_state* st, double* c, double* eta, double* u, int32_t on_device);

@@ -104,6 +104,9 @@ const char* validate(const nks_grid* g, const nks_params* p) {
   if (p->gmres_restart < 1 || p->gmres_restart > 60) return "gmres_restart must be in 1..60";
   if (p->newton_maxit < 0 || p->gmres_maxit < 1) return "bad iteration limits";
   if (p->pc_type != NKS_PC_NONE && p->pc_type != NKS_PC_RAS_BILU0) return "unknown pc_type";
+  if (g->zghost != 0 && g->zghost != 2) return "zghost must be 0 or 2";
+  if (g->zghost == 2 && (g->dim != 3 || g->n[2] < 5 || p->pc_type != NKS_PC_NONE))
+    return "z-slab states (zghost = 2) are 3D, need n[2] >= 5 and pc_type NONE";
   if (p->pc_type == NKS_PC_RAS_BILU0) {
     for (int j = 0; j < 3; ++j)
       if (g->nsub[j] < 1 || g->nsub[j] > g->n[j]) return "nsub[j] must be in 1..n[j]";
@@ -163,6 +166,7 @@ DevParams make_devparams(const nks_grid& g, const nks_params& p) {
   DevParams P{};
   P.dim = g.dim;
   P.nx = g.n[0]; P.ny = g.n[1]; P.nz = g.n[2];
+  P.zg = g.zghost;
   P.N = (long long)g.n[0] * g.n[1] * g.n[2];
   P.h = g.h;
   P.inv_h2 = 1.0 / (g.h * g.h);
@@ -759,6 +763,17 @@ nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, con
       st->err = "initial state inadmissible";
       return NKS_E_DOMAIN;
     }
+    return NKS_OK;
+  });
+}
+
+nks_status nks_set_cbar0(nks_state* st, double cbar0) {
+  if (!st) return NKS_E_INVALID;
+  if (!st->have_fields) return NKS_E_STATE;
+  return guarded(st, [&]() -> nks_status {
+    st->dp.cbar0 = cbar0;
+    level_prep(st);
+    sync(st);
     return NKS_OK;
   });
 }

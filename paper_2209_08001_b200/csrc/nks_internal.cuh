@@ -21,6 +21,7 @@ constexpr int kRedThreads = 256;
 // Parameters passed by value to every kernel (fp64 model constants derived on the host).
 struct DevParams {
   int dim, nx, ny, nz;
+  int zg;               // z ghost planes per side (0: periodic in z; 2: slab of a z-sharded grid, no z wrap)
   long long N;          // points
   double h, inv_h2, inv_2h, inv_4h2;
   double dt, inv_dt;

@@ -89,10 +89,11 @@ __global__ void __launch_bounds__(tj::NT) k_jv_tiled(DevParams P, const double* 
   double* sw = sa + 2 * PL;                  // [N3][RL]
 
   const long long N = P.N;
-  const int nx = P.nx, ny = P.ny, nz = P.nz;
+  const int nx = P.nx, ny = P.ny, nz = P.nz, zg = P.zg;
+  const int ncz = nz - 2 * zg;                 // computed planes (all, or the slab's own planes)
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int z0 = DIM == 3 ? blockIdx.z * zc : 0;
-  const int z1 = DIM == 3 ? min(z0 + zc, nz) : 1;
+  const int z1 = DIM == 3 ? min(z0 + zc, ncz) : 1;
   const int tid = threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
 
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(tj::NT) k_jv_tiled(DevParams P, const double* 
     gy = ((gy % ny) + ny) % ny;
     goff[r] = (long long)gy * nx + gx;
   }
-  auto zw = [&](int z) { return z < 0 ? z + nz : (z >= nz ? z - nz : z); };
+  auto zw = [&](int z) { return zg ? z + zg : (z < 0 ? z + nz : (z >= nz ? z - nz : z)); };   // memory plane
   auto load_plane = [&](double* dst, const double* src, int z) {
     const long long base = (long long)zw(z) * nx * ny;
 #pragma unroll
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(tj::NT) k_jv_tiled(DevParams P, const double* 
       __syncthreads();
     }
     if (inside) {
-      const long long i = ((long long)z * ny + y) * nx + x;
+      const long long i = ((long long)(z + zg) * ny + y) * nx + x;
       const double* C0 = sc + slot(z, NC) * PL;
       const double* E0 = se + slot(z, N3) * PL;
       const double* M0 = smo + slot(z, N3) * PL;
@@ -299,10 +300,11 @@ __global__ void __launch_bounds__(tj::NT) k_residual_tiled(DevParams P, const do
   double* sg = sT + PL;                      // [N3][RL]       G_c
 
   const long long N = P.N;
-  const int nx = P.nx, ny = P.ny, nz = P.nz;
+  const int nx = P.nx, ny = P.ny, nz = P.nz, zg = P.zg;
+  const int ncz = nz - 2 * zg;                 // computed planes (all, or the slab's own planes)
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int z0 = DIM == 3 ? blockIdx.z * zc : 0;
-  const int z1 = DIM == 3 ? min(z0 + zc, nz) : 1;
+  const int z1 = DIM == 3 ? min(z0 + zc, ncz) : 1;
   const int tid = threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
   int cell[2];
@@ -316,7 +318,7 @@ __global__ void __launch_bounds__(tj::NT) k_residual_tiled(DevParams P, const do
     gy = ((gy % ny) + ny) % ny;
     goff[r] = (long long)gy * nx + gx;
   }
-  auto zw = [&](int z) { return z < 0 ? z + nz : (z >= nz ? z - nz : z); };
+  auto zw = [&](int z) { return zg ? z + zg : (z < 0 ? z + nz : (z >= nz ? z - nz : z)); };   // memory plane
   auto load_plane = [&](double* dst, const double* src, int z) {
     const long long base = (long long)zw(z) * nx * ny;
 #pragma unroll
@@ -372,7 +374,7 @@ __global__ void __launch_bounds__(tj::NT) k_residual_tiled(DevParams P, const do
           const int m1 = tslot(z - 1, N3) * PL + k, p1 = tslot(z + 1, N3) * PL + k;
           le += (sea[m1] + seb[m1]) + (sea[p1] + seb[p1]) - 2.0 * (ea + eb);
         }
-        const long long i = ((long long)z * ny + py) * nx + px;
+        const long long i = ((long long)(z + zg) * ny + py) * nx + px;
         F[N + i] = (eb - ea) * P.inv_dt + ge + gel * le;
       }
     }
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(tj::NT) k_residual_tiled(DevParams P, const do
       __syncthreads();
     }
     if (inside) {
-      const long long i = ((long long)z * ny + y) * nx + x;
+      const long long i = ((long long)(z + zg) * ny + y) * nx + x;
       const double* CA = sca + tslot(z, NC) * PL;
       const double* CB = scb + tslot(z, NC) * PL;
       const double* G0 = sg + tslot(z, N3) * RL;
@@ -503,10 +505,11 @@ void launch_residual_tiled(const DevParams& P, const double* Xa, const double* X
   const int tiles = ((P.nx + TX - 1) / TX) * ((P.ny + TY - 1) / TY);
   int zc = 1;
   if (dim == 3) {
-    zc = P.nz;
-    while (zc > 16 && (long long)tiles * ((P.nz + zc - 1) / zc) < 148 * 2 * 4) zc = (zc + 1) / 2;
+    const int ncz = P.nz - 2 * P.zg;
+    zc = ncz;
+    while (zc > 16 && (long long)tiles * ((ncz + zc - 1) / zc) < 148 * 2 * 4) zc = (zc + 1) / 2;
   }
-  dim3 grid((P.nx + TX - 1) / TX, (P.ny + TY - 1) / TY, dim == 3 ? (P.nz + zc - 1) / zc : 1);
+  dim3 grid((P.nx + TX - 1) / TX, (P.ny + TY - 1) / TY, dim == 3 ? (P.nz - 2 * P.zg + zc - 1) / zc : 1);
   if (dim == 2) k_residual_tiled<2><<<grid, NT, smem, s>>>(P, Xa, Xb, Ta, F, zc);
   else k_residual_tiled<3><<<grid, NT, smem, s>>>(P, Xa, Xb, Ta, F, zc);
 }
@@ -532,10 +535,11 @@ void launch_jv_tiled(const DevParams& P, const double* Xa, const double* jac4, c
   int zc = 1;
   if (dim == 3) {
     // z chunks: enough CTAs for ~4 waves of 2 CTAs/SM, chunks long enough to amortise the 4-plane prologue
-    zc = P.nz;
-    while (zc > 16 && (long long)tiles * ((P.nz + zc - 1) / zc) < 148 * 2 * 4) zc = (zc + 1) / 2;
+    const int ncz = P.nz - 2 * P.zg;
+    zc = ncz;
+    while (zc > 16 && (long long)tiles * ((ncz + zc - 1) / zc) < 148 * 2 * 4) zc = (zc + 1) / 2;
   }
-  dim3 grid((P.nx + TX - 1) / TX, (P.ny + TY - 1) / TY, dim == 3 ? (P.nz + zc - 1) / zc : 1);
+  dim3 grid((P.nx + TX - 1) / TX, (P.ny + TY - 1) / TY, dim == 3 ? (P.nz - 2 * P.zg + zc - 1) / zc : 1);
   if (dim == 2) k_jv_tiled<2><<<grid, NT, smem, s>>>(P, Xa, jac4, v, out, zc);
   else k_jv_tiled<3><<<grid, NT, smem, s>>>(P, Xa, jac4, v, out, zc);
 }

@@ -25,7 +25,7 @@ PHASES = ["residual", "jv", "ras_apply", "assemble", "factor", "gmres_vec", "red
 
 class Grid(C.Structure):
     _fields_ = [("dim", C.c_int32), ("n", C.c_int32 * 3), ("h", C.c_double), ("nsub", C.c_int32 * 3),
-                ("overlap", C.c_int32)]
+                ("overlap", C.c_int32), ("zghost", C.c_int32)]
 
 
 class Params(C.Structure):
@@ -68,6 +68,7 @@ _SIGS = {
     "nks_set_fields": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
     "nks_get_fields": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
     "nks_set_state": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
+    "nks_set_cbar0": (C.c_int, [_P, C.c_double]),
     "nks_step": (C.c_int, [_P, C.c_double, C.POINTER(StepInfo)]),
     "nks_run_adaptive": (C.c_int, [_P, C.c_int32, C.c_double, C.POINTER(StepInfo), C.POINTER(C.c_int32)]),
     "nks_energy": (C.c_int, [_P, _D, _D]),
@@ -109,7 +110,7 @@ class NKSError(RuntimeError):
         self.status = status
 
 
-def make_grid(shape, h=0.25, nsub=None, overlap=2) -> Grid:
+def make_grid(shape, h=0.25, nsub=None, overlap=2, zghost=0) -> Grid:
     """shape and nsub in C order: (ny, nx) or (nz, ny, nx)."""
     d = len(shape)
     g = Grid()
@@ -123,6 +124,7 @@ def make_grid(shape, h=0.25, nsub=None, overlap=2) -> Grid:
     for j in range(3):
         g.nsub[j] = int(ns[j])
     g.overlap = int(overlap)
+    g.zghost = int(zghost)
     return g
 
 
@@ -148,7 +150,7 @@ class Solver:
     """One NKS state on the current CUDA device (single GPU)."""
 
     def __init__(self, shape, model: dict, solver: dict, h=0.25, nsub=None, overlap=2,
-                 pc_type=PC_RAS_BILU0, pc_reuse=1, device=None):
+                 pc_type=PC_RAS_BILU0, pc_reuse=1, device=None, zghost=0):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2209_08001_b200 needs a CUDA device (B200, sm_100a)")
@@ -159,7 +161,7 @@ class Solver:
         self.nf = 2 + self.d
         self.N = int(np.prod(shape))
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.grid = make_grid(shape, h, nsub, overlap)
+        self.grid = make_grid(shape, h, nsub, overlap, zghost)
         self.params = make_params(model, solver, pc_type, pc_reuse)
         nbytes = self.lib.nks_workspace_bytes(C.byref(self.grid), C.byref(self.params))
         if nbytes == 0:
@@ -222,6 +224,9 @@ class Solver:
         rc = self.lib.nks_set_state(self.st, C.c_void_p(tc.data_ptr()), C.c_void_p(te.data_ptr()),
                                     C.c_void_p(tu.data_ptr()), 1)
         self._check(rc, "nks_set_state")
+
+    def set_cbar0(self, cbar0):
+        self._check(self.lib.nks_set_cbar0(self.st, C.c_double(cbar0)), "nks_set_cbar0")
 
     def get_state(self):
         """X^n as a (2+d, *shape) float64 numpy array."""
