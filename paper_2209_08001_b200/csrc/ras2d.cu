@@ -337,6 +337,12 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
     const unsigned bar_sa = smem_u32(mbar + w * NSW), ebar_sa = smem_u32(ebar + w * NSW);
     const unsigned stage_bytes = (unsigned)(stage_elems * 8);
     const unsigned fbytes = (unsigned)(kGR * kPF * 8), bbytes = (unsigned)(kGR * kPB * 8);
+    auto test_stage = [&](int stg, unsigned par) -> unsigned {     // non-blocking probe, issued early
+      unsigned ok;
+      asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                   : "=r"(ok) : "r"(bar_sa + stg * 8), "r"(par));
+      return ok;
+    };
     auto wait_stage = [&](int stg, unsigned par) {
       const unsigned a = bar_sa + stg * 8;
       unsigned done = 0;
@@ -378,6 +384,7 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
         const bool active = row_ok && i >= 0 && i < ex;
         const int ic = min(max(i, 0), ex - 1);
         __syncwarp();
+        const unsigned ready = test_stage(stg, par);
         // row two above at t-4 = the row above's Ya3 (before it shifts); lag-1 vectors at t-1
         double Yaa4[4], n_o1[4], n_a1[4];
 #pragma unroll
@@ -389,11 +396,8 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
         if (has_up) {
           const int need = min(t - 1, tf1_up);
           if (seen < need) {
-            int v = 0;
-            if (lane == 0) {
-              do { v = ld_acq_cluster(myF); } while (v < need);
-            }
-            __syncwarp();
+            int v;
+            do { v = ld_acq_cluster(myF); } while (__any_sync(0xffffffffu, v < need));
             seen = __shfl_sync(0xffffffffu, v, 0);
           }
         }
@@ -404,20 +408,20 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
         }
         // the group's first rows take the rows above straight from S (the group above ran steps this
         // warp never executed, so there is no history to shift)
-        if (rl == 0) {
+        {
+          // uniform loads (valid rows for every lane), selected for the group's first rows: no branch
           const double2 p1 = lds2(Sup1 + (ic + 1) * 4), p2 = lds2(Sup1 + (ic + 1) * 4 + 2);
           const double2 q1 = lds2(Sup1 + ic * 4), q2 = lds2(Sup1 + ic * 4 + 2);
           const double2 r1 = lds2(Sup1 + (ic - 1) * 4), r2 = lds2(Sup1 + (ic - 1) * 4 + 2);
           const double2 s1 = lds2(Sup2 + ic * 4), s2 = lds2(Sup2 + ic * 4 + 2);
-          Ya1[0] = p1.x; Ya1[1] = p1.y; Ya1[2] = p2.x; Ya1[3] = p2.y;
-          Ya2[0] = q1.x; Ya2[1] = q1.y; Ya2[2] = q2.x; Ya2[3] = q2.y;
-          Ya3[0] = r1.x; Ya3[1] = r1.y; Ya3[2] = r2.x; Ya3[3] = r2.y;
-          Yaa4[0] = s1.x; Yaa4[1] = s1.y; Yaa4[2] = s2.x; Yaa4[3] = s2.y;
-        } else if (rl == 1) {
-          const double2 s1 = lds2(Sup2 + ic * 4), s2 = lds2(Sup2 + ic * 4 + 2);
-          Yaa4[0] = s1.x; Yaa4[1] = s1.y; Yaa4[2] = s2.x; Yaa4[3] = s2.y;
+          const bool b0 = rl == 0, b01 = rl < 2;
+          Ya1[0] = b0 ? p1.x : Ya1[0]; Ya1[1] = b0 ? p1.y : Ya1[1]; Ya1[2] = b0 ? p2.x : Ya1[2]; Ya1[3] = b0 ? p2.y : Ya1[3];
+          Ya2[0] = b0 ? q1.x : Ya2[0]; Ya2[1] = b0 ? q1.y : Ya2[1]; Ya2[2] = b0 ? q2.x : Ya2[2]; Ya2[3] = b0 ? q2.y : Ya2[3];
+          Ya3[0] = b0 ? r1.x : Ya3[0]; Ya3[1] = b0 ? r1.y : Ya3[1]; Ya3[2] = b0 ? r2.x : Ya3[2]; Ya3[3] = b0 ? r2.y : Ya3[3];
+          Yaa4[0] = b01 ? s1.x : Yaa4[0]; Yaa4[1] = b01 ? s1.y : Yaa4[1];
+          Yaa4[2] = b01 ? s2.x : Yaa4[2]; Yaa4[3] = b01 ? s2.y : Yaa4[3];
         }
-        wait_stage(stg, par);
+        if (!ready) wait_stage(stg, par);
         const double* L = tile0 + (size_t)stg * stage_elems;
         double a0 = Sown[ic * 4 + f], a1 = 0.0;
         fms4(L + 0 * 16, Yaa4, a0, a1);      // (0,-2)
@@ -457,6 +461,7 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
         const bool active = row_ok && i >= 0 && i < ex;
         const int ic = min(max(i, 0), ex - 1);
         __syncwarp();
+        const unsigned ready = test_stage(stg, par);
         double Xbb4[4], n_o1[4], n_b1[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -467,11 +472,8 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
         if (has_dn) {
           const int need = max(t + 1, tf0_dn);
           if (seen > need) {
-            int v = 0;
-            if (lane == 0) {
-              do { v = ld_acq_cluster(myB); } while (v > need);
-            }
-            __syncwarp();
+            int v;
+            do { v = ld_acq_cluster(myB); } while (__any_sync(0xffffffffu, v > need));
             seen = __shfl_sync(0xffffffffu, v, 0);
           }
         }
@@ -480,20 +482,23 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
           Xb3[c] = Xb2[c]; Xb2[c] = Xb1[c]; Xb1[c] = n_b1[c];
           Xo2[c] = Xo1[c]; Xo1[c] = n_o1[c];
         }
-        if (row_ok && (rl == kGR - 1 || j == R1 - 1)) {
-          const double2 p1 = lds2(Sdn1 + (ic - 1) * 4), p2 = lds2(Sdn1 + (ic - 1) * 4 + 2);
-          const double2 q1 = lds2(Sdn1 + ic * 4), q2 = lds2(Sdn1 + ic * 4 + 2);
-          const double2 r1 = lds2(Sdn1 + (ic + 1) * 4), r2 = lds2(Sdn1 + (ic + 1) * 4 + 2);
-          const double2 s1 = lds2(Sdn2 + ic * 4), s2 = lds2(Sdn2 + ic * 4 + 2);
-          Xb1[0] = p1.x; Xb1[1] = p1.y; Xb1[2] = p2.x; Xb1[3] = p2.y;
-          Xb2[0] = q1.x; Xb2[1] = q1.y; Xb2[2] = q2.x; Xb2[3] = q2.y;
-          Xb3[0] = r1.x; Xb3[1] = r1.y; Xb3[2] = r2.x; Xb3[3] = r2.y;
-          Xbb4[0] = s1.x; Xbb4[1] = s1.y; Xbb4[2] = s2.x; Xbb4[3] = s2.y;
-        } else if (row_ok && (rl == kGR - 2 || j == R1 - 2)) {
-          const double2 s1 = lds2(Sdn2 + ic * 4), s2 = lds2(Sdn2 + ic * 4 + 2);
-          Xbb4[0] = s1.x; Xbb4[1] = s1.y; Xbb4[2] = s2.x; Xbb4[3] = s2.y;
+        {
+          // uniform loads; lanes of rows past the group's end read their own row (never selected)
+          const bool last = row_ok && (rl == kGR - 1 || j == R1 - 1);
+          const bool last2 = row_ok && (rl >= kGR - 2 || j >= R1 - 2);
+          const double* d1 = row_ok ? Sdn1 : Sown;
+          const double* d2 = row_ok ? Sdn2 : Sown;
+          const double2 p1 = lds2(d1 + (ic - 1) * 4), p2 = lds2(d1 + (ic - 1) * 4 + 2);
+          const double2 q1 = lds2(d1 + ic * 4), q2 = lds2(d1 + ic * 4 + 2);
+          const double2 r1 = lds2(d1 + (ic + 1) * 4), r2 = lds2(d1 + (ic + 1) * 4 + 2);
+          const double2 s1 = lds2(d2 + ic * 4), s2 = lds2(d2 + ic * 4 + 2);
+          Xb1[0] = last ? p1.x : Xb1[0]; Xb1[1] = last ? p1.y : Xb1[1]; Xb1[2] = last ? p2.x : Xb1[2]; Xb1[3] = last ? p2.y : Xb1[3];
+          Xb2[0] = last ? q1.x : Xb2[0]; Xb2[1] = last ? q1.y : Xb2[1]; Xb2[2] = last ? q2.x : Xb2[2]; Xb2[3] = last ? q2.y : Xb2[3];
+          Xb3[0] = last ? r1.x : Xb3[0]; Xb3[1] = last ? r1.y : Xb3[1]; Xb3[2] = last ? r2.x : Xb3[2]; Xb3[3] = last ? r2.y : Xb3[3];
+          Xbb4[0] = last2 ? s1.x : Xbb4[0]; Xbb4[1] = last2 ? s1.y : Xbb4[1];
+          Xbb4[2] = last2 ? s2.x : Xbb4[2]; Xbb4[3] = last2 ? s2.y : Xbb4[3];
         }
-        wait_stage(stg, par);
+        if (!ready) wait_stage(stg, par);
         const double* U = utile0 + (size_t)stg * stage_elems;
         double a0 = Sown[ic * 4 + f], a1 = 0.0;
         fms4(U + 6 * 16, Xbb4, a0, a1);      // (0,2)
