@@ -187,7 +187,7 @@ __device__ __forceinline__ void block_partials_32(double (&acc)[32], double* __r
 }
 
 // out[k] = V_k . w (k < nk), out[nk] = w . w, out[nk+1..31] = 0
-__global__ void __launch_bounds__(kRedThreads) k_cgs_dot(long long n, int nk, const double* __restrict__ V, long long ld,
+__global__ void __launch_bounds__(kRedThreads, 2) k_cgs_dot(long long n, int nk, const double* __restrict__ V, long long ld,
                                                        const double* __restrict__ w, double* __restrict__ part,
                                                        double* __restrict__ out, unsigned* __restrict__ counter) {
   double acc[32];
@@ -305,7 +305,7 @@ void launch_update_scale(long long n, int nk, const double* V, long long ld, con
   NK_DISPATCH(nk, k_update_scale, <<<vec_blocks(n), 256, 0, s>>>(n, nk, V, ld, h, scale, w));
 }
 
-static int cgs_blocks(long long n) { return (int)std::min<long long>((n + kRedThreads - 1) / kRedThreads, 148); }
+static int cgs_blocks(long long n) { return (int)std::min<long long>((n + kRedThreads - 1) / kRedThreads, 148 * 2); }
 
 void launch_cgs_dot(long long n, int nk, const double* V, long long ld, const double* w, double* part, double* out,
                     unsigned* counter, cudaStream_t s) {
@@ -314,7 +314,8 @@ void launch_cgs_dot(long long n, int nk, const double* V, long long ld, const do
 
 void launch_cgs_update_dot(long long n, int nk, const double* V, long long ld, const double* h, double* w, double* part,
                            double* out, unsigned* counter, cudaStream_t s) {
-  k_cgs_update_dot<<<cgs_blocks(n), kRedThreads, 0, s>>>(n, nk, V, ld, h, w, part, out, counter);
+  k_cgs_update_dot<<<(int)std::min<long long>((n + kRedThreads - 1) / kRedThreads, 148), kRedThreads, 0, s>>>(
+      n, nk, V, ld, h, w, part, out, counter);
 }
 
 void launch_update_scale_dev(long long n, int nk, const double* V, long long ld, const double* hv, double* w,
