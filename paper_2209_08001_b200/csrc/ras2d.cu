@@ -213,7 +213,7 @@ __device__ __forceinline__ void fms4(const double* p, const double (&v)[4], doub
   a1 = fma(-b23.y, v[3], a1);
 }
 
-__global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
+__global__ void __launch_bounds__(256) k_ras2d(Ras2dArgs A) {
   extern __shared__ __align__(128) unsigned char smem[];
   long long T0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(T0));
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
       double Yo1[4] = {0, 0, 0, 0}, Yo2[4] = {0, 0, 0, 0};                 // own row at t-1, t-2
       double Ya1[4] = {0, 0, 0, 0}, Ya2[4] = {0, 0, 0, 0}, Ya3[4] = {0, 0, 0, 0};   // row above at t-1..t-3
       int i = tf0 - 2 * j;
-#pragma unroll 6
+#pragma unroll 2
       for (int k = 0; k < nF; ++k, ++i) {
         const int t = tf0 + k;
         const bool active = row_ok && i >= 0 && i < ex;
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(512) k_ras2d(Ras2dArgs A) {
       double Xo1[4] = {0, 0, 0, 0}, Xo2[4] = {0, 0, 0, 0};                 // own row at t+1, t+2 (i+1, i+2)
       double Xb1[4] = {0, 0, 0, 0}, Xb2[4] = {0, 0, 0, 0}, Xb3[4] = {0, 0, 0, 0};   // row below at t+1..t+3 (i-1, i, i+1)
       int i = tf1 - 2 * j;
-#pragma unroll 6
+#pragma unroll 2
       for (int kb = 0; kb < nF; ++kb, --i) {
         const int t = tf1 - kb;
         const bool active = row_ok && i >= 0 && i < ex;
@@ -599,7 +599,7 @@ static bool ras2d_geom(const nks_grid& g, Ras2dGeom& Gm, int cs_try = 0) {
   Gm.CS = CS;
   Gm.Wmax = (Gm.NGmax + CS - 1) / CS;
   Gm.KG = 2 * (kGR - 1) + Gm.exmax;
-  return Gm.Wmax <= 15;
+  return Gm.Wmax <= 7;      // 32 (Wmax + 1) threads <= 256 (launch bound)
 }
 
 // Workspace bytes for the packed chunks + geometry (0 when the pipelined path does not apply).
