@@ -303,3 +303,37 @@ def test_full_size_sampled_residual_and_jv(cfg_id):
         Jg = Jv[(slice(None),) + ctr]
         np.testing.assert_allclose(Fg, Fo, rtol=1e-11, atol=1e-11 * np.abs(F).max(axis=tuple(range(1, d + 1))).max())
         np.testing.assert_allclose(Jg, Jo, rtol=1e-11, atol=1e-11 * np.abs(Jv).max())
+
+
+# ---------------------------------------------------------------------------------------- second workload
+
+@pytest.mark.parametrize("Lscale", [3.0])
+def test_single_particle_workload_parity(Lscale):
+    """the paper's single-particle initial state (a sphere with c = 0.238,
+    eta = 0.01 inside and c = 0.1375, eta = 0.99 outside), here r = 1 on a 3D 10^3 grid, with the
+    paper's elastic multiplier script-L = 3 (the 80^3 run with script-L = 1 is tools/single_particle.py); two adaptive steps, GPU vs
+    oracle.  (script-L = 0 leaves u undetermined -- all u rows vanish -- so it is not a case of the
+    coupled system as formulated here.)"""
+    shape = (10, 10, 10)
+    d = 3
+    model = dict(MODEL)
+    model["Lscale"] = Lscale
+    m = scheme.Model.from_dict(d, 0.25, model)
+    c, eta = ni.sphere_fields(shape, 0.25, 1.0, 0.238, 0.01, 0.1375, 0.99)
+    cbar = c.mean()
+    Xo = np.concatenate([c[None], eta[None], solver.init_displacement(m, c, cbar)])
+    Xo, recs_o = solver.run_adaptive(m, Xo, cbar, SOL, 2)
+    from paper_2209_08001_b200 import Solver
+    g = Solver(shape, model, SOL, h=0.25, nsub=(1, 2, 2), overlap=2)
+    g.set_fields(c, eta, None)
+    recs_g = g.run_adaptive(2)
+    for rg, ro in zip(recs_g, recs_o):
+        assert rg["dt"] == pytest.approx(ro["dt"], rel=1e-9)
+        assert rg["energy"] == pytest.approx(ro["energy"], rel=1e-10)
+    Xg = g.get_state()
+    for f in range(2 + d):
+        nrm = np.linalg.norm(Xo[f])
+        if nrm > 0:
+            assert np.linalg.norm(Xg[f] - Xo[f]) <= 1e-8 * nrm, f
+        else:
+            assert np.abs(Xg[f]).max() == 0.0
