@@ -102,6 +102,10 @@ typedef struct {
   double zeta, dt_min, dt_max, dt_init;
   double dt_floor_factor;            /* abort when the retried dt < dt_min * factor            */
   int32_t xd_norm;                   /* ||X^n - X^{n-1}||: 0 RMS, 1 Euclidean, 2 (c,eta) Eucl. */
+  int32_t factor_fp32;               /* 1: the level-synchronous subdomain solves read fp32 copies */
+                                     /* of the BILU(0) factors (factorisation stays fp64; the    */
+                                     /* preconditioner only changes GMRES's iteration count, not */
+                                     /* the converged step -- SURVEY 8(f)-1).  0: fp64 factors.  */
 } nks_params;
 
 typedef struct {

@@ -59,8 +59,9 @@ void launch_ras2d_pack(void* plan, const double* fac, long long ld, cudaStream_t
 void ras2d_free(void* plan);
 int ras2d_cluster(void* plan);
 cudaError_t launch_ras2d(void* plan, const double* r, double* z, cudaStream_t s);
-void launch_ras_apply(const BoxSet& B, int nf, long long N, const double* fac, const double* r, double* y, double* z,
-                      cudaStream_t s);
+void launch_ras_apply(const BoxSet& B, int nf, long long N, const double* fac, const float* fac32, const double* r,
+                      double* y, double* z, cudaStream_t s);
+void launch_fac_to_fp32(const BoxSet& B, int nf, const double* fac, float* fac32, cudaStream_t s);
 // init_fft.cu
 int init_displacement_fft(const DevParams& P, const double* c, double* u, void* scratch, cudaStream_t s, std::string& err);
 }  // namespace nks
@@ -84,7 +85,7 @@ struct CudaError {
 struct Layout {
   size_t off_X[7];
   size_t off_Ta, off_jac4, off_V, off_Z, off_W2, off_part, off_out;
-  size_t off_fac, off_ybox, off_gidx, off_nbr, off_levoff, off_levptr, off_posoff, off_geo;
+  size_t off_fac, off_fac32, off_ybox, off_gidx, off_nbr, off_levoff, off_levptr, off_posoff, off_geo;
   size_t total;
   long long P, ld;
   size_t geo_bytes;
@@ -149,6 +150,7 @@ Layout make_layout(const nks_grid& g, const nks_params& p) {
     L.nlevptr = (int)nl;
     L.ld = (L.P + 31) / 32 * 32;
     L.off_fac = o; o = align256(o + (size_t)nslots * nf * nf * L.ld * sizeof(double));
+    L.off_fac32 = o; o = align256(o + (p.factor_fp32 ? (size_t)nslots * nf * nf * L.ld * sizeof(float) : 0));
     L.off_ybox = o; o = align256(o + (size_t)nf * L.P * sizeof(double));
     L.off_gidx = o; o = align256(o + (size_t)L.P * sizeof(int));
     L.off_nbr = o; o = align256(o + (size_t)nslots * L.P * sizeof(int));
@@ -291,7 +293,7 @@ void pc_apply(nks_state* st, const double* r, double* z) {
   }
   PhaseScope ps(st, PH_RAS);
   if (st->ras2d) CK(launch_ras2d(st->ras2d, r, z, st->stream));
-  else launch_ras_apply(st->boxes, st->nf, st->N, st->fac, r, st->ybox, z, st->stream);
+  else launch_ras_apply(st->boxes, st->nf, st->N, st->fac, st->fac32, r, st->ybox, z, st->stream);
   st->launches += 1;
 }
 
@@ -308,6 +310,10 @@ void pc_setup(nks_state* st, const double* Xb) {
     st->launches += 1;
     if (st->ras2d) {
       launch_ras2d_pack(st->ras2d, st->fac, st->boxes.ld, st->stream);
+      st->launches += 1;
+    }
+    if (st->fac32 && !st->ras2d) {
+      launch_fac_to_fp32(st->boxes, st->nf, st->fac, st->fac32, st->stream);
       st->launches += 1;
     }
   }
@@ -686,6 +692,7 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
       B.max_level_width = H.max_width;
       if ((long long)H.lev_ptr.size() > L.nlevptr) throw std::runtime_error("level table overflow");
       st->fac = (double*)(w + L.off_fac);
+      st->fac32 = params->factor_fp32 ? (float*)(w + L.off_fac32) : nullptr;
       st->ybox = (double*)(w + L.off_ybox);
       B.gidx = (int*)(w + L.off_gidx);
       B.nbr = (int*)(w + L.off_nbr);

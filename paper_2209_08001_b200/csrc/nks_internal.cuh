@@ -115,6 +115,7 @@ struct nks_state {
   // preconditioner
   nks::BoxSet boxes;
   double* fac = nullptr;    // [nslots][nf][nf][P]
+  float* fac32 = nullptr;   // fp32 copy of fac (factor_fp32), read by the level-synchronous apply
   double* ybox = nullptr;   // [nf][P]
   bool pc_valid = false;
   void* ras2d = nullptr;    // plan of the row-pipelined 2D RAS apply (ras2d.cu), or null

@@ -380,11 +380,11 @@ __global__ void k_bilu0(SlotTables T, const int* __restrict__ nbr, const int* __
 // NL = number of lower (= upper) slots: 6 in 2D, 12 in 3D; the slot loops are unrolled so that every
 // neighbour index and neighbour vector of a point is requested before the first one is used (two
 // dependent memory latencies per wavefront level instead of 2*NL).
-template <int NF, int NL>
+template <int NF, int NL, typename FT>
 __global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const int* __restrict__ nbr,
                             const int* __restrict__ box_lev_off, const int* __restrict__ lev_ptr,
                             const int* __restrict__ box_pos_off, long long Ptot, long long ld, long long N,
-                            const double* __restrict__ fac, const double* __restrict__ r, double* y,
+                            const FT* __restrict__ fac, const double* __restrict__ r, double* y,
                             double* __restrict__ z) {
   const int b = blockIdx.x;
   const int q0 = box_pos_off[b], q1 = box_pos_off[b + 1];
@@ -414,11 +414,12 @@ __global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const in
       for (int f = 0; f < NF; ++f) acc[f] = y[f * Ptot + pos];
 #pragma unroll
       for (int a = 0; a < NL; ++a) {
-        const double* L = fac + (long long)(T.lower[a] * NF * NF) * ld + pos;
+        const FT* L = fac + (long long)(T.lower[a] * NF * NF) * ld + pos;
 #pragma unroll
         for (int rr = 0; rr < NF; ++rr)
 #pragma unroll
-          for (int c = 0; c < NF; ++c) acc[rr] = fma(-__ldg(L + (long long)(rr * NF + c) * ld), yk[a][c], acc[rr]);
+          for (int c = 0; c < NF; ++c)
+            acc[rr] = fma(-(double)__ldg(L + (long long)(rr * NF + c) * ld), yk[a][c], acc[rr]);
       }
 #pragma unroll
       for (int f = 0; f < NF; ++f) y[f * Ptot + pos] = acc[f];
@@ -442,19 +443,20 @@ __global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const in
       for (int f = 0; f < NF; ++f) acc[f] = y[f * Ptot + pos];
 #pragma unroll
       for (int a = 0; a < NL; ++a) {
-        const double* U = fac + (long long)(T.upper[a] * NF * NF) * ld + pos;
+        const FT* U = fac + (long long)(T.upper[a] * NF * NF) * ld + pos;
 #pragma unroll
         for (int rr = 0; rr < NF; ++rr)
 #pragma unroll
-          for (int c = 0; c < NF; ++c) acc[rr] = fma(-__ldg(U + (long long)(rr * NF + c) * ld), xk[a][c], acc[rr]);
+          for (int c = 0; c < NF; ++c)
+            acc[rr] = fma(-(double)__ldg(U + (long long)(rr * NF + c) * ld), xk[a][c], acc[rr]);
       }
-      const double* D = fac + (long long)(T.diag * NF * NF) * ld + pos;
+      const FT* D = fac + (long long)(T.diag * NF * NF) * ld + pos;
       double xo[NF];
 #pragma unroll
       for (int rr = 0; rr < NF; ++rr) {
         double s = 0.0;
 #pragma unroll
-        for (int c = 0; c < NF; ++c) s = fma(__ldg(D + (long long)(rr * NF + c) * ld), acc[c], s);
+        for (int c = 0; c < NF; ++c) s = fma((double)__ldg(D + (long long)(rr * NF + c) * ld), acc[c], s);
         xo[rr] = s;
       }
 #pragma unroll
@@ -498,14 +500,35 @@ void launch_factor(const BoxSet& B, int nf, double* fac, cudaStream_t s) {
   else k_bilu0<5><<<B.nbox, threads, 0, s>>>(T, B.nbr, B.box_lev_off, B.lev_ptr, B.P, B.ld, fac);
 }
 
-void launch_ras_apply(const BoxSet& B, int nf, long long N, const double* fac, const double* r, double* y, double* z,
-                      cudaStream_t s) {
+__global__ void k_to_fp32(long long n, const double* __restrict__ a, float* __restrict__ b) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    b[i] = (float)a[i];
+}
+
+void launch_fac_to_fp32(const BoxSet& B, int nf, const double* fac, float* fac32, cudaStream_t s) {
+  const long long n = (long long)B.nslots * nf * nf * B.ld;
+  k_to_fp32<<<148 * 8, 256, 0, s>>>(n, fac, fac32);
+}
+
+void launch_ras_apply(const BoxSet& B, int nf, long long N, const double* fac, const float* fac32, const double* r,
+                      double* y, double* z, cudaStream_t s) {
   const SlotTables T = make_tables(B, nf);
   const int threads = std::min(256, std::max(32, ((B.max_level_width + 31) / 32) * 32));
-  if (nf == 4)
-    k_ras_apply<4, 6><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, B.ld, N, fac, r, y, z);
-  else
-    k_ras_apply<5, 12><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, B.ld, N, fac, r, y, z);
+  if (nf == 4) {
+    if (fac32)
+      k_ras_apply<4, 6, float><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off,
+                                                          B.P, B.ld, N, fac32, r, y, z);
+    else
+      k_ras_apply<4, 6, double><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off,
+                                                           B.P, B.ld, N, fac, r, y, z);
+  } else {
+    if (fac32)
+      k_ras_apply<5, 12, float><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off,
+                                                           B.P, B.ld, N, fac32, r, y, z);
+    else
+      k_ras_apply<5, 12, double><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr,
+                                                            B.box_pos_off, B.P, B.ld, N, fac, r, y, z);
+  }
 }
 
 }  // namespace nks

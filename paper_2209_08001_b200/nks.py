@@ -40,7 +40,7 @@ class Params(C.Structure):
         ("gmres_maxit", C.c_int32), ("pc_type", C.c_int32), ("pc_reuse", C.c_int32),
         ("ls_alpha", C.c_double), ("ls_max_halvings", C.c_int32),
         ("zeta", C.c_double), ("dt_min", C.c_double), ("dt_max", C.c_double), ("dt_init", C.c_double),
-        ("dt_floor_factor", C.c_double), ("xd_norm", C.c_int32),
+        ("dt_floor_factor", C.c_double), ("xd_norm", C.c_int32), ("factor_fp32", C.c_int32),
     ]
 
 
@@ -143,6 +143,7 @@ def make_params(model: dict, solver: dict, pc_type=PC_RAS_BILU0, pc_reuse=1) -> 
     p.pc_type = int(pc_type)
     p.pc_reuse = int(pc_reuse)
     p.xd_norm = {"rms": 0, "l2": 1, "ceta_l2": 2}[solver.get("xd_norm", "rms")]
+    p.factor_fp32 = int(solver.get("factor_fp32", 0))
     return p
 
 

@@ -60,7 +60,7 @@ int main(void) {
   printf("nks_step_info %zu\n", sizeof(nks_step_info));
   F(nks_grid, h) F(nks_grid, nsub) F(nks_grid, overlap) F(nks_grid, zghost)
   F(nks_params, S) F(nks_params, newton_rtol) F(nks_params, pc_reuse) F(nks_params, ls_alpha)
-  F(nks_params, zeta) F(nks_params, xd_norm)
+  F(nks_params, zeta) F(nks_params, xd_norm) F(nks_params, factor_fp32)
   F(nks_step_info, dt) F(nks_step_info, energy_parts) F(nks_step_info, mass) F(nks_step_info, xd)
   return 0;
 }

@@ -166,14 +166,14 @@ def test_gmres_solves_the_newton_system(shape, nsub):
 
 # ---------------------------------------------------------------------------------------- time steps
 
-def _run_parity(shape, dts, nsub, delta, seed=0, pc_type=2):
+def _run_parity(shape, dts, nsub, delta, seed=0, pc_type=2, fp32=False):
     d = len(shape)
     m = oracle_model(d)
     c, eta = ni.initial_fields(shape, seed)
     cbar = c.mean()
     u0 = solver.init_displacement(m, c, cbar)
     Xo = np.concatenate([c[None], eta[None], u0])
-    g = gpu_solver(shape, nsub=nsub, overlap=delta, pc_type=pc_type)
+    g = gpu_solver(shape, nsub=nsub, overlap=delta, pc_type=pc_type, sol={"factor_fp32": int(fp32)})
     g.set_fields(c, eta, None)          # the library solves its own u^0 (FFT)
     mass0 = scheme.mass(m, Xo)
     out = []
@@ -337,3 +337,22 @@ def test_single_particle_workload_parity(Lscale):
             assert np.linalg.norm(Xg[f] - Xo[f]) <= 1e-8 * nrm, f
         else:
             assert np.abs(Xg[f]).max() == 0.0
+
+
+def test_fp32_factors_change_iterations_not_the_step():
+    """factor_fp32: the level-synchronous subdomain solves read fp32 copies of the
+    BILU(0) factors.  The preconditioner only steers GMRES, so the accepted step still matches the
+    oracle at BASELINE's bar, and the apply itself stays within fp32 rounding of the fp64 apply."""
+    shape = (10, 12, 12)
+    out = _run_parity(shape, [0.01, 0.3], (1, 2, 2), 2, fp32=True)
+    assert len(out) == 2
+    Xa, Xb = states(shape)
+    r = ni.random_direction(5, shape, 11)
+    z = []
+    for f32 in (0, 1):
+        g = gpu_solver(shape, nsub=(1, 2, 2), overlap=2, sol={"factor_fp32": f32})
+        g.set_fields(Xa[0], Xa[1], Xa[2:])
+        g.pc_setup(Xb, 0.3)
+        z.append(g.pc_apply(r).cpu().numpy())
+    rel = np.abs(z[1] - z[0]).max() / np.abs(z[0]).max()
+    assert 0 < rel < 1e-4, rel

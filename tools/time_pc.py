@@ -10,7 +10,9 @@ if "SHAPE" in os.environ:
     cfg["shape"] = tuple(int(v) for v in os.environ["SHAPE"].split(","))
     cfg["nsub"] = tuple(int(v) for v in os.environ["NSUB"].split(","))
 shape = cfg["shape"]; d = len(shape); nf = 2 + d
-g = Solver(shape, ni.model_default(), ni.solver_default(), nsub=cfg["nsub"], overlap=cfg["overlap"])
+sol = ni.solver_default()
+sol["factor_fp32"] = int(os.environ.get("FP32", "0"))
+g = Solver(shape, ni.model_default(), sol, nsub=cfg["nsub"], overlap=cfg["overlap"])
 c, eta = ni.initial_fields(shape, 0)
 g.set_fields(c, eta, None)
 X = g.get_state()
@@ -23,4 +25,5 @@ for _ in range(20):
     g.pc_apply(r)
 ph = g.phase_times(reset=True)
 print("ras_apply ms/launch", ph["ras_apply"]["ms"] / ph["ras_apply"]["count"])
-np.save(os.environ.get("OUT", "gpurun_out/z.npy"), z.cpu().numpy())
+if "OUT" in os.environ:
+    np.save(os.environ["OUT"], z.cpu().numpy())
