@@ -66,12 +66,24 @@ typedef struct {
   double h;          /* uniform mesh size (0.25)                                         */
   int32_t nsub[3];   /* RAS subdomain boxes per axis (1 <= nsub[j] <= n[j]); nsub[2]=1 in 2D     */
   int32_t overlap;   /* delta: cells added on each side of every box (0..8)      */
-  int32_t zghost;    /* 0: periodic grid.  2: this state is one z-slab of a z-sharded 3D grid --  */
-                     /* n[2] counts 2 ghost planes per side that the caller fills (halo exchange, */
-                     /* paper_2209_08001_b200/shard.py); F and J.v are evaluated on the own       */
-                     /* planes only, with no z wrap.  Slab states serve nks_eval_residual /       */
-                     /* nks_eval_jv; pc_type must be NKS_PC_NONE.        */
+  int32_t zghost;    /* 0: periodic grid.  2..8: this state is one z-slab of a z-sharded 3D grid  */
+                     /* (SURVEY 8(e)): n[2] counts zghost ghost planes on each side, filled by the  */
+                     /* halo callback of nks_set_comm (or by the caller for the eval hooks); F,    */
+                     /* J.v, energy and the gauge sums cover the own planes only, with no z wrap.  */
+                     /* With pc_type RAS the nsub[2] boxes split the OWN planes (the caller aligns */
+                     /* slabs with the global box grid) and zghost >= overlap + 1.                 */
 } nks_grid;
+
+/* ---- communication callbacks of a z-sharded state --------------------------------
+ * Both are called from inside the library's calls, on the calling thread, with the state's stream;
+ * the callback must leave its result ordered on that stream (e.g. an NCCL collective enqueued on
+ * it, or a host-staged exchange followed by a copy on it).  Return 0 on success; any other value
+ * makes the library call fail with NKS_E_NCCL. */
+/* Sum n doubles at device pointer buf over all ranks, in place; every rank must get identical bits. */
+typedef int32_t (*nks_allreduce_fn)(void* user, double* buf, int64_t n, void* cuda_stream);
+/* Fill the zghost ghost planes on both z sides of nfields fields (field f at vec + f*field_stride,
+ * each a local (n[2], n[1], n[0]) C-order array) from the periodic z neighbours' own planes. */
+typedef int32_t (*nks_halo_fn)(void* user, double* vec, int32_t nfields, int64_t field_stride, void* cuda_stream);
 
 typedef struct {
   /* ---- model, dimensionless (App. A/B).  CALPHAD-style coefficients in units of
@@ -158,6 +170,17 @@ NKS_API nks_status nks_set_state(nks_state* st, const double* c, const double* e
 /* Set cbar0, the mean composition of the eigenstrain, explicitly -- used by z-slab states,
  * whose local mean is not the grid's.  Recomputes T^n. */
 NKS_API nks_status nks_set_cbar0(nks_state* st, double cbar0);
+
+/* Attach a z-sharded state (grid.zghost > 0) to its process group: this rank owns global planes
+ * [z_offset, z_offset + n[2] - 2*zghost) of an nz_global-plane periodic grid.  allreduce may be NULL
+ * only when nranks == 1; halo must not be NULL.  Call before nks_set_fields; required by
+ * nks_set_fields / nks_set_state / nks_step / nks_run_adaptive / nks_energy on slab states
+ * (NKS_E_STATE otherwise).  Every rank must make the same sequence of calls: all control decisions
+ * (Newton and GMRES convergence, line search, dt) are taken from allreduced values.  On a slab state
+ * nks_set_fields takes local arrays including ghost planes (ghost values are ignored) and needs u
+ * (the FFT initial displacement is a single-grid operation); cbar0 is the global mean of c. */
+NKS_API nks_status nks_set_comm(nks_state* st, int32_t rank, int32_t nranks, int32_t z_offset, int32_t nz_global,
+                                nks_allreduce_fn allreduce, nks_halo_fn halo, void* user);
 
 /* Copy X^n out (same layout as nks_set_fields; u must hold d*N doubles). */
 NKS_API nks_status nks_get_fields(const nks_state* st, double* c, double* eta, double* u, int32_t on_device);

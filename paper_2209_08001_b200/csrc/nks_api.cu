@@ -31,6 +31,9 @@ void launch_jv_tiled(const DevParams& P, const double* Xa, const double* jac4, c
 void launch_norm_admissible(long long N, int nf, const double* F, const double* X, double* part, double* out, cudaStream_t s);
 void launch_energy(const DevParams& P, const double* X, double* part, double* out, cudaStream_t s);
 void launch_gauge(const DevParams& P, double* X, double* part, double* out, cudaStream_t s);
+int launch_gauge_sums(const DevParams& P, const double* X, double* part, double* out, cudaStream_t s);
+void launch_gauge_apply(const DevParams& P, double* X, const double* out, cudaStream_t s);
+void launch_zero_ghosts(const DevParams& P, int nf, double* v, cudaStream_t s);
 // krylov.cu
 void launch_mdot(long long n, int nk, const double* V, long long ld, const double* w, double* part, double* out, cudaStream_t s);
 void launch_update_dot(long long n, int nk, const double* V, long long ld, const double* h, double* w, double* part,
@@ -72,6 +75,8 @@ namespace {
 
 enum Phase { PH_F = 0, PH_JV = 1, PH_RAS = 2, PH_ASM = 3, PH_FACT = 4, PH_VEC = 5, PH_RED = 6, PH_OTHER = 7 };
 
+struct CommError {};   // a communication callback returned non-zero
+
 struct CudaError {
   cudaError_t e;
 };
@@ -105,9 +110,15 @@ const char* validate(const nks_grid* g, const nks_params* p) {
   if (p->gmres_restart < 1 || p->gmres_restart > 60) return "gmres_restart must be in 1..60";
   if (p->newton_maxit < 0 || p->gmres_maxit < 1) return "bad iteration limits";
   if (p->pc_type != NKS_PC_NONE && p->pc_type != NKS_PC_RAS_BILU0) return "unknown pc_type";
-  if (g->zghost != 0 && g->zghost != 2) return "zghost must be 0 or 2";
-  if (g->zghost == 2 && (g->dim != 3 || g->n[2] < 5 || p->pc_type != NKS_PC_NONE))
-    return "z-slab states (zghost = 2) are 3D, need n[2] >= 5 and pc_type NONE";
+  if (g->zghost != 0 && (g->zghost < 2 || g->zghost > 8)) return "zghost must be 0 or 2..8";
+  if (g->zghost > 0) {
+    if (g->dim != 3) return "z-slab states (zghost > 0) are 3D";
+    if (g->n[2] - 2 * g->zghost < 2) return "a z-slab must own at least 2 planes";
+    if (p->pc_type == NKS_PC_RAS_BILU0 && g->overlap + 1 > g->zghost)
+      return "z-slab with RAS needs zghost >= overlap + 1 (assembly reads one cell beyond the box)";
+    if (p->pc_type == NKS_PC_RAS_BILU0 && (g->nsub[2] < 1 || g->nsub[2] > g->n[2] - 2 * g->zghost))
+      return "z-slab: nsub[2] must be in 1..own planes";
+  }
   if (p->pc_type == NKS_PC_RAS_BILU0) {
     for (int j = 0; j < 3; ++j)
       if (g->nsub[j] < 1 || g->nsub[j] > g->n[j]) return "nsub[j] must be in 1..n[j]";
@@ -251,6 +262,35 @@ void sync(nks_state* st) {
   st->syncs++;
 }
 
+// ---- z-slab communication ------------------------------------------------------------------------
+bool slab(const nks_state* st) { return st->grid.zghost > 0; }
+
+// Points of the whole (global) grid: own planes of every rank.
+long long global_points(const nks_state* st) {
+  if (!slab(st)) return st->N;
+  const long long nxy = (long long)st->grid.n[0] * st->grid.n[1];
+  return st->dp.nzg > 0 ? nxy * st->dp.nzg : nxy * (st->grid.n[2] - 2 * st->grid.zghost);
+}
+
+void comm_allreduce(nks_state* st, double* buf, long long n) {
+  if (!st->comm_set || st->nranks == 1) return;
+  if (st->comm_allreduce(st->comm_user, buf, n, (void*)st->stream) != 0) throw CommError();
+}
+
+// Fill the ghost planes of the nf fields of vec (no-op on periodic states).
+void halo(nks_state* st, double* vec, int nf) {
+  if (!slab(st) || !st->comm_set) return;
+  PhaseScope ps(st, PH_OTHER);   // halo exchanges are accounted under "other"
+  if (st->comm_halo(st->comm_user, vec, nf, st->N, (void*)st->stream) != 0) throw CommError();
+}
+
+// Zero the ghost planes of a Krylov-space vector: vectors that enter dot products keep zero ghosts.
+void clean(nks_state* st, double* vec, int nf) {
+  if (!slab(st)) return;
+  launch_zero_ghosts(st->dp, nf, vec, st->stream);
+  st->launches += 1;
+}
+
 void residual(nks_state* st, const double* Xb, double* F) {
   PhaseScope ps(st, PH_F);
   static const bool old_f = std::getenv("NKS_F_OLD") != nullptr;
@@ -266,6 +306,7 @@ void norm_adm(nks_state* st, const double* F, const double* X, double& nrm, doub
     launch_norm_admissible(st->N, st->nf, F, X, st->red_part, st->red_out, st->stream);
     st->launches += 2;
   }
+  comm_allreduce(st, st->red_out, 2);
   CK(cudaMemcpyAsync(st->h_red, st->red_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
   sync(st);
   nrm = std::sqrt(st->h_red[0]);
@@ -274,7 +315,9 @@ void norm_adm(nks_state* st, const double* F, const double* X, double& nrm, doub
 
 void gauge(nks_state* st, double* X) {
   PhaseScope ps(st, PH_RED);
-  launch_gauge(st->dp, X, st->red_part, st->red_out + 128, st->stream);
+  const int nsum = launch_gauge_sums(st->dp, X, st->red_part, st->red_out + 128, st->stream);
+  comm_allreduce(st, st->red_out + 128, nsum);     // global sub-lattice sums (slab: own planes of every rank)
+  launch_gauge_apply(st->dp, X, st->red_out + 128, st->stream);
   st->launches += 3;
 }
 
@@ -358,19 +401,26 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
     auto launch_iter = [&](int jj) {
       double* vj = V + (long long)jj * n;
       double* w = V + (long long)(jj + 1) * n;
+      if (st->prm.pc_type != NKS_PC_NONE) halo(st, vj, st->nf);   // RAS reads delta ghost planes of its input
       pc_apply(st, vj, st->Z);
+      if (st->prm.pc_type != NKS_PC_NONE) clean(st, vj, st->nf);
+      halo(st, st->Z, st->nf);
       jv(st, st->Z, w);
       {
         PhaseScope ps(st, PH_VEC);
+        // slab states: one allreduce after each CGS pass (jj+1 projections, then jj+1 corrections + |w|^2)
         if (jj + 2 <= 32) {      // register-resident CGS2 passes with last-block reductions
           launch_cgs_dot(n, jj + 1, V, n, w, st->red_part, st->red_out, st->red_cnt, st->stream);
+          comm_allreduce(st, st->red_out, jj + 1);
           launch_cgs_update_dot(n, jj + 1, V, n, st->red_out, w, st->red_part, st->red_out + 64, st->red_cnt, st->stream);
           st->launches += 2;
         } else {
           launch_mdot(n, jj + 1, V, n, w, st->red_part, st->red_out, st->stream);
+          comm_allreduce(st, st->red_out, jj + 1);
           launch_update_dot(n, jj + 1, V, n, st->red_out, w, st->red_part, st->red_out + 64, st->stream);
           st->launches += 4;
         }
+        comm_allreduce(st, st->red_out + 64, jj + 2);
         launch_update_scale_dev(n, jj + 1, V, n, st->red_out + 64, w, st->stream);
         st->launches += 1;
       }
@@ -427,7 +477,9 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
       launch_lincomb(n, j, V, n, y.data(), st->W2, st->stream);
       st->launches += 1;
     }
+    if (st->prm.pc_type != NKS_PC_NONE) halo(st, st->W2, st->nf);
     pc_apply(st, st->W2, st->Z);
+    clean(st, st->W2, st->nf);          // W2 receives J s below and must keep zero ghosts
     {
       PhaseScope ps(st, PH_VEC);
       launch_axpby(n, 1.0, st->Z, 1.0, s, st->stream);
@@ -438,6 +490,7 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
     if (its >= st->prm.gmres_maxit) return 1;
     (void)done;
     // restart: r = b - J s  -> V[0]
+    halo(st, s, st->nf);
     jv(st, s, st->W2);
     {
       PhaseScope ps(st, PH_VEC);
@@ -449,6 +502,7 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
       launch_norm_admissible(n / st->nf, st->nf, V, nullptr, st->red_part, st->red_out, st->stream);
       st->launches += 2;
     }
+    comm_allreduce(st, st->red_out, 1);
     CK(cudaMemcpyAsync(st->h_red, st->red_out, sizeof(double), cudaMemcpyDeviceToHost, st->stream));
     sync(st);
     {
@@ -469,6 +523,7 @@ void energy(nks_state* st, const double* X, double parts[4], double& mass) {
     launch_energy(st->dp, X, st->red_part, st->red_out, st->stream);
     st->launches += 2;
   }
+  comm_allreduce(st, st->red_out, 5);
   CK(cudaMemcpyAsync(st->h_red, st->red_out, 5 * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
   sync(st);
   const double vol = std::pow(st->grid.h, st->d);
@@ -537,6 +592,7 @@ nks_status step_impl(nks_state* st, double dt, nks_step_info* info) {
     // sub-lattice-mean projection as the gauge) keeps GMRES from chasing an unreachable residual;
     // the oracle's pinned-row direct solve drops the same component.
     gauge(st, st->Ft);
+    clean(st, st->Ft, st->nf);
     int gits = 0;
     const double tol = std::max(p.gmres_rtol * f, p.gmres_atol);
     const int grc = gmres(st, st->Ft, f, st->S, tol, gits);
@@ -557,6 +613,7 @@ nks_status step_impl(nks_state* st, double dt, nks_step_info* info) {
         launch_xpay(st->nvec, st->Xb, lam, st->S, st->Xt, st->stream);
         st->launches += 1;
       }
+      halo(st, st->Xt, st->nf);
       residual(st, st->Xt, st->Ft);
       norm_adm(st, st->Ft, st->Xt, ft, bad);
       if (bad == 0 && std::isfinite(ft) && ft <= (1.0 - p.ls_alpha * lam) * f) {
@@ -604,15 +661,17 @@ double change_rate(nks_state* st) {
     launch_xpay(n, st->Xn, -1.0, st->Xprev, st->W2, st->stream);
     st->launches += 1;
   }
+  clean(st, st->W2, (int)(n / st->N));
   {
     PhaseScope ps(st, PH_RED);
     launch_norm_admissible(n, 1, st->W2, nullptr, st->red_part, st->red_out, st->stream);
     st->launches += 2;
   }
+  comm_allreduce(st, st->red_out, 1);
   CK(cudaMemcpyAsync(st->h_red, st->red_out, sizeof(double), cudaMemcpyDeviceToHost, st->stream));
   sync(st);
   double nrm = std::sqrt(st->h_red[0]);
-  if (p.xd_norm == 0) nrm /= std::sqrt((double)st->nvec);
+  if (p.xd_norm == 0) nrm /= std::sqrt((double)global_points(st) * st->nf);
   return nrm / st->dt_prev;
 }
 
@@ -623,6 +682,9 @@ nks_status guarded(nks_state* st, F&& fn) {
   } catch (const CudaError& e) {
     if (st) st->err = std::string("CUDA error: ") + cudaGetErrorString(e.e);
     return NKS_E_CUDA;
+  } catch (const CommError&) {
+    if (st) st->err = "communication callback failed";
+    return NKS_E_NCCL;
   } catch (const std::exception& e) {
     if (st) st->err = e.what();
     return NKS_E_CUDA;
@@ -678,6 +740,7 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
     st->red_out = (double*)(w + L.off_out);
     st->red_cnt = (unsigned*)(st->red_out + 255);
     CK(cudaMemsetAsync(st->red_cnt, 0, sizeof(unsigned), st->stream));
+    if (grid->zghost > 0) CK(cudaMemsetAsync(w, 0, L.off_part, st->stream));   // zero ghosts of every vector
     CK(cudaMallocHost(&st->h_red, 256 * sizeof(double)));
     CK(cudaMallocHost(&st->h_ring, 4 * 128 * sizeof(double)));
     for (int k = 0; k < 4; ++k) CK(cudaEventCreateWithFlags(&st->gm_ev[k], cudaEventDisableTiming));
@@ -733,21 +796,24 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
 
 nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, const double* u, int32_t on_device) {
   if (!st || !c || !eta) return NKS_E_INVALID;
+  if (slab(st) && !u) return NKS_E_INVALID;     // the FFT u^0 is a whole-grid operation
   return guarded(st, [&]() -> nks_status {
     const long long N = st->N;
     CK(cudaMemcpyAsync(st->Xn, c, N * sizeof(double), kind_in(on_device), st->stream));
     CK(cudaMemcpyAsync(st->Xn + N, eta, N * sizeof(double), kind_in(on_device), st->stream));
-    // cbar0 = mean(c): the energy kernel's 5th sum is sum c
+    if (u) CK(cudaMemcpyAsync(st->Xn + 2 * N, u, st->d * N * sizeof(double), kind_in(on_device), st->stream));
+    halo(st, st->Xn, st->nf);
+    // cbar0 = mean(c): the energy kernel's 5th sum is sum c (own planes; allreduced on slabs)
     {
       PhaseScope ps(st, PH_RED);
       launch_energy(st->dp, st->Xn, st->red_part, st->red_out, st->stream);  // u garbage only affects E3 here
       st->launches += 2;
     }
+    comm_allreduce(st, st->red_out, 5);
     CK(cudaMemcpyAsync(st->h_red, st->red_out, 5 * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
     sync(st);
-    st->dp.cbar0 = st->h_red[4] / (double)N;
+    st->dp.cbar0 = st->h_red[4] / (double)global_points(st);
     if (u) {
-      CK(cudaMemcpyAsync(st->Xn + 2 * N, u, st->d * N * sizeof(double), kind_in(on_device), st->stream));
     } else {
       std::string e;
       if (init_displacement_fft(st->dp, st->Xn, st->Xn + 2 * N, st->V, st->stream, e) != 0) {
@@ -774,6 +840,25 @@ nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, con
   });
 }
 
+nks_status nks_set_comm(nks_state* st, int32_t rank, int32_t nranks, int32_t z_offset, int32_t nz_global,
+                        nks_allreduce_fn allreduce, nks_halo_fn halo_fn, void* user) {
+  if (!st || !slab(st) || nranks < 1 || rank < 0 || rank >= nranks || !halo_fn) return NKS_E_INVALID;
+  if (nranks > 1 && !allreduce) return NKS_E_INVALID;
+  const int own = st->grid.n[2] - 2 * st->grid.zghost;
+  if (z_offset < 0 || nz_global < own || z_offset + own > nz_global) return NKS_E_INVALID;
+  if (nz_global < 5) return NKS_E_INVALID;
+  st->rank = rank;
+  st->nranks = nranks;
+  st->comm_allreduce = allreduce;
+  st->comm_halo = halo_fn;
+  st->comm_user = user;
+  st->comm_set = true;
+  st->dp.zoff = z_offset;
+  st->dp.nzg = nz_global;
+  st->pc_valid = false;
+  return NKS_OK;
+}
+
 nks_status nks_set_cbar0(nks_state* st, double cbar0) {
   if (!st) return NKS_E_INVALID;
   if (!st->have_fields) return NKS_E_STATE;
@@ -788,11 +873,13 @@ nks_status nks_set_cbar0(nks_state* st, double cbar0) {
 nks_status nks_set_state(nks_state* st, const double* c, const double* eta, const double* u, int32_t on_device) {
   if (!st || !c || !eta || !u) return NKS_E_INVALID;
   if (!st->have_fields) return NKS_E_STATE;
+  if (slab(st) && !st->comm_set) return NKS_E_STATE;
   return guarded(st, [&]() -> nks_status {
     const long long N = st->N;
     CK(cudaMemcpyAsync(st->Xn, c, N * sizeof(double), kind_in(on_device), st->stream));
     CK(cudaMemcpyAsync(st->Xn + N, eta, N * sizeof(double), kind_in(on_device), st->stream));
     CK(cudaMemcpyAsync(st->Xn + 2 * N, u, st->d * N * sizeof(double), kind_in(on_device), st->stream));
+    halo(st, st->Xn, st->nf);
     gauge(st, st->Xn);
     level_prep(st);
     double nrm, bad;
@@ -824,12 +911,14 @@ nks_status nks_get_fields(const nks_state* cst, double* c, double* eta, double* 
 nks_status nks_step(nks_state* st, double dt, nks_step_info* info) {
   if (!st) return NKS_E_INVALID;
   if (!st->have_fields) return NKS_E_STATE;
+  if (slab(st) && !st->comm_set) return NKS_E_STATE;
   return guarded(st, [&]() { return step_impl(st, dt, info); });
 }
 
 nks_status nks_run_adaptive(nks_state* st, int32_t max_steps, double t_end, nks_step_info* per_step, int32_t* done) {
   if (!st || max_steps < 0) return NKS_E_INVALID;
   if (!st->have_fields) return NKS_E_STATE;
+  if (slab(st) && !st->comm_set) return NKS_E_STATE;
   if (done) *done = 0;
   return guarded(st, [&]() -> nks_status {
     const nks_params& p = st->prm;
@@ -871,6 +960,7 @@ nks_status nks_run_adaptive(nks_state* st, int32_t max_steps, double t_end, nks_
 nks_status nks_energy(nks_state* st, double parts[4], double* mass) {
   if (!st || !parts || !mass) return NKS_E_INVALID;
   if (!st->have_fields) return NKS_E_STATE;
+  if (slab(st) && !st->comm_set) return NKS_E_STATE;
   return guarded(st, [&]() -> nks_status {
     energy(st, st->Xn, parts, *mass);
     return NKS_OK;

@@ -21,7 +21,9 @@ constexpr int kRedThreads = 256;
 // Parameters passed by value to every kernel (fp64 model constants derived on the host).
 struct DevParams {
   int dim, nx, ny, nz;
-  int zg;               // z ghost planes per side (0: periodic in z; 2: slab of a z-sharded grid, no z wrap)
+  int zg;               // z ghost planes per side (0: periodic in z; >= 2: slab of a z-sharded grid, no z wrap)
+  int zoff;             // slab: global z of the first own plane (parity classes of the gauge)
+  int nzg;              // slab: global number of planes (0 when not a slab)
   long long N;          // points
   double h, inv_h2, inv_2h, inv_4h2;
   double dt, inv_dt;
@@ -127,6 +129,12 @@ struct nks_state {
   bool have_fields = false;
   bool have_prev = false;
   bool debug = false;          // NKS_DEBUG set: per-cycle GMRES trace on stderr
+  // z-slab communication (nks_set_comm): null callbacks = not attached
+  int rank = 0, nranks = 1;
+  nks_allreduce_fn comm_allreduce = nullptr;
+  nks_halo_fn comm_halo = nullptr;
+  void* comm_user = nullptr;
+  bool comm_set = false;
   // counters
   long long launches = 0;
   long long syncs = 0;

@@ -71,10 +71,24 @@ static void split_axis(int n, int nsub, std::vector<int>& start, std::vector<int
   }
 }
 
+// Box extents per axis.  A z-slab state (zghost > 0) splits only its own planes along z, and its
+// boxes address the local array directly: the overlap planes are ghost planes, which hold the
+// periodic neighbours' values, so no z wrap is needed (RAS needs one width-delta halo
+// of its input, assembly one of width delta+1).
+static void split_boxes(const nks_grid& g, std::vector<int> (&st)[3], std::vector<int> (&ln)[3]) {
+  for (int j = 0; j < 2; ++j) split_axis(g.n[j], g.nsub[j], st[j], ln[j]);
+  if (g.zghost > 0) {
+    split_axis(g.n[2] - 2 * g.zghost, g.nsub[2], st[2], ln[2]);
+    for (auto& v : st[2]) v += g.zghost;
+  } else {
+    split_axis(g.n[2], g.nsub[2], st[2], ln[2]);
+  }
+}
+
 long long box_positions(const nks_grid& g) {
   std::vector<int> st[3], ln[3];
   long long P = 0;
-  for (int j = 0; j < 3; ++j) split_axis(g.n[j], g.nsub[j], st[j], ln[j]);
+  split_boxes(g, st, ln);
   const int dz = g.dim == 3 ? g.overlap : 0;
   for (int bz = 0; bz < g.nsub[2]; ++bz)
     for (int by = 0; by < g.nsub[1]; ++by)
@@ -86,7 +100,7 @@ long long box_positions(const nks_grid& g) {
 HostBoxes build_boxes_host(const nks_grid& g, const BoxSet& B) {
   HostBoxes H;
   std::vector<int> st[3], ln[3];
-  for (int j = 0; j < 3; ++j) split_axis(g.n[j], g.nsub[j], st[j], ln[j]);
+  split_boxes(g, st, ln);
   const int delta = g.overlap;
   const int dz = g.dim == 3 ? delta : 0;
   H.P = box_positions(g);

@@ -361,6 +361,7 @@ __global__ void k_energy(DevParams P, const double* __restrict__ X, double* __re
     const int x = (int)(i % P.nx);
     const int y = (int)((i / P.nx) % P.ny);
     const int z = (int)(i / ((long long)P.nx * P.ny));
+    if (z < P.zg || z >= P.nz - P.zg) continue;       // slab: own planes only
     const double c = c_[i], eta = e_[i];
     double e1, e2;
     local_energy(P, c, eta, e1, e2);
@@ -414,8 +415,9 @@ __global__ void k_gauge_sums(DevParams P, const double* __restrict__ X, int even
     const int x = (int)(i % P.nx);
     const int y = (int)((i / P.nx) % P.ny);
     const int z = (int)(i / ((long long)P.nx * P.ny));
+    if (z < P.zg || z >= P.nz - P.zg) continue;       // slab: own planes only
     int cls = 0, bit = 0;
-    const int co[3] = {x, y, z};
+    const int co[3] = {x, y, z - P.zg + P.zoff};        // global coordinates (parity classes)
 #pragma unroll
     for (int j = 0; j < DIM; ++j)
       if (evenmask & (1 << j)) { cls |= (co[j] & 1) << bit; ++bit; }
@@ -442,7 +444,7 @@ __global__ void k_gauge_apply(DevParams P, double* __restrict__ X, int evenmask,
     const int y = (int)((i / P.nx) % P.ny);
     const int z = (int)(i / ((long long)P.nx * P.ny));
     int cls = 0, bit = 0;
-    const int co[3] = {x, y, z};
+    const int co[3] = {x, y, z - P.zg + P.zoff};        // ghost planes get their (global) class too
 #pragma unroll
     for (int j = 0; j < DIM; ++j)
       if (evenmask & (1 << j)) { cls |= (co[j] & 1) << bit; ++bit; }
@@ -501,26 +503,61 @@ void launch_energy(const DevParams& P, const double* X, double* part, double* ou
 int gauge_classes(const DevParams& P, int& evenmask) {
   evenmask = 0;
   int nbits = 0;
-  const int n[3] = {P.nx, P.ny, P.nz};
+  const int n[3] = {P.nx, P.ny, P.nzg > 0 ? P.nzg : P.nz};
   for (int j = 0; j < P.dim; ++j)
     if (n[j] % 2 == 0) { evenmask |= 1 << j; ++nbits; }
   return 1 << nbits;
 }
 
-void launch_gauge(const DevParams& P, double* X, double* part, double* out, cudaStream_t s) {
+// Gauge in two halves so that a sharded state can allreduce the class sums in between.
+int launch_gauge_sums(const DevParams& P, const double* X, double* part, double* out, cudaStream_t s) {
   int evenmask;
   const int ncls = gauge_classes(P, evenmask);
-  const double inv_count = (double)ncls / (double)P.N;
-  const int blocks = (int)std::min<long long>((P.N + 255) / 256, 148 * 16);
   if (P.dim == 2) {
     k_gauge_sums<2><<<kRedBlocks, kRedThreads, 0, s>>>(P, X, evenmask, part);
     k_reduce_final<<<1, kRedThreads, 0, s>>>(part, kRedBlocks, 2 * 4, out);
-    k_gauge_apply<2><<<blocks, 256, 0, s>>>(P, X, evenmask, out, inv_count);
   } else {
     k_gauge_sums<3><<<kRedBlocks, kRedThreads, 0, s>>>(P, X, evenmask, part);
     k_reduce_final<<<1, kRedThreads, 0, s>>>(part, kRedBlocks, 3 * 8, out);
-    k_gauge_apply<3><<<blocks, 256, 0, s>>>(P, X, evenmask, out, inv_count);
   }
+  return P.dim * (P.dim == 2 ? 4 : 8);   // number of sums (component x class slots)
+  (void)ncls;
+}
+
+void launch_gauge_apply(const DevParams& P, double* X, const double* out, cudaStream_t s) {
+  int evenmask;
+  const int ncls = gauge_classes(P, evenmask);
+  const long long nown = P.N / P.nz * (P.nz - 2 * P.zg);
+  const long long nglob = P.nzg > 0 ? nown / (P.nz - 2 * P.zg) * P.nzg : P.N;
+  const double inv_count = (double)ncls / (double)nglob;
+  const int blocks = (int)std::min<long long>((P.N + 255) / 256, 148 * 16);
+  if (P.dim == 2) k_gauge_apply<2><<<blocks, 256, 0, s>>>(P, X, evenmask, out, inv_count);
+  else k_gauge_apply<3><<<blocks, 256, 0, s>>>(P, X, evenmask, out, inv_count);
+}
+
+void launch_gauge(const DevParams& P, double* X, double* part, double* out, cudaStream_t s) {
+  launch_gauge_sums(P, X, part, out, s);
+  launch_gauge_apply(P, X, out, s);
+}
+
+// Zero the ghost planes of nf fields (slab states): vectors that enter dot products keep zero ghosts.
+__global__ void k_zero_ghosts(long long nxy, int nz, int zg, int nf, long long N, double* __restrict__ v) {
+  const long long per = 2LL * zg * nxy;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < per * nf; t += (long long)gridDim.x * blockDim.x) {
+    const int f = (int)(t / per);
+    const long long r = t % per;
+    const long long plane = r / nxy, off = r % nxy;
+    const long long z = plane < zg ? plane : (nz - 2 * zg + plane);
+    v[f * N + z * nxy + off] = 0.0;
+  }
+}
+
+void launch_zero_ghosts(const DevParams& P, int nf, double* v, cudaStream_t s) {
+  if (P.zg <= 0) return;
+  const long long nxy = (long long)P.nx * P.ny;
+  const long long work = 2LL * P.zg * nxy * nf;
+  const int blocks = (int)std::min<long long>((work + 255) / 256, 148 * 8);
+  k_zero_ghosts<<<blocks, 256, 0, s>>>(nxy, P.nz, P.zg, nf, P.N, v);
 }
 
 }  // namespace nks

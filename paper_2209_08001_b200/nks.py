@@ -62,6 +62,9 @@ class StepInfo(C.Structure):
 
 _P = C.c_void_p
 _D = C.POINTER(C.c_double)
+# communication callbacks of a z-sharded state (nks.h: nks_allreduce_fn, nks_halo_fn)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+HALO_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_void_p)
 _SIGS = {
     "nks_workspace_bytes": (C.c_size_t, [C.POINTER(Grid), C.POINTER(Params)]),
     "nks_create": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), _P, C.c_size_t, _P, C.POINTER(_P)]),
@@ -69,6 +72,7 @@ _SIGS = {
     "nks_get_fields": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
     "nks_set_state": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
     "nks_set_cbar0": (C.c_int, [_P, C.c_double]),
+    "nks_set_comm": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, ALLREDUCE_FN, HALO_FN, _P]),
     "nks_step": (C.c_int, [_P, C.c_double, C.POINTER(StepInfo)]),
     "nks_run_adaptive": (C.c_int, [_P, C.c_int32, C.c_double, C.POINTER(StepInfo), C.POINTER(C.c_int32)]),
     "nks_energy": (C.c_int, [_P, _D, _D]),
@@ -181,7 +185,8 @@ class Solver:
     # ---------------------------------------------------------------- helpers
     def _check(self, rc, what):
         if rc != NKS_OK:
-            raise NKSError(rc, f"{what}: {self.lib.nks_last_error(self.st).decode()}")
+            extra = f" ({self.comm_error!r})" if getattr(self, "comm_error", None) is not None else ""
+            raise NKSError(rc, f"{what}: {self.lib.nks_last_error(self.st).decode()}{extra}")
 
     def _dev(self, a, n):
         """Device fp64 contiguous tensor for an array-like (numpy or torch)."""
@@ -225,6 +230,36 @@ class Solver:
         rc = self.lib.nks_set_state(self.st, C.c_void_p(tc.data_ptr()), C.c_void_p(te.data_ptr()),
                                     C.c_void_p(tu.data_ptr()), 1)
         self._check(rc, "nks_set_state")
+
+    def set_comm(self, rank, nranks, z_offset, nz_global, allreduce, halo):
+        """Attach this z-slab state to its process group (nks_set_comm).  allreduce(ptr, n, stream) and
+        halo(ptr, nfields, field_stride, stream) are Python callables on raw device pointers that return
+        0 on success; the ctypes trampolines are kept alive by this object."""
+        def _ar(user, buf, n, stream):
+            try:
+                return int(allreduce(buf, n, stream) or 0)
+            except Exception as e:          # never let an exception unwind through C
+                self.comm_error = e
+                return 1
+
+        def _halo(user, vec, nf, stride, stream):
+            try:
+                return int(halo(vec, nf, stride, stream) or 0)
+            except Exception as e:
+                self.comm_error = e
+                return 1
+        self._comm_cbs = (ALLREDUCE_FN(_ar), HALO_FN(_halo))
+        self.comm_error = None
+        self._check(self.lib.nks_set_comm(self.st, int(rank), int(nranks), int(z_offset), int(nz_global),
+                                          self._comm_cbs[0], self._comm_cbs[1], None), "nks_set_comm")
+
+    def device_view(self, ptr, n):
+        """fp64 tensor aliasing n doubles at device pointer ptr inside this state's workspace."""
+        base = self.workspace.data_ptr()
+        off = int(ptr) - base
+        if off < 0 or off % 8 or off + 8 * int(n) > self.workspace_bytes:
+            raise ValueError("pointer outside the workspace")
+        return self.workspace[off:off + 8 * int(n)].view(self.torch.float64)
 
     def set_cbar0(self, cbar0):
         self._check(self.lib.nks_set_cbar0(self.st, C.c_double(cbar0)), "nks_set_cbar0")

@@ -39,27 +39,38 @@ def _world(group=None):
     return dist.get_world_size(group), dist.get_rank(group)
 
 
-def halo_exchange(t, group=None):
-    """Fill the 2 ghost planes on each side of t[..., nz_own + 4, ny, nx] from the periodic neighbours.
+def _is_gloo(group=None):
+    import torch.distributed as dist
+    return dist.get_backend(group) == "gloo"
 
-    t is a torch tensor (CPU with gloo, CUDA with NCCL); its own planes are t[..., 2:-2, :, :].
-    group: a torch.distributed ProcessGroup or None (the default group; no group initialised means
-    one rank).  Uses batched isend/irecv; returns after the exchange completed.
+
+def halo_exchange(t, group=None, ghost: int = GHOST):
+    """Fill the `ghost` ghost planes on each side of t[..., nz_own + 2*ghost, ny, nx] from the periodic
+    neighbours.
+
+    t is a torch tensor (CPU or CUDA); its own planes are t[..., ghost:-ghost, :, :].  group: a
+    torch.distributed ProcessGroup or None (the default group; no group initialised means one rank).
+    NCCL exchanges device tensors directly (send/recv over NVLink); gloo stages CUDA tensors through
+    host memory.  Uses batched isend/irecv; returns after the exchange completed.
     """
     import torch
+    g = int(ghost)
     nz_loc = t.shape[-3]
-    own = nz_loc - 2 * GHOST
-    if own < GHOST:
-        raise ValueError("a slab must own at least 2 planes")
+    own = nz_loc - 2 * g
+    if own < g:
+        raise ValueError(f"a slab must own at least {g} planes")
     # contiguous send/recv buffers (the planes are strided when leading field axes exist)
-    send_lo = t[..., GHOST:2 * GHOST, :, :].contiguous()             # my first own planes -> rank-1's top ghosts
-    send_hi = t[..., own:own + GHOST, :, :].contiguous()            # my last own planes -> rank+1's bottom ghosts
+    send_lo = t[..., g:2 * g, :, :].contiguous()             # my first own planes -> rank-1's top ghosts
+    send_hi = t[..., own:own + g, :, :].contiguous()         # my last own planes -> rank+1's bottom ghosts
     world, rank = _world(group)
     if world == 1:
-        t[..., nz_loc - GHOST:, :, :] = send_lo
-        t[..., :GHOST, :, :] = send_hi
+        t[..., nz_loc - g:, :, :] = send_lo
+        t[..., :g, :, :] = send_hi
         return t
     import torch.distributed as dist
+    stage = t.is_cuda and _is_gloo(group)
+    if stage:
+        send_lo, send_hi = send_lo.cpu(), send_hi.cpu()
     up, dn = (rank + 1) % world, (rank - 1) % world
     gu = dist.get_global_rank(group, up) if group is not None else up
     gd = dist.get_global_rank(group, dn) if group is not None else dn
@@ -71,9 +82,44 @@ def halo_exchange(t, group=None):
            dist.P2POp(dist.irecv, recv_lo, gd, group=group, tag=0), dist.P2POp(dist.irecv, recv_hi, gu, group=group, tag=1)]
     for req in dist.batch_isend_irecv(ops):
         req.wait()
-    t[..., :GHOST, :, :] = recv_lo
-    t[..., nz_loc - GHOST:, :, :] = recv_hi
+    t[..., :g, :, :] = recv_lo.to(t.device, non_blocking=False) if stage else recv_lo
+    t[..., nz_loc - g:, :, :] = recv_hi.to(t.device, non_blocking=False) if stage else recv_hi
     return t
+
+
+def allreduce_fixed_order(buf, group=None):
+    """In-place sum of buf over the ranks, added in rank order 0, 1, ..., world-1 on every rank.
+
+    An all-gather followed by a left-to-right sum: every rank obtains bitwise identical values (so
+    control decisions taken from them agree across ranks) and the result does not depend on the
+    collective's internal algorithm (reading R37; SURVEY Z34 fixed-order reductions).
+    """
+    import torch
+    import torch.distributed as dist
+    world, _ = _world(group)
+    if world == 1:
+        return buf
+    src = buf.cpu() if (buf.is_cuda and _is_gloo(group)) else buf.contiguous()
+    parts = [torch.empty_like(src) for _ in range(world)]
+    dist.all_gather(parts, src, group=group)
+    acc = parts[0].clone()
+    for r in range(1, world):
+        acc += parts[r]
+    buf.copy_(acc)
+    return buf
+
+
+def box_slab_bounds(nz: int, nsub_z: int, world: int, rank: int):
+    """z range and box count of `rank` when the nsub_z global boxes along z (split like the library's
+    split: the first nz % nsub_z boxes one plane longer) are dealt out contiguously.  A slab made of
+    whole boxes keeps the global subdomain grid -- and so GMRES's iteration counts -- independent of
+    the number of ranks."""
+    if nsub_z < world:
+        raise ValueError(f"nsub_z = {nsub_z} boxes cannot be dealt to {world} ranks")
+    base, rem = divmod(nz, nsub_z)
+    starts = [b * base + min(b, rem) for b in range(nsub_z + 1)]
+    b0, b1 = slab_bounds(nsub_z, world, rank)
+    return starts[b0], starts[b1], b1 - b0
 
 
 class SlabOperators:
@@ -117,3 +163,141 @@ class SlabOperators:
             Xb = halo_exchange(Xb, self.group)
             v = halo_exchange(v, self.group)
         return self.solver.eval_jv(Xb, v, dt)[:, GHOST:-GHOST]
+
+
+class ShardedSolver:
+    """One z-slab of a 3D periodic grid per rank, stepped by the library's full NKS step.
+
+    Every rank holds the own planes of its slab plus zghost ghost planes per side; the library calls
+    back into this object for the halo exchanges (before F, J.v, the RAS input and after every state
+    update) and for the allreduces (norms, admissibility counts, CGS2 projections, gauge sums, energy).
+    The RAS boxes are the global box grid dealt out whole to the ranks, so the preconditioner -- and
+    the iteration counts -- do not depend on the number of ranks.
+
+    shape_global / nsub: C order (nz, ny, nx).  group: a torch.distributed process group (NCCL on
+    GPUs; gloo stages through host memory) or None for the default group / one rank.
+    """
+
+    def __init__(self, shape_global, model, solver, h=0.25, nsub=(1, 1, 1), overlap=2, pc_type=None,
+                 pc_reuse=1, group=None, device=None):
+        import torch
+        from .nks import PC_RAS_BILU0, Solver
+        if len(shape_global) != 3:
+            raise ValueError("z-slab sharding is 3D")
+        self.torch = torch
+        self.group = group
+        self.world, self.rank = _world(group)
+        self.shape_global = tuple(int(v) for v in shape_global)
+        nz, ny, nx = self.shape_global
+        self.pc_type = PC_RAS_BILU0 if pc_type is None else pc_type
+        ras = self.pc_type == PC_RAS_BILU0
+        self.nsub_z = int(nsub[0])
+        if ras:
+            self.lo, self.hi, nbz = box_slab_bounds(nz, int(nsub[0]), self.world, self.rank)
+            self.zghost = max(GHOST, int(overlap) + 1)
+        else:
+            self.lo, self.hi = slab_bounds(nz, self.world, self.rank)
+            nbz = 1
+            self.zghost = GHOST
+        self.own = self.hi - self.lo
+        zg = self.zghost
+        self.local_shape = (self.own + 2 * zg, ny, nx)
+        self.model, self.solver_cfg, self.h = model, solver, h
+        self.solver = Solver(self.local_shape, model, solver, h=h, nsub=(nbz, int(nsub[1]), int(nsub[2])),
+                             overlap=overlap, pc_type=self.pc_type, pc_reuse=pc_reuse, zghost=zg, device=device)
+        self.device = self.solver.device
+        self.halo_calls = 0
+        self.allreduce_calls = 0
+        self.solver.set_comm(self.rank, self.world, self.lo, nz, self._allreduce, self._halo)
+
+    # ---------------------------------------------------------------- callbacks (library -> here)
+    def _allreduce(self, ptr, n, stream):
+        self.allreduce_calls += 1
+        with self.torch.cuda.stream(self.solver.stream):
+            allreduce_fixed_order(self.solver.device_view(ptr, n), self.group)
+        return 0
+
+    def _halo(self, ptr, nf, stride, stream):
+        self.halo_calls += 1
+        nz_loc, ny, nx = self.local_shape
+        if stride != nz_loc * ny * nx:
+            raise ValueError("unexpected field stride")
+        v = self.solver.device_view(ptr, nf * stride).view(nf, nz_loc, ny, nx)
+        with self.torch.cuda.stream(self.solver.stream):
+            halo_exchange(v, self.group, self.zghost)
+        return 0
+
+    # ---------------------------------------------------------------- API (global arrays in, local work)
+    def local(self, field):
+        """This rank's local slab (own planes + ghosts) of a global (..., nz, ny, nx) field."""
+        nz = self.shape_global[0]
+        idx = [(z % nz) for z in range(self.lo - self.zghost, self.hi + self.zghost)]
+        if isinstance(field, np.ndarray):
+            return field[..., idx, :, :].copy()
+        t = self.torch
+        return field[..., t.tensor(idx, device=field.device), :, :].contiguous()
+
+    def initial_displacement(self, c, eta):
+        """u^0 of the whole grid (a0: cuFFT on one device) from a temporary full-grid state."""
+        from .nks import PC_NONE, Solver
+        cfg = dict(self.solver_cfg)
+        cfg["gmres_restart"] = 1
+        helper = Solver(self.shape_global, self.model, cfg, h=self.h, pc_type=PC_NONE, device=self.device)
+        helper.set_fields(c, eta)
+        u = helper.get_state_device()[2:].clone()
+        del helper
+        return u
+
+    def set_fields(self, c, eta, u=None):
+        """Global c, eta (nz, ny, nx) and optionally u (3, nz, ny, nx), the same on every rank."""
+        t = self.torch
+        c = t.as_tensor(np.asarray(c) if not isinstance(c, t.Tensor) else c, dtype=t.float64).to(self.device)
+        eta = t.as_tensor(np.asarray(eta) if not isinstance(eta, t.Tensor) else eta, dtype=t.float64).to(self.device)
+        if u is None:
+            u = self.initial_displacement(c, eta)
+        else:
+            u = t.as_tensor(np.asarray(u) if not isinstance(u, t.Tensor) else u, dtype=t.float64).to(self.device)
+        self.solver.set_fields(self.local(c), self.local(eta), self.local(u))
+
+    def step(self, dt, raise_on_fail=True):
+        return self.solver.step(dt, raise_on_fail=raise_on_fail)
+
+    def run_adaptive(self, max_steps, t_end=0.0):
+        return self.solver.run_adaptive(max_steps, t_end)
+
+    def energy(self):
+        return self.solver.energy()
+
+    def own_state(self):
+        """X^n on the own planes, (5, own, ny, nx) device tensor."""
+        zg = self.zghost
+        return self.solver.get_state_device()[:, zg:zg + self.own]
+
+    def gather_state(self):
+        """The global X^n (5, nz, ny, nx) as numpy, on every rank (all-gather of the own planes)."""
+        import torch.distributed as dist
+        own = self.own_state()
+        if self.world == 1:
+            return own.cpu().numpy()
+        nz, ny, nx = self.shape_global
+        src = own.contiguous().cpu() if _is_gloo(self.group) else own.contiguous()
+        sizes = [hi - lo for lo, hi in (self.slab_of(r) for r in range(self.world))]
+        parts = [self.torch.empty((5, sz, ny, nx), dtype=src.dtype, device=src.device) for sz in sizes]
+        if len(set(sizes)) == 1:
+            dist.all_gather(parts, src, group=self.group)
+        else:      # unequal slabs: pad to the largest
+            m = max(sizes)
+            pad = self.torch.zeros((5, m, ny, nx), dtype=src.dtype, device=src.device)
+            pad[:, :src.shape[1]] = src
+            full = [self.torch.empty_like(pad) for _ in range(self.world)]
+            dist.all_gather(full, pad, group=self.group)
+            parts = [f[:, :sz] for f, sz in zip(full, sizes)]
+        return self.torch.cat([p.cpu() for p in parts], dim=1).numpy()
+
+    def slab_of(self, r):
+        """(lo, hi) global z range of rank r."""
+        from .nks import PC_RAS_BILU0
+        nz = self.shape_global[0]
+        if self.pc_type == PC_RAS_BILU0:
+            return box_slab_bounds(nz, self.nsub_z, self.world, r)[:2]
+        return slab_bounds(nz, self.world, r)

@@ -63,3 +63,55 @@ def test_halo_exchange_gloo(world, nz):
     mp.spawn(_worker, args=(world, _free_port(), nz, out), nprocs=world, join=True)
     assert sorted(out.keys()) == list(range(world))
     assert all(v == 0.0 for v in out.values()), dict(out)
+
+
+def _worker_wide(rank, world, port, nz, ghost, out):
+    """Ghost width 3 (RAS overlap 2 + 1) and the fixed-order allreduce of the sharded step."""
+    from paper_2209_08001_b200.shard import allreduce_fixed_order
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        g = np.random.default_rng(7).standard_normal((5, nz, 3, 4))
+        lo, hi = slab_bounds(nz, world, rank)
+        idx = [(z % nz) for z in range(lo - ghost, hi + ghost)]
+        want = g[:, idx].copy()
+        loc = torch.from_numpy(want.copy())
+        loc[:, :ghost] = np.nan
+        loc[:, -ghost:] = np.nan
+        halo_exchange(loc, ghost=ghost)
+        err = float(np.abs(loc.numpy() - want).max())
+        # allreduce: the per-rank partial sums of a global vector, added in rank order 0..world-1
+        vals = np.random.default_rng(11).standard_normal((world, 6))
+        buf = torch.from_numpy(vals[rank].copy())
+        allreduce_fixed_order(buf)
+        ref = vals[0].copy()
+        for r in range(1, world):
+            ref = ref + vals[r]
+        out[rank] = (err, buf.numpy().tobytes() == ref.tobytes())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,nz,ghost", [(2, 12, 3), (3, 18, 3), (2, 16, 4)])
+def test_wide_halo_and_fixed_order_allreduce_gloo(world, nz, ghost):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_wide, args=(world, _free_port(), nz, ghost, out), nprocs=world, join=True)
+    assert sorted(out.keys()) == list(range(world))
+    for r, (err, exact) in out.items():
+        assert err == 0.0, (r, err)
+        assert exact, r              # bitwise identical on every rank, and equal to the rank-ordered sum
+
+
+def test_box_slab_bounds_keep_whole_boxes():
+    from paper_2209_08001_b200.shard import box_slab_bounds
+    for nz, nb in ((16, 4), (10, 4), (18, 6), (256, 8), (129, 8)):
+        base, rem = divmod(nz, nb)
+        starts = {b * base + min(b, rem) for b in range(nb + 1)}
+        for world in (1, 2, 3, 4, 8):
+            if world > nb:
+                continue
+            b = [box_slab_bounds(nz, nb, world, r) for r in range(world)]
+            assert b[0][0] == 0 and b[-1][1] == nz
+            assert all(b[r][1] == b[r + 1][0] for r in range(world - 1))
+            assert all(lo in starts and hi in starts for lo, hi, _ in b)
+            assert sum(k for _, _, k in b) == nb
