@@ -62,6 +62,14 @@ void launch_ras2d_pack(void* plan, const double* fac, long long ld, cudaStream_t
 void ras2d_free(void* plan);
 int ras2d_cluster(void* plan);
 cudaError_t launch_ras2d(void* plan, const double* r, double* z, cudaStream_t s);
+namespace r2 {
+size_t workspace_bytes(const nks_grid& g);
+void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaStream_t stream, std::string& why);
+void free_plan(void* p);
+int cluster_of(void* p);
+void launch_pack(void* plan, const double* fac, long long ld, cudaStream_t s);
+cudaError_t launch_apply(void* plan, const double* r, double* z, cudaStream_t s);
+}  // namespace r2
 void launch_ras_apply(const BoxSet& B, int nf, long long N, const double* fac, const float* fac32, const double* r,
                       double* y, double* z, cudaStream_t s);
 void launch_fac_to_fp32(const BoxSet& B, int nf, const double* fac, float* fac32, cudaStream_t s);
@@ -168,8 +176,9 @@ Layout make_layout(const nks_grid& g, const nks_params& p) {
     L.off_levoff = o; o = align256(o + (size_t)(L.nbox + 1) * sizeof(int));
     L.off_levptr = o; o = align256(o + (size_t)nl * sizeof(int));
     L.off_posoff = o; o = align256(o + (size_t)(L.nbox + 1) * sizeof(int));
-    L.off_geo = o; o = align256(o + (d == 2 ? ras2d_workspace_bytes(g) : 0));
-    L.geo_bytes = d == 2 ? ras2d_workspace_bytes(g) : 0;
+    // one of the two pipelined 2D applies uses this slice (ras2d_rows.cu by default)
+    L.geo_bytes = d == 2 ? std::max(ras2d_workspace_bytes(g), r2::workspace_bytes(g)) : 0;
+    L.off_geo = o; o = align256(o + L.geo_bytes);
   }
   L.total = o;
   return L;
@@ -335,7 +344,8 @@ void pc_apply(nks_state* st, const double* r, double* z) {
     return;
   }
   PhaseScope ps(st, PH_RAS);
-  if (st->ras2d) CK(launch_ras2d(st->ras2d, r, z, st->stream));
+  if (st->ras2d_kind == 2) CK(r2::launch_apply(st->ras2d, r, z, st->stream));
+  else if (st->ras2d_kind == 1) CK(launch_ras2d(st->ras2d, r, z, st->stream));
   else launch_ras_apply(st->boxes, st->nf, st->N, st->fac, st->fac32, r, st->ybox, z, st->stream);
   st->launches += 1;
 }
@@ -352,7 +362,8 @@ void pc_setup(nks_state* st, const double* Xb) {
     launch_factor(st->boxes, st->nf, st->fac, st->stream);
     st->launches += 1;
     if (st->ras2d) {
-      launch_ras2d_pack(st->ras2d, st->fac, st->boxes.ld, st->stream);
+      if (st->ras2d_kind == 2) r2::launch_pack(st->ras2d, st->fac, st->boxes.ld, st->stream);
+      else launch_ras2d_pack(st->ras2d, st->fac, st->boxes.ld, st->stream);
       st->launches += 1;
     }
     if (st->fac32 && !st->ras2d) {
@@ -774,9 +785,18 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
       CK(cudaStreamSynchronize(st->stream));
       if (grid->dim == 2 && std::getenv("NKS_RAS_LEVEL") == nullptr) {
         std::string why;
-        st->ras2d = ras2d_plan(*grid, B, w + L.off_geo, L.geo_bytes, st->stream, why);
-        if (st->debug) std::fprintf(stderr, "[nks] ras2d pipeline: %s (cluster %d)\n", st->ras2d ? "on" : why.c_str(),
-                                    ras2d_cluster(st->ras2d));
+        // one lane per row (ras2d_rows.cu); NKS_RAS2D_OLD selects the 4-lanes-per-row design (ras2d.cu)
+        if (std::getenv("NKS_RAS2D_OLD") == nullptr) {
+          st->ras2d = r2::plan(*grid, B, w + L.off_geo, L.geo_bytes, st->stream, why);
+          if (st->ras2d) st->ras2d_kind = 2;
+        }
+        if (!st->ras2d) {
+          st->ras2d = ras2d_plan(*grid, B, w + L.off_geo, L.geo_bytes, st->stream, why);
+          if (st->ras2d) st->ras2d_kind = 1;
+        }
+        if (st->debug)
+          std::fprintf(stderr, "[nks] ras2d pipeline: %s (kind %d, cluster %d)\n", st->ras2d ? "on" : why.c_str(),
+                       st->ras2d_kind, st->ras2d_kind == 2 ? r2::cluster_of(st->ras2d) : ras2d_cluster(st->ras2d));
         CK(cudaStreamSynchronize(st->stream));
       }
     }
@@ -1107,7 +1127,8 @@ nks_status nks_destroy(nks_state* st) {
   if (st->h_ring) cudaFreeHost(st->h_ring);
   for (int k = 0; k < 4; ++k)
     if (st->gm_ev[k]) cudaEventDestroy(st->gm_ev[k]);
-  if (st->ras2d) ras2d_free(st->ras2d);
+  if (st->ras2d_kind == 2) r2::free_plan(st->ras2d);
+  else if (st->ras2d) ras2d_free(st->ras2d);
   delete st;
   return NKS_OK;
 }

@@ -121,6 +121,7 @@ struct nks_state {
   double* ybox = nullptr;   // [nf][P]
   bool pc_valid = false;
   void* ras2d = nullptr;    // plan of the row-pipelined 2D RAS apply (ras2d.cu), or null
+  int ras2d_kind = 0;       // 1: ras2d.cu (4 lanes per row), 2: ras2d_rows.cu (one lane per row)
   double pc_dt = 0.0;
   // history / controller
   double time = 0.0;
