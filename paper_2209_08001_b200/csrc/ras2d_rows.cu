@@ -64,6 +64,7 @@ struct Args {
   int nx, ny;
   int CS, RPC, KG, NSW;
   int prof;               // NKS_RAS2D_PROF: per-CTA cycle accounting into g_prof
+  int dbg;                // NKS_RAS2D_DBG bits (timing experiments only; results are wrong when set)
   const double* r;
   double* z;
 };
@@ -104,22 +105,76 @@ __device__ __forceinline__ void st_remote4(double* local_equiv, unsigned rank, c
   asm volatile("st.relaxed.cluster.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(raddr + 16), "d"(v[2]), "d"(v[3])
                : "memory");
 }
+// predicated variants (no branch in the sweeps)
+__device__ __forceinline__ void st_remote4_if(bool pred, double* local_equiv, unsigned rank, const double (&v)[4]) {
+  unsigned raddr;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(local_equiv)), "r"(rank));
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %0, 0;\n"
+               " @p st.relaxed.cluster.shared::cluster.v2.f64 [%1], {%2, %3};\n"
+               " @p st.relaxed.cluster.shared::cluster.v2.f64 [%4], {%5, %6};\n}\n"
+               ::"r"((int)pred), "r"(raddr), "d"(v[0]), "d"(v[1]), "r"(raddr + 16), "d"(v[2]), "d"(v[3])
+               : "memory");
+}
+__device__ __forceinline__ void st_remote4_weak_if(bool pred, double* local_equiv, unsigned rank, const double (&v)[4]) {
+  unsigned raddr;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(local_equiv)), "r"(rank));
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %0, 0;\n"
+               " @p st.shared::cluster.v2.f64 [%1], {%2, %3};\n"
+               " @p st.shared::cluster.v2.f64 [%4], {%5, %6};\n}\n"
+               ::"r"((int)pred), "r"(raddr), "d"(v[0]), "d"(v[1]), "r"(raddr + 16), "d"(v[2]), "d"(v[3])
+               : "memory");
+}
+__device__ __forceinline__ void st_global_if(bool pred, double* p, double v) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %0, 0;\n @p st.global.f64 [%1], %2;\n}\n" ::"r"((int)pred), "l"(p),
+               "d"(v)
+               : "memory");
+}
+__device__ __forceinline__ bool ready4(const double* p) {      // no sentinel in the cell (volatile)
+  double v[4];
+  return ld_vol4(p, v);
+}
 __device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
   const double2 a = *reinterpret_cast<const double2*>(p), b = *reinterpret_cast<const double2*>(p + 2);
   v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
 
-// acc[c] -= B[c][:] . v  for a row-major 4x4 block B in shared memory
+// acc[c] -= B[c][:] . v  for a row-major 4x4 block B in shared memory.  The 16 entries are loaded
+// first and the FMAs issued input-component-outer, so every round is 4 independent DFMAs (chain
+// depth 4 per block instead of a serial 16-FMA walk).
 __device__ __forceinline__ void blk_sub(const double* B, const double (&v)[4], double (&acc)[4]) {
+  double b[4][4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const double2 p = *reinterpret_cast<const double2*>(B + c * 4);
     const double2 q = *reinterpret_cast<const double2*>(B + c * 4 + 2);
-    acc[c] = fma(-p.x, v[0], acc[c]);
-    acc[c] = fma(-p.y, v[1], acc[c]);
-    acc[c] = fma(-q.x, v[2], acc[c]);
-    acc[c] = fma(-q.y, v[3], acc[c]);
+    b[c][0] = p.x; b[c][1] = p.y; b[c][2] = q.x; b[c][3] = q.y;
   }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[c] = fma(-b[c][k], v[k], acc[c]);
+}
+
+// two blocks into two accumulator sets, interleaved round by round (8 independent DFMAs per round)
+__device__ __forceinline__ void blk_sub2(const double* B1, const double (&v1)[4], double (&a1)[4], const double* B2,
+                                         const double (&v2)[4], double (&a2)[4]) {
+  double b[4][4], e[4][4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double2 p = *reinterpret_cast<const double2*>(B1 + c * 4);
+    const double2 q = *reinterpret_cast<const double2*>(B1 + c * 4 + 2);
+    const double2 r = *reinterpret_cast<const double2*>(B2 + c * 4);
+    const double2 t = *reinterpret_cast<const double2*>(B2 + c * 4 + 2);
+    b[c][0] = p.x; b[c][1] = p.y; b[c][2] = q.x; b[c][3] = q.y;
+    e[c][0] = r.x; e[c][1] = r.y; e[c][2] = t.x; e[c][3] = t.y;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      a1[c] = fma(-b[c][k], v1[k], a1[c]);
+      a2[c] = fma(-e[c][k], v2[k], a2[c]);
+    }
 }
 
 // ---------------------------------------------------------------------------------- repack
@@ -197,11 +252,12 @@ __global__ void __launch_bounds__(64, 1) k_apply(Args A) {
     // ---- producer: one bulk copy of the active rows of every step, forward then backward
     if (lane == 0) {
       const unsigned full0 = smem_u32(fullb), empty0 = smem_u32(emptyb), stage0 = smem_u32(stage);
-      for (int q = 0; q < 2 * nFp; ++q) {
+      // 2 nFp chunks, then one dummy (the consumer's look-ahead wait past the last step)
+      for (int q = 0; q <= 2 * nFp; ++q) {
         const int st = q % NSW, use = q / NSW;
         if (use > 0) mbar_wait(empty0 + st * 8, (unsigned)((use - 1) & 1));
         const bool fw = q < nFp;
-        const int k = fw ? q : 2 * nFp - 1 - q;
+        const int k = q == 2 * nFp ? 0 : (fw ? q : 2 * nFp - 1 - q);
         // rows with 0 <= k - 2 rl < ex (one dummy row on the padding steps; KG covers them)
         const int lo = min(R - 1, max(0, (k - ex + 2) / 2)), hi = max(lo, min(R - 1, k / 2));
         const int pf = fw ? kPF : kPB;
@@ -239,7 +295,7 @@ __global__ void __launch_bounds__(64, 1) k_apply(Args A) {
     };
     auto load_r = [&](int k, double (&o)[4]) {
       const int i = k - 2 * rl;
-      if (row_ok && i >= 0 && i < ex && k < nF) {
+      if (row_ok && i >= 0 && i < ex && k < nF && !(A.dbg & 1)) {
         const int gx = gx_of(i);
 #pragma unroll
         for (int c = 0; c < 4; ++c) o[c] = __ldg(rrow + c * N + gx);
@@ -263,11 +319,6 @@ __global__ void __launch_bounds__(64, 1) k_apply(Args A) {
       mbar_wait(full0 + stg_ * 8, par_);
       if (A.prof) t_stage += clock64() - c0;
     };
-    auto release_stage = [&](int stg_) {
-      __syncwarp();
-      // relaxed: the stage's shared-memory reads all fed DFMAs issued before (no release fence needed)
-      if (lane == 0) asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(emptyb) + stg_ * 8) : "memory");
-    };
     const double* const stage_row0 = stage + (size_t)min(rl, RPC - 1) * kPB;   // pitch applied below
     const int rowc = min(rl, RPC - 1);
     // Software pipeline: iteration k finishes step k (only the two lag-1 blocks, the loop-carried
@@ -280,6 +331,31 @@ __global__ void __launch_bounds__(64, 1) k_apply(Args A) {
       if (++stn == NSW) { stn = 0; parn ^= 1u; }
     };
     (void)stage_row0;
+    // wait for the stages of the next four steps (stn and the three after it)
+    auto wait_next4 = [&]() {
+      int st_ = stn;
+      unsigned pa_ = parn;
+      const long long c0 = A.prof ? clock64() : 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        mbar_wait(full0 + st_ * 8, pa_);
+        if (++st_ == NSW) { st_ = 0; pa_ ^= 1u; }
+      }
+      if (A.prof) t_stage += clock64() - c0;
+    };
+    // release the four stages used by a group (from s0 on)
+    auto release4 = [&](int s0) {
+      __syncwarp();
+      if (lane == 0) {
+        int st_ = s0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          // relaxed: the stage's shared-memory reads all fed DFMAs issued before (no release fence needed)
+          asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(emptyb) + st_ * 8) : "memory");
+          if (++st_ == NSW) st_ = 0;
+        }
+      }
+    };
 
     const long long cf0 = clock64();
     long long gt0;
@@ -312,10 +388,9 @@ __global__ void __launch_bounds__(64, 1) k_apply(Args A) {
       auto fiter = [&](int k, const double (&rn)[4]) {
         const int i = k - 2 * rl;
         const bool active = row_ok && i >= 0 && i < ex;
-        const bool more = k + 1 < nFp;
-        if (more) wait_stage(stn, parn);
         double hAn[4], hBn[4];
-        poll2(hclamp(1, k + 2), hclamp(0, k + 1), hAn, hBn);      // lane 0's cells for step k+1
+        ld4(hclamp(1, k + 2), hAn);        // lane 0's cells for step k+1 (written: checked per group)
+        ld4(hclamp(0, k + 1), hBn);
         double Ya1[4], aa4n[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -329,17 +404,16 @@ __global__ void __launch_bounds__(64, 1) k_apply(Args A) {
         double a0[4], a1[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int c = 0; c < 4; ++c) a0[c] = pre[c];
-        blk_sub(L + 3 * 16, Ya1, a0);   // (1,-1)
-        blk_sub(L + 5 * 16, yp, a1);    // (-1,0)
+        if (!(A.dbg & 16)) blk_sub2(L + 3 * 16, Ya1, a0, L + 5 * 16, yp, a1);   // (1,-1), (-1,0)
         // ---- step k+1: the older blocks (aa4 (0,-2), Ya3 = Ya2_k (-1,-1), Ya2 = Ya1_k (0,-1), Yo2 = y_{k-1} (-2,0))
         const double* Ln = stage + (size_t)stn * stage_elems + (size_t)rowc * kPF;
         double p0[4], p1[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int c = 0; c < 4; ++c) p0[c] = rn[c];
-        blk_sub(Ln + 0 * 16, aa4n, p0);
-        blk_sub(Ln + 1 * 16, Ya2, p1);
-        blk_sub(Ln + 2 * 16, Ya1, p0);
-        blk_sub(Ln + 4 * 16, yp, p1);
+        if (!(A.dbg & 8)) {
+          blk_sub2(Ln + 0 * 16, aa4n, p0, Ln + 1 * 16, Ya2, p1);
+          blk_sub2(Ln + 2 * 16, Ya1, p0, Ln + 4 * 16, yp, p1);
+        }
         double y[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -347,17 +421,35 @@ __global__ void __launch_bounds__(64, 1) k_apply(Args A) {
           pre[c] = p0[c] + p1[c];
           Ya3[c] = Ya2[c]; Ya2[c] = Ya1[c]; yp[c] = y[c]; hA[c] = hAn[c];
         }
-        release_stage(stg);
         advance();
-        *reinterpret_cast<double2*>(ybuf + (size_t)k * 128) = make_double2(y[0], y[1]);
-        *reinterpret_cast<double2*>(ybuf + (size_t)k * 128 + 2) = make_double2(y[2], y[3]);
-        if (dn_remote && active && rl >= R - 2) st_remote4(hcell(rl - (R - 2), i), (unsigned)(s + 1), y);
+        if (!(A.dbg & 2)) {
+          *reinterpret_cast<double2*>(ybuf + (size_t)k * 128) = make_double2(y[0], y[1]);
+          *reinterpret_cast<double2*>(ybuf + (size_t)k * 128 + 2) = make_double2(y[2], y[3]);
+        }
+        if (A.dbg & 64) st_remote4_weak_if(!(A.dbg & 4) && dn_remote && active && rl >= R - 2,
+                      hcell(min(max(rl - (R - 2), 0), 1), min(max(i, 0), ex - 1)), (unsigned)min(s + 1, CS - 1), y);
+        else st_remote4_if(!(A.dbg & 4) && dn_remote && active && rl >= R - 2, hcell(min(max(rl - (R - 2), 0), 1), min(max(i, 0), ex - 1)),
+                      (unsigned)min(s + 1, CS - 1), y);
       };
       for (int k0 = 0; k0 < nFp; k0 += 4) {
+        // once per 4 steps: the stages of steps k0+1..k0+4 are resident and lane 0's halo cells for
+        // them are written (one uniform poll loop), so the four steps below are branch-free
+        wait_next4();
+        {
+          unsigned spins = 0;
+          const long long c0 = A.prof ? clock64() : 0;
+          while (!(A.dbg & 32) && !(ready4(hclamp(1, k0 + 2)) & ready4(hclamp(1, k0 + 3)) & ready4(hclamp(1, k0 + 4)) &
+                   ready4(hclamp(1, k0 + 5)) & ready4(hclamp(0, k0 + 1)) & ready4(hclamp(0, k0 + 2)) &
+                   ready4(hclamp(0, k0 + 3)) & ready4(hclamp(0, k0 + 4))))
+            if (++spins > (1u << 28)) __trap();      // a lost neighbour would otherwise hang the GPU
+          if (A.prof) t_halo += clock64() - c0;
+        }
+        const int s0 = stg;
         fiter(k0, q1); load_r(k0 + 5, q1);
         fiter(k0 + 1, q2); load_r(k0 + 6, q2);
         fiter(k0 + 2, q3); load_r(k0 + 7, q3);
         fiter(k0 + 3, q0); load_r(k0 + 8, q0);
+        release4(s0);
       }
     }
 
@@ -397,11 +489,10 @@ __global__ void __launch_bounds__(64, 1) k_apply(Args A) {
       auto biter = [&](int k, const double (&yn)[4]) {
         const int i = k - 2 * rl;
         const bool active = row_ok && i >= 0 && i < ex;
-        const bool more = k > 0;
-        if (more) wait_stage(stn, parn);
         const int iR = k - dR;            // lane R-1's point at step k
         double hAn[4], hBn[4];
-        poll2(hclamp(2, iR - 2), hclamp(3, iR - 1), hAn, hBn);   // lane R-1's cells for step k-1
+        ld4(hclamp(2, iR - 2), hAn);      // lane R-1's cells for step k-1 (written: checked per group)
+        ld4(hclamp(3, iR - 1), hBn);
         double Xb1[4], bb4n[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -415,8 +506,7 @@ __global__ void __launch_bounds__(64, 1) k_apply(Args A) {
         double a0[4], a1[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int c = 0; c < 4; ++c) a0[c] = pre[c];
-        blk_sub(U + 3 * 16, Xb1, a0);   // (-1,1)
-        blk_sub(U + 1 * 16, xp, a1);    // (1,0)
+        blk_sub2(U + 3 * 16, Xb1, a0, U + 1 * 16, xp, a1);   // (-1,1), (1,0)
         double v[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) v[c] = a0[c] + a1[c];
@@ -432,32 +522,43 @@ __global__ void __launch_bounds__(64, 1) k_apply(Args A) {
         double p0[4], p1[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int c = 0; c < 4; ++c) p0[c] = yn[c];
-        blk_sub(Un + 6 * 16, bb4n, p0);
-        blk_sub(Un + 5 * 16, Xb2, p1);
-        blk_sub(Un + 4 * 16, Xb1, p0);
-        blk_sub(Un + 2 * 16, xp, p1);
+        blk_sub2(Un + 6 * 16, bb4n, p0, Un + 5 * 16, Xb2, p1);
+        blk_sub2(Un + 4 * 16, Xb1, p0, Un + 2 * 16, xp, p1);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           x[c] = active ? x[c] : 0.0;
           pre[c] = p0[c] + p1[c];
           Xb3[c] = Xb2[c]; Xb2[c] = Xb1[c]; xp[c] = x[c]; hA[c] = hAn[c];
         }
-        release_stage(stg);
         advance();
-        if (active && own_row && i >= G.ox0 && i < G.ox0 + G.ownx) {
-          const int gx = gx_of(i);
+        {
+          const bool own = active && own_row && i >= G.ox0 && i < G.ox0 + G.ownx;
+          double* zp = zrow + gx_of(min(max(i, 0), ex - 1));
 #pragma unroll
-          for (int c = 0; c < 4; ++c) zrow[c * N + gx] = x[c];
+          for (int c = 0; c < 4; ++c) st_global_if(own, zp + c * N, x[c]);
         }
-        if (up_remote && active && rl < 2) st_remote4(hcell(2 + rl, i), (unsigned)(s - 1), x);
+        st_remote4_if(up_remote && active && rl < 2, hcell(2 + min(rl, 1), min(max(i, 0), ex - 1)), (unsigned)max(s - 1, 0), x);
       };
       // iteration for step k uses y_{k-1}: k = nFp-1-kb; ring q1, q2, q3, q0 holds y_{nFp-2-kb}
       for (int kb0 = 0; kb0 < nFp; kb0 += 4) {
         const int k0 = nFp - 1 - kb0;
+        wait_next4();
+        {
+          const int iR = k0 - dR;
+          unsigned spins = 0;
+          const long long c0 = A.prof ? clock64() : 0;
+          while (!(A.dbg & 32) && !(ready4(hclamp(2, iR - 2)) & ready4(hclamp(2, iR - 3)) & ready4(hclamp(2, iR - 4)) &
+                   ready4(hclamp(2, iR - 5)) & ready4(hclamp(3, iR - 1)) & ready4(hclamp(3, iR - 2)) &
+                   ready4(hclamp(3, iR - 3)) & ready4(hclamp(3, iR - 4))))
+            if (++spins > (1u << 28)) __trap();
+          if (A.prof) t_halo += clock64() - c0;
+        }
+        const int s0 = stg;
         biter(k0, q1); load_y(k0 - 5, q1);
         biter(k0 - 1, q2); load_y(k0 - 6, q2);
         biter(k0 - 2, q3); load_y(k0 - 7, q3);
         biter(k0 - 3, q0); load_y(k0 - 8, q0);
+        release4(s0);
       }
     }
     if (A.prof && lane == 0) {
@@ -547,9 +648,9 @@ void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaSt
   for (int cs = 8; cs >= 1; --cs) {
     if (!cs_ok(D, cs) || (cs_env && cs != std::atoi(cs_env))) continue;
     const int rpc = (D.eymax + cs - 1) / cs;
-    int nsw = 12;
+    int nsw = 12;   // >= 6: a group of 4 steps holds 5 stages
     if (const char* e = std::getenv("NKS_RAS2D_NSW")) nsw = std::max(2, std::atoi(e));
-    while (nsw > 2 && smem_for(D, rpc, nsw) > (size_t)maxsm) --nsw;
+    while (nsw > 6 && smem_for(D, rpc, nsw) > (size_t)maxsm) --nsw;
     const size_t sm = smem_for(D, rpc, nsw);
     if (sm > (size_t)maxsm) continue;
     if (cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
@@ -610,7 +711,7 @@ void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaSt
   if (cudaMemcpyAsync(gd, geo.data(), geo.size() * sizeof(Geo), cudaMemcpyHostToDevice, stream) != cudaSuccess) {
     why = "copy"; delete P; return nullptr;
   }
-  P->A = Args{gd, B.lev_ptr, cF, cB, ys, (long long)g.n[0] * g.n[1], g.n[0], g.n[1], CS, RPC, P->KG, NSW, 0, nullptr, nullptr};
+  P->A = Args{gd, B.lev_ptr, cF, cB, ys, (long long)g.n[0] * g.n[1], g.n[0], g.n[1], CS, RPC, P->KG, NSW, 0, 0, nullptr, nullptr};
   if (std::getenv("NKS_DEBUG"))
     std::fprintf(stderr, "[nks] ras2d rows: %d boxes, cluster %d, %d rows/CTA, NSW %d, smem %zu B, max active clusters %d\n",
                  P->nbox, CS, RPC, NSW, P->smem, P->max_clusters);
@@ -647,6 +748,8 @@ cudaError_t launch_apply(void* plan, const double* r, double* z, cudaStream_t s)
   cfg.numAttrs = 1;
   static const bool prof = std::getenv("NKS_RAS2D_PROF") != nullptr;
   A.prof = prof ? 1 : 0;
+  static const int dbg = std::getenv("NKS_RAS2D_DBG") ? std::atoi(std::getenv("NKS_RAS2D_DBG")) : 0;
+  A.dbg = dbg;
   cudaError_t e = cudaLaunchKernelEx(&cfg, k_apply, A);
   if (prof && e == cudaSuccess) {
     static int calls = 0;

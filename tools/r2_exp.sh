@@ -1,0 +1,3 @@
+for d in 0 32 36 60 64 96; do
+  echo "dbg $d: $(NKS_RAS2D_DBG=$d NKS_RAS2D_PROF=1 CFG=2 timeout 60 python tools/time_pc.py 2>&1 | grep -E 'cta  0|ras_apply' | tail -2 | tr '\n' ' ')"
+done
