@@ -64,7 +64,7 @@ int ras2d_cluster(void* plan);
 cudaError_t launch_ras2d(void* plan, const double* r, double* z, cudaStream_t s);
 namespace r2 {
 size_t workspace_bytes(const nks_grid& g);
-void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaStream_t stream, std::string& why);
+void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaStream_t stream, std::string& why, bool f32);
 void free_plan(void* p);
 int cluster_of(void* p);
 void launch_pack(void* plan, const double* fac, long long ld, cudaStream_t s);
@@ -787,7 +787,7 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
         std::string why;
         // one lane per row (ras2d_rows.cu); NKS_RAS2D_OLD selects the 4-lanes-per-row design (ras2d.cu)
         if (std::getenv("NKS_RAS2D_OLD") == nullptr) {
-          st->ras2d = r2::plan(*grid, B, w + L.off_geo, L.geo_bytes, st->stream, why);
+          st->ras2d = r2::plan(*grid, B, w + L.off_geo, L.geo_bytes, st->stream, why, params->factor_fp32 != 0);
           if (st->ras2d) st->ras2d_kind = 2;
         }
         if (!st->ras2d) {

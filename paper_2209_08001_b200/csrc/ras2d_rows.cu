@@ -46,10 +46,23 @@ namespace nks {
 namespace r2 {
 
 constexpr int kRPC = 32;   // rows per CTA at most (one lane per row)
-constexpr int kPF = 98;    // forward row pitch: 6 lower blocks = 96 doubles; 784 B = 16 mod 128
-constexpr int kPB = 114;   // backward row pitch: diagonal + 6 upper = 112 doubles; 912 B = 16 mod 128
-constexpr int kG = 2;      // steps per group (one bulk copy)
-constexpr int kNSW = 4;    // group buffers
+// Stream element type: fp64 factors (default) or fp32 copies (factor_fp32: preconditioner only).
+// Row pitches are odd multiples of 16 bytes, so the 16-byte loads of 8 lanes hit distinct banks.
+template <bool F32> struct Strm {
+  using T = double;
+  static constexpr int PF = 98;    // forward: 6 lower blocks = 96 doubles, 784 B
+  static constexpr int PB = 114;   // backward: diagonal + 6 upper = 112 doubles, 912 B
+  static constexpr int G = 2;      // steps per group (one bulk copy)
+  static constexpr int NS = 4;     // group buffers
+};
+template <> struct Strm<true> {
+  using T = float;
+  static constexpr int PF = 100;   // 400 B
+  static constexpr int PB = 116;   // 464 B
+  static constexpr int G = 4;
+  static constexpr int NS = 4;
+};
+constexpr int kGmax = 4;
 
 struct Geo {
   int s0x, s0y;       // global coordinate of local (0,0) (may be negative: wraps)
@@ -64,8 +77,8 @@ struct Args {
   const Geo* boxes;
   const int* lev_ptr;
   const int* offt;        // [box][stripe][KGp]: rows of the compact stream before step k
-  const double* chunkF;   // [box][stripe][RPC*exmax rows][kPF]
-  const double* chunkB;   // [box][stripe][RPC*exmax rows][kPB]
+  const void* chunkF;     // [box][stripe][RPC*exmax rows][PF] of Strm<F32>::T
+  const void* chunkB;     // [box][stripe][RPC*exmax rows][PB]
   double* yscr;           // [box][stripe][KGp][32][4]
   long long N;
   int nx, ny;
@@ -106,6 +119,10 @@ __device__ __forceinline__ bool ready4(const double* p) {
   asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(c), "=l"(d) : "r"(sa + 16) : "memory");
   return a != kSentinel && b != kSentinel && c != kSentinel && d != kSentinel;
 }
+__device__ __forceinline__ void ld4(const float* p, double (&v)[4]) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+}
 __device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
   const double2 a = *reinterpret_cast<const double2*>(p), b = *reinterpret_cast<const double2*>(p + 2);
   v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
@@ -137,8 +154,12 @@ __device__ __forceinline__ void st_global_if(bool pred, double* p, double v) {
 // ---------------------------------------------------------------------------------- repack
 // One thread per (box point, plane): the point's row in its stripe's compact stream is
 // off[k] + (rl - lo(k)), k = i + 2 rl.
-__global__ void k_pack(Args A, const double* __restrict__ fac, long long ld, int nbox, long long work, double* chunkF,
-                       double* chunkB) {
+template <bool F32>
+__global__ void k_pack(Args A, const double* __restrict__ fac, long long ld, int nbox, long long work) {
+  using S = Strm<F32>;
+  using T = typename S::T;
+  T* chunkF = (T*)A.chunkF;
+  T* chunkB = (T*)A.chunkB;
   for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < work; w += (long long)gridDim.x * blockDim.x) {
     long long rem = w;
     const int plane = (int)(rem % 208);
@@ -162,13 +183,17 @@ __global__ void k_pack(Args A, const double* __restrict__ fac, long long ld, int
     const long long sb = (long long)b * A.CS + s;
     const long long row = sb * A.RPC * A.exmax + A.offt[sb * A.KGp + k] + (rl - lo_of(k, G.ex, R));
     const double v = fac[(long long)plane * ld + pos];
-    if (plane < 96) chunkF[row * kPF + plane] = v;
-    else chunkB[row * kPB + (plane - 96)] = v;
+    if (plane < 96) chunkF[row * S::PF + plane] = (T)v;
+    else chunkB[row * S::PB + (plane - 96)] = (T)v;
   }
 }
 
 // ---------------------------------------------------------------------------------- apply
+template <bool F32>
 __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
+  using S = Strm<F32>;
+  using T = typename S::T;
+  constexpr int kPF = S::PF, kPB = S::PB, kG = S::G, kNSW = S::NS;
   extern __shared__ __align__(128) unsigned char smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const int s = (int)cluster.block_rank();
@@ -186,7 +211,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   const long long sb = (long long)b * CS + s;
   const int* off_g = A.offt + sb * A.KGp;     // off[0 .. nFp] in global memory (copied to shared below)
   const size_t stage_elems = (size_t)kG * RPC * kPB;
-  double* stage = reinterpret_cast<double*>(smem);                     // [kNSW][kG*RPC rows][pitch]
+  T* stage = reinterpret_cast<T*>(smem);                               // [kNSW][kG*RPC rows][pitch]
   uint64_t* fullb = reinterpret_cast<uint64_t*>(stage + kNSW * stage_elems);
   uint64_t* emptyb = fullb + kNSW;
   const int pitch = (ex + 4) * 4;
@@ -239,12 +264,12 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       const int r_lo = off[k0];
       const int nrows = max(1, off[k0 + kG] - r_lo);
       const int pf = fw ? kPF : kPB;
-      const double* src = fw ? A.chunkF + (base + r_lo) * kPF : A.chunkB + (base + r_lo) * kPB;
-      const unsigned bytes = (unsigned)(nrows * pf * 8);
+      const T* src = fw ? (const T*)A.chunkF + (base + r_lo) * kPF : (const T*)A.chunkB + (base + r_lo) * kPB;
+      const unsigned bytes = (unsigned)(nrows * pf * sizeof(T));
       const unsigned bar = full0 + (q % kNSW) * 8;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       stage0 + (unsigned)((q % kNSW) * stage_elems * 8)),
+                       stage0 + (unsigned)((q % kNSW) * stage_elems * sizeof(T))),
                    "l"(src), "r"(bytes), "r"(bar)
                    : "memory");
     };
@@ -360,7 +385,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     auto v_bar = [&]() { asm volatile("bar.sync 2, 128;" ::: "memory"); };
     auto e_bar = [&]() { asm volatile("bar.sync 3, 128;" ::: "memory"); };
     // this lane's block row c of step k (processing step p) in its group's buffer; nullptr-safe row 0
-    auto rowp = [&](int k, int p, int pf) -> const double* {
+    auto rowp = [&](int k, int p, int pf) -> const T* {
       const int q = gof(p);
       const int kb = klo(q);
       const int kc = min(max(k, 0), nFp);
@@ -368,7 +393,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       const int rr = (k >= 0 && k < nFp && rl >= lo && rl <= hi) ? off[kc] - off[kb] + (rl - lo) : 0;
       return stage + (size_t)(q % kNSW) * stage_elems + (size_t)rr * pf + c * 4;
     };
-    auto ldrow = [&](const double* p, double (&v)[4]) { ld4(p, v); };
+    auto ldrow = [&](const T* p, double (&v)[4]) { ld4(p, v); };
     auto zero4 = [&](double (&v)[4]) { v[0] = v[1] = v[2] = v[3] = 0.0; };
     auto dot4 = [&](const double (&m)[4], const double (&v)[4], double acc) {
       acc = fma(-m[0], v[0], acc);
@@ -463,11 +488,11 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       double U3[4], U1[4], D[4], N4[4], N2[4], M6[4], M5[4];
       auto preload = [&](int k) {      // rows for iteration k
         if (k >= 0) {
-          const double* u = rowp(k, pofk(k), kPB);
+          const T* u = rowp(k, pofk(k), kPB);
           ldrow(u + 3 * 16, U3); ldrow(u + 1 * 16, U1); ldrow(u, D);
         } else { zero4(U3); zero4(U1); zero4(D); }
-        if (k - 1 >= 0) { const double* u = rowp(k - 1, pofk(k - 1), kPB); ldrow(u + 4 * 16, N4); ldrow(u + 2 * 16, N2); } else { zero4(N4); zero4(N2); }
-        if (k - 2 >= 0) { const double* u = rowp(k - 2, pofk(k - 2), kPB); ldrow(u + 6 * 16, M6); ldrow(u + 5 * 16, M5); } else { zero4(M6); zero4(M5); }
+        if (k - 1 >= 0) { const T* u = rowp(k - 1, pofk(k - 1), kPB); ldrow(u + 4 * 16, N4); ldrow(u + 2 * 16, N2); } else { zero4(N4); zero4(N2); }
+        if (k - 2 >= 0) { const T* u = rowp(k - 2, pofk(k - 2), kPB); ldrow(u + 6 * 16, M6); ldrow(u + 5 * 16, M5); } else { zero4(M6); zero4(M5); }
       };
       double q0, q1, q2, q3;          // y prefetch ring: y(k-2) is used at iteration k
       auto load_y = [&](int k) -> double { return k >= 0 ? ybuf[(size_t)k * 128] : 0.0; };
@@ -491,10 +516,10 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
           bb4[u] = bot ? h3a[u] : (bot2 ? h2c[u] : 0.0);
           bb4n[u] = bot ? h3b[u] : (bot2 ? h2b[u] : 0.0);
         }
-        const double* u = rowp(K, pofk(K), kPB);
+        const T* u = rowp(K, pofk(K), kPB);
         ldrow(u + 6 * 16, a); ldrow(u + 5 * 16, bb); ldrow(u + 4 * 16, cc);
         pre = dot4(cc, Xb2, dot4(bb, Xb3, dot4(a, bb4, yK)));     // (0,2), (1,1), (0,1)
-        const double* un = rowp(K - 1, pofk(K - 1), kPB);
+        const T* un = rowp(K - 1, pofk(K - 1), kPB);
         ldrow(un + 6 * 16, a); ldrow(un + 5 * 16, bb);
         half = dot4(bb, Xb2, dot4(a, bb4n, yK1));                 // (0,2), (1,1) of step K-1 (Xb3(K-1) = Xb2(K))
         preload(K);
@@ -551,6 +576,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
 // ------------------------------------------------------------------------------------------ host
 struct Plan {
   int CS = 1, RPC = 32, KGp = 1, nbox = 0, max_clusters = 0;
+  bool f32 = false;         // fp32 factor stream (factor_fp32)
   size_t smem = 0;
   long long npts_total = 0;
   Args A{};
@@ -587,14 +613,14 @@ static int cs_min(const Dims& D) { return (D.eymax + kRPC - 1) / kRPC; }
 // cluster sizes this grid admits: every stripe <= 32 rows and >= 2 rows, portable cluster size <= 8
 static bool cs_ok(const Dims& D, int CS) { return CS >= cs_min(D) && CS <= 8 && D.eymin / CS >= 2; }
 
-static int kgp_of(const Dims& D, int RPC) { return D.exmax + 2 * (RPC - 1) + 4 * kG + 1; }
+static int kgp_of(const Dims& D, int RPC) { return D.exmax + 2 * (RPC - 1) + 4 * kGmax + 1; }
 
 static size_t chunk_bytes(const Dims& D, int CS) {
   const int RPC = (D.eymax + CS - 1) / CS;
   const size_t nsb = (size_t)D.nbox * CS;
   const size_t rows = nsb * RPC * D.exmax;
   const size_t yscr = nsb * kgp_of(D, RPC) * 128;
-  return (rows * (kPF + kPB) + yscr) * sizeof(double) + nsb * kgp_of(D, RPC) * sizeof(int) + 256;
+  return (rows * (Strm<false>::PF + Strm<false>::PB) + yscr) * sizeof(double) + nsb * kgp_of(D, RPC) * sizeof(int) + 256;
 }
 
 size_t workspace_bytes(const nks_grid& g) {
@@ -606,12 +632,13 @@ size_t workspace_bytes(const nks_grid& g) {
   return m ? m + (size_t)D.nbox * sizeof(Geo) + 1024 : 0;
 }
 
-static size_t smem_for(const Dims& D, int RPC) {
-  return (size_t)kNSW * kG * RPC * kPB * 8 + 2 * (size_t)kNSW * 8 + (size_t)4 * (D.exmax + 4) * 4 * 8 +
-         (size_t)9 * 128 * 8 + (size_t)kgp_of(D, RPC) * 4;
+static size_t smem_for(const Dims& D, int RPC, bool f32) {
+  const size_t stage = f32 ? (size_t)Strm<true>::NS * Strm<true>::G * RPC * Strm<true>::PB * sizeof(float)
+                           : (size_t)Strm<false>::NS * Strm<false>::G * RPC * Strm<false>::PB * sizeof(double);
+  return stage + 2 * (size_t)4 * 8 + (size_t)4 * (D.exmax + 4) * 4 * 8 + (size_t)9 * 128 * 8 + (size_t)kgp_of(D, RPC) * 4;
 }
-
-void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaStream_t stream, std::string& why) {
+static const void* apply_fn(bool f32) { return f32 ? (const void*)k_apply<true> : (const void*)k_apply<false>; }
+void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaStream_t stream, std::string& why, bool f32) {
   Dims D;
   if (!dims_of(g, D)) { why = "not 2D"; return nullptr; }
   if (B.nslots != 13 || B.diag != 6) { why = "unexpected slot table"; return nullptr; }
@@ -628,9 +655,9 @@ void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaSt
   for (int cs = 8; cs >= 1; --cs) {
     if (!cs_ok(D, cs) || (cs_env && cs != std::atoi(cs_env))) continue;
     const int rpc = (D.eymax + cs - 1) / cs;
-    const size_t sm = smem_for(D, rpc);
+    const size_t sm = smem_for(D, rpc, f32);
     if (sm > (size_t)maxsm) continue;
-    if (cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
+    if (cudaFuncSetAttribute(apply_fn(f32), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
       cudaGetLastError();
       continue;
     }
@@ -643,7 +670,7 @@ void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaSt
     at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.attrs = at; cfg.numAttrs = 1;
     int mc = 0;
-    if (cudaOccupancyMaxActiveClusters(&mc, k_apply, &cfg) != cudaSuccess) mc = 0;
+    if (cudaOccupancyMaxActiveClusters(&mc, apply_fn(f32), &cfg) != cudaSuccess) mc = 0;
     cudaGetLastError();
     if (mc < 1) continue;
     if (CS == 0 || (mc >= D.nbox && ncl < D.nbox) || (ncl < D.nbox && mc > ncl)) { CS = cs; smem = sm; ncl = mc; }
@@ -656,7 +683,8 @@ void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaSt
   P->CS = CS; P->RPC = RPC; P->KGp = KGp; P->nbox = D.nbox;
   P->smem = smem;
   P->max_clusters = ncl;
-  if (cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem) != cudaSuccess) {
+  P->f32 = f32;
+  if (cudaFuncSetAttribute(apply_fn(f32), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem) != cudaSuccess) {
     cudaGetLastError();
     why = "smem attribute"; delete P; return nullptr;
   }
@@ -693,8 +721,8 @@ void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaSt
   const size_t nsb = (size_t)D.nbox * CS;
   const size_t rows = nsb * RPC * D.exmax;
   double* cF = (double*)w;
-  double* cB = cF + rows * kPF;
-  double* ys = cB + rows * kPB;
+  double* cB = cF + rows * Strm<false>::PF;     // fp64-sized slots; an fp32 stream uses half of each
+  double* ys = cB + rows * Strm<false>::PB;
   int* ot = (int*)(ys + nsb * KGp * 128);
   Geo* gd = (Geo*)((char*)ot + ((nsb * KGp * sizeof(int) + 255) & ~(size_t)255));
   if (cudaMemcpyAsync(gd, geo.data(), geo.size() * sizeof(Geo), cudaMemcpyHostToDevice, stream) != cudaSuccess ||
@@ -705,8 +733,8 @@ void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaSt
   P->A = Args{gd, B.lev_ptr, ot, cF, cB, ys, (long long)g.n[0] * g.n[1], g.n[0], g.n[1], CS, RPC, KGp, D.exmax, 0, 0,
               nullptr, nullptr};
   if (std::getenv("NKS_DEBUG"))
-    std::fprintf(stderr, "[nks] ras2d rows: %d boxes, cluster %d, %d rows/CTA, %d-step groups, smem %zu B, max active clusters %d\n",
-                 P->nbox, CS, RPC, kG, P->smem, P->max_clusters);
+    std::fprintf(stderr, "[nks] ras2d rows: %d boxes, cluster %d, %d rows/CTA, %s stream, smem %zu B, max active clusters %d\n",
+                 P->nbox, CS, RPC, f32 ? "fp32" : "fp64", P->smem, P->max_clusters);
   return P;
 }
 
@@ -717,8 +745,8 @@ void launch_pack(void* plan, const double* fac, long long ld, cudaStream_t s) {
   Plan* P = (Plan*)plan;
   const long long work = P->npts_total * 208;
   const int blocks = (int)std::min<long long>((work + 255) / 256, 148 * 16);
-  k_pack<<<blocks, 256, 0, s>>>(P->A, fac, ld, P->nbox, work, const_cast<double*>(P->A.chunkF),
-                                const_cast<double*>(P->A.chunkB));
+  if (P->f32) k_pack<true><<<blocks, 256, 0, s>>>(P->A, fac, ld, P->nbox, work);
+  else k_pack<false><<<blocks, 256, 0, s>>>(P->A, fac, ld, P->nbox, work);
 }
 
 cudaError_t launch_apply(void* plan, const double* r, double* z, cudaStream_t s) {
@@ -742,7 +770,7 @@ cudaError_t launch_apply(void* plan, const double* r, double* z, cudaStream_t s)
   A.prof = prof ? 1 : 0;
   static const int dbg = std::getenv("NKS_RAS2D_DBG") ? std::atoi(std::getenv("NKS_RAS2D_DBG")) : 0;
   A.dbg = dbg;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_apply, A);
+  cudaError_t e = P->f32 ? cudaLaunchKernelEx(&cfg, k_apply<true>, A) : cudaLaunchKernelEx(&cfg, k_apply<false>, A);
   if (prof && e == cudaSuccess) {
     static int calls = 0;
     if (++calls % 10 == 0) {

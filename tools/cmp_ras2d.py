@@ -19,7 +19,9 @@ for shape, nsub, ov in CASES:
         for k in ("NKS_RAS2D_OLD", "NKS_RAS_LEVEL"):
             os.environ.pop(k, None)
         os.environ.update(env)
-        g = Solver(shape, ni.model_default(), ni.solver_default(), nsub=nsub, overlap=ov)
+        sol = ni.solver_default()
+        sol["factor_fp32"] = int(os.environ.get("FP32", "0"))
+        g = Solver(shape, ni.model_default(), sol, nsub=nsub, overlap=ov)
         g.set_fields(c, eta, None)
         X = g.get_state()
         g.pc_setup(X, 0.3)
