@@ -18,9 +18,11 @@ roofline = the dominant kernel of the step (per-phase CUDA events recorded by th
          against MEASURED_PEAKS.json hbm_gbs;
 cpu_baseline = the oracle (oracle/, plain NumPy/SciPy) as it stands, on a bounded sample.
 
-N > 1: the configs' partitioning over GPUs (sharded subdomains with halo exchange) is not
-built yet; ranks run independent replicas of the config, scaling
-"weak", value = all ranks' steps / max-over-ranks time.
+N > 1: config 2 (2D) runs independent replicas per rank (the 2D sweep is not sharded; DESIGN.md
+"Multi-GPU"), scaling "weak", value = all ranks' steps / max-over-ranks time.  3D configs
+(--config 3/4) run the z-slab SHARDED step at N > 1 (or with --sharded at N = 1): every rank owns
+whole RAS boxes of the global box grid, the library calls back for NCCL halo exchanges and
+fixed-order allreduces (paper_2209_08001_b200/shard.py), value = steps/s of the one global run.
 """
 from __future__ import annotations
 
@@ -54,6 +56,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-micro", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="3D configs: run the z-slab sharded NKS step (ShardedSolver, NCCL halos/allreduces); "
+                         "implied for 3D configs at N > 1")
     return ap.parse_args()
 
 
@@ -194,7 +199,7 @@ def run_reference(args, world, rank, pg):
     print(json.dumps(line), flush=True)
 
 
-def config_dict(cfg, ngpus):
+def config_dict(cfg, ngpus, sharded=False):
     d = len(cfg["shape"])
     return {"workload": f"config {2 if cfg['name'] == '2d_512' else cfg['name']}: {cfg['name']} "
                         f"{'x'.join(map(str, cfg['shape']))} periodic, adaptive dt (P:596-607), "
@@ -202,7 +207,8 @@ def config_dict(cfg, ngpus):
             "grid": list(cfg["shape"]), "dof": (2 + d) * int(np.prod(cfg["shape"])),
             "nsub": list(cfg["nsub"]), "overlap": cfg["overlap"], "newton_rtol": 1e-11, "gmres_rtol": 1e-10,
             "init": "c=0.1622+U(-0.005,0.005), eta=0.1+U(-0.01,0.01), seed 0, u0=FFT equilibrium",
-            "parallelism": "replicas" if ngpus > 1 else "1 GPU",
+            "parallelism": (f"z-slabs x {ngpus} (sharded NKS step, NCCL halo exchange + allreduce)" if sharded
+                            else ("replicas" if ngpus > 1 else "1 GPU")),
             "l2": "working set > 126 MB L2 (BILU factors ~0.46 GB + Krylov basis ~0.26 GB); no flush"}
 
 
@@ -317,9 +323,18 @@ def run_gpu(args, world, rank, local, pg):
     nf = 2 + d
     N = int(np.prod(shape))
     model, sol = ni.model_default(), ni.solver_default()
-    g = Solver(shape, model, sol, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"], pc_reuse=1)
+    sharded = d == 3 and (world > 1 or args.sharded)
     c, eta = ni.initial_fields(shape, 0)
-    g.set_fields(c, eta, None)
+    if sharded:
+        # one z-slab per rank; the library calls back for halo exchanges and fixed-order allreduces
+        from paper_2209_08001_b200.shard import ShardedSolver
+        sh = ShardedSolver(shape, model, sol, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"], pc_reuse=1)
+        sh.set_fields(c, eta)
+        g = sh.solver
+    else:
+        sh = None
+        g = Solver(shape, model, sol, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"], pc_reuse=1)
+        g.set_fields(c, eta, None)
     recs = []
     for _ in range(args.warmup):
         recs += g.run_adaptive(1)
@@ -347,7 +362,8 @@ def run_gpu(args, world, rank, local, pg):
     g.set_profiling(False)
     t_max = max_over_ranks(pg, t_ms)
     ms_per_step = t_max / args.steps
-    value = world * args.steps / (t_max / 1e3)
+    # sharded: all ranks advance ONE global grid (strong scaling); replicas: world independent runs
+    value = (1 if sharded else world) * args.steps / (t_max / 1e3)
 
     # ---- roofline of the dominant kernel (phase with the largest share of the timed region)
     dom = max(phases, key=lambda k: phases[k]["ms"])
@@ -386,7 +402,7 @@ def run_gpu(args, world, rank, local, pg):
     # (nks_set_state, on_device = 0: keeps the controller's history), advances one adaptive step
     # (nks_run_adaptive, retries included, exactly the device leg's work) and downloads X^{n+1}
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not sharded:
         import ctypes as C
         from paper_2209_08001_b200.nks import StepInfo
         g2 = Solver(shape, model, sol, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"], pc_reuse=1)
@@ -426,15 +442,16 @@ def run_gpu(args, world, rank, local, pg):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = oracle_sample(cfg)
 
-    sharded = None
+    micro_sh = None
     if world > 1 and not args.no_micro:
         del g
         torch.cuda.empty_cache()
         try:
-            sharded = {"grid": [512, 512, 512], "sharding": f"z-slabs x {world}", **micro_sharded((512, 512, 512), pg)}
+            micro_sh = {"grid": [512, 512, 512], "sharding": f"z-slabs x {world}", **micro_sharded((512, 512, 512), pg)}
         except Exception as e:
-            sharded = {"error": str(e)[:200]}
+            micro_sh = {"error": str(e)[:200]}
         g = None
+        sh = None
     micro = {}
     if not args.no_micro and world == 1:
         del g
@@ -463,10 +480,10 @@ def run_gpu(args, world, rank, local, pg):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": config_dict(cfg, world), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config_dict(cfg, world, sharded), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks,
-                "kernels": kern, "kernels_micro": micro, "kernels_micro_sharded": sharded,
+                "kernels": kern, "kernels_micro": micro, "kernels_micro_sharded": micro_sh,
                 "phases_ms": {k: round(v["ms"], 3) for k, v in phases.items()},
                 "solver": {"newton_its": [r["newton_its"] for r in timed], "gmres_its": [r["gmres_its"] for r in timed],
                            "dt": [r["dt"] for r in timed], "retries": [r["retries"] for r in timed],
