@@ -104,26 +104,44 @@ __global__ void k_update_scale(long long n, int nk, const double* __restrict__ V
 // w = (w - sum_k h2[k] V_k) / nrm with nrm = sqrt(max(ww - sum_k h2[k]^2, 0)) computed on the device from
 // the re-orthogonalisation dots (h2 = hv[0..nk), ww = hv[nk]) in the same order as the host's copy, so
 // the host (one iteration behind) and the device agree on the value and on breakdown (nrm <= 1e-300).
-template <int NK>
+template <int NK, int VW>
 __global__ void k_update_scale_dev(long long n, int nk, const double* __restrict__ V, long long ld,
                                    const double* __restrict__ hv, double* __restrict__ w) {
   __shared__ double sh[NK];
   __shared__ double s_scale;
   if (threadIdx.x < nk) sh[threadIdx.x] = hv[threadIdx.x];
-  if (threadIdx.x == 0) {
-    double h2sq = 0.0;
-    for (int k = 0; k < nk; ++k) h2sq += hv[k] * hv[k];
-    const double nrm = sqrt(fmax(hv[nk] - h2sq, 0.0));
-    s_scale = nrm > 1e-300 ? 1.0 / nrm : 0.0;
+  if (threadIdx.x < 32) {            // sum_k h2[k]^2 in the host's order: lane 0 adds the lane partials in order
+    double part = 0.0;
+    if (threadIdx.x == 0)
+      for (int k = 0; k < nk; ++k) part += hv[k] * hv[k];
+    if (threadIdx.x == 0) {
+      const double nrm = sqrt(fmax(hv[nk] - part, 0.0));
+      s_scale = nrm > 1e-300 ? 1.0 / nrm : 0.0;
+    }
   }
   __syncthreads();
   const double scale = s_scale;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    double wi = w[i];
+  const long long m = n / VW;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < m; t += (long long)gridDim.x * blockDim.x) {
+    if (VW == 2) {
+      double2 wi = reinterpret_cast<double2*>(w)[t];
 #pragma unroll
-    for (int k = 0; k < NK; ++k)
-      if (k < nk) wi = fma(-sh[k], __ldg(V + k * ld + i), wi);
-    w[i] = wi * scale;
+      for (int k = 0; k < NK; ++k)
+        if (k < nk) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(V + k * ld) + t);
+          wi.x = fma(-sh[k], v.x, wi.x);
+          wi.y = fma(-sh[k], v.y, wi.y);
+        }
+      wi.x *= scale;
+      wi.y *= scale;
+      reinterpret_cast<double2*>(w)[t] = wi;
+    } else {
+      double wi = w[t];
+#pragma unroll
+      for (int k = 0; k < NK; ++k)
+        if (k < nk) wi = fma(-sh[k], __ldg(V + k * ld + t), wi);
+      w[t] = wi * scale;
+    }
   }
 }
 
@@ -186,7 +204,10 @@ __device__ __forceinline__ void block_partials_32(double (&acc)[32], double* __r
   }
 }
 
-// out[k] = V_k . w (k < nk), out[nk] = w . w, out[nk+1..31] = 0
+// out[k] = V_k . w (k < nk), out[nk] = w . w, out[nk+1..31] = 0.  VW = 2: 16-byte loads (n even), which
+// doubles the contiguous run per column and warp -- 1D streams over 30 columns reach ~85 % of HBM with
+// 16-byte loads against ~60 % with 8-byte ones (tools/cgs_probe.cu).
+template <int NK, int VW>
 __global__ void __launch_bounds__(kRedThreads, 2) k_cgs_dot(long long n, int nk, const double* __restrict__ V, long long ld,
                                                        const double* __restrict__ w, double* __restrict__ part,
                                                        double* __restrict__ out, unsigned* __restrict__ counter) {
@@ -194,25 +215,39 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_cgs_dot(long long n, int nk,
 #pragma unroll
   for (int k = 0; k < 32; ++k) acc[k] = 0.0;
   double ww = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const double wi = w[i];
+  const long long m = n / VW;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < m; t += (long long)gridDim.x * blockDim.x) {
+    if (VW == 2) {
+      const double2 wi = reinterpret_cast<const double2*>(w)[t];
 #pragma unroll
-    for (int k = 0; k < 31; ++k) {
-      const double vk = k < nk ? __ldg(V + k * ld + i) : 0.0;
-      acc[k] = fma(vk, wi, acc[k]);
+      for (int k = 0; k < (NK < 31 ? NK : 31); ++k)
+        if (k < nk) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(V + k * ld) + t);
+          acc[k] = fma(v.x, wi.x, fma(v.y, wi.y, acc[k]));
+        }
+      ww = fma(wi.x, wi.x, fma(wi.y, wi.y, ww));
+    } else {
+      const double wi = w[t];
+#pragma unroll
+      for (int k = 0; k < (NK < 31 ? NK : 31); ++k) {
+        const double vk = k < nk ? __ldg(V + k * ld + t) : 0.0;
+        acc[k] = fma(vk, wi, acc[k]);
+      }
+      ww = fma(wi, wi, ww);
     }
-    ww = fma(wi, wi, ww);
   }
 #pragma unroll
   for (int k = 0; k < 32; ++k) acc[k] = k == nk ? ww : acc[k];
   block_partials_32(acc, part, out, counter);
 }
 
-// w <- w - sum_k h[k] V_k ; out[k] = V_k . w_new (k < nk), out[nk] = w_new . w_new
-__global__ void __launch_bounds__(kRedThreads) k_cgs_update_dot(long long n, int nk, const double* __restrict__ V,
-                                                              long long ld, const double* __restrict__ h,
-                                                              double* __restrict__ w, double* __restrict__ part,
-                                                              double* __restrict__ out, unsigned* __restrict__ counter) {
+// w <- w - sum_k h[k] V_k ; out[k] = V_k . w_new (k < nk), out[nk] = w_new . w_new.  The columns are
+// read twice (the second pass mostly from L1/L2) so that only the 32 accumulators live in registers.
+template <int NK, int VW>
+__global__ void __launch_bounds__(kRedThreads, NK <= 16 ? 2 : 1) k_cgs_update_dot(long long n, int nk, const double* __restrict__ V,
+                                                                 long long ld, const double* __restrict__ h,
+                                                                 double* __restrict__ w, double* __restrict__ part,
+                                                                 double* __restrict__ out, unsigned* __restrict__ counter) {
   __shared__ double sh[32];
   if (threadIdx.x < 32) sh[threadIdx.x] = threadIdx.x < nk ? h[threadIdx.x] : 0.0;
   __syncthreads();
@@ -220,18 +255,36 @@ __global__ void __launch_bounds__(kRedThreads) k_cgs_update_dot(long long n, int
 #pragma unroll
   for (int k = 0; k < 32; ++k) acc[k] = 0.0;
   double ww = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    double vk[31];
-    double wi = w[i];
+  const long long m = n / VW;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < m; t += (long long)gridDim.x * blockDim.x) {
+    if (VW == 2) {
+      double2 wi = reinterpret_cast<double2*>(w)[t];
 #pragma unroll
-    for (int k = 0; k < 31; ++k) {
-      vk[k] = k < nk ? __ldg(V + k * ld + i) : 0.0;
-      wi = fma(-sh[k], vk[k], wi);
+      for (int k = 0; k < (NK < 31 ? NK : 31); ++k)
+        if (k < nk) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(V + k * ld) + t);
+          wi.x = fma(-sh[k], v.x, wi.x);
+          wi.y = fma(-sh[k], v.y, wi.y);
+        }
+      reinterpret_cast<double2*>(w)[t] = wi;
+#pragma unroll
+      for (int k = 0; k < (NK < 31 ? NK : 31); ++k)
+        if (k < nk) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(V + k * ld) + t);
+          acc[k] = fma(v.x, wi.x, fma(v.y, wi.y, acc[k]));
+        }
+      ww = fma(wi.x, wi.x, fma(wi.y, wi.y, ww));
+    } else {
+      double wi = w[t];
+#pragma unroll
+      for (int k = 0; k < (NK < 31 ? NK : 31); ++k)
+        if (k < nk) wi = fma(-sh[k], __ldg(V + k * ld + t), wi);
+      w[t] = wi;
+#pragma unroll
+      for (int k = 0; k < (NK < 31 ? NK : 31); ++k)
+        if (k < nk) acc[k] = fma(__ldg(V + k * ld + t), wi, acc[k]);
+      ww = fma(wi, wi, ww);
     }
-    w[i] = wi;
-#pragma unroll
-    for (int k = 0; k < 31; ++k) acc[k] = fma(vk[k], wi, acc[k]);
-    ww = fma(wi, wi, ww);
   }
 #pragma unroll
   for (int k = 0; k < 32; ++k) acc[k] = k == nk ? ww : acc[k];
@@ -307,20 +360,47 @@ void launch_update_scale(long long n, int nk, const double* V, long long ld, con
 
 static int cgs_blocks(long long n) { return (int)std::min<long long>((n + kRedThreads - 1) / kRedThreads, 148 * 2); }
 
+// 16-byte columns need an even length and leading dimension (every real grid has an even N)
+static bool vec2(long long n, long long ld) { return (n % 2) == 0 && (ld % 2) == 0; }
+
 void launch_cgs_dot(long long n, int nk, const double* V, long long ld, const double* w, double* part, double* out,
                     unsigned* counter, cudaStream_t s) {
-  k_cgs_dot<<<cgs_blocks(n), kRedThreads, 0, s>>>(n, nk, V, ld, w, part, out, counter);
+  // the unrolled column loop is as long as the template NK (8, 16 or 31 live columns), not always 31
+  if (vec2(n, ld)) {
+    if (nk <= 8) k_cgs_dot<8, 2><<<cgs_blocks(n / 2), kRedThreads, 0, s>>>(n, nk, V, ld, w, part, out, counter);
+    else if (nk <= 16) k_cgs_dot<16, 2><<<cgs_blocks(n / 2), kRedThreads, 0, s>>>(n, nk, V, ld, w, part, out, counter);
+    else k_cgs_dot<32, 2><<<cgs_blocks(n / 2), kRedThreads, 0, s>>>(n, nk, V, ld, w, part, out, counter);
+  } else {
+    k_cgs_dot<32, 1><<<cgs_blocks(n), kRedThreads, 0, s>>>(n, nk, V, ld, w, part, out, counter);
+  }
 }
 
 void launch_cgs_update_dot(long long n, int nk, const double* V, long long ld, const double* h, double* w, double* part,
                            double* out, unsigned* counter, cudaStream_t s) {
-  k_cgs_update_dot<<<(int)std::min<long long>((n + kRedThreads - 1) / kRedThreads, 148), kRedThreads, 0, s>>>(
-      n, nk, V, ld, h, w, part, out, counter);
+  // one 256-thread block per SM: the 32 accumulators + the second column pass need > 128 registers
+  const int nb1 = (int)std::min<long long>((n + kRedThreads - 1) / kRedThreads, 148);
+  const int nb2 = cgs_blocks(vec2(n, ld) ? n / 2 : n);
+  if (vec2(n, ld)) {
+    if (nk <= 8) k_cgs_update_dot<8, 2><<<nb2, kRedThreads, 0, s>>>(n, nk, V, ld, h, w, part, out, counter);
+    else if (nk <= 16) k_cgs_update_dot<16, 2><<<nb2, kRedThreads, 0, s>>>(n, nk, V, ld, h, w, part, out, counter);
+    else k_cgs_update_dot<32, 2><<<nb1, kRedThreads, 0, s>>>(n, nk, V, ld, h, w, part, out, counter);
+  } else {
+    k_cgs_update_dot<32, 1><<<nb1, kRedThreads, 0, s>>>(n, nk, V, ld, h, w, part, out, counter);
+  }
 }
+
+#define NK_DISPATCH2(nk, VW, KERNEL, ...)                      \
+  do {                                                         \
+    if ((nk) <= 8) KERNEL<8, VW>__VA_ARGS__;                   \
+    else if ((nk) <= 16) KERNEL<16, VW>__VA_ARGS__;            \
+    else if ((nk) <= 32) KERNEL<32, VW>__VA_ARGS__;            \
+    else KERNEL<64, VW>__VA_ARGS__;                            \
+  } while (0)
 
 void launch_update_scale_dev(long long n, int nk, const double* V, long long ld, const double* hv, double* w,
                              cudaStream_t s) {
-  NK_DISPATCH(nk, k_update_scale_dev, <<<vec_blocks(n), 256, 0, s>>>(n, nk, V, ld, hv, w));
+  if (vec2(n, ld)) NK_DISPATCH2(nk, 2, k_update_scale_dev, <<<vec_blocks(n / 2), 256, 0, s>>>(n, nk, V, ld, hv, w));
+  else NK_DISPATCH2(nk, 1, k_update_scale_dev, <<<vec_blocks(n), 256, 0, s>>>(n, nk, V, ld, hv, w));
 }
 
 void launch_lincomb(long long n, int nk, const double* V, long long ld, const double* y, double* out, cudaStream_t s) {
