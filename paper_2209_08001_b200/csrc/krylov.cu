@@ -241,6 +241,78 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_cgs_dot(long long n, int nk,
   block_partials_32(acc, part, out, counter);
 }
 
+// Column-split variant of k_cgs_dot (16-byte loads, n even): the 8 warps of a block walk the same
+// 32-element-pair tiles and warp q owns columns q, q+8, q+16, q+24, so a thread keeps <= 4 accumulators,
+// occupancy is high and every column is read in 512-byte runs.  Block sums of each column go to
+// part[block][32]; the last block to finish adds them in block order (deterministic).
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int NK>
+__global__ void __launch_bounds__(256) k_cgs_dot_cs(long long n, int nk, const double* __restrict__ V, long long ld,
+                                                  const double* __restrict__ w, double* __restrict__ part,
+                                                  double* __restrict__ out, unsigned* __restrict__ counter) {
+  constexpr int CPW = NK / 8;
+  __shared__ double cs[32];
+  __shared__ double sw[8][32];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double acc[CPW];
+#pragma unroll
+  for (int q = 0; q < CPW; ++q) acc[q] = 0.0;
+  double ww = 0.0;
+  const long long m = n / 2;
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  for (long long t = blockIdx.x * 32LL + lane; t < m; t += (long long)gridDim.x * 32) {
+    const double2 wv = w2[t];
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) {
+      const int k = wid + 8 * q;
+      if (k < nk) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(V + k * ld) + t);
+        acc[q] = fma(v.x, wv.x, fma(v.y, wv.y, acc[q]));
+      }
+    }
+    if (wid == 0) ww = fma(wv.x, wv.x, fma(wv.y, wv.y, ww));
+  }
+  if (threadIdx.x < 32) cs[threadIdx.x] = 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < CPW; ++q) {
+    const int k = wid + 8 * q;
+    const double v = warp_sum(acc[q]);
+    if (lane == 0 && k < nk) cs[k] = v;
+  }
+  if (wid == 0) {
+    const double v = warp_sum(ww);
+    if (lane == 0) cs[nk] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    part[blockIdx.x * 32 + threadIdx.x] = cs[threadIdx.x];
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double a = 0.0;
+  for (int blk = wid; blk < (int)gridDim.x; blk += 8) a += part[blk * 32 + lane];
+  sw[wid][lane] = a;
+  __syncthreads();
+  if (wid == 0) {
+    double tsum = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tsum += sw[k][lane];
+    out[lane] = tsum;
+    if (lane == 0) *counter = 0u;
+  }
+}
+
 // w <- w - sum_k h[k] V_k ; out[k] = V_k . w_new (k < nk), out[nk] = w_new . w_new.  The columns are
 // read twice (the second pass mostly from L1/L2) so that only the 32 accumulators live in registers.
 template <int NK, int VW>
@@ -367,8 +439,11 @@ void launch_cgs_dot(long long n, int nk, const double* V, long long ld, const do
                     unsigned* counter, cudaStream_t s) {
   // the unrolled column loop is as long as the template NK (8, 16 or 31 live columns), not always 31
   if (vec2(n, ld)) {
-    if (nk <= 8) k_cgs_dot<8, 2><<<cgs_blocks(n / 2), kRedThreads, 0, s>>>(n, nk, V, ld, w, part, out, counter);
-    else if (nk <= 16) k_cgs_dot<16, 2><<<cgs_blocks(n / 2), kRedThreads, 0, s>>>(n, nk, V, ld, w, part, out, counter);
+    // column-split kernel; blocks <= kRedBlocks (the partials buffer holds kRedBlocks x 32)
+    const int nbc = (int)std::min<long long>((n / 2 + 31) / 32, kRedBlocks);
+    // measured at config 2: column split wins up to 15 columns, the register-resident kernel above
+    if (nk <= 7) k_cgs_dot_cs<8><<<nbc, 256, 0, s>>>(n, nk, V, ld, w, part, out, counter);
+    else if (nk <= 15) k_cgs_dot_cs<16><<<nbc, 256, 0, s>>>(n, nk, V, ld, w, part, out, counter);
     else k_cgs_dot<32, 2><<<cgs_blocks(n / 2), kRedThreads, 0, s>>>(n, nk, V, ld, w, part, out, counter);
   } else {
     k_cgs_dot<32, 1><<<cgs_blocks(n), kRedThreads, 0, s>>>(n, nk, V, ld, w, part, out, counter);
