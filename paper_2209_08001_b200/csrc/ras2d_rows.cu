@@ -632,7 +632,7 @@ __global__ void __launch_bounds__(160, 1) k_apply_ld(Args A) {
     // ================================================================ halo gatekeeper
     // lane l checks double l & 3 of one of three cells; the step barrier then hands the cells over
     auto poll3 = [&](bool on, int q0_, int c0_, int q1_, int c1_, int q2_, int c2_) {
-      if (!on || (A.dbg & 1)) return;
+      if (!on || (A.dbg & 17)) return;
       const int which = min(lane >> 2, 2);
       const int qq = which == 0 ? q0_ : (which == 1 ? q1_ : q2_);
       const int cc = which == 0 ? c0_ : (which == 1 ? c1_ : c2_);
@@ -686,7 +686,7 @@ __global__ void __launch_bounds__(160, 1) k_apply_ld(Args A) {
     // issue the copies of processing step p (forward k = p, backward k = 2 nFp - 1 - p): row c of
     // each block of this lane's row, if the row is active at that step; always one commit group
     auto issue = [&](int p) {
-      if (p < 2 * nFp) {
+      if (p < 2 * nFp && !(A.dbg & 2)) {
         const bool fw = p < nFp;
         const int k = fw ? p : 2 * nFp - 1 - p;
         const int lo = lo_of(k, ex, R), hi = hi_of(k, R);
@@ -779,8 +779,8 @@ __global__ void __launch_bounds__(160, 1) k_apply_ld(Args A) {
         const double c1 = dot4(M1, Ya1, 0.0);
         pre = b0 + b1;
         half = c0 + c1;
-        ybuf[(size_t)k * 128] = y;
-        st_remote1_if(dn_remote && active && rl >= R - 2, hcell(min(max(rl - (R - 2), 0), 1), i) + c,
+        if (!(A.dbg & 4)) ybuf[(size_t)k * 128] = y;
+        st_remote1_if(!(A.dbg & 4) && dn_remote && active && rl >= R - 2, hcell(min(max(rl - (R - 2), 0), 1), i) + c,
                       (unsigned)min(s + 1, CS - 1), y);
         issue(k + kLD);                                               // slot of step k is free now
       };
@@ -860,8 +860,8 @@ __global__ void __launch_bounds__(160, 1) k_apply_ld(Args A) {
         E[((k & 7) * 32 + rl) * 4 + c] = x;
         pre = b0 + b1;
         half = c0 + c1;
-        st_global_if(active && own_row && i >= G.ox0 && i < G.ox0 + G.ownx, zrow + gx_of(min(max(i, 0), ex - 1)), x);
-        st_remote1_if(up_remote && active && rl < 2, hcell(2 + min(rl, 1), i) + c, (unsigned)max(s - 1, 0), x);
+        st_global_if(!(A.dbg & 4) && active && own_row && i >= G.ox0 && i < G.ox0 + G.ownx, zrow + gx_of(min(max(i, 0), ex - 1)), x);
+        st_remote1_if(!(A.dbg & 4) && up_remote && active && rl < 2, hcell(2 + min(rl, 1), i) + c, (unsigned)max(s - 1, 0), x);
         issue(p + kLD);
       };
       for (int kb0 = 0; kb0 < nFp; kb0 += 4) {
