@@ -56,8 +56,14 @@ enum { NKS_REASON_NONE = 0, NKS_REASON_NEWTON_MAXIT = 1, NKS_REASON_LINE_SEARCH 
        NKS_REASON_GMRES_MAXIT = 3, NKS_REASON_DOMAIN = 4, NKS_REASON_DT_FLOOR = 5,
        NKS_REASON_GMRES_STAGNATION = 6 /* 3 restart cycles each removing < 0.1 % of the residual */ };
 
-/* Preconditioner types. */
-enum { NKS_PC_NONE = 0, NKS_PC_RAS_BILU0 = 2 };
+/* Preconditioner types (the variants are SURVEY 8(f)-1's Schwarz family, Cai-Sarkis):
+ *   RAS    z = sum_i R_i^{0T} (L_i U_i)^{-1} R_i^delta r     (left restricted additive Schwarz, default)
+ *   AS     z = sum_i R_i^{deltaT} (L_i U_i)^{-1} R_i^delta r (classical additive Schwarz)
+ *   RRAS   z = sum_i R_i^{deltaT} (L_i U_i)^{-1} R_i^0 r     (right-restricted: input restricted to owned points)
+ * AS and RRAS sum the overlapping boxes' contributions in a fixed box order (deterministic); they are
+ * single-state only (a z-slab state would need a reverse halo exchange) and use the level-synchronous
+ * subdomain solve. */
+enum { NKS_PC_NONE = 0, NKS_PC_RAS_BILU0 = 2, NKS_PC_AS_BILU0 = 3, NKS_PC_RRAS_BILU0 = 4 };
 
 typedef struct {
   int32_t dim;       /* 2 or 3                                                          */
@@ -105,7 +111,7 @@ typedef struct {
   int32_t newton_maxit;              /* > this many Newton iterations -> DIVERGED             */
   int32_t gmres_restart;             /* GMRES(m) restart length, 1..64                        */
   int32_t gmres_maxit;               /* total GMRES iterations per Newton solve -> DIVERGED    */
-  int32_t pc_type;                   /* NKS_PC_NONE or NKS_PC_RAS_BILU0                       */
+  int32_t pc_type;                   /* NKS_PC_NONE, NKS_PC_RAS_BILU0, _AS_BILU0, _RRAS_BILU0 */
   int32_t pc_reuse;                  /* 0: refactor every Newton iterate; 1: once per step;    */
                                      /* 2: keep factors across steps while dt is unchanged     */
   double ls_alpha;                   /* sufficient decrease ||F(X+lS)|| <= (1-alpha l)||F||    */

@@ -147,9 +147,17 @@ def is_owned(box, l):
 
 
 class RAS:
-    """Left-RAS preconditioner with BILU(0) (or exact LU, ``exact=True``) subdomain solves."""
+    """Schwarz preconditioner with BILU(0) (or exact LU, ``exact=True``) subdomain solves.
 
-    def __init__(self, J, shape, nf, nsub, delta, exact: bool = False):
+    variant (Cai-Sarkis):
+      "ras"  z = sum_i R_i^{0T} A_i^{-1} R_i^delta r      left restricted additive Schwarz
+      "as"   z = sum_i R_i^{deltaT} A_i^{-1} R_i^delta r  classical additive Schwarz
+      "rras" z = sum_i R_i^{deltaT} A_i^{-1} R_i^0 r      right-restricted (input restricted to owned points)
+    """
+
+    def __init__(self, J, shape, nf, nsub, delta, exact: bool = False, variant: str = "ras"):
+        assert variant in ("ras", "as", "rras")
+        self.variant = variant
         self.shape = shape
         self.nf = nf
         self.npts = int(np.prod(shape))
@@ -178,11 +186,18 @@ class RAS:
         for b, (kind, fac, pts) in zip(self.boxes, self.fact):
             gidx = [global_index(b, l) for l in pts]
             rl = rf[:, gidx].T.copy()                  # R_i^delta r   (npts_box, nf)
+            if self.variant == "rras":                 # R_i^0 r: zero on the overlap
+                for p, l in enumerate(pts):
+                    if not is_owned(b, l):
+                        rl[p] = 0.0
             if kind == "lu":
                 xl = np.linalg.solve(fac, rl.ravel()).reshape(len(pts), nf)
             else:
                 xl = lu_solve(fac[0], fac[1], rl, len(pts))
-            for p, l in enumerate(pts):                # R_i^{0T}: owned points only
-                if is_owned(b, l):
-                    z[:, gidx[p]] = xl[p]
+            for p, l in enumerate(pts):
+                if self.variant == "ras":              # R_i^{0T}: owned points only
+                    if is_owned(b, l):
+                        z[:, gidx[p]] = xl[p]
+                else:                                  # R_i^{deltaT}: every box point adds its value
+                    z[:, gidx[p]] += xl[p]
         return z.reshape(r.shape)

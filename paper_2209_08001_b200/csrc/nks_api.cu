@@ -99,6 +99,7 @@ struct Layout {
   size_t off_X[7];
   size_t off_Ta, off_jac4, off_V, off_Z, off_W2, off_part, off_out;
   size_t off_fac, off_fac32, off_ybox, off_gidx, off_nbr, off_levoff, off_levptr, off_posoff, off_geo;
+  size_t off_cover_off, off_cover_pos;
   size_t total;
   long long P, ld;
   size_t geo_bytes;
@@ -117,17 +118,21 @@ const char* validate(const nks_grid* g, const nks_params* p) {
   if (p->S < 1 || p->S > kMaxS) return "S must be in 1..16";
   if (p->gmres_restart < 1 || p->gmres_restart > 60) return "gmres_restart must be in 1..60";
   if (p->newton_maxit < 0 || p->gmres_maxit < 1) return "bad iteration limits";
-  if (p->pc_type != NKS_PC_NONE && p->pc_type != NKS_PC_RAS_BILU0) return "unknown pc_type";
+  if (p->pc_type != NKS_PC_NONE && p->pc_type != NKS_PC_RAS_BILU0 && p->pc_type != NKS_PC_AS_BILU0 &&
+      p->pc_type != NKS_PC_RRAS_BILU0)
+    return "unknown pc_type";
+  if (g->zghost > 0 && (p->pc_type == NKS_PC_AS_BILU0 || p->pc_type == NKS_PC_RRAS_BILU0))
+    return "z-slab states support pc_type NONE or RAS (AS / RRAS need a reverse halo exchange)";
   if (g->zghost != 0 && (g->zghost < 2 || g->zghost > 8)) return "zghost must be 0 or 2..8";
   if (g->zghost > 0) {
     if (g->dim != 3) return "z-slab states (zghost > 0) are 3D";
     if (g->n[2] - 2 * g->zghost < 2) return "a z-slab must own at least 2 planes";
-    if (p->pc_type == NKS_PC_RAS_BILU0 && g->overlap + 1 > g->zghost)
+    if (p->pc_type != NKS_PC_NONE && g->overlap + 1 > g->zghost)
       return "z-slab with RAS needs zghost >= overlap + 1 (assembly reads one cell beyond the box)";
-    if (p->pc_type == NKS_PC_RAS_BILU0 && (g->nsub[2] < 1 || g->nsub[2] > g->n[2] - 2 * g->zghost))
+    if (p->pc_type != NKS_PC_NONE && (g->nsub[2] < 1 || g->nsub[2] > g->n[2] - 2 * g->zghost))
       return "z-slab: nsub[2] must be in 1..own planes";
   }
-  if (p->pc_type == NKS_PC_RAS_BILU0) {
+  if (p->pc_type != NKS_PC_NONE) {
     for (int j = 0; j < 3; ++j)
       if (g->nsub[j] < 1 || g->nsub[j] > g->n[j]) return "nsub[j] must be in 1..n[j]";
     if (g->dim == 2 && g->nsub[2] != 1) return "nsub[2] must be 1 in 2D";
@@ -152,7 +157,7 @@ Layout make_layout(const nks_grid& g, const nks_params& p) {
   L.off_part = o; o = align256(o + (size_t)kRedBlocks * 80 * sizeof(double));
   L.off_out = o; o = align256(o + 256 * sizeof(double));
   L.P = 0;
-  if (p.pc_type == NKS_PC_RAS_BILU0) {
+  if (p.pc_type != NKS_PC_NONE) {
     const int nslots = d == 2 ? 13 : 25;
     L.nslots = nslots;
     L.nbox = g.nsub[0] * g.nsub[1] * g.nsub[2];
@@ -176,6 +181,9 @@ Layout make_layout(const nks_grid& g, const nks_params& p) {
     L.off_levoff = o; o = align256(o + (size_t)(L.nbox + 1) * sizeof(int));
     L.off_levptr = o; o = align256(o + (size_t)nl * sizeof(int));
     L.off_posoff = o; o = align256(o + (size_t)(L.nbox + 1) * sizeof(int));
+    const bool cover = p.pc_type == NKS_PC_AS_BILU0 || p.pc_type == NKS_PC_RRAS_BILU0;
+    L.off_cover_off = o; o = align256(o + (cover ? (size_t)(N + 1) * sizeof(int) : 0));
+    L.off_cover_pos = o; o = align256(o + (cover ? (size_t)L.P * sizeof(int) : 0));
     // one of the two pipelined 2D applies uses this slice (ras2d_rows.cu by default)
     L.geo_bytes = d == 2 ? std::max(ras2d_workspace_bytes(g), r2::workspace_bytes(g)) : 0;
     L.off_geo = o; o = align256(o + L.geo_bytes);
@@ -755,7 +763,7 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
     CK(cudaMallocHost(&st->h_red, 256 * sizeof(double)));
     CK(cudaMallocHost(&st->h_ring, 4 * 128 * sizeof(double)));
     for (int k = 0; k < 4; ++k) CK(cudaEventCreateWithFlags(&st->gm_ev[k], cudaEventDisableTiming));
-    if (params->pc_type == NKS_PC_RAS_BILU0) {
+    if (params->pc_type != NKS_PC_NONE) {
       BoxSet& B = st->boxes;
       build_slot_tables(grid->dim, B);
       HostBoxes H = build_boxes_host(*grid, B);
@@ -782,8 +790,29 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
       CK(cudaMemcpyAsync(B.lev_ptr, H.lev_ptr.data(), H.lev_ptr.size() * sizeof(int), cudaMemcpyHostToDevice, st->stream));
       CK(cudaMemcpyAsync(B.box_pos_off, H.box_pos_off.data(), H.box_pos_off.size() * sizeof(int), cudaMemcpyHostToDevice,
                          st->stream));
+      B.variant = params->pc_type == NKS_PC_AS_BILU0 ? 1 : (params->pc_type == NKS_PC_RRAS_BILU0 ? 2 : 0);
+      std::vector<int> cov_off, cov_pos;
+      if (B.variant != 0) {        // CSR of the box positions covering every grid point, increasing position
+        const long long Np = st->N;
+        cov_off.assign(Np + 1, 0);
+        for (long long q = 0; q < H.P; ++q) {
+          const int gi = H.gidx[q] >= 0 ? H.gidx[q] : ~H.gidx[q];
+          cov_off[gi + 1]++;
+        }
+        for (long long i = 0; i < Np; ++i) cov_off[i + 1] += cov_off[i];
+        cov_pos.assign(H.P, 0);
+        std::vector<int> fill(cov_off.begin(), cov_off.end() - 1);
+        for (long long q = 0; q < H.P; ++q) {
+          const int gi = H.gidx[q] >= 0 ? H.gidx[q] : ~H.gidx[q];
+          cov_pos[fill[gi]++] = (int)q;
+        }
+        B.cover_off = (int*)(w + L.off_cover_off);
+        B.cover_pos = (int*)(w + L.off_cover_pos);
+        CK(cudaMemcpyAsync(B.cover_off, cov_off.data(), cov_off.size() * sizeof(int), cudaMemcpyHostToDevice, st->stream));
+        CK(cudaMemcpyAsync(B.cover_pos, cov_pos.data(), cov_pos.size() * sizeof(int), cudaMemcpyHostToDevice, st->stream));
+      }
       CK(cudaStreamSynchronize(st->stream));
-      if (grid->dim == 2 && std::getenv("NKS_RAS_LEVEL") == nullptr) {
+      if (grid->dim == 2 && B.variant == 0 && std::getenv("NKS_RAS_LEVEL") == nullptr) {
         std::string why;
         // one lane per row (ras2d_rows.cu); NKS_RAS2D_OLD selects the 4-lanes-per-row design (ras2d.cu)
         if (std::getenv("NKS_RAS2D_OLD") == nullptr) {

@@ -52,6 +52,9 @@ struct BoxSet {
   int* box_lev_off = nullptr;   // [nbox+1] offset into lev_ptr
   int* lev_ptr = nullptr;       // concatenated per-box level pointers (absolute positions)
   int* box_pos_off = nullptr;   // [nbox+1]
+  int* cover_off = nullptr;     // AS / RRAS: [N+1] CSR of the box positions covering each grid point
+  int* cover_pos = nullptr;     // [P] positions, increasing (fixed summation order)
+  int variant = 0;              // 0 RAS, 1 AS, 2 RRAS
   // host copies
   std::vector<int> h_box_lev_off, h_box_pos_off;
   // slot tables (host, copied into kernel params)

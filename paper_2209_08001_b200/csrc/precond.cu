@@ -399,15 +399,16 @@ __global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const in
                             const int* __restrict__ box_lev_off, const int* __restrict__ lev_ptr,
                             const int* __restrict__ box_pos_off, long long Ptot, long long ld, long long N,
                             const FT* __restrict__ fac, const double* __restrict__ r, double* y,
-                            double* __restrict__ z) {
+                            double* __restrict__ z, int variant) {
   const int b = blockIdx.x;
   const int q0 = box_pos_off[b], q1 = box_pos_off[b + 1];
-  // R_i^delta r
+  // R_i^delta r (RAS, AS) or R_i^0 r (RRAS: the overlap points read zero)
   for (int pos = q0 + threadIdx.x; pos < q1; pos += blockDim.x) {
     int gi = gidx[pos];
+    const bool owned = gi >= 0;
     if (gi < 0) gi = ~gi;
 #pragma unroll
-    for (int f = 0; f < NF; ++f) y[f * Ptot + pos] = r[f * N + gi];
+    for (int f = 0; f < NF; ++f) y[f * Ptot + pos] = (variant == 2 && !owned) ? 0.0 : r[f * N + gi];
   }
   __syncthreads();
   const int l0 = box_lev_off[b], l1 = box_lev_off[b + 1] - 1;
@@ -478,12 +479,27 @@ __global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const in
     }
     __syncthreads();
   }
-  // R_i^{0T}: owned points only
+  // R_i^{0T}: owned points only (RAS); AS / RRAS keep the box solutions in y for k_schwarz_gather
+  if (variant != 0) return;
   for (int pos = q0 + threadIdx.x; pos < q1; pos += blockDim.x) {
     const int gi = gidx[pos];
     if (gi < 0) continue;
 #pragma unroll
     for (int f = 0; f < NF; ++f) z[f * N + gi] = y[f * Ptot + pos];
+  }
+}
+
+// sum_i R_i^{deltaT} x_i: every grid point adds the solutions of the box positions covering it, in
+// increasing position order (deterministic; a periodic self-overlapping box covers a point twice)
+__global__ void k_schwarz_gather(long long N, int nf, long long Ptot, const int* __restrict__ cover_off,
+                                 const int* __restrict__ cover_pos, const double* __restrict__ y, double* __restrict__ z) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+    const int e0 = cover_off[i], e1 = cover_off[i + 1];
+    for (int f = 0; f < nf; ++f) {
+      double acc = 0.0;
+      for (int e = e0; e < e1; ++e) acc += y[f * Ptot + cover_pos[e]];
+      z[f * N + i] = acc;
+    }
   }
 }
 
@@ -531,17 +547,21 @@ void launch_ras_apply(const BoxSet& B, int nf, long long N, const double* fac, c
   if (nf == 4) {
     if (fac32)
       k_ras_apply<4, 6, float><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off,
-                                                          B.P, B.ld, N, fac32, r, y, z);
+                                                          B.P, B.ld, N, fac32, r, y, z, B.variant);
     else
       k_ras_apply<4, 6, double><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off,
-                                                           B.P, B.ld, N, fac, r, y, z);
+                                                           B.P, B.ld, N, fac, r, y, z, B.variant);
   } else {
     if (fac32)
       k_ras_apply<5, 12, float><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off,
-                                                           B.P, B.ld, N, fac32, r, y, z);
+                                                           B.P, B.ld, N, fac32, r, y, z, B.variant);
     else
       k_ras_apply<5, 12, double><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr,
-                                                            B.box_pos_off, B.P, B.ld, N, fac, r, y, z);
+                                                            B.box_pos_off, B.P, B.ld, N, fac, r, y, z, B.variant);
+  }
+  if (B.variant != 0) {
+    const int blocks = (int)std::min<long long>((N + 255) / 256, 148 * 8);
+    k_schwarz_gather<<<blocks, 256, 0, s>>>(N, nf, B.P, B.cover_off, B.cover_pos, y, z);
   }
 }
 

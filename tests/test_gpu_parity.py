@@ -139,6 +139,37 @@ def test_ras_bilu0_apply_parity(shape, nsub, delta):
     assert max(errs) < 1e-10, errs
 
 
+SCHWARZ_CASES = [((16, 16), (2, 2), 2, "as"), ((16, 16), (2, 2), 2, "rras"), ((12, 14), (1, 1), 2, "as"),
+                 ((10, 13), (3, 2), 1, "rras"), ((6, 7, 6), (1, 1, 2), 1, "as"), ((6, 7, 6), (2, 1, 1), 1, "rras")]
+
+
+@pytest.mark.parametrize("shape,nsub,delta,variant", SCHWARZ_CASES)
+def test_schwarz_variant_apply_parity(shape, nsub, delta, variant):
+    """Classical AS and right-restricted AS against the oracle's Schwarz apply; the
+    overlapping boxes' sums include a periodic self-overlapping box (nsub = 1 along an axis)."""
+    from paper_2209_08001_b200 import PC_AS_BILU0, PC_RRAS_BILU0
+    d = len(shape)
+    nf = 2 + d
+    Xa, Xb = states(shape)
+    dt = 0.3
+    g = gpu_solver(shape, nsub=nsub, overlap=delta, pc_type=PC_AS_BILU0 if variant == "as" else PC_RRAS_BILU0)
+    g.set_fields(Xa[0], Xa[1], Xa[2:])
+    g.pc_setup(Xb, dt)
+    r = ni.random_direction(nf, shape, 11)
+    zg = g.pc_apply(r).cpu().numpy()
+    J = jacobian.assemble(oracle_model(d), Xa, Xb, dt)
+    zo = pc.RAS(J, shape, nf, tuple(reversed(nsub)), delta, variant=variant).apply(r)
+    errs = field_rel_err(zg, zo)
+    assert max(errs) < 1e-10, errs
+
+
+@pytest.mark.parametrize("variant", ["as", "rras"])
+def test_schwarz_variant_step_parity(variant):
+    """A whole NKS step preconditioned by AS / RRAS: the same converged step as the oracle."""
+    from paper_2209_08001_b200 import PC_AS_BILU0, PC_RRAS_BILU0
+    _run_parity((16, 16), [0.5], (2, 2), 2, pc_type=PC_AS_BILU0 if variant == "as" else PC_RRAS_BILU0)
+
+
 @pytest.mark.parametrize("shape,nsub", [((24, 24), (2, 2)), ((8, 8, 8), (2, 1, 1))])
 def test_gmres_solves_the_newton_system(shape, nsub):
     d = len(shape)

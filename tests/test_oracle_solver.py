@@ -250,6 +250,42 @@ def test_ras_exact_matches_textbook_formula():
     np.testing.assert_allclose(z.ravel(), zref, rtol=1e-10, atol=1e-12)
 
 
+@pytest.mark.parametrize("variant", ["as", "rras"])
+def test_schwarz_variants_match_textbook_formulas(variant):
+    """Classical AS: z = sum_i R_i^T A_i^{-1} R_i r; right-restricted: z = sum_i R_i^T A_i^{-1} R_i^0 r, with
+    explicit 0/1 restriction matrices and exact subdomain solves (Cai-Sarkis)."""
+    d, shape, nf = 2, (16, 16), 4
+    m, Xa, Xb, cbar = state(d, shape)
+    Jsp = jacobian.assemble(m, Xa, Xb, 0.1)
+    J = Jsp.toarray()
+    n = 256
+    pre = pc.RAS(Jsp, shape, nf, (2, 2), 2, exact=True, variant=variant)
+    r = np.random.default_rng(3).normal(size=(nf,) + shape)
+    z = pre.apply(r)
+    zref = np.zeros(nf * n)
+    for b in pre.boxes:
+        pts = pc.local_points(b)
+        g = [pc.global_index(b, l) for l in pts]
+        cols = [f * n + gi for gi in g for f in range(nf)]
+        R = np.zeros((len(cols), nf * n))
+        R[np.arange(len(cols)), cols] = 1
+        own = np.array([pc.is_owned(b, l) for l in pts for f in range(nf)])
+        Rin = R * own[:, None] if variant == "rras" else R
+        zref += R.T @ np.linalg.solve(R @ J @ R.T, Rin @ r.ravel())
+    np.testing.assert_allclose(z.ravel(), zref, rtol=1e-10, atol=1e-12)
+
+
+def test_schwarz_variants_coincide_without_overlap():
+    """delta = 0: the boxes tile the grid, R_i^0 = R_i^delta, so RAS = AS = RRAS (block Jacobi over boxes)."""
+    d, shape, nf = 2, (12, 12), 4
+    m, Xa, Xb, cbar = state(d, shape)
+    Jsp = jacobian.assemble(m, Xa, Xb, 0.2)
+    r = np.random.default_rng(4).normal(size=(nf,) + shape)
+    zs = [pc.RAS(Jsp, shape, nf, (3, 2), 0, variant=v).apply(r) for v in ("ras", "as", "rras")]
+    np.testing.assert_array_equal(zs[0], zs[1])
+    np.testing.assert_array_equal(zs[0], zs[2])
+
+
 def test_ras_block_diagonal_reduces_to_block_jacobi():
     """With a block-diagonal J, BILU(0)-RAS = point-block Jacobi: z_p = J_pp^{-1} r_p."""
     import scipy.sparse as sp
