@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     };
     // poll halo cells (q0, c0), (q1, c1), (q2, c2): lane l checks double l & 3 of cell l >> 2
     auto poll3 = [&](bool on, int q0_, int c0_, int q1_, int c1_, int q2_, int c2_) {
-      if (!on) return;
+      if (!on || (A.dbg & 16)) return;
       const int which = min(lane >> 2, 2);
       const int qq = which == 0 ? q0_ : (which == 1 ? q1_ : q2_);
       const int cc = which == 0 ? c0_ : (which == 1 ? c1_ : c2_);
@@ -418,6 +418,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       double pre, half;
       double L3[4], L5[4], N2[4], N4[4], M0[4], M1[4];
       auto preload = [&](int k) {      // rows for iteration k
+        if (A.dbg & 32) return;
         if (k < nFp) { ldrow(rowp(k, k, kPF) + 3 * 16, L3); ldrow(rowp(k, k, kPF) + 5 * 16, L5); } else { zero4(L3); zero4(L5); }
         if (k + 1 < nFp) { ldrow(rowp(k + 1, k + 1, kPF) + 2 * 16, N2); ldrow(rowp(k + 1, k + 1, kPF) + 4 * 16, N4); } else { zero4(N2); zero4(N4); }
         if (k + 2 < nFp) { ldrow(rowp(k + 2, k + 2, kPF) + 0 * 16, M0); ldrow(rowp(k + 2, k + 2, kPF) + 1 * 16, M1); } else { zero4(M0); zero4(M1); }
@@ -458,8 +459,8 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         const double c1 = dot4(M1, Ya1, 0.0);                         //            (-1,-1)
         pre = b0 + b1;
         half = c0 + c1;
-        ybuf[(size_t)k * 128] = y;
-        st_remote1_if(dn_remote && active && rl >= R - 2, hcell(min(max(rl - (R - 2), 0), 1), i) + c,
+        if (!(A.dbg & 4)) ybuf[(size_t)k * 128] = y;
+        st_remote1_if(!(A.dbg & 4) && dn_remote && active && rl >= R - 2, hcell(min(max(rl - (R - 2), 0), 1), i) + c,
                       (unsigned)min(s + 1, CS - 1), y);
         preload(k + 1);
         if (k % kG == kG - 2) release_group(gof(k));   // the group's last rows are in registers now
