@@ -30,14 +30,28 @@ __device__ __forceinline__ double horner_only(const DevParams& P, double x) {
   return acc * x;
 }
 
-// Psi_S[y_b, y_a] (symmetric in its arguments).
+// P(x) with the trip count fixed at compile time (S = 10, the paper's order): the loop
+// unrolls, so the six Horner chains of a point (three Psi_S, two arguments each) interleave.
+template <int K>
+__device__ __forceinline__ double horner_fixed(const DevParams& P, double x) {
+  double acc = 0.0;
+#pragma unroll
+  for (int k = K; k >= 1; --k) acc = fma(acc, x, P.pcoef[k - 1]);
+  return acc * x;
+}
+
+// Psi_S[y_b, y_a] (symmetric in its arguments).  One division for both reciprocals:
+// 1/ybar = (1-ybar) r, 1/(1-ybar) = ybar r with r = 1/(ybar (1-ybar)).
 __device__ __forceinline__ double psiS(const DevParams& P, double ya, double yb) {
   const double ybar = 0.5 * (ya + yb);
   const double e = 0.5 * (yb - ya);
   const double D = e * e;
-  const double iy = 1.0 / ybar;
-  const double iz = 1.0 / (1.0 - ybar);
+  const double zbar = 1.0 - ybar;
+  const double rr = 1.0 / (ybar * zbar);
+  const double iy = zbar * rr;
+  const double iz = ybar * rr;
   const double a = D * iy * iy, b = D * iz * iz;
+  if (P.S == 10) return log(ybar * iz) + horner_fixed<9>(P, b) - horner_fixed<9>(P, a);
   return log(ybar * iz) + horner_only(P, b) - horner_only(P, a);
 }
 

@@ -17,9 +17,15 @@
 namespace nks {
 
 namespace tj {
-constexpr int TX = 32, TY = 16, NT = TX * TY;   // 512 threads, 1 CTA/SM (J.v 30 -> 36 % of HBM at 256^3 vs 32x8)
+#ifndef NKS_TILE_Y
+#define NKS_TILE_Y 16
+#endif
+constexpr int TX = 32, TY = NKS_TILE_Y, NT = TX * TY;   // 32x16: 512 threads, 1 CTA/SM (J.v 30 -> 36 % of HBM at 256^3 vs 32x8)
 constexpr int HX = TX + 4, HY = TY + 4, PL = HX * HY;     // plane with 2-cell halo
 constexpr int RX = TX + 2, RY = TY + 2, RL = RX * RY;     // one-cell ring
+// F: 640 threads, so the ring pass (612 evaluations of the pointwise DVD quotients, the expensive part)
+// is one pass instead of 512 + 100; threads >= TX*TY idle in the interior pass
+constexpr int NTF = (RL + 31) / 32 * 32;
 }  // namespace tj
 
 __device__ __forceinline__ int tslot(int z, int n) { return ((z % n) + n) % n; }
@@ -283,7 +289,7 @@ __global__ void __launch_bounds__(tj::NT) k_jv_tiled(DevParams P, const double* 
 }
 
 template <int DIM>
-__global__ void __launch_bounds__(tj::NT) k_residual_tiled(DevParams P, const double* __restrict__ Xa,
+__global__ void __launch_bounds__(tj::NTF) k_residual_tiled(DevParams P, const double* __restrict__ Xa,
                                                            const double* __restrict__ Xb, const double* __restrict__ Ta,
                                                            double* __restrict__ F, int zc) {
   using namespace tj;
@@ -311,7 +317,7 @@ __global__ void __launch_bounds__(tj::NT) k_residual_tiled(DevParams P, const do
   long long goff[2];
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    const int c = tid + r * NT;
+    const int c = tid + r * NTF;
     cell[r] = c < PL ? c : -1;
     int gx = x0 + (c % HX) - 2, gy = y0 + (c / HX) - 2;
     gx = ((gx % nx) + nx) % nx;
@@ -344,7 +350,7 @@ __global__ void __launch_bounds__(tj::NT) k_residual_tiled(DevParams P, const do
     const double* Ux = su + (0 * NU + tslot(z, NU)) * PL;
     const double* Uy = su + (1 * NU + tslot(z, NU)) * PL;
     double* Gp = sg + tslot(z, N3) * RL;
-    for (int r = tid; r < RL; r += NT) {
+    for (int r = tid; r < RL; r += NTF) {
       const int rx = r % RX, ry = r / RX;
       const int k = (ry + 1) * HX + (rx + 1);
       const double ca = CA[k], cb = CB[k];
@@ -415,7 +421,7 @@ __global__ void __launch_bounds__(tj::NT) k_residual_tiled(DevParams P, const do
   const int hc = (ty + 2) * HX + (tx + 2);
   const int rc = (ty + 1) * RX + (tx + 1);
   const int x = x0 + tx, y = y0 + ty;
-  const bool inside = x < nx && y < ny;
+  const bool inside = x < nx && y < ny && tid < NT;
 
   // register prefetch of the next iteration's planes: u^b (3), c^b, c^a, eta^a, eta^b at z+2; T^a at z+1
   double R[8][2];
@@ -510,8 +516,8 @@ void launch_residual_tiled(const DevParams& P, const double* Xa, const double* X
     while (zc > 16 && (long long)tiles * ((ncz + zc - 1) / zc) < 148 * 2 * 4) zc = (zc + 1) / 2;
   }
   dim3 grid((P.nx + TX - 1) / TX, (P.ny + TY - 1) / TY, dim == 3 ? (P.nz - 2 * P.zg + zc - 1) / zc : 1);
-  if (dim == 2) k_residual_tiled<2><<<grid, NT, smem, s>>>(P, Xa, Xb, Ta, F, zc);
-  else k_residual_tiled<3><<<grid, NT, smem, s>>>(P, Xa, Xb, Ta, F, zc);
+  if (dim == 2) k_residual_tiled<2><<<grid, NTF, smem, s>>>(P, Xa, Xb, Ta, F, zc);
+  else k_residual_tiled<3><<<grid, NTF, smem, s>>>(P, Xa, Xb, Ta, F, zc);
 }
 
 size_t jv_tiled_smem(int dim) {

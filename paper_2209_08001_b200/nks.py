@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libnks.so")
+LIB_PATH = os.environ.get("NKS_LIB", os.path.join(_HERE, "lib", "libnks.so"))   # NKS_LIB: experiments only
 
 NKS_OK, NKS_E_INVALID, NKS_E_DOMAIN, NKS_E_DIVERGED, NKS_E_CUDA, NKS_E_NCCL, NKS_E_OOM, NKS_E_STATE = range(8)
 STATUS = {0: "OK", 1: "INVALID", 2: "DOMAIN", 3: "DIVERGED", 4: "CUDA", 5: "NCCL", 6: "OOM", 7: "STATE"}

@@ -27,7 +27,9 @@ def run(name, shape, hbm):
     d = len(shape)
     nf = 2 + d
     N = int(np.prod(shape))
-    g = Solver(shape, ni.model_default(), ni.solver_default(), pc_type=PC_NONE)
+    sol = dict(ni.solver_default())
+    sol["gmres_restart"] = 1            # no Krylov basis needed (512^3 would not fit with 31 vectors)
+    g = Solver(shape, ni.model_default(), sol, pc_type=PC_NONE)
     gen = torch.Generator(device="cuda").manual_seed(0)
     c = 0.1622 + (torch.rand(shape, device="cuda", dtype=torch.float64, generator=gen) - 0.5) * 0.01
     eta = 0.1 + (torch.rand(shape, device="cuda", dtype=torch.float64, generator=gen) - 0.5) * 0.02
