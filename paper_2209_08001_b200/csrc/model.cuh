@@ -55,18 +55,37 @@ __device__ __forceinline__ double psiS(const DevParams& P, double ya, double yb)
   return log(ybar * iz) + horner_only(P, b) - horner_only(P, a);
 }
 
+template <int K>
+__device__ __forceinline__ void horner_P_fixed(const DevParams& P, double x, double& p, double& dp) {
+  double acc = 0.0, dacc = 0.0;
+#pragma unroll
+  for (int k = K; k >= 1; --k) {
+    dacc = fma(dacc, x, acc);
+    acc = fma(acc, x, P.pcoef[k - 1]);
+  }
+  p = acc * x;
+  dp = fma(dacc, x, acc);
+}
+
 // Psi_S and its derivative with respect to the level-b argument y_b.
 __device__ __forceinline__ void psiS_d(const DevParams& P, double ya, double yb, double& val, double& dval) {
   const double ybar = 0.5 * (ya + yb);
   const double e = 0.5 * (yb - ya);
   const double D = e * e;
-  const double iy = 1.0 / ybar;
-  const double iz = 1.0 / (1.0 - ybar);
+  const double zbar = 1.0 - ybar;
+  const double rr = 1.0 / (ybar * zbar);
+  const double iy = zbar * rr;
+  const double iz = ybar * rr;
   const double iy2 = iy * iy, iz2 = iz * iz;
   const double a = D * iy2, b = D * iz2;
   double pa, dpa, pb, dpb;
-  horner_P(P, a, pa, dpa);
-  horner_P(P, b, pb, dpb);
+  if (P.S == 10) {
+    horner_P_fixed<9>(P, a, pa, dpa);
+    horner_P_fixed<9>(P, b, pb, dpb);
+  } else {
+    horner_P(P, a, pa, dpa);
+    horner_P(P, b, pb, dpb);
+  }
   val = log(ybar * iz) + pb - pa;
   // d/dy_b = 1/2 d/dybar + e d/dD
   dval = 0.5 * iy * iz + dpb * b * iz + dpa * a * iy + e * (dpb * iz2 - dpa * iy2);

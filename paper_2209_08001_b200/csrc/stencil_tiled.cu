@@ -79,7 +79,7 @@ __device__ __forceinline__ double elastic_row_tile(const DevParams& P, int I, co
 }
 
 template <int DIM>
-__global__ void __launch_bounds__(tj::NT) k_jv_tiled(DevParams P, const double* __restrict__ Xa,
+__global__ void __launch_bounds__(tj::NTF) k_jv_tiled(DevParams P, const double* __restrict__ Xa,
                                                      const double* __restrict__ jac4, const double* __restrict__ v,
                                                      double* __restrict__ out, int zc) {
   using namespace tj;
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(tj::NT) k_jv_tiled(DevParams P, const double* 
   long long goff[2];
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    const int c = tid + r * NT;
+    const int c = tid + r * NTF;
     cell[r] = c < PL ? c : -1;
     int gx = x0 + (c % HX) - 2, gy = y0 + (c / HX) - 2;
     gx = ((gx % nx) + nx) % nx;        // tiles may be wider than the grid
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(tj::NT) k_jv_tiled(DevParams P, const double* 
     const double* Ux = su + (0 * NU + slot(z, NU)) * PL;
     const double* Uy = su + (1 * NU + slot(z, NU)) * PL;
     double* W = sw + slot(z, N3) * RL;
-    for (int r = tid; r < RL; r += NT) {
+    for (int r = tid; r < RL; r += NTF) {
       const int rx = r % RX, ry = r / RX;
       const int k = (ry + 1) * HX + (rx + 1);
       const double vc = C0[k];
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(tj::NT) k_jv_tiled(DevParams P, const double* 
   const int hc = (ty + 2) * HX + (tx + 2);     // centre in the halo plane
   const int rc = (ty + 1) * RX + (tx + 1);     // centre in the ring
   const int x = x0 + tx, y = y0 + ty;
-  const bool inside = x < nx && y < ny;
+  const bool inside = x < nx && y < ny && tid < NT;
 
   // register prefetch of the planes the NEXT iteration commits to shared memory (hides HBM latency
   // behind this iteration's arithmetic): u_x,u_y,u_z, v_c at z+2; v_eta, c^a, a11, a12 at z+1
@@ -546,8 +546,8 @@ void launch_jv_tiled(const DevParams& P, const double* Xa, const double* jac4, c
     while (zc > 16 && (long long)tiles * ((ncz + zc - 1) / zc) < 148 * 2 * 4) zc = (zc + 1) / 2;
   }
   dim3 grid((P.nx + TX - 1) / TX, (P.ny + TY - 1) / TY, dim == 3 ? (P.nz - 2 * P.zg + zc - 1) / zc : 1);
-  if (dim == 2) k_jv_tiled<2><<<grid, NT, smem, s>>>(P, Xa, jac4, v, out, zc);
-  else k_jv_tiled<3><<<grid, NT, smem, s>>>(P, Xa, jac4, v, out, zc);
+  if (dim == 2) k_jv_tiled<2><<<grid, NTF, smem, s>>>(P, Xa, jac4, v, out, zc);
+  else k_jv_tiled<3><<<grid, NTF, smem, s>>>(P, Xa, jac4, v, out, zc);
 }
 
 }  // namespace nks
