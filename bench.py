@@ -42,6 +42,9 @@ import numpy as np  # noqa: E402
 
 import nks_inputs as ni  # noqa: E402
 
+# fp64 thread-level operations per grid point (DFMA + DADD + DMUL), counted by ncu at 3D 256^3
+# (profiles/r01_ncu_F_Jv_fp64_ops_3d256.txt): F is bound by the fp64 pipe, J.v by HBM
+FP64_OPS_PER_POINT = {"residual": 515.7, "jv": 138.5}
 METRIC = "NKS time steps/s (inverse NKS time-step wall time; BASELINE: NKS time-step wall time and F/J.v GDOF/s)"
 UNIT = "steps/s"
 
@@ -464,6 +467,15 @@ def run_gpu(args, world, rank, local, pg):
                 continue
             for k in r:
                 r[k]["frac_hbm"] = r[k]["GB_s"] / hbm
+                # fp64 ALU roofline: thread-level fp64 ops per point counted by ncu (DFMA+DADD+DMUL,
+                # profiles/r01_ncu_F_Jv_fp64_ops_3d256.txt) against 148 SMs x 64 fp64 lanes x max SM clock
+                ops = FP64_OPS_PER_POINT.get(k)
+                if ops and len(shp) == 3:
+                    peak_ops = 148 * 64 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+                    npts = float(np.prod(shp))
+                    r[k]["fp64_ops_per_point"] = ops
+                    r[k]["frac_fp64_alu"] = ops * npts / (r[k]["ms"] * 1e-3) / peak_ops
+                    r[k]["bound"] = "alu" if k == "residual" else "hbm"
             micro[name] = r
 
     # DRAM traffic of the roofline kernel from the committed ncu --set full capture (per launch), if any
