@@ -45,6 +45,9 @@ import nks_inputs as ni  # noqa: E402
 # fp64 thread-level operations per grid point (DFMA + DADD + DMUL), counted by ncu at 3D 256^3
 # (profiles/r01_ncu_F_Jv_fp64_ops_3d256.txt): F is bound by the fp64 pipe, J.v by HBM
 FP64_OPS_PER_POINT = {"residual": 515.7, "jv": 138.5}
+# measured fp64 peak: 36.77 TFLOP/s DFMA = 18.4e12 fp64 pipe operations/s (profiles/r01_fp64_peak_probe.txt,
+# tools/lat_probe.cu); nominal 148 SMs x 64 lanes x 1.965 GHz = 18.6e12
+FP64_OPS_PEAK = 36.77e12 / 2
 METRIC = "NKS time steps/s (inverse NKS time-step wall time; BASELINE: NKS time-step wall time and F/J.v GDOF/s)"
 UNIT = "steps/s"
 
@@ -471,7 +474,7 @@ def run_gpu(args, world, rank, local, pg):
                 # profiles/r01_ncu_F_Jv_fp64_ops_3d256.txt) against 148 SMs x 64 fp64 lanes x max SM clock
                 ops = FP64_OPS_PER_POINT.get(k)
                 if ops and len(shp) == 3:
-                    peak_ops = 148 * 64 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+                    peak_ops = FP64_OPS_PEAK
                     npts = float(np.prod(shp))
                     r[k]["fp64_ops_per_point"] = ops
                     r[k]["frac_fp64_alu"] = ops * npts / (r[k]["ms"] * 1e-3) / peak_ops
