@@ -17,6 +17,11 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 BUILDDIR = os.path.join(PKG, "build")
 LIB = os.path.join(LIBDIR, "libnks.so")
+# experiments only: NKS_BUILD_TAG=x NKS_BUILD_DEFS="-DFOO=1" builds lib/libnks_x.so (load it with NKS_LIB)
+TAG = os.environ.get("NKS_BUILD_TAG", "")
+if TAG:
+    LIB = os.path.join(LIBDIR, f"libnks_{TAG}.so")
+    BUILDDIR = os.path.join(BUILDDIR, TAG)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -44,7 +49,7 @@ def build(force: bool = False, verbose: bool = False, ptxas: bool = False) -> st
     deps = _deps()
     if not force and not _stale(LIB, deps):
         return LIB
-    extra = ["-Xptxas", "-v"] if ptxas else []
+    extra = (["-Xptxas", "-v"] if ptxas else []) + os.environ.get("NKS_BUILD_DEFS", "").split()
 
     def compile_one(src):
         obj = os.path.join(BUILDDIR, os.path.basename(src) + ".o")

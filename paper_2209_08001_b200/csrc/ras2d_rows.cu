@@ -52,8 +52,14 @@ template <bool F32> struct Strm {
   using T = double;
   static constexpr int PF = 98;    // forward: 6 lower blocks = 96 doubles, 784 B
   static constexpr int PB = 114;   // backward: diagonal + 6 upper = 112 doubles, 912 B
-  static constexpr int G = 2;      // steps per group (one bulk copy)
-  static constexpr int NS = 4;     // group buffers
+#ifndef NKS_R2_G
+#define NKS_R2_G 2
+#endif
+#ifndef NKS_R2_NS
+#define NKS_R2_NS 4
+#endif
+  static constexpr int G = NKS_R2_G;     // steps per group (one bulk copy)
+  static constexpr int NS = NKS_R2_NS;   // group buffers
 };
 template <> struct Strm<true> {
   using T = float;
@@ -62,7 +68,7 @@ template <> struct Strm<true> {
   static constexpr int G = 4;
   static constexpr int NS = 4;
 };
-constexpr int kGmax = 4;
+constexpr int kGmax = Strm<false>::G > 4 ? Strm<false>::G : 4;
 
 struct Geo {
   int s0x, s0y;       // global coordinate of local (0,0) (may be negative: wraps)
@@ -91,7 +97,8 @@ struct Args {
 
 // per CTA: [fwd cycles, bwd cycles, halo-wait cycles, stage-wait cycles, start (globaltimer), end, bar wait, 0]
 __device__ long long g_prof[1024 * 8];
-__device__ long long g_gt[72 * 8];   // NKS_RAS2D_PROF: CTA 0, warp 0, forward groups 8..15: per-phase clocks
+__device__ long long g_gt[72 * 8];
+__device__ long long g_cp[64 * 4];   // NKS_RAS2D_PROF: CTA 0 producer, groups 8..71: issue / first test / ready clocks   // NKS_RAS2D_PROF: CTA 0, warp 0, forward groups 8..15: per-phase clocks
 
 __device__ __forceinline__ int jmin_of(int t, int ex) { return max(0, (t - ex + 2) >> 1); }
 __host__ __device__ __forceinline__ int lo_of(int k, int ex, int R) { return min(R, max(0, (k - ex + 2) / 2)); }
@@ -218,7 +225,9 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   double* H = reinterpret_cast<double*>(emptyb + kNSW);               // 4 halo rows (16-byte aligned)
   double* E = H + 4 * (size_t)pitch;                                  // [8][32][4] exchange ring
   double* V = E + 8 * 128;                                            // [32][4] backward pre-diagonal exchange
-  int* off = reinterpret_cast<int*>(V + 128);                         // off[] in shared memory: the stage
+  int4* tb = reinterpret_cast<int4*>(V + 128);                        // per processing step p: stage element
+                                                                      // offset of row 0, active rows [lo, hi]
+  int* off = reinterpret_cast<int*>(tb + 2 * A.KGp);                  // off[] in shared memory: the stage
                                                                       // addresses are on the step's chain
   auto hcell = [&](int q, int i) -> double* { return H + (size_t)q * pitch + (min(max(i, -2), ex + 1) + 2) * 4; };
   const bool up_remote = s > 0, dn_remote = s < CS - 1;
@@ -237,6 +246,18 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       mbar_init(&emptyb[k], 4);       // one arrive per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // Row table: lane rl's block row at processing step p (forward k = p, backward k = 2 nFp - 1 - p) is
+  // stage + tb[p].x + rl * pitch when tb[p].y <= rl <= tb[p].z, so the per-step preload needs one
+  // broadcast shared load instead of the group/offset arithmetic and two off[] loads per row.
+  for (int p = tid; p < 2 * nFp; p += blockDim.x) {
+    const int k = p < nFp ? p : 2 * nFp - 1 - p;
+    const int q = p / kG;
+    const int kb = q < nGr ? q * kG : nFp - kG * (q - nGr + 1);
+    const int lo = lo_of(k, ex, R), hi = hi_of(k, R);
+    const int pf = p < nFp ? kPF : kPB;
+    tb[p] = make_int4((int)((q % kNSW) * stage_elems) + (off[k] - off[kb] - lo) * pf, lo, hi, 0);
   }
   __syncthreads();
   cluster.sync();
@@ -267,6 +288,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       const T* src = fw ? (const T*)A.chunkF + (base + r_lo) * kPF : (const T*)A.chunkB + (base + r_lo) * kPB;
       const unsigned bytes = (unsigned)(nrows * pf * sizeof(T));
       const unsigned bar = full0 + (q % kNSW) * 8;
+      if (A.prof && blockIdx.x == 0 && q >= 8 && q < 72) g_cp[(q - 8) * 4] = clock64();
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                        stage0 + (unsigned)((q % kNSW) * stage_elems * sizeof(T))),
@@ -279,15 +301,27 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
                    : "=r"(ok) : "r"(bar), "r"(par) : "memory");
       return __all_sync(0xffffffffu, ok);
     };
+    // Step barriers passed so far.  Group g covers processing steps [g kG, g kG + kG) of both sweeps and
+    // is released (empty-barrier arrive) by every consumer warp inside iteration p = g kG + kG - 2, which
+    // starts after step barrier p + 1 and ends before barrier p + 2 (forward; backward p + 2 / p + 3, its
+    // prologue barrier comes first).  So once the producer has passed barrier p + 2 (p + 3) the buffer
+    // is free without testing the mbarrier (a test_wait costs ~150 cycles and sat on the producer's
+    // per-step path); the mbarrier test remains only as the blocking fallback.
+    int nbars = 0;
+    auto freed = [&](int g) {
+      const int pr = g * kG + kG - 2;
+      return nbars >= pr + 3 + (pr >= nFp ? 1 : 0);
+    };
     // issue groups in order up to G; blocking: wait for the buffer, else stop at the first busy one
     auto issue_upto = [&](int G, bool block) {
       G = min(G, 2 * nGr - 1);
       while (issued <= G) {
         const int st = issued % kNSW, use = issued / kNSW;
-        if (use > 0) {
+        if (use > 0 && !freed(issued - kNSW)) {
+          if (!block) break;              // opportunistic issue: by the barrier count only (no test_wait)
           const unsigned bar = empty0 + st * 8, par = (unsigned)((use - 1) & 1);
-          if (block) { unsigned sp = 0; while (!test_bar(bar, par)) if (++sp > (1u << 26)) __trap(); }
-          else if (!test_bar(bar, par)) break;
+          unsigned sp = 0;
+          while (!test_bar(bar, par)) if (++sp > (1u << 26)) __trap();
         }
         if (lane == 0) issue_one(issued);
         __syncwarp();
@@ -295,13 +329,17 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       }
     };
     auto ensure = [&](int G) {          // groups <= G resident
+      if ((A.dbg & 128) && issued > 0) return;   // ablation: no copy management after the first groups
       G = min(G, 2 * nGr - 1);
-      issue_upto(G, true);
+      if (issued <= G) issue_upto(G, true);
       while (ready < G) {
         ++ready;
         unsigned sp = 0;
+        const bool rec = A.prof && blockIdx.x == 0 && lane == 0 && ready >= 8 && ready < 72;
+        if (rec) g_cp[(ready - 8) * 4 + 1] = clock64();
         while (!test_bar(full0 + (ready % kNSW) * 8, (unsigned)((ready / kNSW) & 1)))
           if (++sp > (1u << 26)) __trap();
+        if (rec) { g_cp[(ready - 8) * 4 + 2] = clock64(); g_cp[(ready - 8) * 4 + 3] = sp; }
       }
       issue_upto(G + kNSW - 1, false);  // start the next copies as soon as their buffers are free
     };
@@ -320,7 +358,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         if (++sp > (1u << 26)) __trap();          // a lost neighbour would otherwise hang the GPU
       }
     };
-    auto step_bar = [&]() { asm volatile("bar.sync 1, 160;" ::: "memory"); };
+    auto step_bar = [&]() { asm volatile("bar.sync 1, 160;" ::: "memory"); ++nbars; };
     // ---- forward: prologue barrier, then one barrier per step k
     ensure(gof(2));
     poll3(up_remote, 1, 0, 0, 0, 0, 1);
@@ -373,6 +411,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     };
     auto load_r = [&](int k) -> double {
       const int i = k - 2 * rl;
+      if (A.dbg & 64) return 1e-3 * i;            // ablation: no global loads on the step chain
       return (row_ok && i >= 0 && i < ex && k < nF) ? __ldg(rrow + gx_of(i)) : 0.0;
     };
     auto release_group = [&](int q) {
@@ -395,6 +434,16 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     };
     auto ldrow = [&](const T* p, double (&v)[4]) { ld4(p, v); };
     auto zero4 = [&](double (&v)[4]) { v[0] = v[1] = v[2] = v[3] = 0.0; };
+    // the block rows of processing step p (0 <= p < 2 nFp) from the row table: lanes without a row at
+    // that step skip the shared loads (their outputs of that step are discarded)
+    struct RowRef { const T* ptr; bool on; };
+    auto rowt = [&](int p, int pf) -> RowRef {
+      const int4 t = tb[p];
+      return RowRef{stage + t.x + rl * pf + c * 4, rl >= t.y && rl <= t.z};
+    };
+    auto ldrow_if = [&](const RowRef& r, int blk, double (&v)[4]) {
+      if (r.on) ld4(r.ptr + blk * 16, v); else zero4(v);
+    };
     auto dot4 = [&](const double (&m)[4], const double (&v)[4], double acc) {
       acc = fma(-m[0], v[0], acc);
       acc = fma(-m[1], v[1], acc);
@@ -416,12 +465,16 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     // ================================================================ forward sweep (L y = r)
     {
       double pre, half;
-      double L3[4], L5[4], N2[4], N4[4], M0[4], M1[4];
-      auto preload = [&](int k) {      // rows for iteration k
+      // two register sets of block rows: iteration k computes with one while the loads of iteration
+      // k + 1's rows into the other are in flight (issued right after its exchange loads, so the next
+      // step's exchange loads do not queue behind them)
+      struct FRows { double L3[4], L5[4], N2[4], N4[4], M0[4], M1[4]; };
+      FRows SA, SB;
+      auto preload = [&](FRows& S, int k) {      // rows for iteration k
         if (A.dbg & 32) return;
-        if (k < nFp) { ldrow(rowp(k, k, kPF) + 3 * 16, L3); ldrow(rowp(k, k, kPF) + 5 * 16, L5); } else { zero4(L3); zero4(L5); }
-        if (k + 1 < nFp) { ldrow(rowp(k + 1, k + 1, kPF) + 2 * 16, N2); ldrow(rowp(k + 1, k + 1, kPF) + 4 * 16, N4); } else { zero4(N2); zero4(N4); }
-        if (k + 2 < nFp) { ldrow(rowp(k + 2, k + 2, kPF) + 0 * 16, M0); ldrow(rowp(k + 2, k + 2, kPF) + 1 * 16, M1); } else { zero4(M0); zero4(M1); }
+        if (k < nFp) { const RowRef r = rowt(k, kPF); ldrow_if(r, 3, S.L3); ldrow_if(r, 5, S.L5); } else { zero4(S.L3); zero4(S.L5); }
+        if (k + 1 < nFp) { const RowRef r = rowt(k + 1, kPF); ldrow_if(r, 2, S.N2); ldrow_if(r, 4, S.N4); } else { zero4(S.N2); zero4(S.N4); }
+        if (k + 2 < nFp) { const RowRef r = rowt(k + 2, kPF); ldrow_if(r, 0, S.M0); ldrow_if(r, 1, S.M1); } else { zero4(S.M0); zero4(S.M1); }
       };
       double q0, q1, q2, q3;                       // r prefetch ring: r(k+2) is used at iteration k
       q0 = load_r(2); q1 = load_r(3); q2 = load_r(4); q3 = load_r(5);
@@ -439,9 +492,9 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         pre = dot4(bb, h10, dot4(a, h00, r0v));        // (0,-2), (0,-1) of step 0
         ldrow(rowp(1, 1, kPF) + 0 * 16, a); ldrow(rowp(1, 1, kPF) + 1 * 16, bb);
         half = dot4(bb, h10, dot4(a, h01, r1v));       // (0,-2), (-1,-1) of step 1
-        preload(0);
+        preload(SA, 0);
       }
-      auto fiter = [&](int k, double r2) {
+      auto fiter = [&](int k, double r2, FRows& cur, FRows& nxt) {
         const int i = k - 2 * rl;
         const bool active = row_ok && i >= 0 && i < ex;
         step_bar();                                                   // E[k-1] complete; stages/cells ready
@@ -449,27 +502,27 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         ld4(rl >= 1 ? Erow(k - 1, rl - 1) : hcell(1, k + 1), Ya1);   // (i+1, j-1) at step k-1
         ld4(Erow(k - 1, rl), yp);                                     // own row at step k-1
         ld4(rl >= 2 ? Erow(k - 2, rl - 2) : (rl == 1 ? hcell(1, k) : hcell(0, k + 2)), aa4);
-        const double a0 = dot4(L3, Ya1, pre);                         // (1,-1)
-        const double a1 = dot4(L5, yp, 0.0);                          // (-1,0)
+        preload(nxt, k + 1);
+        const double a0 = dot4(cur.L3, Ya1, pre);                     // (1,-1)
+        const double a1 = dot4(cur.L5, yp, 0.0);                      // (-1,0)
         const double y = active ? a0 + a1 : 0.0;
         E[((k & 7) * 32 + rl) * 4 + c] = y;
-        const double b0 = dot4(N2, Ya1, half);                        // pre(k+1): (0,-1)
-        const double b1 = dot4(N4, yp, 0.0);                          //           (-2,0)
-        const double c0 = dot4(M0, aa4, r2);                          // half(k+2): (0,-2)
-        const double c1 = dot4(M1, Ya1, 0.0);                         //            (-1,-1)
+        const double b0 = dot4(cur.N2, Ya1, half);                    // pre(k+1): (0,-1)
+        const double b1 = dot4(cur.N4, yp, 0.0);                      //           (-2,0)
+        const double c0 = dot4(cur.M0, aa4, r2);                      // half(k+2): (0,-2)
+        const double c1 = dot4(cur.M1, Ya1, 0.0);                     //            (-1,-1)
         pre = b0 + b1;
         half = c0 + c1;
-        if (!(A.dbg & 4)) ybuf[(size_t)k * 128] = y;
+        if (!(A.dbg & 260)) ybuf[(size_t)k * 128] = y;
         st_remote1_if(!(A.dbg & 4) && dn_remote && active && rl >= R - 2, hcell(min(max(rl - (R - 2), 0), 1), i) + c,
                       (unsigned)min(s + 1, CS - 1), y);
-        preload(k + 1);
         if (k % kG == kG - 2) release_group(gof(k));   // the group's last rows are in registers now
       };
       for (int k0 = 0; k0 < nFp; k0 += 4) {
-        fiter(k0, q0); q0 = load_r(k0 + 6);
-        fiter(k0 + 1, q1); q1 = load_r(k0 + 7);
-        fiter(k0 + 2, q2); q2 = load_r(k0 + 8);
-        fiter(k0 + 3, q3); q3 = load_r(k0 + 9);
+        fiter(k0, q0, SA, SB); q0 = load_r(k0 + 6);
+        fiter(k0 + 1, q1, SB, SA); q1 = load_r(k0 + 7);
+        fiter(k0 + 2, q2, SA, SB); q2 = load_r(k0 + 8);
+        fiter(k0 + 3, q3, SB, SA); q3 = load_r(k0 + 9);
       }
     }
     const long long cf1 = clock64();
@@ -486,17 +539,18 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       const int K = nFp - 1;
       auto pofk = [&](int k) { return 2 * nFp - 1 - k; };
       double pre, half;
-      double U3[4], U1[4], D[4], N4[4], N2[4], M6[4], M5[4];
-      auto preload = [&](int k) {      // rows for iteration k
+      struct BRows { double U3[4], U1[4], D[4], N4[4], N2[4], M6[4], M5[4]; };
+      BRows SA, SB;
+      auto preload = [&](BRows& S, int k) {      // rows for iteration k
         if (k >= 0) {
-          const T* u = rowp(k, pofk(k), kPB);
-          ldrow(u + 3 * 16, U3); ldrow(u + 1 * 16, U1); ldrow(u, D);
-        } else { zero4(U3); zero4(U1); zero4(D); }
-        if (k - 1 >= 0) { const T* u = rowp(k - 1, pofk(k - 1), kPB); ldrow(u + 4 * 16, N4); ldrow(u + 2 * 16, N2); } else { zero4(N4); zero4(N2); }
-        if (k - 2 >= 0) { const T* u = rowp(k - 2, pofk(k - 2), kPB); ldrow(u + 6 * 16, M6); ldrow(u + 5 * 16, M5); } else { zero4(M6); zero4(M5); }
+          const RowRef r = rowt(pofk(k), kPB);
+          ldrow_if(r, 3, S.U3); ldrow_if(r, 1, S.U1); ldrow_if(r, 0, S.D);
+        } else { zero4(S.U3); zero4(S.U1); zero4(S.D); }
+        if (k - 1 >= 0) { const RowRef r = rowt(pofk(k - 1), kPB); ldrow_if(r, 4, S.N4); ldrow_if(r, 2, S.N2); } else { zero4(S.N4); zero4(S.N2); }
+        if (k - 2 >= 0) { const RowRef r = rowt(pofk(k - 2), kPB); ldrow_if(r, 6, S.M6); ldrow_if(r, 5, S.M5); } else { zero4(S.M6); zero4(S.M5); }
       };
       double q0, q1, q2, q3;          // y prefetch ring: y(k-2) is used at iteration k
-      auto load_y = [&](int k) -> double { return k >= 0 ? ybuf[(size_t)k * 128] : 0.0; };
+      auto load_y = [&](int k) -> double { return (A.dbg & 64) ? 1e-3 * k : (k >= 0 ? ybuf[(size_t)k * 128] : 0.0); };
       q0 = load_y(K - 2); q1 = load_y(K - 3); q2 = load_y(K - 4); q3 = load_y(K - 5);
       const double yK = load_y(K), yK1 = load_y(K - 1);
       step_bar();                     // first backward groups resident, lane R-1 / R-2 cells of the first steps written
@@ -523,9 +577,9 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         const T* un = rowp(K - 1, pofk(K - 1), kPB);
         ldrow(un + 6 * 16, a); ldrow(un + 5 * 16, bb);
         half = dot4(bb, Xb2, dot4(a, bb4n, yK1));                 // (0,2), (1,1) of step K-1 (Xb3(K-1) = Xb2(K))
-        preload(K);
+        preload(SA, K);
       }
-      auto biter = [&](int k, double y2) {
+      auto biter = [&](int k, double y2, BRows& cur, BRows& nxt) {
         const int i = k - 2 * rl;
         const bool active = row_ok && i >= 0 && i < ex;
         const int iR = k - dR;
@@ -534,32 +588,32 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         ld4(rl <= R - 2 ? Erow(k + 1, rl + 1) : hcell(2, iR - 1), Xb1);   // (i-1, j+1) at step k+1
         ld4(Erow(k + 1, rl), xp);                                          // own row at step k+1
         ld4(rl <= R - 3 ? Erow(k + 2, rl + 2) : (rl == R - 2 ? hcell(2, iR) : hcell(3, iR - 2)), bb4);
-        const double a0 = dot4(U3, Xb1, pre);                         // (-1,1)
-        const double a1 = dot4(U1, xp, 0.0);                          // (1,0)
+        preload(nxt, k - 1);
+        const double a0 = dot4(cur.U3, Xb1, pre);                     // (-1,1)
+        const double a1 = dot4(cur.U1, xp, 0.0);                      // (1,0)
         V[rl * 4 + c] = a0 + a1;
-        const double b0 = dot4(N4, Xb1, half);                        // pre(k-1): (0,1)
-        const double b1 = dot4(N2, xp, 0.0);                          //           (2,0)
-        const double c0 = dot4(M6, bb4, y2);                          // half(k-2): (0,2)
-        const double c1 = dot4(M5, Xb1, 0.0);                         //            (1,1)
+        const double b0 = dot4(cur.N4, Xb1, half);                    // pre(k-1): (0,1)
+        const double b1 = dot4(cur.N2, xp, 0.0);                      //           (2,0)
+        const double c0 = dot4(cur.M6, bb4, y2);                      // half(k-2): (0,2)
+        const double c1 = dot4(cur.M5, Xb1, 0.0);                     //            (1,1)
         v_bar();                                                      // V complete
         double v[4];
         ld4(V + rl * 4, v);
-        const double x = active ? -dot4(D, v, 0.0) : 0.0;            // inverted diagonal block, row c
+        const double x = active ? -dot4(cur.D, v, 0.0) : 0.0;        // inverted diagonal block, row c
         E[((k & 7) * 32 + rl) * 4 + c] = x;
         pre = b0 + b1;
         half = c0 + c1;
-        st_global_if(active && own_row && i >= G.ox0 && i < G.ox0 + G.ownx, zrow + gx_of(min(max(i, 0), ex - 1)), x);
+        st_global_if(!(A.dbg & 256) && active && own_row && i >= G.ox0 && i < G.ox0 + G.ownx, zrow + gx_of(min(max(i, 0), ex - 1)), x);
         st_remote1_if(up_remote && active && rl < 2, hcell(2 + min(rl, 1), i) + c, (unsigned)max(s - 1, 0), x);
-        preload(k - 1);
         const int p = pofk(k);
         if (p % kG == kG - 2) release_group(gof(p));
       };
       for (int kb0 = 0; kb0 < nFp; kb0 += 4) {
         const int k0 = K - kb0;
-        biter(k0, q0); q0 = load_y(k0 - 6);
-        biter(k0 - 1, q1); q1 = load_y(k0 - 7);
-        biter(k0 - 2, q2); q2 = load_y(k0 - 8);
-        biter(k0 - 3, q3); q3 = load_y(k0 - 9);
+        biter(k0, q0, SA, SB); q0 = load_y(k0 - 6);
+        biter(k0 - 1, q1, SB, SA); q1 = load_y(k0 - 7);
+        biter(k0 - 2, q2, SA, SB); q2 = load_y(k0 - 8);
+        biter(k0 - 3, q3, SB, SA); q3 = load_y(k0 - 9);
       }
     }
     if (A.prof && tid == 0) {
@@ -921,7 +975,11 @@ static bool dims_of(const nks_grid& g, Dims& D) {
 static int cs_min(const Dims& D) { return (D.eymax + kRPC - 1) / kRPC; }
 
 // cluster sizes this grid admits: every stripe <= 32 rows and >= 2 rows, portable cluster size <= 8
-static bool cs_ok(const Dims& D, int CS) { return CS >= cs_min(D) && CS <= 8 && D.eymin / CS >= 2; }
+static int cs_max() {
+  const char* e = std::getenv("NKS_RAS2D_CSMAX");
+  return e ? std::max(1, std::min(16, std::atoi(e))) : 8;
+}
+static bool cs_ok(const Dims& D, int CS) { return CS >= cs_min(D) && CS <= cs_max() && D.eymin / CS >= 2; }
 
 static int kgp_of(const Dims& D, int RPC) { return D.exmax + 2 * (RPC - 1) + 4 * kGmax + 1; }
 
@@ -937,7 +995,7 @@ size_t workspace_bytes(const nks_grid& g) {
   Dims D;
   if (!dims_of(g, D)) return 0;
   size_t m = 0;
-  for (int cs = 1; cs <= 8; ++cs)
+  for (int cs = 1; cs <= 16; ++cs)
     if (cs_ok(D, cs)) m = std::max(m, chunk_bytes(D, cs));
   return m ? m + (size_t)D.nbox * sizeof(Geo) + 1024 : 0;
 }
@@ -945,7 +1003,9 @@ size_t workspace_bytes(const nks_grid& g) {
 static size_t smem_for(const Dims& D, int RPC, bool f32) {
   const size_t stage = f32 ? (size_t)Strm<true>::NS * Strm<true>::G * RPC * Strm<true>::PB * sizeof(float)
                            : (size_t)Strm<false>::NS * Strm<false>::G * RPC * Strm<false>::PB * sizeof(double);
-  return stage + 2 * (size_t)4 * 8 + (size_t)4 * (D.exmax + 4) * 4 * 8 + (size_t)9 * 128 * 8 + (size_t)kgp_of(D, RPC) * 4;
+  const int ns = f32 ? Strm<true>::NS : Strm<false>::NS;
+  return stage + 2 * (size_t)ns * 8 + (size_t)4 * (D.exmax + 4) * 4 * 8 + (size_t)9 * 128 * 8 + (size_t)kgp_of(D, RPC) * 4 +
+         (size_t)2 * kgp_of(D, RPC) * 16;
 }
 // bulk-copy gatekeeper kernel (default, 0.52 ms at config 2) or the per-lane cp.async variant
 // (NKS_RAS2D_LD=1: 0.75 ms -- the per-step work, not the copy pipeline, bounds the step)
@@ -971,8 +1031,12 @@ void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaSt
   int CS = 0, ncl = 0;
   size_t smem = 0;
   const char* cs_env = std::getenv("NKS_RAS2D_CS");
-  for (int cs = 8; cs >= 1; --cs) {
+  for (int cs = cs_max(); cs >= 1; --cs) {
     if (!cs_ok(D, cs) || (cs_env && cs != std::atoi(cs_env))) continue;
+    if (cs > 8 && cudaFuncSetAttribute(apply_fn(f32), cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
     const int rpc = (D.eymax + cs - 1) / cs;
     const size_t sm = use_ld() ? smem_ld(D, rpc) : smem_for(D, rpc, f32);
     if (sm > (size_t)maxsm) continue;
@@ -1109,6 +1173,14 @@ cudaError_t launch_apply(void* plan, const double* r, double* z, cudaStream_t s)
           std::fprintf(stderr, "  producer step %d: ensure %lld, poll %lld, bar %lld, to next %lld\n", 40 + k, q[1] - q[0], q[2] - q[1],
                        q[3] - q[2], k < 7 ? gt[(k + 1) * 8] - q[3] : 0);
         }
+      }
+      {
+        std::vector<long long> cp(64 * 4);
+        cudaMemcpyFromSymbol(cp.data(), g_cp, cp.size() * 8);
+        for (int q = 0; q < 24; ++q)
+          std::fprintf(stderr, "  group %d: issue->first test %lld, issue->ready %lld, spins %lld, ready gap %lld\n", q + 8,
+                       cp[q * 4 + 1] - cp[q * 4], cp[q * 4 + 2] - cp[q * 4], cp[q * 4 + 3],
+                       q ? cp[q * 4 + 2] - cp[(q - 1) * 4 + 2] : 0);
       }
       std::vector<long long> gt(72 * 8);
       cudaMemcpyFromSymbol(gt.data(), g_gt, gt.size() * 8);
