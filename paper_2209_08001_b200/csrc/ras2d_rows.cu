@@ -130,6 +130,14 @@ __device__ __forceinline__ void ld4(const float* p, double (&v)[4]) {
   const float4 a = *reinterpret_cast<const float4*>(p);
   v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
 }
+__device__ __forceinline__ void ldg4(const float* p, double (&v)[4]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+}
+__device__ __forceinline__ void ldg4(const double* p, double (&v)[4]) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p + 2));
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
 __device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
   const double2 a = *reinterpret_cast<const double2*>(p), b = *reinterpret_cast<const double2*>(p + 2);
   v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
@@ -189,14 +197,29 @@ __global__ void k_pack(Args A, const double* __restrict__ fac, long long ld, int
     const int k = i + 2 * rl;
     const long long sb = (long long)b * A.CS + s;
     const long long row = sb * A.RPC * A.exmax + A.offt[sb * A.KGp + k] + (rl - lo_of(k, G.ex, R));
-    const double v = fac[(long long)plane * ld + pos];
+    double v;
+    if (plane < 112) {
+      v = fac[(long long)plane * ld + pos];            // lower blocks; inverted diagonal block D^-1
+    } else {
+      // upper block U_j folded with the inverted diagonal: (D^-1 U_j)[r][cc] = sum_m D^-1[r][m] U_j[m][cc]
+      // (backward sweep x = D^-1 y - sum_j (D^-1 U_j) x_j: one exchange per step, no diagonal solve)
+      const int jb = (plane - 96) >> 4, r = (plane >> 2) & 3, cc = plane & 3;
+      v = 0.0;
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        v = fma(fac[(long long)(96 + r * 4 + m) * ld + pos], fac[(long long)(96 + jb * 16 + m * 4 + cc) * ld + pos], v);
+    }
     if (plane < 96) chunkF[row * S::PF + plane] = (T)v;
     else chunkB[row * S::PB + (plane - 96)] = (T)v;
   }
 }
 
 // ---------------------------------------------------------------------------------- apply
-template <bool F32>
+// GL = true: the consumers load their block rows straight from the packed stream in global memory
+// (LDG, one step ahead into the second register set) and the producer only prefetches the groups
+// ahead into L2 -- no shared-memory staging, so the factor bytes cross the SM's L1/shared data path
+// once instead of twice (bulk-copy write + LDS read).
+template <bool F32, bool GL>
 __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   using S = Strm<F32>;
   using T = typename S::T;
@@ -224,7 +247,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   const int pitch = (ex + 4) * 4;
   double* H = reinterpret_cast<double*>(emptyb + kNSW);               // 4 halo rows (16-byte aligned)
   double* E = H + 4 * (size_t)pitch;                                  // [8][32][4] exchange ring
-  double* V = E + 8 * 128;                                            // [32][4] backward pre-diagonal exchange
+  double* V = E + 8 * 128;                                            // [32][4] (unused since the diagonal fold)
   int4* tb = reinterpret_cast<int4*>(V + 128);                        // per processing step p: stage element
                                                                       // offset of row 0, active rows [lo, hi]
   int* off = reinterpret_cast<int*>(tb + 2 * A.KGp);                  // off[] in shared memory: the stage
@@ -257,7 +280,8 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     const int kb = q < nGr ? q * kG : nFp - kG * (q - nGr + 1);
     const int lo = lo_of(k, ex, R), hi = hi_of(k, R);
     const int pf = p < nFp ? kPF : kPB;
-    tb[p] = make_int4((int)((q % kNSW) * stage_elems) + (off[k] - off[kb] - lo) * pf, lo, hi, 0);
+    if (GL) tb[p] = make_int4((int)((sb * RPC * A.exmax + off[k] - lo) * pf), lo, hi, 0);
+    else tb[p] = make_int4((int)((q % kNSW) * stage_elems) + (off[k] - off[kb] - lo) * pf, lo, hi, 0);
   }
   __syncthreads();
   cluster.sync();
@@ -270,8 +294,8 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   // threads).  Before arriving for step p the producer has made the factor groups the consumers will
   // read during step p resident (mbarrier waits) and has seen the halo cells they will read written
   // (sentinel polls), so the consumers themselves never wait on an mbarrier or poll: their loop is
-  // the exchange barrier, a few shared loads and the DFMA chains.  Barrier 2 (128) orders the
-  // backward sweep's V exchange, barrier 3 (128) the E reset between the sweeps.
+  // the exchange barrier, a few shared loads and the DFMA chains.  Barrier 3 (128) orders the E reset
+  // between the sweeps.
   auto gof = [&](int p) { return p / kG; };   // group of processing step p (forward k = p, backward k = 2 nFp - 1 - p)
 
   if (w == 4) {
@@ -328,7 +352,22 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         ++issued;
       }
     };
+    auto prefetch_one = [&](int q) {    // GL: group q's rows into L2
+      const bool fw = q < nGr;
+      const int k0 = klo(q);
+      const int r_lo = off[k0];
+      const int nrows = max(1, off[k0 + kG] - r_lo);
+      const int pf = fw ? kPF : kPB;
+      const T* src = fw ? (const T*)A.chunkF + (base + r_lo) * kPF : (const T*)A.chunkB + (base + r_lo) * kPB;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((unsigned)(nrows * pf * sizeof(T))) : "memory");
+    };
     auto ensure = [&](int G) {          // groups <= G resident
+      if (GL) {                         // prefetch 4 groups past the ones the consumers read next
+        const int G2 = min(G + 4, 2 * nGr - 1);
+        if (lane == 0) for (; issued <= G2; ++issued) prefetch_one(issued);
+        issued = __shfl_sync(0xffffffffu, issued, 0);
+        return;
+      }
       if ((A.dbg & 128) && issued > 0) return;   // ablation: no copy management after the first groups
       G = min(G, 2 * nGr - 1);
       if (issued <= G) issue_upto(G, true);
@@ -415,13 +454,13 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       return (row_ok && i >= 0 && i < ex && k < nF) ? __ldg(rrow + gx_of(i)) : 0.0;
     };
     auto release_group = [&](int q) {
+      if (GL) return;
       __syncwarp();
       // relaxed: the stage's shared-memory reads all completed into registers before (no fence needed)
       if (lane == 0)
         asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(empty0 + (q % kNSW) * 8) : "memory");
     };
     auto step_bar = [&]() { asm volatile("bar.sync 1, 160;" ::: "memory"); };
-    auto v_bar = [&]() { asm volatile("bar.sync 2, 128;" ::: "memory"); };
     auto e_bar = [&]() { asm volatile("bar.sync 3, 128;" ::: "memory"); };
     // this lane's block row c of step k (processing step p) in its group's buffer; nullptr-safe row 0
     auto rowp = [&](int k, int p, int pf) -> const T* {
@@ -430,6 +469,10 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       const int kc = min(max(k, 0), nFp);
       const int lo = lo_of(kc, ex, R), hi = hi_of(kc, R);
       const int rr = (k >= 0 && k < nFp && rl >= lo && rl <= hi) ? off[kc] - off[kb] + (rl - lo) : 0;
+      if (GL) {
+        const int rg = (k >= 0 && k < nFp && rl >= lo && rl <= hi) ? off[kc] + (rl - lo) : off[min(kc, nFp - 1)];
+        return (p < nFp ? (const T*)A.chunkF : (const T*)A.chunkB) + (size_t)(sb * RPC * A.exmax + rg) * pf + c * 4;
+      }
       return stage + (size_t)(q % kNSW) * stage_elems + (size_t)rr * pf + c * 4;
     };
     auto ldrow = [&](const T* p, double (&v)[4]) { ld4(p, v); };
@@ -439,10 +482,12 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     struct RowRef { const T* ptr; bool on; };
     auto rowt = [&](int p, int pf) -> RowRef {
       const int4 t = tb[p];
-      return RowRef{stage + t.x + rl * pf + c * 4, rl >= t.y && rl <= t.z};
+      const T* b0 = GL ? (p < nFp ? (const T*)A.chunkF : (const T*)A.chunkB) : stage;
+      return RowRef{b0 + t.x + rl * pf + c * 4, rl >= t.y && rl <= t.z};
     };
     auto ldrow_if = [&](const RowRef& r, int blk, double (&v)[4]) {
-      if (r.on) ld4(r.ptr + blk * 16, v); else zero4(v);
+      if (!r.on) { zero4(v); return; }
+      if (GL) ldg4(r.ptr + blk * 16, v); else ld4(r.ptr + blk * 16, v);
     };
     auto dot4 = [&](const double (&m)[4], const double (&v)[4], double acc) {
       acc = fma(-m[0], v[0], acc);
@@ -531,28 +576,43 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     e_bar();
 
     // ================================================================ backward sweep (U x = y)
-    //   v(k)      = pre(k)    - U3(k).Xb1(k) - U1(k).x(k+1);  x(k) = Dinv(k) v(k)      (chain)
-    //   pre(k-1)  = half(k-1) - U4(k-1).Xb1(k) - U2(k-1).x(k+1)    (Xb2(k-1) = Xb1(k), Xo2(k-1) = x(k+1))
-    //   half(k-2) = y(k-2)    - U6(k-2).bb4(k-2) - U5(k-2).Xb1(k)  (Xb3(k-2) = Xb1(k), bb4(k-2) = row j+2 at k+2)
+    // With the inverted diagonal folded into the upper blocks at pack time (U'_j = D^-1 U_j,
+    // y' = D^-1 y), x = y' - sum_j U'_j x_j has the forward sweep's shape: one exchange per step.
+    //   x(k)      = pre(k)    - U'3(k).Xb1(k) - U'1(k).x(k+1)           (chain)
+    //   pre(k-1)  = half(k-1) - U'4(k-1).Xb1(k) - U'2(k-1).x(k+1)    (Xb2(k-1) = Xb1(k), Xo2(k-1) = x(k+1))
+    //   half(k-2) = y'(k-2)   - U'6(k-2).bb4(k-2) - U'5(k-2).Xb1(k)  (Xb3(k-2) = Xb1(k), bb4(k-2) = row j+2 at k+2)
+    // y'(k)_c = (D^-1(k) row c) . y(k), from the forward sweep's y of all four components.
     {
       const int dR = 2 * (R - 1);     // lane R-1 processes i = k - dR
       const int K = nFp - 1;
       auto pofk = [&](int k) { return 2 * nFp - 1 - k; };
       double pre, half;
-      struct BRows { double U3[4], U1[4], D[4], N4[4], N2[4], M6[4], M5[4]; };
+      struct BRows { double U3[4], U1[4], N4[4], N2[4], M6[4], M5[4], DM[4]; };
       BRows SA, SB;
       auto preload = [&](BRows& S, int k) {      // rows for iteration k
-        if (k >= 0) {
-          const RowRef r = rowt(pofk(k), kPB);
-          ldrow_if(r, 3, S.U3); ldrow_if(r, 1, S.U1); ldrow_if(r, 0, S.D);
-        } else { zero4(S.U3); zero4(S.U1); zero4(S.D); }
+        if (k >= 0) { const RowRef r = rowt(pofk(k), kPB); ldrow_if(r, 3, S.U3); ldrow_if(r, 1, S.U1); } else { zero4(S.U3); zero4(S.U1); }
         if (k - 1 >= 0) { const RowRef r = rowt(pofk(k - 1), kPB); ldrow_if(r, 4, S.N4); ldrow_if(r, 2, S.N2); } else { zero4(S.N4); zero4(S.N2); }
-        if (k - 2 >= 0) { const RowRef r = rowt(pofk(k - 2), kPB); ldrow_if(r, 6, S.M6); ldrow_if(r, 5, S.M5); } else { zero4(S.M6); zero4(S.M5); }
+        if (k - 2 >= 0) {
+          const RowRef r = rowt(pofk(k - 2), kPB);
+          ldrow_if(r, 6, S.M6); ldrow_if(r, 5, S.M5); ldrow_if(r, 0, S.DM);
+        } else { zero4(S.M6); zero4(S.M5); zero4(S.DM); }
       };
-      double q0, q1, q2, q3;          // y prefetch ring: y(k-2) is used at iteration k
-      auto load_y = [&](int k) -> double { return (A.dbg & 64) ? 1e-3 * k : (k >= 0 ? ybuf[(size_t)k * 128] : 0.0); };
-      q0 = load_y(K - 2); q1 = load_y(K - 3); q2 = load_y(K - 4); q3 = load_y(K - 5);
-      const double yK = load_y(K), yK1 = load_y(K - 1);
+      const double* yrow = A.yscr + sb * A.KGp * 128 + rl * 4;    // y(k) of this row: yrow[k * 128 + 0..3]
+      auto load_y4 = [&](int k, double (&v)[4]) {
+        if (A.dbg & 64) { v[0] = v[1] = v[2] = v[3] = 1e-3 * k; return; }
+        if (k >= 0) {
+          const double2 a = *reinterpret_cast<const double2*>(yrow + (size_t)k * 128);
+          const double2 b = *reinterpret_cast<const double2*>(yrow + (size_t)k * 128 + 2);
+          v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+        } else { zero4(v); }
+      };
+      auto ydot = [&](const double (&d)[4], const double (&y4)[4]) {   // (D^-1 row c) . y
+        return fma(d[3], y4[3], fma(d[2], y4[2], fma(d[1], y4[1], d[0] * y4[0])));
+      };
+      double q0[4], q1[4], q2[4], q3[4];   // y prefetch ring: y(k-2) is used at iteration k
+      load_y4(K - 2, q0); load_y4(K - 3, q1); load_y4(K - 4, q2); load_y4(K - 5, q3);
+      double yK[4], yK1[4];
+      load_y4(K, yK); load_y4(K - 1, yK1);
       step_bar();                     // first backward groups resident, lane R-1 / R-2 cells of the first steps written
       {
         const int iR = K - dR;
@@ -563,7 +623,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         ld4(hcell(2, iR + 2), h2c);   // bb4(K) for lane R-2
         ld4(hcell(3, iR), h3a);       // bb4(K) for lane R-1
         ld4(hcell(3, iR - 1), h3b);   // bb4(K-1) for lane R-1
-        double Xb2[4], Xb3[4], bb4[4], bb4n[4], a[4], bb[4], cc[4];
+        double Xb2[4], Xb3[4], bb4[4], bb4n[4], a[4], bb[4], cc[4], dd[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           Xb2[u] = bot ? h2a[u] : 0.0;
@@ -572,14 +632,14 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
           bb4n[u] = bot ? h3b[u] : (bot2 ? h2b[u] : 0.0);
         }
         const T* u = rowp(K, pofk(K), kPB);
-        ldrow(u + 6 * 16, a); ldrow(u + 5 * 16, bb); ldrow(u + 4 * 16, cc);
-        pre = dot4(cc, Xb2, dot4(bb, Xb3, dot4(a, bb4, yK)));     // (0,2), (1,1), (0,1)
+        ldrow(u + 6 * 16, a); ldrow(u + 5 * 16, bb); ldrow(u + 4 * 16, cc); ldrow(u, dd);
+        pre = dot4(cc, Xb2, dot4(bb, Xb3, dot4(a, bb4, ydot(dd, yK))));     // (0,2), (1,1), (0,1)
         const T* un = rowp(K - 1, pofk(K - 1), kPB);
-        ldrow(un + 6 * 16, a); ldrow(un + 5 * 16, bb);
-        half = dot4(bb, Xb2, dot4(a, bb4n, yK1));                 // (0,2), (1,1) of step K-1 (Xb3(K-1) = Xb2(K))
+        ldrow(un + 6 * 16, a); ldrow(un + 5 * 16, bb); ldrow(un, dd);
+        half = dot4(bb, Xb2, dot4(a, bb4n, ydot(dd, yK1)));                 // (0,2), (1,1) of step K-1 (Xb3(K-1) = Xb2(K))
         preload(SA, K);
       }
-      auto biter = [&](int k, double y2, BRows& cur, BRows& nxt) {
+      auto biter = [&](int k, const double (&y2)[4], BRows& cur, BRows& nxt) {
         const int i = k - 2 * rl;
         const bool active = row_ok && i >= 0 && i < ex;
         const int iR = k - dR;
@@ -591,16 +651,12 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         preload(nxt, k - 1);
         const double a0 = dot4(cur.U3, Xb1, pre);                     // (-1,1)
         const double a1 = dot4(cur.U1, xp, 0.0);                      // (1,0)
-        V[rl * 4 + c] = a0 + a1;
+        const double x = active ? a0 + a1 : 0.0;
+        E[((k & 7) * 32 + rl) * 4 + c] = x;
         const double b0 = dot4(cur.N4, Xb1, half);                    // pre(k-1): (0,1)
         const double b1 = dot4(cur.N2, xp, 0.0);                      //           (2,0)
-        const double c0 = dot4(cur.M6, bb4, y2);                      // half(k-2): (0,2)
+        const double c0 = dot4(cur.M6, bb4, ydot(cur.DM, y2));        // half(k-2): (0,2)
         const double c1 = dot4(cur.M5, Xb1, 0.0);                     //            (1,1)
-        v_bar();                                                      // V complete
-        double v[4];
-        ld4(V + rl * 4, v);
-        const double x = active ? -dot4(cur.D, v, 0.0) : 0.0;        // inverted diagonal block, row c
-        E[((k & 7) * 32 + rl) * 4 + c] = x;
         pre = b0 + b1;
         half = c0 + c1;
         st_global_if(!(A.dbg & 256) && active && own_row && i >= G.ox0 && i < G.ox0 + G.ownx, zrow + gx_of(min(max(i, 0), ex - 1)), x);
@@ -610,10 +666,10 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       };
       for (int kb0 = 0; kb0 < nFp; kb0 += 4) {
         const int k0 = K - kb0;
-        biter(k0, q0, SA, SB); q0 = load_y(k0 - 6);
-        biter(k0 - 1, q1, SB, SA); q1 = load_y(k0 - 7);
-        biter(k0 - 2, q2, SA, SB); q2 = load_y(k0 - 8);
-        biter(k0 - 3, q3, SB, SA); q3 = load_y(k0 - 9);
+        biter(k0, q0, SA, SB); load_y4(k0 - 6, q0);
+        biter(k0 - 1, q1, SB, SA); load_y4(k0 - 7, q1);
+        biter(k0 - 2, q2, SA, SB); load_y4(k0 - 8, q2);
+        biter(k0 - 3, q3, SB, SA); load_y4(k0 - 9, q3);
       }
     }
     if (A.prof && tid == 0) {
@@ -628,314 +684,6 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   
 }
 
-
-// ---------------------------------------------------------------------------------- apply, per-lane async copies
-// Same sweep as k_apply, but every consumer lane fetches its own block rows (row c of each block of its
-// box row) with cp.async (LDGSTS, 16 bytes each) kLD processing steps ahead into a private shared ring
-// slot and waits with cp.async.wait_group: no bulk copies (whose fixed ~540-cycle cost serialises per
-// SM), no mbarriers, no group bookkeeping; the copies of many steps are in flight at once.  The
-// producer warp only gates the halo cells and joins the per-step barrier.
-constexpr int kLD = 6;            // prefetch depth in processing steps (steps p, p+1, p+2 are read at p)
-constexpr int kSLOTB = 240;       // bytes per lane and step: 7 block rows of 32 B (fp64), odd multiple of 16
-
-__device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-template <bool F32>
-__global__ void __launch_bounds__(160, 1) k_apply_ld(Args A) {
-  using S = Strm<F32>;
-  using T = typename S::T;
-  constexpr int kPF = S::PF, kPB = S::PB;
-  extern __shared__ __align__(128) unsigned char smem[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int s = (int)cluster.block_rank();
-  const int CS = A.CS;
-  const int b = blockIdx.x / CS;
-  const Geo G = A.boxes[b];
-  const int ex = G.ex, ey = G.ey;
-  const int r0 = (s * ey) / CS, r1 = ((s + 1) * ey) / CS, R = r1 - r0;
-  const int RPC = A.RPC;
-  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int nF = ex + 2 * (R - 1);            // steps per sweep of this stripe
-  const int nFp = (nF + 3) & ~3;              // whole 4-step unrolls (the padding steps have no active row)
-  const long long sb = (long long)b * CS + s;
-  const int* off_g = A.offt + sb * A.KGp;
-  unsigned char* ring = smem;                                         // [kLD][128 lanes][kSLOTB]
-  const int pitch = (ex + 4) * 4;
-  double* H = reinterpret_cast<double*>(smem + (size_t)kLD * 128 * kSLOTB);   // 4 halo rows
-  double* E = H + 4 * (size_t)pitch;                                  // [8][32][4] exchange ring
-  double* V = E + 8 * 128;                                            // [32][4] backward pre-diagonal exchange
-  int* off = reinterpret_cast<int*>(V + 128);                         // off[0 .. nFp]
-  auto hcell = [&](int q, int i) -> double* { return H + (size_t)q * pitch + (min(max(i, -2), ex + 1) + 2) * 4; };
-  const bool up_remote = s > 0, dn_remote = s < CS - 1;
-
-  for (int k = tid; k < 4 * pitch; k += blockDim.x) {
-    const int q = k / pitch, cell = (k % pitch) / 4 - 2;
-    const bool remote = (q < 2 ? up_remote : dn_remote) && cell >= 0 && cell < ex;
-    H[k] = remote ? __longlong_as_double((long long)kSentinel) : 0.0;
-  }
-  for (int k = tid; k < 9 * 128; k += blockDim.x) E[k] = 0.0;
-  for (int k = tid; k <= nFp; k += blockDim.x) off[k] = off_g[k];
-  __syncthreads();
-  cluster.sync();
-
-  if (w == 4) {
-    // ================================================================ halo gatekeeper
-    // lane l checks double l & 3 of one of three cells; the step barrier then hands the cells over
-    auto poll3 = [&](bool on, int q0_, int c0_, int q1_, int c1_, int q2_, int c2_) {
-      if (!on || (A.dbg & 17)) return;
-      const int which = min(lane >> 2, 2);
-      const int qq = which == 0 ? q0_ : (which == 1 ? q1_ : q2_);
-      const int cc = which == 0 ? c0_ : (which == 1 ? c1_ : c2_);
-      const unsigned sa = smem_u32(hcell(qq, cc) + (lane & 3));
-      unsigned sp = 0;
-      while (true) {
-        unsigned long long v;
-        asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"(sa) : "memory");
-        if (__all_sync(0xffffffffu, v != kSentinel)) break;
-        if (++sp > (1u << 26)) __trap();          // a lost neighbour would otherwise hang the GPU
-      }
-    };
-    auto step_bar = [&]() { asm volatile("bar.sync 1, 160;" ::: "memory"); };
-    poll3(up_remote, 1, 0, 0, 0, 0, 1);
-    step_bar();
-    for (int k = 0; k < nFp; ++k) {
-      poll3(up_remote, 1, k + 1, 0, k + 2, 1, k);
-      step_bar();
-    }
-    const int dR = 2 * (R - 1);
-    {
-      const int iR = nFp - 1 - dR;
-      poll3(dn_remote, 2, iR, 2, iR + 1, 2, iR + 2);
-      poll3(dn_remote, 3, iR, 3, iR - 1, 2, iR - 1);
-      step_bar();
-    }
-    for (int k = nFp - 1; k >= 0; --k) {
-      const int iR = k - dR;
-      poll3(dn_remote, 2, iR - 1, 2, iR, 3, iR - 2);
-      step_bar();
-    }
-  } else {
-    // ================================================================ consumers
-    const int c = w;
-    const int rl = lane;
-    const bool row_ok = rl < R;
-    const int j = r0 + rl;
-    int gy = (G.s0y + j) % A.ny;
-    if (gy < 0) gy += A.ny;
-    const bool own_row = row_ok && j >= G.oy0 && j < G.oy0 + G.owny;
-    const long long N = A.N;
-    const double* rrow = A.r + (long long)c * N + (long long)gy * A.nx;
-    double* zrow = A.z + (long long)c * N + (long long)gy * A.nx;
-    double* ybuf = A.yscr + sb * A.KGp * 128 + rl * 4 + c;
-    const long long base = sb * RPC * A.exmax;
-    const T* chF = (const T*)A.chunkF + base * kPF + c * 4;
-    const T* chB = (const T*)A.chunkB + base * kPB + c * 4;
-    const unsigned ring0 = smem_u32(ring) + (unsigned)tid * kSLOTB;
-    auto slot_addr = [&](int p) { return ring0 + (unsigned)((p % kLD) * 128 * kSLOTB); };
-    auto slot_ptr = [&](int p) -> const T* { return reinterpret_cast<const T*>(ring + ((size_t)(p % kLD) * 128 + tid) * kSLOTB); };
-    // issue the copies of processing step p (forward k = p, backward k = 2 nFp - 1 - p): row c of
-    // each block of this lane's row, if the row is active at that step; always one commit group
-    auto issue = [&](int p) {
-      if (p < 2 * nFp && !(A.dbg & 2)) {
-        const bool fw = p < nFp;
-        const int k = fw ? p : 2 * nFp - 1 - p;
-        const int lo = lo_of(k, ex, R), hi = hi_of(k, R);
-        if (rl >= lo && rl <= hi) {
-          const long long row = off[k] + (rl - lo);
-          const unsigned dst = slot_addr(p);
-          const int nb = fw ? 6 : 7;
-          const T* src = fw ? chF + row * kPF : chB + row * kPB;
-          for (int bb = 0; bb < nb; ++bb) {
-            if (F32) {
-              cp_async16(dst + bb * 16, src + bb * 16);
-            } else {
-              cp_async16(dst + bb * 32, src + bb * 16);
-              cp_async16(dst + bb * 32 + 16, src + bb * 16 + 2);
-            }
-          }
-        }
-      }
-      cp_commit();
-    };
-    auto blk = [&](const T* sl, int bb, double (&v)[4]) { ld4(sl + bb * 4, v); };
-    auto gx_of = [&](int i) {
-      int gx = G.s0x + i;
-      gx += gx < 0 ? A.nx : 0;
-      return gx >= A.nx ? gx - A.nx : gx;
-    };
-    auto load_r = [&](int k) -> double {
-      const int i = k - 2 * rl;
-      return (row_ok && i >= 0 && i < ex && k < nF) ? __ldg(rrow + gx_of(i)) : 0.0;
-    };
-    auto step_bar = [&]() { asm volatile("bar.sync 1, 160;" ::: "memory"); };
-    auto v_bar = [&]() { asm volatile("bar.sync 2, 128;" ::: "memory"); };
-    auto e_bar = [&]() { asm volatile("bar.sync 3, 128;" ::: "memory"); };
-    auto dot4 = [&](const double (&m)[4], const double (&v)[4], double acc) {
-      acc = fma(-m[0], v[0], acc);
-      acc = fma(-m[1], v[1], acc);
-      acc = fma(-m[2], v[2], acc);
-      return fma(-m[3], v[3], acc);
-    };
-    auto Erow = [&](int k, int row) -> const double* { return E + ((k & 7) * 32 + row) * 4; };
-
-    const long long cf0 = clock64();
-    long long gt0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
-    for (int p = 0; p < kLD; ++p) issue(p);
-    // ================================================================ forward sweep (L y = r)
-    //   y(k) = pre(k) - L3(k).Ya1 - L5(k).y(k-1);  pre(k+1) = half(k+1) - L2.Ya1 - L4.y(k-1);
-    //   half(k+2) = r(k+2) - L0.aa4(k+2) - L1.Ya1   (two-step look-ahead as in k_apply)
-    {
-      double pre, half;
-      double q0, q1, q2, q3;
-      q0 = load_r(2); q1 = load_r(3); q2 = load_r(4); q3 = load_r(5);
-      const double r0v = load_r(0), r1v = load_r(1);
-      cp_wait<kLD - 3>();                          // steps 0..2 landed
-      step_bar();
-      {
-        const bool top = rl == 0;
-        double h10[4], h00[4], h01[4], a[4], bb[4];
-        ld4(hcell(1, 0), h10);
-        ld4(hcell(0, 0), h00);
-        ld4(hcell(0, 1), h01);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) { h10[u] = top ? h10[u] : 0.0; h00[u] = top ? h00[u] : 0.0; h01[u] = top ? h01[u] : 0.0; }
-        blk(slot_ptr(0), 0, a); blk(slot_ptr(0), 2, bb);
-        pre = dot4(bb, h10, dot4(a, h00, r0v));        // (0,-2), (0,-1) of step 0
-        blk(slot_ptr(1), 0, a); blk(slot_ptr(1), 1, bb);
-        half = dot4(bb, h10, dot4(a, h01, r1v));       // (0,-2), (-1,-1) of step 1
-      }
-      auto fiter = [&](int k, double r2) {
-        if (A.dbg & 1) { step_bar(); return; }
-        const int i = k - 2 * rl;
-        const bool active = row_ok && i >= 0 && i < ex;
-        double L3[4], L5[4], N2[4], N4[4], M0[4], M1[4];
-        cp_wait<kLD - 3>();                                           // steps k, k+1, k+2 landed
-        blk(slot_ptr(k), 3, L3); blk(slot_ptr(k), 5, L5);
-        blk(slot_ptr(k + 1), 2, N2); blk(slot_ptr(k + 1), 4, N4);
-        blk(slot_ptr(k + 2), 0, M0); blk(slot_ptr(k + 2), 1, M1);
-        step_bar();                                                   // E[k-1] complete; halo cells ready
-        double Ya1[4], yp[4], aa4[4];
-        ld4(rl >= 1 ? Erow(k - 1, rl - 1) : hcell(1, k + 1), Ya1);
-        ld4(Erow(k - 1, rl), yp);
-        ld4(rl >= 2 ? Erow(k - 2, rl - 2) : (rl == 1 ? hcell(1, k) : hcell(0, k + 2)), aa4);
-        const double a0 = dot4(L3, Ya1, pre);
-        const double a1 = dot4(L5, yp, 0.0);
-        const double y = active ? a0 + a1 : 0.0;
-        E[((k & 7) * 32 + rl) * 4 + c] = y;
-        const double b0 = dot4(N2, Ya1, half);
-        const double b1 = dot4(N4, yp, 0.0);
-        const double c0 = dot4(M0, aa4, r2);
-        const double c1 = dot4(M1, Ya1, 0.0);
-        pre = b0 + b1;
-        half = c0 + c1;
-        if (!(A.dbg & 4)) ybuf[(size_t)k * 128] = y;
-        st_remote1_if(!(A.dbg & 4) && dn_remote && active && rl >= R - 2, hcell(min(max(rl - (R - 2), 0), 1), i) + c,
-                      (unsigned)min(s + 1, CS - 1), y);
-        issue(k + kLD);                                               // slot of step k is free now
-      };
-      for (int k0 = 0; k0 < nFp; k0 += 4) {
-        fiter(k0, q0); q0 = load_r(k0 + 6);
-        fiter(k0 + 1, q1); q1 = load_r(k0 + 7);
-        fiter(k0 + 2, q2); q2 = load_r(k0 + 8);
-        fiter(k0 + 3, q3); q3 = load_r(k0 + 9);
-      }
-    }
-    const long long cf1 = clock64();
-    e_bar();
-    for (int k = tid; k < 8 * 128; k += 128) E[k] = 0.0;
-    e_bar();
-
-    // ================================================================ backward sweep (U x = y)
-    {
-      const int dR = 2 * (R - 1);
-      const int K = nFp - 1;
-      auto pofk = [&](int k) { return 2 * nFp - 1 - k; };
-      double pre, half;
-      double q0, q1, q2, q3;
-      auto load_y = [&](int k) -> double { return k >= 0 ? ybuf[(size_t)k * 128] : 0.0; };
-      q0 = load_y(K - 2); q1 = load_y(K - 3); q2 = load_y(K - 4); q3 = load_y(K - 5);
-      const double yK = load_y(K), yK1 = load_y(K - 1);
-      cp_wait<kLD - 3>();                          // the first three backward steps landed
-      step_bar();
-      {
-        const int iR = K - dR;
-        const bool bot = rl == R - 1, bot2 = rl == R - 2;
-        double h2a[4], h2b[4], h2c[4], h3a[4], h3b[4];
-        ld4(hcell(2, iR), h2a);
-        ld4(hcell(2, iR + 1), h2b);
-        ld4(hcell(2, iR + 2), h2c);
-        ld4(hcell(3, iR), h3a);
-        ld4(hcell(3, iR - 1), h3b);
-        double Xb2[4], Xb3[4], bb4[4], bb4n[4], a[4], bb[4], cc[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          Xb2[u] = bot ? h2a[u] : 0.0;
-          Xb3[u] = bot ? h2b[u] : 0.0;
-          bb4[u] = bot ? h3a[u] : (bot2 ? h2c[u] : 0.0);
-          bb4n[u] = bot ? h3b[u] : (bot2 ? h2b[u] : 0.0);
-        }
-        blk(slot_ptr(pofk(K)), 6, a); blk(slot_ptr(pofk(K)), 5, bb); blk(slot_ptr(pofk(K)), 4, cc);
-        pre = dot4(cc, Xb2, dot4(bb, Xb3, dot4(a, bb4, yK)));     // (0,2), (1,1), (0,1)
-        blk(slot_ptr(pofk(K - 1)), 6, a); blk(slot_ptr(pofk(K - 1)), 5, bb);
-        half = dot4(bb, Xb2, dot4(a, bb4n, yK1));                 // (0,2), (1,1) of step K-1
-      }
-      auto biter = [&](int k, double y2) {
-        if (A.dbg & 1) { step_bar(); v_bar(); return; }
-        const int i = k - 2 * rl;
-        const bool active = row_ok && i >= 0 && i < ex;
-        const int iR = k - dR;
-        const int p = pofk(k);
-        double U3[4], U1[4], Dg[4], N4[4], N2[4], M6[4], M5[4];
-        cp_wait<kLD - 3>();
-        blk(slot_ptr(p), 3, U3); blk(slot_ptr(p), 1, U1); blk(slot_ptr(p), 0, Dg);
-        blk(slot_ptr(p + 1), 4, N4); blk(slot_ptr(p + 1), 2, N2);
-        blk(slot_ptr(p + 2), 6, M6); blk(slot_ptr(p + 2), 5, M5);
-        step_bar();                                                   // E[k+1] complete; halo cells ready
-        double Xb1[4], xp[4], bb4[4];
-        ld4(rl <= R - 2 ? Erow(k + 1, rl + 1) : hcell(2, iR - 1), Xb1);
-        ld4(Erow(k + 1, rl), xp);
-        ld4(rl <= R - 3 ? Erow(k + 2, rl + 2) : (rl == R - 2 ? hcell(2, iR) : hcell(3, iR - 2)), bb4);
-        const double a0 = dot4(U3, Xb1, pre);
-        const double a1 = dot4(U1, xp, 0.0);
-        V[rl * 4 + c] = a0 + a1;
-        const double b0 = dot4(N4, Xb1, half);
-        const double b1 = dot4(N2, xp, 0.0);
-        const double c0 = dot4(M6, bb4, y2);
-        const double c1 = dot4(M5, Xb1, 0.0);
-        v_bar();
-        double v[4];
-        ld4(V + rl * 4, v);
-        const double x = active ? -dot4(Dg, v, 0.0) : 0.0;
-        E[((k & 7) * 32 + rl) * 4 + c] = x;
-        pre = b0 + b1;
-        half = c0 + c1;
-        st_global_if(!(A.dbg & 4) && active && own_row && i >= G.ox0 && i < G.ox0 + G.ownx, zrow + gx_of(min(max(i, 0), ex - 1)), x);
-        st_remote1_if(!(A.dbg & 4) && up_remote && active && rl < 2, hcell(2 + min(rl, 1), i) + c, (unsigned)max(s - 1, 0), x);
-        issue(p + kLD);
-      };
-      for (int kb0 = 0; kb0 < nFp; kb0 += 4) {
-        const int k0 = K - kb0;
-        biter(k0, q0); q0 = load_y(k0 - 6);
-        biter(k0 - 1, q1); q1 = load_y(k0 - 7);
-        biter(k0 - 2, q2); q2 = load_y(k0 - 8);
-        biter(k0 - 3, q3); q3 = load_y(k0 - 9);
-      }
-    }
-    cp_wait<0>();
-    if (A.prof && tid == 0) {
-      long long gt1;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
-      long long* pq = g_prof + blockIdx.x * 8;
-      pq[0] = cf1 - cf0; pq[1] = clock64() - cf1; pq[2] = 0; pq[3] = 0; pq[4] = gt0; pq[5] = gt1; pq[6] = 0;
-    }
-  }
-}
 
 // ------------------------------------------------------------------------------------------ host
 struct Plan {
@@ -1007,15 +755,12 @@ static size_t smem_for(const Dims& D, int RPC, bool f32) {
   return stage + 2 * (size_t)ns * 8 + (size_t)4 * (D.exmax + 4) * 4 * 8 + (size_t)9 * 128 * 8 + (size_t)kgp_of(D, RPC) * 4 +
          (size_t)2 * kgp_of(D, RPC) * 16;
 }
-// bulk-copy gatekeeper kernel (default, 0.52 ms at config 2) or the per-lane cp.async variant
-// (NKS_RAS2D_LD=1: 0.75 ms -- the per-step work, not the copy pipeline, bounds the step)
-static bool use_ld() { return std::getenv("NKS_RAS2D_LD") != nullptr; }
+// (A per-lane cp.async variant of the apply -- every consumer lane fetching its own block rows with
+// LDGSTS, no bulk copies -- measured 0.75 ms against the bulk-copy kernel's 0.52 ms and was removed.)
+static bool use_gl() { return std::getenv("NKS_RAS2D_GL") != nullptr; }
 static const void* apply_fn(bool f32) {
-  if (use_ld()) return f32 ? (const void*)k_apply_ld<true> : (const void*)k_apply_ld<false>;
-  return f32 ? (const void*)k_apply<true> : (const void*)k_apply<false>;
-}
-static size_t smem_ld(const Dims& D, int RPC) {
-  return (size_t)kLD * 128 * kSLOTB + (size_t)4 * (D.exmax + 4) * 4 * 8 + (size_t)9 * 128 * 8 + (size_t)kgp_of(D, RPC) * 4;
+  if (use_gl()) return f32 ? (const void*)k_apply<true, true> : (const void*)k_apply<false, true>;
+  return f32 ? (const void*)k_apply<true, false> : (const void*)k_apply<false, false>;
 }
 void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaStream_t stream, std::string& why, bool f32) {
   Dims D;
@@ -1038,7 +783,7 @@ void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaSt
       continue;
     }
     const int rpc = (D.eymax + cs - 1) / cs;
-    const size_t sm = use_ld() ? smem_ld(D, rpc) : smem_for(D, rpc, f32);
+    const size_t sm = smem_for(D, rpc, f32);
     if (sm > (size_t)maxsm) continue;
     if (cudaFuncSetAttribute(apply_fn(f32), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
       cudaGetLastError();
@@ -1153,8 +898,8 @@ cudaError_t launch_apply(void* plan, const double* r, double* z, cudaStream_t s)
   A.prof = prof ? 1 : 0;
   static const int dbg = std::getenv("NKS_RAS2D_DBG") ? std::atoi(std::getenv("NKS_RAS2D_DBG")) : 0;
   A.dbg = dbg;
-  cudaError_t e = use_ld() ? (P->f32 ? cudaLaunchKernelEx(&cfg, k_apply_ld<true>, A) : cudaLaunchKernelEx(&cfg, k_apply_ld<false>, A))
-                           : (P->f32 ? cudaLaunchKernelEx(&cfg, k_apply<true>, A) : cudaLaunchKernelEx(&cfg, k_apply<false>, A));
+  cudaError_t e = use_gl() ? (P->f32 ? cudaLaunchKernelEx(&cfg, k_apply<true, true>, A) : cudaLaunchKernelEx(&cfg, k_apply<false, true>, A))
+                           : (P->f32 ? cudaLaunchKernelEx(&cfg, k_apply<true, false>, A) : cudaLaunchKernelEx(&cfg, k_apply<false, false>, A));
   if (prof && e == cudaSuccess) {
     static int calls = 0;
     if (++calls % 10 == 0) {
