@@ -215,7 +215,20 @@ def config_dict(cfg, ngpus, sharded=False):
             "init": "c=0.1622+U(-0.005,0.005), eta=0.1+U(-0.01,0.01), seed 0, u0=FFT equilibrium",
             "parallelism": (f"z-slabs x {ngpus} (sharded NKS step, NCCL halo exchange + allreduce)" if sharded
                             else ("replicas" if ngpus > 1 else "1 GPU")),
-            "l2": "working set > 126 MB L2 (BILU factors ~0.46 GB + Krylov basis ~0.26 GB); no flush"}
+            "l2": l2_note(cfg)}
+
+
+def l2_note(cfg):
+    """Working set of the timed step against the 126 MB L2: the BILU factors over the overlapped boxes
+    (13 / 25 point blocks of nf x nf doubles per box position) and the GMRES(30) basis."""
+    d = len(cfg["shape"])
+    nf = 2 + d
+    ext = [n // s + 2 * cfg["overlap"] for n, s in zip(cfg["shape"], cfg["nsub"])]
+    P = int(np.prod(ext)) * int(np.prod(cfg["nsub"]))
+    fac = 8 * (13 if d == 2 else 25) * nf * nf * P
+    basis = 8 * 31 * nf * int(np.prod(cfg["shape"]))
+    return (f"working set > 126 MB L2 (BILU factors ~{fac / 1e9:.2f} GB + Krylov basis ~{basis / 1e9:.2f} GB); "
+            "no flush")
 
 
 # ------------------------------------------------------------------------------------------- GPU arm

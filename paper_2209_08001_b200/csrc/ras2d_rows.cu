@@ -7,7 +7,7 @@
 // above] and (i,j-2).  Lane rl owns box row j = r0 + rl and processes point i = k - 2 rl at step k,
 // so every step of the CTA is one wavefront t = 2 r0 + k.  Warp c computes output component c of
 // every row (a quarter of the arithmetic per step: 24 DFMA and 12 16-byte loads of its block rows);
-// the four warps exchange each step's 4-vectors through a shared ring E[8][32][4] with one named
+// the four warps exchange each step's 4-vectors through a shared ring E (two planes [8][32][2]) with one named
 // barrier per step (two in the backward sweep, whose inverted diagonal block mixes components).
 // Only the two lag-1 blocks are on the loop-carried chain: iteration k finishes step k with them and
 // accumulates the four older-neighbour blocks of step k+1 (software pipeline).
@@ -495,7 +495,16 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       acc = fma(-m[2], v[2], acc);
       return fma(-m[3], v[3], acc);
     };
-    auto Erow = [&](int k, int row) -> const double* { return E + ((k & 7) * 32 + row) * 4; };
+    // E holds components (0,1) and (2,3) in two planes [8][32][2] 512 doubles apart, so a lane's two
+    // 16-byte loads of a neighbour's 4-vector hit consecutive 16-byte slots (4 wavefronts per warp
+    // load instead of 8 with the interleaved [8][32][4] layout); halo cells keep 4 contiguous doubles
+    auto Erow = [&](int k, int row) -> const double* { return E + ((k & 7) * 32 + row) * 2; };
+    constexpr int kEP = 512;          // plane offset of components (2,3)
+    auto ld4s = [&](const double* p, int off2, double (&v)[4]) {
+      const double2 a = *reinterpret_cast<const double2*>(p), b = *reinterpret_cast<const double2*>(p + off2);
+      v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    };
+    auto Est = [&](int k, double val) { E[(c >> 1) * kEP + ((k & 7) * 32 + rl) * 2 + (c & 1)] = val; };
     long long t_bar = 0, t_stage = 0, t_poll = 0;
     (void)t_bar;
 
@@ -544,14 +553,14 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         const bool active = row_ok && i >= 0 && i < ex;
         step_bar();                                                   // E[k-1] complete; stages/cells ready
         double Ya1[4], yp[4], aa4[4];
-        ld4(rl >= 1 ? Erow(k - 1, rl - 1) : hcell(1, k + 1), Ya1);   // (i+1, j-1) at step k-1
-        ld4(Erow(k - 1, rl), yp);                                     // own row at step k-1
-        ld4(rl >= 2 ? Erow(k - 2, rl - 2) : (rl == 1 ? hcell(1, k) : hcell(0, k + 2)), aa4);
+        ld4s(rl >= 1 ? Erow(k - 1, rl - 1) : hcell(1, k + 1), rl >= 1 ? kEP : 2, Ya1);   // (i+1, j-1) at step k-1
+        ld4s(Erow(k - 1, rl), kEP, yp);                                                    // own row at step k-1
+        ld4s(rl >= 2 ? Erow(k - 2, rl - 2) : (rl == 1 ? hcell(1, k) : hcell(0, k + 2)), rl >= 2 ? kEP : 2, aa4);
         preload(nxt, k + 1);
         const double a0 = dot4(cur.L3, Ya1, pre);                     // (1,-1)
         const double a1 = dot4(cur.L5, yp, 0.0);                      // (-1,0)
         const double y = active ? a0 + a1 : 0.0;
-        E[((k & 7) * 32 + rl) * 4 + c] = y;
+        Est(k, y);
         const double b0 = dot4(cur.N2, Ya1, half);                    // pre(k+1): (0,-1)
         const double b1 = dot4(cur.N4, yp, 0.0);                      //           (-2,0)
         const double c0 = dot4(cur.M0, aa4, r2);                      // half(k+2): (0,-2)
@@ -645,14 +654,14 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         const int iR = k - dR;
         step_bar();                                                   // E[k+1] complete; stages/cells ready
         double Xb1[4], xp[4], bb4[4];
-        ld4(rl <= R - 2 ? Erow(k + 1, rl + 1) : hcell(2, iR - 1), Xb1);   // (i-1, j+1) at step k+1
-        ld4(Erow(k + 1, rl), xp);                                          // own row at step k+1
-        ld4(rl <= R - 3 ? Erow(k + 2, rl + 2) : (rl == R - 2 ? hcell(2, iR) : hcell(3, iR - 2)), bb4);
+        ld4s(rl <= R - 2 ? Erow(k + 1, rl + 1) : hcell(2, iR - 1), rl <= R - 2 ? kEP : 2, Xb1);   // (i-1, j+1) at step k+1
+        ld4s(Erow(k + 1, rl), kEP, xp);                                                            // own row at step k+1
+        ld4s(rl <= R - 3 ? Erow(k + 2, rl + 2) : (rl == R - 2 ? hcell(2, iR) : hcell(3, iR - 2)), rl <= R - 3 ? kEP : 2, bb4);
         preload(nxt, k - 1);
         const double a0 = dot4(cur.U3, Xb1, pre);                     // (-1,1)
         const double a1 = dot4(cur.U1, xp, 0.0);                      // (1,0)
         const double x = active ? a0 + a1 : 0.0;
-        E[((k & 7) * 32 + rl) * 4 + c] = x;
+        Est(k, x);
         const double b0 = dot4(cur.N4, Xb1, half);                    // pre(k-1): (0,1)
         const double b1 = dot4(cur.N2, xp, 0.0);                      //           (2,0)
         const double c0 = dot4(cur.M6, bb4, ydot(cur.DM, y2));        // half(k-2): (0,2)
