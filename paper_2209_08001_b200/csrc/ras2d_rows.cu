@@ -219,11 +219,16 @@ __global__ void k_pack(Args A, const double* __restrict__ fac, long long ld, int
 // (LDG, one step ahead into the second register set) and the producer only prefetches the groups
 // ahead into L2 -- no shared-memory staging, so the factor bytes cross the SM's L1/shared data path
 // once instead of twice (bulk-copy write + LDS read).
-template <bool F32, bool GL>
+// W1 = true: one consumer warp computes all four components of its rows (lane = row, neighbour rows by
+// warp shuffles), so the step needs no cross-warp exchange; the CTA is that warp plus the producer.
+template <bool F32, bool GL, bool W1>
 __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   using S = Strm<F32>;
   using T = typename S::T;
   constexpr int kPF = S::PF, kPB = S::PB, kG = S::G, kNSW = S::NS;
+  constexpr int NCW = W1 ? 1 : 4;             // consumer warps; the producer is warp NCW
+  constexpr int NT = 32 * (NCW + 1);          // threads on the step barrier
+  constexpr int kRel = W1 ? 1 : 2;            // group g is released in iteration g kG + kG - kRel
   extern __shared__ __align__(128) unsigned char smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const int s = (int)cluster.block_rank();
@@ -266,7 +271,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   if (tid == 0) {
     for (int k = 0; k < kNSW; ++k) {
       mbar_init(&fullb[k], 1);
-      mbar_init(&emptyb[k], 4);       // one arrive per consumer warp
+      mbar_init(&emptyb[k], NCW);     // one arrive per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -298,7 +303,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   // between the sweeps.
   auto gof = [&](int p) { return p / kG; };   // group of processing step p (forward k = p, backward k = 2 nFp - 1 - p)
 
-  if (w == 4) {
+  if (w == NCW) {
     // ================================================================ producer / gatekeeper
     const unsigned full0 = smem_u32(fullb), empty0 = smem_u32(emptyb), stage0 = smem_u32(stage);
     const long long base = sb * RPC * A.exmax;
@@ -333,7 +338,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     // per-step path); the mbarrier test remains only as the blocking fallback.
     int nbars = 0;
     auto freed = [&](int g) {
-      const int pr = g * kG + kG - 2;
+      const int pr = g * kG + kG - kRel;
       return nbars >= pr + 3 + (pr >= nFp ? 1 : 0);
     };
     // issue groups in order up to G; blocking: wait for the buffer, else stop at the first busy one
@@ -397,7 +402,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         if (++sp > (1u << 26)) __trap();          // a lost neighbour would otherwise hang the GPU
       }
     };
-    auto step_bar = [&]() { asm volatile("bar.sync 1, 160;" ::: "memory"); ++nbars; };
+    auto step_bar = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); ++nbars; };
     // ---- forward: prologue barrier, then one barrier per step k
     ensure(gof(2));
     poll3(up_remote, 1, 0, 0, 0, 0, 1);
@@ -428,6 +433,222 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       ensure(gof(p + 3));
       poll3(dn_remote, 2, iR - 1, 2, iR, 3, iR - 2);
       step_bar();
+    }
+  } else if constexpr (W1) {
+    // ================================================================ one consumer warp, all components
+    const int rl = lane;
+    const bool row_ok = rl < R;
+    const int j = r0 + rl;
+    int gy = (G.s0y + j) % A.ny;
+    if (gy < 0) gy += A.ny;
+    const bool own_row = row_ok && j >= G.oy0 && j < G.oy0 + G.owny;
+    const long long N = A.N;
+    const double* rrow = A.r + (long long)gy * A.nx;            // + c N
+    double* zrow = A.z + (long long)gy * A.nx;                  // + c N
+    double* yrow = A.yscr + sb * A.KGp * 128 + rl * 4;          // y(k) of this row: yrow[k * 128 + 0..3]
+    const unsigned empty0 = smem_u32(emptyb);
+    auto gx_of = [&](int i) {
+      int gx = G.s0x + i;
+      gx += gx < 0 ? A.nx : 0;
+      return gx >= A.nx ? gx - A.nx : gx;
+    };
+    auto zero4 = [&](double (&v)[4]) { v[0] = v[1] = v[2] = v[3] = 0.0; };
+    auto load_r4 = [&](int k, double (&v)[4]) {
+      const int i = k - 2 * rl;
+      if (row_ok && i >= 0 && i < ex && k < nF) {
+        const int gx = gx_of(i);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] = __ldg(rrow + c * N + gx);
+      } else zero4(v);
+    };
+    auto release_group = [&](int q) {
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(empty0 + (q % kNSW) * 8) : "memory");
+    };
+    auto step_bar = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); };
+    // block rows of processing step p: block b, row c at ptr + b * 16 + c * 4 (active lanes only)
+    struct Ref { const T* ptr; bool on; };
+    auto rowt = [&](int p, int pf) -> Ref {
+      const int4 t = tb[p];
+      return Ref{stage + t.x + rl * pf, rl >= t.y && rl <= t.z};
+    };
+    // acc_c -= B(row c) . v for the four rows c of block b
+    auto mv4 = [&](const Ref& r, int blk, const double (&v)[4], double (&acc)[4]) {
+      if (!r.on) return;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double m[4];
+        ld4(r.ptr + blk * 16 + c * 4, m);
+        acc[c] = fma(-m[0], v[0], fma(-m[1], v[1], fma(-m[2], v[2], fma(-m[3], v[3], acc[c]))));
+      }
+    };
+    auto shfl_up4 = [&](const double (&v)[4], int d, double (&o)[4]) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) o[c] = __shfl_up_sync(0xffffffffu, v[c], d);
+    };
+    auto shfl_dn4 = [&](const double (&v)[4], int d, double (&o)[4]) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) o[c] = __shfl_down_sync(0xffffffffu, v[c], d);
+    };
+    // ---------------------------------------------------------------- forward sweep (L y = r)
+    {
+      double pre[4], half[4], yp[4], yp2[4];
+      zero4(yp); zero4(yp2);
+      double q0[4], q1[4], q2[4], q3[4];
+      load_r4(2, q0); load_r4(3, q1); load_r4(4, q2); load_r4(5, q3);
+      double r0v[4], r1v[4];
+      load_r4(0, r0v); load_r4(1, r1v);
+      step_bar();
+      {
+        const bool top = rl == 0;
+        double h10[4], h00[4], h01[4];
+        ld4(hcell(1, 0), h10); ld4(hcell(0, 0), h00); ld4(hcell(0, 1), h01);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { h10[u] = top ? h10[u] : 0.0; h00[u] = top ? h00[u] : 0.0; h01[u] = top ? h01[u] : 0.0; }
+        const Ref a0 = rowt(0, kPF), a1 = rowt(1, kPF);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { pre[c] = r0v[c]; half[c] = r1v[c]; }
+        mv4(a0, 0, h00, pre); mv4(a0, 2, h10, pre);       // (0,-2), (0,-1) of step 0
+        mv4(a1, 0, h01, half); mv4(a1, 1, h10, half);     // (0,-2), (-1,-1) of step 1
+      }
+      auto fiter = [&](int k, const double (&r2)[4]) {
+        const int i = k - 2 * rl;
+        const bool active = row_ok && i >= 0 && i < ex;
+        step_bar();
+        double Ya1[4], aa4[4];
+        shfl_up4(yp, 1, Ya1);                              // (i+1, j-1) at step k-1
+        shfl_up4(yp2, 2, aa4);                             // row j-2 at step k-2
+        if (rl == 0) { ld4(hcell(1, k + 1), Ya1); ld4(hcell(0, k + 2), aa4); }
+        if (rl == 1) ld4(hcell(1, k), aa4);
+        const Ref rk = rowt(k, kPF);
+        const Ref rk1 = k + 1 < nFp ? rowt(k + 1, kPF) : Ref{stage, false};
+        const Ref rk2 = k + 2 < nFp ? rowt(k + 2, kPF) : Ref{stage, false};
+        double y[4], a1[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { y[c] = pre[c]; a1[c] = 0.0; }
+        mv4(rk, 3, Ya1, y);                                // (1,-1)
+        mv4(rk, 5, yp, a1);                                // (-1,0)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) y[c] = active ? y[c] + a1[c] : 0.0;
+        double b1[4], c1[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { pre[c] = half[c]; b1[c] = 0.0; half[c] = r2[c]; c1[c] = 0.0; }
+        mv4(rk1, 2, Ya1, pre); mv4(rk1, 4, yp, b1);        // pre(k+1): (0,-1), (-2,0)
+        mv4(rk2, 0, aa4, half); mv4(rk2, 1, Ya1, c1);      // half(k+2): (0,-2), (-1,-1)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { pre[c] += b1[c]; half[c] += c1[c]; yp2[c] = yp[c]; yp[c] = y[c]; }
+        if (row_ok) {
+          reinterpret_cast<double2*>(yrow + (size_t)k * 128)[0] = make_double2(y[0], y[1]);
+          reinterpret_cast<double2*>(yrow + (size_t)k * 128)[1] = make_double2(y[2], y[3]);
+        }
+        const bool push = dn_remote && active && rl >= R - 2;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          st_remote1_if(push, hcell(min(max(rl - (R - 2), 0), 1), i) + c, (unsigned)min(s + 1, CS - 1), y[c]);
+        if (k % kG == kG - kRel) release_group(gof(k));
+      };
+      for (int k0 = 0; k0 < nFp; k0 += 4) {
+        fiter(k0, q0); load_r4(k0 + 6, q0);
+        fiter(k0 + 1, q1); load_r4(k0 + 7, q1);
+        fiter(k0 + 2, q2); load_r4(k0 + 8, q2);
+        fiter(k0 + 3, q3); load_r4(k0 + 9, q3);
+      }
+    }
+    __syncwarp();
+    // ---------------------------------------------------------------- backward sweep (U' x = y', folded)
+    {
+      const int dR = 2 * (R - 1);
+      const int K = nFp - 1;
+      auto pofk = [&](int k) { return 2 * nFp - 1 - k; };
+      auto load_y4 = [&](int k, double (&v)[4]) {
+        if (k >= 0) {
+          const double2 a = *reinterpret_cast<const double2*>(yrow + (size_t)k * 128);
+          const double2 b = *reinterpret_cast<const double2*>(yrow + (size_t)k * 128 + 2);
+          v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+        } else zero4(v);
+      };
+      // acc_c = (D^-1 row c) . y
+      auto dy4 = [&](const Ref& r, const double (&y4)[4], double (&acc)[4]) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          double m[4];
+          if (r.on) ld4(r.ptr + c * 4, m); else zero4(m);
+          acc[c] = fma(m[3], y4[3], fma(m[2], y4[2], fma(m[1], y4[1], m[0] * y4[0])));
+        }
+      };
+      double pre[4], half[4], xp[4], xp2[4];
+      zero4(xp); zero4(xp2);
+      double q0[4], q1[4], q2[4], q3[4];
+      load_y4(K - 2, q0); load_y4(K - 3, q1); load_y4(K - 4, q2); load_y4(K - 5, q3);
+      double yK[4], yK1[4];
+      load_y4(K, yK); load_y4(K - 1, yK1);
+      step_bar();
+      {
+        const int iR = K - dR;
+        const bool bot = rl == R - 1, bot2 = rl == R - 2;
+        double h2a[4], h2b[4], h2c[4], h3a[4], h3b[4];
+        ld4(hcell(2, iR), h2a); ld4(hcell(2, iR + 1), h2b); ld4(hcell(2, iR + 2), h2c);
+        ld4(hcell(3, iR), h3a); ld4(hcell(3, iR - 1), h3b);
+        double Xb2[4], Xb3[4], bb4[4], bb4n[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          Xb2[u] = bot ? h2a[u] : 0.0;
+          Xb3[u] = bot ? h2b[u] : 0.0;
+          bb4[u] = bot ? h3a[u] : (bot2 ? h2c[u] : 0.0);
+          bb4n[u] = bot ? h3b[u] : (bot2 ? h2b[u] : 0.0);
+        }
+        const Ref u0 = rowt(pofk(K), kPB), u1 = rowt(pofk(K - 1), kPB);
+        dy4(u0, yK, pre);
+        mv4(u0, 6, bb4, pre); mv4(u0, 5, Xb3, pre); mv4(u0, 4, Xb2, pre);    // (0,2), (1,1), (0,1)
+        dy4(u1, yK1, half);
+        mv4(u1, 6, bb4n, half); mv4(u1, 5, Xb2, half);                       // (0,2), (1,1) of step K-1
+      }
+      auto biter = [&](int k, const double (&y2)[4]) {
+        const int i = k - 2 * rl;
+        const bool active = row_ok && i >= 0 && i < ex;
+        const int iR = k - dR;
+        step_bar();
+        double Xb1[4], bb4[4];
+        shfl_dn4(xp, 1, Xb1);                              // (i-1, j+1) at step k+1
+        shfl_dn4(xp2, 2, bb4);                             // row j+2 at step k+2
+        if (rl == R - 1) { ld4(hcell(2, iR - 1), Xb1); ld4(hcell(3, iR - 2), bb4); }
+        if (rl == R - 2) ld4(hcell(2, iR), bb4);
+        const int p = pofk(k);
+        const Ref rk = rowt(p, kPB);
+        const Ref rk1 = k - 1 >= 0 ? rowt(p + 1, kPB) : Ref{stage, false};
+        const Ref rk2 = k - 2 >= 0 ? rowt(p + 2, kPB) : Ref{stage, false};
+        double x[4], a1[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { x[c] = pre[c]; a1[c] = 0.0; }
+        mv4(rk, 3, Xb1, x);                                // (-1,1)
+        mv4(rk, 1, xp, a1);                                // (1,0)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) x[c] = active ? x[c] + a1[c] : 0.0;
+        double b1[4], c1[4], yd[4];
+        dy4(rk2, y2, yd);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { pre[c] = half[c]; b1[c] = 0.0; half[c] = yd[c]; c1[c] = 0.0; }
+        mv4(rk1, 4, Xb1, pre); mv4(rk1, 2, xp, b1);        // pre(k-1): (0,1), (2,0)
+        mv4(rk2, 6, bb4, half); mv4(rk2, 5, Xb1, c1);      // half(k-2): (0,2), (1,1)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { pre[c] += b1[c]; half[c] += c1[c]; xp2[c] = xp[c]; xp[c] = x[c]; }
+        const bool own = active && own_row && i >= G.ox0 && i < G.ox0 + G.ownx;
+        const int gx = gx_of(min(max(i, 0), ex - 1));
+#pragma unroll
+        for (int c = 0; c < 4; ++c) st_global_if(own, zrow + c * N + gx, x[c]);
+        const bool push = up_remote && active && rl < 2;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) st_remote1_if(push, hcell(2 + min(rl, 1), i) + c, (unsigned)max(s - 1, 0), x[c]);
+        if (p % kG == kG - kRel) release_group(gof(p));
+      };
+      for (int kb0 = 0; kb0 < nFp; kb0 += 4) {
+        const int k0 = K - kb0;
+        biter(k0, q0); load_y4(k0 - 6, q0);
+        biter(k0 - 1, q1); load_y4(k0 - 7, q1);
+        biter(k0 - 2, q2); load_y4(k0 - 8, q2);
+        biter(k0 - 3, q3); load_y4(k0 - 9, q3);
+      }
     }
   } else {
     // ================================================================ consumers
@@ -767,10 +988,13 @@ static size_t smem_for(const Dims& D, int RPC, bool f32) {
 // (A per-lane cp.async variant of the apply -- every consumer lane fetching its own block rows with
 // LDGSTS, no bulk copies -- measured 0.75 ms against the bulk-copy kernel's 0.52 ms and was removed.)
 static bool use_gl() { return std::getenv("NKS_RAS2D_GL") != nullptr; }
+static bool use_w1() { return std::getenv("NKS_RAS2D_W1") != nullptr; }
 static const void* apply_fn(bool f32) {
-  if (use_gl()) return f32 ? (const void*)k_apply<true, true> : (const void*)k_apply<false, true>;
-  return f32 ? (const void*)k_apply<true, false> : (const void*)k_apply<false, false>;
+  if (use_w1()) return f32 ? (const void*)k_apply<true, false, true> : (const void*)k_apply<false, false, true>;
+  if (use_gl()) return f32 ? (const void*)k_apply<true, true, false> : (const void*)k_apply<false, true, false>;
+  return f32 ? (const void*)k_apply<true, false, false> : (const void*)k_apply<false, false, false>;
 }
+static int apply_threads() { return use_w1() ? 64 : 160; }
 void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaStream_t stream, std::string& why, bool f32) {
   Dims D;
   if (!dims_of(g, D)) { why = "not 2D"; return nullptr; }
@@ -800,7 +1024,7 @@ void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaSt
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(D.nbox * cs, 1, 1);
-    cfg.blockDim = dim3(160, 1, 1);
+    cfg.blockDim = dim3(apply_threads(), 1, 1);
     cfg.dynamicSmemBytes = sm;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -893,7 +1117,7 @@ cudaError_t launch_apply(void* plan, const double* r, double* z, cudaStream_t s)
   A.z = z;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P->nbox * P->CS, 1, 1);
-  cfg.blockDim = dim3(160, 1, 1);
+  cfg.blockDim = dim3(apply_threads(), 1, 1);
   cfg.dynamicSmemBytes = P->smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -907,8 +1131,10 @@ cudaError_t launch_apply(void* plan, const double* r, double* z, cudaStream_t s)
   A.prof = prof ? 1 : 0;
   static const int dbg = std::getenv("NKS_RAS2D_DBG") ? std::atoi(std::getenv("NKS_RAS2D_DBG")) : 0;
   A.dbg = dbg;
-  cudaError_t e = use_gl() ? (P->f32 ? cudaLaunchKernelEx(&cfg, k_apply<true, true>, A) : cudaLaunchKernelEx(&cfg, k_apply<false, true>, A))
-                           : (P->f32 ? cudaLaunchKernelEx(&cfg, k_apply<true, false>, A) : cudaLaunchKernelEx(&cfg, k_apply<false, false>, A));
+  cudaError_t e;
+  if (use_w1()) e = P->f32 ? cudaLaunchKernelEx(&cfg, k_apply<true, false, true>, A) : cudaLaunchKernelEx(&cfg, k_apply<false, false, true>, A);
+  else if (use_gl()) e = P->f32 ? cudaLaunchKernelEx(&cfg, k_apply<true, true, false>, A) : cudaLaunchKernelEx(&cfg, k_apply<false, true, false>, A);
+  else e = P->f32 ? cudaLaunchKernelEx(&cfg, k_apply<true, false, false>, A) : cudaLaunchKernelEx(&cfg, k_apply<false, false, false>, A);
   if (prof && e == cudaSuccess) {
     static int calls = 0;
     if (++calls % 10 == 0) {
