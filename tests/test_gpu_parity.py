@@ -139,6 +139,32 @@ def test_ras_bilu0_apply_parity(shape, nsub, delta):
     assert max(errs) < 1e-10, errs
 
 
+RAS2D_VARIANTS = {"rows": {}, "rows_w1": {"NKS_RAS2D_W1": "1"}, "rows_gl": {"NKS_RAS2D_GL": "1"},
+                  "rows_cs16": {"NKS_RAS2D_CSMAX": "16"}, "quad": {"NKS_RAS2D_OLD": "1"}}
+
+
+@pytest.mark.parametrize("variant", sorted(RAS2D_VARIANTS))
+@pytest.mark.parametrize("shape,nsub,delta", [((96, 80), (3, 2), 2), ((70, 130), (1, 2), 1)])
+def test_ras2d_kernel_variants_apply_parity(monkeypatch, shape, nsub, delta, variant):
+    """Every 2D RAS apply kernel design (the default four-warp rows kernel, its one-warp-per-stripe and
+    global-load variants, up to 16 stripes per box, and the first quad-lane design) against the
+    oracle's left-RAS on boxes of several stripes with ragged stripe heights."""
+    for k, v in RAS2D_VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
+    nf = 4
+    Xa, Xb = states(shape)
+    dt = 0.3
+    g = gpu_solver(shape, nsub=nsub, overlap=delta)
+    g.set_fields(Xa[0], Xa[1], Xa[2:])
+    g.pc_setup(Xb, dt)
+    r = ni.random_direction(nf, shape, 12)
+    zg = g.pc_apply(r).cpu().numpy()
+    J = jacobian.assemble(oracle_model(2), Xa, Xb, dt)
+    zo = pc.RAS(J, shape, nf, tuple(reversed(nsub)), delta).apply(r)
+    errs = field_rel_err(zg, zo)
+    assert max(errs) < 1e-10, errs
+
+
 SCHWARZ_CASES = [((16, 16), (2, 2), 2, "as"), ((16, 16), (2, 2), 2, "rras"), ((12, 14), (1, 1), 2, "as"),
                  ((10, 13), (3, 2), 1, "rras"), ((6, 7, 6), (1, 1, 2), 1, "as"), ((6, 7, 6), (2, 1, 1), 1, "rras")]
 
