@@ -138,6 +138,20 @@ __device__ __forceinline__ void ldg4(const double* p, double (&v)[4]) {
   const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p + 2));
   v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
+// v <- p[0..3] (shared memory) when on, else unchanged; predicated, so it needs no divergent branch
+__device__ __forceinline__ void ld4_shared_if(bool on, const double* p, double (&v)[4]) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %4, 0;\n @q ld.shared.v2.f64 {%0, %1}, [%5];\n"
+               " @q ld.shared.v2.f64 {%2, %3}, [%5+16];\n}\n"
+               : "+d"(v[0]), "+d"(v[1]), "+d"(v[2]), "+d"(v[3])
+               : "r"((int)on), "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void ld4_shared_if(bool on, const float* p, double (&v)[4]) {
+  float a = 0.f, b = 0.f, c = 0.f, d = 0.f;
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %4, 0;\n @q ld.shared.v4.f32 {%0, %1, %2, %3}, [%5];\n}\n"
+               : "+f"(a), "+f"(b), "+f"(c), "+f"(d)
+               : "r"((int)on), "r"(smem_u32(p)));
+  if (on) { v[0] = a; v[1] = b; v[2] = c; v[3] = d; }
+}
 __device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
   const double2 a = *reinterpret_cast<const double2*>(p), b = *reinterpret_cast<const double2*>(p + 2);
   v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
@@ -403,20 +417,37 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       }
     };
     auto step_bar = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); ++nbars; };
+    // per-step path kept short (the producer shares an SM sub-partition with consumer warp 0): the copy
+    // bookkeeping only when a group boundary or a freed buffer needs it, and one poll per lane at a
+    // per-lane fixed cell offset (lanes 0-3 / 4-7 / 8-31 watch the step's three halo cells)
+    auto ensure_fast = [&](int G) {
+      G = min(G, 2 * nGr - 1);
+      const bool more = issued <= min(G + kNSW - 1, 2 * nGr - 1) && (issued < kNSW || freed(issued - kNSW));
+      if (ready >= G && !more && !GL) return;
+      ensure(G);
+    };
+    const int which = min(lane >> 2, 2);
+    const int qf = which == 1 ? 0 : 1, dcf = which == 0 ? 1 : (which == 1 ? 2 : 0);     // (1,k+1) (0,k+2) (1,k)
+    const int qb = which == 2 ? 3 : 2, dcb = which == 0 ? -1 : (which == 1 ? 0 : -2);  // (2,iR-1) (2,iR) (3,iR-2)
+    auto poll1 = [&](int q, int i) {
+      if (A.dbg & 16) return;
+      const unsigned sa = smem_u32(hcell(q, i) + (lane & 3));
+      unsigned sp = 0;
+      while (true) {
+        unsigned long long v;
+        asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"(sa) : "memory");
+        if (__all_sync(0xffffffffu, v != kSentinel)) break;
+        if (++sp > (1u << 26)) __trap();
+      }
+    };
     // ---- forward: prologue barrier, then one barrier per step k
     ensure(gof(2));
     poll3(up_remote, 1, 0, 0, 0, 0, 1);
     step_bar();
     for (int k = 0; k < nFp; ++k) {
-      const bool rec = A.prof && blockIdx.x == 0 && lane == 0 && k >= 40 && k < 48;
-      long long* gq = g_gt + (k - 40) * 8;
-      if (rec) gq[0] = clock64();
-      ensure(gof(k + 3));
-      if (rec) gq[1] = clock64();
-      poll3(up_remote, 1, k + 1, 0, k + 2, 1, k);
-      if (rec) gq[2] = clock64();
+      ensure_fast(gof(k + 3));
+      if (up_remote) poll1(qf, k + dcf);
       step_bar();
-      if (rec) gq[3] = clock64();
     }
     // ---- backward: prologue barrier, then one barrier per step (processing p = nFp .. 2 nFp - 1)
     const int dR = 2 * (R - 1);
@@ -429,9 +460,8 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     }
     for (int k = nFp - 1; k >= 0; --k) {
       const int p = 2 * nFp - 1 - k;
-      const int iR = k - dR;
-      ensure(gof(p + 3));
-      poll3(dn_remote, 2, iR - 1, 2, iR, 3, iR - 2);
+      ensure_fast(gof(p + 3));
+      if (dn_remote) poll1(qb, k - dR + dcb);
       step_bar();
     }
   } else if constexpr (W1) {
@@ -706,9 +736,12 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       const T* b0 = GL ? (p < nFp ? (const T*)A.chunkF : (const T*)A.chunkB) : stage;
       return RowRef{b0 + t.x + rl * pf + c * 4, rl >= t.y && rl <= t.z};
     };
+    // lanes without a row at that step keep stale (finite) values: every output of such a (lane, step)
+    // is discarded (y = active ? ... : 0), and no zeroing keeps ~60 selects and moves per step off the
+    // issue path
     auto ldrow_if = [&](const RowRef& r, int blk, double (&v)[4]) {
-      if (!r.on) { zero4(v); return; }
-      if (GL) ldg4(r.ptr + blk * 16, v); else ld4(r.ptr + blk * 16, v);
+      if (GL) { if (r.on) ldg4(r.ptr + blk * 16, v); return; }
+      ld4_shared_if(r.on, r.ptr + blk * 16, v);       // predicated loads: no divergent branch per row
     };
     auto dot4 = [&](const double (&m)[4], const double (&v)[4], double acc) {
       acc = fma(-m[0], v[0], acc);
@@ -745,12 +778,13 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       // step's exchange loads do not queue behind them)
       struct FRows { double L3[4], L5[4], N2[4], N4[4], M0[4], M1[4]; };
       FRows SA, SB;
-      auto preload = [&](FRows& S, int k) {      // rows for iteration k
+      auto preload = [&](FRows& S, int k) {      // rows for iteration k (steps past the sweep: none)
         if (A.dbg & 32) return;
-        if (k < nFp) { const RowRef r = rowt(k, kPF); ldrow_if(r, 3, S.L3); ldrow_if(r, 5, S.L5); } else { zero4(S.L3); zero4(S.L5); }
-        if (k + 1 < nFp) { const RowRef r = rowt(k + 1, kPF); ldrow_if(r, 2, S.N2); ldrow_if(r, 4, S.N4); } else { zero4(S.N2); zero4(S.N4); }
-        if (k + 2 < nFp) { const RowRef r = rowt(k + 2, kPF); ldrow_if(r, 0, S.M0); ldrow_if(r, 1, S.M1); } else { zero4(S.M0); zero4(S.M1); }
+        if (k < nFp) { const RowRef r = rowt(k, kPF); ldrow_if(r, 3, S.L3); ldrow_if(r, 5, S.L5); }
+        if (k + 1 < nFp) { const RowRef r = rowt(k + 1, kPF); ldrow_if(r, 2, S.N2); ldrow_if(r, 4, S.N4); }
+        if (k + 2 < nFp) { const RowRef r = rowt(k + 2, kPF); ldrow_if(r, 0, S.M0); ldrow_if(r, 1, S.M1); }
       };
+      for (FRows* S : {&SA, &SB}) { zero4(S->L3); zero4(S->L5); zero4(S->N2); zero4(S->N4); zero4(S->M0); zero4(S->M1); }
       double q0, q1, q2, q3;                       // r prefetch ring: r(k+2) is used at iteration k
       q0 = load_r(2); q1 = load_r(3); q2 = load_r(4); q3 = load_r(5);
       const double r0v = load_r(0), r1v = load_r(1);
@@ -819,14 +853,12 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       double pre, half;
       struct BRows { double U3[4], U1[4], N4[4], N2[4], M6[4], M5[4], DM[4]; };
       BRows SA, SB;
-      auto preload = [&](BRows& S, int k) {      // rows for iteration k
-        if (k >= 0) { const RowRef r = rowt(pofk(k), kPB); ldrow_if(r, 3, S.U3); ldrow_if(r, 1, S.U1); } else { zero4(S.U3); zero4(S.U1); }
-        if (k - 1 >= 0) { const RowRef r = rowt(pofk(k - 1), kPB); ldrow_if(r, 4, S.N4); ldrow_if(r, 2, S.N2); } else { zero4(S.N4); zero4(S.N2); }
-        if (k - 2 >= 0) {
-          const RowRef r = rowt(pofk(k - 2), kPB);
-          ldrow_if(r, 6, S.M6); ldrow_if(r, 5, S.M5); ldrow_if(r, 0, S.DM);
-        } else { zero4(S.M6); zero4(S.M5); zero4(S.DM); }
+      auto preload = [&](BRows& S, int k) {      // rows for iteration k (steps past the sweep: none)
+        if (k >= 0) { const RowRef r = rowt(pofk(k), kPB); ldrow_if(r, 3, S.U3); ldrow_if(r, 1, S.U1); }
+        if (k - 1 >= 0) { const RowRef r = rowt(pofk(k - 1), kPB); ldrow_if(r, 4, S.N4); ldrow_if(r, 2, S.N2); }
+        if (k - 2 >= 0) { const RowRef r = rowt(pofk(k - 2), kPB); ldrow_if(r, 6, S.M6); ldrow_if(r, 5, S.M5); ldrow_if(r, 0, S.DM); }
       };
+      for (BRows* S : {&SA, &SB}) { zero4(S->U3); zero4(S->U1); zero4(S->N4); zero4(S->N2); zero4(S->M6); zero4(S->M5); zero4(S->DM); }
       const double* yrow = A.yscr + sb * A.KGp * 128 + rl * 4;    // y(k) of this row: yrow[k * 128 + 0..3]
       auto load_y4 = [&](int k, double (&v)[4]) {
         if (A.dbg & 64) { v[0] = v[1] = v[2] = v[3] = 1e-3 * k; return; }
@@ -1145,15 +1177,6 @@ cudaError_t launch_apply(void* plan, const double* r, double* z, cudaStream_t s)
       long long tmin = h[4], tmax = 0;
       for (int c = 0; c < nc; ++c) { tmin = std::min(tmin, h[c * 8 + 4]); tmax = std::max(tmax, h[c * 8 + 5]); }
       std::fprintf(stderr, "[ras2d rows prof] CS %d RPC %d, span %lld ns\n", P->CS, P->RPC, tmax - tmin);
-      {
-        std::vector<long long> gt(72 * 8);
-        cudaMemcpyFromSymbol(gt.data(), g_gt, gt.size() * 8);
-        for (int k = 0; k < 8; ++k) {
-          const long long* q = &gt[k * 8];
-          std::fprintf(stderr, "  producer step %d: ensure %lld, poll %lld, bar %lld, to next %lld\n", 40 + k, q[1] - q[0], q[2] - q[1],
-                       q[3] - q[2], k < 7 ? gt[(k + 1) * 8] - q[3] : 0);
-        }
-      }
       {
         std::vector<long long> cp(64 * 4);
         cudaMemcpyFromSymbol(cp.data(), g_cp, cp.size() * 8);
