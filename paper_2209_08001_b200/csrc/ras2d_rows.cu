@@ -174,6 +174,16 @@ __device__ __forceinline__ void st_remote1_if(bool pred, double* local_equiv, un
                ::"r"((int)pred), "r"(raddr), "d"(v)
                : "memory");
 }
+__device__ __forceinline__ unsigned mapa_u32(const void* local_equiv, unsigned rank) {
+  unsigned raddr;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(local_equiv)), "r"(rank));
+  return raddr;
+}
+__device__ __forceinline__ void st_cluster_if(bool pred, unsigned raddr, double v) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %0, 0;\n @p st.relaxed.cluster.shared::cluster.f64 [%1], %2;\n}\n"
+               ::"r"((int)pred), "r"(raddr), "d"(v)
+               : "memory");
+}
 __device__ __forceinline__ void st_global_if(bool pred, double* p, double v) {
   asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %0, 0;\n @p st.global.f64 [%1], %2;\n}\n" ::"r"((int)pred), "l"(p),
                "d"(v)
@@ -544,7 +554,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       }
       auto fiter = [&](int k, const double (&r2)[4]) {
         const int i = k - 2 * rl;
-        const bool active = row_ok && i >= 0 && i < ex;
+        const bool active = row_ok && (unsigned)i < (unsigned)ex;
         step_bar();
         double Ya1[4], aa4[4];
         shfl_up4(yp, 1, Ya1);                              // (i+1, j-1) at step k-1
@@ -636,7 +646,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       }
       auto biter = [&](int k, const double (&y2)[4]) {
         const int i = k - 2 * rl;
-        const bool active = row_ok && i >= 0 && i < ex;
+        const bool active = row_ok && (unsigned)i < (unsigned)ex;
         const int iR = k - dR;
         step_bar();
         double Xb1[4], bb4[4];
@@ -803,9 +813,12 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         half = dot4(bb, h10, dot4(a, h01, r1v));       // (0,-2), (-1,-1) of step 1
         preload(SA, 0);
       }
+      // lanes R-2, R-1 push y into the next stripe's halo rows 0, 1 (cluster address of cell 0, + 32 B per i)
+      const bool dn_push = dn_remote && rl >= R - 2 && rl < R;
+      const unsigned dn_base = mapa_u32(hcell(min(max(rl - (R - 2), 0), 1), 0) + c, (unsigned)min(s + 1, CS - 1));
       auto fiter = [&](int k, double r2, FRows& cur, FRows& nxt) {
         const int i = k - 2 * rl;
-        const bool active = row_ok && i >= 0 && i < ex;
+        const bool active = row_ok && (unsigned)i < (unsigned)ex;
         step_bar();                                                   // E[k-1] complete; stages/cells ready
         double Ya1[4], yp[4], aa4[4];
         ld4s(rl >= 1 ? Erow(k - 1, rl - 1) : hcell(1, k + 1), rl >= 1 ? kEP : 2, Ya1);   // (i+1, j-1) at step k-1
@@ -823,8 +836,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         pre = b0 + b1;
         half = c0 + c1;
         if (!(A.dbg & 260)) ybuf[(size_t)k * 128] = y;
-        st_remote1_if(!(A.dbg & 4) && dn_remote && active && rl >= R - 2, hcell(min(max(rl - (R - 2), 0), 1), i) + c,
-                      (unsigned)min(s + 1, CS - 1), y);
+        st_cluster_if(!(A.dbg & 4) && dn_push && active, dn_base + (unsigned)(i * 32), y);
         if (k % kG == kG - 2) release_group(gof(k));   // the group's last rows are in registers now
       };
       for (int k0 = 0; k0 < nFp; k0 += 4) {
@@ -901,9 +913,12 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         half = dot4(bb, Xb2, dot4(a, bb4n, ydot(dd, yK1)));                 // (0,2), (1,1) of step K-1 (Xb3(K-1) = Xb2(K))
         preload(SA, K);
       }
+      // lanes 0, 1 push x into the previous stripe's halo rows 2, 3
+      const bool up_push = up_remote && rl < 2;
+      const unsigned up_base = mapa_u32(hcell(2 + min(rl, 1), 0) + c, (unsigned)max(s - 1, 0));
       auto biter = [&](int k, const double (&y2)[4], BRows& cur, BRows& nxt) {
         const int i = k - 2 * rl;
-        const bool active = row_ok && i >= 0 && i < ex;
+        const bool active = row_ok && (unsigned)i < (unsigned)ex;
         const int iR = k - dR;
         step_bar();                                                   // E[k+1] complete; stages/cells ready
         double Xb1[4], xp[4], bb4[4];
@@ -922,7 +937,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         pre = b0 + b1;
         half = c0 + c1;
         st_global_if(!(A.dbg & 256) && active && own_row && i >= G.ox0 && i < G.ox0 + G.ownx, zrow + gx_of(min(max(i, 0), ex - 1)), x);
-        st_remote1_if(up_remote && active && rl < 2, hcell(2 + min(rl, 1), i) + c, (unsigned)max(s - 1, 0), x);
+        st_cluster_if(up_push && active, up_base + (unsigned)(i * 32), x);
         const int p = pofk(k);
         if (p % kG == kG - 2) release_group(gof(p));
       };
