@@ -709,10 +709,18 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       gx += gx < 0 ? A.nx : 0;
       return gx >= A.nx ? gx - A.nx : gx;
     };
+    // r at (row, i = k - 2 rl): global x = s0x + i wraps at most once; 32-bit index arithmetic and a
+    // predicated load keep this off the per-step issue budget
+    const int gx0 = G.s0x - 2 * rl, nxg = A.nx;
+    const int nFr = row_ok ? nF : 0;              // rows past the stripe load nothing
     auto load_r = [&](int k) -> double {
       const int i = k - 2 * rl;
       if (A.dbg & 64) return 1e-3 * i;            // ablation: no global loads on the step chain
-      return (row_ok && i >= 0 && i < ex && k < nF) ? __ldg(rrow + gx_of(i)) : 0.0;
+      const int gi = gx0 + k;
+      const int gx = gi < 0 ? gi + nxg : (gi >= nxg ? gi - nxg : gi);
+      double v = 0.0;
+      if ((unsigned)i < (unsigned)ex && k < nFr) v = __ldg(rrow + gx);
+      return v;
     };
     auto release_group = [&](int q) {
       if (GL) return;
