@@ -777,6 +777,16 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
     };
     auto Est = [&](int k, double val) { E[(c >> 1) * kEP + ((k & 7) * 32 + rl) * 2 + (c & 1)] = val; };
+    // the same loads on 32-bit shared addresses: per-lane ring bases, one select between the ring and the
+    // halo cell for the boundary lanes (no divergent branch)
+    const unsigned sE = smem_u32(E), sH = smem_u32(H);
+    auto ld4a = [&](unsigned a, unsigned off2, double (&v)[4]) {
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(a) : "memory");
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[2]), "=d"(v[3]) : "r"(a + off2) : "memory");
+    };
+    auto ering = [&](int k, int row) { return sE + (unsigned)(((k & 7) * 32 + row) * 16); };
+    auto hcella = [&](int q, int i) { return sH + (unsigned)(q * pitch * 8 + (min(max(i, -2), ex + 1) + 2) * 32); };
+    constexpr unsigned kEPB = kEP * 8;    // plane offset in bytes
     long long t_bar = 0, t_stage = 0, t_poll = 0;
     (void)t_bar;
 
@@ -829,9 +839,9 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         const bool active = row_ok && (unsigned)i < (unsigned)ex;
         step_bar();                                                   // E[k-1] complete; stages/cells ready
         double Ya1[4], yp[4], aa4[4];
-        ld4s(rl >= 1 ? Erow(k - 1, rl - 1) : hcell(1, k + 1), rl >= 1 ? kEP : 2, Ya1);   // (i+1, j-1) at step k-1
-        ld4s(Erow(k - 1, rl), kEP, yp);                                                    // own row at step k-1
-        ld4s(rl >= 2 ? Erow(k - 2, rl - 2) : (rl == 1 ? hcell(1, k) : hcell(0, k + 2)), rl >= 2 ? kEP : 2, aa4);
+        ld4a(rl >= 1 ? ering(k - 1, rl - 1) : hcella(1, k + 1), rl >= 1 ? kEPB : 16u, Ya1);   // (i+1, j-1) at step k-1
+        ld4a(ering(k - 1, rl), kEPB, yp);                                                     // own row at step k-1
+        ld4a(rl >= 2 ? ering(k - 2, rl - 2) : hcella(rl == 1 ? 1 : 0, rl == 1 ? k : k + 2), rl >= 2 ? kEPB : 16u, aa4);
         preload(nxt, k + 1);
         const double a0 = dot4(cur.L3, Ya1, pre);                     // (1,-1)
         const double a1 = dot4(cur.L5, yp, 0.0);                      // (-1,0)
@@ -921,6 +931,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         half = dot4(bb, Xb2, dot4(a, bb4n, ydot(dd, yK1)));                 // (0,2), (1,1) of step K-1 (Xb3(K-1) = Xb2(K))
         preload(SA, K);
       }
+      const int gz0 = G.s0x - 2 * rl;
       // lanes 0, 1 push x into the previous stripe's halo rows 2, 3
       const bool up_push = up_remote && rl < 2;
       const unsigned up_base = mapa_u32(hcell(2 + min(rl, 1), 0) + c, (unsigned)max(s - 1, 0));
@@ -930,9 +941,9 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         const int iR = k - dR;
         step_bar();                                                   // E[k+1] complete; stages/cells ready
         double Xb1[4], xp[4], bb4[4];
-        ld4s(rl <= R - 2 ? Erow(k + 1, rl + 1) : hcell(2, iR - 1), rl <= R - 2 ? kEP : 2, Xb1);   // (i-1, j+1) at step k+1
-        ld4s(Erow(k + 1, rl), kEP, xp);                                                            // own row at step k+1
-        ld4s(rl <= R - 3 ? Erow(k + 2, rl + 2) : (rl == R - 2 ? hcell(2, iR) : hcell(3, iR - 2)), rl <= R - 3 ? kEP : 2, bb4);
+        ld4a(rl <= R - 2 ? ering(k + 1, rl + 1) : hcella(2, iR - 1), rl <= R - 2 ? kEPB : 16u, Xb1);   // (i-1, j+1) at step k+1
+        ld4a(ering(k + 1, rl), kEPB, xp);                                                              // own row at step k+1
+        ld4a(rl <= R - 3 ? ering(k + 2, rl + 2) : hcella(rl == R - 2 ? 2 : 3, rl == R - 2 ? iR : iR - 2), rl <= R - 3 ? kEPB : 16u, bb4);
         preload(nxt, k - 1);
         const double a0 = dot4(cur.U3, Xb1, pre);                     // (-1,1)
         const double a1 = dot4(cur.U1, xp, 0.0);                      // (1,0)
@@ -944,7 +955,11 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         const double c1 = dot4(cur.M5, Xb1, 0.0);                     //            (1,1)
         pre = b0 + b1;
         half = c0 + c1;
-        st_global_if(!(A.dbg & 256) && active && own_row && i >= G.ox0 && i < G.ox0 + G.ownx, zrow + gx_of(min(max(i, 0), ex - 1)), x);
+        {
+          const int gi = gz0 + k;                  // s0x + i, wraps at most once
+          const int gx = gi < 0 ? gi + A.nx : (gi >= A.nx ? gi - A.nx : gi);
+          st_global_if(!(A.dbg & 256) && active && own_row && (unsigned)(i - G.ox0) < (unsigned)G.ownx, zrow + gx, x);
+        }
         st_cluster_if(up_push && active, up_base + (unsigned)(i * 32), x);
         const int p = pofk(k);
         if (p % kG == kG - 2) release_group(gof(p));
