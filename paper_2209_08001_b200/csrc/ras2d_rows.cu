@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   double* V = E + 8 * 128;                                            // [32][4] (unused since the diagonal fold)
   int4* tb = reinterpret_cast<int4*>(V + 128);                        // per processing step p: stage element
                                                                       // offset of row 0, active rows [lo, hi]
-  int* off = reinterpret_cast<int*>(tb + 2 * A.KGp);                  // off[] in shared memory: the stage
+  int* off = reinterpret_cast<int*>(tb + 2 * A.KGp + 8);              // off[] in shared memory: the stage
                                                                       // addresses are on the step's chain
   auto hcell = [&](int q, int i) -> double* { return H + (size_t)q * pitch + (min(max(i, -2), ex + 1) + 2) * 4; };
   const bool up_remote = s > 0, dn_remote = s < CS - 1;
@@ -301,16 +301,21 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   }
   __syncthreads();
   // Row table: lane rl's block row at processing step p (forward k = p, backward k = 2 nFp - 1 - p) is
-  // stage + tb[p].x + rl * pitch when tb[p].y <= rl <= tb[p].z, so the per-step preload needs one
-  // broadcast shared load instead of the group/offset arithmetic and two off[] loads per row.
-  for (int p = tid; p < 2 * nFp; p += blockDim.x) {
+  // stage + tb[e].x + rl * pitch when tb[e].y <= rl <= tb[e].z, e = p (forward) or p + 3 (backward), so
+  // the per-step preload needs one broadcast shared load instead of the group/offset arithmetic and two
+  // off[] loads per row.  Three empty entries after each sweep let the look-ahead (rows of steps k+1..k+3
+  // loaded in iteration k) run past its end without range checks.
+  for (int e = tid; e < 2 * nFp + 6; e += blockDim.x) {
+    const bool pad = (e >= nFp && e < nFp + 3) || e >= 2 * nFp + 3;
+    if (pad) { tb[e] = make_int4(0, 1, 0, 0); continue; }
+    const int p = e < nFp ? e : e - 3;
     const int k = p < nFp ? p : 2 * nFp - 1 - p;
     const int q = p / kG;
     const int kb = q < nGr ? q * kG : nFp - kG * (q - nGr + 1);
     const int lo = lo_of(k, ex, R), hi = hi_of(k, R);
     const int pf = p < nFp ? kPF : kPB;
-    if (GL) tb[p] = make_int4((int)((sb * RPC * A.exmax + off[k] - lo) * pf), lo, hi, 0);
-    else tb[p] = make_int4((int)((q % kNSW) * stage_elems) + (off[k] - off[kb] - lo) * pf, lo, hi, 0);
+    if (GL) tb[e] = make_int4((int)((sb * RPC * A.exmax + off[k] - lo) * pf), lo, hi, 0);
+    else tb[e] = make_int4((int)((q % kNSW) * stage_elems) + (off[k] - off[kb] - lo) * pf, lo, hi, 0);
   }
   __syncthreads();
   cluster.sync();
@@ -509,8 +514,8 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     auto step_bar = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); };
     // block rows of processing step p: block b, row c at ptr + b * 16 + c * 4 (active lanes only)
     struct Ref { const T* ptr; bool on; };
-    auto rowt = [&](int p, int pf) -> Ref {
-      const int4 t = tb[p];
+    auto rowt = [&](int p, int pf) -> Ref {          // forward p / backward p (table entry p + 3)
+      const int4 t = tb[p < nFp ? p : p + 3];
       return Ref{stage + t.x + rl * pf, rl >= t.y && rl <= t.z};
     };
     // acc_c -= B(row c) . v for the four rows c of block b
@@ -749,9 +754,9 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     // the block rows of processing step p (0 <= p < 2 nFp) from the row table: lanes without a row at
     // that step skip the shared loads (their outputs of that step are discarded)
     struct RowRef { const T* ptr; bool on; };
-    auto rowt = [&](int p, int pf) -> RowRef {
-      const int4 t = tb[p];
-      const T* b0 = GL ? (p < nFp ? (const T*)A.chunkF : (const T*)A.chunkB) : stage;
+    auto rowt = [&](int e, int pf) -> RowRef {      // e: row-table entry (forward p, backward p + 3)
+      const int4 t = tb[e];
+      const T* b0 = GL ? (e < nFp ? (const T*)A.chunkF : (const T*)A.chunkB) : stage;
       return RowRef{b0 + t.x + rl * pf + c * 4, rl >= t.y && rl <= t.z};
     };
     // lanes without a row at that step keep stale (finite) values: every output of such a (lane, step)
@@ -808,9 +813,9 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       FRows SA, SB;
       auto preload = [&](FRows& S, int k) {      // rows for iteration k (steps past the sweep: none)
         if (A.dbg & 32) return;
-        if (k < nFp) { const RowRef r = rowt(k, kPF); ldrow_if(r, 3, S.L3); ldrow_if(r, 5, S.L5); }
-        if (k + 1 < nFp) { const RowRef r = rowt(k + 1, kPF); ldrow_if(r, 2, S.N2); ldrow_if(r, 4, S.N4); }
-        if (k + 2 < nFp) { const RowRef r = rowt(k + 2, kPF); ldrow_if(r, 0, S.M0); ldrow_if(r, 1, S.M1); }
+        { const RowRef r = rowt(k, kPF); ldrow_if(r, 3, S.L3); ldrow_if(r, 5, S.L5); }
+        { const RowRef r = rowt(k + 1, kPF); ldrow_if(r, 2, S.N2); ldrow_if(r, 4, S.N4); }
+        { const RowRef r = rowt(k + 2, kPF); ldrow_if(r, 0, S.M0); ldrow_if(r, 1, S.M1); }
       };
       for (FRows* S : {&SA, &SB}) { zero4(S->L3); zero4(S->L5); zero4(S->N2); zero4(S->N4); zero4(S->M0); zero4(S->M1); }
       double q0, q1, q2, q3;                       // r prefetch ring: r(k+2) is used at iteration k
@@ -884,9 +889,9 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       struct BRows { double U3[4], U1[4], N4[4], N2[4], M6[4], M5[4], DM[4]; };
       BRows SA, SB;
       auto preload = [&](BRows& S, int k) {      // rows for iteration k (steps past the sweep: none)
-        if (k >= 0) { const RowRef r = rowt(pofk(k), kPB); ldrow_if(r, 3, S.U3); ldrow_if(r, 1, S.U1); }
-        if (k - 1 >= 0) { const RowRef r = rowt(pofk(k - 1), kPB); ldrow_if(r, 4, S.N4); ldrow_if(r, 2, S.N2); }
-        if (k - 2 >= 0) { const RowRef r = rowt(pofk(k - 2), kPB); ldrow_if(r, 6, S.M6); ldrow_if(r, 5, S.M5); ldrow_if(r, 0, S.DM); }
+        { const RowRef r = rowt(pofk(k) + 3, kPB); ldrow_if(r, 3, S.U3); ldrow_if(r, 1, S.U1); }
+        { const RowRef r = rowt(pofk(k - 1) + 3, kPB); ldrow_if(r, 4, S.N4); ldrow_if(r, 2, S.N2); }
+        { const RowRef r = rowt(pofk(k - 2) + 3, kPB); ldrow_if(r, 6, S.M6); ldrow_if(r, 5, S.M5); ldrow_if(r, 0, S.DM); }
       };
       for (BRows* S : {&SA, &SB}) { zero4(S->U3); zero4(S->U1); zero4(S->N4); zero4(S->N2); zero4(S->M6); zero4(S->M5); zero4(S->DM); }
       const double* yrow = A.yscr + sb * A.KGp * 128 + rl * 4;    // y(k) of this row: yrow[k * 128 + 0..3]
@@ -1053,7 +1058,7 @@ static size_t smem_for(const Dims& D, int RPC, bool f32) {
                            : (size_t)Strm<false>::NS * Strm<false>::G * RPC * Strm<false>::PB * sizeof(double);
   const int ns = f32 ? Strm<true>::NS : Strm<false>::NS;
   return stage + 2 * (size_t)ns * 8 + (size_t)4 * (D.exmax + 4) * 4 * 8 + (size_t)9 * 128 * 8 + (size_t)kgp_of(D, RPC) * 4 +
-         (size_t)2 * kgp_of(D, RPC) * 16;
+         ((size_t)2 * kgp_of(D, RPC) + 8) * 16;
 }
 // (A per-lane cp.async variant of the apply -- every consumer lane fetching its own block rows with
 // LDGSTS, no bulk copies -- measured 0.75 ms against the bulk-copy kernel's 0.52 ms and was removed.)
