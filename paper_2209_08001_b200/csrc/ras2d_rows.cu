@@ -96,6 +96,16 @@ struct Args {
 };
 
 // per CTA: [fwd cycles, bwd cycles, halo-wait cycles, stage-wait cycles, start (globaltimer), end, bar wait, 0]
+// Ablation switches (NKS_RAS2D_DBG) and clock instrumentation (NKS_RAS2D_PROF) of the apply kernel are
+// compiled in only with -DNKS_R2_ABLATE (python -m paper_2209_08001_b200.build with NKS_BUILD_DEFS); the
+// production kernel tests constant zeros, which removes their per-step instructions.
+#ifdef NKS_R2_ABLATE
+#define R2_DBG(A) ((A).dbg)
+#define R2_PROF(A) ((A).prof)
+#else
+#define R2_DBG(A) 0
+#define R2_PROF(A) 0
+#endif
 __device__ long long g_prof[1024 * 8];
 __device__ long long g_gt[72 * 8];
 __device__ long long g_cp[64 * 4];   // NKS_RAS2D_PROF: CTA 0 producer, groups 8..71: issue / first test / ready clocks   // NKS_RAS2D_PROF: CTA 0, warp 0, forward groups 8..15: per-phase clocks
@@ -346,7 +356,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       const T* src = fw ? (const T*)A.chunkF + (base + r_lo) * kPF : (const T*)A.chunkB + (base + r_lo) * kPB;
       const unsigned bytes = (unsigned)(nrows * pf * sizeof(T));
       const unsigned bar = full0 + (q % kNSW) * 8;
-      if (A.prof && blockIdx.x == 0 && q >= 8 && q < 72) g_cp[(q - 8) * 4] = clock64();
+      if (R2_PROF(A) && blockIdx.x == 0 && q >= 8 && q < 72) g_cp[(q - 8) * 4] = clock64();
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                        stage0 + (unsigned)((q % kNSW) * stage_elems * sizeof(T))),
@@ -402,13 +412,13 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         issued = __shfl_sync(0xffffffffu, issued, 0);
         return;
       }
-      if ((A.dbg & 128) && issued > 0) return;   // ablation: no copy management after the first groups
+      if ((R2_DBG(A) & 128) && issued > 0) return;   // ablation: no copy management after the first groups
       G = min(G, 2 * nGr - 1);
       if (issued <= G) issue_upto(G, true);
       while (ready < G) {
         ++ready;
         unsigned sp = 0;
-        const bool rec = A.prof && blockIdx.x == 0 && lane == 0 && ready >= 8 && ready < 72;
+        const bool rec = R2_PROF(A) && blockIdx.x == 0 && lane == 0 && ready >= 8 && ready < 72;
         if (rec) g_cp[(ready - 8) * 4 + 1] = clock64();
         while (!test_bar(full0 + (ready % kNSW) * 8, (unsigned)((ready / kNSW) & 1)))
           if (++sp > (1u << 26)) __trap();
@@ -418,7 +428,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     };
     // poll halo cells (q0, c0), (q1, c1), (q2, c2): lane l checks double l & 3 of cell l >> 2
     auto poll3 = [&](bool on, int q0_, int c0_, int q1_, int c1_, int q2_, int c2_) {
-      if (!on || (A.dbg & 16)) return;
+      if (!on || (R2_DBG(A) & 16)) return;
       const int which = min(lane >> 2, 2);
       const int qq = which == 0 ? q0_ : (which == 1 ? q1_ : q2_);
       const int cc = which == 0 ? c0_ : (which == 1 ? c1_ : c2_);
@@ -445,7 +455,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     const int qf = which == 1 ? 0 : 1, dcf = which == 0 ? 1 : (which == 1 ? 2 : 0);     // (1,k+1) (0,k+2) (1,k)
     const int qb = which == 2 ? 3 : 2, dcb = which == 0 ? -1 : (which == 1 ? 0 : -2);  // (2,iR-1) (2,iR) (3,iR-2)
     auto poll1 = [&](int q, int i) {
-      if (A.dbg & 16) return;
+      if (R2_DBG(A) & 16) return;
       const unsigned sa = smem_u32(hcell(q, i) + (lane & 3));
       unsigned sp = 0;
       while (true) {
@@ -720,7 +730,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     const int nFr = row_ok ? nF : 0;              // rows past the stripe load nothing
     auto load_r = [&](int k) -> double {
       const int i = k - 2 * rl;
-      if (A.dbg & 64) return 1e-3 * i;            // ablation: no global loads on the step chain
+      if (R2_DBG(A) & 64) return 1e-3 * i;            // ablation: no global loads on the step chain
       const int gi = gx0 + k;
       const int gx = gi < 0 ? gi + nxg : (gi >= nxg ? gi - nxg : gi);
       double v = 0.0;
@@ -812,7 +822,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       struct FRows { double L3[4], L5[4], N2[4], N4[4], M0[4], M1[4]; };
       FRows SA, SB;
       auto preload = [&](FRows& S, int k) {      // rows for iteration k (steps past the sweep: none)
-        if (A.dbg & 32) return;
+        if (R2_DBG(A) & 32) return;
         { const RowRef r = rowt(k, kPF); ldrow_if(r, 3, S.L3); ldrow_if(r, 5, S.L5); }
         { const RowRef r = rowt(k + 1, kPF); ldrow_if(r, 2, S.N2); ldrow_if(r, 4, S.N4); }
         { const RowRef r = rowt(k + 2, kPF); ldrow_if(r, 0, S.M0); ldrow_if(r, 1, S.M1); }
@@ -858,8 +868,8 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         const double c1 = dot4(cur.M1, Ya1, 0.0);                     //            (-1,-1)
         pre = b0 + b1;
         half = c0 + c1;
-        if (!(A.dbg & 260)) ybuf[(size_t)k * 128] = y;
-        st_cluster_if(!(A.dbg & 4) && dn_push && active, dn_base + (unsigned)(i * 32), y);
+        if (!(R2_DBG(A) & 260)) ybuf[(size_t)k * 128] = y;
+        st_cluster_if(!(R2_DBG(A) & 4) && dn_push && active, dn_base + (unsigned)(i * 32), y);
         if (k % kG == kG - 2) release_group(gof(k));   // the group's last rows are in registers now
       };
       for (int k0 = 0; k0 < nFp; k0 += 4) {
@@ -896,7 +906,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       for (BRows* S : {&SA, &SB}) { zero4(S->U3); zero4(S->U1); zero4(S->N4); zero4(S->N2); zero4(S->M6); zero4(S->M5); zero4(S->DM); }
       const double* yrow = A.yscr + sb * A.KGp * 128 + rl * 4;    // y(k) of this row: yrow[k * 128 + 0..3]
       auto load_y4 = [&](int k, double (&v)[4]) {
-        if (A.dbg & 64) { v[0] = v[1] = v[2] = v[3] = 1e-3 * k; return; }
+        if (R2_DBG(A) & 64) { v[0] = v[1] = v[2] = v[3] = 1e-3 * k; return; }
         if (k >= 0) {
           const double2 a = *reinterpret_cast<const double2*>(yrow + (size_t)k * 128);
           const double2 b = *reinterpret_cast<const double2*>(yrow + (size_t)k * 128 + 2);
@@ -963,7 +973,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         {
           const int gi = gz0 + k;                  // s0x + i, wraps at most once
           const int gx = gi < 0 ? gi + A.nx : (gi >= A.nx ? gi - A.nx : gi);
-          st_global_if(!(A.dbg & 256) && active && own_row && (unsigned)(i - G.ox0) < (unsigned)G.ownx, zrow + gx, x);
+          st_global_if(!(R2_DBG(A) & 256) && active && own_row && (unsigned)(i - G.ox0) < (unsigned)G.ownx, zrow + gx, x);
         }
         st_cluster_if(up_push && active, up_base + (unsigned)(i * 32), x);
         const int p = pofk(k);
@@ -977,7 +987,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         biter(k0 - 3, q3, SB, SA); load_y4(k0 - 9, q3);
       }
     }
-    if (A.prof && tid == 0) {
+    if (R2_PROF(A) && tid == 0) {
       long long gt1;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
       long long* pq = g_prof + blockIdx.x * 8;
