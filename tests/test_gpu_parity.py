@@ -413,3 +413,34 @@ def test_fp32_factors_change_iterations_not_the_step():
         z.append(g.pc_apply(r).cpu().numpy())
     rel = np.abs(z[1] - z[0]).max() / np.abs(z[0]).max()
     assert 0 < rel < 1e-4, rel
+
+
+PCI_CASES = [((1, 1), 2, 1, 0), ((4, 4), 2, 1, 0), ((4, 4), 0, 1, 0), ((4, 4), 2, 0, 0), ((4, 4), 2, 2, 0),
+             ((4, 4), 2, 1, 1), ((2, 4), 1, 2, 1)]
+
+
+@pytest.mark.parametrize("nsub,overlap,reuse,fp32", PCI_CASES)
+def test_preconditioner_independence(nsub, overlap, reuse, fp32):
+    """SURVEY 8(c).3 'preconditioner independence' (the Newton solve is insensitive to the
+    subdomain solver): two steps of the same dt (so pc_reuse = 2 keeps the factors across steps) with
+    different box counts, overlaps, factorisation reuse and factor precision reach the same X^{n+1}
+    as the single-box reference to 1e-10 relative, with the same Newton counts (+-1 at the tolerance)."""
+    shape = (32, 32)
+    c, eta = ni.initial_fields(shape, 0)
+    dts = [0.3, 0.3]
+
+    def run(nsub_, ov_, reuse_, f32_):
+        g = gpu_solver(shape, nsub=nsub_, overlap=ov_, pc_reuse=reuse_,
+                       sol={"factor_fp32": f32_, "gmres_maxit": 6000})
+        g.set_fields(c, eta)
+        infos = [g.step(dt) for dt in dts]
+        return g.get_state(), infos
+
+    X0, i0 = run((1, 1), 2, 1, 0)
+    X1, i1 = run(nsub, overlap, reuse, fp32)
+    for f in range(X0.shape[0]):
+        rel = np.linalg.norm(X1[f] - X0[f]) / np.linalg.norm(X0[f])
+        assert rel <= 1e-10, (f, rel)
+    for a, b in zip(i0, i1):
+        assert abs(a["newton_its"] - b["newton_its"]) <= 1, (a["newton_its"], b["newton_its"])
+        assert abs(a["energy"] - b["energy"]) <= 1e-10 * abs(a["energy"])
