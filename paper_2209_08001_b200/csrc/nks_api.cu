@@ -21,11 +21,9 @@
 namespace nks {
 // stencil.cu
 void launch_level_prep(const DevParams& P, const double* X, double* T, cudaStream_t s);
-void launch_residual(const DevParams& P, const double* Xa, const double* Xb, const double* Ta, double* F, cudaStream_t s);
 void launch_residual_tiled(const DevParams& P, const double* Xa, const double* Xb, const double* Ta, double* F,
                            cudaStream_t s);
 void launch_pointwise_jac(const DevParams& P, const double* Xa, const double* Xb, double* jac4, cudaStream_t s);
-void launch_jv(const DevParams& P, const double* Xa, const double* jac4, const double* v, double* out, cudaStream_t s);
 void launch_jv_tiled(const DevParams& P, const double* Xa, const double* jac4, const double* v, double* out,
                      cudaStream_t s);
 void launch_norm_admissible(long long N, int nf, const double* F, const double* X, double* part, double* out, cudaStream_t s);
@@ -56,12 +54,6 @@ HostBoxes build_boxes_host(const nks_grid& g, const BoxSet& B);
 void launch_assemble(const DevParams& P, const BoxSet& B, int nf, const double* Xa, const double* jac4, double* fac,
                      cudaStream_t s);
 void launch_factor(const BoxSet& B, int nf, double* fac, cudaStream_t s);
-size_t ras2d_workspace_bytes(const nks_grid& g);
-void* ras2d_plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaStream_t stream, std::string& why);
-void launch_ras2d_pack(void* plan, const double* fac, long long ld, cudaStream_t s);
-void ras2d_free(void* plan);
-int ras2d_cluster(void* plan);
-cudaError_t launch_ras2d(void* plan, const double* r, double* z, cudaStream_t s);
 namespace r2 {
 size_t workspace_bytes(const nks_grid& g);
 void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaStream_t stream, std::string& why, bool f32);
@@ -117,7 +109,7 @@ const char* validate(const nks_grid* g, const nks_params* p) {
   if (!(g->h > 0)) return "h must be > 0";
   if (p->S < 1 || p->S > kMaxS) return "S must be in 1..16";
   if (p->gmres_restart < 1 || p->gmres_restart > 60) return "gmres_restart must be in 1..60";
-  if (p->newton_maxit < 0 || p->gmres_maxit < 1) return "bad iteration limits";
+  if (p->newton_maxit < 0 || p->gmres_maxit < 1 || p->gmres_stall_cycles < 0) return "bad iteration limits";
   if (p->pc_type != NKS_PC_NONE && p->pc_type != NKS_PC_RAS_BILU0 && p->pc_type != NKS_PC_AS_BILU0 &&
       p->pc_type != NKS_PC_RRAS_BILU0)
     return "unknown pc_type";
@@ -184,8 +176,8 @@ Layout make_layout(const nks_grid& g, const nks_params& p) {
     const bool cover = p.pc_type == NKS_PC_AS_BILU0 || p.pc_type == NKS_PC_RRAS_BILU0;
     L.off_cover_off = o; o = align256(o + (cover ? (size_t)(N + 1) * sizeof(int) : 0));
     L.off_cover_pos = o; o = align256(o + (cover ? (size_t)L.P * sizeof(int) : 0));
-    // one of the two pipelined 2D applies uses this slice (ras2d_rows.cu by default)
-    L.geo_bytes = d == 2 ? std::max(ras2d_workspace_bytes(g), r2::workspace_bytes(g)) : 0;
+    // the pipelined 2D apply (ras2d_rows.cu) uses this slice
+    L.geo_bytes = d == 2 ? r2::workspace_bytes(g) : 0;
     L.off_geo = o; o = align256(o + L.geo_bytes);
   }
   L.total = o;
@@ -222,6 +214,14 @@ DevParams make_devparams(const nks_grid& g, const nks_params& p) {
   P.K = p.Lscale * (p.C11 + (g.dim - 1) * p.C12);
   P.cbar0 = 0.0;
   return P;
+}
+
+// Every group of kernel launches is followed by a launch-error check, so a failed launch (bad
+// configuration, shared-memory opt-in missing on this device, ...) becomes NKS_E_CUDA at once instead
+// of leaving stale data in its outputs.
+void count_launch(nks_state* st, long long n) {
+  st->launches += n;
+  CK(cudaGetLastError());
 }
 
 // ---- phase profiling ---------------------------------------------------------------------------
@@ -270,7 +270,7 @@ void ph_end(nks_state* st) {
 struct PhaseScope {
   nks_state* st;
   PhaseScope(nks_state* s, int ph) : st(s) { ph_begin(st, ph); }
-  ~PhaseScope() { ph_end(st); }
+  ~PhaseScope() noexcept(false) { ph_end(st); }
 };
 
 // ---- building blocks -------------------------------------------------------------------------------
@@ -305,15 +305,13 @@ void halo(nks_state* st, double* vec, int nf) {
 void clean(nks_state* st, double* vec, int nf) {
   if (!slab(st)) return;
   launch_zero_ghosts(st->dp, nf, vec, st->stream);
-  st->launches += 1;
+  count_launch(st, 1);
 }
 
 void residual(nks_state* st, const double* Xb, double* F) {
   PhaseScope ps(st, PH_F);
-  static const bool old_f = std::getenv("NKS_F_OLD") != nullptr;
-  if (old_f) launch_residual(st->dp, st->Xn, Xb, st->Ta, F, st->stream);
-  else launch_residual_tiled(st->dp, st->Xn, Xb, st->Ta, F, st->stream);
-  st->launches += 1;
+  launch_residual_tiled(st->dp, st->Xn, Xb, st->Ta, F, st->stream);
+  count_launch(st, 1);
 }
 
 // (||F||, #inadmissible points of X) -- host sync
@@ -321,7 +319,7 @@ void norm_adm(nks_state* st, const double* F, const double* X, double& nrm, doub
   {
     PhaseScope ps(st, PH_RED);
     launch_norm_admissible(st->N, st->nf, F, X, st->red_part, st->red_out, st->stream);
-    st->launches += 2;
+    count_launch(st, 2);
   }
   comm_allreduce(st, st->red_out, 2);
   CK(cudaMemcpyAsync(st->h_red, st->red_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
@@ -335,15 +333,13 @@ void gauge(nks_state* st, double* X) {
   const int nsum = launch_gauge_sums(st->dp, X, st->red_part, st->red_out + 128, st->stream);
   comm_allreduce(st, st->red_out + 128, nsum);     // global sub-lattice sums (slab: own planes of every rank)
   launch_gauge_apply(st->dp, X, st->red_out + 128, st->stream);
-  st->launches += 3;
+  count_launch(st, 3);
 }
 
 void jv(nks_state* st, const double* v, double* out) {
   PhaseScope ps(st, PH_JV);
-  static const bool old_jv = std::getenv("NKS_JV_OLD") != nullptr;
-  if (old_jv) launch_jv(st->dp, st->Xn, st->jac4, v, out, st->stream);
-  else launch_jv_tiled(st->dp, st->Xn, st->jac4, v, out, st->stream);
-  st->launches += 1;
+  launch_jv_tiled(st->dp, st->Xn, st->jac4, v, out, st->stream);
+  count_launch(st, 1);
 }
 
 void pc_apply(nks_state* st, const double* r, double* z) {
@@ -352,10 +348,9 @@ void pc_apply(nks_state* st, const double* r, double* z) {
     return;
   }
   PhaseScope ps(st, PH_RAS);
-  if (st->ras2d_kind == 2) CK(r2::launch_apply(st->ras2d, r, z, st->stream));
-  else if (st->ras2d_kind == 1) CK(launch_ras2d(st->ras2d, r, z, st->stream));
+  if (st->ras2d) CK(r2::launch_apply(st->ras2d, r, z, st->stream));
   else launch_ras_apply(st->boxes, st->nf, st->N, st->fac, st->fac32, r, st->ybox, z, st->stream);
-  st->launches += 1;
+  count_launch(st, 1);
 }
 
 void pc_setup(nks_state* st, const double* Xb) {
@@ -363,20 +358,19 @@ void pc_setup(nks_state* st, const double* Xb) {
   {
     PhaseScope ps(st, PH_ASM);
     launch_assemble(st->dp, st->boxes, st->nf, st->Xn, st->jac4, st->fac, st->stream);
-    st->launches += 1;
+    count_launch(st, 1);
   }
   {
     PhaseScope ps(st, PH_FACT);
     launch_factor(st->boxes, st->nf, st->fac, st->stream);
-    st->launches += 1;
+    count_launch(st, 1);
     if (st->ras2d) {
-      if (st->ras2d_kind == 2) r2::launch_pack(st->ras2d, st->fac, st->boxes.ld, st->stream);
-      else launch_ras2d_pack(st->ras2d, st->fac, st->boxes.ld, st->stream);
-      st->launches += 1;
+      r2::launch_pack(st->ras2d, st->fac, st->boxes.ld, st->stream);
+      count_launch(st, 1);
     }
     if (st->fac32 && !st->ras2d) {
       launch_fac_to_fp32(st->boxes, st->nf, st->fac, st->fac32, st->stream);
-      st->launches += 1;
+      count_launch(st, 1);
     }
   }
   (void)Xb;
@@ -405,7 +399,7 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
     {
       PhaseScope ps(st, PH_VEC);
       launch_axpby(n, 1.0 / beta, first ? b : V, 0.0, V, st->stream);
-      st->launches += 1;
+      count_launch(st, 1);
     }
     first = false;
     std::fill(g.begin(), g.end(), 0.0);
@@ -432,16 +426,16 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
           launch_cgs_dot(n, jj + 1, V, n, w, st->red_part, st->red_out, st->red_cnt, st->stream);
           comm_allreduce(st, st->red_out, jj + 1);
           launch_cgs_update_dot(n, jj + 1, V, n, st->red_out, w, st->red_part, st->red_out + 64, st->red_cnt, st->stream);
-          st->launches += 2;
+          count_launch(st, 2);
         } else {
           launch_mdot(n, jj + 1, V, n, w, st->red_part, st->red_out, st->stream);
           comm_allreduce(st, st->red_out, jj + 1);
           launch_update_dot(n, jj + 1, V, n, st->red_out, w, st->red_part, st->red_out + 64, st->stream);
-          st->launches += 4;
+          count_launch(st, 4);
         }
         comm_allreduce(st, st->red_out + 64, jj + 2);
         launch_update_scale_dev(n, jj + 1, V, n, st->red_out + 64, w, st->stream);
-        st->launches += 1;
+        count_launch(st, 1);
       }
       double* slot = st->h_ring + (jj % 4) * 128;
       CK(cudaMemcpyAsync(slot, st->red_out, (64 + jj + 2) * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
@@ -494,7 +488,7 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
     {
       PhaseScope ps(st, PH_VEC);
       launch_lincomb(n, j, V, n, y.data(), st->W2, st->stream);
-      st->launches += 1;
+      count_launch(st, 1);
     }
     if (st->prm.pc_type != NKS_PC_NONE) halo(st, st->W2, st->nf);
     pc_apply(st, st->W2, st->Z);
@@ -502,7 +496,7 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
     {
       PhaseScope ps(st, PH_VEC);
       launch_axpby(n, 1.0, st->Z, 1.0, s, st->stream);
-      st->launches += 1;
+      count_launch(st, 1);
     }
     if (st->debug) std::fprintf(stderr, "[nks] gmres cycle its=%d beta=%.3e resid_est=%.3e tol=%.3e\n", its, beta, resid, tol);
     if (resid <= tol) return 0;
@@ -514,12 +508,12 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
     {
       PhaseScope ps(st, PH_VEC);
       launch_xpay(n, b, -1.0, st->W2, V, st->stream);
-      st->launches += 1;
+      count_launch(st, 1);
     }
     {
       PhaseScope ps(st, PH_RED);
       launch_norm_admissible(n / st->nf, st->nf, V, nullptr, st->red_part, st->red_out, st->stream);
-      st->launches += 2;
+      count_launch(st, 2);
     }
     comm_allreduce(st, st->red_out, 1);
     CK(cudaMemcpyAsync(st->h_red, st->red_out, sizeof(double), cudaMemcpyDeviceToHost, st->stream));
@@ -527,10 +521,11 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
     {
       const double prev = beta;
       beta = std::sqrt(st->h_red[0]);
-      // Stagnation (reading R18): a restart cycle that removes less than 0.1 % of the true residual,
-      // three cycles in a row, is reported as divergence instead of running to gmres_maxit.
+      // Stagnation (opt-in, nks_params.gmres_stall_cycles, reading R18): k restart cycles in a row that
+      // each remove less than 0.1 % of the true residual are reported as divergence instead of running
+      // to gmres_maxit.  Off by default (the paper's solver fails only at its iteration limit).
       stall = (beta > 0.999 * prev) ? stall + 1 : 0;
-      if (stall >= 3) return 2;
+      if (st->prm.gmres_stall_cycles > 0 && stall >= st->prm.gmres_stall_cycles) return 2;
     }
     // V already holds r; scale below uses V as source (first == false)
   }
@@ -540,7 +535,7 @@ void energy(nks_state* st, const double* X, double parts[4], double& mass) {
   {
     PhaseScope ps(st, PH_RED);
     launch_energy(st->dp, X, st->red_part, st->red_out, st->stream);
-    st->launches += 2;
+    count_launch(st, 2);
   }
   comm_allreduce(st, st->red_out, 5);
   CK(cudaMemcpyAsync(st->h_red, st->red_out, 5 * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
@@ -553,7 +548,7 @@ void energy(nks_state* st, const double* X, double parts[4], double& mass) {
 void level_prep(nks_state* st) {
   PhaseScope ps(st, PH_OTHER);
   launch_level_prep(st->dp, st->Xn, st->Ta, st->stream);
-  st->launches += 1;
+  count_launch(st, 1);
 }
 
 // One NKS step (transactional).
@@ -589,7 +584,7 @@ nks_status step_impl(nks_state* st, double dt, nks_step_info* info) {
     {
       PhaseScope ps(st, PH_OTHER);
       launch_pointwise_jac(st->dp, st->Xn, st->Xb, st->jac4, st->stream);
-      st->launches += 1;
+      count_launch(st, 1);
     }
     if (p.pc_type != NKS_PC_NONE) {
       bool refactor = p.pc_reuse == 0 || (p.pc_reuse == 1 && it == 0) ||
@@ -603,7 +598,7 @@ nks_status step_impl(nks_state* st, double dt, nks_step_info* info) {
     {
       PhaseScope ps(st, PH_VEC);
       launch_axpby(st->nvec, -1.0, st->F, 0.0, st->Ft, st->stream);
-      st->launches += 1;
+      count_launch(st, 1);
     }
     // Project b onto range(J): the left null space of J is spanned by the indicators of the u_I rows
     // on each parity sub-lattice (sub-lattice sums of D^(.) vanish identically, reading R14), so
@@ -619,7 +614,7 @@ nks_status step_impl(nks_state* st, double dt, nks_step_info* info) {
     if (grc != 0) {
       I.reason = grc == 2 ? NKS_REASON_GMRES_STAGNATION : NKS_REASON_GMRES_MAXIT;
       I.fnorm = f;
-      st->err = grc == 2 ? "GMRES stagnated (3 restart cycles with < 0.1 % residual reduction)"
+      st->err = grc == 2 ? "GMRES stagnated (gmres_stall_cycles restart cycles with < 0.1 % residual reduction)"
                          : "GMRES reached gmres_maxit";
       return NKS_E_DIVERGED;
     }
@@ -630,7 +625,7 @@ nks_status step_impl(nks_state* st, double dt, nks_step_info* info) {
       {
         PhaseScope ps(st, PH_VEC);
         launch_xpay(st->nvec, st->Xb, lam, st->S, st->Xt, st->stream);
-        st->launches += 1;
+        count_launch(st, 1);
       }
       halo(st, st->Xt, st->nf);
       residual(st, st->Xt, st->Ft);
@@ -678,13 +673,13 @@ double change_rate(nks_state* st) {
   {
     PhaseScope ps(st, PH_VEC);
     launch_xpay(n, st->Xn, -1.0, st->Xprev, st->W2, st->stream);
-    st->launches += 1;
+    count_launch(st, 1);
   }
   clean(st, st->W2, (int)(n / st->N));
   {
     PhaseScope ps(st, PH_RED);
     launch_norm_admissible(n, 1, st->W2, nullptr, st->red_part, st->red_out, st->stream);
-    st->launches += 2;
+    count_launch(st, 2);
   }
   comm_allreduce(st, st->red_out, 1);
   CK(cudaMemcpyAsync(st->h_red, st->red_out, sizeof(double), cudaMemcpyDeviceToHost, st->stream));
@@ -812,20 +807,14 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
         CK(cudaMemcpyAsync(B.cover_pos, cov_pos.data(), cov_pos.size() * sizeof(int), cudaMemcpyHostToDevice, st->stream));
       }
       CK(cudaStreamSynchronize(st->stream));
-      if (grid->dim == 2 && B.variant == 0 && std::getenv("NKS_RAS_LEVEL") == nullptr) {
+      if (grid->dim == 2 && B.variant == 0) {
+        // one lane per row, one warp per component, a cluster of stripes per box (ras2d_rows.cu); boxes
+        // the plan cannot take (e.g. > 8 stripes) use the level-synchronous apply of precond.cu
         std::string why;
-        // one lane per row (ras2d_rows.cu); NKS_RAS2D_OLD selects the 4-lanes-per-row design (ras2d.cu)
-        if (std::getenv("NKS_RAS2D_OLD") == nullptr) {
-          st->ras2d = r2::plan(*grid, B, w + L.off_geo, L.geo_bytes, st->stream, why, params->factor_fp32 != 0);
-          if (st->ras2d) st->ras2d_kind = 2;
-        }
-        if (!st->ras2d) {
-          st->ras2d = ras2d_plan(*grid, B, w + L.off_geo, L.geo_bytes, st->stream, why);
-          if (st->ras2d) st->ras2d_kind = 1;
-        }
+        st->ras2d = r2::plan(*grid, B, w + L.off_geo, L.geo_bytes, st->stream, why, params->factor_fp32 != 0);
         if (st->debug)
-          std::fprintf(stderr, "[nks] ras2d pipeline: %s (kind %d, cluster %d)\n", st->ras2d ? "on" : why.c_str(),
-                       st->ras2d_kind, st->ras2d_kind == 2 ? r2::cluster_of(st->ras2d) : ras2d_cluster(st->ras2d));
+          std::fprintf(stderr, "[nks] ras2d pipeline: %s (cluster %d)\n", st->ras2d ? "on" : why.c_str(),
+                       r2::cluster_of(st->ras2d));
         CK(cudaStreamSynchronize(st->stream));
       }
     }
@@ -856,7 +845,7 @@ nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, con
     {
       PhaseScope ps(st, PH_RED);
       launch_energy(st->dp, st->Xn, st->red_part, st->red_out, st->stream);  // u garbage only affects E3 here
-      st->launches += 2;
+      count_launch(st, 2);
     }
     comm_allreduce(st, st->red_out, 5);
     CK(cudaMemcpyAsync(st->h_red, st->red_out, 5 * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
@@ -869,7 +858,7 @@ nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, con
         st->err = e;
         return NKS_E_CUDA;
       }
-      st->launches += 3 + st->d;
+      count_launch(st, 3 + st->d);
     }
     gauge(st, st->Xn);
     level_prep(st);
@@ -1041,7 +1030,7 @@ nks_status nks_eval_jv(nks_state* st, double dt, const double* x_b, const double
     {
       PhaseScope ps(st, PH_OTHER);
       launch_pointwise_jac(st->dp, st->Xn, st->Xt, st->jac4, st->stream);
-      st->launches += 1;
+      count_launch(st, 1);
     }
     jv(st, st->W2, st->Ft);
     CK(cudaMemcpyAsync(Jv, st->Ft, nb, kind_out(on_device), st->stream));
@@ -1059,7 +1048,7 @@ nks_status nks_pc_setup(nks_state* st, double dt, const double* x_b, int32_t on_
     {
       PhaseScope ps(st, PH_OTHER);
       launch_pointwise_jac(st->dp, st->Xn, st->Xb, st->jac4, st->stream);
-      st->launches += 1;
+      count_launch(st, 1);
     }
     pc_setup(st, st->Xb);
     sync(st);
@@ -1092,7 +1081,7 @@ nks_status nks_gmres_solve(nks_state* st, double dt, const double* x_b, const do
     {
       PhaseScope ps(st, PH_OTHER);
       launch_pointwise_jac(st->dp, st->Xn, st->Xb, st->jac4, st->stream);
-      st->launches += 1;
+      count_launch(st, 1);
     }
     if (st->prm.pc_type != NKS_PC_NONE) pc_setup(st, st->Xb);
     double bn, bad;
@@ -1156,8 +1145,7 @@ nks_status nks_destroy(nks_state* st) {
   if (st->h_ring) cudaFreeHost(st->h_ring);
   for (int k = 0; k < 4; ++k)
     if (st->gm_ev[k]) cudaEventDestroy(st->gm_ev[k]);
-  if (st->ras2d_kind == 2) r2::free_plan(st->ras2d);
-  else if (st->ras2d) ras2d_free(st->ras2d);
+  if (st->ras2d) r2::free_plan(st->ras2d);
   delete st;
   return NKS_OK;
 }

@@ -123,8 +123,7 @@ struct nks_state {
   float* fac32 = nullptr;   // fp32 copy of fac (factor_fp32), read by the level-synchronous apply
   double* ybox = nullptr;   // [nf][P]
   bool pc_valid = false;
-  void* ras2d = nullptr;    // plan of the row-pipelined 2D RAS apply (ras2d.cu), or null
-  int ras2d_kind = 0;       // 1: ras2d.cu (4 lanes per row), 2: ras2d_rows.cu (one lane per row)
+  void* ras2d = nullptr;    // plan of the row-pipelined 2D RAS apply (ras2d_rows.cu), or null
   double pc_dt = 0.0;
   // history / controller
   double time = 0.0;

@@ -140,14 +140,6 @@ __device__ __forceinline__ void ld4(const float* p, double (&v)[4]) {
   const float4 a = *reinterpret_cast<const float4*>(p);
   v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
 }
-__device__ __forceinline__ void ldg4(const float* p, double (&v)[4]) {
-  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
-  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-}
-__device__ __forceinline__ void ldg4(const double* p, double (&v)[4]) {
-  const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p + 2));
-  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
-}
 // v <- p[0..3] (shared memory) when on, else unchanged; predicated, so it needs no divergent branch
 __device__ __forceinline__ void ld4_shared_if(bool on, const double* p, double (&v)[4]) {
   asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %4, 0;\n @q ld.shared.v2.f64 {%0, %1}, [%5];\n"
@@ -249,20 +241,17 @@ __global__ void k_pack(Args A, const double* __restrict__ fac, long long ld, int
 }
 
 // ---------------------------------------------------------------------------------- apply
-// GL = true: the consumers load their block rows straight from the packed stream in global memory
-// (LDG, one step ahead into the second register set) and the producer only prefetches the groups
-// ahead into L2 -- no shared-memory staging, so the factor bytes cross the SM's L1/shared data path
-// once instead of twice (bulk-copy write + LDS read).
-// W1 = true: one consumer warp computes all four components of its rows (lane = row, neighbour rows by
-// warp shuffles), so the step needs no cross-warp exchange; the CTA is that warp plus the producer.
-template <bool F32, bool GL, bool W1>
+// (Two alternatives measured in round 1 and removed: block rows read straight from global memory with
+// an L2 prefetch by the producer, 0.62 ms; one warp computing all four components with shuffles,
+// 0.61 ms -- against 0.337 ms for this kernel at config 2.)
+template <bool F32>
 __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   using S = Strm<F32>;
   using T = typename S::T;
   constexpr int kPF = S::PF, kPB = S::PB, kG = S::G, kNSW = S::NS;
-  constexpr int NCW = W1 ? 1 : 4;             // consumer warps; the producer is warp NCW
+  constexpr int NCW = 4;                      // consumer warps; the producer is warp NCW
   constexpr int NT = 32 * (NCW + 1);          // threads on the step barrier
-  constexpr int kRel = W1 ? 1 : 2;            // group g is released in iteration g kG + kG - kRel
+  constexpr int kRel = 2;                     // group g is released in iteration g kG + kG - kRel
   extern __shared__ __align__(128) unsigned char smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const int s = (int)cluster.block_rank();
@@ -324,8 +313,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     const int kb = q < nGr ? q * kG : nFp - kG * (q - nGr + 1);
     const int lo = lo_of(k, ex, R), hi = hi_of(k, R);
     const int pf = p < nFp ? kPF : kPB;
-    if (GL) tb[e] = make_int4((int)((sb * RPC * A.exmax + off[k] - lo) * pf), lo, hi, 0);
-    else tb[e] = make_int4((int)((q % kNSW) * stage_elems) + (off[k] - off[kb] - lo) * pf, lo, hi, 0);
+    tb[e] = make_int4((int)((q % kNSW) * stage_elems) + (off[k] - off[kb] - lo) * pf, lo, hi, 0);
   }
   __syncthreads();
   cluster.sync();
@@ -396,22 +384,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         ++issued;
       }
     };
-    auto prefetch_one = [&](int q) {    // GL: group q's rows into L2
-      const bool fw = q < nGr;
-      const int k0 = klo(q);
-      const int r_lo = off[k0];
-      const int nrows = max(1, off[k0 + kG] - r_lo);
-      const int pf = fw ? kPF : kPB;
-      const T* src = fw ? (const T*)A.chunkF + (base + r_lo) * kPF : (const T*)A.chunkB + (base + r_lo) * kPB;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((unsigned)(nrows * pf * sizeof(T))) : "memory");
-    };
     auto ensure = [&](int G) {          // groups <= G resident
-      if (GL) {                         // prefetch 4 groups past the ones the consumers read next
-        const int G2 = min(G + 4, 2 * nGr - 1);
-        if (lane == 0) for (; issued <= G2; ++issued) prefetch_one(issued);
-        issued = __shfl_sync(0xffffffffu, issued, 0);
-        return;
-      }
       if ((R2_DBG(A) & 128) && issued > 0) return;   // ablation: no copy management after the first groups
       G = min(G, 2 * nGr - 1);
       if (issued <= G) issue_upto(G, true);
@@ -448,7 +421,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     auto ensure_fast = [&](int G) {
       G = min(G, 2 * nGr - 1);
       const bool more = issued <= min(G + kNSW - 1, 2 * nGr - 1) && (issued < kNSW || freed(issued - kNSW));
-      if (ready >= G && !more && !GL) return;
+      if (ready >= G && !more) return;
       ensure(G);
     };
     const int which = min(lane >> 2, 2);
@@ -489,222 +462,6 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       if (dn_remote) poll1(qb, k - dR + dcb);
       step_bar();
     }
-  } else if constexpr (W1) {
-    // ================================================================ one consumer warp, all components
-    const int rl = lane;
-    const bool row_ok = rl < R;
-    const int j = r0 + rl;
-    int gy = (G.s0y + j) % A.ny;
-    if (gy < 0) gy += A.ny;
-    const bool own_row = row_ok && j >= G.oy0 && j < G.oy0 + G.owny;
-    const long long N = A.N;
-    const double* rrow = A.r + (long long)gy * A.nx;            // + c N
-    double* zrow = A.z + (long long)gy * A.nx;                  // + c N
-    double* yrow = A.yscr + sb * A.KGp * 128 + rl * 4;          // y(k) of this row: yrow[k * 128 + 0..3]
-    const unsigned empty0 = smem_u32(emptyb);
-    auto gx_of = [&](int i) {
-      int gx = G.s0x + i;
-      gx += gx < 0 ? A.nx : 0;
-      return gx >= A.nx ? gx - A.nx : gx;
-    };
-    auto zero4 = [&](double (&v)[4]) { v[0] = v[1] = v[2] = v[3] = 0.0; };
-    auto load_r4 = [&](int k, double (&v)[4]) {
-      const int i = k - 2 * rl;
-      if (row_ok && i >= 0 && i < ex && k < nF) {
-        const int gx = gx_of(i);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) v[c] = __ldg(rrow + c * N + gx);
-      } else zero4(v);
-    };
-    auto release_group = [&](int q) {
-      __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(empty0 + (q % kNSW) * 8) : "memory");
-    };
-    auto step_bar = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); };
-    // block rows of processing step p: block b, row c at ptr + b * 16 + c * 4 (active lanes only)
-    struct Ref { const T* ptr; bool on; };
-    auto rowt = [&](int p, int pf) -> Ref {          // forward p / backward p (table entry p + 3)
-      const int4 t = tb[p < nFp ? p : p + 3];
-      return Ref{stage + t.x + rl * pf, rl >= t.y && rl <= t.z};
-    };
-    // acc_c -= B(row c) . v for the four rows c of block b
-    auto mv4 = [&](const Ref& r, int blk, const double (&v)[4], double (&acc)[4]) {
-      if (!r.on) return;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        double m[4];
-        ld4(r.ptr + blk * 16 + c * 4, m);
-        acc[c] = fma(-m[0], v[0], fma(-m[1], v[1], fma(-m[2], v[2], fma(-m[3], v[3], acc[c]))));
-      }
-    };
-    auto shfl_up4 = [&](const double (&v)[4], int d, double (&o)[4]) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) o[c] = __shfl_up_sync(0xffffffffu, v[c], d);
-    };
-    auto shfl_dn4 = [&](const double (&v)[4], int d, double (&o)[4]) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) o[c] = __shfl_down_sync(0xffffffffu, v[c], d);
-    };
-    // ---------------------------------------------------------------- forward sweep (L y = r)
-    {
-      double pre[4], half[4], yp[4], yp2[4];
-      zero4(yp); zero4(yp2);
-      double q0[4], q1[4], q2[4], q3[4];
-      load_r4(2, q0); load_r4(3, q1); load_r4(4, q2); load_r4(5, q3);
-      double r0v[4], r1v[4];
-      load_r4(0, r0v); load_r4(1, r1v);
-      step_bar();
-      {
-        const bool top = rl == 0;
-        double h10[4], h00[4], h01[4];
-        ld4(hcell(1, 0), h10); ld4(hcell(0, 0), h00); ld4(hcell(0, 1), h01);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) { h10[u] = top ? h10[u] : 0.0; h00[u] = top ? h00[u] : 0.0; h01[u] = top ? h01[u] : 0.0; }
-        const Ref a0 = rowt(0, kPF), a1 = rowt(1, kPF);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) { pre[c] = r0v[c]; half[c] = r1v[c]; }
-        mv4(a0, 0, h00, pre); mv4(a0, 2, h10, pre);       // (0,-2), (0,-1) of step 0
-        mv4(a1, 0, h01, half); mv4(a1, 1, h10, half);     // (0,-2), (-1,-1) of step 1
-      }
-      auto fiter = [&](int k, const double (&r2)[4]) {
-        const int i = k - 2 * rl;
-        const bool active = row_ok && (unsigned)i < (unsigned)ex;
-        step_bar();
-        double Ya1[4], aa4[4];
-        shfl_up4(yp, 1, Ya1);                              // (i+1, j-1) at step k-1
-        shfl_up4(yp2, 2, aa4);                             // row j-2 at step k-2
-        if (rl == 0) { ld4(hcell(1, k + 1), Ya1); ld4(hcell(0, k + 2), aa4); }
-        if (rl == 1) ld4(hcell(1, k), aa4);
-        const Ref rk = rowt(k, kPF);
-        const Ref rk1 = k + 1 < nFp ? rowt(k + 1, kPF) : Ref{stage, false};
-        const Ref rk2 = k + 2 < nFp ? rowt(k + 2, kPF) : Ref{stage, false};
-        double y[4], a1[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) { y[c] = pre[c]; a1[c] = 0.0; }
-        mv4(rk, 3, Ya1, y);                                // (1,-1)
-        mv4(rk, 5, yp, a1);                                // (-1,0)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) y[c] = active ? y[c] + a1[c] : 0.0;
-        double b1[4], c1[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) { pre[c] = half[c]; b1[c] = 0.0; half[c] = r2[c]; c1[c] = 0.0; }
-        mv4(rk1, 2, Ya1, pre); mv4(rk1, 4, yp, b1);        // pre(k+1): (0,-1), (-2,0)
-        mv4(rk2, 0, aa4, half); mv4(rk2, 1, Ya1, c1);      // half(k+2): (0,-2), (-1,-1)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) { pre[c] += b1[c]; half[c] += c1[c]; yp2[c] = yp[c]; yp[c] = y[c]; }
-        if (row_ok) {
-          reinterpret_cast<double2*>(yrow + (size_t)k * 128)[0] = make_double2(y[0], y[1]);
-          reinterpret_cast<double2*>(yrow + (size_t)k * 128)[1] = make_double2(y[2], y[3]);
-        }
-        const bool push = dn_remote && active && rl >= R - 2;
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          st_remote1_if(push, hcell(min(max(rl - (R - 2), 0), 1), i) + c, (unsigned)min(s + 1, CS - 1), y[c]);
-        if (k % kG == kG - kRel) release_group(gof(k));
-      };
-      for (int k0 = 0; k0 < nFp; k0 += 4) {
-        fiter(k0, q0); load_r4(k0 + 6, q0);
-        fiter(k0 + 1, q1); load_r4(k0 + 7, q1);
-        fiter(k0 + 2, q2); load_r4(k0 + 8, q2);
-        fiter(k0 + 3, q3); load_r4(k0 + 9, q3);
-      }
-    }
-    __syncwarp();
-    // ---------------------------------------------------------------- backward sweep (U' x = y', folded)
-    {
-      const int dR = 2 * (R - 1);
-      const int K = nFp - 1;
-      auto pofk = [&](int k) { return 2 * nFp - 1 - k; };
-      auto load_y4 = [&](int k, double (&v)[4]) {
-        if (k >= 0) {
-          const double2 a = *reinterpret_cast<const double2*>(yrow + (size_t)k * 128);
-          const double2 b = *reinterpret_cast<const double2*>(yrow + (size_t)k * 128 + 2);
-          v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
-        } else zero4(v);
-      };
-      // acc_c = (D^-1 row c) . y
-      auto dy4 = [&](const Ref& r, const double (&y4)[4], double (&acc)[4]) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          double m[4];
-          if (r.on) ld4(r.ptr + c * 4, m); else zero4(m);
-          acc[c] = fma(m[3], y4[3], fma(m[2], y4[2], fma(m[1], y4[1], m[0] * y4[0])));
-        }
-      };
-      double pre[4], half[4], xp[4], xp2[4];
-      zero4(xp); zero4(xp2);
-      double q0[4], q1[4], q2[4], q3[4];
-      load_y4(K - 2, q0); load_y4(K - 3, q1); load_y4(K - 4, q2); load_y4(K - 5, q3);
-      double yK[4], yK1[4];
-      load_y4(K, yK); load_y4(K - 1, yK1);
-      step_bar();
-      {
-        const int iR = K - dR;
-        const bool bot = rl == R - 1, bot2 = rl == R - 2;
-        double h2a[4], h2b[4], h2c[4], h3a[4], h3b[4];
-        ld4(hcell(2, iR), h2a); ld4(hcell(2, iR + 1), h2b); ld4(hcell(2, iR + 2), h2c);
-        ld4(hcell(3, iR), h3a); ld4(hcell(3, iR - 1), h3b);
-        double Xb2[4], Xb3[4], bb4[4], bb4n[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          Xb2[u] = bot ? h2a[u] : 0.0;
-          Xb3[u] = bot ? h2b[u] : 0.0;
-          bb4[u] = bot ? h3a[u] : (bot2 ? h2c[u] : 0.0);
-          bb4n[u] = bot ? h3b[u] : (bot2 ? h2b[u] : 0.0);
-        }
-        const Ref u0 = rowt(pofk(K), kPB), u1 = rowt(pofk(K - 1), kPB);
-        dy4(u0, yK, pre);
-        mv4(u0, 6, bb4, pre); mv4(u0, 5, Xb3, pre); mv4(u0, 4, Xb2, pre);    // (0,2), (1,1), (0,1)
-        dy4(u1, yK1, half);
-        mv4(u1, 6, bb4n, half); mv4(u1, 5, Xb2, half);                       // (0,2), (1,1) of step K-1
-      }
-      auto biter = [&](int k, const double (&y2)[4]) {
-        const int i = k - 2 * rl;
-        const bool active = row_ok && (unsigned)i < (unsigned)ex;
-        const int iR = k - dR;
-        step_bar();
-        double Xb1[4], bb4[4];
-        shfl_dn4(xp, 1, Xb1);                              // (i-1, j+1) at step k+1
-        shfl_dn4(xp2, 2, bb4);                             // row j+2 at step k+2
-        if (rl == R - 1) { ld4(hcell(2, iR - 1), Xb1); ld4(hcell(3, iR - 2), bb4); }
-        if (rl == R - 2) ld4(hcell(2, iR), bb4);
-        const int p = pofk(k);
-        const Ref rk = rowt(p, kPB);
-        const Ref rk1 = k - 1 >= 0 ? rowt(p + 1, kPB) : Ref{stage, false};
-        const Ref rk2 = k - 2 >= 0 ? rowt(p + 2, kPB) : Ref{stage, false};
-        double x[4], a1[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) { x[c] = pre[c]; a1[c] = 0.0; }
-        mv4(rk, 3, Xb1, x);                                // (-1,1)
-        mv4(rk, 1, xp, a1);                                // (1,0)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) x[c] = active ? x[c] + a1[c] : 0.0;
-        double b1[4], c1[4], yd[4];
-        dy4(rk2, y2, yd);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) { pre[c] = half[c]; b1[c] = 0.0; half[c] = yd[c]; c1[c] = 0.0; }
-        mv4(rk1, 4, Xb1, pre); mv4(rk1, 2, xp, b1);        // pre(k-1): (0,1), (2,0)
-        mv4(rk2, 6, bb4, half); mv4(rk2, 5, Xb1, c1);      // half(k-2): (0,2), (1,1)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) { pre[c] += b1[c]; half[c] += c1[c]; xp2[c] = xp[c]; xp[c] = x[c]; }
-        const bool own = active && own_row && i >= G.ox0 && i < G.ox0 + G.ownx;
-        const int gx = gx_of(min(max(i, 0), ex - 1));
-#pragma unroll
-        for (int c = 0; c < 4; ++c) st_global_if(own, zrow + c * N + gx, x[c]);
-        const bool push = up_remote && active && rl < 2;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) st_remote1_if(push, hcell(2 + min(rl, 1), i) + c, (unsigned)max(s - 1, 0), x[c]);
-        if (p % kG == kG - kRel) release_group(gof(p));
-      };
-      for (int kb0 = 0; kb0 < nFp; kb0 += 4) {
-        const int k0 = K - kb0;
-        biter(k0, q0); load_y4(k0 - 6, q0);
-        biter(k0 - 1, q1); load_y4(k0 - 7, q1);
-        biter(k0 - 2, q2); load_y4(k0 - 8, q2);
-        biter(k0 - 3, q3); load_y4(k0 - 9, q3);
-      }
-    }
   } else {
     // ================================================================ consumers
     const int c = w;                  // output component of this warp
@@ -738,7 +495,6 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       return v;
     };
     auto release_group = [&](int q) {
-      if (GL) return;
       __syncwarp();
       // relaxed: the stage's shared-memory reads all completed into registers before (no fence needed)
       if (lane == 0)
@@ -753,10 +509,6 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       const int kc = min(max(k, 0), nFp);
       const int lo = lo_of(kc, ex, R), hi = hi_of(kc, R);
       const int rr = (k >= 0 && k < nFp && rl >= lo && rl <= hi) ? off[kc] - off[kb] + (rl - lo) : 0;
-      if (GL) {
-        const int rg = (k >= 0 && k < nFp && rl >= lo && rl <= hi) ? off[kc] + (rl - lo) : off[min(kc, nFp - 1)];
-        return (p < nFp ? (const T*)A.chunkF : (const T*)A.chunkB) + (size_t)(sb * RPC * A.exmax + rg) * pf + c * 4;
-      }
       return stage + (size_t)(q % kNSW) * stage_elems + (size_t)rr * pf + c * 4;
     };
     auto ldrow = [&](const T* p, double (&v)[4]) { ld4(p, v); };
@@ -766,14 +518,12 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     struct RowRef { const T* ptr; bool on; };
     auto rowt = [&](int e, int pf) -> RowRef {      // e: row-table entry (forward p, backward p + 3)
       const int4 t = tb[e];
-      const T* b0 = GL ? (e < nFp ? (const T*)A.chunkF : (const T*)A.chunkB) : stage;
-      return RowRef{b0 + t.x + rl * pf + c * 4, rl >= t.y && rl <= t.z};
+      return RowRef{stage + t.x + rl * pf + c * 4, rl >= t.y && rl <= t.z};
     };
     // lanes without a row at that step keep stale (finite) values: every output of such a (lane, step)
     // is discarded (y = active ? ... : 0), and no zeroing keeps ~60 selects and moves per step off the
     // issue path
     auto ldrow_if = [&](const RowRef& r, int blk, double (&v)[4]) {
-      if (GL) { if (r.on) ldg4(r.ptr + blk * 16, v); return; }
       ld4_shared_if(r.on, r.ptr + blk * 16, v);       // predicated loads: no divergent branch per row
     };
     auto dot4 = [&](const double (&m)[4], const double (&v)[4], double acc) {
@@ -1038,10 +788,7 @@ static bool dims_of(const nks_grid& g, Dims& D) {
 static int cs_min(const Dims& D) { return (D.eymax + kRPC - 1) / kRPC; }
 
 // cluster sizes this grid admits: every stripe <= 32 rows and >= 2 rows, portable cluster size <= 8
-static int cs_max() {
-  const char* e = std::getenv("NKS_RAS2D_CSMAX");
-  return e ? std::max(1, std::min(16, std::atoi(e))) : 8;
-}
+static int cs_max() { return 8; }
 static bool cs_ok(const Dims& D, int CS) { return CS >= cs_min(D) && CS <= cs_max() && D.eymin / CS >= 2; }
 
 static int kgp_of(const Dims& D, int RPC) { return D.exmax + 2 * (RPC - 1) + 4 * kGmax + 1; }
@@ -1072,14 +819,8 @@ static size_t smem_for(const Dims& D, int RPC, bool f32) {
 }
 // (A per-lane cp.async variant of the apply -- every consumer lane fetching its own block rows with
 // LDGSTS, no bulk copies -- measured 0.75 ms against the bulk-copy kernel's 0.52 ms and was removed.)
-static bool use_gl() { return std::getenv("NKS_RAS2D_GL") != nullptr; }
-static bool use_w1() { return std::getenv("NKS_RAS2D_W1") != nullptr; }
-static const void* apply_fn(bool f32) {
-  if (use_w1()) return f32 ? (const void*)k_apply<true, false, true> : (const void*)k_apply<false, false, true>;
-  if (use_gl()) return f32 ? (const void*)k_apply<true, true, false> : (const void*)k_apply<false, true, false>;
-  return f32 ? (const void*)k_apply<true, false, false> : (const void*)k_apply<false, false, false>;
-}
-static int apply_threads() { return use_w1() ? 64 : 160; }
+static const void* apply_fn(bool f32) { return f32 ? (const void*)k_apply<true> : (const void*)k_apply<false>; }
+static int apply_threads() { return 160; }
 void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaStream_t stream, std::string& why, bool f32) {
   Dims D;
   if (!dims_of(g, D)) { why = "not 2D"; return nullptr; }
@@ -1093,9 +834,8 @@ void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaSt
   // stripe) whose nbox clusters fit in one wave, else the one with the most resident clusters.
   int CS = 0, ncl = 0;
   size_t smem = 0;
-  const char* cs_env = std::getenv("NKS_RAS2D_CS");
   for (int cs = cs_max(); cs >= 1; --cs) {
-    if (!cs_ok(D, cs) || (cs_env && cs != std::atoi(cs_env))) continue;
+    if (!cs_ok(D, cs)) continue;
     if (cs > 8 && cudaFuncSetAttribute(apply_fn(f32), cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
       cudaGetLastError();
       continue;
@@ -1200,6 +940,10 @@ cudaError_t launch_apply(void* plan, const double* r, double* z, cudaStream_t s)
   Args A = P->A;
   A.r = r;
   A.z = z;
+  // The dynamic shared memory limit is an attribute of the kernel function, not of the plan: another
+  // state's plan may have lowered it since this plan was made, so it is set before every launch.
+  cudaError_t e = cudaFuncSetAttribute(apply_fn(P->f32), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P->nbox * P->CS, 1, 1);
   cfg.blockDim = dim3(apply_threads(), 1, 1);
@@ -1212,14 +956,15 @@ cudaError_t launch_apply(void* plan, const double* r, double* z, cudaStream_t s)
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+#ifdef NKS_R2_ABLATE
+  // ablation / clock-instrumentation build only (tools/, -DNKS_R2_ABLATE)
   static const bool prof = std::getenv("NKS_RAS2D_PROF") != nullptr;
   A.prof = prof ? 1 : 0;
-  static const int dbg = std::getenv("NKS_RAS2D_DBG") ? std::atoi(std::getenv("NKS_RAS2D_DBG")) : 0;
-  A.dbg = dbg;
-  cudaError_t e;
-  if (use_w1()) e = P->f32 ? cudaLaunchKernelEx(&cfg, k_apply<true, false, true>, A) : cudaLaunchKernelEx(&cfg, k_apply<false, false, true>, A);
-  else if (use_gl()) e = P->f32 ? cudaLaunchKernelEx(&cfg, k_apply<true, true, false>, A) : cudaLaunchKernelEx(&cfg, k_apply<false, true, false>, A);
-  else e = P->f32 ? cudaLaunchKernelEx(&cfg, k_apply<true, false, false>, A) : cudaLaunchKernelEx(&cfg, k_apply<false, false, false>, A);
+  A.dbg = std::getenv("NKS_RAS2D_DBG") ? std::atoi(std::getenv("NKS_RAS2D_DBG")) : 0;
+#else
+  const bool prof = false;
+#endif
+  e = P->f32 ? cudaLaunchKernelEx(&cfg, k_apply<true>, A) : cudaLaunchKernelEx(&cfg, k_apply<false>, A);
   if (prof && e == cudaSuccess) {
     static int calls = 0;
     if (++calls % 10 == 0) {
@@ -1230,20 +975,9 @@ cudaError_t launch_apply(void* plan, const double* r, double* z, cudaStream_t s)
       long long tmin = h[4], tmax = 0;
       for (int c = 0; c < nc; ++c) { tmin = std::min(tmin, h[c * 8 + 4]); tmax = std::max(tmax, h[c * 8 + 5]); }
       std::fprintf(stderr, "[ras2d rows prof] CS %d RPC %d, span %lld ns\n", P->CS, P->RPC, tmax - tmin);
-      {
-        std::vector<long long> cp(64 * 4);
-        cudaMemcpyFromSymbol(cp.data(), g_cp, cp.size() * 8);
-        for (int q = 0; q < 24; ++q)
-          std::fprintf(stderr, "  group %d: issue->first test %lld, issue->ready %lld, spins %lld, ready gap %lld\n", q + 8,
-                       cp[q * 4 + 1] - cp[q * 4], cp[q * 4 + 2] - cp[q * 4], cp[q * 4 + 3],
-                       q ? cp[q * 4 + 2] - cp[(q - 1) * 4 + 2] : 0);
-      }
-      std::vector<long long> gt(72 * 8);
-      cudaMemcpyFromSymbol(gt.data(), g_gt, gt.size() * 8);
       for (int c = 0; c < std::min(nc, 2 * P->CS); ++c)
-        std::fprintf(stderr, "  cta %2d (stripe %d): fwd %lld cyc, bwd %lld cyc, halo wait %lld, stage wait %lld, bar wait %lld, "
-                     "start +%lld ns, end +%lld ns\n", c, c % P->CS, h[c * 8], h[c * 8 + 1], h[c * 8 + 2], h[c * 8 + 3],
-                     h[c * 8 + 6], h[c * 8 + 4] - tmin, h[c * 8 + 5] - tmin);
+        std::fprintf(stderr, "  cta %2d (stripe %d): fwd %lld cyc, bwd %lld cyc, start +%lld ns, end +%lld ns\n", c,
+                     c % P->CS, h[c * 8], h[c * 8 + 1], h[c * 8 + 4] - tmin, h[c * 8 + 5] - tmin);
     }
   }
   return e;

@@ -1,21 +1,13 @@
-// Stencil kernels of the NKS step: level-n prep (K3), residual F (K1), pointwise Jacobian cache,
-// matrix-free J.v (K2), energy/mass (K8), gauge (K9), admissibility + norm.
+// Pointwise kernels of the NKS step: level-n prep (K3), pointwise Jacobian cache, energy/mass (K8),
+// gauge (K9), admissibility + norm, fixed-order reductions.  (The residual F (K1) and J.v (K2) are the
+// z-marching tiled kernels of stencil_tiled.cu.)
 //
 // Layout: SoA fp64, field f of a state vector at base + f*N, point index (z*ny + y)*nx + x,
-// periodic wrap in the index arithmetic.  F and J.v use an xy tile of TX x TY points per
-// CTA marching along z ("2.5D"): G_c (resp. w_c) is evaluated once per point of the tile plus a
-// one-cell xy ring into a 3-plane shared-memory ring buffer, so the D M~ D operator reads its
-// neighbours from shared memory and the transcendental work is not recomputed along z.
+// periodic wrap in the index arithmetic.
 #include "model.cuh"
 #include "nks_internal.cuh"
 
 namespace nks {
-
-constexpr int TX = 32;
-constexpr int TY = 8;
-constexpr int RX = TX + 2;
-constexpr int RY = TY + 2;
-constexpr int NT = TX * TY;
 
 __device__ __forceinline__ int wrapc(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
 
@@ -32,27 +24,6 @@ __device__ __forceinline__ long long nb(const Geo& g, int x, int y, int z, int J
   return g.id(x + (J == 0 ? s : 0), y + (J == 1 ? s : 0), z + (J == 2 ? s : 0));
 }
 
-// Laplacian (sum over axes) of f at (x,y,z), f = (fa + fb)/2 if two arrays given.
-template <int DIM>
-__device__ __forceinline__ double lap_half(const Geo& g, const double* __restrict__ fa, const double* __restrict__ fb,
-                                           int x, int y, int z, double fc) {
-  double acc = 0.0;
-#pragma unroll
-  for (int J = 0; J < DIM; ++J) {
-    const long long ip = nb<DIM>(g, x, y, z, J, 1), im = nb<DIM>(g, x, y, z, J, -1);
-    acc += 0.5 * (__ldg(fa + ip) + __ldg(fb + ip)) + 0.5 * (__ldg(fa + im) + __ldg(fb + im)) - 2.0 * fc;
-  }
-  return acc;
-}
-
-template <int DIM>
-__device__ __forceinline__ double lap1(const Geo& g, const double* __restrict__ f, int x, int y, int z, double fc) {
-  double acc = 0.0;
-#pragma unroll
-  for (int J = 0; J < DIM; ++J) acc += __ldg(f + nb<DIM>(g, x, y, z, J, 1)) + __ldg(f + nb<DIM>(g, x, y, z, J, -1)) - 2.0 * fc;
-  return acc;
-}
-
 // sum_J D^_J u_J at (x,y,z); u = base of u_1 (field stride N).
 template <int DIM>
 __device__ __forceinline__ double div_hat(const Geo& g, const double* __restrict__ u, int x, int y, int z, double inv_2h) {
@@ -63,36 +34,6 @@ __device__ __forceinline__ double div_hat(const Geo& g, const double* __restrict
     acc += __ldg(uj + nb<DIM>(g, x, y, z, J, 1)) - __ldg(uj + nb<DIM>(g, x, y, z, J, -1));
   }
   return acc * inv_2h;
-}
-
-// Elastic operator row I: L[C11 D^_I^2 u_I + C44 sum_{J!=I} D^_J^2 u_I + (C12+C44) sum_{M!=I} D^_I D^_M u_M]
-// - K eps0 D^_I c  (= sum_J D^_J sigma^el_IJ, D^ operators commute).
-template <int DIM>
-__device__ __forceinline__ double elastic_row(const DevParams& P, const Geo& g, const double* __restrict__ u,
-                                              const double* __restrict__ c, int I, int x, int y, int z) {
-  const double* uI = u + (long long)I * g.N;
-  const double uc = __ldg(uI + g.id(x, y, z));
-  double diag = 0.0, offd = 0.0, mixed = 0.0;
-#pragma unroll
-  for (int J = 0; J < DIM; ++J) {
-    const double s2 = __ldg(uI + nb<DIM>(g, x, y, z, J, 2)) + __ldg(uI + nb<DIM>(g, x, y, z, J, -2)) - 2.0 * uc;
-    if (J == I) diag = s2; else offd += s2;
-  }
-#pragma unroll
-  for (int M = 0; M < DIM; ++M) {
-    if (M == I) continue;
-    const double* uM = u + (long long)M * g.N;
-    const int dxI = I == 0, dyI = I == 1, dzI = I == 2;
-    const int dxM = M == 0, dyM = M == 1, dzM = M == 2;
-    const double pp = __ldg(uM + g.id(x + dxI + dxM, y + dyI + dyM, z + dzI + dzM));
-    const double pm = __ldg(uM + g.id(x + dxI - dxM, y + dyI - dyM, z + dzI - dzM));
-    const double mp = __ldg(uM + g.id(x - dxI + dxM, y - dyI + dyM, z - dzI + dzM));
-    const double mm = __ldg(uM + g.id(x - dxI - dxM, y - dyI - dyM, z - dzI - dzM));
-    mixed += (pp - pm) - (mp - mm);
-  }
-  const double el = P.Ls * (P.C11 * diag + P.C44 * offd + (P.C12 + P.C44) * mixed) * P.inv_4h2;
-  const double dc = (__ldg(c + nb<DIM>(g, x, y, z, I, 1)) - __ldg(c + nb<DIM>(g, x, y, z, I, -1))) * P.inv_2h;
-  return el - P.K * P.eps0 * dc;
 }
 
 // -------------------------------------------------------------------------------------- K3
@@ -108,87 +49,6 @@ __global__ void k_level_prep(DevParams P, const double* __restrict__ X, double* 
   }
 }
 
-// -------------------------------------------------------------------------------------- K1
-template <int DIM>
-__global__ void __launch_bounds__(NT) k_residual(DevParams P, const double* __restrict__ Xa, const double* __restrict__ Xb,
-                                                 const double* __restrict__ Ta, double* __restrict__ F, int zc) {
-  __shared__ double sG[3][RY][RX];
-  __shared__ double sE[2][TY][TX];
-  const Geo g{P.nx, P.ny, P.nz, P.N};
-  const long long N = P.N;
-  const double* ca_ = Xa;
-  const double* ea_ = Xa + N;
-  const double* cb_ = Xb;
-  const double* eb_ = Xb + N;
-  const double* ub_ = Xb + 2 * N;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int z0 = blockIdx.z * zc;
-  const int z1 = min(z0 + zc, P.nz);
-  const int tid = threadIdx.x;
-
-  auto ring = [&](int z, int slot) {
-    for (int r = tid; r < RX * RY; r += NT) {
-      const int rx = r % RX - 1, ry = r / RX - 1;
-      const int x = x0 + rx, y = y0 + ry;
-      const long long i = g.id(x, y, z);
-      const double ca = __ldg(ca_ + i), cb = __ldg(cb_ + i), ea = __ldg(ea_ + i), eb = __ldg(eb_ + i);
-      double gc, ge;
-      pointwise_G(P, ca, cb, ea, eb, gc, ge);
-      const double ch = 0.5 * (ca + cb);
-      const double Tb = P.K * (div_hat<DIM>(g, ub_, x, y, z, P.inv_2h) - DIM * P.eps0 * (cb - P.cbar0));
-      gc += -0.5 * P.eps0 * (__ldg(Ta + i) + Tb) - P.gamma_c * P.inv_h2 * lap_half<DIM>(g, ca_, cb_, x, y, z, ch);
-      sG[slot][ry + 1][rx + 1] = gc;
-      if (rx >= 0 && rx < TX && ry >= 0 && ry < TY) {
-        const double eh = 0.5 * (ea + eb);
-        ge += -3.0 * P.gamma_eta * P.inv_h2 * lap_half<DIM>(g, ea_, eb_, x, y, z, eh);
-        sE[z & 1][ry][rx] = ge;
-      }
-    }
-  };
-
-  auto fpass = [&](int z, int sm, int s0, int sp) {
-    const int tx = tid % TX, ty = tid / TX;
-    const int x = x0 + tx, y = y0 + ty;
-    if (x >= P.nx || y >= P.ny) return;
-    const long long i = g.id(x, y, z);
-    const double ca = __ldg(ca_ + i), cb = __ldg(cb_ + i);
-    const double G = sG[s0][ty + 1][tx + 1];
-    const double mi = ca * (1.0 - ca);
-    double div = 0.0;
-#pragma unroll
-    for (int J = 0; J < DIM; ++J) {
-      const double cp = __ldg(ca_ + nb<DIM>(g, x, y, z, J, 1)), cm = __ldg(ca_ + nb<DIM>(g, x, y, z, J, -1));
-      double Gp, Gm;
-      if (J == 0) { Gp = sG[s0][ty + 1][tx + 2]; Gm = sG[s0][ty + 1][tx]; }
-      else if (J == 1) { Gp = sG[s0][ty + 2][tx + 1]; Gm = sG[s0][ty][tx + 1]; }
-      else { Gp = sG[sp][ty + 1][tx + 1]; Gm = sG[sm][ty + 1][tx + 1]; }
-      div += (mi + cp * (1.0 - cp)) * (Gp - G) - (mi + cm * (1.0 - cm)) * (G - Gm);
-    }
-    div *= 0.5 * P.kappa * P.inv_h2;
-    F[i] = (cb - ca) * P.inv_dt - div;
-    F[N + i] = (__ldg(eb_ + i) - __ldg(ea_ + i)) * P.inv_dt + sE[z & 1][ty][tx];
-#pragma unroll
-    for (int I = 0; I < DIM; ++I) F[(2 + I) * N + i] = elastic_row<DIM>(P, g, ub_, cb_, I, x, y, z);
-  };
-
-  if (DIM == 2) {
-    ring(0, 0);
-    __syncthreads();
-    fpass(0, 0, 0, 0);
-    return;
-  }
-  // z-marching: planes z0-1, z0 first, then for z = z0+1 .. z1: compute plane z, emit F at z-1.
-  ring(z0 - 1, 0);
-  ring(z0, 1);
-  for (int z = z0 + 1; z <= z1; ++z) {
-    const int k = z - z0 + 1;          // slot of plane z is k % 3
-    ring(z, k % 3);
-    __syncthreads();
-    fpass(z - 1, (k + 1) % 3, (k + 2) % 3, k % 3);
-    __syncthreads();
-  }
-}
-
 // Pointwise partials a11, a12, a21, a22 (cached per Newton iterate; used by J.v and assembly).
 __global__ void k_pointwise_jac(DevParams P, const double* __restrict__ Xa, const double* __restrict__ Xb,
                                 double* __restrict__ jac4) {
@@ -200,82 +60,6 @@ __global__ void k_pointwise_jac(DevParams P, const double* __restrict__ Xa, cons
     jac4[N + i] = a12;
     jac4[2 * N + i] = a21;
     jac4[3 * N + i] = a22;
-  }
-}
-
-// -------------------------------------------------------------------------------------- K2
-template <int DIM>
-__global__ void __launch_bounds__(NT) k_jv(DevParams P, const double* __restrict__ Xa, const double* __restrict__ jac4,
-                                           const double* __restrict__ v, double* __restrict__ out, int zc) {
-  __shared__ double sW[3][RY][RX];
-  const Geo g{P.nx, P.ny, P.nz, P.N};
-  const long long N = P.N;
-  const double* ca_ = Xa;
-  const double* vc_ = v;
-  const double* ve_ = v + N;
-  const double* vu_ = v + 2 * N;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int z0 = blockIdx.z * zc;
-  const int z1 = min(z0 + zc, P.nz);
-  const int tid = threadIdx.x;
-  const double cT = 0.5 * P.K * DIM * P.eps0 * P.eps0;     // d(G3_c)/d(c^b)
-  const double cU = -0.5 * P.eps0 * P.K;                    // d(G3_c)/d(sum D^ u)
-  const double cL = -0.5 * P.gamma_c * P.inv_h2;            // d(G4_c)/d(c^b) Laplacian weight
-
-  auto ring = [&](int z, int slot) {
-    for (int r = tid; r < RX * RY; r += NT) {
-      const int rx = r % RX - 1, ry = r / RX - 1;
-      const int x = x0 + rx, y = y0 + ry;
-      const long long i = g.id(x, y, z);
-      const double vc = __ldg(vc_ + i);
-      const double w = __ldg(jac4 + i) * vc + __ldg(jac4 + N + i) * __ldg(ve_ + i) + cT * vc +
-                       cU * div_hat<DIM>(g, vu_, x, y, z, P.inv_2h) + cL * lap1<DIM>(g, vc_, x, y, z, vc);
-      sW[slot][ry + 1][rx + 1] = w;
-    }
-  };
-
-  auto fpass = [&](int z, int sm, int s0, int sp) {
-    const int tx = tid % TX, ty = tid / TX;
-    const int x = x0 + tx, y = y0 + ty;
-    if (x >= P.nx || y >= P.ny) return;
-    const long long i = g.id(x, y, z);
-    const double ca = __ldg(ca_ + i);
-    const double W = sW[s0][ty + 1][tx + 1];
-    const double mi = ca * (1.0 - ca);
-    double div = 0.0;
-#pragma unroll
-    for (int J = 0; J < DIM; ++J) {
-      const double cp = __ldg(ca_ + nb<DIM>(g, x, y, z, J, 1)), cm = __ldg(ca_ + nb<DIM>(g, x, y, z, J, -1));
-      double Wp, Wm;
-      if (J == 0) { Wp = sW[s0][ty + 1][tx + 2]; Wm = sW[s0][ty + 1][tx]; }
-      else if (J == 1) { Wp = sW[s0][ty + 2][tx + 1]; Wm = sW[s0][ty][tx + 1]; }
-      else { Wp = sW[sp][ty + 1][tx + 1]; Wm = sW[sm][ty + 1][tx + 1]; }
-      div += (mi + cp * (1.0 - cp)) * (Wp - W) - (mi + cm * (1.0 - cm)) * (W - Wm);
-    }
-    div *= 0.5 * P.kappa * P.inv_h2;
-    const double vc = __ldg(vc_ + i), ve = __ldg(ve_ + i);
-    out[i] = vc * P.inv_dt - div;
-    out[N + i] = ve * P.inv_dt + __ldg(jac4 + 2 * N + i) * vc + __ldg(jac4 + 3 * N + i) * ve -
-                 1.5 * P.gamma_eta * P.inv_h2 * lap1<DIM>(g, ve_, x, y, z, ve);
-    // u rows: elastic operator on v_u with eigen-term -K eps0 D^_I v_c (the constant cbar0 drops)
-#pragma unroll
-    for (int I = 0; I < DIM; ++I) out[(2 + I) * N + i] = elastic_row<DIM>(P, g, vu_, vc_, I, x, y, z);
-  };
-
-  if (DIM == 2) {
-    ring(0, 0);
-    __syncthreads();
-    fpass(0, 0, 0, 0);
-    return;
-  }
-  ring(z0 - 1, 0);
-  ring(z0, 1);
-  for (int z = z0 + 1; z <= z1; ++z) {
-    const int k = z - z0 + 1;
-    ring(z, k % 3);
-    __syncthreads();
-    fpass(z - 1, (k + 1) % 3, (k + 2) % 3, k % 3);
-    __syncthreads();
   }
 }
 
@@ -454,38 +238,15 @@ __global__ void k_gauge_apply(DevParams P, double* __restrict__ X, int evenmask,
 }
 
 // -------------------------------------------------------------------------------------- host launchers
-static int zchunk_for(const DevParams& P) {
-  if (P.dim == 2) return 1;
-  // enough CTAs to fill the chip several times, long columns to amortise the z-ring
-  const long long tiles = (long long)((P.nx + TX - 1) / TX) * ((P.ny + TY - 1) / TY);
-  int zc = P.nz;
-  while (zc > 4 && tiles * ((P.nz + zc - 1) / zc) < 4 * 148) zc = (zc + 1) / 2;
-  return zc;
-}
-
 void launch_level_prep(const DevParams& P, const double* X, double* T, cudaStream_t s) {
   const int blocks = (int)std::min<long long>((P.N + 255) / 256, 148 * 16);
   if (P.dim == 2) k_level_prep<2><<<blocks, 256, 0, s>>>(P, X, T);
   else k_level_prep<3><<<blocks, 256, 0, s>>>(P, X, T);
 }
 
-void launch_residual(const DevParams& P, const double* Xa, const double* Xb, const double* Ta, double* F, cudaStream_t s) {
-  const int zc = zchunk_for(P);
-  dim3 grid((P.nx + TX - 1) / TX, (P.ny + TY - 1) / TY, (P.nz + zc - 1) / zc);
-  if (P.dim == 2) k_residual<2><<<grid, NT, 0, s>>>(P, Xa, Xb, Ta, F, zc);
-  else k_residual<3><<<grid, NT, 0, s>>>(P, Xa, Xb, Ta, F, zc);
-}
-
 void launch_pointwise_jac(const DevParams& P, const double* Xa, const double* Xb, double* jac4, cudaStream_t s) {
   const int blocks = (int)std::min<long long>((P.N + 255) / 256, 148 * 16);
   k_pointwise_jac<<<blocks, 256, 0, s>>>(P, Xa, Xb, jac4);
-}
-
-void launch_jv(const DevParams& P, const double* Xa, const double* jac4, const double* v, double* out, cudaStream_t s) {
-  const int zc = zchunk_for(P);
-  dim3 grid((P.nx + TX - 1) / TX, (P.ny + TY - 1) / TY, (P.nz + zc - 1) / zc);
-  if (P.dim == 2) k_jv<2><<<grid, NT, 0, s>>>(P, Xa, jac4, v, out, zc);
-  else k_jv<3><<<grid, NT, 0, s>>>(P, Xa, jac4, v, out, zc);
 }
 
 void launch_norm_admissible(long long N, int nf, const double* F, const double* X, double* part, double* out,

@@ -502,11 +502,14 @@ void launch_residual_tiled(const DevParams& P, const double* Xa, const double* X
   using namespace tj;
   const int dim = P.dim;
   const size_t smem = residual_tiled_smem(dim);
-  static bool attr[4] = {false, false, false, false};
-  if (!attr[dim]) {
+  // the smem opt-in is per device: cached per (device, dim); a failure surfaces at the launch below
+  static bool attr[64][4] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr[dev][dim]) {
     if (dim == 2) cudaFuncSetAttribute(k_residual_tiled<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     else cudaFuncSetAttribute(k_residual_tiled<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr[dim] = true;
+    if (dev >= 0 && dev < 64) attr[dev][dim] = true;
   }
   const int tiles = ((P.nx + TX - 1) / TX) * ((P.ny + TY - 1) / TY);
   int zc = 1;
@@ -531,11 +534,14 @@ void launch_jv_tiled(const DevParams& P, const double* Xa, const double* jac4, c
   using namespace tj;
   const int dim = P.dim;
   const size_t smem = jv_tiled_smem(dim);
-  static bool attr[4] = {false, false, false, false};
-  if (!attr[dim]) {
+  // the smem opt-in is per device: cached per (device, dim); a failure surfaces at the launch below
+  static bool attr[64][4] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr[dev][dim]) {
     if (dim == 2) cudaFuncSetAttribute(k_jv_tiled<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     else cudaFuncSetAttribute(k_jv_tiled<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr[dim] = true;
+    if (dev >= 0 && dev < 64) attr[dev][dim] = true;
   }
   const int tiles = ((P.nx + TX - 1) / TX) * ((P.ny + TY - 1) / TY);
   int zc = 1;

@@ -41,6 +41,7 @@ class Params(C.Structure):
         ("ls_alpha", C.c_double), ("ls_max_halvings", C.c_int32),
         ("zeta", C.c_double), ("dt_min", C.c_double), ("dt_max", C.c_double), ("dt_init", C.c_double),
         ("dt_floor_factor", C.c_double), ("xd_norm", C.c_int32), ("factor_fp32", C.c_int32),
+        ("gmres_stall_cycles", C.c_int32),
     ]
 
 
@@ -148,6 +149,7 @@ def make_params(model: dict, solver: dict, pc_type=PC_RAS_BILU0, pc_reuse=1) -> 
     p.pc_reuse = int(pc_reuse)
     p.xd_norm = {"rms": 0, "l2": 1, "ceta_l2": 2}[solver.get("xd_norm", "rms")]
     p.factor_fp32 = int(solver.get("factor_fp32", 0))
+    p.gmres_stall_cycles = int(solver.get("gmres_stall_cycles", 0))
     return p
 
 
