@@ -144,15 +144,27 @@ def norm(F):
     return float(np.sqrt(np.sum(F * F)))
 
 
-def newton_step(m: scheme.Model, Xa, dt, cbar0, sol: dict, X0=None):
-    """One NSOA-1 time step by exact Newton.  Returns (X^b, info)."""
+def direct_linsolve(m: scheme.Model, Xa, X, dt, cbar0, b, fnorm):
+    """J S = b by the gauge-pinned sparse direct LU (reading R14): exact up to rounding."""
+    J = jacobian.assemble(m, Xa, X, dt)
+    A, bb = pin(J, b.ravel(), pinned_rows(X.shape[1:], m.d))
+    return spla.spsolve(A, bb).reshape(X.shape)
+
+
+def newton_step(m: scheme.Model, Xa, dt, cbar0, sol: dict, X0=None, linsolve=None):
+    """One NSOA-1 time step by Newton.  Returns (X^b, info).
+
+    linsolve(m, Xa, X, dt, cbar0, b, fnorm) -> S solves J(X) S = b with b = -F(X) whose u rows are
+    projected onto range(J) (the u_I sub-lattice sums span the left null space, reading R14); the
+    default is the exact gauge-pinned direct LU, ``krylov.make_linsolve`` the GMRES path of the
+    large-grid parity cases.  A linsolve returning None is a linear-solver failure (DIVERGED)."""
     d = m.d
     shape = Xa.shape[1:]
     X = (Xa if X0 is None else X0).copy()          # X_0 = X^n (reading R29)
     F = scheme.residual(m, Xa, X, dt, cbar0)
     f0 = norm(F)
     hist = [f0]
-    rows = pinned_rows(shape, d)
+    solve = linsolve if linsolve is not None else direct_linsolve
     info = {"converged": False, "reason": "", "newton_its": 0, "fnorm0": f0, "hist": hist,
             "lambdas": []}
     for it in range(sol["newton_maxit"] + 1):
@@ -162,9 +174,10 @@ def newton_step(m: scheme.Model, Xa, dt, cbar0, sol: dict, X0=None):
         if it == sol["newton_maxit"]:
             info["reason"] = "newton_maxit"
             return Xa.copy(), info
-        J = jacobian.assemble(m, Xa, X, dt)
-        A, b = pin(J, -F.ravel(), rows)
-        S = spla.spsolve(A, b).reshape(X.shape)
+        S = solve(m, Xa, X, dt, cbar0, gauge_project(-F), hist[-1])
+        if S is None:
+            info["reason"] = "linear_solver"
+            return Xa.copy(), info
         lam, fn = 1.0, hist[-1]
         accepted = False
         for _ in range(sol["ls_max_halvings"] + 1):
@@ -216,7 +229,7 @@ def change_rate(Xn, Xprev, dt_prev, kind: str = "rms") -> float:
     return nrm / dt_prev
 
 
-def run_adaptive(m: scheme.Model, X0, cbar0, sol: dict, nsteps: int, forced_dts=None):
+def run_adaptive(m: scheme.Model, X0, cbar0, sol: dict, nsteps: int, forced_dts=None, linsolve=None):
     """Adaptive time stepping.  forced_dts: optional list of accepted dt to replay."""
     X = X0.copy()
     Xprev = None
@@ -232,7 +245,7 @@ def run_adaptive(m: scheme.Model, X0, cbar0, sol: dict, nsteps: int, forced_dts=
             dt = predict_dt(change_rate(X, Xprev, dt_prev, sol["xd_norm"]), zeta, sol["dt_min"], sol["dt_max"])
         retries = 0
         while True:
-            Xb, info = newton_step(m, X, dt, cbar0, sol)
+            Xb, info = newton_step(m, X, dt, cbar0, sol, linsolve=linsolve)
             if info["converged"] or forced_dts is not None:
                 break
             dt /= math.sqrt(2)
