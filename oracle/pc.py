@@ -13,6 +13,9 @@ writes out the textbook definitions with the readings of DESIGN.md:
 * ILU(0) (R21): natural (x fastest) ordering of the local points, point blocks of size 2+d,
   pattern = the block footprint; the unique unit-lower L, upper U with (LU)_pq = A_pq on the
   pattern, computed by the IKJ elimination.
+* ILU(k) (Table 1: ILU(1), ILU(2), LU): the same IKJ elimination on the
+  level-of-fill pattern of Saad's ILU(p) (symbolic phase `fill_levels`); no level limit gives the
+  exact block LU (no pivoting, natural order).
 * left-RAS (R19): z = sum_i R_i^{0T} (L_i U_i)^{-1} R_i^delta r -- gather on the extended box,
   scatter the owned points only.
 """
@@ -118,6 +121,54 @@ def bilu0(A, npts):
     return L, U
 
 
+def fill_levels(A, npts, k):
+    """Symbolic ILU(k) (Saad, Iterative Methods, Sec. 10.3.3 / Alg. 10.5): level-of-fill of every block
+    entry, lev(i,j) = 0 on the pattern of A and lev(i,j) = min over k < min(i,j) of
+    lev(i,k) + lev(k,j) + 1 for fill, keeping only entries with lev <= k.  k = None: no limit
+    (the pattern of the exact LU factors).  Returns {row: {col: level}}."""
+    rows = {i: {} for i in range(npts)}
+    for (p, q) in A:
+        rows[p][q] = 0
+    for i in range(npts):
+        row = rows[i]
+        done = set()
+        while True:
+            cand = [q for q in row if q < i and q not in done]
+            if not cand:
+                break
+            kk = min(cand)
+            done.add(kk)
+            lik = row[kk]
+            for j, lkj in rows[kk].items():
+                if j <= kk:
+                    continue
+                lev = lik + lkj + 1
+                if (k is None or lev <= k) and (j not in row or row[j] > lev):
+                    row[j] = lev
+    return rows
+
+
+def biluk(A, npts, k):
+    """Point-block ILU(k), IKJ variant on the level-k pattern (Saad Alg. 10.5 with blocks; k = 0 is
+    ILU(0), k = None the exact block LU without pivoting).  Returns (L, U) dicts (L unit lower)."""
+    levels = fill_levels(A, npts, k)
+    nf = next(iter(A.values())).shape[0]
+    W = {}
+    for i in range(npts):
+        for j in levels[i]:
+            W[(i, j)] = A[(i, j)].copy() if (i, j) in A else np.zeros((nf, nf))
+    cols = {i: sorted(levels[i]) for i in range(npts)}
+    for i in range(npts):
+        for kk in [q for q in cols[i] if q < i]:
+            W[(i, kk)] = W[(i, kk)] @ np.linalg.inv(W[(kk, kk)])
+            for j in [q for q in cols[kk] if q > kk]:
+                if (i, j) in W:
+                    W[(i, j)] = W[(i, j)] - W[(i, kk)] @ W[(kk, j)]
+    L = {key: v for key, v in W.items() if key[1] < key[0]}
+    U = {key: v for key, v in W.items() if key[1] >= key[0]}
+    return L, U
+
+
 def lu_solve(L, U, r, npts):
     """Solve (L U) x = r with r of shape (npts, nf): forward then backward block substitution."""
     rowsL, rowsU = {}, {}
@@ -155,7 +206,9 @@ class RAS:
       "rras" z = sum_i R_i^{deltaT} A_i^{-1} R_i^0 r      right-restricted (input restricted to owned points)
     """
 
-    def __init__(self, J, shape, nf, nsub, delta, exact: bool = False, variant: str = "ras"):
+    def __init__(self, J, shape, nf, nsub, delta, exact: bool = False, variant: str = "ras", fill=0):
+        """fill: subdomain solver ILU(fill) (0 = BILU(0), the default; k > 0 = level-k ILU; None = the
+        exact block LU through the level-of-fill path); exact=True: dense LAPACK solve of A_i."""
         assert variant in ("ras", "as", "rras")
         self.variant = variant
         self.shape = shape
@@ -167,8 +220,11 @@ class RAS:
             A, pts = box_blocks(J, b, nf, self.npts)
             if exact:
                 self.fact.append(("lu", self._dense(A, len(pts)), pts))
-            else:
+            elif fill == 0:
                 L, U = bilu0(A, len(pts))
+                self.fact.append(("ilu", (L, U), pts))
+            else:
+                L, U = biluk(A, len(pts), fill)
                 self.fact.append(("ilu", (L, U), pts))
 
     def _dense(self, A, npts):

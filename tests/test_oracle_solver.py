@@ -306,3 +306,101 @@ def test_ras_block_diagonal_reduces_to_block_jacobi():
     z = ras.apply(r).reshape(nf, 64)
     zref = np.stack([np.linalg.solve(blocks[p], r.reshape(nf, 64)[:, p]) for p in range(64)], axis=1)
     np.testing.assert_allclose(z, zref, rtol=1e-12)
+
+
+# ----------------------------------------------------------------------------- ILU(k) subdomain solvers
+
+def _box_matrix(shape=(8, 8), nsub=(2, 2), delta=1, dt=0.1):
+    m, Xa, Xb, cbar = state(2, shape)
+    J = jacobian.assemble(m, Xa, Xb, dt)
+    b = pc.boxes(shape, nsub, delta)[0]
+    A, pts = pc.box_blocks(J, b, 4, int(np.prod(shape)))
+    return A, len(pts)
+
+
+def _fill_path_levels(A, n):
+    """Level of fill by the fill-path theorem (Hysom & Pothen 2001): lev(i, j) = (edges of the shortest
+    path i -> j in the graph of A whose interior vertices are all < min(i, j)) - 1; brute force BFS."""
+    adj = {i: set() for i in range(n)}
+    for (p, q) in A:
+        if p != q:
+            adj[p].add(q)
+    lev = {}
+    for i in range(n):
+        for j in range(n):
+            if i == j:
+                continue
+            lim = min(i, j)
+            dist = {i: 0}
+            frontier = [i]
+            found = None
+            while frontier and found is None:
+                nxt = []
+                for v in frontier:
+                    for w in adj[v]:
+                        if w == j:
+                            found = dist[v] + 1
+                            break
+                        if w < lim and w not in dist:
+                            dist[w] = dist[v] + 1
+                            nxt.append(w)
+                    if found is not None:
+                        break
+                frontier = nxt
+            if found is not None:
+                lev[(i, j)] = found - 1
+    return lev
+
+
+def test_fill_levels_match_the_fill_path_theorem():
+    A, n = _box_matrix(shape=(6, 6), nsub=(1, 1), delta=0)        # 36 points, 13-point pattern
+    ref = _fill_path_levels(A, n)
+    for k in (0, 1, 2, 3):
+        got = pc.fill_levels(A, n, k)
+        want = {(i, j) for (i, j), lv in ref.items() if lv <= k}
+        have = {(i, j) for i in range(n) for j, lv in got[i].items() if i != j}
+        assert have == want, k
+        for (i, j) in have:
+            assert got[i][j] == ref[(i, j)]
+
+
+def test_biluk_level0_is_bilu0():
+    A, n = _box_matrix()
+    L0, U0 = pc.bilu0(A, n)
+    L, U = pc.biluk(A, n, 0)
+    assert set(L) == set(L0) and set(U) == set(U0)
+    for key in L0:
+        np.testing.assert_allclose(L[key], L0[key], rtol=1e-14, atol=1e-14 * np.abs(L0[key]).max())
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_biluk_defining_property(k):
+    """(L U)_pq = A_pq on the level-k pattern (the definition of ILU(k)); the pattern grows with k."""
+    A, n = _box_matrix()
+    L, U = pc.biluk(A, n, k)
+    pattern = set(L) | set(U)
+    assert len(pattern) > len(A)
+    nf = 4
+    for (p, q) in pattern:
+        acc = np.zeros((nf, nf))
+        for kk in range(min(p, q) + 1):
+            lpk = np.eye(nf) if kk == p else L.get((p, kk))
+            ukq = U.get((kk, q))
+            if lpk is not None and ukq is not None:
+                acc += lpk @ ukq
+        ref = A.get((p, q), np.zeros((nf, nf)))
+        scale = max(np.abs(ref).max(), 1.0)
+        np.testing.assert_allclose(acc, ref, rtol=0, atol=1e-10 * scale)
+
+
+def test_biluk_unlimited_is_the_exact_lu():
+    """No level limit: L U = A exactly, and the RAS apply equals the one with dense LAPACK box solves."""
+    shape, nsub, delta = (8, 8), (2, 2), 1
+    m, Xa, Xb, cbar = state(2, shape)
+    J = jacobian.assemble(m, Xa, Xb, 0.1)
+    r = ni.random_direction(4, shape, 3)
+    z_lu = pc.RAS(J, shape, 4, nsub, delta, fill=None).apply(r)
+    z_ex = pc.RAS(J, shape, 4, nsub, delta, exact=True).apply(r)
+    np.testing.assert_allclose(z_lu, z_ex, rtol=0, atol=1e-10 * np.abs(z_ex).max())
+    z0 = pc.RAS(J, shape, 4, nsub, delta).apply(r)
+    assert np.abs(z0 - z_ex).max() > 1e-6 * np.abs(z_ex).max()   # ILU(0) is not exact on these boxes
