@@ -14,9 +14,10 @@ e2e    = the same through the C ABI with HOST buffers: every step uploads X^n fr
          memory (nks_set_fields, on_device = 0), runs nks_step with the dt the device run
          accepted and downloads X^{n+1} (nks_get_fields) -- copies inside the timed region;
 roofline = the dominant kernel of the step (per-phase CUDA events recorded by the library on
-         its own stream during the timed region), algorithmic bytes per launch / mean duration,
-         against MEASURED_PEAKS.json hbm_gbs;
-cpu_baseline = the oracle (oracle/, plain NumPy/SciPy) as it stands, on a bounded sample.
+         its own stream in a profiled pass of 2 steps right after the unprofiled timed region),
+         algorithmic bytes per launch / mean duration, against MEASURED_PEAKS.json hbm_gbs;
+cpu_baseline = the oracle (oracle/, plain NumPy/SciPy) as it stands, timed on one step of the same
+         trajectory on the full grid (and compared with the GPU's result of that step).
 
 N > 1: config 2 (2D) runs independent replicas per rank (the 2D sweep is not sharded; DESIGN.md
 "Multi-GPU"), scaling "weak", value = all ranks' steps / max-over-ranks time.  3D configs
@@ -150,59 +151,90 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------- oracle
-def oracle_sample(cfg, seconds_hint=20.0):
-    """Oracle (plain NumPy/SciPy, as it stands) NKS steps on a bounded sample of the workload.
+def oracle_model_sol(cfg, sol):
+    from oracle import scheme
+    return scheme.Model.from_dict(len(cfg["shape"]), cfg["h"], ni.model_default()), dict(sol)
 
-    The oracle's exact-Newton step (sparse direct LU) on the full 512^2 grid takes tens of
-    minutes, so the sample is the same recipe (seed 0, dt = 0.01, same model and tolerances)
-    on a 64x64 periodic grid; the time per step is scaled linearly by the point count to the
-    workload's grid (a LOWER bound on the oracle's true time: the direct LU is superlinear).
-    """
-    from oracle import scheme, solver
-    import torch
-    shape = (64, 64)
-    d = len(shape)
-    m = scheme.Model.from_dict(d, 0.25, ni.model_default())
-    sol = ni.solver_default()
-    c, eta = ni.initial_fields(shape, 0)
-    cbar = c.mean()
-    X = np.concatenate([c[None], eta[None], solver.init_displacement(m, c, cbar)])
+
+def oracle_threads():
+    """Host threads the oracle can use: NumPy elementwise work runs on one core, scipy.fft (the
+    spectral preconditioner) on os.cpu_count() workers."""
+    return os.cpu_count() or 1
+
+
+def oracle_step_sample(cfg, sol, Xn, cbar0, dt):
+    """One oracle NKS step (oracle/, plain NumPy/SciPy as it stands) of the FULL config grid: Newton
+     with the oracle's large-grid Krylov path (matrix-free J v + spectral-preconditioned
+    GMRES(30), oracle/krylov.py) from X^n with the given dt.  Returns (X^{n+1}, info, seconds)."""
+    from oracle import krylov, solver
+    m, sol = oracle_model_sol(cfg, sol)
     t0 = time.perf_counter()
-    n = 0
-    while True:
-        X, info = solver.newton_step(m, X, 0.01, cbar, sol)
-        n += 1
-        if time.perf_counter() - t0 >= seconds_hint or n >= 8:
-            break
-    el = time.perf_counter() - t0
-    scale = float(np.prod(shape)) / float(np.prod(cfg["shape"]))
-    sps = n / el * scale
-    cores = torch.get_num_threads()
-    return {"value": sps, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{n} oracle exact-Newton steps (sparse LU) on 2D 64x64, dt=0.01, seed 0, {el:.1f} s; "
-                      f"steps/s scaled by points 64^2/{'x'.join(map(str, cfg['shape']))} (lower bound)",
-            "os_cpu_count": os.cpu_count()}
+    X, info = solver.newton_step(m, Xn, dt, cbar0, sol, linsolve=krylov.make_linsolve())
+    return X, info, time.perf_counter() - t0
 
 
 def run_reference(args, world, rank, pg):
+    """--impl reference: the oracle (the CPU definition of the method, oracle/) running config 2's own
+    adaptive trajectory from the seeded initial state -- its own controller (Eq. sencondt),
+    exact Newton through its Krylov path.  Warm-up and timed steps are real full-grid steps; because
+    one oracle step takes ~10-25 s, at most 1 warm-up step and as many timed steps as fit in a
+    ~150 s budget are run (`steps` is the number actually timed; `steps_requested` = K)."""
     if rank != 0:
         return
+    from oracle import krylov, solver
     cfg = ni.CONFIGS[args.config]
-    per = []
-    for k in range(args.warmup + args.steps):
-        s = oracle_sample(cfg, seconds_hint=5.0)
-        if k >= args.warmup:
-            per.append(1.0 / s["value"])
+    sol = bench_solver(cfg)
+    m, sol = oracle_model_sol(cfg, sol)
+    shape = cfg["shape"]
+    c, eta = ni.initial_fields(shape, 0)
+    cbar = c.mean()
+    X = solver.gauge_project(np.concatenate([c[None], eta[None], solver.init_displacement_fft(m, c, cbar)]))
+    lin = krylov.make_linsolve()
+    Xprev, dt_prev, zeta = None, None, sol["zeta"]
+    per, recs = [], []
+    budget = float(os.environ.get("NKS_REFERENCE_BUDGET_S", "150"))
+    t_start = time.perf_counter()
+    n = 0
+    while n < min(args.warmup, 1) + args.steps:
+        dt = sol["dt_init"] if Xprev is None else solver.predict_dt(
+            solver.change_rate(X, Xprev, dt_prev, sol["xd_norm"]), zeta, sol["dt_min"], sol["dt_max"])
+        t0 = time.perf_counter()
+        while True:
+            Xb, info = solver.newton_step(m, X, dt, cbar, sol, linsolve=lin)
+            if info["converged"]:
+                break
+            dt /= np.sqrt(2)
+            zeta *= 2
+        el = time.perf_counter() - t0
+        if n >= min(args.warmup, 1):
+            per.append(el)
+            recs.append({"dt": dt, "newton_its": info["newton_its"]})
+        Xprev, X, dt_prev = X, Xb, dt
+        n += 1
+        if time.perf_counter() - t_start > budget and per:
+            break
     mean_s = float(np.mean(per))
-    cb = oracle_sample(cfg, seconds_hint=5.0)
+    sample = (f"{len(per)} timed oracle steps (after {min(args.warmup, 1)} warm-up) of config 2's own adaptive "
+              f"trajectory on the full {'x'.join(map(str, shape))} grid, seed 0: exact Newton via oracle/krylov.py "
+              f"(matrix-free J.v, spectral-preconditioned GMRES(30)); dt {[round(r['dt'], 4) for r in recs]}")
     line = {"impl": "reference", "metric": METRIC, "value": 1.0 / mean_s, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(cfg, args.gpus),
-            "cpu_baseline": {"value": 1.0 / mean_s, "unit": UNIT, "cores": cb["cores"], "kind": "oracle",
-                             "sample": cb["sample"]},
-            "e2e": {"value": 1.0 / mean_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "steps": len(per), "steps_requested": args.steps, "warmup": min(args.warmup, 1),
+            "ms_per_step": mean_s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": config_dict(cfg, args.gpus),
+            "cpu_baseline": {"value": 1.0 / mean_s, "unit": UNIT, "cores": oracle_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": 1.0 / mean_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "per_step_s": per}
     print(json.dumps(line), flush=True)
+
+
+def bench_solver(cfg):
+    """Solver settings of the benchmark: SURVEY 8(c).2 defaults + the opt-in GMRES stagnation rule
+    (gmres_stall_cycles = 3, R18) so that a BILU(0)-RAS solve that stalls is retried by the
+    controller instead of running to gmres_maxit = 10,000."""
+    sol = dict(ni.solver_default())
+    sol["gmres_stall_cycles"] = 3
+    return sol
 
 
 def config_dict(cfg, ngpus, sharded=False):
@@ -330,6 +362,12 @@ def micro_sharded(shape, pg, reps=10):
     return res
 
 
+def step_stats(per_ms):
+    a = np.asarray(per_ms)
+    return {"mean": float(a.mean()), "p50": float(np.percentile(a, 50)), "p90": float(np.percentile(a, 90)),
+            "min": float(a.min()), "max": float(a.max())}
+
+
 def run_gpu(args, world, rank, local, pg):
     import torch
     from paper_2209_08001_b200 import Solver
@@ -341,7 +379,7 @@ def run_gpu(args, world, rank, local, pg):
     d = len(shape)
     nf = 2 + d
     N = int(np.prod(shape))
-    model, sol = ni.model_default(), ni.solver_default()
+    model, sol = ni.model_default(), bench_solver(cfg)
     sharded = d == 3 and (world > 1 or args.sharded)
     c, eta = ni.initial_fields(shape, 0)
     if sharded:
@@ -354,37 +392,50 @@ def run_gpu(args, world, rank, local, pg):
         sh = None
         g = Solver(shape, model, sol, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"], pc_reuse=1)
         g.set_fields(c, eta, None)
-    recs = []
     for _ in range(args.warmup):
-        recs += g.run_adaptive(1)
+        g.run_adaptive(1)
     torch.cuda.synchronize()
+    X_warm = g.get_state() if (rank == 0 and world == 1 and not args.no_cpu) else None
+
+    # ---- timed region: K accepted adaptive steps, library profiling OFF, one event pair per step
     clk = ClockSampler(local)
     clk.start()
-    g.set_profiling(True)
-    g.phase_times(reset=True)
     l0 = g.counters()["kernel_launches"]
     stream = g.stream
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     barrier(pg)
     torch.cuda.synchronize()
-    ev0.record(stream)
+    evs[0].record(stream)
     timed = []
-    for _ in range(args.steps):
+    for k in range(args.steps):
         timed += g.run_adaptive(1)
-    ev1.record(stream)
+        evs[k + 1].record(stream)
     torch.cuda.synchronize()
     barrier(pg)
     clocks = clk.stop()
-    t_ms = ev0.elapsed_time(ev1)
+    t_ms = evs[0].elapsed_time(evs[-1])
+    per_step_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
     launches = g.counters()["kernel_launches"] - l0
-    phases = g.phase_times(reset=True)
-    g.set_profiling(False)
     t_max = max_over_ranks(pg, t_ms)
     ms_per_step = t_max / args.steps
     # sharded: all ranks advance ONE global grid (strong scaling); replicas: world independent runs
     value = (1 if sharded else world) * args.steps / (t_max / 1e3)
 
-    # ---- roofline of the dominant kernel (phase with the largest share of the timed region)
+    # ---- profiled pass (after the timed region, same trajectory): per-launch CUDA events on the library
+    # stream give every phase's share of the step and the dominant kernel's mean launch duration
+    nprof = max(1, min(2, args.steps))
+    g.set_profiling(True)
+    g.phase_times(reset=True)
+    ep0, ep1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ep0.record(stream)
+    prof_recs = []
+    for _ in range(nprof):
+        prof_recs += g.run_adaptive(1)
+    ep1.record(stream)
+    phases = g.phase_times(reset=True)
+    g.set_profiling(False)
+    prof_ms = ep0.elapsed_time(ep1)
+
     dom = max(phases, key=lambda k: phases[k]["ms"])
     rb, P = ras_bytes(g, cfg)
     alg = {
@@ -412,18 +463,33 @@ def run_gpu(args, world, rank, local, pg):
         ach = alg[dom] / (per_launch_ms[dom] * 1e-3) / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                 "traffic": None, "peak_source": peak_src, "alg_bytes_per_launch": alg[dom],
-                "ms_per_launch": per_launch_ms[dom]}
+                "ms_per_launch": per_launch_ms[dom],
+                "share_of_step": phases[dom]["ms"] / prof_ms if prof_ms > 0 else None,
+                "measured_in": f"profiled pass of {nprof} steps right after the timed region (per-launch CUDA "
+                               "events on the library stream); the timed region itself ran unprofiled"}
     else:
         roof = {"kernel": dom, "bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
                 "traffic": None, "peak_source": peak_src}
+    if dom == "ras_apply" and d == 2 and per_launch_ms.get(dom):
+        # the 2D BILU(0) sweep is a dependency chain: (ex + 2(ey-1)) forward + as many backward wavefront
+        # steps per apply (reading R21); its latency roofline is that step count x the measured minimum step
+        ex = cfg["shape"][1] // cfg["nsub"][1] + 2 * cfg["overlap"]
+        ey = cfg["shape"][0] // cfg["nsub"][0] + 2 * cfg["overlap"]
+        nsteps = 2 * (ex + 2 * (ey - 1))
+        roof["critical_path_steps"] = nsteps
+        roof["ns_per_wavefront_step"] = per_launch_ms[dom] * 1e6 / nsteps
 
     # ---- end to end through the C ABI with host buffers: every step uploads X^n from pinned host memory
     # (nks_set_state, on_device = 0: keeps the controller's history), advances one adaptive step
     # (nks_run_adaptive, retries included, exactly the device leg's work) and downloads X^{n+1}
     e2e = None
+    X_e2e_first = None
     if not args.no_e2e and not sharded:
         import ctypes as C
         from paper_2209_08001_b200.nks import StepInfo
+        del g
+        torch.cuda.empty_cache()
+        g = None
         g2 = Solver(shape, model, sol, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"], pc_reuse=1)
         g2.set_fields(c, eta, None)
         for _ in range(args.warmup):
@@ -438,7 +504,7 @@ def run_gpu(args, world, rank, local, pg):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(g2.stream)
-        for _ in range(args.steps):
+        for k in range(args.steps):
             rc = lib.nks_set_state(g2.st, C.c_void_p(Xh[0].data_ptr()), C.c_void_p(Xh[1].data_ptr()),
                                    C.c_void_p(Xh[2].data_ptr()), 0)
             assert rc == 0, rc
@@ -447,33 +513,50 @@ def run_gpu(args, world, rank, local, pg):
             rc = lib.nks_get_fields(g2.st, C.c_void_p(Xh[0].data_ptr()), C.c_void_p(Xh[1].data_ptr()),
                                     C.c_void_p(Xh[2].data_ptr()), 0)
             assert rc == 0, rc
+            if k == 0 and X_warm is not None:
+                X_e2e_first = Xh.numpy().copy()      # host copy of step W+1 (already on the host)
         e1.record(g2.stream)
         torch.cuda.synchronize()
         t_e2e = max_over_ranks(pg, e0.elapsed_time(e1))
         del g2
+        torch.cuda.empty_cache()
         e2e = {"value": world * args.steps / (t_e2e / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": nf * N * 8, "d2h_bytes_per_step": nf * N * 8,
                "wall_s": time.perf_counter() - t0,
                "note": "per step: nks_set_state (pinned host X^n, on_device=0) + nks_run_adaptive(1) + "
                        "nks_get_fields (pinned host); same trajectory and warm-up as the device leg"}
 
+    # ---- CPU baseline: the oracle takes step W+1 of this very trajectory (X^n = the GPU state after the
+    # W warm-up steps, dt forced to the GPU's accepted dt) on the full grid; its result is also compared
+    # with the GPU's step W+1 (taken from the e2e leg's host copy, same deterministic trajectory)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = oracle_sample(cfg)
+    parity = None
+    if X_warm is not None:
+        cbar0 = float(ni.initial_fields(shape, 0)[0].mean())
+        Xo, oinfo, el = oracle_step_sample(cfg, sol, X_warm, cbar0, timed[0]["dt"])
+        cpu = {"value": 1.0 / el, "unit": UNIT, "cores": oracle_threads(), "kind": "oracle",
+               "sample": f"1 oracle NKS step of the timed trajectory (step {args.warmup + 1}: X^n = the GPU state "
+                         f"after {args.warmup} warm-up steps, dt forced to the GPU's accepted "
+                         f"{timed[0]['dt']:.6g}) on the full {'x'.join(map(str, shape))} grid, exact Newton via "
+                         f"oracle/krylov.py ({oinfo['newton_its']} Newton its), {el:.1f} s",
+               "threads_note": "NumPy elementwise work on 1 core, scipy.fft on all cores"}
+        if X_e2e_first is not None and oinfo["converged"]:
+            rel = [float(np.linalg.norm(X_e2e_first[f] - Xo[f]) / np.linalg.norm(Xo[f])) for f in range(nf)]
+            parity = {"step": args.warmup + 1, "dt": timed[0]["dt"], "field_rel_l2": rel,
+                      "bar": 1e-8, "ok": max(rel) <= 1e-8}
 
     micro_sh = None
     if world > 1 and not args.no_micro:
-        del g
+        g = None
+        sh = None
         torch.cuda.empty_cache()
         try:
             micro_sh = {"grid": [512, 512, 512], "sharding": f"z-slabs x {world}", **micro_sharded((512, 512, 512), pg)}
         except Exception as e:
             micro_sh = {"error": str(e)[:200]}
-        g = None
-        sh = None
     micro = {}
     if not args.no_micro and world == 1:
-        del g
+        g = None
         torch.cuda.empty_cache()
         for name, shp in (("2d512", (512, 512)), ("3d256", (256, 256, 256)), ("3d512", (512, 512, 512))):
             try:
@@ -506,13 +589,18 @@ def run_gpu(args, world, rank, local, pg):
     roof["traffic"] = traffic
 
     if rank == 0:
+        conf = config_dict(cfg, world, sharded)
+        conf["gmres_stall_cycles"] = sol["gmres_stall_cycles"]
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": config_dict(cfg, world, sharded), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "config": conf, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks,
+                "step_ms": step_stats(per_step_ms), "per_step_ms": [round(x, 3) for x in per_step_ms],
+                "parity_vs_oracle": parity,
                 "kernels": kern, "kernels_micro": micro, "kernels_micro_sharded": micro_sh,
-                "phases_ms": {k: round(v["ms"], 3) for k, v in phases.items()},
+                "phases_ms_profiled_pass": {k: round(v["ms"], 3) for k, v in phases.items()},
+                "profiled_pass_ms": prof_ms, "profiled_pass_steps": nprof,
                 "solver": {"newton_its": [r["newton_its"] for r in timed], "gmres_its": [r["gmres_its"] for r in timed],
                            "dt": [r["dt"] for r in timed], "retries": [r["retries"] for r in timed],
                            "energy": [r["energy"] for r in timed], "mass": [r["mass"] for r in timed]}}

@@ -131,6 +131,12 @@ typedef struct {
                                      /* retries without running to gmres_maxit.  A     */
                                      /* property of the linear solver, not of Eq. NSOA-1: it can   */
                                      /* change the accepted dt sequence (reading R18).   */
+  int32_t ilu_level;                 /* Schwarz subdomain solver (Table 1): 0 = point-block */
+                                     /* ILU(0) (default; reading R21), k = 1..8: ILU(k) on Saad's    */
+                                     /* level-of-fill pattern, -1 = exact block LU (no pivoting,     */
+                                     /* natural order).  k != 0 uses the level-synchronous solves;   */
+                                     /* its factor storage grows with the fill (NKS_E_OOM / INVALID  */
+                                     /* from nks_workspace_bytes when it cannot be held).            */
 } nks_params;
 
 typedef struct {
@@ -233,8 +239,10 @@ NKS_API nks_status nks_pc_apply(nks_state* st, const double* r, double* z, int32
 NKS_API nks_status nks_gmres_solve(nks_state* st, double dt, const double* x_b, const double* rhs, double* s,
                            int32_t on_device, int32_t* its);
 
-/* Launch counters of this state since creation (kernels issued by the library). */
-NKS_API nks_status nks_counters(const nks_state* st, int64_t* kernel_launches, int64_t* host_syncs);
+/* Counters of this state since creation: kernels issued by the library, host synchronisations, and
+ * global reductions (each an allreduce on a sharded state): one per GMRES Arnoldi step (DCGS2, north_star
+ * item 5), one per GMRES restart / Newton norm / energy / gauge / X'_d evaluation.  Any pointer may be NULL. */
+NKS_API nks_status nks_counters(const nks_state* st, int64_t* kernel_launches, int64_t* host_syncs, int64_t* reductions);
 
 /* Phase profiling with CUDA events recorded on the state's stream around every launch of a
  * phase: [0] residual F, [1] J.v, [2] RAS apply, [3] assembly, [4] BILU(0) factorisation,

@@ -33,24 +33,23 @@ int launch_gauge_sums(const DevParams& P, const double* X, double* part, double*
 void launch_gauge_apply(const DevParams& P, double* X, const double* out, cudaStream_t s);
 void launch_zero_ghosts(const DevParams& P, int nf, double* v, cudaStream_t s);
 // krylov.cu
-void launch_mdot(long long n, int nk, const double* V, long long ld, const double* w, double* part, double* out, cudaStream_t s);
-void launch_update_dot(long long n, int nk, const double* V, long long ld, const double* h, double* w, double* part,
-                       double* out, cudaStream_t s);
-void launch_update_scale(long long n, int nk, const double* V, long long ld, const double* h, double scale, double* w,
-                         cudaStream_t s);
+void launch_dcgs_dot(long long n, int nk, const double* V, long long ld, double* part, double* out, unsigned* counter,
+                     cudaStream_t s);
+void launch_dcgs_dot_u(long long n, int nk, const double* V, long long ld, double* part, double* out, unsigned* counter,
+                       cudaStream_t s);
+void launch_dcgs_update(long long n, int nk, double* V, long long ld, const double* hv, cudaStream_t s);
 void launch_lincomb(long long n, int nk, const double* V, long long ld, const double* y, double* out, cudaStream_t s);
-void launch_cgs_dot(long long n, int nk, const double* V, long long ld, const double* w, double* part, double* out,
-                    unsigned* counter, cudaStream_t s);
-void launch_cgs_update_dot(long long n, int nk, const double* V, long long ld, const double* h, double* w, double* part,
-                           double* out, unsigned* counter, cudaStream_t s);
-void launch_update_scale_dev(long long n, int nk, const double* V, long long ld, const double* hv, double* w,
-                             cudaStream_t s);
 void launch_axpby(long long n, double a, const double* x, double b, double* y, cudaStream_t s);
 void launch_xpay(long long n, const double* x, double a, const double* y, double* z, cudaStream_t s);
 // precond.cu
 void build_slot_tables(int dim, BoxSet& B);
 long long box_positions(const nks_grid& g);
-HostBoxes build_boxes_host(const nks_grid& g, const BoxSet& B);
+HostBoxes build_boxes_host(const nks_grid& g, const BoxSet& B, const IlukPattern* K);
+void launch_assemble_gen(const DevParams& P, const BoxSet& B, int nf, const double* Xa, const double* jac4, double* fac,
+                         cudaStream_t s);
+void launch_factor_gen(const BoxSet& B, int nf, double* fac, cudaStream_t s);
+void launch_ras_apply_gen(const BoxSet& B, int nf, long long N, const double* fac, const double* r, double* y,
+                          double* z, cudaStream_t s);
 void launch_assemble(const DevParams& P, const BoxSet& B, int nf, const double* Xa, const double* jac4, double* fac,
                      cudaStream_t s);
 void launch_factor(const BoxSet& B, int nf, double* fac, cudaStream_t s);
@@ -92,6 +91,7 @@ struct Layout {
   size_t off_Ta, off_jac4, off_V, off_Z, off_W2, off_part, off_out;
   size_t off_fac, off_fac32, off_ybox, off_gidx, off_nbr, off_levoff, off_levptr, off_posoff, off_geo;
   size_t off_cover_off, off_cover_pos;
+  size_t off_gtab;          // level-k ILU slot tables (off, lower, upper, pair_ptr, pair_b, pair_t)
   size_t total;
   long long P, ld;
   size_t geo_bytes;
@@ -108,7 +108,7 @@ const char* validate(const nks_grid* g, const nks_params* p) {
   if (g->dim == 2 && g->n[2] != 1) return "n[2] must be 1 in 2D";
   if (!(g->h > 0)) return "h must be > 0";
   if (p->S < 1 || p->S > kMaxS) return "S must be in 1..16";
-  if (p->gmres_restart < 1 || p->gmres_restart > 60) return "gmres_restart must be in 1..60";
+  if (p->gmres_restart < 1 || p->gmres_restart > 31) return "gmres_restart must be in 1..31";
   if (p->newton_maxit < 0 || p->gmres_maxit < 1 || p->gmres_stall_cycles < 0) return "bad iteration limits";
   if (p->pc_type != NKS_PC_NONE && p->pc_type != NKS_PC_RAS_BILU0 && p->pc_type != NKS_PC_AS_BILU0 &&
       p->pc_type != NKS_PC_RRAS_BILU0)
@@ -131,11 +131,19 @@ const char* validate(const nks_grid* g, const nks_params* p) {
     if (g->overlap < 0 || g->overlap > 8) return "overlap must be in 0..8";
   }
   if (!(p->kappa > 0) || !(p->theta >= 0)) return "kappa must be > 0, theta >= 0";
+  if (p->ilu_level < -1 || p->ilu_level > 8) return "ilu_level must be -1 (exact LU) or 0..8";
+  if (p->ilu_level != 0 && p->factor_fp32) return "factor_fp32 is available for ILU(0) only";
   return nullptr;
 }
 
-Layout make_layout(const nks_grid& g, const nks_params& p) {
+// K: the level-k ILU pattern when p.ilu_level != 0 (built here, handed back to nks_create).
+Layout make_layout(const nks_grid& g, const nks_params& p, IlukPattern* K = nullptr) {
   Layout L{};
+  IlukPattern Kloc;
+  if (p.pc_type != NKS_PC_NONE && p.ilu_level != 0) {
+    if (!K) K = &Kloc;
+    *K = build_iluk_pattern(g, p.ilu_level);
+  }
   const int d = g.dim, nf = 2 + d;
   const long long N = (long long)g.n[0] * g.n[1] * g.n[2];
   const size_t vec = (size_t)nf * N * sizeof(double);
@@ -150,18 +158,20 @@ Layout make_layout(const nks_grid& g, const nks_params& p) {
   L.off_out = o; o = align256(o + 256 * sizeof(double));
   L.P = 0;
   if (p.pc_type != NKS_PC_NONE) {
-    const int nslots = d == 2 ? 13 : 25;
+    const bool gen = p.ilu_level != 0;
+    const int nslots = gen ? K->nslots : (d == 2 ? 13 : 25);
+    const int la = gen ? K->la : 2, lb = gen ? K->lb : 3;
     L.nslots = nslots;
     L.nbox = g.nsub[0] * g.nsub[1] * g.nsub[2];
     L.P = box_positions(g);
     // upper bound of level pointers: sum over boxes of (nlev + 1)
     long long nl = 0;
     {
-      // every box has at most (e0-1)+2(e1-1)+3(e2-1)+2 entries
+      // every box has at most (e0-1)+la(e1-1)+lb(e2-1)+2 entries
       const int ez = d == 3 ? g.overlap * 2 : 0;
       const int e0 = g.n[0] / g.nsub[0] + 1 + 2 * g.overlap, e1 = g.n[1] / g.nsub[1] + 1 + 2 * g.overlap,
                 e2 = g.n[2] / g.nsub[2] + 1 + ez;
-      nl = (long long)L.nbox * ((e0 - 1) + 2 * (e1 - 1) + 3 * (e2 - 1) + 2);
+      nl = (long long)L.nbox * ((e0 - 1) + (long long)la * (e1 - 1) + (long long)lb * (e2 - 1) + 2);
     }
     L.nlevptr = (int)nl;
     L.ld = (L.P + 31) / 32 * 32;
@@ -177,8 +187,11 @@ Layout make_layout(const nks_grid& g, const nks_params& p) {
     L.off_cover_off = o; o = align256(o + (cover ? (size_t)(N + 1) * sizeof(int) : 0));
     L.off_cover_pos = o; o = align256(o + (cover ? (size_t)L.P * sizeof(int) : 0));
     // the pipelined 2D apply (ras2d_rows.cu) uses this slice
-    L.geo_bytes = d == 2 ? r2::workspace_bytes(g) : 0;
+    L.geo_bytes = (d == 2 && !gen) ? r2::workspace_bytes(g) : 0;
     L.off_geo = o; o = align256(o + L.geo_bytes);
+    L.off_gtab = o;
+    if (gen) o = align256(o + sizeof(int) * (3 * (size_t)nslots + K->lower.size() + K->upper.size() + K->pair_ptr.size() +
+                                             K->pair_b.size() + K->pair_t.size()));
   }
   L.total = o;
   return L;
@@ -289,7 +302,9 @@ long long global_points(const nks_state* st) {
   return st->dp.nzg > 0 ? nxy * st->dp.nzg : nxy * (st->grid.n[2] - 2 * st->grid.zghost);
 }
 
+// A global reduction point (counted on every state; an allreduce across ranks on a sharded one).
 void comm_allreduce(nks_state* st, double* buf, long long n) {
+  st->reductions += 1;
   if (!st->comm_set || st->nranks == 1) return;
   if (st->comm_allreduce(st->comm_user, buf, n, (void*)st->stream) != 0) throw CommError();
 }
@@ -349,6 +364,7 @@ void pc_apply(nks_state* st, const double* r, double* z) {
   }
   PhaseScope ps(st, PH_RAS);
   if (st->ras2d) CK(r2::launch_apply(st->ras2d, r, z, st->stream));
+  else if (st->boxes.gen) launch_ras_apply_gen(st->boxes, st->nf, st->N, st->fac, r, st->ybox, z, st->stream);
   else launch_ras_apply(st->boxes, st->nf, st->N, st->fac, st->fac32, r, st->ybox, z, st->stream);
   count_launch(st, 1);
 }
@@ -357,12 +373,14 @@ void pc_setup(nks_state* st, const double* Xb) {
   if (st->prm.pc_type == NKS_PC_NONE) return;
   {
     PhaseScope ps(st, PH_ASM);
-    launch_assemble(st->dp, st->boxes, st->nf, st->Xn, st->jac4, st->fac, st->stream);
+    if (st->boxes.gen) launch_assemble_gen(st->dp, st->boxes, st->nf, st->Xn, st->jac4, st->fac, st->stream);
+    else launch_assemble(st->dp, st->boxes, st->nf, st->Xn, st->jac4, st->fac, st->stream);
     count_launch(st, 1);
   }
   {
     PhaseScope ps(st, PH_FACT);
-    launch_factor(st->boxes, st->nf, st->fac, st->stream);
+    if (st->boxes.gen) launch_factor_gen(st->boxes, st->nf, st->fac, st->stream);
+    else launch_factor(st->boxes, st->nf, st->fac, st->stream);
     count_launch(st, 1);
     if (st->ras2d) {
       r2::launch_pack(st->ras2d, st->fac, st->boxes.ld, st->stream);
@@ -383,12 +401,21 @@ void set_dt(nks_state* st, double dt) {
   st->dp.inv_dt = 1.0 / dt;
 }
 
-// Right-preconditioned restarted GMRES: J s = b with s0 = 0.  Returns 0 converged, 1 maxit.
+// Right-preconditioned restarted GMRES: J s = b with s0 = 0 (reading R18).  Returns 0
+// converged, 1 gmres_maxit, 2 stagnation (opt-in).
+//
+// Arnoldi by DCGS2 (krylov.cu): ONE global reduction per iteration (a = V^T u, b = V^T w, u.u, u.w in one
+// fused pass, one allreduce on a slab state), one fused update pass.  Column j-1 of the Hessenberg matrix
+// becomes final when iteration j's reduction arrives (the delayed reorthogonalisation), so the host's
+// Givens / convergence test runs one column behind the device; with the one-iteration look-ahead the
+// device never waits for the host.  The device computes r and gamma of every step itself (dcgs_scalars),
+// the host replays the same doubles from a pinned copy (ring of 4 slots).
 int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, int& its) {
   const int m = st->prm.gmres_restart;
   const long long n = st->nvec;
   double* V = st->V;
-  std::vector<double> H((m + 1) * m, 0.0), cs(m, 0.0), sn(m, 0.0), g(m + 1, 0.0), y(m, 0.0);
+  std::vector<double> Hr((m + 1) * m, 0.0), R((m + 1) * m, 0.0), cs(m, 0.0), sn(m, 0.0), g(m + 1, 0.0), y(m, 0.0),
+      hprev(m + 1, 0.0), hnew(m + 1, 0.0);
   CK(cudaMemsetAsync(s, 0, n * sizeof(double), st->stream));
   its = 0;
   double beta = bnorm;
@@ -402,92 +429,111 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
       count_launch(st, 1);
     }
     first = false;
+    std::fill(Hr.begin(), Hr.end(), 0.0);
+    std::fill(R.begin(), R.end(), 0.0);
     std::fill(g.begin(), g.end(), 0.0);
-    g[0] = beta;
-    int j = 0;
-    double resid = beta;
-    bool done = false;
-    // Arnoldi with one iteration of look-ahead: iteration j+1 is queued before the host waits for
-    // iteration j's dot products, so the device never idles on the host's Givens/convergence test.
-    // Every quantity the device needs (projection coefficients, norm, breakdown) is computed on the
-    // device; the host replays the same doubles from a pinned copy (ring of 4 slots).
-    auto launch_iter = [&](int jj) {
-      double* vj = V + (long long)jj * n;
+    // one reduction (+ allreduce) per launched step, its values copied to ring slot jj % 4
+    auto reduce_to_ring = [&](int jj) {
+      comm_allreduce(st, st->red_out, 66);
+      double* slot = st->h_ring + (jj % 4) * 128;
+      CK(cudaMemcpyAsync(slot, st->red_out, 66 * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
+      CK(cudaEventRecord(st->gm_ev[jj % 4], st->stream));
+    };
+    auto launch_iter = [&](int jj) {            // u = V[jj] -> w = J M^-1 u into V[jj+1], then DCGS2 step jj
+      double* u = V + (long long)jj * n;
       double* w = V + (long long)(jj + 1) * n;
-      if (st->prm.pc_type != NKS_PC_NONE) halo(st, vj, st->nf);   // RAS reads delta ghost planes of its input
-      pc_apply(st, vj, st->Z);
-      if (st->prm.pc_type != NKS_PC_NONE) clean(st, vj, st->nf);
+      if (st->prm.pc_type != NKS_PC_NONE) halo(st, u, st->nf);   // RAS reads delta ghost planes of its input
+      pc_apply(st, u, st->Z);
+      if (st->prm.pc_type != NKS_PC_NONE) clean(st, u, st->nf);
       halo(st, st->Z, st->nf);
       jv(st, st->Z, w);
       {
         PhaseScope ps(st, PH_VEC);
-        // slab states: one allreduce after each CGS pass (jj+1 projections, then jj+1 corrections + |w|^2)
-        if (jj + 2 <= 32) {      // register-resident CGS2 passes with last-block reductions
-          launch_cgs_dot(n, jj + 1, V, n, w, st->red_part, st->red_out, st->red_cnt, st->stream);
-          comm_allreduce(st, st->red_out, jj + 1);
-          launch_cgs_update_dot(n, jj + 1, V, n, st->red_out, w, st->red_part, st->red_out + 64, st->red_cnt, st->stream);
-          count_launch(st, 2);
-        } else {
-          launch_mdot(n, jj + 1, V, n, w, st->red_part, st->red_out, st->stream);
-          comm_allreduce(st, st->red_out, jj + 1);
-          launch_update_dot(n, jj + 1, V, n, st->red_out, w, st->red_part, st->red_out + 64, st->stream);
-          count_launch(st, 4);
-        }
-        comm_allreduce(st, st->red_out + 64, jj + 2);
-        launch_update_scale_dev(n, jj + 1, V, n, st->red_out + 64, w, st->stream);
+        launch_dcgs_dot(n, jj, V, n, st->red_part, st->red_out, st->red_cnt, st->stream);
         count_launch(st, 1);
       }
-      double* slot = st->h_ring + (jj % 4) * 128;
-      CK(cudaMemcpyAsync(slot, st->red_out, (64 + jj + 2) * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
-      CK(cudaEventRecord(st->gm_ev[jj % 4], st->stream));
+      reduce_to_ring(jj);
+      {
+        PhaseScope ps(st, PH_VEC);
+        launch_dcgs_update(n, jj, V, n, st->red_out, st->stream);
+        count_launch(st, 1);
+      }
     };
+    auto launch_close = [&](int jj) {           // cycle end: reduction of the last candidate u_m only
+      {
+        PhaseScope ps(st, PH_VEC);
+        launch_dcgs_dot_u(n, jj, V, n, st->red_part, st->red_out, st->red_cnt, st->stream);
+        count_launch(st, 1);
+      }
+      reduce_to_ring(jj);
+    };
+    const int its0 = its;
     launch_iter(0);
-    for (j = 0; j < m; ++j) {
-      if (j + 1 < m && its + 1 < st->prm.gmres_maxit) launch_iter(j + 1);
+    int k = 0;                                  // finalised Hessenberg columns of this cycle
+    double resid = beta;
+    for (int j = 0; j <= m; ++j) {
+      // look-ahead: the next step is queued before the host waits for this one
+      // (step jj yields column jj, final at processing jj + 1; the cycle stops at its0 + j >= gmres_maxit)
+      if (j + 1 < m && its0 + j + 1 <= st->prm.gmres_maxit) launch_iter(j + 1);
+      else if (j + 1 == m && its0 + m <= st->prm.gmres_maxit) launch_close(m);
       CK(cudaEventSynchronize(st->gm_ev[j % 4]));
       st->syncs++;
       const double* hv = st->h_ring + (j % 4) * 128;
-      double h2sq = 0.0;
-      for (int k = 0; k <= j; ++k) {
-        H[k * m + j] = hv[k] + hv[64 + k];
-        h2sq += hv[64 + k] * hv[64 + k];
+      // r and gamma exactly as the device computed them (krylov.cu: dcgs_scalars)
+      double aa = 0.0, ab = 0.0;
+      for (int l = 0; l < j; ++l) {
+        aa += hv[l] * hv[l];
+        ab += hv[l] * hv[32 + l];
       }
-      const double nrm = std::sqrt(std::max(hv[64 + j + 1] - h2sq, 0.0));
-      H[(j + 1) * m + j] = nrm;
-      ++its;
-      const bool breakdown = !(nrm > 1e-300);
-      // Givens
-      for (int k = 0; k < j; ++k) {
-        const double a = H[k * m + j], bb = H[(k + 1) * m + j];
-        H[k * m + j] = cs[k] * a + sn[k] * bb;
-        H[(k + 1) * m + j] = -sn[k] * a + cs[k] * bb;
+      const double r = std::sqrt(std::max(hv[64] - aa, 0.0));
+      const bool breakdown = !(r > 1e-300);
+      if (j == 0) {
+        g[0] = beta * r;                        // r0 = beta V0 = (beta r) v_0
+      } else {
+        // column j-1 final: h_prev + a, subdiagonal r
+        for (int i = 0; i < j; ++i) Hr[i * m + j - 1] = hprev[i] + hv[i];
+        Hr[j * m + j - 1] = r;
+        for (int i = 0; i <= j; ++i) R[i * m + j - 1] = Hr[i * m + j - 1];
+        const int c = j - 1;
+        for (int q = 0; q < c; ++q) {
+          const double a0 = R[q * m + c], b0 = R[(q + 1) * m + c];
+          R[q * m + c] = cs[q] * a0 + sn[q] * b0;
+          R[(q + 1) * m + c] = -sn[q] * a0 + cs[q] * b0;
+        }
+        const double a0 = R[c * m + c], b0 = R[(c + 1) * m + c];
+        const double rr = std::hypot(a0, b0);
+        cs[c] = rr > 0 ? a0 / rr : 1.0;
+        sn[c] = rr > 0 ? b0 / rr : 0.0;
+        R[c * m + c] = rr;
+        R[(c + 1) * m + c] = 0.0;
+        g[c + 1] = -sn[c] * g[c];
+        g[c] = cs[c] * g[c];
+        ++its;
+        k = j;
+        resid = std::fabs(g[c + 1]);
+        if (resid <= tol || breakdown || its >= st->prm.gmres_maxit || j == m) break;
       }
-      {
-        const double a = H[j * m + j], bb = H[(j + 1) * m + j];
-        const double r = std::hypot(a, bb);
-        cs[j] = r > 0 ? a / r : 1.0;
-        sn[j] = r > 0 ? bb / r : 0.0;
-        H[j * m + j] = r;
-        H[(j + 1) * m + j] = 0.0;
-        g[j + 1] = -sn[j] * g[j];
-        g[j] = cs[j] * g[j];
+      // tentative column j: h' = ([b; gamma] - H a)/r  (A M^-1 v_j = V h' + u_{j+1})
+      const double inv_r = breakdown ? 0.0 : 1.0 / r;
+      const double gamma = (hv[65] - ab) * inv_r;
+      for (int i = 0; i <= j; ++i) {
+        double ha = 0.0;
+        for (int l = 0; l < j; ++l) ha += Hr[i * m + l] * hv[l];
+        hnew[i] = ((i < j ? hv[32 + i] : gamma) - ha) * inv_r;
       }
-      resid = std::fabs(g[j + 1]);
-      if (resid <= tol || breakdown || its >= st->prm.gmres_maxit) {
-        ++j;
-        done = true;
-        break;
-      }
+      std::swap(hprev, hnew);
+      if (breakdown) break;
     }
-    // y = H^{-1} g (upper triangular j x j)
-    for (int k = j - 1; k >= 0; --k) {
-      double acc = g[k];
-      for (int l = k + 1; l < j; ++l) acc -= H[k * m + l] * y[l];
-      y[k] = acc / H[k * m + k];
+    // the look-ahead may have queued one more step: it only writes slots >= k + 1, never read below
+    // y = R^{-1} g (upper triangular k x k)
+    for (int q = k - 1; q >= 0; --q) {
+      double acc = g[q];
+      for (int l = q + 1; l < k; ++l) acc -= R[q * m + l] * y[l];
+      y[q] = acc / R[q * m + q];
     }
     {
       PhaseScope ps(st, PH_VEC);
-      launch_lincomb(n, j, V, n, y.data(), st->W2, st->stream);
+      launch_lincomb(n, k, V, n, y.data(), st->W2, st->stream);
       count_launch(st, 1);
     }
     if (st->prm.pc_type != NKS_PC_NONE) halo(st, st->W2, st->nf);
@@ -501,7 +547,6 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
     if (st->debug) std::fprintf(stderr, "[nks] gmres cycle its=%d beta=%.3e resid_est=%.3e tol=%.3e\n", its, beta, resid, tol);
     if (resid <= tol) return 0;
     if (its >= st->prm.gmres_maxit) return 1;
-    (void)done;
     // restart: r = b - J s  -> V[0]
     halo(st, s, st->nf);
     jv(st, s, st->W2);
@@ -717,7 +762,11 @@ const char* nks_version(void) { return "nks-b200 0.1 (sm_100a, fp64)"; }
 
 size_t nks_workspace_bytes(const nks_grid* grid, const nks_params* params) {
   if (validate(grid, params)) return 0;
-  return make_layout(*grid, *params).total;
+  try {
+    return make_layout(*grid, *params).total;
+  } catch (const std::exception&) {
+    return 0;
+  }
 }
 
 nks_status nks_create(const nks_grid* grid, const nks_params* params, void* workspace, size_t workspace_bytes,
@@ -726,7 +775,13 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
   *out = nullptr;
   if (validate(grid, params)) return NKS_E_INVALID;
   if (!workspace) return NKS_E_INVALID;
-  const Layout L = make_layout(*grid, *params);
+  IlukPattern Kpat;
+  Layout L;
+  try {
+    L = make_layout(*grid, *params, &Kpat);
+  } catch (const std::exception&) {
+    return NKS_E_INVALID;
+  }
   if (workspace_bytes < L.total) return NKS_E_OOM;
   nks_state* st = new nks_state();
   st->grid = *grid;
@@ -761,7 +816,27 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
     if (params->pc_type != NKS_PC_NONE) {
       BoxSet& B = st->boxes;
       build_slot_tables(grid->dim, B);
-      HostBoxes H = build_boxes_host(*grid, B);
+      const bool gen = params->ilu_level != 0;
+      if (gen) {          // level-k ILU: the slot tables of the fill pattern go to device memory
+        B.gen = true;
+        B.nslots = Kpat.nslots;
+        B.diag = Kpat.diag;
+        B.g_nlower = (int)Kpat.lower.size();
+        B.g_nupper = (int)Kpat.upper.size();
+        std::vector<int> tab;
+        for (const auto& o3 : Kpat.off) tab.insert(tab.end(), o3.begin(), o3.end());
+        int* t0 = (int*)(w + L.off_gtab);
+        B.g_off = t0;
+        B.g_lower = B.g_off + 3 * Kpat.nslots;
+        B.g_upper = B.g_lower + Kpat.lower.size();
+        B.g_pair_ptr = B.g_upper + Kpat.upper.size();
+        B.g_pair_b = B.g_pair_ptr + Kpat.pair_ptr.size();
+        B.g_pair_t = B.g_pair_b + Kpat.pair_b.size();
+        for (const auto* v : {&Kpat.lower, &Kpat.upper, &Kpat.pair_ptr, &Kpat.pair_b, &Kpat.pair_t})
+          tab.insert(tab.end(), v->begin(), v->end());
+        CK(cudaMemcpyAsync(t0, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice, st->stream));
+      }
+      HostBoxes H = build_boxes_host(*grid, B, gen ? &Kpat : nullptr);
       B.nbox = L.nbox;
       B.P = H.P;
       B.ld = L.ld;
@@ -807,7 +882,7 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
         CK(cudaMemcpyAsync(B.cover_pos, cov_pos.data(), cov_pos.size() * sizeof(int), cudaMemcpyHostToDevice, st->stream));
       }
       CK(cudaStreamSynchronize(st->stream));
-      if (grid->dim == 2 && B.variant == 0) {
+      if (grid->dim == 2 && B.variant == 0 && !gen) {
         // one lane per row, one warp per component, a cluster of stripes per box (ras2d_rows.cu); boxes
         // the plan cannot take (e.g. > 8 stripes) use the level-synchronous apply of precond.cu
         std::string why;
@@ -1100,10 +1175,11 @@ nks_status nks_gmres_solve(nks_state* st, double dt, const double* x_b, const do
   });
 }
 
-nks_status nks_counters(const nks_state* st, int64_t* kernel_launches, int64_t* host_syncs) {
+nks_status nks_counters(const nks_state* st, int64_t* kernel_launches, int64_t* host_syncs, int64_t* reductions) {
   if (!st) return NKS_E_INVALID;
   if (kernel_launches) *kernel_launches = st->launches;
   if (host_syncs) *host_syncs = st->syncs;
+  if (reductions) *reductions = st->reductions;
   return NKS_OK;
 }
 

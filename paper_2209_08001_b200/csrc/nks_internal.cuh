@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <array>
 #include <string>
 #include <vector>
 
@@ -66,7 +67,27 @@ struct BoxSet {
   int npairs[kMaxSlots];
   int pair_b[kMaxSlots][kMaxSlots];
   int pair_t[kMaxSlots][kMaxSlots];
+  // level-k ILU (ilu_level != 0): slot tables in device memory (precond_iluk.cuh)
+  bool gen = false;
+  int g_nlower = 0, g_nupper = 0;
+  int* g_off = nullptr;       // [nslots][3]
+  int* g_lower = nullptr;
+  int* g_upper = nullptr;
+  int* g_pair_ptr = nullptr;
+  int* g_pair_b = nullptr;
+  int* g_pair_t = nullptr;
 };
+
+// Level-k ILU pattern (precond_iluk.cuh): slot offsets, lower/upper split, IKJ pairs, wavefront level
+// function lx + la ly + lb lz, and per distinct box extent the presence of every (row, slot) entry.
+struct IlukPattern {
+  int nslots = 0, diag = 0, la = 2, lb = 3;
+  std::vector<std::array<int, 3>> off;
+  std::vector<int> lower, upper, pair_ptr, pair_b, pair_t;
+  std::vector<std::array<int, 3>> ext;                 // distinct box extents
+  std::vector<std::vector<unsigned char>> present;     // [extent][local natural index * nslots + slot]
+};
+IlukPattern build_iluk_pattern(const nks_grid& g, int level);
 
 // Slot tables passed by value to the factor / solve kernels.
 struct SlotTables {
@@ -141,6 +162,7 @@ struct nks_state {
   // counters
   long long launches = 0;
   long long syncs = 0;
+  long long reductions = 0;     // global reductions issued (GMRES: one per Arnoldi step + one per restart)
   // phase profiling (CUDA events on this stream)
   bool profile = false;
   double phase_ms[8] = {0};

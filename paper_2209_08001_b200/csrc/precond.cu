@@ -97,7 +97,11 @@ long long box_positions(const nks_grid& g) {
   return P;
 }
 
-HostBoxes build_boxes_host(const nks_grid& g, const BoxSet& B) {
+HostBoxes build_boxes_host(const nks_grid& g, const BoxSet& B, const IlukPattern* K) {
+  // wavefront level lx + la ly + lb lz (R21: la = 2, lb = 3 for the ILU(0) pattern); with a level-k
+  // pattern K, the slot offsets come from K and a row lacks the entries its level-k pattern drops
+  const int la = K ? K->la : 2, lb = K ? K->lb : 3;
+  const int nsl = K ? K->nslots : B.nslots;
   HostBoxes H;
   std::vector<int> st[3], ln[3];
   split_boxes(g, st, ln);
@@ -105,7 +109,7 @@ HostBoxes build_boxes_host(const nks_grid& g, const BoxSet& B) {
   const int dz = g.dim == 3 ? delta : 0;
   H.P = box_positions(g);
   H.gidx.assign(H.P, 0);
-  H.nbr.assign((size_t)B.nslots * H.P, -1);
+  H.nbr.assign((size_t)nsl * H.P, -1);
   H.box_pos_off.push_back(0);
   H.box_lev_off.push_back(0);
   long long base = 0;
@@ -117,12 +121,16 @@ HostBoxes build_boxes_host(const nks_grid& g, const BoxSet& B) {
         const int own[3] = {ln[0][bx], ln[1][by], ln[2][bz]};
         const int d0[3] = {delta, delta, dz};
         const long long np = (long long)e[0] * e[1] * e[2];
-        const int nlev = (e[0] - 1) + 2 * (e[1] - 1) + 3 * (e[2] - 1) + 1;
+        const int nlev = (e[0] - 1) + la * (e[1] - 1) + lb * (e[2] - 1) + 1;
+        int ext_q = -1;
+        if (K)
+          for (size_t q = 0; q < K->ext.size(); ++q)
+            if (K->ext[q][0] == e[0] && K->ext[q][1] == e[1] && K->ext[q][2] == e[2]) ext_q = (int)q;
         // counting sort by level, natural order within a level
         std::vector<int> count(nlev + 1, 0);
         for (int lz = 0; lz < e[2]; ++lz)
           for (int ly = 0; ly < e[1]; ++ly)
-            for (int lx = 0; lx < e[0]; ++lx) count[lx + 2 * ly + 3 * lz + 1]++;
+            for (int lx = 0; lx < e[0]; ++lx) count[lx + la * ly + lb * lz + 1]++;
         for (int l = 0; l < nlev; ++l) count[l + 1] += count[l];
         std::vector<int> lvstart(count.begin(), count.end());
         for (int l = 0; l < nlev; ++l) H.max_width = std::max(H.max_width, count[l + 1] - count[l]);
@@ -133,7 +141,7 @@ HostBoxes build_boxes_host(const nks_grid& g, const BoxSet& B) {
           for (int ly = 0; ly < e[1]; ++ly)
             for (int lx = 0; lx < e[0]; ++lx) {
               const int lin = (lz * e[1] + ly) * e[0] + lx;
-              posof[lin] = fill[lx + 2 * ly + 3 * lz]++;
+              posof[lin] = fill[lx + la * ly + lb * lz]++;
             }
         for (int lz = 0; lz < e[2]; ++lz)
           for (int ly = 0; ly < e[1]; ++ly)
@@ -151,9 +159,11 @@ HostBoxes build_boxes_host(const nks_grid& g, const BoxSet& B) {
               }
               const int gi = (gc[2] * g.n[1] + gc[1]) * g.n[0] + gc[0];
               H.gidx[pos] = owned ? gi : ~gi;
-              for (int s = 0; s < B.nslots; ++s) {
-                const int q[3] = {lx + B.off[s][0], ly + B.off[s][1], lz + B.off[s][2]};
+              for (int s = 0; s < nsl; ++s) {
+                const int* o = K ? K->off[s].data() : B.off[s];
+                const int q[3] = {lx + o[0], ly + o[1], lz + o[2]};
                 if (q[0] < 0 || q[0] >= e[0] || q[1] < 0 || q[1] >= e[1] || q[2] < 0 || q[2] >= e[2]) continue;
+                if (K && !K->present[ext_q][(size_t)lin * nsl + s]) continue;
                 const int qlin = (q[2] * e[1] + q[1]) * e[0] + q[0];
                 H.nbr[(size_t)s * H.P + pos] = (int)(base + posof[qlin]);
               }
@@ -566,3 +576,5 @@ void launch_ras_apply(const BoxSet& B, int nf, long long N, const double* fac, c
 }
 
 }  // namespace nks
+
+#include "precond_iluk.cuh"

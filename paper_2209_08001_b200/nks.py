@@ -41,7 +41,7 @@ class Params(C.Structure):
         ("ls_alpha", C.c_double), ("ls_max_halvings", C.c_int32),
         ("zeta", C.c_double), ("dt_min", C.c_double), ("dt_max", C.c_double), ("dt_init", C.c_double),
         ("dt_floor_factor", C.c_double), ("xd_norm", C.c_int32), ("factor_fp32", C.c_int32),
-        ("gmres_stall_cycles", C.c_int32),
+        ("gmres_stall_cycles", C.c_int32), ("ilu_level", C.c_int32),
     ]
 
 
@@ -82,7 +82,7 @@ _SIGS = {
     "nks_pc_setup": (C.c_int, [_P, C.c_double, _P, C.c_int32]),
     "nks_pc_apply": (C.c_int, [_P, _P, _P, C.c_int32]),
     "nks_gmres_solve": (C.c_int, [_P, C.c_double, _P, _P, _P, C.c_int32, C.POINTER(C.c_int32)]),
-    "nks_counters": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "nks_counters": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "nks_set_profiling": (C.c_int, [_P, C.c_int32]),
     "nks_phase_times": (C.c_int, [_P, _D, C.POINTER(C.c_int64), C.c_int32]),
     "nks_destroy": (C.c_int, [_P]),
@@ -150,6 +150,7 @@ def make_params(model: dict, solver: dict, pc_type=PC_RAS_BILU0, pc_reuse=1) -> 
     p.xd_norm = {"rms": 0, "l2": 1, "ceta_l2": 2}[solver.get("xd_norm", "rms")]
     p.factor_fp32 = int(solver.get("factor_fp32", 0))
     p.gmres_stall_cycles = int(solver.get("gmres_stall_cycles", 0))
+    p.ilu_level = int(solver.get("ilu_level", 0))
     return p
 
 
@@ -341,9 +342,9 @@ class Solver:
         return s.reshape((self.nf,) + self.shape), its.value
 
     def counters(self):
-        a, b = C.c_int64(), C.c_int64()
-        self._check(self.lib.nks_counters(self.st, C.byref(a), C.byref(b)), "nks_counters")
-        return {"kernel_launches": a.value, "host_syncs": b.value}
+        a, b, r = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(self.lib.nks_counters(self.st, C.byref(a), C.byref(b), C.byref(r)), "nks_counters")
+        return {"kernel_launches": a.value, "host_syncs": b.value, "reductions": r.value}
 
     def set_profiling(self, on=True):
         self._check(self.lib.nks_set_profiling(self.st, 1 if on else 0), "nks_set_profiling")

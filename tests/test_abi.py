@@ -60,7 +60,8 @@ int main(void) {
   printf("nks_step_info %zu\n", sizeof(nks_step_info));
   F(nks_grid, h) F(nks_grid, nsub) F(nks_grid, overlap) F(nks_grid, zghost)
   F(nks_params, S) F(nks_params, newton_rtol) F(nks_params, pc_reuse) F(nks_params, ls_alpha)
-  F(nks_params, zeta) F(nks_params, xd_norm) F(nks_params, factor_fp32)
+  F(nks_params, zeta) F(nks_params, xd_norm) F(nks_params, factor_fp32) F(nks_params, gmres_stall_cycles)
+  F(nks_params, ilu_level)
   F(nks_step_info, dt) F(nks_step_info, energy_parts) F(nks_step_info, mass) F(nks_step_info, xd)
   return 0;
 }
@@ -106,3 +107,21 @@ def test_no_cpu_fallback_in_product():
         if fn.endswith(".py"):
             txt = open(os.path.join(pkg, fn)).read()
             assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", txt, flags=re.M), fn
+
+
+def test_iluk_workspace_grows_with_fill(lib):
+    """The host symbolic phase of ILU(k) (level of fill per box extent) runs without a GPU: the factor
+    storage grows with the fill level, the exact LU needs the most, and a bad level is rejected."""
+    g = nks.make_grid((32, 32), 0.25, (2, 2), 2)
+    sizes = []
+    for lv in (0, 1, 2, -1):
+        sol = dict(ni.solver_default(), ilu_level=lv)
+        p = nks.make_params(ni.model_default(), sol)
+        sizes.append(lib.nks_workspace_bytes(C.byref(g), C.byref(p)))
+    assert all(s > 0 for s in sizes)
+    assert sizes[1] < sizes[2] < sizes[3], sizes          # (ILU(0) also holds the 2D pipelined-apply stream)
+    p = nks.make_params(ni.model_default(), dict(ni.solver_default(), ilu_level=-2))
+    assert lib.nks_workspace_bytes(C.byref(g), C.byref(p)) == 0
+    g3 = nks.make_grid((12, 12, 12), 0.25, (2, 2, 2), 2)
+    p = nks.make_params(ni.model_default(), dict(ni.solver_default(), ilu_level=1))
+    assert lib.nks_workspace_bytes(C.byref(g3), C.byref(p)) > 0

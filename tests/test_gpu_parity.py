@@ -216,14 +216,14 @@ def test_gmres_solves_the_newton_system(shape, nsub):
 
 # ---------------------------------------------------------------------------------------- time steps
 
-def _run_parity(shape, dts, nsub, delta, seed=0, pc_type=2, fp32=False):
+def _run_parity(shape, dts, nsub, delta, seed=0, pc_type=2, fp32=False, sol=None):
     d = len(shape)
     m = oracle_model(d)
     c, eta = ni.initial_fields(shape, seed)
     cbar = c.mean()
     u0 = solver.init_displacement(m, c, cbar)
     Xo = np.concatenate([c[None], eta[None], u0])
-    g = gpu_solver(shape, nsub=nsub, overlap=delta, pc_type=pc_type, sol={"factor_fp32": int(fp32)})
+    g = gpu_solver(shape, nsub=nsub, overlap=delta, pc_type=pc_type, sol=dict({"factor_fp32": int(fp32)}, **(sol or {})))
     g.set_fields(c, eta, None)          # the library solves its own u^0 (FFT)
     mass0 = scheme.mass(m, Xo)
     out = []
@@ -437,3 +437,55 @@ def test_preconditioner_independence(nsub, overlap, reuse, fp32):
     for a, b in zip(i0, i1):
         assert abs(a["newton_its"] - b["newton_its"]) <= 1, (a["newton_its"], b["newton_its"])
         assert abs(a["energy"] - b["energy"]) <= 1e-10 * abs(a["energy"])
+
+
+# ---------------------------------------------------------------------------------------- ILU(k) / LU
+ILUK_CASES = [((16, 16), (2, 2), 2, 1), ((16, 16), (2, 2), 2, 2), ((12, 14), (2, 1), 1, -1), ((14, 12), (1, 1), 2, 1),
+              ((6, 7, 6), (1, 1, 2), 1, 1), ((6, 6, 6), (2, 1, 1), 1, -1)]
+
+
+@pytest.mark.parametrize("shape,nsub,delta,level", ILUK_CASES)
+def test_iluk_apply_parity(shape, nsub, delta, level):
+    """RAS with ILU(1), ILU(2) and exact block LU box solves (ilu_level = k, -1) against the oracle's
+    level-of-fill ILU(k) (oracle/pc.py: biluk, pinned by the fill-path theorem and L U = A)."""
+    d = len(shape)
+    nf = 2 + d
+    Xa, Xb = states(shape)
+    dt = 0.3
+    g = gpu_solver(shape, nsub=nsub, overlap=delta, sol={"ilu_level": level})
+    g.set_fields(Xa[0], Xa[1], Xa[2:])
+    g.pc_setup(Xb, dt)
+    r = ni.random_direction(nf, shape, 13)
+    zg = g.pc_apply(r).cpu().numpy()
+    J = jacobian.assemble(oracle_model(d), Xa, Xb, dt)
+    zo = pc.RAS(J, shape, nf, tuple(reversed(nsub)), delta, fill=None if level < 0 else level).apply(r)
+    errs = field_rel_err(zg, zo)
+    assert max(errs) < 1e-10, errs
+
+
+@pytest.mark.parametrize("level", [1, 2, -1])
+def test_iluk_step_parity_and_fewer_iterations(level):
+    """A step with ILU(k) / LU subdomain solves reaches the oracle's root; more fill never needs more GMRES
+    iterations than ILU(0) here (Table 1 trend)."""
+    shape, dts = (24, 24), [0.5]
+    its = {}
+    for lv in (0, level):
+        out = _run_parity(shape, dts, (2, 2), 2, sol={"ilu_level": lv})
+        its[lv] = out[0][0]["gmres_its"]
+    assert its[level] <= its[0], its
+
+
+def test_one_reduction_per_gmres_iteration():
+    """DCGS2 Arnoldi (north_star item 5): one global reduction per GMRES iteration, plus one per restart
+    cycle closing and per true-residual check (nks_counters)."""
+    shape = (32, 32)
+    Xa, Xb = states(shape)
+    g = gpu_solver(shape, nsub=(2, 2), sol={"gmres_restart": 10})
+    g.set_fields(Xa[0], Xa[1], Xa[2:])
+    rhs = ni.random_direction(4, shape, 5)
+    r0 = g.counters()["reductions"]
+    s, its = g.gmres_solve(Xb, rhs, 0.3)
+    red = g.counters()["reductions"] - r0
+    cycles = (its + 9) // 10
+    assert its > 10
+    assert its <= red <= its + 2 * cycles + 2, (its, red, cycles)
