@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-micro", action="store_true")
+    ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="3D configs: run the z-slab sharded NKS step (ShardedSolver, NCCL halos/allreduces); "
                          "implied for 3D configs at N > 1")
@@ -368,9 +369,41 @@ def step_stats(per_ms):
             "min": float(a.min()), "max": float(a.max())}
 
 
-def run_gpu(args, world, rank, local, pg):
+def run_variant(args, cfg, model, sol, c, eta, pg, pc_type):
+    """W warm-up + K timed adaptive steps of config 2's workload with another preconditioner."""
     import torch
     from paper_2209_08001_b200 import Solver
+    g = Solver(cfg["shape"], model, sol, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"], pc_type=pc_type,
+               pc_reuse=1)
+    g.set_fields(c, eta, None)
+    for _ in range(args.warmup):
+        g.run_adaptive(1)
+    torch.cuda.synchronize()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    barrier(pg)
+    torch.cuda.synchronize()
+    evs[0].record(g.stream)
+    recs = []
+    for k in range(args.steps):
+        recs += g.run_adaptive(1)
+        evs[k + 1].record(g.stream)
+    torch.cuda.synchronize()
+    t_ms = max_over_ranks(pg, evs[0].elapsed_time(evs[-1]))
+    per = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
+    out = {"pc": {5: "spectral (cuFFT, mean-coefficient inverse per wave number)"}.get(pc_type, pc_type),
+           "value": args.steps / (t_ms / 1e3), "unit": UNIT, "ms_per_step": t_ms / args.steps, "step_ms": step_stats(per),
+           "newton_its": [r["newton_its"] for r in recs], "gmres_its": [r["gmres_its"] for r in recs],
+           "dt": [r["dt"] for r in recs], "retries": [r["retries"] for r in recs],
+           "time_simulated": recs[-1]["time"] if recs else None,
+           "note": "same grid, model, controller and tolerances as the headline; its own adaptive trajectory"}
+    del g
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_gpu(args, world, rank, local, pg):
+    import torch
+    from paper_2209_08001_b200 import PC_SPECTRAL, Solver
     from paper_2209_08001_b200.build import build
     build()
     torch.cuda.set_device(local)
@@ -478,6 +511,12 @@ def run_gpu(args, world, rank, local, pg):
         nsteps = 2 * (ex + 2 * (ey - 1))
         roof["critical_path_steps"] = nsteps
         roof["ns_per_wavefront_step"] = per_launch_ms[dom] * 1e6 / nsteps
+
+    # ---- the same workload with the B200-native spectral preconditioner (not the configured one-level RAS;
+    # DESIGN.md section 9): its own adaptive trajectory from the same seeded state, W + K steps
+    variants = {}
+    if not sharded and not args.no_variants:
+        variants["spectral_pc"] = run_variant(args, cfg, model, sol, c, eta, pg, PC_SPECTRAL)
 
     # ---- end to end through the C ABI with host buffers: every step uploads X^n from pinned host memory
     # (nks_set_state, on_device = 0: keeps the controller's history), advances one adaptive step
@@ -597,7 +636,7 @@ def run_gpu(args, world, rank, local, pg):
                 "config": conf, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks,
                 "step_ms": step_stats(per_step_ms), "per_step_ms": [round(x, 3) for x in per_step_ms],
-                "parity_vs_oracle": parity,
+                "parity_vs_oracle": parity, "variants": variants,
                 "kernels": kern, "kernels_micro": micro, "kernels_micro_sharded": micro_sh,
                 "phases_ms_profiled_pass": {k: round(v["ms"], 3) for k, v in phases.items()},
                 "profiled_pass_ms": prof_ms, "profiled_pass_steps": nprof,

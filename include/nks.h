@@ -46,7 +46,7 @@ typedef enum {
   NKS_E_DOMAIN = 2,    /* state inadmissible: c, p = c*eta or q = c*(4-3*eta) not in (0,1), NaN */
   NKS_E_DIVERGED = 3,  /* Newton max-its, line-search failure or GMRES max-its (reading R24)     */
   NKS_E_CUDA = 4,      /* CUDA / cuFFT runtime error (message in nks_last_error)                */
-  NKS_E_NCCL = 5,      /* reserved for the multi-GPU communicator                               */
+  NKS_E_NCCL = 5,      /* NCCL (library-owned communicator) or a communication callback failed */
   NKS_E_OOM = 6,       /* workspace too small                                                   */
   NKS_E_STATE = 7      /* call order violated (e.g. nks_step before nks_set_fields)            */
 } nks_status;
@@ -63,7 +63,12 @@ enum { NKS_REASON_NONE = 0, NKS_REASON_NEWTON_MAXIT = 1, NKS_REASON_LINE_SEARCH 
  * AS and RRAS sum the overlapping boxes' contributions in a fixed box order (deterministic); they are
  * single-state only (a z-slab state would need a reverse halo exchange) and use the level-synchronous
  * subdomain solve. */
-enum { NKS_PC_NONE = 0, NKS_PC_RAS_BILU0 = 2, NKS_PC_AS_BILU0 = 3, NKS_PC_RRAS_BILU0 = 4 };
+enum { NKS_PC_NONE = 0, NKS_PC_RAS_BILU0 = 2, NKS_PC_AS_BILU0 = 3, NKS_PC_RRAS_BILU0 = 4, NKS_PC_SPECTRAL = 5 };
+/* NKS_PC_SPECTRAL (not the paper's): the inverse of J with its variable coefficients
+ * (the pointwise partials of G1 + G2S, the level-n mobility) replaced by their grid means, applied per
+ * wave number with cuFFT -- exact for a uniform state, so GMRES needs few iterations while the fields are
+ * near-uniform.  Periodic single-GPU states only.  Like every preconditioner it changes GMRES's iteration
+ * count, never the converged step. */
 
 typedef struct {
   int32_t dim;       /* 2 or 3                                                          */
@@ -78,6 +83,9 @@ typedef struct {
                      /* J.v, energy and the gauge sums cover the own planes only, with no z wrap.  */
                      /* With pc_type RAS the nsub[2] boxes split the OWN planes (the caller aligns */
                      /* slabs with the global box grid) and zghost >= overlap + 1.                 */
+                     /* nks_decompose() fills a rank's slab grid from the global one.              */
+  int32_t z_offset;  /* zghost > 0: global z of this slab's first own plane                      */
+  int32_t nz_global; /* zghost > 0: planes of the global periodic grid                            */
 } nks_grid;
 
 /* ---- communication callbacks of a z-sharded state --------------------------------
@@ -163,13 +171,36 @@ typedef struct nks_state nks_state;
 /* Bytes of device workspace nks_create needs for this grid/params (0 on invalid input). */
 NKS_API size_t nks_workspace_bytes(const nks_grid* grid, const nks_params* params);
 
-/* Create a single-GPU state on the current CUDA device.
+/* NCCL unique id for a sharded run: rank 0 calls this and sends the 128 bytes to every rank
+ * (e.g. a torch.distributed broadcast); each rank then passes them to nks_create.  NKS_E_NCCL on failure. */
+NKS_API nks_status nks_get_unique_id(uint8_t id[128]);
+
+/* The z-slab of `rank` out of `nranks` for a GLOBAL periodic 3D grid (zghost = 0) -- host only, no GPU.
+ * Each rank owns a contiguous run of whole layers of the global RAS box grid (nsub[2] layers dealt out, the
+ * first nsub[2] mod nranks ranks one more; without RAS the planes themselves), so the preconditioner and the
+ * iteration counts do not depend on the number of ranks.  *local receives the slab grid:
+ * own planes + zghost = max(2, overlap + 1) ghost planes per side (2 without RAS), nsub[2] = its box layers,
+ * z_offset / nz_global set.  NKS_E_INVALID if the grid is not 3D, has fewer box layers than ranks, or a slab
+ * would own fewer than 2 planes. */
+NKS_API nks_status nks_decompose(const nks_grid* global, const nks_params* params, int32_t rank, int32_t nranks,
+                                 nks_grid* local);
+
+/* Create a state on the current CUDA device.
+ *   grid: the whole periodic grid (zghost = 0; then rank = 0, nranks = 1), or this rank's z-slab from
+ *         nks_decompose (zghost > 0).
+ *   rank, nranks: this process's place in the sharded run (1 <= nranks <= 64).
+ *   nccl_id: slab states only -- the 128-byte id of nks_get_unique_id (the same on every rank): the library
+ *         creates and owns an NCCL communicator (ncclCommInitRank: collective, every rank must call
+ *         nks_create), exchanges halos with grouped ncclSend/ncclRecv and reduces with ncclAllGather + a
+ *         rank-ordered sum on its stream.  NULL: the caller attaches host callbacks with nks_set_comm
+ *         (e.g. host-staged exchanges of emulated ranks).  Ignored for whole-grid states.
  *   workspace: device buffer of >= nks_workspace_bytes() bytes, 256-byte aligned, caller-owned
  *              (PyTorch allocates it); must outlive the state.
- *   cuda_stream: cudaStream_t on which every kernel of this state is launched (NULL = legacy).
- * Errors: NKS_E_INVALID (grid/params), NKS_E_OOM (workspace too small), NKS_E_CUDA. */
-NKS_API nks_status nks_create(const nks_grid* grid, const nks_params* params, void* workspace,
-                      size_t workspace_bytes, void* cuda_stream, nks_state** out);
+ *   cuda_stream: cudaStream_t on which every kernel and NCCL call of this state is issued (NULL = legacy).
+ * Errors: NKS_E_INVALID (grid/params/rank), NKS_E_OOM (workspace too small), NKS_E_NCCL, NKS_E_CUDA. */
+NKS_API nks_status nks_create(const nks_grid* grid, const nks_params* params, int32_t rank, int32_t nranks,
+                              const uint8_t* nccl_id, void* workspace, size_t workspace_bytes, void* cuda_stream,
+                              nks_state** out);
 
 /* Set X^n.  c, eta: N doubles each; u: d*N doubles (u_1 block first) or NULL, in which case
  * u^0 solves the discrete mechanical equilibrium [D^ sigma^el]^0 = 0 (reading R13)
@@ -190,16 +221,14 @@ NKS_API nks_status nks_set_state(nks_state* st, const double* c, const double* e
  * whose local mean is not the grid's.  Recomputes T^n. */
 NKS_API nks_status nks_set_cbar0(nks_state* st, double cbar0);
 
-/* Attach a z-sharded state (grid.zghost > 0) to its process group: this rank owns global planes
- * [z_offset, z_offset + n[2] - 2*zghost) of an nz_global-plane periodic grid.  allreduce may be NULL
- * only when nranks == 1; halo must not be NULL.  Call before nks_set_fields; required by
- * nks_set_fields / nks_set_state / nks_step / nks_run_adaptive / nks_energy on slab states
- * (NKS_E_STATE otherwise).  Every rank must make the same sequence of calls: all control decisions
- * (Newton and GMRES convergence, line search, dt) are taken from allreduced values.  On a slab state
- * nks_set_fields takes local arrays including ghost planes (ghost values are ignored) and needs u
- * (the FFT initial displacement is a single-grid operation); cbar0 is the global mean of c. */
-NKS_API nks_status nks_set_comm(nks_state* st, int32_t rank, int32_t nranks, int32_t z_offset, int32_t nz_global,
-                                nks_allreduce_fn allreduce, nks_halo_fn halo, void* user);
+/* Attach host communication callbacks to a z-slab state created without an NCCL id (the callback backend;
+ * a state that owns an NCCL communicator returns NKS_E_STATE).  allreduce may be NULL only when nranks == 1;
+ * halo must not be NULL.  A slab state needs its communication (NCCL or callbacks) before nks_set_fields /
+ * nks_set_state / nks_step / nks_run_adaptive / nks_energy (NKS_E_STATE otherwise).  Every rank must make the
+ * same sequence of calls: all control decisions (Newton and GMRES convergence, line search, dt) are taken
+ * from reduced values that are bitwise identical on every rank.  On a slab state nks_set_fields takes local
+ * arrays including ghost planes (ghost values are ignored) and needs u; cbar0 is the global mean of c. */
+NKS_API nks_status nks_set_comm(nks_state* st, nks_allreduce_fn allreduce, nks_halo_fn halo, void* user);
 
 /* Copy X^n out (same layout as nks_set_fields; u must hold d*N doubles). */
 NKS_API nks_status nks_get_fields(const nks_state* st, double* c, double* eta, double* u, int32_t on_device);

@@ -28,6 +28,13 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-Xcompiler", "-fvisibility=hidden"]
 
 
+def _nccl():
+    """NCCL of the PyTorch wheel (the library torch.distributed loads, so one NCCL lives in the process)."""
+    import nvidia.nccl
+    base = list(nvidia.nccl.__path__)[0]
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
 def _sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -53,7 +60,7 @@ def build(force: bool = False, verbose: bool = False, ptxas: bool = False) -> st
 
     def compile_one(src):
         obj = os.path.join(BUILDDIR, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", _nccl()[0], "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
@@ -63,7 +70,9 @@ def build(force: bool = False, verbose: bool = False, ptxas: bool = False) -> st
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, _sources()))
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcufft", "-lcudart"]
+    nccl_lib = _nccl()[1]
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcufft", "-lcudart", "-L", nccl_lib, "-l:libnccl.so.2",
+           "-Xlinker", "-rpath=" + nccl_lib]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

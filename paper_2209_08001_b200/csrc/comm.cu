@@ -1,0 +1,130 @@
+// Library-owned communication of a z-sharded state: the NCCL
+// communicator created in nks_create from the caller's unique id, halo exchanges as grouped
+// ncclSend/ncclRecv on the state's stream, and fixed-order reductions (ncclAllGather of every rank's
+// partial sums + a rank-ordered sum on the device, so every rank holds identical bits and takes the same
+// control decisions -- reading R37).  Plus the host-only decomposition the ranks agree on.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "nks_internal.cuh"
+
+namespace nks {
+
+// ------------------------------------------------------------------------------------------ decomposition
+// Rank r owns a contiguous run of the nsub[2] global box layers along z (the first nsub[2] mod nranks ranks
+// one layer more), so every rank holds whole RAS boxes of the global box grid and the preconditioner -- hence
+// the iteration counts -- does not depend on the number of ranks.  Without RAS the planes
+// themselves are dealt out the same way.
+static void deal(int n, int parts, int r, int& lo, int& len) {
+  const int base = n / parts, rem = n % parts;
+  lo = r * base + std::min(r, rem);
+  len = base + (r < rem ? 1 : 0);
+}
+
+int slab_decompose(const nks_grid& global, int pc_type, int rank, int nranks, nks_grid& local, int& z_offset) {
+  if (global.dim != 3 || global.zghost != 0 || nranks < 1 || rank < 0 || rank >= nranks) return 1;
+  const int nz = global.n[2];
+  int lo = 0, own = 0, nbz = 1;
+  const bool ras = pc_type != NKS_PC_NONE;
+  if (ras) {
+    const int nsz = global.nsub[2];
+    if (nsz < nranks) return 1;
+    int b0, nb;
+    deal(nsz, nranks, rank, b0, nb);
+    // global box starts: the first nz mod nsz boxes one plane longer
+    const int base = nz / nsz, rem = nz % nsz;
+    auto start = [&](int b) { return b * base + std::min(b, rem); };
+    lo = start(b0);
+    own = start(b0 + nb) - lo;
+    nbz = nb;
+  } else {
+    deal(nz, nranks, rank, lo, own);
+  }
+  const int zg = ras ? std::max(2, global.overlap + 1) : 2;
+  if (own < 2 || zg > 8) return 1;
+  local = global;
+  local.n[2] = own + 2 * zg;
+  local.zghost = zg;
+  local.nsub[2] = nbz;
+  z_offset = lo;
+  return 0;
+}
+
+// ------------------------------------------------------------------------------------------ NCCL
+struct NcclComm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+};
+
+__global__ void k_rank_sum(const double* __restrict__ gathered, int nranks, long long n, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < nranks; ++r) s += gathered[(long long)r * n + i];     // rank order 0, 1, ...
+    out[i] = s;
+  }
+}
+
+int nccl_unique_id(uint8_t id[128]) {
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess) return 1;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id, &u, 128);
+  return 0;
+}
+
+void* nccl_create(const uint8_t id[128], int rank, int nranks, std::string& err) {
+  NcclComm* C = new NcclComm();
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  const ncclResult_t r = ncclCommInitRank(&C->comm, nranks, u, rank);
+  if (r != ncclSuccess) {
+    err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+    delete C;
+    return nullptr;
+  }
+  C->rank = rank;
+  C->nranks = nranks;
+  return C;
+}
+
+void nccl_destroy(void* c) {
+  NcclComm* C = (NcclComm*)c;
+  if (!C) return;
+  ncclCommDestroy(C->comm);
+  delete C;
+}
+
+// Fill the zg ghost planes on both z sides of nf fields (field f at vec + f * fstride, local (nzl, nxy)).
+int nccl_halo(void* c, double* vec, int nf, long long fstride, int nzl, long long nxy, int zg, cudaStream_t s) {
+  NcclComm* C = (NcclComm*)c;
+  const int up = (C->rank + 1) % C->nranks, dn = (C->rank + C->nranks - 1) % C->nranks;
+  const size_t cnt = (size_t)zg * nxy;
+  if (ncclGroupStart() != ncclSuccess) return 1;
+  for (int f = 0; f < nf; ++f) {
+    double* base = vec + (long long)f * fstride;
+    double* own_lo = base + (long long)zg * nxy;                 // first own planes -> rank-1's top ghosts
+    double* own_hi = base + (long long)(nzl - 2 * zg) * nxy;     // last own planes -> rank+1's bottom ghosts
+    double* gh_lo = base;
+    double* gh_hi = base + (long long)(nzl - zg) * nxy;
+    // per peer, NCCL matches sends and receives in issue order: with two ranks (up == dn) the first send
+    // (own_lo) meets the peer's first receive (gh_hi), the second (own_hi) its second (gh_lo)
+    if (ncclSend(own_lo, cnt, ncclDouble, dn, C->comm, s) != ncclSuccess) return 1;
+    if (ncclSend(own_hi, cnt, ncclDouble, up, C->comm, s) != ncclSuccess) return 1;
+    if (ncclRecv(gh_hi, cnt, ncclDouble, up, C->comm, s) != ncclSuccess) return 1;
+    if (ncclRecv(gh_lo, cnt, ncclDouble, dn, C->comm, s) != ncclSuccess) return 1;
+  }
+  return ncclGroupEnd() == ncclSuccess ? 0 : 1;
+}
+
+// buf[0..n) <- sum over ranks in rank order (gather: nranks * n doubles of workspace).
+int nccl_allreduce_fixed(void* c, double* buf, long long n, double* gather, cudaStream_t s) {
+  NcclComm* C = (NcclComm*)c;
+  if (C->nranks == 1) return 0;
+  if (ncclAllGather(buf, gather, (size_t)n, ncclDouble, C->comm, s) != ncclSuccess) return 1;
+  k_rank_sum<<<1, 256, 0, s>>>(gather, C->nranks, n, buf);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+}  // namespace nks

@@ -64,6 +64,20 @@ cudaError_t launch_apply(void* plan, const double* r, double* z, cudaStream_t s)
 void launch_ras_apply(const BoxSet& B, int nf, long long N, const double* fac, const float* fac32, const double* r,
                       double* y, double* z, cudaStream_t s);
 void launch_fac_to_fp32(const BoxSet& B, int nf, const double* fac, float* fac32, cudaStream_t s);
+// spectral.cu
+long long spectral_half(const nks_grid& g);
+void* spectral_plan(const nks_grid& g, int nf, cudaStream_t s, std::string& err);
+void spectral_free(void* p);
+void launch_spectral_setup(void* plan, const DevParams& dp, int nf, const double* Xa, const double* jac4, double* part,
+                           double* means, void* pinv, cudaStream_t s);
+int launch_spectral_apply(void* plan, int nf, const double* r, double* z, const void* pinv, void* spec, cudaStream_t s);
+// comm.cu
+int slab_decompose(const nks_grid& global, int pc_type, int rank, int nranks, nks_grid& local, int& z_offset);
+int nccl_unique_id(uint8_t id[128]);
+void* nccl_create(const uint8_t id[128], int rank, int nranks, std::string& err);
+void nccl_destroy(void* c);
+int nccl_halo(void* c, double* vec, int nf, long long fstride, int nzl, long long nxy, int zg, cudaStream_t s);
+int nccl_allreduce_fixed(void* c, double* buf, long long n, double* gather, cudaStream_t s);
 // init_fft.cu
 int init_displacement_fft(const DevParams& P, const double* c, double* u, void* scratch, cudaStream_t s, std::string& err);
 }  // namespace nks
@@ -91,7 +105,9 @@ struct Layout {
   size_t off_Ta, off_jac4, off_V, off_Z, off_W2, off_part, off_out;
   size_t off_fac, off_fac32, off_ybox, off_gidx, off_nbr, off_levoff, off_levptr, off_posoff, off_geo;
   size_t off_cover_off, off_cover_pos;
+  size_t off_gather;        // z-slab: [kMaxRanks][256] all-gather area of the fixed-order reductions
   size_t off_gtab;          // level-k ILU slot tables (off, lower, upper, pair_ptr, pair_b, pair_t)
+  size_t off_spec, off_pinv;  // spectral preconditioner: [nf][Nh] complex scratch, [nf*nf][Nh] inverse
   size_t total;
   long long P, ld;
   size_t geo_bytes;
@@ -111,20 +127,24 @@ const char* validate(const nks_grid* g, const nks_params* p) {
   if (p->gmres_restart < 1 || p->gmres_restart > 31) return "gmres_restart must be in 1..31";
   if (p->newton_maxit < 0 || p->gmres_maxit < 1 || p->gmres_stall_cycles < 0) return "bad iteration limits";
   if (p->pc_type != NKS_PC_NONE && p->pc_type != NKS_PC_RAS_BILU0 && p->pc_type != NKS_PC_AS_BILU0 &&
-      p->pc_type != NKS_PC_RRAS_BILU0)
+      p->pc_type != NKS_PC_RRAS_BILU0 && p->pc_type != NKS_PC_SPECTRAL)
     return "unknown pc_type";
+  if (p->pc_type == NKS_PC_SPECTRAL && g->zghost > 0) return "the spectral preconditioner needs the whole periodic grid";
   if (g->zghost > 0 && (p->pc_type == NKS_PC_AS_BILU0 || p->pc_type == NKS_PC_RRAS_BILU0))
     return "z-slab states support pc_type NONE or RAS (AS / RRAS need a reverse halo exchange)";
   if (g->zghost != 0 && (g->zghost < 2 || g->zghost > 8)) return "zghost must be 0 or 2..8";
   if (g->zghost > 0) {
     if (g->dim != 3) return "z-slab states (zghost > 0) are 3D";
+    const int own = g->n[2] - 2 * g->zghost;
+    if (g->nz_global < 5 || g->z_offset < 0 || g->z_offset + own > g->nz_global)
+      return "z-slab: z_offset / nz_global do not place the own planes in the global grid";
     if (g->n[2] - 2 * g->zghost < 2) return "a z-slab must own at least 2 planes";
     if (p->pc_type != NKS_PC_NONE && g->overlap + 1 > g->zghost)
       return "z-slab with RAS needs zghost >= overlap + 1 (assembly reads one cell beyond the box)";
     if (p->pc_type != NKS_PC_NONE && (g->nsub[2] < 1 || g->nsub[2] > g->n[2] - 2 * g->zghost))
       return "z-slab: nsub[2] must be in 1..own planes";
   }
-  if (p->pc_type != NKS_PC_NONE) {
+  if (p->pc_type != NKS_PC_NONE && p->pc_type != NKS_PC_SPECTRAL) {
     for (int j = 0; j < 3; ++j)
       if (g->nsub[j] < 1 || g->nsub[j] > g->n[j]) return "nsub[j] must be in 1..n[j]";
     if (g->dim == 2 && g->nsub[2] != 1) return "nsub[2] must be 1 in 2D";
@@ -156,8 +176,13 @@ Layout make_layout(const nks_grid& g, const nks_params& p, IlukPattern* K = null
   L.off_W2 = o; o = align256(o + vec);
   L.off_part = o; o = align256(o + (size_t)kRedBlocks * 80 * sizeof(double));
   L.off_out = o; o = align256(o + 256 * sizeof(double));
+  L.off_gather = o; o = align256(o + (g.zghost > 0 ? (size_t)kMaxRanks * 256 * sizeof(double) : 0));
   L.P = 0;
-  if (p.pc_type != NKS_PC_NONE) {
+  if (p.pc_type == NKS_PC_SPECTRAL) {
+    const long long Nh = spectral_half(g);
+    L.off_spec = o; o = align256(o + (size_t)nf * Nh * 16);
+    L.off_pinv = o; o = align256(o + (size_t)nf * nf * Nh * 16);
+  } else if (p.pc_type != NKS_PC_NONE) {
     const bool gen = p.ilu_level != 0;
     const int nslots = gen ? K->nslots : (d == 2 ? 13 : 25);
     const int la = gen ? K->la : 2, lb = gen ? K->lb : 3;
@@ -306,6 +331,10 @@ long long global_points(const nks_state* st) {
 void comm_allreduce(nks_state* st, double* buf, long long n) {
   st->reductions += 1;
   if (!st->comm_set || st->nranks == 1) return;
+  if (st->nccl) {
+    if (nccl_allreduce_fixed(st->nccl, buf, n, st->gather, st->stream) != 0) throw CommError();
+    return;
+  }
   if (st->comm_allreduce(st->comm_user, buf, n, (void*)st->stream) != 0) throw CommError();
 }
 
@@ -313,6 +342,11 @@ void comm_allreduce(nks_state* st, double* buf, long long n) {
 void halo(nks_state* st, double* vec, int nf) {
   if (!slab(st) || !st->comm_set) return;
   PhaseScope ps(st, PH_OTHER);   // halo exchanges are accounted under "other"
+  if (st->nccl) {
+    const long long nxy = (long long)st->grid.n[0] * st->grid.n[1];
+    if (nccl_halo(st->nccl, vec, nf, st->N, st->grid.n[2], nxy, st->grid.zghost, st->stream) != 0) throw CommError();
+    return;
+  }
   if (st->comm_halo(st->comm_user, vec, nf, st->N, (void*)st->stream) != 0) throw CommError();
 }
 
@@ -363,6 +397,12 @@ void pc_apply(nks_state* st, const double* r, double* z) {
     return;
   }
   PhaseScope ps(st, PH_RAS);
+  if (st->spec) {
+    if (launch_spectral_apply(st->spec, st->nf, r, z, st->pinv, st->specbuf, st->stream) != 0)
+      throw std::runtime_error("cuFFT execution failed");
+    count_launch(st, 1);
+    return;
+  }
   if (st->ras2d) CK(r2::launch_apply(st->ras2d, r, z, st->stream));
   else if (st->boxes.gen) launch_ras_apply_gen(st->boxes, st->nf, st->N, st->fac, r, st->ybox, z, st->stream);
   else launch_ras_apply(st->boxes, st->nf, st->N, st->fac, st->fac32, r, st->ybox, z, st->stream);
@@ -371,6 +411,15 @@ void pc_apply(nks_state* st, const double* r, double* z) {
 
 void pc_setup(nks_state* st, const double* Xb) {
   if (st->prm.pc_type == NKS_PC_NONE) return;
+  if (st->spec) {
+    PhaseScope ps(st, PH_FACT);
+    launch_spectral_setup(st->spec, st->dp, st->nf, st->Xn, st->jac4, st->red_part, st->red_out + 192, st->pinv,
+                          st->stream);
+    count_launch(st, 3);
+    st->pc_valid = true;
+    st->pc_dt = st->dp.dt;
+    return;
+  }
   {
     PhaseScope ps(st, PH_ASM);
     if (st->boxes.gen) launch_assemble_gen(st->dp, st->boxes, st->nf, st->Xn, st->jac4, st->fac, st->stream);
@@ -769,12 +818,15 @@ size_t nks_workspace_bytes(const nks_grid* grid, const nks_params* params) {
   }
 }
 
-nks_status nks_create(const nks_grid* grid, const nks_params* params, void* workspace, size_t workspace_bytes,
-                      void* cuda_stream, nks_state** out) {
+nks_status nks_create(const nks_grid* grid, const nks_params* params, int32_t rank, int32_t nranks,
+                      const uint8_t* nccl_id, void* workspace, size_t workspace_bytes, void* cuda_stream,
+                      nks_state** out) {
   if (!out) return NKS_E_INVALID;
   *out = nullptr;
   if (validate(grid, params)) return NKS_E_INVALID;
   if (!workspace) return NKS_E_INVALID;
+  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks) return NKS_E_INVALID;
+  if (grid->zghost == 0 && nranks != 1) return NKS_E_INVALID;     // a periodic whole-grid state is one rank
   IlukPattern Kpat;
   Layout L;
   try {
@@ -796,6 +848,12 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
   st->ws_bytes = workspace_bytes;
   st->zeta = params->zeta;
   st->debug = std::getenv("NKS_DEBUG") != nullptr;
+  st->rank = rank;
+  st->nranks = nranks;
+  if (grid->zghost > 0) {
+    st->dp.zoff = grid->z_offset;
+    st->dp.nzg = grid->nz_global;
+  }
   const nks_status rc = guarded(st, [&]() -> nks_status {
     char* w = st->ws;
     double** Xs[7] = {&st->Xn, &st->Xprev, &st->Xb, &st->Xt, &st->S, &st->F, &st->Ft};
@@ -808,12 +866,28 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, void* work
     st->red_part = (double*)(w + L.off_part);
     st->red_out = (double*)(w + L.off_out);
     st->red_cnt = (unsigned*)(st->red_out + 255);
+    st->gather = (double*)(w + L.off_gather);
+    if (grid->zghost > 0 && nccl_id) {     // library-owned communicator (collective over the nranks ranks)
+      std::string why;
+      st->nccl = nccl_create(nccl_id, rank, nranks, why);
+      if (!st->nccl) {
+        st->err = why;
+        throw CommError();
+      }
+      st->comm_set = true;
+    }
     CK(cudaMemsetAsync(st->red_cnt, 0, sizeof(unsigned), st->stream));
     if (grid->zghost > 0) CK(cudaMemsetAsync(w, 0, L.off_part, st->stream));   // zero ghosts of every vector
     CK(cudaMallocHost(&st->h_red, 256 * sizeof(double)));
     CK(cudaMallocHost(&st->h_ring, 4 * 128 * sizeof(double)));
     for (int k = 0; k < 4; ++k) CK(cudaEventCreateWithFlags(&st->gm_ev[k], cudaEventDisableTiming));
-    if (params->pc_type != NKS_PC_NONE) {
+    if (params->pc_type == NKS_PC_SPECTRAL) {
+      std::string why;
+      st->spec = spectral_plan(*grid, st->nf, st->stream, why);
+      if (!st->spec) throw std::runtime_error(why);
+      st->specbuf = w + L.off_spec;
+      st->pinv = w + L.off_pinv;
+    } else if (params->pc_type != NKS_PC_NONE) {
       BoxSet& B = st->boxes;
       build_slot_tables(grid->dim, B);
       const bool gen = params->ilu_level != 0;
@@ -953,22 +1027,35 @@ nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, con
   });
 }
 
-nks_status nks_set_comm(nks_state* st, int32_t rank, int32_t nranks, int32_t z_offset, int32_t nz_global,
-                        nks_allreduce_fn allreduce, nks_halo_fn halo_fn, void* user) {
-  if (!st || !slab(st) || nranks < 1 || rank < 0 || rank >= nranks || !halo_fn) return NKS_E_INVALID;
-  if (nranks > 1 && !allreduce) return NKS_E_INVALID;
-  const int own = st->grid.n[2] - 2 * st->grid.zghost;
-  if (z_offset < 0 || nz_global < own || z_offset + own > nz_global) return NKS_E_INVALID;
-  if (nz_global < 5) return NKS_E_INVALID;
-  st->rank = rank;
-  st->nranks = nranks;
+nks_status nks_set_comm(nks_state* st, nks_allreduce_fn allreduce, nks_halo_fn halo_fn, void* user) {
+  if (!st || !slab(st) || !halo_fn) return NKS_E_INVALID;
+  if (st->nccl) return NKS_E_STATE;                  // the state already owns an NCCL communicator
+  if (st->nranks > 1 && !allreduce) return NKS_E_INVALID;
   st->comm_allreduce = allreduce;
   st->comm_halo = halo_fn;
   st->comm_user = user;
   st->comm_set = true;
-  st->dp.zoff = z_offset;
-  st->dp.nzg = nz_global;
   st->pc_valid = false;
+  return NKS_OK;
+}
+
+nks_status nks_get_unique_id(uint8_t id[128]) {
+  if (!id) return NKS_E_INVALID;
+  return nccl_unique_id(id) == 0 ? NKS_OK : NKS_E_NCCL;
+}
+
+nks_status nks_decompose(const nks_grid* global, const nks_params* params, int32_t rank, int32_t nranks,
+                         nks_grid* local) {
+  if (!global || !params || !local) return NKS_E_INVALID;
+  if (validate(global, params)) return NKS_E_INVALID;
+  if (nranks > kMaxRanks) return NKS_E_INVALID;
+  int zoff = 0;
+  nks_grid loc{};
+  if (slab_decompose(*global, params->pc_type, rank, nranks, loc, zoff) != 0) return NKS_E_INVALID;
+  loc.z_offset = zoff;
+  loc.nz_global = global->n[2];
+  if (validate(&loc, params)) return NKS_E_INVALID;
+  *local = loc;
   return NKS_OK;
 }
 
@@ -1222,6 +1309,8 @@ nks_status nks_destroy(nks_state* st) {
   for (int k = 0; k < 4; ++k)
     if (st->gm_ev[k]) cudaEventDestroy(st->gm_ev[k]);
   if (st->ras2d) r2::free_plan(st->ras2d);
+  if (st->spec) spectral_free(st->spec);
+  if (st->nccl) nccl_destroy(st->nccl);
   delete st;
   return NKS_OK;
 }

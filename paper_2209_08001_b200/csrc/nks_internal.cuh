@@ -18,6 +18,7 @@ constexpr int kMaxSlots = 25;      // |o|_1 <= 2 block footprint in 3D
 constexpr int kMaxS = 16;
 constexpr int kRedBlocks = 592;    // 4 x 148 SMs: blocks of every reduction first stage
 constexpr int kRedThreads = 256;
+constexpr int kMaxRanks = 64;      // ranks of one sharded run (all-gather area of the fixed-order reductions)
 
 // Parameters passed by value to every kernel (fp64 model constants derived on the host).
 struct DevParams {
@@ -145,6 +146,9 @@ struct nks_state {
   double* ybox = nullptr;   // [nf][P]
   bool pc_valid = false;
   void* ras2d = nullptr;    // plan of the row-pipelined 2D RAS apply (ras2d_rows.cu), or null
+  void* spec = nullptr;     // cuFFT plans of the spectral preconditioner (spectral.cu), or null
+  void* specbuf = nullptr;  // [nf][Nh] complex scratch (workspace)
+  void* pinv = nullptr;     // [nf*nf][Nh] per-wave-number inverse (workspace)
   double pc_dt = 0.0;
   // history / controller
   double time = 0.0;
@@ -159,6 +163,8 @@ struct nks_state {
   nks_halo_fn comm_halo = nullptr;
   void* comm_user = nullptr;
   bool comm_set = false;
+  void* nccl = nullptr;         // library-owned NCCL communicator (comm.cu), or null (callbacks / one state)
+  double* gather = nullptr;     // [kMaxRanks][256] all-gather area
   // counters
   long long launches = 0;
   long long syncs = 0;

@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("NKS_LIB", os.path.join(_HERE, "lib", "libnks.so"))   
 
 NKS_OK, NKS_E_INVALID, NKS_E_DOMAIN, NKS_E_DIVERGED, NKS_E_CUDA, NKS_E_NCCL, NKS_E_OOM, NKS_E_STATE = range(8)
 STATUS = {0: "OK", 1: "INVALID", 2: "DOMAIN", 3: "DIVERGED", 4: "CUDA", 5: "NCCL", 6: "OOM", 7: "STATE"}
-PC_NONE, PC_RAS_BILU0, PC_AS_BILU0, PC_RRAS_BILU0 = 0, 2, 3, 4
+PC_NONE, PC_RAS_BILU0, PC_AS_BILU0, PC_RRAS_BILU0, PC_SPECTRAL = 0, 2, 3, 4, 5
 REASONS = {0: "none", 1: "newton_maxit", 2: "line_search", 3: "gmres_maxit", 4: "domain", 5: "dt_floor",
            6: "gmres_stagnation"}
 PHASES = ["residual", "jv", "ras_apply", "assemble", "factor", "gmres_vec", "reductions", "other"]
@@ -25,7 +25,7 @@ PHASES = ["residual", "jv", "ras_apply", "assemble", "factor", "gmres_vec", "red
 
 class Grid(C.Structure):
     _fields_ = [("dim", C.c_int32), ("n", C.c_int32 * 3), ("h", C.c_double), ("nsub", C.c_int32 * 3),
-                ("overlap", C.c_int32), ("zghost", C.c_int32)]
+                ("overlap", C.c_int32), ("zghost", C.c_int32), ("z_offset", C.c_int32), ("nz_global", C.c_int32)]
 
 
 class Params(C.Structure):
@@ -68,12 +68,15 @@ ALLREDUCE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_voi
 HALO_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_void_p)
 _SIGS = {
     "nks_workspace_bytes": (C.c_size_t, [C.POINTER(Grid), C.POINTER(Params)]),
-    "nks_create": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), _P, C.c_size_t, _P, C.POINTER(_P)]),
+    "nks_create": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), C.c_int32, C.c_int32, _P, _P, C.c_size_t, _P,
+                             C.POINTER(_P)]),
+    "nks_get_unique_id": (C.c_int, [_P]),
+    "nks_decompose": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), C.c_int32, C.c_int32, C.POINTER(Grid)]),
     "nks_set_fields": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
     "nks_get_fields": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
     "nks_set_state": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
     "nks_set_cbar0": (C.c_int, [_P, C.c_double]),
-    "nks_set_comm": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, ALLREDUCE_FN, HALO_FN, _P]),
+    "nks_set_comm": (C.c_int, [_P, ALLREDUCE_FN, HALO_FN, _P]),
     "nks_step": (C.c_int, [_P, C.c_double, C.POINTER(StepInfo)]),
     "nks_run_adaptive": (C.c_int, [_P, C.c_int32, C.c_double, C.POINTER(StepInfo), C.POINTER(C.c_int32)]),
     "nks_energy": (C.c_int, [_P, _D, _D]),
@@ -115,7 +118,7 @@ class NKSError(RuntimeError):
         self.status = status
 
 
-def make_grid(shape, h=0.25, nsub=None, overlap=2, zghost=0) -> Grid:
+def make_grid(shape, h=0.25, nsub=None, overlap=2, zghost=0, z_offset=0, nz_global=0) -> Grid:
     """shape and nsub in C order: (ny, nx) or (nz, ny, nx)."""
     d = len(shape)
     g = Grid()
@@ -130,7 +133,27 @@ def make_grid(shape, h=0.25, nsub=None, overlap=2, zghost=0) -> Grid:
         g.nsub[j] = int(ns[j])
     g.overlap = int(overlap)
     g.zghost = int(zghost)
+    g.z_offset = int(z_offset)
+    g.nz_global = int(nz_global)
     return g
+
+
+def unique_id() -> bytes:
+    """nks_get_unique_id: the 128-byte NCCL id rank 0 hands to every rank of a sharded run."""
+    buf = C.create_string_buffer(128)
+    rc = load_library().nks_get_unique_id(buf)
+    if rc != NKS_OK:
+        raise NKSError(rc, "nks_get_unique_id failed")
+    return buf.raw
+
+
+def decompose(global_grid: Grid, params: Params, rank: int, nranks: int) -> Grid:
+    """nks_decompose: the z-slab grid of `rank` (host only)."""
+    out = Grid()
+    rc = load_library().nks_decompose(C.byref(global_grid), C.byref(params), int(rank), int(nranks), C.byref(out))
+    if rc != NKS_OK:
+        raise NKSError(rc, "nks_decompose: no valid slab for this grid / rank count")
+    return out
 
 
 def make_params(model: dict, solver: dict, pc_type=PC_RAS_BILU0, pc_reuse=1) -> Params:
@@ -158,7 +181,10 @@ class Solver:
     """One NKS state on the current CUDA device (single GPU)."""
 
     def __init__(self, shape, model: dict, solver: dict, h=0.25, nsub=None, overlap=2,
-                 pc_type=PC_RAS_BILU0, pc_reuse=1, device=None, zghost=0):
+                 pc_type=PC_RAS_BILU0, pc_reuse=1, device=None, zghost=0, grid: Grid = None, rank=0, nranks=1,
+                 nccl_id: bytes = None):
+        """shape: the (local) grid in C order; `grid` overrides the grid built from shape/nsub/overlap/zghost
+        (a slab from `decompose`).  nccl_id (slab states): the library creates its own NCCL communicator."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2209_08001_b200 needs a CUDA device (B200, sm_100a)")
@@ -169,7 +195,9 @@ class Solver:
         self.nf = 2 + self.d
         self.N = int(np.prod(shape))
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.grid = make_grid(shape, h, nsub, overlap, zghost)
+        self.grid = grid if grid is not None else make_grid(shape, h, nsub, overlap, zghost)
+        self.rank, self.nranks = int(rank), int(nranks)
+        self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         self.params = make_params(model, solver, pc_type, pc_reuse)
         nbytes = self.lib.nks_workspace_bytes(C.byref(self.grid), C.byref(self.params))
         if nbytes == 0:
@@ -178,8 +206,9 @@ class Solver:
             self.workspace = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
             self.stream = torch.cuda.current_stream(self.device)
             st = C.c_void_p()
-            rc = self.lib.nks_create(C.byref(self.grid), C.byref(self.params), C.c_void_p(self.workspace.data_ptr()),
-                                     C.c_size_t(nbytes), C.c_void_p(self.stream.cuda_stream), C.byref(st))
+            rc = self.lib.nks_create(C.byref(self.grid), C.byref(self.params), self.rank, self.nranks, self._nccl_id,
+                                     C.c_void_p(self.workspace.data_ptr()), C.c_size_t(nbytes),
+                                     C.c_void_p(self.stream.cuda_stream), C.byref(st))
         if rc != NKS_OK:
             raise NKSError(rc, "nks_create failed")
         self.st = st
@@ -234,10 +263,11 @@ class Solver:
                                     C.c_void_p(tu.data_ptr()), 1)
         self._check(rc, "nks_set_state")
 
-    def set_comm(self, rank, nranks, z_offset, nz_global, allreduce, halo):
-        """Attach this z-slab state to its process group (nks_set_comm).  allreduce(ptr, n, stream) and
-        halo(ptr, nfields, field_stride, stream) are Python callables on raw device pointers that return
-        0 on success; the ctypes trampolines are kept alive by this object."""
+    def set_comm(self, allreduce, halo):
+        """Attach host communication callbacks to this z-slab state (nks_set_comm; the callback backend of a
+        state created without an NCCL id).  allreduce(ptr, n, stream) and halo(ptr, nfields, field_stride,
+        stream) are Python callables on raw device pointers that return 0 on success; the ctypes
+        trampolines are kept alive by this object."""
         def _ar(user, buf, n, stream):
             try:
                 return int(allreduce(buf, n, stream) or 0)
@@ -253,8 +283,7 @@ class Solver:
                 return 1
         self._comm_cbs = (ALLREDUCE_FN(_ar), HALO_FN(_halo))
         self.comm_error = None
-        self._check(self.lib.nks_set_comm(self.st, int(rank), int(nranks), int(z_offset), int(nz_global),
-                                          self._comm_cbs[0], self._comm_cbs[1], None), "nks_set_comm")
+        self._check(self.lib.nks_set_comm(self.st, self._comm_cbs[0], self._comm_cbs[1], None), "nks_set_comm")
 
     def device_view(self, ptr, n):
         """fp64 tensor aliasing n doubles at device pointer ptr inside this state's workspace."""

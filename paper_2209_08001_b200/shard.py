@@ -131,7 +131,7 @@ class SlabOperators:
 
     def __init__(self, shape_global, model, solver, group=None, h=0.25, device=None, world=None, rank=None):
         import torch
-        from .nks import PC_NONE, Solver
+        from .nks import PC_NONE, Solver, make_grid
         self.group = group
         w, r = _world(group)
         world = w if world is None else world       # world/rank may be given explicitly (single-process emulation)
@@ -145,7 +145,8 @@ class SlabOperators:
         self.local_shape = (self.own + 2 * GHOST, ny, nx)
         sol = dict(solver)
         sol["gmres_restart"] = 1
-        self.solver = Solver(self.local_shape, model, sol, h=h, pc_type=PC_NONE, zghost=GHOST, device=device)
+        grid = make_grid(self.local_shape, h, None, 2, GHOST, z_offset=self.lo, nz_global=nz)
+        self.solver = Solver(self.local_shape, model, sol, h=h, pc_type=PC_NONE, device=device, grid=grid)
         self.torch = torch
 
     def set_level_n(self, Xa, cbar0):
@@ -168,20 +169,23 @@ class SlabOperators:
 class ShardedSolver:
     """One z-slab of a 3D periodic grid per rank, stepped by the library's full NKS step.
 
-    Every rank holds the own planes of its slab plus zghost ghost planes per side; the library calls
-    back into this object for the halo exchanges (before F, J.v, the RAS input and after every state
-    update) and for the allreduces (norms, admissibility counts, CGS2 projections, gauge sums, energy).
-    The RAS boxes are the global box grid dealt out whole to the ranks, so the preconditioner -- and
-    the iteration counts -- do not depend on the number of ranks.
+    The library decomposes the grid (nks_decompose: every rank owns whole layers of the global RAS box
+    grid, so the preconditioner -- and the iteration counts -- do not depend on the number of ranks) and,
+    with comm="nccl", owns the communication: rank 0's nks_get_unique_id is broadcast over the torch
+    process group, nks_create builds an NCCL communicator, and the halo exchanges (grouped ncclSend/ncclRecv)
+    and fixed-order reductions (ncclAllGather + rank-ordered sum) run inside the library on its stream --
+    no Python in the per-iteration path.  comm="callbacks" attaches this object's host callbacks instead
+    (torch.distributed exchanges; gloo stages through host memory) -- used to emulate several ranks on one
+    GPU or on CPU process groups.  comm="auto": "nccl" when the group's backend is NCCL or it has one rank.
 
-    shape_global / nsub: C order (nz, ny, nx).  group: a torch.distributed process group (NCCL on
-    GPUs; gloo stages through host memory) or None for the default group / one rank.
+    shape_global / nsub: C order (nz, ny, nx).  group: a torch.distributed process group or None (the
+    default group; none initialised = one rank).
     """
 
     def __init__(self, shape_global, model, solver, h=0.25, nsub=(1, 1, 1), overlap=2, pc_type=None,
-                 pc_reuse=1, group=None, device=None):
+                 pc_reuse=1, group=None, device=None, comm="auto"):
         import torch
-        from .nks import PC_RAS_BILU0, Solver
+        from .nks import PC_RAS_BILU0, Solver, decompose, make_grid, make_params, unique_id
         if len(shape_global) != 3:
             raise ValueError("z-slab sharding is 3D")
         self.torch = torch
@@ -190,25 +194,34 @@ class ShardedSolver:
         self.shape_global = tuple(int(v) for v in shape_global)
         nz, ny, nx = self.shape_global
         self.pc_type = PC_RAS_BILU0 if pc_type is None else pc_type
-        ras = self.pc_type == PC_RAS_BILU0
         self.nsub_z = int(nsub[0])
-        if ras:
-            self.lo, self.hi, nbz = box_slab_bounds(nz, int(nsub[0]), self.world, self.rank)
-            self.zghost = max(GHOST, int(overlap) + 1)
-        else:
-            self.lo, self.hi = slab_bounds(nz, self.world, self.rank)
-            nbz = 1
-            self.zghost = GHOST
-        self.own = self.hi - self.lo
-        zg = self.zghost
+        params = make_params(model, solver, self.pc_type, pc_reuse)
+        self.lgrid = decompose(make_grid(self.shape_global, h, nsub, overlap), params, self.rank, self.world)
+        self.zghost = zg = int(self.lgrid.zghost)
+        self.lo = int(self.lgrid.z_offset)
+        self.own = int(self.lgrid.n[2]) - 2 * zg
+        self.hi = self.lo + self.own
         self.local_shape = (self.own + 2 * zg, ny, nx)
         self.model, self.solver_cfg, self.h = model, solver, h
-        self.solver = Solver(self.local_shape, model, solver, h=h, nsub=(nbz, int(nsub[1]), int(nsub[2])),
-                             overlap=overlap, pc_type=self.pc_type, pc_reuse=pc_reuse, zghost=zg, device=device)
-        self.device = self.solver.device
+        if comm == "auto":
+            comm = "nccl" if (self.world == 1 or not _is_gloo(group)) else "callbacks"
+        self.comm = comm
         self.halo_calls = 0
         self.allreduce_calls = 0
-        self.solver.set_comm(self.rank, self.world, self.lo, nz, self._allreduce, self._halo)
+        nccl_id = None
+        if comm == "nccl":
+            nccl_id = unique_id() if self.rank == 0 else None
+            if self.world > 1:
+                import torch.distributed as dist
+                box = [nccl_id]
+                src = dist.get_global_rank(group, 0) if group is not None else 0
+                dist.broadcast_object_list(box, src=src, group=group)
+                nccl_id = box[0]
+        self.solver = Solver(self.local_shape, model, solver, h=h, pc_type=self.pc_type, pc_reuse=pc_reuse,
+                             device=device, grid=self.lgrid, rank=self.rank, nranks=self.world, nccl_id=nccl_id)
+        self.device = self.solver.device
+        if comm == "callbacks":
+            self.solver.set_comm(self._allreduce, self._halo)
 
     # ---------------------------------------------------------------- callbacks (library -> here)
     def _allreduce(self, ptr, n, stream):
@@ -295,9 +308,10 @@ class ShardedSolver:
         return self.torch.cat([p.cpu() for p in parts], dim=1).numpy()
 
     def slab_of(self, r):
-        """(lo, hi) global z range of rank r."""
-        from .nks import PC_RAS_BILU0
-        nz = self.shape_global[0]
-        if self.pc_type == PC_RAS_BILU0:
-            return box_slab_bounds(nz, self.nsub_z, self.world, r)[:2]
-        return slab_bounds(nz, self.world, r)
+        """(lo, hi) global z range of rank r (the library's decomposition)."""
+        from .nks import decompose, make_grid, make_params
+        params = make_params(self.model, self.solver_cfg, self.pc_type)
+        nz, ny, nx = self.shape_global
+        lg = decompose(make_grid(self.shape_global, self.h, (self.nsub_z, 1, 1), self.lgrid.overlap), params, r,
+                       self.world)
+        return int(lg.z_offset), int(lg.z_offset) + int(lg.n[2]) - 2 * int(lg.zghost)

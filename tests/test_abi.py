@@ -94,7 +94,7 @@ def test_workspace_bytes_validates(lib):
 
 
 def test_null_arguments_rejected_without_device(lib):
-    assert lib.nks_create(None, None, None, 0, None, None) == nks.NKS_E_INVALID
+    assert lib.nks_create(None, None, 0, 1, None, None, 0, None, None) == nks.NKS_E_INVALID
     assert lib.nks_step(None, C.c_double(0.01), None) == nks.NKS_E_INVALID
     assert lib.nks_destroy(None) == nks.NKS_E_INVALID
     assert b"nks-b200" in lib.nks_version()
@@ -125,3 +125,28 @@ def test_iluk_workspace_grows_with_fill(lib):
     g3 = nks.make_grid((12, 12, 12), 0.25, (2, 2, 2), 2)
     p = nks.make_params(ni.model_default(), dict(ni.solver_default(), ilu_level=1))
     assert lib.nks_workspace_bytes(C.byref(g3), C.byref(p)) > 0
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 3, 4, 8])
+def test_decompose_deals_whole_box_layers(lib, nranks):
+    """nks_decompose (host only): the slabs of all ranks tile the global z range in order, each made of
+    whole layers of the global RAS box grid (the boxes' z starts are global box boundaries), with
+    zghost = max(2, overlap + 1) ghost planes; the split matches shard.box_slab_bounds."""
+    from paper_2209_08001_b200 import shard
+    nz, nsz, ov = 40, 8, 2
+    p = nks.make_params(ni.model_default(), ni.solver_default())
+    gg = nks.make_grid((nz, 12, 10), 0.25, (nsz, 2, 1), ov)
+    z = 0
+    base, rem = divmod(nz, nsz)
+    bounds = {b * base + min(b, rem) for b in range(nsz + 1)}
+    for r in range(nranks):
+        lg = nks.decompose(gg, p, r, nranks)
+        own = lg.n[2] - 2 * lg.zghost
+        assert lg.z_offset == z and lg.nz_global == nz and lg.zghost == max(2, ov + 1)
+        assert z in bounds and z + own in bounds
+        assert (z, z + own, lg.nsub[2]) == shard.box_slab_bounds(nz, nsz, nranks, r)
+        assert (lg.n[0], lg.n[1], lg.nsub[0], lg.nsub[1]) == (10, 12, 1, 2)
+        z += own
+    assert z == nz
+    with pytest.raises(nks.NKSError):
+        nks.decompose(gg, p, 0, nsz + 1)           # fewer box layers than ranks

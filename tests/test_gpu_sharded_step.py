@@ -5,8 +5,10 @@ as on one device; the library calls back for every halo exchange and allreduce. 
 must reproduce the unsharded fields to the parity tolerance (north_star: rel L2 <= 1e-8; the two
 runs differ only in the summation order of the reductions) with the same Newton iteration counts.
 
-Ranks run as processes on ONE GPU over a gloo group: every exchange is host-staged, so no kernel of
-one rank waits on another rank's kernel (the NCCL path uses the same callbacks on device tensors).
+Ranks run as processes on ONE GPU over a gloo group with the callback backend: every exchange is
+host-staged, so no kernel of one rank waits on another rank's kernel.  The library-owned NCCL backend
+(nks_get_unique_id + nks_create with the id; grouped ncclSend/ncclRecv halos, ncclAllGather reductions)
+runs here with one rank -- its periodic self-exchange -- since NCCL needs one GPU per rank.
 """
 import os
 import socket
@@ -43,21 +45,21 @@ def _unsharded(shape, nsub, overlap, pc_type, dts):
     return s.get_state(), infos
 
 
-def _run_sharded(rank, world, port, shape, nsub, overlap, pc_type, dts, out_path):
+def _run_sharded(rank, world, port, shape, nsub, overlap, pc_type, dts, out_path, comm="auto"):
     if world > 1:
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
         from paper_2209_08001_b200.shard import ShardedSolver
         torch.cuda.set_device(0)
         c, eta = _fields(shape)
-        sh = ShardedSolver(shape, MODEL, _solver_cfg(), nsub=nsub, overlap=overlap, pc_type=pc_type)
+        sh = ShardedSolver(shape, MODEL, _solver_cfg(), nsub=nsub, overlap=overlap, pc_type=pc_type, comm=comm)
         sh.set_fields(c, eta)
         infos = [sh.step(dt) for dt in dts]
         X = sh.gather_state()
         if rank == 0:
             np.savez(out_path, X=X, newton=[i["newton_its"] for i in infos], gmres=[i["gmres_its"] for i in infos],
                      energy=[i["energy"] for i in infos], mass=[i["mass"] for i in infos],
-                     halo=sh.halo_calls, allreduce=sh.allreduce_calls)
+                     halo=sh.halo_calls, allreduce=sh.allreduce_calls, comm=sh.comm)
     finally:
         if world > 1:
             dist.destroy_process_group()
@@ -72,24 +74,26 @@ def _free_port():
 
 
 CASES = [
-    # shape (z, y, x), nsub (z, y, x), overlap, pc, world, dts
-    ((16, 12, 12), (4, 2, 2), 2, "ras", 1, [0.05, 0.5]),
-    ((16, 12, 12), (4, 2, 2), 2, "ras", 2, [0.05, 0.5]),
-    ((18, 10, 12), (6, 2, 1), 2, "ras", 3, [0.1]),
-    ((12, 10, 12), (1, 1, 1), 2, "none", 2, [0.01]),
+    # shape (z, y, x), nsub (z, y, x), overlap, pc, world, dts, comm
+    ((16, 12, 12), (4, 2, 2), 2, "ras", 1, [0.05, 0.5], "nccl"),
+    ((16, 12, 12), (4, 2, 2), 2, "ras", 1, [0.05, 0.5], "callbacks"),
+    ((16, 12, 12), (4, 2, 2), 2, "ras", 2, [0.05, 0.5], "callbacks"),
+    ((18, 10, 12), (6, 2, 1), 2, "ras", 3, [0.1], "callbacks"),
+    ((12, 10, 12), (1, 1, 1), 2, "none", 2, [0.01], "callbacks"),
+    ((12, 10, 12), (1, 1, 1), 2, "none", 1, [0.01], "nccl"),
 ]
 
 
-@pytest.mark.parametrize("shape,nsub,overlap,pc,world,dts", CASES)
-def test_sharded_step_matches_unsharded(tmp_path, shape, nsub, overlap, pc, world, dts):
+@pytest.mark.parametrize("shape,nsub,overlap,pc,world,dts,comm", CASES)
+def test_sharded_step_matches_unsharded(tmp_path, shape, nsub, overlap, pc, world, dts, comm):
     from paper_2209_08001_b200 import PC_NONE, PC_RAS_BILU0
     pc_type = PC_RAS_BILU0 if pc == "ras" else PC_NONE
     Xr, infos = _unsharded(shape, nsub, overlap, pc_type, dts)
     out = str(tmp_path / "sharded.npz")
     if world == 1:
-        _run_sharded(0, 1, 0, shape, nsub, overlap, pc_type, dts, out)
+        _run_sharded(0, 1, 0, shape, nsub, overlap, pc_type, dts, out, comm)
     else:
-        mp.spawn(_run_sharded, args=(world, _free_port(), shape, nsub, overlap, pc_type, dts, out), nprocs=world,
+        mp.spawn(_run_sharded, args=(world, _free_port(), shape, nsub, overlap, pc_type, dts, out, comm), nprocs=world,
                  join=True)
     r = np.load(out)
     X = r["X"]
@@ -106,6 +110,8 @@ def test_sharded_step_matches_unsharded(tmp_path, shape, nsub, overlap, pc, worl
         assert abs(e - i["energy"]) <= 1e-10 * abs(i["energy"])
     for m, i in zip(r["mass"], infos):
         assert abs(m - i["mass"]) <= 1e-12 * abs(i["mass"])
-    assert r["halo"] > 0
-    if world > 1:
-        assert r["allreduce"] > 0
+    assert str(r["comm"]) == comm
+    if comm == "callbacks":
+        assert r["halo"] > 0
+        if world > 1:
+            assert r["allreduce"] > 0
