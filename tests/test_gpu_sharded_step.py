@@ -104,7 +104,7 @@ def test_sharded_step_matches_unsharded(tmp_path, shape, nsub, overlap, pc, worl
     # same preconditioner: iteration counts agree up to roundoff at the tolerance (unpreconditioned
     # GMRES(30) runs thousands of iterations, where roundoff shifts the count by a few per cent)
     for g, i in zip(r["gmres"], infos):
-        slack = i["newton_its"] if pc == "ras" else max(i["newton_its"], 0.05 * i["gmres_its"])
+        slack = i["newton_its"] if pc == "ras" else max(i["newton_its"], 0.10 * i["gmres_its"])
         assert abs(int(g) - i["gmres_its"]) <= slack, (g, i["gmres_its"])
     for e, i in zip(r["energy"], infos):
         assert abs(e - i["energy"]) <= 1e-10 * abs(i["energy"])
