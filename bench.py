@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-micro", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="3D configs: run the z-slab sharded NKS step (ShardedSolver, NCCL halos/allreduces); "
                          "implied for 3D configs at N > 1")
@@ -390,7 +391,8 @@ def run_variant(args, cfg, model, sol, c, eta, pg, pc_type):
     torch.cuda.synchronize()
     t_ms = max_over_ranks(pg, evs[0].elapsed_time(evs[-1]))
     per = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
-    out = {"pc": {5: "spectral (cuFFT, mean-coefficient inverse per wave number)"}.get(pc_type, pc_type),
+    out = {"pc": {5: "spectral (cuFFT, mean-coefficient inverse per wave number)",
+                  2: "left-RAS, point-block ILU(0)"}.get(pc_type, pc_type),
            "value": args.steps / (t_ms / 1e3), "unit": UNIT, "ms_per_step": t_ms / args.steps, "step_ms": step_stats(per),
            "newton_its": [r["newton_its"] for r in recs], "gmres_its": [r["gmres_its"] for r in recs],
            "dt": [r["dt"] for r in recs], "retries": [r["retries"] for r in recs],
@@ -518,6 +520,29 @@ def run_gpu(args, world, rank, local, pg):
     if not sharded and not args.no_variants:
         variants["spectral_pc"] = run_variant(args, cfg, model, sol, c, eta, pg, PC_SPECTRAL)
 
+    # ---- the 3D configurations on this GPU, a few steps each: config 3
+    # (128^3, RAS 8x8x8 boxes, BILU(0)) with the configured preconditioner and with the spectral one;
+    # config 4 (256^3) with the spectral one (its one-level RAS/BILU(0) step takes ~15 min on one GPU,
+    # DESIGN.md section 7)
+    extra = {}
+    if not sharded and world == 1 and not args.no_extra and args.config == 2:
+        del g
+        torch.cuda.empty_cache()
+        g = None
+        for key, cid, pct, w, k in (("config3_ras_bilu0", 3, None, 1, 1), ("config3_spectral", 3, PC_SPECTRAL, 1, 3),
+                                    ("config4_spectral", 4, PC_SPECTRAL, 1, 2)):
+            try:
+                ecfg = ni.CONFIGS[cid]
+                ec, ee = ni.initial_fields(ecfg["shape"], 0)
+                ea = argparse.Namespace(warmup=w, steps=k)
+                extra[key] = run_variant(ea, ecfg, model, sol, ec, ee, pg, pct if pct is not None else 2)
+                extra[key]["grid"] = list(ecfg["shape"])
+                extra[key]["nsub"] = list(ecfg["nsub"])
+                extra[key]["warmup"], extra[key]["steps"] = w, k
+            except Exception as e:
+                extra[key] = {"error": str(e)[:300]}
+            torch.cuda.empty_cache()
+
     # ---- end to end through the C ABI with host buffers: every step uploads X^n from pinned host memory
     # (nks_set_state, on_device = 0: keeps the controller's history), advances one adaptive step
     # (nks_run_adaptive, retries included, exactly the device leg's work) and downloads X^{n+1}
@@ -526,9 +551,8 @@ def run_gpu(args, world, rank, local, pg):
     if not args.no_e2e and not sharded:
         import ctypes as C
         from paper_2209_08001_b200.nks import StepInfo
-        del g
-        torch.cuda.empty_cache()
         g = None
+        torch.cuda.empty_cache()
         g2 = Solver(shape, model, sol, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"], pc_reuse=1)
         g2.set_fields(c, eta, None)
         for _ in range(args.warmup):
@@ -636,7 +660,7 @@ def run_gpu(args, world, rank, local, pg):
                 "config": conf, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks,
                 "step_ms": step_stats(per_step_ms), "per_step_ms": [round(x, 3) for x in per_step_ms],
-                "parity_vs_oracle": parity, "variants": variants,
+                "parity_vs_oracle": parity, "variants": variants, "configs_3d_one_gpu": extra,
                 "kernels": kern, "kernels_micro": micro, "kernels_micro_sharded": micro_sh,
                 "phases_ms_profiled_pass": {k: round(v["ms"], 3) for k, v in phases.items()},
                 "profiled_pass_ms": prof_ms, "profiled_pass_steps": nprof,
