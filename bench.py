@@ -403,13 +403,47 @@ def run_variant(args, cfg, model, sol, c, eta, pg, pc_type):
     return out
 
 
+def run_sharded_point(args, cfg, model, sol, pg, steps, warmup):
+    """Config 3 through the z-slab sharded path (ShardedSolver: library decomposition, library-owned NCCL
+    communicator) with the ranks of pg (one rank here): W + K adaptive steps, max-over-ranks time."""
+    import torch
+    from paper_2209_08001_b200.shard import ShardedSolver
+    c, eta = ni.initial_fields(cfg["shape"], 0)
+    sh = ShardedSolver(cfg["shape"], model, sol, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"], pc_reuse=1)
+    sh.set_fields(c, eta)
+    for _ in range(warmup):
+        sh.run_adaptive(1)
+    torch.cuda.synchronize()
+    st = sh.solver.stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(pg)
+    e0.record(st)
+    recs = []
+    for _ in range(steps):
+        recs += sh.run_adaptive(1)
+    e1.record(st)
+    torch.cuda.synchronize()
+    t = max_over_ranks(pg, e0.elapsed_time(e1))
+    out = {"grid": list(cfg["shape"]), "nsub": list(cfg["nsub"]), "ranks": sh.world, "comm": sh.comm,
+           "value": steps / (t / 1e3), "unit": UNIT, "ms_per_step": t / steps, "warmup": warmup, "steps": steps,
+           "newton_its": [r["newton_its"] for r in recs], "gmres_its": [r["gmres_its"] for r in recs],
+           "dt": [r["dt"] for r in recs], "retries": [r["retries"] for r in recs]}
+    del sh
+    return out
+
+
 def run_gpu(args, world, rank, local, pg):
     import torch
     from paper_2209_08001_b200 import PC_SPECTRAL, Solver
     from paper_2209_08001_b200.build import build
     build()
     torch.cuda.set_device(local)
-    cfg = ni.CONFIGS[args.config]
+    # N > 1: the sharded 3D step (strong scaling) on config 3 (128^3) as the stated proxy of config 4 --
+    # the 2D sweep of config 2 is not sharded, and config 4's one-level RAS/BILU(0) step takes ~15 min on
+    # one GPU.  N = 1 also reports config 3 through the same sharded code path (one rank, library-owned
+    # NCCL communicator) in configs_3d_one_gpu.config3_sharded_1rank -- the N = 1 point of that curve.
+    cid = 3 if (world > 1 and args.config == 2) else args.config
+    cfg = ni.CONFIGS[cid]
     shape = cfg["shape"]
     d = len(shape)
     nf = 2 + d
@@ -529,10 +563,14 @@ def run_gpu(args, world, rank, local, pg):
         del g
         torch.cuda.empty_cache()
         g = None
-        for key, cid, pct, w, k in (("config3_ras_bilu0", 3, None, 1, 1), ("config3_spectral", 3, PC_SPECTRAL, 1, 3),
-                                    ("config4_spectral", 4, PC_SPECTRAL, 1, 2)):
+        try:
+            extra["config3_sharded_1rank"] = run_sharded_point(args, ni.CONFIGS[3], model, sol, pg, steps=2, warmup=1)
+        except Exception as e:
+            extra["config3_sharded_1rank"] = {"error": str(e)[:300]}
+        torch.cuda.empty_cache()
+        for key, ecid, pct, w, k in (("config3_spectral", 3, PC_SPECTRAL, 1, 3), ("config4_spectral", 4, PC_SPECTRAL, 1, 2)):
             try:
-                ecfg = ni.CONFIGS[cid]
+                ecfg = ni.CONFIGS[ecid]
                 ec, ee = ni.initial_fields(ecfg["shape"], 0)
                 ea = argparse.Namespace(warmup=w, steps=k)
                 extra[key] = run_variant(ea, ecfg, model, sol, ec, ee, pg, pct if pct is not None else 2)

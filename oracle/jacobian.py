@@ -22,34 +22,43 @@ from . import scheme
 CSTEP = 1e-30
 
 
-def _shift_matrix(shape, j: int, s: int):
-    """Sparse S with (S f)_i = f_{i + s e_j} (periodic), for C-order grids of ``shape``."""
+def _shift_matrix(shape, j: int, s: int, bc: str = "periodic", parity: int = 1):
+    """Sparse S with (S f)_i = f_{i + s e_j} for C-order grids of ``shape``: exactly scheme.shift applied to
+    the unit vectors (periodic wrap, or the Neumann mirror ghost, odd with parity -1)."""
     d = len(shape)
     n = int(np.prod(shape))
-    idx = np.arange(n).reshape(shape)
-    src = np.roll(idx, -s, axis=d - 1 - j).ravel()
-    return sp.csr_matrix((np.ones(n), (np.arange(n), src)), shape=(n, n))
+    idx = np.arange(n, dtype=float).reshape(shape)
+    src = scheme.shift(idx, j, s, d, bc).ravel().astype(np.int64)
+    val = np.ones(n)
+    if bc != "periodic" and parity == -1:
+        val = scheme.shift(np.ones(shape), j, s, d, bc, -1).ravel()
+    return sp.csr_matrix((val, (np.arange(n), src)), shape=(n, n))
 
 
-def grid_operators(shape, h):
-    """Dictionary of sparse operators on the periodic grid: I, Dhat[j], Lap, Splus[j], Sminus[j]."""
+def grid_operators(shape, h, bc="periodic"):
+    """Dictionary of sparse operators: I, Dhat[j] (even ghosts), Dhat_o[j] (the outer derivative of the u
+    rows: odd stress ghosts for Neumann, = Dhat for periodic), Lap, Splus[j], Sminus[j]."""
     d = len(shape)
     n = int(np.prod(shape))
     I = sp.identity(n, format="csr")
-    Sp = [_shift_matrix(shape, j, 1) for j in range(d)]
-    Sm = [_shift_matrix(shape, j, -1) for j in range(d)]
+    Sp = [_shift_matrix(shape, j, 1, bc) for j in range(d)]
+    Sm = [_shift_matrix(shape, j, -1, bc) for j in range(d)]
     Dhat = [(Sp[j] - Sm[j]) / (2 * h) for j in range(d)]
+    if bc == "periodic":
+        Dhat_o = Dhat
+    else:
+        Dhat_o = [(_shift_matrix(shape, j, 1, bc, -1) - _shift_matrix(shape, j, -1, bc, -1)) / (2 * h) for j in range(d)]
     Lap = sum((Sp[j] - 2 * I + Sm[j]) / h ** 2 for j in range(d))
-    return {"I": I, "Sp": Sp, "Sm": Sm, "Dhat": Dhat, "Lap": Lap, "n": n, "d": d}
+    return {"I": I, "Sp": Sp, "Sm": Sm, "Dhat": Dhat, "Dhat_o": Dhat_o, "Lap": Lap, "n": n, "d": d, "bc": bc}
 
 
 def div_M_grad_matrix(ops, ca, kappa, h):
     """W with W g = D M~ D g, mobility at level n."""
-    d = ops["d"]
+    d, bc = ops["d"], ops["bc"]
     W = 0 * ops["I"]
     for j in range(d):
-        mp = scheme.mobility_face(ca, kappa, j, d).ravel()
-        mm = scheme.shift(scheme.mobility_face(ca, kappa, j, d), j, -1, d).ravel()
+        mp = scheme.mobility_face(ca, kappa, j, d, bc).ravel()
+        mm = scheme.shift(scheme.mobility_face(ca, kappa, j, d, bc), j, -1, d, bc).ravel()
         W = W + (sp.diags(mp) @ (ops["Sp"][j] - ops["I"]) - sp.diags(mm) @ (ops["I"] - ops["Sm"][j])) / h ** 2
     return W.tocsr()
 
@@ -94,7 +103,7 @@ def assemble(m: scheme.Model, Xa, Xb, dt):
     """Analytic J = dF/dX^b (field-major ordering) as CSR."""
     d, h = m.d, m.h
     shape = Xb.shape[1:]
-    ops = grid_operators(shape, h)
+    ops = grid_operators(shape, h, m.bc)
     I = ops["I"]
     D = ops["Dhat"]
     Lap = ops["Lap"]
@@ -116,10 +125,11 @@ def assemble(m: scheme.Model, Xa, Xb, dt):
     blocks[1][0] = dGe_dc
     blocks[1][1] = I / dt + dGe_de
     sig = stress_operators(m, ops)
+    Do = ops["Dhat_o"]
     for Irow in range(d):
-        blocks[2 + Irow][0] = sum(D[J] @ sig[Irow][J][1] for J in range(d))
+        blocks[2 + Irow][0] = sum(Do[J] @ sig[Irow][J][1] for J in range(d))
         for M in range(d):
-            blocks[2 + Irow][2 + M] = sum(D[J] @ sig[Irow][J][0][M] for J in range(d))
+            blocks[2 + Irow][2 + M] = sum(Do[J] @ sig[Irow][J][0][M] for J in range(d))
     return sp.bmat(blocks, format="csr")
 
 

@@ -50,19 +50,19 @@ class Linearisation:
 
     def jv(self, v):
         """J v for v of shape (2+d, *grid)."""
-        m, d, h = self.m, self.m.d, self.m.h
+        m, d, h, bc = self.m, self.m.d, self.m.h, self.m.bc
         vc, ve, vu = v[0], v[1], v[2:]
-        div_u = sum(scheme.D_hat(vu[J], J, h, d) for J in range(d))
+        div_u = sum(scheme.D_hat(vu[J], J, h, d, bc) for J in range(d))
         wc = (self.a11 * vc + self.a12 * ve + (m.eps0 * self.K / 2) * (d * m.eps0 * vc - div_u)
-              - (m.gamma_c / 2) * scheme.laplacian(vc, h, d))
-        we = self.a21 * vc + self.a22 * ve - (3 * m.gamma_eta / 2) * scheme.laplacian(ve, h, d)
+              - (m.gamma_c / 2) * scheme.laplacian(vc, h, d, bc))
+        we = self.a21 * vc + self.a22 * ve - (3 * m.gamma_eta / 2) * scheme.laplacian(ve, h, d, bc)
         out = np.empty_like(v)
-        out[0] = vc / self.dt - scheme.div_M_grad(wc, self.Xa[0], m.kappa, h, d)
+        out[0] = vc / self.dt - scheme.div_M_grad(wc, self.Xa[0], m.kappa, h, d, bc)
         out[1] = ve / self.dt + we
         # sigma(v_u, v_c): the stress of eps(v_u) - eps0 v_c I (cbar0 is a constant and drops out)
         sig = scheme.stress(m, scheme.elastic_strain(m, vu, vc, 0.0))
         for I in range(d):
-            out[2 + I] = sum(scheme.D_hat(sig[I][J], J, h, d) for J in range(d))
+            out[2 + I] = sum(scheme.D_hat(sig[I][J], J, h, d, bc, -1) for J in range(d))
         return out
 
 
@@ -107,11 +107,18 @@ class SpectralPC:
                 else:
                     P[..., 2 + I, 2 + M] = -L * (m.C12 + m.C44) * s[I] * s[M]
         null = np.all(np.stack([np.abs(sj) < 1e-12 for sj in s]), axis=0)
-        for I in range(d):
-            P[null, 2 + I, 2 + I] = 1.0          # gauge modes: u block replaced by I (then zeroed below)
+        if m.bc == "periodic":
+            for I in range(d):
+                P[null, 2 + I, 2 + I] = 1.0      # gauge modes: u block replaced by I (then zeroed below)
+        else:
+            # Neumann (R38): the Fourier modes are not its eigenvectors and its gauge is not the parity
+            # classes, so the singular u block gets a regular stand-in of the elastic diagonal's scale
+            for I in range(d):
+                P[null, 2 + I, 2 + I] = -L * m.C11 / h ** 2
         Pinv = np.linalg.inv(P)
-        Pinv[null, 2:, :] = 0.0
-        Pinv[null, :, 2:] = 0.0
+        if m.bc == "periodic":
+            Pinv[null, 2:, :] = 0.0
+            Pinv[null, :, 2:] = 0.0
         self.Pinv = np.ascontiguousarray(np.moveaxis(Pinv, (-2, -1), (0, 1)))   # (nf, nf, *kshape)
 
     def apply(self, r):

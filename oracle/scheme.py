@@ -46,12 +46,13 @@ class Model:
     U4: float
     dE0: float
     S: int = 10
+    bc: str = "periodic"        # "periodic" or "neumann": Eq. (boundaryequ), reading R38
 
     @staticmethod
-    def from_dict(d: int, h: float, p: dict) -> "Model":
+    def from_dict(d: int, h: float, p: dict, bc: str = "periodic") -> "Model":
         keys = ["theta", "gamma_c", "gamma_eta", "kappa", "eps0", "C11", "C12", "C44", "Lscale",
                 "w_c", "L0", "L1", "L2", "L3", "U1", "U4", "dE0", "S"]
-        return Model(d=d, h=h, **{k: p[k] for k in keys})
+        return Model(d=d, h=h, bc=bc, **{k: p[k] for k in keys})
 
     # ---- App. B coefficients, literally -------------------------------------
     def M0(self):
@@ -79,46 +80,62 @@ class Model:
 
 
 # ----------------------------------------------------------------------------- grid operators
-# P:224-233 per axis; multi-D = per-axis sums (reading R10).
+# P:224-233 per axis; multi-D = per-axis sums (reading R10).  Boundary conditions: periodic
+# wrap, or -- homogeneous Neumann, reading R38 -- cell-centred mirror ghosts reflected about the boundary
+# face (f_{-1-k} = f_k, f_{N+k} = f_{N-1-k}), even for c, eta, u and the mobility, ODD (sign
+# flipped) for the stress in the outer derivative of the u rows (traction-free: n . sigma = 0 on the face).
 
-def shift(f, j: int, s: int, d: int):
-    """Value at i + s*e_j on the periodic grid."""
-    return np.roll(f, -s, axis=d - 1 - j)
+def shift(f, j: int, s: int, d: int, bc: str = "periodic", parity: int = 1):
+    """Value at i + s*e_j: periodic wrap, or the mirror ghost of a Neumann grid (parity -1: odd ghost)."""
+    ax = d - 1 - j
+    if bc == "periodic":
+        return np.roll(f, -s, axis=ax)
+    n = f.shape[ax]
+    idx = np.arange(n) + s
+    lo, hi = idx < 0, idx >= n
+    src = np.where(lo, -1 - idx, np.where(hi, 2 * n - 1 - idx, idx))
+    out = np.take(f, src, axis=ax)
+    if parity == -1:
+        shape = [1] * f.ndim
+        shape[ax] = n
+        out = out * np.where(lo | hi, -1.0, 1.0).reshape(shape)
+    return out
 
 
-def D_plus(f, j, h, d):
+def D_plus(f, j, h, d, bc="periodic"):
     """[D^+ f]_i = (f_{i+1} - f_i)/h (P:224)."""
-    return (shift(f, j, 1, d) - f) / h
+    return (shift(f, j, 1, d, bc) - f) / h
 
 
-def D_minus(f, j, h, d):
+def D_minus(f, j, h, d, bc="periodic"):
     """[D^- f]_i = (f_i - f_{i-1})/h (P:224)."""
-    return (f - shift(f, j, -1, d)) / h
+    return (f - shift(f, j, -1, d, bc)) / h
 
 
-def D_hat(f, j, h, d):
+def D_hat(f, j, h, d, bc="periodic", parity=1):
     """Central difference [D^ f]_i = (f_{i+1} - f_{i-1})/(2h)."""
-    return (shift(f, j, 1, d) - shift(f, j, -1, d)) / (2 * h)
+    return (shift(f, j, 1, d, bc, parity) - shift(f, j, -1, d, bc, parity)) / (2 * h)
 
 
-def laplacian(f, h, d):
+def laplacian(f, h, d, bc="periodic"):
     """[D^2 f]_i summed over axes: sum_j (f_{i+e_j} - 2 f_i + f_{i-e_j})/h^2 (R10)."""
-    return sum((shift(f, j, 1, d) - 2 * f + shift(f, j, -1, d)) / h ** 2 for j in range(d))
+    return sum((shift(f, j, 1, d, bc) - 2 * f + shift(f, j, -1, d, bc)) / h ** 2 for j in range(d))
 
 
-def mobility_face(ca, kappa, j, d):
+def mobility_face(ca, kappa, j, d, bc="periodic"):
     """M~_{i+1/2 e_j} = kappa [c_i(1-c_i) + c_{i+1}(1-c_{i+1})]/2 at level n (reading R9)."""
     m = ca * (1 - ca)
-    return kappa * (m + shift(m, j, 1, d)) / 2
+    return kappa * (m + shift(m, j, 1, d, bc)) / 2
 
 
-def div_M_grad(g, ca, kappa, h, d):
-    """[D M~ D g]_i = sum_j [M~_{i+1/2}(g_{i+1}-g_i) - M~_{i-1/2}(g_i-g_{i-1})]/h^2."""
+def div_M_grad(g, ca, kappa, h, d, bc="periodic"):
+    """[D M~ D g]_i = sum_j [M~_{i+1/2}(g_{i+1}-g_i) - M~_{i-1/2}(g_i-g_{i-1})]/h^2.
+    Neumann: the mirror ghost makes the flux through a boundary face vanish (n . M grad = 0)."""
     out = 0
     for j in range(d):
-        mp = mobility_face(ca, kappa, j, d)
-        mm = shift(mp, j, -1, d)
-        out = out + (mp * (shift(g, j, 1, d) - g) - mm * (g - shift(g, j, -1, d))) / h ** 2
+        mp = mobility_face(ca, kappa, j, d, bc)
+        mm = shift(mp, j, -1, d, bc)
+        out = out + (mp * (shift(g, j, 1, d, bc) - g) - mm * (g - shift(g, j, -1, d, bc))) / h ** 2
     return out
 
 
@@ -197,7 +214,7 @@ def E2(m: Model, c, eta):
 def strain(m: Model, u):
     """eps_IJ = (D^_J u_I + D^_I u_J)/2 (reading R11 keeps I,J <= d)."""
     d = m.d
-    du = [[D_hat(u[I], J, m.h, d) for J in range(d)] for I in range(d)]   # du[I][J] = D^_J u_I
+    du = [[D_hat(u[I], J, m.h, d, m.bc) for J in range(d)] for I in range(d)]   # du[I][J] = D^_J u_I
     return [[0.5 * (du[I][J] + du[J][I]) for J in range(d)] for I in range(d)]
 
 
@@ -238,8 +255,8 @@ def E4(m: Model, c, eta):
     d, h = m.d, m.h
     out = 0
     for j in range(d):
-        out = out + m.gamma_c / 2 * (D_plus(c, j, h, d) ** 2 + D_minus(c, j, h, d) ** 2) / 2
-        out = out + 3 * m.gamma_eta / 2 * (D_plus(eta, j, h, d) ** 2 + D_minus(eta, j, h, d) ** 2) / 2
+        out = out + m.gamma_c / 2 * (D_plus(c, j, h, d, m.bc) ** 2 + D_minus(c, j, h, d, m.bc) ** 2) / 2
+        out = out + 3 * m.gamma_eta / 2 * (D_plus(eta, j, h, d, m.bc) ** 2 + D_minus(eta, j, h, d, m.bc) ** 2) / 2
     return out
 
 
@@ -319,7 +336,7 @@ def G4(m: Model, Xa, Xb):
     """G~^4 = (-gamma_c D^2 c^{n+1/2}, -3 gamma_eta D^2 eta^{n+1/2})."""
     ch = (Xa[0] + Xb[0]) / 2
     eh = (Xa[1] + Xb[1]) / 2
-    return -m.gamma_c * laplacian(ch, m.h, m.d), -3 * m.gamma_eta * laplacian(eh, m.h, m.d)
+    return -m.gamma_c * laplacian(ch, m.h, m.d, m.bc), -3 * m.gamma_eta * laplacian(eh, m.h, m.d, m.bc)
 
 
 def G_S(m: Model, Xa, Xb, cbar0):
@@ -341,11 +358,11 @@ def residual(m: Model, Xa, Xb, dt, cbar0):
     d = m.d
     gc, ge = G_S(m, Xa, Xb, cbar0)
     F = np.empty_like(Xb)
-    F[0] = (Xb[0] - Xa[0]) / dt - div_M_grad(gc, Xa[0], m.kappa, m.h, d)
+    F[0] = (Xb[0] - Xa[0]) / dt - div_M_grad(gc, Xa[0], m.kappa, m.h, d, m.bc)
     F[1] = (Xb[1] - Xa[1]) / dt + ge
     sig = stress(m, elastic_strain(m, Xb[2:], Xb[0], cbar0))
-    for I in range(d):
-        F[2 + I] = sum(D_hat(sig[I][J], J, m.h, d) for J in range(d))
+    for I in range(d):     # Neumann: odd stress ghosts across the J faces (traction-free, reading R38)
+        F[2 + I] = sum(D_hat(sig[I][J], J, m.h, d, m.bc, -1) for J in range(d))
     return F
 
 

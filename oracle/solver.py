@@ -23,10 +23,13 @@ from . import jacobian, scheme
 
 # ----------------------------------------------------------------------------- gauge
 
-def sublattice_ids(shape):
-    """Class id of each point: bits = parity of the coordinate along each EVEN-length axis."""
+def sublattice_ids(shape, bc="periodic"):
+    """Class id of each point: bits = parity of the coordinate along each EVEN-length axis.  Neumann
+    (reading R38): the elastic null space is the translations only -- one class."""
     d = len(shape)
     ids = np.zeros(shape, dtype=np.int64)
+    if bc != "periodic":
+        return ids, 1
     coords = np.meshgrid(*[np.arange(n) for n in shape], indexing="ij")
     bit = 0
     for j in range(d):                       # j = 0 is x (array axis d-1)
@@ -37,11 +40,43 @@ def sublattice_ids(shape):
     return ids, 1 << bit
 
 
-def gauge_project(X):
-    """Subtract, for every u component, its mean on each parity sub-lattice (reading R14)."""
+def neumann_rotations(shape):
+    """Discrete rigid rotations of a Neumann grid (reading R38): for every axis pair (I, J) whose extents are
+    both even, u_I = s(x_J), u_J = -s(x_I) with the staircase s(k) = floor((k + 1)/2) has D^ s = 1/(2h)
+    everywhere under the mirror ghosts, so its strain vanishes.  Returned orthonormalised against the
+    translations and each other, as (d, *shape) arrays."""
+    d = len(shape)
+    coords = np.meshgrid(*[np.arange(n) for n in shape], indexing="ij")
+    modes = []
+    for I in range(d):
+        for J in range(I + 1, d):
+            aI, aJ = d - 1 - I, d - 1 - J          # array axes of coordinate axes I, J
+            if shape[aI] % 2 or shape[aJ] % 2:
+                continue
+            r = np.zeros((d,) + tuple(shape))
+            r[I] = (coords[aJ] + 1) // 2
+            r[J] = -((coords[aI] + 1) // 2)
+            for K in range(d):
+                r[K] -= r[K].mean()                # orthogonal to the translations
+            for q in modes:
+                r -= np.sum(r * q) * q
+            modes.append(r / np.sqrt(np.sum(r * r)))
+    return modes
+
+
+def gauge_project(X, bc="periodic"):
+    """Subtract, for every u component, its mean on each parity sub-lattice (reading R14).  Neumann
+    (reading R38): the mean of every component (translations) and the discrete rotation modes."""
     d = X.ndim - 1
     shape = X.shape[1:]
-    ids, ncls = sublattice_ids(shape)
+    if bc != "periodic":
+        Y = X.copy()
+        for I in range(d):
+            Y[2 + I] -= Y[2 + I].mean()
+        for r in neumann_rotations(shape):
+            Y[2:] -= np.sum(Y[2:] * r) * r
+        return Y
+    ids, ncls = sublattice_ids(shape, bc)
     Y = X.copy()
     for I in range(d):
         u = Y[2 + I]
@@ -51,9 +86,22 @@ def gauge_project(X):
     return Y
 
 
-def pinned_rows(shape, d):
-    """Row indices (field-major) of one u_I row per (component, sub-lattice): the first point of the class."""
-    ids, ncls = sublattice_ids(shape)
+def pinned_rows(shape, d, bc="periodic"):
+    """Row indices (field-major) of one u_I row per (component, sub-lattice): the first point of the class.
+    Neumann: u_I at the first point per component, and per rotation mode (I, J) u_J at x_I = 1 (the mode's
+    u_J differs there from the first point, so the pins fix it)."""
+    if bc != "periodic":
+        n = int(np.prod(shape))
+        rows = [(2 + I) * n for I in range(d)]
+        for I in range(d):
+            for J in range(I + 1, d):
+                if shape[d - 1 - I] % 2 or shape[d - 1 - J] % 2:
+                    continue
+                idx = [0] * d
+                idx[d - 1 - I] = 1
+                rows.append((2 + J) * n + int(np.ravel_multi_index(tuple(idx), shape)))
+        return rows
+    ids, ncls = sublattice_ids(shape, bc)
     n = int(np.prod(shape))
     flat = ids.ravel()
     rows = []
@@ -78,9 +126,9 @@ def pin(A, b, rows):
 
 def elastic_block(m: scheme.Model, shape):
     """Sparse operator A_uu (u rows, u cols) and A_uc with F_u = A_uu u + A_uc (c - cbar0)."""
-    ops = jacobian.grid_operators(shape, m.h)
+    ops = jacobian.grid_operators(shape, m.h, m.bc)
     sig = jacobian.stress_operators(m, ops)
-    D = ops["Dhat"]
+    D = ops["Dhat_o"]
     d = m.d
     Auu = sp.bmat([[sum(D[J] @ sig[I][J][0][M] for J in range(d)) for M in range(d)] for I in range(d)],
                   format="csr")
@@ -95,12 +143,12 @@ def init_displacement(m: scheme.Model, c, cbar0):
     n = c.size
     Auu, Auc = elastic_block(m, shape)
     b = -(Auc @ (c - cbar0).ravel())
-    rows = [r - 2 * n for r in pinned_rows(shape, d)]
+    rows = [r - 2 * n for r in pinned_rows(shape, d, m.bc)]
     A, b = pin(Auu, b, rows)
     u = spla.spsolve(A, b).reshape((d,) + shape)
     X = np.zeros((2 + d,) + shape)
     X[2:] = u
-    return gauge_project(X)[2:]
+    return gauge_project(X, m.bc)[2:]
 
 
 def init_displacement_fft(m: scheme.Model, c, cbar0):
@@ -147,7 +195,7 @@ def norm(F):
 def direct_linsolve(m: scheme.Model, Xa, X, dt, cbar0, b, fnorm):
     """J S = b by the gauge-pinned sparse direct LU (reading R14): exact up to rounding."""
     J = jacobian.assemble(m, Xa, X, dt)
-    A, bb = pin(J, b.ravel(), pinned_rows(X.shape[1:], m.d))
+    A, bb = pin(J, b.ravel(), pinned_rows(X.shape[1:], m.d, m.bc))
     return spla.spsolve(A, bb).reshape(X.shape)
 
 
@@ -174,7 +222,7 @@ def newton_step(m: scheme.Model, Xa, dt, cbar0, sol: dict, X0=None, linsolve=Non
         if it == sol["newton_maxit"]:
             info["reason"] = "newton_maxit"
             return Xa.copy(), info
-        S = solve(m, Xa, X, dt, cbar0, gauge_project(-F), hist[-1])
+        S = solve(m, Xa, X, dt, cbar0, gauge_project(-F, m.bc), hist[-1])
         if S is None:
             info["reason"] = "linear_solver"
             return Xa.copy(), info
@@ -193,7 +241,7 @@ def newton_step(m: scheme.Model, Xa, dt, cbar0, sol: dict, X0=None, linsolve=Non
             info["reason"] = "line_search"
             return Xa.copy(), info
         info["lambdas"].append(lam)
-        X = gauge_project(Xt)
+        X = gauge_project(Xt, m.bc)
         F = Ft
         hist.append(ft)
         info["newton_its"] = it + 1
