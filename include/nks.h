@@ -86,6 +86,10 @@ typedef struct {
                      /* nks_decompose() fills a rank's slab grid from the global one.              */
   int32_t z_offset;  /* zghost > 0: global z of this slab's first own plane                      */
   int32_t nz_global; /* zghost > 0: planes of the global periodic grid                            */
+  int32_t bc;        /* 0: periodic.  1: homogeneous Neumann, Eq. (boundaryequ)    */
+                     /* (reading R38: cell-centred mirror ghosts; traction-free u through odd stress */
+                     /* ghosts; gauge = translations + discrete rotations).  Single-GPU states with */
+                     /* pc_type NONE or SPECTRAL; nks_set_fields then needs u (no FFT u^0).        */
 } nks_grid;
 
 /* ---- communication callbacks of a z-sharded state --------------------------------

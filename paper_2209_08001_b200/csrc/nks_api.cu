@@ -71,6 +71,12 @@ void spectral_free(void* p);
 void launch_spectral_setup(void* plan, const DevParams& dp, int nf, const double* Xa, const double* jac4, double* part,
                            double* means, void* pinv, cudaStream_t s);
 int launch_spectral_apply(void* plan, int nf, const double* r, double* z, const void* pinv, void* spec, cudaStream_t s);
+// stencil_neumann.cu
+void launch_residual_neumann(const DevParams& P, const double* Xa, const double* Xb, const double* Ta, double* F,
+                             cudaStream_t s);
+void launch_jv_neumann(const DevParams& P, const double* Xa, const double* jac4, const double* v, double* out,
+                       cudaStream_t s);
+void launch_gauge_neumann(const DevParams& P, double* X, double* part, double* out, cudaStream_t s);
 // comm.cu
 int slab_decompose(const nks_grid& global, int pc_type, int rank, int nranks, nks_grid& local, int& z_offset);
 int nccl_unique_id(uint8_t id[128]);
@@ -133,6 +139,10 @@ const char* validate(const nks_grid* g, const nks_params* p) {
   if (g->zghost > 0 && (p->pc_type == NKS_PC_AS_BILU0 || p->pc_type == NKS_PC_RRAS_BILU0))
     return "z-slab states support pc_type NONE or RAS (AS / RRAS need a reverse halo exchange)";
   if (g->zghost != 0 && (g->zghost < 2 || g->zghost > 8)) return "zghost must be 0 or 2..8";
+  if (g->bc != 0 && g->bc != 1) return "bc must be 0 (periodic) or 1 (Neumann)";
+  if (g->bc == 1 && g->zghost > 0) return "Neumann boundaries: single-GPU states only";
+  if (g->bc == 1 && p->pc_type != NKS_PC_NONE && p->pc_type != NKS_PC_SPECTRAL)
+    return "Neumann boundaries: pc_type NONE or SPECTRAL (the Schwarz boxes are periodic)";
   if (g->zghost > 0) {
     if (g->dim != 3) return "z-slab states (zghost > 0) are 3D";
     const int own = g->n[2] - 2 * g->zghost;
@@ -227,6 +237,7 @@ DevParams make_devparams(const nks_grid& g, const nks_params& p) {
   P.dim = g.dim;
   P.nx = g.n[0]; P.ny = g.n[1]; P.nz = g.n[2];
   P.zg = g.zghost;
+  P.bc = g.bc;
   P.N = (long long)g.n[0] * g.n[1] * g.n[2];
   P.h = g.h;
   P.inv_h2 = 1.0 / (g.h * g.h);
@@ -359,7 +370,8 @@ void clean(nks_state* st, double* vec, int nf) {
 
 void residual(nks_state* st, const double* Xb, double* F) {
   PhaseScope ps(st, PH_F);
-  launch_residual_tiled(st->dp, st->Xn, Xb, st->Ta, F, st->stream);
+  if (st->dp.bc) launch_residual_neumann(st->dp, st->Xn, Xb, st->Ta, F, st->stream);
+  else launch_residual_tiled(st->dp, st->Xn, Xb, st->Ta, F, st->stream);
   count_launch(st, 1);
 }
 
@@ -379,6 +391,12 @@ void norm_adm(nks_state* st, const double* F, const double* X, double& nrm, doub
 
 void gauge(nks_state* st, double* X) {
   PhaseScope ps(st, PH_RED);
+  if (st->dp.bc) {          // Neumann (single state): translations + discrete rotations (reading R38)
+    launch_gauge_neumann(st->dp, X, st->red_part, st->red_out + 128, st->stream);
+    comm_allreduce(st, st->red_out + 128, 0);
+    count_launch(st, 3);
+    return;
+  }
   const int nsum = launch_gauge_sums(st->dp, X, st->red_part, st->red_out + 128, st->stream);
   comm_allreduce(st, st->red_out + 128, nsum);     // global sub-lattice sums (slab: own planes of every rank)
   launch_gauge_apply(st->dp, X, st->red_out + 128, st->stream);
@@ -387,7 +405,8 @@ void gauge(nks_state* st, double* X) {
 
 void jv(nks_state* st, const double* v, double* out) {
   PhaseScope ps(st, PH_JV);
-  launch_jv_tiled(st->dp, st->Xn, st->jac4, v, out, st->stream);
+  if (st->dp.bc) launch_jv_neumann(st->dp, st->Xn, st->jac4, v, out, st->stream);
+  else launch_jv_tiled(st->dp, st->Xn, st->jac4, v, out, st->stream);
   count_launch(st, 1);
 }
 
@@ -984,6 +1003,7 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, int32_t ra
 nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, const double* u, int32_t on_device) {
   if (!st || !c || !eta) return NKS_E_INVALID;
   if (slab(st) && !u) return NKS_E_INVALID;     // the FFT u^0 is a whole-grid operation
+  if (st->dp.bc && !u) return NKS_E_INVALID;    // u^0 by FFT is periodic only; Neumann takes the caller's u
   return guarded(st, [&]() -> nks_status {
     const long long N = st->N;
     CK(cudaMemcpyAsync(st->Xn, c, N * sizeof(double), kind_in(on_device), st->stream));

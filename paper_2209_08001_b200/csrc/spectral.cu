@@ -118,8 +118,11 @@ __global__ void k_spec_build(DevParams P, const double* __restrict__ means, int 
         A[2 + I][2 + M] = {v, 0.0};
       }
     }
+    // gauge modes: periodic -- u block -> I, zeroed below; Neumann (reading R38) -- the Fourier modes are not
+    // its eigenvectors and its gauge is not the parity classes: a regular stand-in of the elastic diagonal's
+    // scale, nothing zeroed (the preconditioner is approximate there, which only costs GMRES iterations)
     if (null)
-      for (int I = 0; I < d; ++I) A[2 + I][2 + I] = {1.0, 0.0};     // gauge modes: u block -> I, zeroed below
+      for (int I = 0; I < d; ++I) A[2 + I][2 + I] = {P.bc ? -P.Ls * P.C11 * P.inv_h2 : 1.0, 0.0};
     // Gauss-Jordan with partial pivoting on the complex NF x NF matrix
     cplx B[NF][NF];
     for (int r = 0; r < NF; ++r)
@@ -146,7 +149,7 @@ __global__ void k_spec_build(DevParams P, const double* __restrict__ means, int 
     }
     for (int r = 0; r < NF; ++r)
       for (int c = 0; c < NF; ++c) {
-        const bool zero = null && (r >= 2 || c >= 2);
+        const bool zero = null && !P.bc && (r >= 2 || c >= 2);
         pinv[(long long)(r * NF + c) * Nh + t] = zero ? make_cuDoubleComplex(0.0, 0.0)
                                                       : make_cuDoubleComplex(B[r][c].re * invN, B[r][c].im * invN);
       }

@@ -10,11 +10,16 @@
 namespace nks {
 
 __device__ __forceinline__ int wrapc(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
+__device__ __forceinline__ int mirc(int v, int n) { return v < 0 ? -1 - v : (v >= n ? 2 * n - 1 - v : v); }
 
+// Index of a (possibly ghost) neighbour: periodic wrap, or the Neumann mirror ghost (bc = 1, reading R38),
+// which makes D^ / D+ / D- / the Laplacian of the level prep and the energy take the boundary closure.
 struct Geo {
   int nx, ny, nz;
   long long N;
+  int bc;
   __device__ __forceinline__ long long id(int x, int y, int z) const {
+    if (bc) return ((long long)mirc(z, nz) * ny + mirc(y, ny)) * nx + mirc(x, nx);
     return ((long long)wrapc(z, nz) * ny + wrapc(y, ny)) * nx + wrapc(x, nx);
   }
 };
@@ -39,7 +44,7 @@ __device__ __forceinline__ double div_hat(const Geo& g, const double* __restrict
 // -------------------------------------------------------------------------------------- K3
 template <int DIM>
 __global__ void k_level_prep(DevParams P, const double* __restrict__ X, double* __restrict__ T) {
-  const Geo g{P.nx, P.ny, P.nz, P.N};
+  const Geo g{P.nx, P.ny, P.nz, P.N, P.bc};
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P.N; i += (long long)gridDim.x * blockDim.x) {
     const int x = (int)(i % P.nx);
     const int y = (int)((i / P.nx) % P.ny);
@@ -135,7 +140,7 @@ __global__ void k_norm_admissible(long long N, int nf, const double* __restrict_
 // Energy parts E1..E4 and sum c.
 template <int DIM>
 __global__ void k_energy(DevParams P, const double* __restrict__ X, double* __restrict__ part) {
-  const Geo g{P.nx, P.ny, P.nz, P.N};
+  const Geo g{P.nx, P.ny, P.nz, P.N, P.bc};
   const long long N = P.N;
   const double* c_ = X;
   const double* e_ = X + N;

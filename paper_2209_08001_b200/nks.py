@@ -25,7 +25,8 @@ PHASES = ["residual", "jv", "ras_apply", "assemble", "factor", "gmres_vec", "red
 
 class Grid(C.Structure):
     _fields_ = [("dim", C.c_int32), ("n", C.c_int32 * 3), ("h", C.c_double), ("nsub", C.c_int32 * 3),
-                ("overlap", C.c_int32), ("zghost", C.c_int32), ("z_offset", C.c_int32), ("nz_global", C.c_int32)]
+                ("overlap", C.c_int32), ("zghost", C.c_int32), ("z_offset", C.c_int32), ("nz_global", C.c_int32),
+                ("bc", C.c_int32)]
 
 
 class Params(C.Structure):
@@ -118,7 +119,7 @@ class NKSError(RuntimeError):
         self.status = status
 
 
-def make_grid(shape, h=0.25, nsub=None, overlap=2, zghost=0, z_offset=0, nz_global=0) -> Grid:
+def make_grid(shape, h=0.25, nsub=None, overlap=2, zghost=0, z_offset=0, nz_global=0, bc=0) -> Grid:
     """shape and nsub in C order: (ny, nx) or (nz, ny, nx)."""
     d = len(shape)
     g = Grid()
@@ -135,6 +136,7 @@ def make_grid(shape, h=0.25, nsub=None, overlap=2, zghost=0, z_offset=0, nz_glob
     g.zghost = int(zghost)
     g.z_offset = int(z_offset)
     g.nz_global = int(nz_global)
+    g.bc = int(bc)
     return g
 
 
@@ -182,7 +184,7 @@ class Solver:
 
     def __init__(self, shape, model: dict, solver: dict, h=0.25, nsub=None, overlap=2,
                  pc_type=PC_RAS_BILU0, pc_reuse=1, device=None, zghost=0, grid: Grid = None, rank=0, nranks=1,
-                 nccl_id: bytes = None):
+                 nccl_id: bytes = None, bc=0):
         """shape: the (local) grid in C order; `grid` overrides the grid built from shape/nsub/overlap/zghost
         (a slab from `decompose`).  nccl_id (slab states): the library creates its own NCCL communicator."""
         import torch
@@ -195,7 +197,7 @@ class Solver:
         self.nf = 2 + self.d
         self.N = int(np.prod(shape))
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.grid = grid if grid is not None else make_grid(shape, h, nsub, overlap, zghost)
+        self.grid = grid if grid is not None else make_grid(shape, h, nsub, overlap, zghost, bc=bc)
         self.rank, self.nranks = int(rank), int(nranks)
         self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         self.params = make_params(model, solver, pc_type, pc_reuse)

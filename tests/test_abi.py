@@ -58,7 +58,8 @@ int main(void) {
   printf("nks_grid %zu\n", sizeof(nks_grid));
   printf("nks_params %zu\n", sizeof(nks_params));
   printf("nks_step_info %zu\n", sizeof(nks_step_info));
-  F(nks_grid, h) F(nks_grid, nsub) F(nks_grid, overlap) F(nks_grid, zghost)
+  F(nks_grid, h) F(nks_grid, nsub) F(nks_grid, overlap) F(nks_grid, zghost) F(nks_grid, z_offset)
+  F(nks_grid, nz_global) F(nks_grid, bc)
   F(nks_params, S) F(nks_params, newton_rtol) F(nks_params, pc_reuse) F(nks_params, ls_alpha)
   F(nks_params, zeta) F(nks_params, xd_norm) F(nks_params, factor_fp32) F(nks_params, gmres_stall_cycles)
   F(nks_params, ilu_level)

@@ -1,0 +1,99 @@
+"""Homogeneous Neumann boundaries (Eq. (boundaryequ); reading R38) on the GPU
+against the oracle (oracle/ with Model(bc="neumann"), pinned in tests/test_oracle_neumann.py): F and J.v
+element by element, energy, the gauge (translations + discrete rotations), and whole steps at the
+BASELINE bar (fields rel. L2 <= 1e-8, energy rel. <= 1e-10, mass drift <= 1e-12)."""
+import numpy as np
+import pytest
+
+import nks_inputs as ni
+from oracle import jacobian, scheme, solver
+
+pytestmark = pytest.mark.gpu
+
+MODEL = ni.model_default()
+SOL = ni.solver_default()
+
+
+def gpu(shape, pc_type=0):
+    from paper_2209_08001_b200 import Solver
+    return Solver(shape, MODEL, SOL, h=0.25, nsub=(1,) * len(shape), overlap=2, pc_type=pc_type, bc=1)
+
+
+def omodel(d):
+    return scheme.Model.from_dict(d, 0.25, MODEL, bc="neumann")
+
+
+def states(shape, seed=0):
+    d = len(shape)
+    ca, ea = ni.initial_fields(shape, seed)
+    ua = ni.random_displacement(d, shape, seed + 2, 1e-3)
+    Xa = solver.gauge_project(np.concatenate([ca[None], ea[None], ua]), "neumann")
+    cb, eb = ni.perturbed_state(ca, ea, seed + 1, 2e-3)
+    Xb = np.concatenate([cb[None], eb[None], Xa[2:] + ni.random_displacement(d, shape, seed + 3, 1e-4)])
+    return Xa, Xb
+
+
+def rel(a, b):
+    return [float(np.abs(a[f] - b[f]).max() / max(np.abs(b[f]).max(), 1e-300)) for f in range(a.shape[0])]
+
+
+@pytest.mark.parametrize("shape", [(14, 18), (9, 7, 11), (6, 8, 8)])
+def test_neumann_residual_jv_energy_parity(shape):
+    d = len(shape)
+    m = omodel(d)
+    Xa, Xb = states(shape)
+    g = gpu(shape)
+    g.set_fields(Xa[0], Xa[1], Xa[2:])
+    cbar = Xa[0].mean()
+    for dt in (0.01, 1.3):
+        Fg = g.eval_residual(Xb, dt).cpu().numpy()
+        Fo = scheme.residual(m, Xa, Xb, dt, cbar)
+        assert max(rel(Fg, Fo)) < 1e-12, rel(Fg, Fo)
+        v = ni.random_direction(2 + d, shape, 7)
+        Jg = g.eval_jv(Xb, v, dt).cpu().numpy()
+        Jo = jacobian.jv(m, Xa, Xb, dt, v)
+        assert max(rel(Jg, Jo)) < 1e-12, rel(Jg, Jo)
+    parts, mass = g.energy()
+    po = scheme.energy_parts(m, Xa, cbar)
+    for a, b in zip(parts, po):
+        assert a == pytest.approx(b, rel=1e-12, abs=1e-12)
+    assert mass == pytest.approx(scheme.mass(m, Xa), rel=1e-13)
+
+
+@pytest.mark.parametrize("shape", [(12, 16), (11, 16), (6, 8, 4)])
+def test_neumann_gauge(shape):
+    """set_fields projects u onto the Neumann gauge exactly like the oracle: zero mean per component and
+    no component along the discrete rotations of even-extent axis pairs."""
+    d = len(shape)
+    c, eta = ni.initial_fields(shape, 1)
+    u = ni.random_displacement(d, shape, 4, 1e-2) + 0.3
+    g = gpu(shape)
+    g.set_fields(c, eta, u)
+    Xg = g.get_state()
+    Xo = solver.gauge_project(np.concatenate([c[None], eta[None], u]), "neumann")
+    np.testing.assert_allclose(Xg[2:], Xo[2:], rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("shape,pc,dts", [((16, 20), 0, [0.01, 0.5]), ((15, 20), 5, [0.01, 2.0]),
+                                          ((6, 8, 8), 5, [0.01, 0.3])])
+def test_neumann_step_parity(shape, pc, dts):
+    """Whole NKS steps with Neumann boundaries (pc NONE or the spectral preconditioner) against the oracle's
+    exact Newton with the gauge-pinned direct LU; u^0 from the oracle's pinned equilibrium solve."""
+    d = len(shape)
+    m = omodel(d)
+    c, eta = ni.initial_fields(shape, 0)
+    cbar = c.mean()
+    Xo = np.concatenate([c[None], eta[None], solver.init_displacement(m, c, cbar)])
+    g = gpu(shape, pc)
+    g.set_fields(c, eta, Xo[2:])
+    mass0 = scheme.mass(m, Xo)
+    for dt in dts:
+        Xo, info_o = solver.newton_step(m, Xo, dt, cbar, SOL)
+        assert info_o["converged"]
+        info_g = g.step(dt)
+        Xg = g.get_state()
+        r = [float(np.linalg.norm(Xg[f] - Xo[f]) / np.linalg.norm(Xo[f])) for f in range(2 + d)]
+        assert max(r) <= 1e-8, (dt, r)
+        assert info_g["energy"] == pytest.approx(scheme.energy(m, Xo, cbar), rel=1e-10)
+        assert abs(info_g["mass"] - mass0) <= 1e-12 * abs(mass0)
+        assert info_g["newton_its"] == info_o["newton_its"]
