@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--no-micro", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="3D sharded runs: strong (a fixed grid split over N ranks) or weak (128^3 per rank)")
     ap.add_argument("--sharded", action="store_true",
                     help="3D configs: run the z-slab sharded NKS step (ShardedSolver, NCCL halos/allreduces); "
                          "implied for 3D configs at N > 1")
@@ -392,7 +394,8 @@ def run_variant(args, cfg, model, sol, c, eta, pg, pc_type):
     t_ms = max_over_ranks(pg, evs[0].elapsed_time(evs[-1]))
     per = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
     out = {"pc": {5: "spectral (cuFFT, mean-coefficient inverse per wave number)",
-                  2: "left-RAS, point-block ILU(0)"}.get(pc_type, pc_type),
+                  2: "left-RAS, point-block ILU(0)",
+                  6: "two-level: spectral global correction + left-RAS 4x4 boxes delta=2 BILU(0)"}.get(pc_type, pc_type),
            "value": args.steps / (t_ms / 1e3), "unit": UNIT, "ms_per_step": t_ms / args.steps, "step_ms": step_stats(per),
            "newton_its": [r["newton_its"] for r in recs], "gmres_its": [r["gmres_its"] for r in recs],
            "dt": [r["dt"] for r in recs], "retries": [r["retries"] for r in recs],
@@ -443,7 +446,14 @@ def run_gpu(args, world, rank, local, pg):
     # one GPU.  N = 1 also reports config 3 through the same sharded code path (one rank, library-owned
     # NCCL communicator) in configs_3d_one_gpu.config3_sharded_1rank -- the N = 1 point of that curve.
     cid = 3 if (world > 1 and args.config == 2) else args.config
-    cfg = ni.CONFIGS[cid]
+    cfg = dict(ni.CONFIGS[cid])
+    if args.scaling == "weak" and len(cfg["shape"]) == 3:
+        # weak scaling (128^3 per GPU): the per-rank block stacked along z, with its
+        # box layers, so every rank owns one 128^3 block of 8x8x8 boxes whatever N
+        b = ni.CONFIGS[3]
+        cfg["shape"] = (b["shape"][0] * world,) + tuple(b["shape"][1:])
+        cfg["nsub"] = (b["nsub"][0] * world,) + tuple(b["nsub"][1:])
+        cfg["name"] = f"3d_128_weak_x{world}"
     shape = cfg["shape"]
     d = len(shape)
     nf = 2 + d
@@ -553,6 +563,7 @@ def run_gpu(args, world, rank, local, pg):
     variants = {}
     if not sharded and not args.no_variants:
         variants["spectral_pc"] = run_variant(args, cfg, model, sol, c, eta, pg, PC_SPECTRAL)
+        variants["two_level_ras_spectral"] = run_variant(args, cfg, model, sol, c, eta, pg, 6)
 
     # ---- the 3D configurations on this GPU, a few steps each: config 3
     # (128^3, RAS 8x8x8 boxes, BILU(0)) with the configured preconditioner and with the spectral one;
@@ -694,7 +705,7 @@ def run_gpu(args, world, rank, local, pg):
         conf["gmres_stall_cycles"] = sol["gmres_stall_cycles"]
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": (args.scaling if sharded else "weak"), "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": conf, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks,
                 "step_ms": step_stats(per_step_ms), "per_step_ms": [round(x, 3) for x in per_step_ms],

@@ -63,7 +63,10 @@ enum { NKS_REASON_NONE = 0, NKS_REASON_NEWTON_MAXIT = 1, NKS_REASON_LINE_SEARCH 
  * AS and RRAS sum the overlapping boxes' contributions in a fixed box order (deterministic); they are
  * single-state only (a z-slab state would need a reverse halo exchange) and use the level-synchronous
  * subdomain solve. */
-enum { NKS_PC_NONE = 0, NKS_PC_RAS_BILU0 = 2, NKS_PC_AS_BILU0 = 3, NKS_PC_RRAS_BILU0 = 4, NKS_PC_SPECTRAL = 5 };
+enum { NKS_PC_NONE = 0, NKS_PC_RAS_BILU0 = 2, NKS_PC_AS_BILU0 = 3, NKS_PC_RRAS_BILU0 = 4, NKS_PC_SPECTRAL = 5,
+       NKS_PC_RAS_SPECTRAL = 6 };
+/* NKS_PC_RAS_SPECTRAL: two-level -- the spectral preconditioner below as a global (coarse) correction, then
+ * left-RAS/BILU(0) on the remaining residual: z1 = S r, z = z1 + RAS(r - J z1).  Periodic single states. */
 /* NKS_PC_SPECTRAL (not the paper's): the inverse of J with its variable coefficients
  * (the pointwise partials of G1 + G2S, the level-n mobility) replaced by their grid means, applied per
  * wave number with cuFFT -- exact for a uniform state, so GMRES needs few iterations while the fields are

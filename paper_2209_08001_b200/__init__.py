@@ -4,5 +4,5 @@ The product is the C-ABI library ``lib/libnks.so`` (include/nks.h); ``nks.py`` i
 ctypes binding.  There is no CPU fallback: without the built library or a CUDA device the
 binding raises.
 """
-from .nks import (PC_AS_BILU0, PC_NONE, PC_RAS_BILU0, PC_RRAS_BILU0, PC_SPECTRAL, Grid, NKSError, Params, Solver, StepInfo,  # noqa: F401
+from .nks import (PC_AS_BILU0, PC_NONE, PC_RAS_BILU0, PC_RRAS_BILU0, PC_RAS_SPECTRAL, PC_SPECTRAL, Grid, NKSError, Params, Solver, StepInfo,  # noqa: F401
                   decompose, load_library, make_grid, make_params, unique_id, version)

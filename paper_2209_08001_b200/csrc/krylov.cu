@@ -98,8 +98,18 @@ __global__ void __launch_bounds__(256) k_dcgs_dot(long long n, int nk, const dou
   for (int base = 0; base < kDOut; base += 32) {
     const int k = base + lane;
     double a = 0.0;
-    if (k < kDOut)
-      for (int blk = wid; blk < (int)gridDim.x; blk += 8) a += part[(long long)blk * kDOut + k];
+    if (k < kDOut) {
+      // independent loads, two accumulators: the block count (<= 2 per SM) keeps this tail short
+      double a2 = 0.0;
+      int blk = wid;
+#pragma unroll 4
+      for (; blk + 8 < (int)gridDim.x; blk += 16) {
+        a += part[(long long)blk * kDOut + k];
+        a2 += part[(long long)(blk + 8) * kDOut + k];
+      }
+      if (blk < (int)gridDim.x) a += part[(long long)blk * kDOut + k];
+      a += a2;
+    }
     if (k < kDOut) sw[wid][k] = a;
   }
   __syncthreads();
@@ -226,7 +236,8 @@ void launch_dcgs_dot(long long n, int nk, const double* V, long long ld, double*
   const double* w = u + ld;
   const bool v2 = vec2(n, ld);
   const long long m = v2 ? n / 2 : n;
-  const int nb = (int)std::min<long long>((m + 31) / 32, kRedBlocks);   // part holds kRedBlocks x kDOut
+  // 2 blocks of 8 streaming warps per SM saturate HBM; more blocks only lengthen the last block's tail sum
+  const int nb = (int)std::min<long long>((m + 31) / 32, 2 * 148);
   if (v2) {
     if (nk <= 8) k_dcgs_dot<8, 2><<<nb, 256, 0, s>>>(n, nk, V, ld, u, w, part, out, counter);
     else if (nk <= 16) k_dcgs_dot<16, 2><<<nb, 256, 0, s>>>(n, nk, V, ld, u, w, part, out, counter);
@@ -245,7 +256,7 @@ void launch_dcgs_dot_u(long long n, int nk, const double* V, long long ld, doubl
   const double* u = V + (long long)nk * ld;
   const bool v2 = vec2(n, ld);
   const long long m = v2 ? n / 2 : n;
-  const int nb = (int)std::min<long long>((m + 31) / 32, kRedBlocks);
+  const int nb = (int)std::min<long long>((m + 31) / 32, 2 * 148);
   if (v2) {
     if (nk <= 8) k_dcgs_dot<8, 2><<<nb, 256, 0, s>>>(n, nk, V, ld, u, u, part, out, counter);
     else if (nk <= 16) k_dcgs_dot<16, 2><<<nb, 256, 0, s>>>(n, nk, V, ld, u, u, part, out, counter);

@@ -114,6 +114,7 @@ struct Layout {
   size_t off_gather;        // z-slab: [kMaxRanks][256] all-gather area of the fixed-order reductions
   size_t off_gtab;          // level-k ILU slot tables (off, lower, upper, pair_ptr, pair_b, pair_t)
   size_t off_spec, off_pinv;  // spectral preconditioner: [nf][Nh] complex scratch, [nf*nf][Nh] inverse
+  size_t off_tl;              // two-level RAS + spectral: 2 scratch vectors
   size_t total;
   long long P, ld;
   size_t geo_bytes;
@@ -133,9 +134,10 @@ const char* validate(const nks_grid* g, const nks_params* p) {
   if (p->gmres_restart < 1 || p->gmres_restart > 31) return "gmres_restart must be in 1..31";
   if (p->newton_maxit < 0 || p->gmres_maxit < 1 || p->gmres_stall_cycles < 0) return "bad iteration limits";
   if (p->pc_type != NKS_PC_NONE && p->pc_type != NKS_PC_RAS_BILU0 && p->pc_type != NKS_PC_AS_BILU0 &&
-      p->pc_type != NKS_PC_RRAS_BILU0 && p->pc_type != NKS_PC_SPECTRAL)
+      p->pc_type != NKS_PC_RRAS_BILU0 && p->pc_type != NKS_PC_SPECTRAL && p->pc_type != NKS_PC_RAS_SPECTRAL)
     return "unknown pc_type";
-  if (p->pc_type == NKS_PC_SPECTRAL && g->zghost > 0) return "the spectral preconditioner needs the whole periodic grid";
+  if ((p->pc_type == NKS_PC_SPECTRAL || p->pc_type == NKS_PC_RAS_SPECTRAL) && g->zghost > 0)
+    return "the spectral preconditioner needs the whole periodic grid";
   if (g->zghost > 0 && (p->pc_type == NKS_PC_AS_BILU0 || p->pc_type == NKS_PC_RRAS_BILU0))
     return "z-slab states support pc_type NONE or RAS (AS / RRAS need a reverse halo exchange)";
   if (g->zghost != 0 && (g->zghost < 2 || g->zghost > 8)) return "zghost must be 0 or 2..8";
@@ -163,6 +165,7 @@ const char* validate(const nks_grid* g, const nks_params* p) {
   if (!(p->kappa > 0) || !(p->theta >= 0)) return "kappa must be > 0, theta >= 0";
   if (p->ilu_level < -1 || p->ilu_level > 8) return "ilu_level must be -1 (exact LU) or 0..8";
   if (p->ilu_level != 0 && p->factor_fp32) return "factor_fp32 is available for ILU(0) only";
+  if (p->pc_type == NKS_PC_RAS_SPECTRAL && p->ilu_level != 0) return "the two-level preconditioner uses BILU(0) boxes";
   return nullptr;
 }
 
@@ -188,11 +191,15 @@ Layout make_layout(const nks_grid& g, const nks_params& p, IlukPattern* K = null
   L.off_out = o; o = align256(o + 256 * sizeof(double));
   L.off_gather = o; o = align256(o + (g.zghost > 0 ? (size_t)kMaxRanks * 256 * sizeof(double) : 0));
   L.P = 0;
-  if (p.pc_type == NKS_PC_SPECTRAL) {
+  if (p.pc_type == NKS_PC_SPECTRAL || p.pc_type == NKS_PC_RAS_SPECTRAL) {
     const long long Nh = spectral_half(g);
     L.off_spec = o; o = align256(o + (size_t)nf * Nh * 16);
     L.off_pinv = o; o = align256(o + (size_t)nf * nf * Nh * 16);
-  } else if (p.pc_type != NKS_PC_NONE) {
+    if (p.pc_type == NKS_PC_RAS_SPECTRAL) {   // two scratch vectors of the two-level apply
+      L.off_tl = o; o = align256(o + 2 * vec);
+    }
+  }
+  if (p.pc_type != NKS_PC_NONE && p.pc_type != NKS_PC_SPECTRAL) {
     const bool gen = p.ilu_level != 0;
     const int nslots = gen ? K->nslots : (d == 2 ? 13 : 25);
     const int la = gen ? K->la : 2, lb = gen ? K->lb : 3;
@@ -415,6 +422,32 @@ void pc_apply(nks_state* st, const double* r, double* z) {
     CK(cudaMemcpyAsync(z, r, st->nvec * sizeof(double), cudaMemcpyDeviceToDevice, st->stream));
     return;
   }
+  if (st->tl1) {
+    // two-level (NKS_PC_RAS_SPECTRAL): global spectral correction, then RAS on the remaining residual
+    //   z1 = S r,  t = r - J z1,  z = z1 + RAS(t)
+    {
+      PhaseScope ps(st, PH_RAS);
+      if (launch_spectral_apply(st->spec, st->nf, r, st->tl1, st->pinv, st->specbuf, st->stream) != 0)
+        throw std::runtime_error("cuFFT execution failed");
+      count_launch(st, 1);
+    }
+    jv(st, st->tl1, st->tl2);
+    {
+      PhaseScope ps(st, PH_VEC);
+      launch_xpay(st->nvec, r, -1.0, st->tl2, st->tl2, st->stream);
+      count_launch(st, 1);
+    }
+    {
+      PhaseScope ps(st, PH_RAS);
+      if (st->ras2d) CK(r2::launch_apply(st->ras2d, st->tl2, z, st->stream));
+      else launch_ras_apply(st->boxes, st->nf, st->N, st->fac, st->fac32, st->tl2, st->ybox, z, st->stream);
+      count_launch(st, 1);
+    }
+    PhaseScope ps(st, PH_VEC);
+    launch_axpby(st->nvec, 1.0, st->tl1, 1.0, z, st->stream);
+    count_launch(st, 1);
+    return;
+  }
   PhaseScope ps(st, PH_RAS);
   if (st->spec) {
     if (launch_spectral_apply(st->spec, st->nf, r, z, st->pinv, st->specbuf, st->stream) != 0)
@@ -435,9 +468,11 @@ void pc_setup(nks_state* st, const double* Xb) {
     launch_spectral_setup(st->spec, st->dp, st->nf, st->Xn, st->jac4, st->red_part, st->red_out + 192, st->pinv,
                           st->stream);
     count_launch(st, 3);
-    st->pc_valid = true;
-    st->pc_dt = st->dp.dt;
-    return;
+    if (!st->tl1) {
+      st->pc_valid = true;
+      st->pc_dt = st->dp.dt;
+      return;
+    }
   }
   {
     PhaseScope ps(st, PH_ASM);
@@ -900,13 +935,18 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, int32_t ra
     CK(cudaMallocHost(&st->h_red, 256 * sizeof(double)));
     CK(cudaMallocHost(&st->h_ring, 4 * 128 * sizeof(double)));
     for (int k = 0; k < 4; ++k) CK(cudaEventCreateWithFlags(&st->gm_ev[k], cudaEventDisableTiming));
-    if (params->pc_type == NKS_PC_SPECTRAL) {
+    if (params->pc_type == NKS_PC_SPECTRAL || params->pc_type == NKS_PC_RAS_SPECTRAL) {
       std::string why;
       st->spec = spectral_plan(*grid, st->nf, st->stream, why);
       if (!st->spec) throw std::runtime_error(why);
       st->specbuf = w + L.off_spec;
       st->pinv = w + L.off_pinv;
-    } else if (params->pc_type != NKS_PC_NONE) {
+      if (params->pc_type == NKS_PC_RAS_SPECTRAL) {
+        st->tl1 = (double*)(w + L.off_tl);
+        st->tl2 = st->tl1 + st->nvec;
+      }
+    }
+    if (params->pc_type != NKS_PC_NONE && params->pc_type != NKS_PC_SPECTRAL) {
       BoxSet& B = st->boxes;
       build_slot_tables(grid->dim, B);
       const bool gen = params->ilu_level != 0;

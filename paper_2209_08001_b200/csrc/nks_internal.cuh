@@ -150,6 +150,8 @@ struct nks_state {
   void* spec = nullptr;     // cuFFT plans of the spectral preconditioner (spectral.cu), or null
   void* specbuf = nullptr;  // [nf][Nh] complex scratch (workspace)
   void* pinv = nullptr;     // [nf*nf][Nh] per-wave-number inverse (workspace)
+  double* tl1 = nullptr;    // two-level preconditioner scratch (NKS_PC_RAS_SPECTRAL), or null
+  double* tl2 = nullptr;
   double pc_dt = 0.0;
   // history / controller
   double time = 0.0;

@@ -517,3 +517,31 @@ def test_spectral_pc_step_parity(shape, dts):
     out = _run_parity(shape, dts, (1,) * len(shape), 2, pc_type=5)
     for info_g, _, _ in out:
         assert info_g["gmres_its"] <= 30 * info_g["newton_its"], info_g
+
+
+@pytest.mark.parametrize("shape,nsub,dt", [((32, 24), (2, 2), 0.3), ((8, 10, 12), (2, 1, 2), 0.05)])
+def test_two_level_pc_apply_parity(shape, nsub, dt):
+    """NKS_PC_RAS_SPECTRAL: z = S r + RAS(r - J S r), the spectral global correction followed by left-RAS /
+    BILU(0) on the remaining residual, against the same composition of the oracle's pieces."""
+    from oracle import krylov
+    d = len(shape)
+    nf = 2 + d
+    Xa, Xb = states(shape)
+    g = gpu_solver(shape, nsub=nsub, overlap=2, pc_type=6)
+    g.set_fields(Xa[0], Xa[1], Xa[2:])
+    g.pc_setup(Xb, dt)
+    r = solver.gauge_project(ni.random_direction(nf, shape, 23))
+    zg = g.pc_apply(r).cpu().numpy()
+    m = oracle_model(d)
+    lin = krylov.Linearisation(m, Xa, Xb, dt)
+    z1 = krylov.SpectralPC(lin).apply(r)
+    J = jacobian.assemble(m, Xa, Xb, dt)
+    z2 = pc.RAS(J, shape, nf, tuple(reversed(nsub)), 2).apply(r - lin.jv(z1))
+    errs = field_rel_err(zg, z1 + z2)
+    assert max(errs) < 1e-10, errs
+
+
+def test_two_level_pc_step_parity():
+    out = _run_parity((48, 40), [0.01, 0.5, 2.0], (2, 2), 2, pc_type=6)
+    for info_g, _, _ in out:
+        assert info_g["gmres_its"] <= 40 * info_g["newton_its"], info_g
