@@ -54,7 +54,8 @@ typedef enum {
 /* Divergence reasons reported in nks_step_info.reason. */
 enum { NKS_REASON_NONE = 0, NKS_REASON_NEWTON_MAXIT = 1, NKS_REASON_LINE_SEARCH = 2,
        NKS_REASON_GMRES_MAXIT = 3, NKS_REASON_DOMAIN = 4, NKS_REASON_DT_FLOOR = 5,
-       NKS_REASON_GMRES_STAGNATION = 6 /* gmres_stall_cycles cycles each removing < 0.1 % of the residual */ };
+       NKS_REASON_GMRES_STAGNATION = 6 /* gmres_stall_cycles cycles each removing < 0.1 % of the residual */,
+       NKS_REASON_GMRES_PROJECTED = 7 /* the solve's mean rate projects it past gmres_maxit (opt-in, same param) */ };
 
 /* Preconditioner types (the variants are SURVEY 8(f)-1's Schwarz family, Cai-Sarkis):
  *   RAS    z = sum_i R_i^{0T} (L_i U_i)^{-1} R_i^delta r     (left restricted additive Schwarz, default)
@@ -142,7 +143,9 @@ typedef struct {
   int32_t gmres_stall_cycles;        /* 0 (default, the paper's behaviour): a Newton solve fails    */
                                      /* only at gmres_maxit.  k > 0: k consecutive restart cycles   */
                                      /* that each remove < 0.1 % of the true residual are reported */
-                                     /* as NKS_REASON_GMRES_STAGNATION (DIVERGED), so the controller */
+                                     /* as NKS_REASON_GMRES_STAGNATION (DIVERGED), and after k      */
+                                     /* cycles a solve whose mean convergence rate projects it past */
+                                     /* gmres_maxit as NKS_REASON_GMRES_PROJECTED, so the controller */
                                      /* retries without running to gmres_maxit.  A     */
                                      /* property of the linear solver, not of Eq. NSOA-1: it can   */
                                      /* change the accepted dt sequence (reading R18).   */

@@ -29,102 +29,91 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Column-split reduction: the 8 warps of a block walk the same 64-element tiles (16-byte loads when VW = 2)
-// and warp q owns basis columns q, q+8, q+16, q+24 (two accumulators each: against u and against w); the
-// block's partials go to part[block][kDOut] and the last block to finish adds them in block order.
-template <int NK, int VW>
+// Row-streaming reduction: block (bx, g) walks rows of the vectors grid-stride (16-byte loads when VW = 2) and
+// accumulates, per thread, the dots of u and w with the CG basis columns of group g (and, group 0, u.u and
+// u.w) -- every column and u, w read in long coalesced runs, u and w once per group (L2 hits after the first).
+// The partials go to part[bx][kDOut] (each group writes its own entries) and the last block to finish sums
+// every entry over bx in order (deterministic).
+template <int CG, int VW>
 __global__ void __launch_bounds__(256) k_dcgs_dot(long long n, int nk, const double* __restrict__ V, long long ld,
                                                 const double* __restrict__ u, const double* __restrict__ w,
                                                 double* __restrict__ part, double* __restrict__ out,
                                                 unsigned* __restrict__ counter) {
-  constexpr int CPW = NK / 8;
-  __shared__ double cs[kDOut];
-  __shared__ double sw[8][kDOut];
+  constexpr int NA = 2 * CG + 2;
+  __shared__ double sred[8][NA];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double au[CPW], aw[CPW];
+  const int g = blockIdx.y, k0 = g * CG;
+  double acc[NA];
 #pragma unroll
-  for (int q = 0; q < CPW; ++q) au[q] = aw[q] = 0.0;
-  double uu = 0.0, uw = 0.0;
+  for (int q = 0; q < NA; ++q) acc[q] = 0.0;
   const long long m = n / VW;
-  for (long long t = blockIdx.x * 32LL + lane; t < m; t += (long long)gridDim.x * 32) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < m; t += (long long)gridDim.x * blockDim.x) {
     double ux, uy = 0.0, wx, wy = 0.0;
     if (VW == 2) {
-      const double2 uv = reinterpret_cast<const double2*>(u)[t], wv = reinterpret_cast<const double2*>(w)[t];
+      const double2 uv = __ldg(reinterpret_cast<const double2*>(u) + t), wv = __ldg(reinterpret_cast<const double2*>(w) + t);
       ux = uv.x; uy = uv.y; wx = wv.x; wy = wv.y;
     } else {
-      ux = u[t]; wx = w[t];
+      ux = __ldg(u + t); wx = __ldg(w + t);
     }
 #pragma unroll
-    for (int q = 0; q < CPW; ++q) {
-      const int k = wid + 8 * q;
-      if (k < nk) {
+    for (int c = 0; c < CG; ++c)
+      if (k0 + c < nk) {
         double vx, vy = 0.0;
         if (VW == 2) {
-          const double2 v = __ldg(reinterpret_cast<const double2*>(V + k * ld) + t);
+          const double2 v = __ldg(reinterpret_cast<const double2*>(V + (long long)(k0 + c) * ld) + t);
           vx = v.x; vy = v.y;
         } else {
-          vx = __ldg(V + k * ld + t);
+          vx = __ldg(V + (long long)(k0 + c) * ld + t);
         }
-        au[q] = fma(vx, ux, fma(vy, uy, au[q]));
-        aw[q] = fma(vx, wx, fma(vy, wy, aw[q]));
+        acc[c] = fma(vx, ux, fma(vy, uy, acc[c]));
+        acc[CG + c] = fma(vx, wx, fma(vy, wy, acc[CG + c]));
       }
+    if (g == 0) {
+      acc[2 * CG] = fma(ux, ux, fma(uy, uy, acc[2 * CG]));
+      acc[2 * CG + 1] = fma(ux, wx, fma(uy, wy, acc[2 * CG + 1]));
     }
-    if (wid == 0) uu = fma(ux, ux, fma(uy, uy, uu));
-    if (wid == 1) uw = fma(ux, wx, fma(uy, wy, uw));
   }
-  for (int k = threadIdx.x; k < kDOut; k += blockDim.x) cs[k] = 0.0;
-  __syncthreads();
 #pragma unroll
-  for (int q = 0; q < CPW; ++q) {
-    const int k = wid + 8 * q;
-    const double su = warp_sum(au[q]), sv = warp_sum(aw[q]);
-    if (lane == 0 && k < nk) { cs[k] = su; cs[32 + k] = sv; }
-  }
-  {
-    const double s0 = warp_sum(uu), s1 = warp_sum(uw);
-    if (lane == 0 && wid == 0) cs[64] = s0;
-    if (lane == 0 && wid == 1) cs[65] = s1;
+  for (int q = 0; q < NA; ++q) {
+    double v = acc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) sred[wid][q] = v;
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < kDOut; k += blockDim.x) part[(long long)blockIdx.x * kDOut + k] = cs[k];
+  if (threadIdx.x < NA) {
+    const int q = threadIdx.x;
+    double v = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v += sred[k][q];
+    double* row = part + (long long)blockIdx.x * kDOut;
+    if (q < CG) { if (k0 + q < 32) row[k0 + q] = v; }
+    else if (q < 2 * CG) { if (k0 + q - CG < 32) row[32 + k0 + q - CG] = v; }
+    else if (g == 0) row[64 + q - 2 * CG] = v;
+  }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x * gridDim.y - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // last block: entry k = lane (+32, +64), block range split over the 8 warps, then warps combined in order
-  for (int base = 0; base < kDOut; base += 32) {
-    const int k = base + lane;
-    double a = 0.0;
-    if (k < kDOut) {
-      // independent loads, two accumulators: the block count (<= 2 per SM) keeps this tail short
-      double a2 = 0.0;
-      int blk = wid;
+  // last block: one thread per entry, the blocks summed in order (two interleaved accumulators)
+  for (int e = threadIdx.x; e < kDOut; e += blockDim.x) {
+    const bool used = (e < 32 && e < nk) || (e >= 32 && e < 64 && e - 32 < nk) || e >= 64;
+    double a = 0.0, a2 = 0.0;
+    if (used) {
+      int bx = 0;
 #pragma unroll 4
-      for (; blk + 8 < (int)gridDim.x; blk += 16) {
-        a += part[(long long)blk * kDOut + k];
-        a2 += part[(long long)(blk + 8) * kDOut + k];
+      for (; bx + 1 < (int)gridDim.x; bx += 2) {
+        a += part[(long long)bx * kDOut + e];
+        a2 += part[(long long)(bx + 1) * kDOut + e];
       }
-      if (blk < (int)gridDim.x) a += part[(long long)blk * kDOut + k];
-      a += a2;
+      if (bx < (int)gridDim.x) a += part[(long long)bx * kDOut + e];
     }
-    if (k < kDOut) sw[wid][k] = a;
+    out[e] = a + a2;
   }
-  __syncthreads();
-  if (wid == 0) {
-    for (int base = 0; base < kDOut; base += 32) {
-      const int k = base + lane;
-      if (k < kDOut) {
-        double t = 0.0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) t += sw[q][k];
-        out[k] = t;
-      }
-    }
-    if (lane == 0) *counter = 0u;
-  }
+  if (threadIdx.x == 0) *counter = 0u;
 }
 
 // r and gamma from the reduced values, in the host's order (so the host replays identical doubles).
@@ -230,23 +219,21 @@ static int vec_blocks(long long n) { return (int)std::min<long long>((n + 255) /
 static bool vec2(long long n, long long ld) { return (n % 2) == 0 && (ld % 2) == 0; }
 
 // One reduction of step nk (nk <= 31 basis columns before the candidate): out[] as documented above.
+static void dcgs_dot(long long n, int nk, const double* V, long long ld, const double* u, const double* w, double* part,
+                     double* out, unsigned* counter, cudaStream_t s) {
+  const bool v2 = vec2(n, ld);
+  const long long m = v2 ? n / 2 : n;
+  const int ng = std::max(1, (nk + 7) / 8);
+  const int nbx = (int)std::min<long long>((m + 255) / 256, std::max(2 * 148 / ng, 74));   // part: kRedBlocks rows
+  const dim3 grid(nbx, ng);
+  if (v2) k_dcgs_dot<8, 2><<<grid, 256, 0, s>>>(n, nk, V, ld, u, w, part, out, counter);
+  else k_dcgs_dot<8, 1><<<grid, 256, 0, s>>>(n, nk, V, ld, u, w, part, out, counter);
+}
+
 void launch_dcgs_dot(long long n, int nk, const double* V, long long ld, double* part, double* out, unsigned* counter,
                      cudaStream_t s) {
   const double* u = V + (long long)nk * ld;
-  const double* w = u + ld;
-  const bool v2 = vec2(n, ld);
-  const long long m = v2 ? n / 2 : n;
-  // 2 blocks of 8 streaming warps per SM saturate HBM; more blocks only lengthen the last block's tail sum
-  const int nb = (int)std::min<long long>((m + 31) / 32, 2 * 148);
-  if (v2) {
-    if (nk <= 8) k_dcgs_dot<8, 2><<<nb, 256, 0, s>>>(n, nk, V, ld, u, w, part, out, counter);
-    else if (nk <= 16) k_dcgs_dot<16, 2><<<nb, 256, 0, s>>>(n, nk, V, ld, u, w, part, out, counter);
-    else k_dcgs_dot<32, 2><<<nb, 256, 0, s>>>(n, nk, V, ld, u, w, part, out, counter);
-  } else {
-    if (nk <= 8) k_dcgs_dot<8, 1><<<nb, 256, 0, s>>>(n, nk, V, ld, u, w, part, out, counter);
-    else if (nk <= 16) k_dcgs_dot<16, 1><<<nb, 256, 0, s>>>(n, nk, V, ld, u, w, part, out, counter);
-    else k_dcgs_dot<32, 1><<<nb, 256, 0, s>>>(n, nk, V, ld, u, w, part, out, counter);
-  }
+  dcgs_dot(n, nk, V, ld, u, u + ld, part, out, counter, s);
 }
 
 // The candidate-only reduction that closes a restart cycle (there is no w = A M^-1 u_m): the same kernel
@@ -254,18 +241,7 @@ void launch_dcgs_dot(long long n, int nk, const double* V, long long ld, double*
 void launch_dcgs_dot_u(long long n, int nk, const double* V, long long ld, double* part, double* out, unsigned* counter,
                        cudaStream_t s) {
   const double* u = V + (long long)nk * ld;
-  const bool v2 = vec2(n, ld);
-  const long long m = v2 ? n / 2 : n;
-  const int nb = (int)std::min<long long>((m + 31) / 32, 2 * 148);
-  if (v2) {
-    if (nk <= 8) k_dcgs_dot<8, 2><<<nb, 256, 0, s>>>(n, nk, V, ld, u, u, part, out, counter);
-    else if (nk <= 16) k_dcgs_dot<16, 2><<<nb, 256, 0, s>>>(n, nk, V, ld, u, u, part, out, counter);
-    else k_dcgs_dot<32, 2><<<nb, 256, 0, s>>>(n, nk, V, ld, u, u, part, out, counter);
-  } else {
-    if (nk <= 8) k_dcgs_dot<8, 1><<<nb, 256, 0, s>>>(n, nk, V, ld, u, u, part, out, counter);
-    else if (nk <= 16) k_dcgs_dot<16, 1><<<nb, 256, 0, s>>>(n, nk, V, ld, u, u, part, out, counter);
-    else k_dcgs_dot<32, 1><<<nb, 256, 0, s>>>(n, nk, V, ld, u, u, part, out, counter);
-  }
+  dcgs_dot(n, nk, V, ld, u, u, part, out, counter, s);
 }
 
 void launch_dcgs_update(long long n, int nk, double* V, long long ld, const double* hv, cudaStream_t s) {

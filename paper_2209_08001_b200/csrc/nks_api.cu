@@ -505,7 +505,7 @@ void set_dt(nks_state* st, double dt) {
 }
 
 // Right-preconditioned restarted GMRES: J s = b with s0 = 0 (reading R18).  Returns 0
-// converged, 1 gmres_maxit, 2 stagnation (opt-in).
+// converged, 1 gmres_maxit, 2 stagnation (opt-in), 3 projected past gmres_maxit (opt-in).
 //
 // Arnoldi by DCGS2 (krylov.cu): ONE global reduction per iteration (a = V^T u, b = V^T w, u.u, u.w in one
 // fused pass, one allreduce on a slab state), one fused update pass.  Column j-1 of the Hessenberg matrix
@@ -674,6 +674,14 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
       // to gmres_maxit.  Off by default (the paper's solver fails only at its iteration limit).
       stall = (beta > 0.999 * prev) ? stall + 1 : 0;
       if (st->prm.gmres_stall_cycles > 0 && stall >= st->prm.gmres_stall_cycles) return 2;
+      // Projection (opt-in, the same parameter): after at least gmres_stall_cycles cycles, the mean
+      // convergence rate of this solve so far projects the iterations still needed; a solve that would not
+      // reach tol within gmres_maxit is reported now instead of after running to the limit.
+      if (st->prm.gmres_stall_cycles > 0 && its >= st->prm.gmres_stall_cycles * m && beta > tol) {
+        const double rate = std::log(beta / bnorm) / its;              // < 0 while converging
+        const double need = rate < 0.0 ? std::log(tol / beta) / rate : 1e300;
+        if (its + need > (double)st->prm.gmres_maxit) return 3;
+      }
     }
     // V already holds r; scale below uses V as source (first == false)
   }
@@ -760,10 +768,11 @@ nks_status step_impl(nks_state* st, double dt, nks_step_info* info) {
     const int grc = gmres(st, st->Ft, f, st->S, tol, gits);
     I.gmres_its += gits;
     if (grc != 0) {
-      I.reason = grc == 2 ? NKS_REASON_GMRES_STAGNATION : NKS_REASON_GMRES_MAXIT;
+      I.reason = grc == 2 ? NKS_REASON_GMRES_STAGNATION : (grc == 3 ? NKS_REASON_GMRES_PROJECTED : NKS_REASON_GMRES_MAXIT);
       I.fnorm = f;
       st->err = grc == 2 ? "GMRES stagnated (gmres_stall_cycles restart cycles with < 0.1 % residual reduction)"
-                         : "GMRES reached gmres_maxit";
+                         : (grc == 3 ? "GMRES projected past gmres_maxit at its mean convergence rate"
+                                     : "GMRES reached gmres_maxit");
       return NKS_E_DIVERGED;
     }
     // line search (reading R17)
@@ -1315,7 +1324,7 @@ nks_status nks_gmres_solve(nks_state* st, double dt, const double* x_b, const do
     CK(cudaMemcpyAsync(s, st->S, nb, kind_out(on_device), st->stream));
     sync(st);
     if (rc != 0) {
-      st->err = rc == 2 ? "GMRES stagnated" : "GMRES reached gmres_maxit";
+      st->err = rc == 2 ? "GMRES stagnated" : (rc == 3 ? "GMRES projected past gmres_maxit" : "GMRES reached gmres_maxit");
       return NKS_E_DIVERGED;
     }
     return NKS_OK;

@@ -19,7 +19,7 @@ NKS_OK, NKS_E_INVALID, NKS_E_DOMAIN, NKS_E_DIVERGED, NKS_E_CUDA, NKS_E_NCCL, NKS
 STATUS = {0: "OK", 1: "INVALID", 2: "DOMAIN", 3: "DIVERGED", 4: "CUDA", 5: "NCCL", 6: "OOM", 7: "STATE"}
 PC_NONE, PC_RAS_BILU0, PC_AS_BILU0, PC_RRAS_BILU0, PC_SPECTRAL, PC_RAS_SPECTRAL = 0, 2, 3, 4, 5, 6
 REASONS = {0: "none", 1: "newton_maxit", 2: "line_search", 3: "gmres_maxit", 4: "domain", 5: "dt_floor",
-           6: "gmres_stagnation"}
+           6: "gmres_stagnation", 7: "gmres_projected"}
 PHASES = ["residual", "jv", "ras_apply", "assemble", "factor", "gmres_vec", "reductions", "other"]
 
 

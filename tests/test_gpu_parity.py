@@ -267,7 +267,7 @@ def test_bilu0_breakdown_is_reported_as_divergence():
     assert g.step(2.0)["converged"]
     X0 = g.get_state()
     info = g.step(2.0, raise_on_fail=False)
-    assert info["status"] == "DIVERGED" and info["reason"] == "gmres_stagnation", info
+    assert info["status"] == "DIVERGED" and info["reason"] in ("gmres_stagnation", "gmres_projected"), info
     assert info["gmres_its"] < 1000
     np.testing.assert_array_equal(g.get_state(), X0)
 

@@ -26,7 +26,8 @@ import numpy as np  # noqa: E402
 
 import nks_inputs as ni  # noqa: E402
 
-SOLVERS = {"ilu0": (2, 0), "ilu1": (2, 1), "ilu2": (2, 2), "lu": (2, -1), "spectral": (5, 0), "none": (0, 0)}
+SOLVERS = {"ilu0": (2, 0), "ilu1": (2, 1), "ilu2": (2, 2), "lu": (2, -1), "spectral": (5, 0), "two_level": (6, 0),
+           "none": (0, 0)}
 
 
 def one(shape, nsub, X, sol, pc, level, dt):
@@ -55,8 +56,8 @@ def one(shape, nsub, X, sol, pc, level, dt):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--dts", default="0.986,2.0")
-    ap.add_argument("--solvers", default="ilu0,ilu1,ilu2,spectral,none")
+    ap.add_argument("--dts", default="0.986,1.414,2.0")
+    ap.add_argument("--solvers", default="ilu0,ilu1,ilu2,spectral,two_level")
     ap.add_argument("--lu-grid", type=int, default=128)
     args = ap.parse_args()
     import torch
