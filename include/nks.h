@@ -155,6 +155,10 @@ typedef struct {
                                      /* natural order).  k != 0 uses the level-synchronous solves;   */
                                      /* its factor storage grows with the fill (NKS_E_OOM / INVALID  */
                                      /* from nks_workspace_bytes when it cannot be held).            */
+  int32_t u0_cg;                     /* u^0 when nks_set_fields gets u = NULL (reading R13): 0 = the */
+                                     /* FFT solve on periodic whole-grid states, conjugate gradients */
+                                     /* on the elastic block otherwise (z-slabs: no whole-grid FFT;  */
+                                     /* Neumann); 1 = conjugate gradients always.                    */
 } nks_params;
 
 typedef struct {
@@ -214,7 +218,8 @@ NKS_API nks_status nks_create(const nks_grid* grid, const nks_params* params, in
 
 /* Set X^n.  c, eta: N doubles each; u: d*N doubles (u_1 block first) or NULL, in which case
  * u^0 solves the discrete mechanical equilibrium [D^ sigma^el]^0 = 0 (reading R13)
- * by an fp64 FFT.  Sets cbar0 = mean(c) and projects u onto the canonical gauge
+ * by an fp64 FFT (periodic whole grid) or by conjugate gradients on the elastic block (z-slabs, with
+ * halos and allreduces; Neumann; params.u0_cg) -- NKS_E_DIVERGED if CG does not converge.  Sets cbar0 = mean(c) and projects u onto the canonical gauge
  * (zero mean per component and parity sub-lattice, reading R14).  Resets time, step history,
  * zeta and cached factors.  NKS_E_DOMAIN if the state is inadmissible. */
 NKS_API nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, const double* u,

@@ -183,6 +183,37 @@ __global__ void __launch_bounds__(256) k_dcgs_update(long long n, int nk, double
   }
 }
 
+// Plain dot product (fixed-order two-stage): part[block] = block sums, then one block sums them in order.
+__global__ void __launch_bounds__(256) k_dot_part(long long n, const double* __restrict__ a, const double* __restrict__ b,
+                                                double* __restrict__ part) {
+  __shared__ double sred[8];
+  double v = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    v = fma(a[i], b[i], v);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < 8; ++k) t += sred[k];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_dot_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  __shared__ double s[256];
+  double a = 0.0;
+  for (int k = threadIdx.x; k < nb; k += blockDim.x) a += part[k];
+  s[threadIdx.x] = a;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = s[0];
+}
+
 // out = sum_k y[k] V_k
 __global__ void k_lincomb(long long n, int nk, const double* __restrict__ V, long long ld, Coefs y,
                           double* __restrict__ out) {
@@ -262,6 +293,12 @@ void launch_lincomb(long long n, int nk, const double* V, long long ld, const do
   Coefs c;
   for (int k = 0; k < nk && k < 64; ++k) c.c[k] = y[k];
   k_lincomb<<<vec_blocks(n), 256, 0, s>>>(n, nk, V, ld, c, out);
+}
+
+void launch_dot(long long n, const double* a, const double* b, double* part, double* out, cudaStream_t s) {
+  const int nb = (int)std::min<long long>((n + 255) / 256, kRedBlocks);
+  k_dot_part<<<nb, 256, 0, s>>>(n, a, b, part);
+  k_dot_final<<<1, 256, 0, s>>>(part, nb, out);
 }
 
 void launch_axpby(long long n, double a, const double* x, double b, double* y, cudaStream_t s) {

@@ -39,6 +39,7 @@ void launch_dcgs_dot_u(long long n, int nk, const double* V, long long ld, doubl
                        cudaStream_t s);
 void launch_dcgs_update(long long n, int nk, double* V, long long ld, const double* hv, cudaStream_t s);
 void launch_lincomb(long long n, int nk, const double* V, long long ld, const double* y, double* out, cudaStream_t s);
+void launch_dot(long long n, const double* a, const double* b, double* part, double* out, cudaStream_t s);
 void launch_axpby(long long n, double a, const double* x, double b, double* y, cudaStream_t s);
 void launch_xpay(long long n, const double* x, double a, const double* y, double* z, cudaStream_t s);
 // precond.cu
@@ -687,6 +688,84 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
   }
 }
 
+// sum of a.b over n doubles (own points: the ghost planes of slab vectors are kept zero), all ranks -- host sync
+double dot(nks_state* st, const double* a, const double* b, long long n) {
+  {
+    PhaseScope ps(st, PH_RED);
+    launch_dot(n, a, b, st->red_part, st->red_out, st->stream);
+    count_launch(st, 2);
+  }
+  comm_allreduce(st, st->red_out, 1);
+  CK(cudaMemcpyAsync(st->h_red, st->red_out, sizeof(double), cudaMemcpyDeviceToHost, st->stream));
+  sync(st);
+  return st->h_red[0];
+}
+
+// u^0 of the current c (reading R13) by conjugate gradients on the elastic block, for the states the FFT
+// does not cover (z-slabs, Neumann boundaries) or on request (nks_params.u0_cg): the u rows of F are
+// A_uu u + A_uc (c - cbar0), A_uu is symmetric negative semi-definite with the gauge as its
+// null space (R14 / R38), so CG on -A_uu u = A_uc (c - cbar0) with the right-hand side projected onto the
+// gauge complement converges to the canonical-gauge equilibrium.  A_uu p is the u part of J (0, 0, p) (the
+// J.v kernels; the pointwise partials are zeroed, they only enter the c and eta rows).  Stops at
+// ||r|| <= 1e-13 ||b|| (or, when roundoff stalls it first, below 1e-10).  Returns 0 or 1 (not converged).
+int init_u0_cg(nks_state* st, int& its_out) {
+  const long long N = st->N, nvec = st->nvec, off = 2 * N, nu = st->d * N;
+  double* x = st->S;
+  double* r = st->Ft;
+  double* p = st->W2;
+  double* q = st->Z;
+  CK(cudaMemsetAsync(st->Xn + off, 0, nu * sizeof(double), st->stream));
+  CK(cudaMemsetAsync(st->jac4, 0, 4 * N * sizeof(double), st->stream));
+  halo(st, st->Xn, st->nf);
+  residual(st, st->Xn, st->F);                                // u rows: A_uc (c - cbar0)
+  for (double* v : {x, r, p, q}) CK(cudaMemsetAsync(v, 0, nvec * sizeof(double), st->stream));
+  {
+    PhaseScope ps(st, PH_VEC);
+    launch_axpby(nu, -1.0, st->F + off, 0.0, r + off, st->stream);
+    count_launch(st, 1);
+  }
+  gauge(st, r);
+  clean(st, r, st->nf);
+  CK(cudaMemcpyAsync(p, r, nvec * sizeof(double), cudaMemcpyDeviceToDevice, st->stream));
+  double rr = dot(st, r + off, r + off, nu);
+  const double bnorm = std::sqrt(rr);
+  double best = bnorm;
+  int since_best = 0, it = 0;
+  const int maxit = 200000;
+  bool ok = bnorm == 0.0;
+  for (; !ok && it < maxit; ++it) {
+    halo(st, p, st->nf);
+    jv(st, p, q);                                             // q_u = A_uu p_u
+    clean(st, p, st->nf);
+    clean(st, q, st->nf);
+    const double pq = -dot(st, p + off, q + off, nu);         // p . (-A) p > 0
+    if (!(pq > 0.0)) break;
+    const double alpha = rr / pq;
+    {
+      PhaseScope ps(st, PH_VEC);
+      launch_axpby(nu, alpha, p + off, 1.0, x + off, st->stream);    // x += alpha p
+      launch_axpby(nu, alpha, q + off, 1.0, r + off, st->stream);    // r -= alpha (-A p)
+      count_launch(st, 2);
+    }
+    if (it % 64 == 63) gauge(st, r);                          // keep roundoff out of the null space
+    const double rr2 = dot(st, r + off, r + off, nu);
+    const double rn = std::sqrt(rr2);
+    if (rn <= 1e-13 * bnorm) { ok = true; ++it; break; }
+    if (rn < 0.5 * best) { best = rn; since_best = 0; } else if (++since_best > 2000) break;
+    const double beta = rr2 / rr;
+    rr = rr2;
+    {
+      PhaseScope ps(st, PH_VEC);
+      launch_axpby(nu, 1.0, r + off, beta, p + off, st->stream);     // p = r + beta p
+      count_launch(st, 1);
+    }
+  }
+  if (!ok && best <= 1e-10 * bnorm) ok = true;
+  its_out = it;
+  CK(cudaMemcpyAsync(st->Xn + off, x + off, nu * sizeof(double), cudaMemcpyDeviceToDevice, st->stream));
+  return ok ? 0 : 1;
+}
+
 void energy(nks_state* st, const double* X, double parts[4], double& mass) {
   {
     PhaseScope ps(st, PH_RED);
@@ -1051,8 +1130,6 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, int32_t ra
 
 nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, const double* u, int32_t on_device) {
   if (!st || !c || !eta) return NKS_E_INVALID;
-  if (slab(st) && !u) return NKS_E_INVALID;     // the FFT u^0 is a whole-grid operation
-  if (st->dp.bc && !u) return NKS_E_INVALID;    // u^0 by FFT is periodic only; Neumann takes the caller's u
   return guarded(st, [&]() -> nks_status {
     const long long N = st->N;
     CK(cudaMemcpyAsync(st->Xn, c, N * sizeof(double), kind_in(on_device), st->stream));
@@ -1069,14 +1146,23 @@ nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, con
     CK(cudaMemcpyAsync(st->h_red, st->red_out, 5 * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
     sync(st);
     st->dp.cbar0 = st->h_red[4] / (double)global_points(st);
-    if (u) {
-    } else {
-      std::string e;
-      if (init_displacement_fft(st->dp, st->Xn, st->Xn + 2 * N, st->V, st->stream, e) != 0) {
-        st->err = e;
-        return NKS_E_CUDA;
+    if (!u) {
+      if (slab(st) || st->dp.bc || st->prm.u0_cg) {
+        // z-slabs (no whole-grid FFT), Neumann boundaries (not diagonalised by the DFT), or on request
+        int its = 0;
+        if (init_u0_cg(st, its) != 0) {
+          st->err = "u0: conjugate gradients on the elastic block did not converge";
+          return NKS_E_DIVERGED;
+        }
+        st->u0_cg_its = its;
+      } else {
+        std::string e;
+        if (init_displacement_fft(st->dp, st->Xn, st->Xn + 2 * N, st->V, st->stream, e) != 0) {
+          st->err = e;
+          return NKS_E_CUDA;
+        }
+        count_launch(st, 3 + st->d);
       }
-      count_launch(st, 3 + st->d);
     }
     gauge(st, st->Xn);
     level_prep(st);

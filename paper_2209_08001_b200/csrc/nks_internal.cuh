@@ -171,7 +171,8 @@ struct nks_state {
   // counters
   long long launches = 0;
   long long syncs = 0;
-  long long reductions = 0;     // global reductions issued (GMRES: one per Arnoldi step + one per restart)
+  long long reductions = 0;
+  int u0_cg_its = 0;            // CG iterations of the last u^0 solve (0: FFT or given)     // global reductions issued (GMRES: one per Arnoldi step + one per restart)
   // phase profiling (CUDA events on this stream)
   bool profile = false;
   double phase_ms[8] = {0};

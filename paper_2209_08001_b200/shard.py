@@ -250,27 +250,17 @@ class ShardedSolver:
         t = self.torch
         return field[..., t.tensor(idx, device=field.device), :, :].contiguous()
 
-    def initial_displacement(self, c, eta):
-        """u^0 of the whole grid (a0: cuFFT on one device) from a temporary full-grid state."""
-        from .nks import PC_NONE, Solver
-        cfg = dict(self.solver_cfg)
-        cfg["gmres_restart"] = 1
-        helper = Solver(self.shape_global, self.model, cfg, h=self.h, pc_type=PC_NONE, device=self.device)
-        helper.set_fields(c, eta)
-        u = helper.get_state_device()[2:].clone()
-        del helper
-        return u
-
     def set_fields(self, c, eta, u=None):
-        """Global c, eta (nz, ny, nx) and optionally u (3, nz, ny, nx), the same on every rank."""
+        """Global c, eta (nz, ny, nx) and optionally u (3, nz, ny, nx), the same on every rank; each rank
+        passes its slab.  Without u the library solves u^0 on the slabs themselves (conjugate gradients on
+        the elastic block with halo exchanges and allreduces, reading R13) -- no rank holds the whole grid."""
         t = self.torch
         c = t.as_tensor(np.asarray(c) if not isinstance(c, t.Tensor) else c, dtype=t.float64).to(self.device)
         eta = t.as_tensor(np.asarray(eta) if not isinstance(eta, t.Tensor) else eta, dtype=t.float64).to(self.device)
-        if u is None:
-            u = self.initial_displacement(c, eta)
-        else:
+        if u is not None:
             u = t.as_tensor(np.asarray(u) if not isinstance(u, t.Tensor) else u, dtype=t.float64).to(self.device)
-        self.solver.set_fields(self.local(c), self.local(eta), self.local(u))
+            u = self.local(u)
+        self.solver.set_fields(self.local(c), self.local(eta), u)
 
     def step(self, dt, raise_on_fail=True):
         return self.solver.step(dt, raise_on_fail=raise_on_fail)

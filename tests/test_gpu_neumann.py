@@ -97,3 +97,18 @@ def test_neumann_step_parity(shape, pc, dts):
         assert info_g["energy"] == pytest.approx(scheme.energy(m, Xo, cbar), rel=1e-10)
         assert abs(info_g["mass"] - mass0) <= 1e-12 * abs(mass0)
         assert info_g["newton_its"] == info_o["newton_its"]
+
+
+@pytest.mark.parametrize("shape", [(16, 20), (15, 12), (6, 8, 7)])
+def test_neumann_u0_by_conjugate_gradients(shape):
+    """Without u, a Neumann state solves u^0 by CG on its elastic block; it equals the oracle's gauge-pinned
+    direct solve (R13, R38)."""
+    d = len(shape)
+    m = omodel(d)
+    c, eta = ni.initial_fields(shape, 3)
+    uo = solver.init_displacement(m, c, c.mean())
+    g = gpu(shape)
+    g.set_fields(c, eta, None)
+    ug = g.get_state()[2:]
+    for I in range(d):
+        assert np.linalg.norm(ug[I] - uo[I]) <= 1e-10 * np.linalg.norm(uo[I])

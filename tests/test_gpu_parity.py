@@ -545,3 +545,17 @@ def test_two_level_pc_step_parity():
     out = _run_parity((48, 40), [0.01, 0.5, 2.0], (2, 2), 2, pc_type=6)
     for info_g, _, _ in out:
         assert info_g["gmres_its"] <= 40 * info_g["newton_its"], info_g
+
+
+@pytest.mark.parametrize("shape", [(64, 48), (16, 12, 20), (11, 13)])
+def test_u0_conjugate_gradients_match_fft(shape):
+    """u^0 by conjugate gradients on the elastic block (the z-slab / Neumann path, forced here with
+    u0_cg = 1) equals the FFT equilibrium in the canonical gauge (reading R13/R14)."""
+    c, eta = ni.initial_fields(shape, 2)
+    g1 = gpu_solver(shape, pc_type=0)
+    g1.set_fields(c, eta, None)
+    g2 = gpu_solver(shape, pc_type=0, sol={"u0_cg": 1})
+    g2.set_fields(c, eta, None)
+    u1, u2 = g1.get_state()[2:], g2.get_state()[2:]
+    for I in range(len(shape)):
+        assert np.linalg.norm(u2[I] - u1[I]) <= 1e-10 * np.linalg.norm(u1[I])
