@@ -788,7 +788,13 @@ static bool dims_of(const nks_grid& g, Dims& D) {
 static int cs_min(const Dims& D) { return (D.eymax + kRPC - 1) / kRPC; }
 
 // cluster sizes this grid admits: every stripe <= 32 rows and >= 2 rows, portable cluster size <= 8
-static int cs_max() { return 8; }
+static int cs_max() {
+#ifdef NKS_R2_ABLATE
+  // ablation build only (tools/ras2d_step_cost.py): cap the stripes per box
+  if (const char* e = std::getenv("NKS_RAS2D_CSMAX")) return std::max(1, std::min(8, std::atoi(e)));
+#endif
+  return 8;
+}
 static bool cs_ok(const Dims& D, int CS) { return CS >= cs_min(D) && CS <= cs_max() && D.eymin / CS >= 2; }
 
 static int kgp_of(const Dims& D, int RPC) { return D.exmax + 2 * (RPC - 1) + 4 * kGmax + 1; }
