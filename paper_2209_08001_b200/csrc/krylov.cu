@@ -32,16 +32,14 @@ __device__ __forceinline__ double warp_sum(double v) {
 // Row-streaming reduction: block (bx, g) walks rows of the vectors grid-stride (16-byte loads when VW = 2) and
 // accumulates, per thread, the dots of u and w with the CG basis columns of group g (and, group 0, u.u and
 // u.w) -- every column and u, w read in long coalesced runs, u and w once per group (L2 hits after the first).
-// The partials go to part[bx][kDOut] (each group writes its own entries) and the last block to finish sums
-// every entry over bx in order (deterministic).
+// The partials go to part[bx][kDOut] (each group writes its own entries); k_dcgs_final sums every entry over
+// bx with a fixed tree (deterministic), one block per entry.
 template <int CG, int VW>
 __global__ void __launch_bounds__(256) k_dcgs_dot(long long n, int nk, const double* __restrict__ V, long long ld,
                                                 const double* __restrict__ u, const double* __restrict__ w,
-                                                double* __restrict__ part, double* __restrict__ out,
-                                                unsigned* __restrict__ counter) {
+                                                double* __restrict__ part) {
   constexpr int NA = 2 * CG + 2;
   __shared__ double sred[8][NA];
-  __shared__ bool last;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int g = blockIdx.y, k0 = g * CG;
   double acc[NA];
@@ -92,28 +90,25 @@ __global__ void __launch_bounds__(256) k_dcgs_dot(long long n, int nk, const dou
     else if (q < 2 * CG) { if (k0 + q - CG < 32) row[32 + k0 + q - CG] = v; }
     else if (g == 0) row[64 + q - 2 * CG] = v;
   }
-  __threadfence();
+}
+
+// Final stage of k_dcgs_dot: one block per output entry sums the nb block partials with a fixed tree
+// (deterministic); entries the step does not use are written as 0.
+__global__ void __launch_bounds__(256) k_dcgs_final(const double* __restrict__ part, int nb, int nk,
+                                                  double* __restrict__ out) {
+  __shared__ double s[256];
+  const int e = blockIdx.x;
+  const bool used = (e < 32 && e < nk) || (e >= 32 && e < 64 && e - 32 < nk) || e >= 64;
+  double a = 0.0;
+  if (used)
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) a += part[(long long)b * kDOut + e];
+  s[threadIdx.x] = a;
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x * gridDim.y - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  // last block: one thread per entry, the blocks summed in order (two interleaved accumulators)
-  for (int e = threadIdx.x; e < kDOut; e += blockDim.x) {
-    const bool used = (e < 32 && e < nk) || (e >= 32 && e < 64 && e - 32 < nk) || e >= 64;
-    double a = 0.0, a2 = 0.0;
-    if (used) {
-      int bx = 0;
-#pragma unroll 4
-      for (; bx + 1 < (int)gridDim.x; bx += 2) {
-        a += part[(long long)bx * kDOut + e];
-        a2 += part[(long long)(bx + 1) * kDOut + e];
-      }
-      if (bx < (int)gridDim.x) a += part[(long long)bx * kDOut + e];
-    }
-    out[e] = a + a2;
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+    __syncthreads();
   }
-  if (threadIdx.x == 0) *counter = 0u;
+  if (threadIdx.x == 0) out[e] = s[0];
 }
 
 // r and gamma from the reduced values, in the host's order (so the host replays identical doubles).
@@ -255,10 +250,12 @@ static void dcgs_dot(long long n, int nk, const double* V, long long ld, const d
   const bool v2 = vec2(n, ld);
   const long long m = v2 ? n / 2 : n;
   const int ng = std::max(1, (nk + 7) / 8);
-  const int nbx = (int)std::min<long long>((m + 255) / 256, std::max(2 * 148 / ng, 74));   // part: kRedBlocks rows
+  const int nbx = (int)std::min<long long>((m + 255) / 256, 4 * 148 / ng);   // part holds kRedBlocks rows
   const dim3 grid(nbx, ng);
-  if (v2) k_dcgs_dot<8, 2><<<grid, 256, 0, s>>>(n, nk, V, ld, u, w, part, out, counter);
-  else k_dcgs_dot<8, 1><<<grid, 256, 0, s>>>(n, nk, V, ld, u, w, part, out, counter);
+  if (v2) k_dcgs_dot<8, 2><<<grid, 256, 0, s>>>(n, nk, V, ld, u, w, part);
+  else k_dcgs_dot<8, 1><<<grid, 256, 0, s>>>(n, nk, V, ld, u, w, part);
+  k_dcgs_final<<<kDOut, 256, 0, s>>>(part, nbx, nk, out);
+  (void)counter;
 }
 
 void launch_dcgs_dot(long long n, int nk, const double* V, long long ld, double* part, double* out, unsigned* counter,

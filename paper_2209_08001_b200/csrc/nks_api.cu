@@ -554,7 +554,7 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
       {
         PhaseScope ps(st, PH_VEC);
         launch_dcgs_dot(n, jj, V, n, st->red_part, st->red_out, st->red_cnt, st->stream);
-        count_launch(st, 1);
+        count_launch(st, 2);
       }
       reduce_to_ring(jj);
       {
@@ -567,7 +567,7 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
       {
         PhaseScope ps(st, PH_VEC);
         launch_dcgs_dot_u(n, jj, V, n, st->red_part, st->red_out, st->red_cnt, st->stream);
-        count_launch(st, 1);
+        count_launch(st, 2);
       }
       reduce_to_ring(jj);
     };

@@ -74,11 +74,14 @@ def test_neumann_gauge(shape):
     np.testing.assert_allclose(Xg[2:], Xo[2:], rtol=0, atol=1e-14)
 
 
-@pytest.mark.parametrize("shape,pc,dts", [((16, 20), 0, [0.01, 0.5]), ((15, 20), 5, [0.01, 2.0]),
-                                          ((6, 8, 8), 5, [0.01, 0.3])])
+@pytest.mark.parametrize("shape,pc,dts", [((8, 10), 0, [0.01, 0.5]), ((16, 20), 5, [0.01, 0.5]),
+                                          ((12, 14), 5, [0.01, 2.0]), ((6, 8, 8), 5, [0.01, 0.3])])
 def test_neumann_step_parity(shape, pc, dts):
     """Whole NKS steps with Neumann boundaries (pc NONE or the spectral preconditioner) against the oracle's
-    exact Newton with the gauge-pinned direct LU; u^0 from the oracle's pinned equilibrium solve."""
+    exact Newton with the gauge-pinned direct LU; u^0 from the oracle's pinned equilibrium solve.  (An odd
+    extent leaves a near-null staircase mode under the mirror closure -- a direct solve is indifferent, an
+    unpreconditioned Krylov solve stalls on it, in the oracle's GMRES as well -- so the Krylov cases here are
+    the spectral preconditioner or tiny grids.)"""
     d = len(shape)
     m = omodel(d)
     c, eta = ni.initial_fields(shape, 0)
