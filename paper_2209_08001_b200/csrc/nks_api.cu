@@ -720,8 +720,9 @@ int init_u0_cg(nks_state* st, int& its_out) {
   residual(st, st->Xn, st->F);                                // u rows: A_uc (c - cbar0)
   for (double* v : {x, r, p, q}) CK(cudaMemsetAsync(v, 0, nvec * sizeof(double), st->stream));
   {
+    // A_uu u = -F_u(0)  <=>  (-A_uu) u = F_u(0): CG on the positive semi-definite -A_uu with b = F_u(0)
     PhaseScope ps(st, PH_VEC);
-    launch_axpby(nu, -1.0, st->F + off, 0.0, r + off, st->stream);
+    launch_axpby(nu, 1.0, st->F + off, 0.0, r + off, st->stream);
     count_launch(st, 1);
   }
   gauge(st, r);
