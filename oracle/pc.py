@@ -44,8 +44,10 @@ def split_axis(n: int, nsub: int):
     return out
 
 
-def boxes(shape, nsub, delta):
-    """List of boxes; each: dict(start[j], own[j], ext[j]) indexed by axis j (0 = x)."""
+def boxes(shape, nsub, delta, bc="periodic"):
+    """List of boxes; each: dict(start[j], own[j], ext[j], s0[j], d0[j]) indexed by axis j (0 = x).  Periodic:
+    the box is extended by delta on each side (wrapping, self-overlapping on a one-box axis, R20).  Neumann
+    (R38): the extension stops at the walls -- there is nothing beyond them."""
     d = len(shape)
     n_xyz = [shape[d - 1 - j] for j in range(d)]
     per_axis = [split_axis(n_xyz[j], nsub[j]) for j in range(d)]
@@ -54,8 +56,14 @@ def boxes(shape, nsub, delta):
         combo = tuple(reversed(combo))   # combo[j] = box index along axis j; x varies fastest
         start = [per_axis[j][combo[j]][0] for j in range(d)]
         own = [per_axis[j][combo[j]][1] for j in range(d)]
-        ext = [own[j] + 2 * delta for j in range(d)]
-        out.append({"start": start, "own": own, "ext": ext, "delta": delta, "n": n_xyz})
+        if bc == "periodic":
+            s0 = [start[j] - delta for j in range(d)]
+            ext = [own[j] + 2 * delta for j in range(d)]
+        else:
+            s0 = [max(start[j] - delta, 0) for j in range(d)]
+            ext = [min(start[j] + own[j] + delta, n_xyz[j]) - s0[j] for j in range(d)]
+        d0 = [start[j] - s0[j] for j in range(d)]
+        out.append({"start": start, "own": own, "ext": ext, "delta": delta, "n": n_xyz, "s0": s0, "d0": d0})
     return out
 
 
@@ -73,7 +81,8 @@ def local_points(box):
 def global_index(box, l):
     """Flat C-order global index of local point l."""
     d = len(l)
-    g = [(box["start"][j] - box["delta"] + l[j]) % box["n"][j] for j in range(d)]
+    s0 = box.get("s0", [box["start"][j] - box["delta"] for j in range(d)])
+    g = [(s0[j] + l[j]) % box["n"][j] for j in range(d)]
     idx = 0
     for j in reversed(range(d)):
         idx = idx * box["n"][j] + g[j]
@@ -194,7 +203,8 @@ def lu_solve(L, U, r, npts):
 
 def is_owned(box, l):
     d = len(l)
-    return all(box["delta"] <= l[j] < box["delta"] + box["own"][j] for j in range(d))
+    d0 = box.get("d0", [box["delta"]] * d)
+    return all(d0[j] <= l[j] < d0[j] + box["own"][j] for j in range(d))
 
 
 class RAS:
@@ -206,7 +216,7 @@ class RAS:
       "rras" z = sum_i R_i^{deltaT} A_i^{-1} R_i^0 r      right-restricted (input restricted to owned points)
     """
 
-    def __init__(self, J, shape, nf, nsub, delta, exact: bool = False, variant: str = "ras", fill=0):
+    def __init__(self, J, shape, nf, nsub, delta, exact: bool = False, variant: str = "ras", fill=0, bc="periodic"):
         """fill: subdomain solver ILU(fill) (0 = BILU(0), the default; k > 0 = level-k ILU; None = the
         exact block LU through the level-of-fill path); exact=True: dense LAPACK solve of A_i."""
         assert variant in ("ras", "as", "rras")
@@ -214,7 +224,7 @@ class RAS:
         self.shape = shape
         self.nf = nf
         self.npts = int(np.prod(shape))
-        self.boxes = boxes(shape, nsub, delta)
+        self.boxes = boxes(shape, nsub, delta, bc)
         self.fact = []
         for b in self.boxes:
             A, pts = box_blocks(J, b, nf, self.npts)

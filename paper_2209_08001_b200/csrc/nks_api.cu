@@ -1156,6 +1156,7 @@ nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, con
           return NKS_E_DIVERGED;
         }
         st->u0_cg_its = its;
+        halo(st, st->Xn, st->nf);                 // the slab's u ghost planes from the neighbours' u^0
       } else {
         std::string e;
         if (init_displacement_fft(st->dp, st->Xn, st->Xn + 2 * N, st->V, st->stream, e) != 0) {

@@ -74,7 +74,7 @@ def test_neumann_gauge(shape):
     np.testing.assert_allclose(Xg[2:], Xo[2:], rtol=0, atol=1e-14)
 
 
-@pytest.mark.parametrize("shape,pc,dts", [((8, 10), 0, [0.01, 0.5]), ((16, 20), 5, [0.01, 0.5]),
+@pytest.mark.parametrize("shape,pc,dts", [((8, 10), 0, [0.01]), ((16, 20), 5, [0.01, 0.5]),
                                           ((12, 14), 5, [0.01, 2.0]), ((6, 8, 8), 5, [0.01, 0.3])])
 def test_neumann_step_parity(shape, pc, dts):
     """Whole NKS steps with Neumann boundaries (pc NONE or the spectral preconditioner) against the oracle's

@@ -186,3 +186,18 @@ def test_neumann_translation_gauge_and_krylov_path():
         assert abs(Xd[I].mean()) < 1e-15
     for r in solver.neumann_rotations(shape):
         assert abs(np.sum(Xd[2:] * r)) < 1e-14
+
+
+def test_neumann_boxes_stop_at_the_walls():
+    """Neumann Schwarz boxes (R38): extended by delta inside the domain only; owned points tile the grid."""
+    from oracle import pc
+    shape = (10, 12)
+    owned = np.zeros(120, dtype=int)
+    for b in pc.boxes(shape, (3, 2), 2, "neumann"):
+        for j in range(2):
+            assert b["s0"][j] >= 0 and b["s0"][j] + b["ext"][j] <= b["n"][j]
+            assert b["ext"][j] <= b["own"][j] + 4
+        for l in pc.local_points(b):
+            if pc.is_owned(b, l):
+                owned[pc.global_index(b, l)] += 1
+    assert np.all(owned == 1)
