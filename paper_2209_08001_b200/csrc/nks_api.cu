@@ -54,6 +54,9 @@ void launch_ras_apply_gen(const BoxSet& B, int nf, long long N, const double* fa
 void launch_assemble(const DevParams& P, const BoxSet& B, int nf, const double* Xa, const double* jac4, double* fac,
                      cudaStream_t s);
 void launch_factor(const BoxSet& B, int nf, double* fac, cudaStream_t s);
+void launch_probe_vector(const DevParams& P, int nf, int q0, int q1, int q2, int f, double* v, cudaStream_t s);
+void launch_probe_scatter(const DevParams& P, const BoxSet& B, int nf, int q0, int q1, int q2, int f, int first,
+                          const double* Jv, double* fac, cudaStream_t s);
 namespace r2 {
 size_t workspace_bytes(const nks_grid& g);
 void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaStream_t stream, std::string& why, bool f32);
@@ -144,8 +147,8 @@ const char* validate(const nks_grid* g, const nks_params* p) {
   if (g->zghost != 0 && (g->zghost < 2 || g->zghost > 8)) return "zghost must be 0 or 2..8";
   if (g->bc != 0 && g->bc != 1) return "bc must be 0 (periodic) or 1 (Neumann)";
   if (g->bc == 1 && g->zghost > 0) return "Neumann boundaries: single-GPU states only";
-  if (g->bc == 1 && p->pc_type != NKS_PC_NONE && p->pc_type != NKS_PC_SPECTRAL)
-    return "Neumann boundaries: pc_type NONE or SPECTRAL (the Schwarz boxes are periodic)";
+  if (g->bc == 1 && (p->pc_type == NKS_PC_RAS_SPECTRAL || p->ilu_level != 0))
+    return "Neumann boundaries: pc_type NONE, SPECTRAL or the Schwarz family with BILU(0) boxes";
   if (g->zghost > 0) {
     if (g->dim != 3) return "z-slab states (zghost > 0) are 3D";
     const int own = g->n[2] - 2 * g->zghost;
@@ -475,7 +478,26 @@ void pc_setup(nks_state* st, const double* Xb) {
       return;
     }
   }
-  {
+  if (st->dp.bc) {
+    // Neumann (R38): the box blocks by probing J with 5^d colours x nf unit fields (precond.cu)
+    const int nq2 = st->d == 3 ? 5 : 1;
+    int first = 1;
+    for (int f = 0; f < st->nf; ++f)
+      for (int q2 = 0; q2 < nq2; ++q2)
+        for (int q1 = 0; q1 < 5; ++q1)
+          for (int q0 = 0; q0 < 5; ++q0) {
+            {
+              PhaseScope ps(st, PH_ASM);
+              launch_probe_vector(st->dp, st->nf, q0, q1, q2, f, st->W2, st->stream);
+              count_launch(st, 1);
+            }
+            jv(st, st->W2, st->Z);
+            PhaseScope ps(st, PH_ASM);
+            launch_probe_scatter(st->dp, st->boxes, st->nf, q0, q1, q2, f, first, st->Z, st->fac, st->stream);
+            count_launch(st, 1);
+            first = 0;
+          }
+  } else {
     PhaseScope ps(st, PH_ASM);
     if (st->boxes.gen) launch_assemble_gen(st->dp, st->boxes, st->nf, st->Xn, st->jac4, st->fac, st->stream);
     else launch_assemble(st->dp, st->boxes, st->nf, st->Xn, st->jac4, st->fac, st->stream);

@@ -85,6 +85,21 @@ static void split_boxes(const nks_grid& g, std::vector<int> (&st)[3], std::vecto
   }
 }
 
+// Extended box along one axis: the owned range [start, start + len) plus `dl` cells per side.  Periodic:
+// always 2 dl more (wrapping; a one-box axis self-overlaps, R20).  Neumann (bc = 1, R38): clipped at the
+// walls.  s0 = global coordinate of local 0 (may be negative on a periodic axis), e = extent, d0 = first
+// owned local index.
+void box_axis(const nks_grid& g, int j, int start, int len, int dl, int& s0, int& e, int& d0) {
+  if (g.bc == 1) {
+    s0 = std::max(start - dl, 0);
+    e = std::min(start + len + dl, g.n[j]) - s0;
+  } else {
+    s0 = start - dl;
+    e = len + 2 * dl;
+  }
+  d0 = start - s0;
+}
+
 long long box_positions(const nks_grid& g) {
   std::vector<int> st[3], ln[3];
   long long P = 0;
@@ -92,8 +107,13 @@ long long box_positions(const nks_grid& g) {
   const int dz = g.dim == 3 ? g.overlap : 0;
   for (int bz = 0; bz < g.nsub[2]; ++bz)
     for (int by = 0; by < g.nsub[1]; ++by)
-      for (int bx = 0; bx < g.nsub[0]; ++bx)
-        P += (long long)(ln[0][bx] + 2 * g.overlap) * (ln[1][by] + 2 * g.overlap) * (ln[2][bz] + 2 * dz);
+      for (int bx = 0; bx < g.nsub[0]; ++bx) {
+        int s0, e[3], d0;
+        box_axis(g, 0, st[0][bx], ln[0][bx], g.overlap, s0, e[0], d0);
+        box_axis(g, 1, st[1][by], ln[1][by], g.overlap, s0, e[1], d0);
+        box_axis(g, 2, st[2][bz], ln[2][bz], dz, s0, e[2], d0);
+        P += (long long)e[0] * e[1] * e[2];
+      }
   return P;
 }
 
@@ -116,10 +136,11 @@ HostBoxes build_boxes_host(const nks_grid& g, const BoxSet& B, const IlukPattern
   for (int bz = 0; bz < g.nsub[2]; ++bz)
     for (int by = 0; by < g.nsub[1]; ++by)
       for (int bx = 0; bx < g.nsub[0]; ++bx) {
-        const int e[3] = {ln[0][bx] + 2 * delta, ln[1][by] + 2 * delta, ln[2][bz] + 2 * dz};
-        const int s0[3] = {st[0][bx] - delta, st[1][by] - delta, st[2][bz] - dz};
+        int e[3], s0[3], d0[3];
+        box_axis(g, 0, st[0][bx], ln[0][bx], delta, s0[0], e[0], d0[0]);
+        box_axis(g, 1, st[1][by], ln[1][by], delta, s0[1], e[1], d0[1]);
+        box_axis(g, 2, st[2][bz], ln[2][bz], dz, s0[2], e[2], d0[2]);
         const int own[3] = {ln[0][bx], ln[1][by], ln[2][bz]};
-        const int d0[3] = {delta, delta, dz};
         const long long np = (long long)e[0] * e[1] * e[2];
         const int nlev = (e[0] - 1) + la * (e[1] - 1) + lb * (e[2] - 1) + 1;
         int ext_q = -1;
@@ -286,6 +307,59 @@ __global__ void k_assemble(DevParams P, SlotTables T, const double* __restrict__
     }
     for (int k = 0; k < nf * nf; ++k) fac[((long long)s * nf * nf + k) * ld + pos] = blk[k];
   }
+}
+
+// ------------------------------------------------------------------------------------------ K4 by probing
+// Assembly of the box blocks from J.v products (Neumann states, reading R38, whose boundary closures the
+// analytic jac_block does not know): with v = e_f on the points whose coordinates are congruent to the colour
+// q modulo 5, (J v)(g) = J(g, g') e_f for the ONE point g' of that colour within the |o|_inf <= 2 footprint of
+// g (J couples only points of the footprint, mirror ghosts included), so 5^d colours x nf fields of J.v give
+// every block column exactly.  No wrap: colours repeat across a periodic seam, so periodic states keep the
+// analytic assembly.
+__global__ void k_probe_vector(DevParams P, int nf, int q0, int q1, int q2, int f, double* __restrict__ v) {
+  const long long N = P.N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nf * N; i += (long long)gridDim.x * blockDim.x) {
+    const int field = (int)(i / N);
+    const long long p = i - field * N;
+    const int x = (int)(p % P.nx), y = (int)((p / P.nx) % P.ny), z = (int)(p / ((long long)P.nx * P.ny));
+    const bool on = field == f && x % 5 == q0 && y % 5 == q1 && (P.dim < 3 || z % 5 == q2);
+    v[i] = on ? 1.0 : 0.0;
+  }
+}
+
+__global__ void k_probe_scatter(DevParams P, int nslots, int nf, int q0, int q1, int q2, int f, int first,
+                                const int* __restrict__ gidx, const int* __restrict__ nbr, long long Ptot, long long ld,
+                                const double* __restrict__ Jv, double* __restrict__ fac) {
+  const long long total = Ptot * nslots;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const long long pos = t % Ptot;
+    const int s = (int)(t / Ptot);
+    const int qp = nbr[(long long)s * Ptot + pos];
+    if (qp < 0) {                                    // outside the box: a zero block, written once
+      if (first)
+        for (int r = 0; r < nf; ++r)
+          for (int c = 0; c < nf; ++c) fac[((long long)(s * nf + r) * nf + c) * ld + pos] = 0.0;
+      continue;
+    }
+    int g = gidx[pos], gq = gidx[qp];
+    if (g < 0) g = ~g;
+    if (gq < 0) gq = ~gq;
+    const int xq = gq % P.nx, yq = (gq / P.nx) % P.ny, zq = gq / (P.nx * P.ny);
+    if (xq % 5 != q0 || yq % 5 != q1 || (P.dim == 3 && zq % 5 != q2)) continue;
+    for (int r = 0; r < nf; ++r) fac[((long long)(s * nf + r) * nf + f) * ld + pos] = Jv[(long long)r * P.N + g];
+  }
+}
+
+void launch_probe_vector(const DevParams& P, int nf, int q0, int q1, int q2, int f, double* v, cudaStream_t s) {
+  const int blocks = (int)std::min<long long>((nf * P.N + 255) / 256, 148 * 16);
+  k_probe_vector<<<blocks, 256, 0, s>>>(P, nf, q0, q1, q2, f, v);
+}
+
+void launch_probe_scatter(const DevParams& P, const BoxSet& B, int nf, int q0, int q1, int q2, int f, int first,
+                          const double* Jv, double* fac, cudaStream_t s) {
+  const long long total = B.P * B.nslots;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 32);
+  k_probe_scatter<<<blocks, 256, 0, s>>>(P, B.nslots, nf, q0, q1, q2, f, first, B.gidx, B.nbr, B.P, B.ld, Jv, fac);
 }
 
 // ------------------------------------------------------------------------------------------ K5 factorisation

@@ -774,14 +774,28 @@ struct Dims {
   int nbox, exmax, eymax, eymin;
 };
 
+}  // namespace r2
+void box_axis(const nks_grid& g, int j, int start, int len, int dl, int& s0, int& e, int& d0);   // precond.cu
+namespace r2 {
+
 static bool dims_of(const nks_grid& g, Dims& D) {
   if (g.dim != 2) return false;
   std::vector<int> st[2], ln[2];
   for (int j = 0; j < 2; ++j) split(g.n[j], g.nsub[j], st[j], ln[j]);
   D.nbox = g.nsub[0] * g.nsub[1];
-  D.exmax = *std::max_element(ln[0].begin(), ln[0].end()) + 2 * g.overlap;
-  D.eymax = *std::max_element(ln[1].begin(), ln[1].end()) + 2 * g.overlap;
-  D.eymin = *std::min_element(ln[1].begin(), ln[1].end()) + 2 * g.overlap;
+  D.exmax = D.eymax = 0;
+  D.eymin = 1 << 30;
+  for (int b = 0; b < g.nsub[0]; ++b) {
+    int s0, e, d0;
+    box_axis(g, 0, st[0][b], ln[0][b], g.overlap, s0, e, d0);
+    D.exmax = std::max(D.exmax, e);
+  }
+  for (int b = 0; b < g.nsub[1]; ++b) {
+    int s0, e, d0;
+    box_axis(g, 1, st[1][b], ln[1][b], g.overlap, s0, e, d0);
+    D.eymax = std::max(D.eymax, e);
+    D.eymin = std::min(D.eymin, e);
+  }
   return true;
 }
 
@@ -887,12 +901,8 @@ void* plan(const nks_grid& g, const BoxSet& B, void* ws, size_t ws_bytes, cudaSt
   for (int by = 0; by < g.nsub[1]; ++by)
     for (int bx = 0; bx < g.nsub[0]; ++bx) {
       Geo q{};
-      q.ex = ln[0][bx] + 2 * g.overlap;
-      q.ey = ln[1][by] + 2 * g.overlap;
-      q.s0x = st[0][bx] - g.overlap;
-      q.s0y = st[1][by] - g.overlap;
-      q.ox0 = g.overlap;
-      q.oy0 = g.overlap;
+      box_axis(g, 0, st[0][bx], ln[0][bx], g.overlap, q.s0x, q.ex, q.ox0);
+      box_axis(g, 1, st[1][by], ln[1][by], g.overlap, q.s0y, q.ey, q.oy0);
       q.ownx = ln[0][bx];
       q.owny = ln[1][by];
       q.lev_off = B.h_box_lev_off[geo.size()];

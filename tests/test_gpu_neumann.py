@@ -115,3 +115,47 @@ def test_neumann_u0_by_conjugate_gradients(shape):
     ug = g.get_state()[2:]
     for I in range(d):
         assert np.linalg.norm(ug[I] - uo[I]) <= 1e-10 * np.linalg.norm(uo[I])
+
+
+@pytest.mark.parametrize("shape,nsub,delta,pc_type,variant", [((40, 36), (3, 2), 2, 2, "ras"), ((20, 24), (1, 1), 2, 2, "ras"),
+                                                           ((9, 10, 11), (2, 1, 2), 1, 2, "ras"),
+                                                           ((16, 18), (2, 2), 2, 3, "as")])
+def test_neumann_schwarz_apply_parity(shape, nsub, delta, pc_type, variant):
+    """Schwarz preconditioners on a Neumann grid: boxes stop at the walls, the box blocks come from probing J
+    with 5^d colours (precond.cu), the 2D boxes run the pipelined apply -- against the oracle's Schwarz
+    apply on the same clipped boxes."""
+    from oracle import pc
+    from paper_2209_08001_b200 import Solver
+    d = len(shape)
+    nf = 2 + d
+    m = omodel(d)
+    Xa, Xb = states(shape)
+    dt = 0.3
+    g = Solver(shape, MODEL, SOL, h=0.25, nsub=nsub, overlap=delta, pc_type=pc_type, bc=1)
+    g.set_fields(Xa[0], Xa[1], Xa[2:])
+    g.pc_setup(Xb, dt)
+    r = ni.random_direction(nf, shape, 14)
+    zg = g.pc_apply(r).cpu().numpy()
+    J = jacobian.assemble(m, Xa, Xb, dt)
+    zo = pc.RAS(J, shape, nf, tuple(reversed(nsub)), delta, variant=variant, bc="neumann").apply(r)
+    assert max(rel(zg, zo)) < 1e-10, rel(zg, zo)
+
+
+@pytest.mark.parametrize("shape,nsub,dts", [((24, 20), (2, 2), [0.01, 0.5]), ((8, 8, 10), (1, 2, 2), [0.01, 0.2])])
+def test_neumann_step_parity_with_ras(shape, nsub, dts):
+    """Whole Neumann steps with the paper's preconditioner (left-RAS, BILU(0) boxes clipped at the walls)."""
+    from paper_2209_08001_b200 import Solver
+    d = len(shape)
+    m = omodel(d)
+    c, eta = ni.initial_fields(shape, 0)
+    cbar = c.mean()
+    Xo = np.concatenate([c[None], eta[None], solver.init_displacement(m, c, cbar)])
+    g = Solver(shape, MODEL, SOL, h=0.25, nsub=nsub, overlap=2, pc_type=2, bc=1)
+    g.set_fields(c, eta, None)                   # u^0 by CG on the elastic block
+    for dt in dts:
+        Xo, info_o = solver.newton_step(m, Xo, dt, cbar, SOL)
+        info_g = g.step(dt)
+        Xg = g.get_state()
+        r = [float(np.linalg.norm(Xg[f] - Xo[f]) / np.linalg.norm(Xo[f])) for f in range(2 + d)]
+        assert max(r) <= 1e-8, (dt, r)
+        assert info_g["energy"] == pytest.approx(scheme.energy(m, Xo, cbar), rel=1e-10)
