@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(256) k_biluk(GenTables T, const int* __restric
 
 // Level-synchronous Schwarz apply with ILU(k) box solves: one warp per row, lanes over the row's slots.
 template <int NF>
-__global__ void __launch_bounds__(256) k_ras_apply_gen(GenTables T, const int* __restrict__ gidx,
+__global__ void __launch_bounds__(1024) k_ras_apply_gen(GenTables T, const int* __restrict__ gidx,
                                                        const int* __restrict__ nbr, const int* __restrict__ box_lev_off,
                                                        const int* __restrict__ lev_ptr,
                                                        const int* __restrict__ box_pos_off, long long Ptot, long long ld,
@@ -446,10 +446,11 @@ void launch_ras_apply_gen(const BoxSet& B, int nf, long long N, const double* fa
                           double* z, cudaStream_t s) {
   const GenTables T = gen_tables(B);
   if (nf == 4)
-    k_ras_apply_gen<4><<<B.nbox, 256, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, B.ld, N, fac,
+    // one warp per row of a wavefront level: 32 warps cover a 2D level (~ex/a rows) in one or two rounds
+    k_ras_apply_gen<4><<<B.nbox, 1024, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, B.ld, N, fac,
                                                r, y, z, B.variant);
   else
-    k_ras_apply_gen<5><<<B.nbox, 256, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, B.ld, N, fac,
+    k_ras_apply_gen<5><<<B.nbox, 1024, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off, B.P, B.ld, N, fac,
                                                r, y, z, B.variant);
   if (B.variant != 0) {
     const int blocks = (int)std::min<long long>((N + 255) / 256, 148 * 8);
