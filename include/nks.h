@@ -199,6 +199,21 @@ NKS_API nks_status nks_get_unique_id(uint8_t id[128]);
 NKS_API nks_status nks_decompose(const nks_grid* global, const nks_params* params, int32_t rank, int32_t nranks,
                                  nks_grid* local);
 
+/* One message of a z-slab halo exchange: kind 0 = send, 1 = receive; peer rank; offset (doubles from the
+ * vector's start, field f at f * n[0]*n[1]*n[2]) and count of a contiguous run of planes. */
+typedef struct {
+  int32_t kind;
+  int32_t peer;
+  int64_t offset;
+  int64_t count;
+} nks_halo_msg;
+
+/* The ordered halo message list the library issues (grouped ncclSend/ncclRecv, matched per peer in issue order)
+ * for a slab grid from nks_decompose -- host only, no GPU.  Writes up to cap messages, returns how many the
+ * exchange has (4 per field), or -1 on invalid input. */
+NKS_API int32_t nks_halo_plan(const nks_grid* local, int32_t rank, int32_t nranks, int32_t nfields, nks_halo_msg* out,
+                              int32_t cap);
+
 /* Create a state on the current CUDA device.
  *   grid: the whole periodic grid (zghost = 0; then rank = 0, nranks = 1), or this rank's z-slab from
  *         nks_decompose (zghost > 0).

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "nks_internal.cuh"
 
@@ -96,24 +97,38 @@ void nccl_destroy(void* c) {
   delete C;
 }
 
+// The halo exchange as an ordered message list (host only; exported as nks_halo_plan so that the CPU tests run
+// the very same plan over gloo): per field, send the first own planes down, the last own planes up, receive the
+// top ghosts from up, the bottom ghosts from down.  NCCL pairs the messages between two ranks in issue order,
+// so with two ranks (up == down) the first send (own_lo) meets the peer's first receive (its top ghosts) and the
+// second (own_hi) its second (its bottom ghosts) -- the planes the periodic neighbours need.
+void halo_plan(int rank, int nranks, int nf, long long fstride, int nzl, long long nxy, int zg,
+               std::vector<nks_halo_msg>& out) {
+  const int up = (rank + 1) % nranks, dn = (rank + nranks - 1) % nranks;
+  const long long cnt = (long long)zg * nxy;
+  out.clear();
+  for (int f = 0; f < nf; ++f) {
+    const long long base = (long long)f * fstride;
+    out.push_back({0, dn, base + (long long)zg * nxy, cnt});               // own_lo -> rank-1's top ghosts
+    out.push_back({0, up, base + (long long)(nzl - 2 * zg) * nxy, cnt});   // own_hi -> rank+1's bottom ghosts
+    out.push_back({1, up, base + (long long)(nzl - zg) * nxy, cnt});       // top ghosts <- rank+1's own_lo
+    out.push_back({1, dn, base, cnt});                                     // bottom ghosts <- rank-1's own_hi
+  }
+}
+
 // Fill the zg ghost planes on both z sides of nf fields (field f at vec + f * fstride, local (nzl, nxy)).
 int nccl_halo(void* c, double* vec, int nf, long long fstride, int nzl, long long nxy, int zg, cudaStream_t s) {
   NcclComm* C = (NcclComm*)c;
-  const int up = (C->rank + 1) % C->nranks, dn = (C->rank + C->nranks - 1) % C->nranks;
-  const size_t cnt = (size_t)zg * nxy;
+  std::vector<nks_halo_msg> plan;
+  halo_plan(C->rank, C->nranks, nf, fstride, nzl, nxy, zg, plan);
   if (ncclGroupStart() != ncclSuccess) return 1;
-  for (int f = 0; f < nf; ++f) {
-    double* base = vec + (long long)f * fstride;
-    double* own_lo = base + (long long)zg * nxy;                 // first own planes -> rank-1's top ghosts
-    double* own_hi = base + (long long)(nzl - 2 * zg) * nxy;     // last own planes -> rank+1's bottom ghosts
-    double* gh_lo = base;
-    double* gh_hi = base + (long long)(nzl - zg) * nxy;
-    // per peer, NCCL matches sends and receives in issue order: with two ranks (up == dn) the first send
-    // (own_lo) meets the peer's first receive (gh_hi), the second (own_hi) its second (gh_lo)
-    if (ncclSend(own_lo, cnt, ncclDouble, dn, C->comm, s) != ncclSuccess) return 1;
-    if (ncclSend(own_hi, cnt, ncclDouble, up, C->comm, s) != ncclSuccess) return 1;
-    if (ncclRecv(gh_hi, cnt, ncclDouble, up, C->comm, s) != ncclSuccess) return 1;
-    if (ncclRecv(gh_lo, cnt, ncclDouble, dn, C->comm, s) != ncclSuccess) return 1;
+  for (const auto& m : plan) {
+    const ncclResult_t r = m.kind == 0 ? ncclSend(vec + m.offset, (size_t)m.count, ncclDouble, m.peer, C->comm, s)
+                                       : ncclRecv(vec + m.offset, (size_t)m.count, ncclDouble, m.peer, C->comm, s);
+    if (r != ncclSuccess) {
+      ncclGroupEnd();
+      return 1;
+    }
   }
   return ncclGroupEnd() == ncclSuccess ? 0 : 1;
 }

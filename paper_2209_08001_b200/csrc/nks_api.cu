@@ -84,6 +84,8 @@ void launch_gauge_neumann(const DevParams& P, double* X, double* part, double* o
 // comm.cu
 int slab_decompose(const nks_grid& global, int pc_type, int rank, int nranks, nks_grid& local, int& z_offset);
 int nccl_unique_id(uint8_t id[128]);
+void halo_plan(int rank, int nranks, int nf, long long fstride, int nzl, long long nxy, int zg,
+               std::vector<nks_halo_msg>& out);
 void* nccl_create(const uint8_t id[128], int rank, int nranks, std::string& err);
 void nccl_destroy(void* c);
 int nccl_halo(void* c, double* vec, int nf, long long fstride, int nzl, long long nxy, int zg, cudaStream_t s);
@@ -1216,6 +1218,16 @@ nks_status nks_set_comm(nks_state* st, nks_allreduce_fn allreduce, nks_halo_fn h
   st->comm_set = true;
   st->pc_valid = false;
   return NKS_OK;
+}
+
+int32_t nks_halo_plan(const nks_grid* local, int32_t rank, int32_t nranks, int32_t nfields, nks_halo_msg* out,
+                      int32_t cap) {
+  if (!local || local->zghost <= 0 || nranks < 1 || rank < 0 || rank >= nranks || nfields < 1) return -1;
+  std::vector<nks_halo_msg> plan;
+  const long long nxy = (long long)local->n[0] * local->n[1];
+  halo_plan(rank, nranks, nfields, nxy * local->n[2], local->n[2], nxy, local->zghost, plan);
+  for (int k = 0; k < (int)plan.size() && k < cap && out; ++k) out[k] = plan[k];
+  return (int32_t)plan.size();
 }
 
 nks_status nks_get_unique_id(uint8_t id[128]) {

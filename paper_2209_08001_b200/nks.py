@@ -46,6 +46,10 @@ class Params(C.Structure):
     ]
 
 
+class HaloMsg(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("peer", C.c_int32), ("offset", C.c_int64), ("count", C.c_int64)]
+
+
 class StepInfo(C.Structure):
     _fields_ = [
         ("converged", C.c_int32), ("reason", C.c_int32), ("newton_its", C.c_int32), ("gmres_its", C.c_int32),
@@ -73,6 +77,7 @@ _SIGS = {
                              C.POINTER(_P)]),
     "nks_get_unique_id": (C.c_int, [_P]),
     "nks_decompose": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), C.c_int32, C.c_int32, C.POINTER(Grid)]),
+    "nks_halo_plan": (C.c_int32, [C.POINTER(Grid), C.c_int32, C.c_int32, C.c_int32, C.POINTER(HaloMsg), C.c_int32]),
     "nks_set_fields": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
     "nks_get_fields": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
     "nks_set_state": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
@@ -147,6 +152,17 @@ def unique_id() -> bytes:
     if rc != NKS_OK:
         raise NKSError(rc, "nks_get_unique_id failed")
     return buf.raw
+
+
+def halo_plan(local: Grid, rank: int, nranks: int, nfields: int):
+    """nks_halo_plan: the ordered (kind, peer, offset, count) messages of the library's halo exchange (host only)."""
+    lib = load_library()
+    n = lib.nks_halo_plan(C.byref(local), int(rank), int(nranks), int(nfields), None, 0)
+    if n < 0:
+        raise NKSError(NKS_E_INVALID, "nks_halo_plan: invalid slab")
+    buf = (HaloMsg * n)()
+    lib.nks_halo_plan(C.byref(local), int(rank), int(nranks), int(nfields), buf, n)
+    return [(m.kind, m.peer, m.offset, m.count) for m in buf]
 
 
 def decompose(global_grid: Grid, params: Params, rank: int, nranks: int) -> Grid:

@@ -115,3 +115,55 @@ def test_box_slab_bounds_keep_whole_boxes():
             assert all(b[r][1] == b[r + 1][0] for r in range(world - 1))
             assert all(lo in starts and hi in starts for lo, hi, _ in b)
             assert sum(k for _, _, k in b) == nb
+
+
+# ---------------------------------------------------------------------------------------- the library's own plan
+def _plan_worker(rank, world, port, out):
+    """Each rank takes its slab from the library (nks_decompose) and executes the library's halo message list
+    (nks_halo_plan -- the ncclSend/ncclRecv sequence the library issues) over gloo.  NCCL pairs the messages of
+    two ranks in issue order; gloo pairs them by tag, so the k-th message between a given sender and receiver
+    gets tag k on both sides -- the same matching."""
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        import nks_inputs as ni
+        from paper_2209_08001_b200 import nks
+        nz, ny, nx, nf = 24, 6, 5, 5
+        params = nks.make_params(ni.model_default(), ni.solver_default())
+        lg = nks.decompose(nks.make_grid((nz, ny, nx), 0.25, (world * 2, 1, 1), 2), params, rank, world)
+        zg, nzl = lg.zghost, lg.n[2]
+        g = np.random.default_rng(7).standard_normal((nf, nz, ny, nx))
+        idx = [(z % nz) for z in range(lg.z_offset - zg, lg.z_offset - zg + nzl)]
+        want = g[:, idx]
+        vec = torch.from_numpy(want.copy()).reshape(-1)
+        flat = vec.view(nf, nzl, ny, nx)
+        flat[:, :zg] = np.nan
+        flat[:, -zg:] = np.nan
+        plan = nks.halo_plan(lg, rank, world, nf)
+        assert len(plan) == 4 * nf
+        seq_send, seq_recv, reqs = {}, {}, []
+        for kind, peer, off, cnt in plan:
+            if kind == 0:
+                tag = seq_send.get(peer, 0)
+                seq_send[peer] = tag + 1
+                reqs.append(dist.isend(vec[off:off + cnt].clone(), peer, tag=tag))
+            else:
+                tag = seq_recv.get(peer, 0)
+                seq_recv[peer] = tag + 1
+                buf = torch.empty(cnt, dtype=vec.dtype)
+                reqs.append((dist.irecv(buf, peer, tag=tag), off, buf))
+        for r in reqs:
+            if isinstance(r, tuple):
+                r[0].wait()
+                vec[r[1]:r[1] + r[2].numel()] = r[2]
+            else:
+                r.wait()
+        out[rank] = float(np.abs(vec.view(nf, nzl, ny, nx).numpy() - want).max())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_library_halo_plan_over_gloo(world):
+    out = mp.Manager().dict()
+    mp.spawn(_plan_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert all(out[r] == 0.0 for r in range(world)), dict(out)
