@@ -249,11 +249,13 @@ static void dcgs_dot(long long n, int nk, const double* V, long long ld, const d
                      double* out, unsigned* counter, cudaStream_t s) {
   const bool v2 = vec2(n, ld);
   const long long m = v2 ? n / 2 : n;
-  const int ng = std::max(1, (nk + 7) / 8);
-  const int nbx = (int)std::min<long long>((m + 255) / 256, 4 * 148 / ng);   // part holds kRedBlocks rows
+  // 4 columns per group: 10 accumulators and 6 loads in flight per thread keep the registers (and so the
+  // occupancy) of a streaming kernel; u and w are re-read per group from L2
+  const int ng = std::max(1, (nk + 3) / 4);
+  const int nbx = (int)std::min<long long>((m + 255) / 256, std::max(4 * 148 / ng, 74));   // part: kRedBlocks rows
   const dim3 grid(nbx, ng);
-  if (v2) k_dcgs_dot<8, 2><<<grid, 256, 0, s>>>(n, nk, V, ld, u, w, part);
-  else k_dcgs_dot<8, 1><<<grid, 256, 0, s>>>(n, nk, V, ld, u, w, part);
+  if (v2) k_dcgs_dot<4, 2><<<grid, 256, 0, s>>>(n, nk, V, ld, u, w, part);
+  else k_dcgs_dot<4, 1><<<grid, 256, 0, s>>>(n, nk, V, ld, u, w, part);
   k_dcgs_final<<<kDOut, 256, 0, s>>>(part, nbx, nk, out);
   (void)counter;
 }
