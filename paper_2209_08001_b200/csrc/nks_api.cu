@@ -549,6 +549,9 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
   double beta = bnorm;
   bool first = true;
   int stall = 0;
+  constexpr int kProjWin = 5;                 // restart cycles in the projection's rate window
+  std::vector<double> hist(1, bnorm);         // true residual at the start of every cycle
+  std::vector<int> hits(1, 0);                // ... and the iterations done before it
   while (true) {
     if (beta <= tol) return 0;
     {
@@ -699,13 +702,21 @@ int gmres(nks_state* st, const double* b, double bnorm, double* s, double tol, i
       // to gmres_maxit.  Off by default (the paper's solver fails only at its iteration limit).
       stall = (beta > 0.999 * prev) ? stall + 1 : 0;
       if (st->prm.gmres_stall_cycles > 0 && stall >= st->prm.gmres_stall_cycles) return 2;
-      // Projection (opt-in, the same parameter): after at least gmres_stall_cycles cycles, the mean
-      // convergence rate of this solve so far projects the iterations still needed; a solve that would not
-      // reach tol within gmres_maxit is reported now instead of after running to the limit.
+      // Projection (opt-in, the same parameter): after at least gmres_stall_cycles cycles, the convergence
+      // rate of the last kProjWin restart cycles (all cycles while fewer) projects the iterations still
+      // needed; a solve that would not reach tol within gmres_maxit even at twice that rate is reported now
+      // instead of after running to the limit.  Restarted GMRES slows down as it stagnates, so the recent
+      // rate is the faithful estimate (the mean since the start carries the first cycles' fast drop: at
+      // config 2 it let a solve that fails at gmres_maxit run 4,350 iterations before being rejected); the
+      // factor 2 keeps a margin for a solve that speeds up again (R18, profiles/r02_attempts*).
+      hist.push_back(beta);
+      hits.push_back(its);
       if (st->prm.gmres_stall_cycles > 0 && its >= st->prm.gmres_stall_cycles * m && beta > tol) {
-        const double rate = std::log(beta / bnorm) / its;              // < 0 while converging
+        const int cyc = (int)hist.size() - 1;                          // hist[0] = bnorm
+        const int w = std::min(cyc, kProjWin);
+        const double rate = std::log(beta / hist[cyc - w]) / (double)std::max(1, its - hits[cyc - w]);   // < 0: converging
         const double need = rate < 0.0 ? std::log(tol / beta) / rate : 1e300;
-        if (its + need > (double)st->prm.gmres_maxit) return 3;
+        if (its + 0.5 * need > (double)st->prm.gmres_maxit) return 3;
       }
     }
     // V already holds r; scale below uses V as source (first == false)

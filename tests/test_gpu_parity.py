@@ -275,6 +275,37 @@ def test_bilu0_breakdown_is_reported_as_divergence():
     np.testing.assert_array_equal(g.get_state(), X0)
 
 
+def test_early_divergence_rule_keeps_the_controllers_decisions():
+    """The opt-in early-divergence rule (gmres_stall_cycles = 3, R18) must only cut work: from the
+    state after three adaptive steps at 128^2 (4x4 boxes, BILU(0)), every forced attempt has the same outcome
+    as with the rule off (the paper's solver, which fails only at gmres_maxit): the accepted ones bit for bit
+    (same GMRES count, same fields), the rejected ones earlier than at gmres_maxit."""
+    shape = (128, 128)
+    c, eta = ni.initial_fields(shape, 0)
+    on = gpu_solver(shape, nsub=(4, 4), sol={"gmres_stall_cycles": 3})
+    off = gpu_solver(shape, nsub=(4, 4), sol={"gmres_stall_cycles": 0})
+    on.set_fields(c, eta, None)
+    on.run_adaptive(3)
+    X = on.get_state()
+    outcomes = []
+    for dt in (0.986, 1.414, 2.0):
+        res = []
+        for g in (on, off):
+            g.set_state(X[0], X[1], X[2:])
+            info = g.step(dt, raise_on_fail=False)
+            res.append((info, g.get_state()))
+        (i_on, X_on), (i_off, X_off) = res
+        assert i_on["status"] == i_off["status"], (dt, i_on, i_off)
+        if i_off["status"] == "OK":
+            assert i_on["gmres_its"] == i_off["gmres_its"]
+            np.testing.assert_array_equal(X_on, X_off)
+        else:
+            assert i_off["reason"] == "gmres_maxit" and i_on["reason"] in ("gmres_stagnation", "gmres_projected")
+            assert i_on["gmres_its"] < i_off["gmres_its"]
+        outcomes.append(i_off["status"])
+    assert "OK" in outcomes and "DIVERGED" in outcomes, outcomes     # both branches exercised
+
+
 def test_step_parity_3d():
     _run_parity((10, 12, 12), [0.01, 0.3], (1, 2, 2), 2)
 

@@ -2,7 +2,7 @@
 same X^n at each trial dt (the accepted one and the rejected ones the controller tries first), reporting
 Newton / GMRES iterations, the failure reason and the wall time; for gmres_stall_cycles in STALL.
 
-    STALL=3,2 python tools/attempt_cost.py
+    STALL=3,0 DTS=2,1.414,1 NKS_DEBUG=1 python tools/attempt_cost.py   (NKS_DEBUG: per-cycle GMRES residuals on stderr)
 """
 import os
 import sys
@@ -27,7 +27,7 @@ for stall in [int(s) for s in os.environ.get("STALL", "3").split(",")]:
         print(f"warm-up step: dt {r['dt']:.4f} retries {r['retries']} newton {r['newton_its']} gmres {r['gmres_its']}",
               flush=True)
     X = g.get_state()
-    for dt in (2.0, 2.0 / 2 ** 0.5, 1.0, 0.5):
+    for dt in [float(x) for x in os.environ.get("DTS", "2.0,1.41421356,1.0").split(",")]:
         g.set_state(X[0], X[1], X[2:])
         torch.cuda.synchronize()
         t0 = time.perf_counter()
