@@ -55,6 +55,11 @@ template <bool F32> struct Strm {
 #ifndef NKS_R2_G
 #define NKS_R2_G 2
 #endif
+// factor stream transport: 1 = 16-byte cp.async by the producer warp's 32 lanes (requests of one SM overlap),
+// 0 = one 1D bulk copy per group (cp.async.bulk; the copies of one SM complete one after another)
+#ifndef NKS_R2_LDGSTS
+#define NKS_R2_LDGSTS 0      // measured: 1 is 1.5x slower at config 2 (the producer's issue loop sits on the step path)
+#endif
 #ifndef NKS_R2_NS
 #define NKS_R2_NS 4
 #endif
@@ -108,6 +113,7 @@ struct Args {
 #endif
 __device__ long long g_prof[1024 * 8];
 __device__ long long g_gt[72 * 8];
+__device__ long long g_st[2][5][32][2];   // NKS_RAS2D_PROF: CTA 0, sweep, warp (4 = producer), steps 40..71: barrier arrive / release clocks
 __device__ long long g_cp[64 * 4];   // NKS_RAS2D_PROF: CTA 0 producer, groups 8..71: issue / first test / ready clocks   // NKS_RAS2D_PROF: CTA 0, warp 0, forward groups 8..15: per-phase clocks
 
 __device__ __forceinline__ int jmin_of(int t, int ex) { return max(0, (t - ex + 2) >> 1); }
@@ -293,7 +299,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   for (int k = tid; k <= nFp; k += blockDim.x) off[k] = off_g[k];
   if (tid == 0) {
     for (int k = 0; k < kNSW; ++k) {
-      mbar_init(&fullb[k], 1);
+      mbar_init(&fullb[k], NKS_R2_LDGSTS ? 32 : 1);   // LDGSTS: one arrive.noinc per producer lane
       mbar_init(&emptyb[k], NCW);     // one arrive per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -341,15 +347,26 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       const int r_lo = off[k0];
       const int nrows = max(1, off[k0 + kG] - r_lo);
       const int pf = fw ? kPF : kPB;
-      const T* src = fw ? (const T*)A.chunkF + (base + r_lo) * kPF : (const T*)A.chunkB + (base + r_lo) * kPB;
+      const int r_src = (R2_DBG(A) & 512) ? 0 : r_lo;     // ablation: every group copies the stream's first rows (L2-resident)
+      const T* src = fw ? (const T*)A.chunkF + (base + r_src) * kPF : (const T*)A.chunkB + (base + r_src) * kPB;
       const unsigned bytes = (unsigned)(nrows * pf * sizeof(T));
       const unsigned bar = full0 + (q % kNSW) * 8;
-      if (R2_PROF(A) && blockIdx.x == 0 && q >= 8 && q < 72) g_cp[(q - 8) * 4] = clock64();
+      if (R2_PROF(A) && blockIdx.x == 0 && lane == 0 && q >= 8 && q < 72) g_cp[(q - 8) * 4] = clock64();
+      const unsigned dst = stage0 + (unsigned)((q % kNSW) * stage_elems * sizeof(T));
+#if NKS_R2_LDGSTS
+      // all 32 lanes: 16-byte cp.async (LDGSTS) over the group's contiguous bytes, then one
+      // arrive.noinc each, so the full barrier (count 32) completes when every lane's copies have landed
+      const char* s8 = reinterpret_cast<const char*>(src);
+#pragma unroll 4
+      for (unsigned o = (unsigned)lane * 16u; o < bytes; o += 512u)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + o), "l"(s8 + o) : "memory");
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+#else
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       stage0 + (unsigned)((q % kNSW) * stage_elems * sizeof(T))),
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                    "l"(src), "r"(bytes), "r"(bar)
                    : "memory");
+#endif
     };
     auto test_bar = [&](unsigned bar, unsigned par) -> bool {
       unsigned ok;
@@ -379,7 +396,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
           unsigned sp = 0;
           while (!test_bar(bar, par)) if (++sp > (1u << 26)) __trap();
         }
-        if (lane == 0) issue_one(issued);
+        if (NKS_R2_LDGSTS || lane == 0) issue_one(issued);
         __syncwarp();
         ++issued;
       }
@@ -442,10 +459,20 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     ensure(gof(2));
     poll3(up_remote, 1, 0, 0, 0, 0, 1);
     step_bar();
+    auto step_bar_p = [&](int sw, int k) {        // NKS_RAS2D_PROF: barrier arrive / release clocks
+      if (R2_PROF(A) && blockIdx.x == 0 && k >= 40 && k < 72) {
+        const long long a = clock64();
+        step_bar();
+        const long long r = clock64();
+        if (lane == 0) { g_st[sw][4][k - 40][0] = a; g_st[sw][4][k - 40][1] = r; }
+      } else {
+        step_bar();
+      }
+    };
     for (int k = 0; k < nFp; ++k) {
       ensure_fast(gof(k + 3));
       if (up_remote) poll1(qf, k + dcf);
-      step_bar();
+      step_bar_p(0, k);
     }
     // ---- backward: prologue barrier, then one barrier per step (processing p = nFp .. 2 nFp - 1)
     const int dR = 2 * (R - 1);
@@ -460,7 +487,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       const int p = 2 * nFp - 1 - k;
       ensure_fast(gof(p + 3));
       if (dn_remote) poll1(qb, k - dR + dcb);
-      step_bar();
+      step_bar_p(1, p - nFp);
     }
   } else {
     // ================================================================ consumers
@@ -501,6 +528,16 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(empty0 + (q % kNSW) * 8) : "memory");
     };
     auto step_bar = [&]() { asm volatile("bar.sync 1, 160;" ::: "memory"); };
+    auto step_bar_c = [&](int sw, int k) {        // NKS_RAS2D_PROF: barrier arrive / release clocks
+      if (R2_PROF(A) && blockIdx.x == 0 && k >= 40 && k < 72) {
+        const long long a = clock64();
+        step_bar();
+        const long long r = clock64();
+        if (lane == 0) { g_st[sw][w][k - 40][0] = a; g_st[sw][w][k - 40][1] = r; }
+      } else {
+        step_bar();
+      }
+    };
     auto e_bar = [&]() { asm volatile("bar.sync 3, 128;" ::: "memory"); };
     // this lane's block row c of step k (processing step p) in its group's buffer; nullptr-safe row 0
     auto rowp = [&](int k, int p, int pf) -> const T* {
@@ -602,7 +639,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       auto fiter = [&](int k, double r2, FRows& cur, FRows& nxt) {
         const int i = k - 2 * rl;
         const bool active = row_ok && (unsigned)i < (unsigned)ex;
-        step_bar();                                                   // E[k-1] complete; stages/cells ready
+        step_bar_c(0, k);                                             // E[k-1] complete; stages/cells ready
         double Ya1[4], yp[4], aa4[4];
         ld4a(rl >= 1 ? ering(k - 1, rl - 1) : hcella(1, k + 1), rl >= 1 ? kEPB : 16u, Ya1);   // (i+1, j-1) at step k-1
         ld4a(ering(k - 1, rl), kEPB, yp);                                                     // own row at step k-1
@@ -704,7 +741,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         const int i = k - 2 * rl;
         const bool active = row_ok && (unsigned)i < (unsigned)ex;
         const int iR = k - dR;
-        step_bar();                                                   // E[k+1] complete; stages/cells ready
+        step_bar_c(1, nFp - 1 - k);                                   // E[k+1] complete; stages/cells ready
         double Xb1[4], xp[4], bb4[4];
         ld4a(rl <= R - 2 ? ering(k + 1, rl + 1) : hcella(2, iR - 1), rl <= R - 2 ? kEPB : 16u, Xb1);   // (i-1, j+1) at step k+1
         ld4a(ering(k + 1, rl), kEPB, xp);                                                              // own row at step k+1
@@ -994,6 +1031,25 @@ cudaError_t launch_apply(void* plan, const double* r, double* z, cudaStream_t s)
       for (int c = 0; c < std::min(nc, 2 * P->CS); ++c)
         std::fprintf(stderr, "  cta %2d (stripe %d): fwd %lld cyc, bwd %lld cyc, start +%lld ns, end +%lld ns\n", c,
                      c % P->CS, h[c * 8], h[c * 8 + 1], h[c * 8 + 4] - tmin, h[c * 8 + 5] - tmin);
+      // CTA 0, steps 40..71 of each sweep: per warp, work = arrive(k) - release(k-1), wait = release(k) - arrive(k)
+      std::vector<long long> st(2 * 5 * 32 * 2);
+      cudaMemcpyFromSymbol(st.data(), g_st, st.size() * 8);
+      auto S = [&](int sw, int w, int k, int x) { return st[((sw * 5 + w) * 32 + k) * 2 + x]; };
+      for (int sw = 0; sw < 2; ++sw) {
+        std::fprintf(stderr, "  cta 0 %s steps 41..71, cycles per step (mean): ", sw ? "bwd" : "fwd");
+        for (int w = 0; w < 5; ++w) {
+          double work = 0, wait = 0;
+          for (int k = 1; k < 32; ++k) { work += S(sw, w, k, 0) - S(sw, w, k - 1, 1); wait += S(sw, w, k, 1) - S(sw, w, k, 0); }
+          std::fprintf(stderr, "%s work %.0f wait %.0f; ", w == 4 ? "producer" : ("warp " + std::to_string(w)).c_str(), work / 31, wait / 31);
+        }
+        std::fprintf(stderr, "period %.0f\n", (double)(S(sw, 0, 31, 1) - S(sw, 0, 0, 1)) / 31);
+        for (int k = 8; k < 12; ++k) {
+          std::fprintf(stderr, "    step %d:", 40 + k);
+          for (int w = 0; w < 5; ++w)
+            std::fprintf(stderr, " w%d arrive %+lld", w, S(sw, w, k, 0) - S(sw, 0, k - 1, 1));
+          std::fprintf(stderr, " release %+lld\n", S(sw, 0, k, 1) - S(sw, 0, k - 1, 1));
+        }
+      }
     }
   }
   return e;

@@ -26,7 +26,10 @@ def main():
     build()
     shape = (512, 512)
     c, eta = ni.initial_fields(shape, 0)
-    for nsub in ((4, 4), (8, 8), (16, 16), (32, 4), (32, 8), (4, 32), (2, 2)):
+    grid = ((4, 4), (8, 8), (16, 16), (32, 4), (32, 8), (4, 32), (2, 2))
+    if os.environ.get("NSUBS"):                  # e.g. NSUBS="4,4;32,4"
+        grid = tuple(tuple(int(v) for v in t.split(",")) for t in os.environ["NSUBS"].split(";"))
+    for nsub in grid:
         delta = 2
         g = Solver(shape, ni.model_default(), ni.solver_default(), nsub=nsub, overlap=delta)
         g.set_fields(c, eta, None)
