@@ -256,8 +256,6 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   using T = typename S::T;
   constexpr int kPF = S::PF, kPB = S::PB, kG = S::G, kNSW = S::NS;
   constexpr int NCW = 4;                      // consumer warps; the producer is warp NCW
-  constexpr int NT = 32 * (NCW + 1);          // threads on the step barrier
-  constexpr int kRel = 2;                     // group g is released in iteration g kG + kG - kRel
   extern __shared__ __align__(128) unsigned char smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const int s = (int)cluster.block_rank();
@@ -328,7 +326,9 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   // [klo(q), klo(q) + kG); one extra dummy group lets the consumer look one group past the end
   auto klo = [&](int q) { return q < nGr ? q * kG : nFp - kG * (q - nGr + 1); };
 
-  // Step barrier: the 4 consumer warps and the producer warp meet once per step (barrier 1, 160
+  // Step barrier: the 4 consumer warps meet once per step (barrier 1, 128 threads); the producer is
+  // not on it (round 2: taking it off cut the step from ~840 to ... cycles).  Old comment kept for the
+  // history of the gatekeeper design:
   // threads).  Before arriving for step p the producer has made the factor groups the consumers will
   // read during step p resident (mbarrier waits) and has seen the halo cells they will read written
   // (sentinel polls), so the consumers themselves never wait on an mbarrier or poll: their loop is
@@ -337,10 +337,12 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   auto gof = [&](int p) { return p / kG; };   // group of processing step p (forward k = p, backward k = 2 nFp - 1 - p)
 
   if (w == NCW) {
-    // ================================================================ producer / gatekeeper
+    // ================================================================ producer (off the step path)
+    // The consumers synchronise among themselves (barrier 1, 128 threads), wait on a group's full
+    // mbarrier once per group and poll the halo cells themselves one step ahead; the producer only
+    // refills the ring: group q goes out as soon as the consumers have released group q - kNSW.
     const unsigned full0 = smem_u32(fullb), empty0 = smem_u32(emptyb), stage0 = smem_u32(stage);
     const long long base = sb * RPC * A.exmax;
-    int issued = 0, ready = -1;
     auto issue_one = [&](int q) {
       const bool fw = q < nGr;
       const int k0 = klo(q);
@@ -368,127 +370,28 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
                    : "memory");
 #endif
     };
-    auto test_bar = [&](unsigned bar, unsigned par) -> bool {
-      unsigned ok;
-      asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-                   : "=r"(ok) : "r"(bar), "r"(par) : "memory");
-      return __all_sync(0xffffffffu, ok);
-    };
-    // Step barriers passed so far.  Group g covers processing steps [g kG, g kG + kG) of both sweeps and
-    // is released (empty-barrier arrive) by every consumer warp inside iteration p = g kG + kG - 2, which
-    // starts after step barrier p + 1 and ends before barrier p + 2 (forward; backward p + 2 / p + 3, its
-    // prologue barrier comes first).  So once the producer has passed barrier p + 2 (p + 3) the buffer
-    // is free without testing the mbarrier (a test_wait costs ~150 cycles and sat on the producer's
-    // per-step path); the mbarrier test remains only as the blocking fallback.
-    int nbars = 0;
-    auto freed = [&](int g) {
-      const int pr = g * kG + kG - kRel;
-      return nbars >= pr + 3 + (pr >= nFp ? 1 : 0);
-    };
-    // issue groups in order up to G; blocking: wait for the buffer, else stop at the first busy one
-    auto issue_upto = [&](int G, bool block) {
-      G = min(G, 2 * nGr - 1);
-      while (issued <= G) {
-        const int st = issued % kNSW, use = issued / kNSW;
-        if (use > 0 && !freed(issued - kNSW)) {
-          if (!block) break;              // opportunistic issue: by the barrier count only (no test_wait)
-          const unsigned bar = empty0 + st * 8, par = (unsigned)((use - 1) & 1);
-          unsigned sp = 0;
-          while (!test_bar(bar, par)) if (++sp > (1u << 26)) __trap();
-        }
-        if (NKS_R2_LDGSTS || lane == 0) issue_one(issued);
-        __syncwarp();
-        ++issued;
-      }
-    };
-    auto ensure = [&](int G) {          // groups <= G resident
-      if ((R2_DBG(A) & 128) && issued > 0) return;   // ablation: no copy management after the first groups
-      G = min(G, 2 * nGr - 1);
-      if (issued <= G) issue_upto(G, true);
-      while (ready < G) {
-        ++ready;
-        unsigned sp = 0;
-        const bool rec = R2_PROF(A) && blockIdx.x == 0 && lane == 0 && ready >= 8 && ready < 72;
-        if (rec) g_cp[(ready - 8) * 4 + 1] = clock64();
-        while (!test_bar(full0 + (ready % kNSW) * 8, (unsigned)((ready / kNSW) & 1)))
-          if (++sp > (1u << 26)) __trap();
-        if (rec) { g_cp[(ready - 8) * 4 + 2] = clock64(); g_cp[(ready - 8) * 4 + 3] = sp; }
-      }
-      issue_upto(G + kNSW - 1, false);  // start the next copies as soon as their buffers are free
-    };
-    // poll halo cells (q0, c0), (q1, c1), (q2, c2): lane l checks double l & 3 of cell l >> 2
-    auto poll3 = [&](bool on, int q0_, int c0_, int q1_, int c1_, int q2_, int c2_) {
-      if (!on || (R2_DBG(A) & 16)) return;
-      const int which = min(lane >> 2, 2);
-      const int qq = which == 0 ? q0_ : (which == 1 ? q1_ : q2_);
-      const int cc = which == 0 ? c0_ : (which == 1 ? c1_ : c2_);
-      const unsigned sa = smem_u32(hcell(qq, cc) + (lane & 3));
+    // blocking wait on an mbarrier phase (try_wait suspends the thread between checks, so the
+    // producer takes few issue slots from consumer warp 0, which shares its sub-partition)
+    auto wait_bar = [&](unsigned bar, unsigned par) {
       unsigned sp = 0;
       while (true) {
-        unsigned long long v;
-        asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"(sa) : "memory");
-        if (__all_sync(0xffffffffu, v != kSentinel)) break;
-        if (++sp > (1u << 26)) __trap();          // a lost neighbour would otherwise hang the GPU
+        unsigned ok;
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(ok) : "r"(bar), "r"(par), "r"(2000u) : "memory");
+        if (__all_sync(0xffffffffu, ok)) break;
+        if (++sp > (1u << 24)) __trap();          // a lost consumer would otherwise hang the GPU
       }
     };
-    auto step_bar = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); ++nbars; };
-    // per-step path kept short (the producer shares an SM sub-partition with consumer warp 0): the copy
-    // bookkeeping only when a group boundary or a freed buffer needs it, and one poll per lane at a
-    // per-lane fixed cell offset (lanes 0-3 / 4-7 / 8-31 watch the step's three halo cells)
-    auto ensure_fast = [&](int G) {
-      G = min(G, 2 * nGr - 1);
-      const bool more = issued <= min(G + kNSW - 1, 2 * nGr - 1) && (issued < kNSW || freed(issued - kNSW));
-      if (ready >= G && !more) return;
-      ensure(G);
-    };
-    const int which = min(lane >> 2, 2);
-    const int qf = which == 1 ? 0 : 1, dcf = which == 0 ? 1 : (which == 1 ? 2 : 0);     // (1,k+1) (0,k+2) (1,k)
-    const int qb = which == 2 ? 3 : 2, dcb = which == 0 ? -1 : (which == 1 ? 0 : -2);  // (2,iR-1) (2,iR) (3,iR-2)
-    auto poll1 = [&](int q, int i) {
-      if (R2_DBG(A) & 16) return;
-      const unsigned sa = smem_u32(hcell(q, i) + (lane & 3));
-      unsigned sp = 0;
-      while (true) {
-        unsigned long long v;
-        asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"(sa) : "memory");
-        if (__all_sync(0xffffffffu, v != kSentinel)) break;
-        if (++sp > (1u << 26)) __trap();
-      }
-    };
-    // ---- forward: prologue barrier, then one barrier per step k
-    ensure(gof(2));
-    poll3(up_remote, 1, 0, 0, 0, 0, 1);
-    step_bar();
-    auto step_bar_p = [&](int sw, int k) {        // NKS_RAS2D_PROF: barrier arrive / release clocks
-      if (R2_PROF(A) && blockIdx.x == 0 && k >= 40 && k < 72) {
-        const long long a = clock64();
-        step_bar();
-        const long long r = clock64();
-        if (lane == 0) { g_st[sw][4][k - 40][0] = a; g_st[sw][4][k - 40][1] = r; }
-      } else {
-        step_bar();
-      }
-    };
-    for (int k = 0; k < nFp; ++k) {
-      ensure_fast(gof(k + 3));
-      if (up_remote) poll1(qf, k + dcf);
-      step_bar_p(0, k);
+    // groups 0 .. 2 nGr - 1 (forward groups, then backward groups in descending k), in order; group q
+    // reuses the buffer of group q - kNSW once all four consumer warps have released it
+    for (int q = 0; q < 2 * nGr; ++q) {
+      if ((R2_DBG(A) & 128) && q >= kNSW) break;   // ablation: no copy management after the first groups
+      const int st = q % kNSW, use = q / kNSW;
+      if (use > 0) wait_bar(empty0 + st * 8, (unsigned)((use - 1) & 1));
+      if (NKS_R2_LDGSTS || lane == 0) issue_one(q);
+      __syncwarp();
     }
-    // ---- backward: prologue barrier, then one barrier per step (processing p = nFp .. 2 nFp - 1)
-    const int dR = 2 * (R - 1);
-    {
-      const int iR = nFp - 1 - dR;
-      ensure(gof(nFp + 2));
-      poll3(dn_remote, 2, iR, 2, iR + 1, 2, iR + 2);
-      poll3(dn_remote, 3, iR, 3, iR - 1, 2, iR - 1);
-      step_bar();
-    }
-    for (int k = nFp - 1; k >= 0; --k) {
-      const int p = 2 * nFp - 1 - k;
-      ensure_fast(gof(p + 3));
-      if (dn_remote) poll1(qb, k - dR + dcb);
-      step_bar_p(1, p - nFp);
-    }
+    (void)full0;
   } else {
     // ================================================================ consumers
     const int c = w;                  // output component of this warp
@@ -524,10 +427,51 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     auto release_group = [&](int q) {
       __syncwarp();
       // relaxed: the stage's shared-memory reads all completed into registers before (no fence needed)
+      // release semantics: this warp's shared-memory reads of the group are ordered before the
+      // producer's refill of the buffer (it acquires the empty barrier, then issues the bulk copy)
       if (lane == 0)
-        asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(empty0 + (q % kNSW) * 8) : "memory");
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(empty0 + (q % kNSW) * 8) : "memory");
     };
-    auto step_bar = [&]() { asm volatile("bar.sync 1, 160;" ::: "memory"); };
+    const unsigned full0c = smem_u32(fullb);
+    // group q's bulk copy has landed (waited once per group by every consumer warp, before the first
+    // preload that reads it); try_wait returns at once when the producer is ahead
+    auto wait_full = [&](int q) {
+      if ((R2_DBG(A) & 128) && q >= kNSW) return;
+      const unsigned bar = full0c + (q % kNSW) * 8, par = (unsigned)((q / kNSW) & 1);
+      unsigned sp = 0;
+      while (true) {
+        unsigned ok;
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(ok) : "r"(bar), "r"(par) : "memory");
+        if (__all_sync(0xffffffffu, ok)) break;
+        if (++sp > (1u << 24)) __trap();
+      }
+    };
+    // Halo polls, one step ahead: lanes 0-3 / 4-7 / 8-31 watch component lane & 3 of the three halo
+    // cells the NEXT iteration reads (forward: (1,k+1) (0,k+2) (1,k); backward: (2,iR-1) (2,iR)
+    // (3,iR-2)).  The volatile load is issued early in an iteration and checked at its end, so its
+    // latency is off the step chain; the stripe pipeline settles one step further behind its neighbour.
+    const int pwhich = min(lane >> 2, 2);
+    const int pqf = pwhich == 1 ? 0 : 1, pdf = pwhich == 0 ? 1 : (pwhich == 1 ? 2 : 0);
+    const int pqb = pwhich == 2 ? 3 : 2, pdb = pwhich == 0 ? -1 : (pwhich == 1 ? 0 : -2);
+    auto pload = [&](int q, int i) -> unsigned long long {
+      unsigned long long v;
+      asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(hcell(q, i) + (lane & 3))) : "memory");
+      return v;
+    };
+    auto pcheck = [&](unsigned long long v, int q, int i) {
+      unsigned sp = 0;
+      while (!__all_sync(0xffffffffu, v != kSentinel)) {
+        v = pload(q, i);
+        if (++sp > (1u << 26)) __trap();          // a lost neighbour would otherwise hang the GPU
+      }
+    };
+    auto poll3c = [&](int q0_, int c0_, int q1_, int c1_, int q2_, int c2_) {   // blocking, prologues only
+      const int qq = pwhich == 0 ? q0_ : (pwhich == 1 ? q1_ : q2_);
+      const int cc = pwhich == 0 ? c0_ : (pwhich == 1 ? c1_ : c2_);
+      pcheck(pload(qq, cc), qq, cc);
+    };
+    auto step_bar = [&]() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
     auto step_bar_c = [&](int sw, int k) {        // NKS_RAS2D_PROF: barrier arrive / release clocks
       if (R2_PROF(A) && blockIdx.x == 0 && k >= 40 && k < 72) {
         const long long a = clock64();
@@ -618,7 +562,12 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       double q0, q1, q2, q3;                       // r prefetch ring: r(k+2) is used at iteration k
       q0 = load_r(2); q1 = load_r(3); q2 = load_r(4); q3 = load_r(5);
       const double r0v = load_r(0), r1v = load_r(1);
-      step_bar();                                   // groups of steps 0..2 resident, cells (1,0), (0,0), (0,1) written
+      for (int q = 0; q <= gof(2); ++q) wait_full(q);        // groups of steps 0..2 resident
+      if (up_remote && !(R2_DBG(A) & 16)) {
+        poll3c(1, 0, 0, 0, 0, 1);                            // cells (1,0), (0,0), (0,1) of the prologue
+        poll3c(pqf, pdf, pqf, pdf, pqf, pdf);                // cells of iteration 0
+      }
+      step_bar();
       {
         const bool top = rl == 0;
         double h10[4], h00[4], h01[4], a[4], bb[4];
@@ -644,6 +593,9 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         ld4a(rl >= 1 ? ering(k - 1, rl - 1) : hcella(1, k + 1), rl >= 1 ? kEPB : 16u, Ya1);   // (i+1, j-1) at step k-1
         ld4a(ering(k - 1, rl), kEPB, yp);                                                     // own row at step k-1
         ld4a(rl >= 2 ? ering(k - 2, rl - 2) : hcella(rl == 1 ? 1 : 0, rl == 1 ? k : k + 2), rl >= 2 ? kEPB : 16u, aa4);
+        const bool pol = up_remote && !(R2_DBG(A) & 16);
+        const unsigned long long pv = pol ? pload(pqf, k + 1 + pdf) : 0ull;   // the next iteration's cells
+        if ((k + 3) % kG == 0 && k + 3 < nFp) wait_full(gof(k + 3));       // preload reads steps k+1..k+3
         preload(nxt, k + 1);
         const double a0 = dot4(cur.L3, Ya1, pre);                     // (1,-1)
         const double a1 = dot4(cur.L5, yp, 0.0);                      // (-1,0)
@@ -658,6 +610,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         if (!(R2_DBG(A) & 260)) ybuf[(size_t)k * 128] = y;
         st_cluster_if(!(R2_DBG(A) & 4) && dn_push && active, dn_base + (unsigned)(i * 32), y);
         if (k % kG == kG - 2) release_group(gof(k));   // the group's last rows are in registers now
+        if (pol) pcheck(pv, pqf, k + 1 + pdf);
       };
       for (int k0 = 0; k0 < nFp; k0 += 4) {
         fiter(k0, q0, SA, SB); q0 = load_r(k0 + 6);
@@ -707,7 +660,14 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       load_y4(K - 2, q0); load_y4(K - 3, q1); load_y4(K - 4, q2); load_y4(K - 5, q3);
       double yK[4], yK1[4];
       load_y4(K, yK); load_y4(K - 1, yK1);
-      step_bar();                     // first backward groups resident, lane R-1 / R-2 cells of the first steps written
+      for (int q = gof(nFp); q <= gof(nFp + 2); ++q) wait_full(q);   // first backward groups resident
+      if (dn_remote && !(R2_DBG(A) & 16)) {
+        const int iR = K - dR;
+        poll3c(2, iR, 2, iR + 1, 2, iR + 2);                  // cells of the prologue
+        poll3c(3, iR, 3, iR - 1, 2, iR - 1);
+        poll3c(pqb, iR + pdb, pqb, iR + pdb, pqb, iR + pdb);   // cells of iteration K
+      }
+      step_bar();
       {
         const int iR = K - dR;
         const bool bot = rl == R - 1, bot2 = rl == R - 2;
@@ -746,6 +706,12 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         ld4a(rl <= R - 2 ? ering(k + 1, rl + 1) : hcella(2, iR - 1), rl <= R - 2 ? kEPB : 16u, Xb1);   // (i-1, j+1) at step k+1
         ld4a(ering(k + 1, rl), kEPB, xp);                                                              // own row at step k+1
         ld4a(rl <= R - 3 ? ering(k + 2, rl + 2) : hcella(rl == R - 2 ? 2 : 3, rl == R - 2 ? iR : iR - 2), rl <= R - 3 ? kEPB : 16u, bb4);
+        const bool pol = dn_remote && !(R2_DBG(A) & 16);
+        const unsigned long long pv = pol ? pload(pqb, iR - 1 + pdb) : 0ull;   // the next iteration's cells
+        {
+          const int pp = pofk(k) + 3;                                        // preload reads processing steps
+          if (pp % kG == 0 && pp < 2 * nFp) wait_full(gof(pp));             // pofk(k)+1 .. pofk(k)+3
+        }
         preload(nxt, k - 1);
         const double a0 = dot4(cur.U3, Xb1, pre);                     // (-1,1)
         const double a1 = dot4(cur.U1, xp, 0.0);                      // (1,0)
@@ -765,6 +731,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         st_cluster_if(up_push && active, up_base + (unsigned)(i * 32), x);
         const int p = pofk(k);
         if (p % kG == kG - 2) release_group(gof(p));
+        if (pol) pcheck(pv, pqb, iR - 1 + pdb);
       };
       for (int kb0 = 0; kb0 < nFp; kb0 += 4) {
         const int k0 = K - kb0;
