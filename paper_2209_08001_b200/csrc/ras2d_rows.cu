@@ -585,17 +585,22 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       // lanes R-2, R-1 push y into the next stripe's halo rows 0, 1 (cluster address of cell 0, + 32 B per i)
       const bool dn_push = dn_remote && rl >= R - 2 && rl < R;
       const unsigned dn_base = mapa_u32(hcell(min(max(rl - (R - 2), 0), 1), 0) + c, (unsigned)min(s + 1, CS - 1));
+      // Control flow inside a step makes the compiler wait for every outstanding load at the branch
+      // (the block-row preloads share its few scoreboards), so the step's two checks -- this iteration's
+      // halo cells (loaded by the previous iteration) and the full barrier of the group the preload
+      // will read -- sit right after the step barrier, where those loads are needed anyway.
+      const bool pol = up_remote && !(R2_DBG(A) & 16);
+      unsigned long long pvn = 0ull;                 // iteration 0's cells were checked in the prologue
       auto fiter = [&](int k, double r2, FRows& cur, FRows& nxt) {
         const int i = k - 2 * rl;
         const bool active = row_ok && (unsigned)i < (unsigned)ex;
         step_bar_c(0, k);                                             // E[k-1] complete; stages/cells ready
+        if (pol) pcheck(pvn, pqf, k + pdf);
+        if ((k + 3) % kG == 0 && k + 3 < nFp) wait_full(gof(k + 3));       // preload reads steps k+1..k+3
         double Ya1[4], yp[4], aa4[4];
         ld4a(rl >= 1 ? ering(k - 1, rl - 1) : hcella(1, k + 1), rl >= 1 ? kEPB : 16u, Ya1);   // (i+1, j-1) at step k-1
         ld4a(ering(k - 1, rl), kEPB, yp);                                                     // own row at step k-1
         ld4a(rl >= 2 ? ering(k - 2, rl - 2) : hcella(rl == 1 ? 1 : 0, rl == 1 ? k : k + 2), rl >= 2 ? kEPB : 16u, aa4);
-        const bool pol = up_remote && !(R2_DBG(A) & 16);
-        const unsigned long long pv = pol ? pload(pqf, k + 1 + pdf) : 0ull;   // the next iteration's cells
-        if ((k + 3) % kG == 0 && k + 3 < nFp) wait_full(gof(k + 3));       // preload reads steps k+1..k+3
         preload(nxt, k + 1);
         const double a0 = dot4(cur.L3, Ya1, pre);                     // (1,-1)
         const double a1 = dot4(cur.L5, yp, 0.0);                      // (-1,0)
@@ -610,7 +615,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         if (!(R2_DBG(A) & 260)) ybuf[(size_t)k * 128] = y;
         st_cluster_if(!(R2_DBG(A) & 4) && dn_push && active, dn_base + (unsigned)(i * 32), y);
         if (k % kG == kG - 2) release_group(gof(k));   // the group's last rows are in registers now
-        if (pol) pcheck(pv, pqf, k + 1 + pdf);
+        if (pol) pvn = pload(pqf, k + 1 + pdf);        // the next iteration's cells (checked after its barrier)
       };
       for (int k0 = 0; k0 < nFp; k0 += 4) {
         fiter(k0, q0, SA, SB); q0 = load_r(k0 + 6);
@@ -697,21 +702,22 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       // lanes 0, 1 push x into the previous stripe's halo rows 2, 3
       const bool up_push = up_remote && rl < 2;
       const unsigned up_base = mapa_u32(hcell(2 + min(rl, 1), 0) + c, (unsigned)max(s - 1, 0));
+      const bool pol = dn_remote && !(R2_DBG(A) & 16);
+      unsigned long long pvn = 0ull;                 // iteration K's cells were checked in the prologue
       auto biter = [&](int k, const double (&y2)[4], BRows& cur, BRows& nxt) {
         const int i = k - 2 * rl;
         const bool active = row_ok && (unsigned)i < (unsigned)ex;
         const int iR = k - dR;
         step_bar_c(1, nFp - 1 - k);                                   // E[k+1] complete; stages/cells ready
-        double Xb1[4], xp[4], bb4[4];
-        ld4a(rl <= R - 2 ? ering(k + 1, rl + 1) : hcella(2, iR - 1), rl <= R - 2 ? kEPB : 16u, Xb1);   // (i-1, j+1) at step k+1
-        ld4a(ering(k + 1, rl), kEPB, xp);                                                              // own row at step k+1
-        ld4a(rl <= R - 3 ? ering(k + 2, rl + 2) : hcella(rl == R - 2 ? 2 : 3, rl == R - 2 ? iR : iR - 2), rl <= R - 3 ? kEPB : 16u, bb4);
-        const bool pol = dn_remote && !(R2_DBG(A) & 16);
-        const unsigned long long pv = pol ? pload(pqb, iR - 1 + pdb) : 0ull;   // the next iteration's cells
+        if (pol) pcheck(pvn, pqb, iR + pdb);
         {
           const int pp = pofk(k) + 3;                                        // preload reads processing steps
           if (pp % kG == 0 && pp < 2 * nFp) wait_full(gof(pp));             // pofk(k)+1 .. pofk(k)+3
         }
+        double Xb1[4], xp[4], bb4[4];
+        ld4a(rl <= R - 2 ? ering(k + 1, rl + 1) : hcella(2, iR - 1), rl <= R - 2 ? kEPB : 16u, Xb1);   // (i-1, j+1) at step k+1
+        ld4a(ering(k + 1, rl), kEPB, xp);                                                              // own row at step k+1
+        ld4a(rl <= R - 3 ? ering(k + 2, rl + 2) : hcella(rl == R - 2 ? 2 : 3, rl == R - 2 ? iR : iR - 2), rl <= R - 3 ? kEPB : 16u, bb4);
         preload(nxt, k - 1);
         const double a0 = dot4(cur.U3, Xb1, pre);                     // (-1,1)
         const double a1 = dot4(cur.U1, xp, 0.0);                      // (1,0)
@@ -731,7 +737,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         st_cluster_if(up_push && active, up_base + (unsigned)(i * 32), x);
         const int p = pofk(k);
         if (p % kG == kG - 2) release_group(gof(p));
-        if (pol) pcheck(pv, pqb, iR - 1 + pdb);
+        if (pol) pvn = pload(pqb, iR - 1 + pdb);        // the next iteration's cells
       };
       for (int kb0 = 0; kb0 < nFp; kb0 += 4) {
         const int k0 = K - kb0;
