@@ -63,6 +63,9 @@ template <bool F32> struct Strm {
 #ifndef NKS_R2_NS
 #define NKS_R2_NS 4
 #endif
+#ifndef NKS_R2_PSLEEP
+#define NKS_R2_PSLEEP 256    // producer back-off (ns) while the ring is full
+#endif
   static constexpr int G = NKS_R2_G;     // steps per group (one bulk copy)
   static constexpr int NS = NKS_R2_NS;   // group buffers
 };
@@ -379,6 +382,9 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
                      : "=r"(ok) : "r"(bar), "r"(par), "r"(2000u) : "memory");
         if (__all_sync(0xffffffffu, ok)) break;
+        // measured: without a sleep this loop issued ~4x the instructions of a consumer warp on the
+        // sub-partition it shares with consumer warp 0 (the try_wait suspend hint does not hold it)
+        __nanosleep(NKS_R2_PSLEEP);
         if (++sp > (1u << 24)) __trap();          // a lost consumer would otherwise hang the GPU
       }
     };
@@ -458,6 +464,22 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       unsigned long long v;
       asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(hcell(q, i) + (lane & 3))) : "memory");
       return v;
+    };
+    // the speculative poll load at the end of a step is a plain shared load: a volatile one is ordered
+    // after this warp's outstanding block-row preloads and waited for them (measured, ncu source page)
+    auto pload_plain = [&](int q, int i) -> unsigned long long {
+      unsigned long long v;
+      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(hcell(q, i) + (lane & 3))));
+      return v;
+    };
+    // non-blocking probe of a group's full barrier, issued one step before the group is needed (the
+    // SYNCS phase check has a long latency; its predicate is consumed after the next step barrier)
+    auto test_full = [&](int q) -> bool {
+      if ((R2_DBG(A) & 128) && q >= kNSW) return true;
+      unsigned ok;
+      asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                   : "=r"(ok) : "r"(full0c + (q % kNSW) * 8), "r"((unsigned)((q / kNSW) & 1)));
+      return ok != 0;
     };
     auto pcheck = [&](unsigned long long v, int q, int i) {
       unsigned sp = 0;
@@ -591,12 +613,17 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       // will read -- sit right after the step barrier, where those loads are needed anyway.
       const bool pol = up_remote && !(R2_DBG(A) & 16);
       unsigned long long pvn = 0ull;                 // iteration 0's cells were checked in the prologue
+      auto fneed = [&](int k) { return (k + 3) % kG == 0 && k + 3 < nFp; };   // preload of k reads steps k+1..k+3
+      bool fok = !fneed(0) || test_full(gof(3));
       auto fiter = [&](int k, double r2, FRows& cur, FRows& nxt) {
         const int i = k - 2 * rl;
         const bool active = row_ok && (unsigned)i < (unsigned)ex;
         step_bar_c(0, k);                                             // E[k-1] complete; stages/cells ready
-        if (pol) pcheck(pvn, pqf, k + pdf);
-        if ((k + 3) % kG == 0 && k + 3 < nFp) wait_full(gof(k + 3));       // preload reads steps k+1..k+3
+        // fast path: one vote on the probes issued during the previous step; slow path: blocking waits
+        if (!__all_sync(0xffffffffu, fok && (!pol || pvn != kSentinel))) {
+          if (pol) pcheck(pvn, pqf, k + pdf);
+          if (fneed(k)) wait_full(gof(k + 3));
+        }
         double Ya1[4], yp[4], aa4[4];
         ld4a(rl >= 1 ? ering(k - 1, rl - 1) : hcella(1, k + 1), rl >= 1 ? kEPB : 16u, Ya1);   // (i+1, j-1) at step k-1
         ld4a(ering(k - 1, rl), kEPB, yp);                                                     // own row at step k-1
@@ -615,7 +642,8 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         if (!(R2_DBG(A) & 260)) ybuf[(size_t)k * 128] = y;
         st_cluster_if(!(R2_DBG(A) & 4) && dn_push && active, dn_base + (unsigned)(i * 32), y);
         if (k % kG == kG - 2) release_group(gof(k));   // the group's last rows are in registers now
-        if (pol) pvn = pload(pqf, k + 1 + pdf);        // the next iteration's cells (checked after its barrier)
+        if (pol) pvn = pload_plain(pqf, k + 1 + pdf);  // the next iteration's cells (checked after its barrier)
+        fok = !fneed(k + 1) || test_full(gof(k + 4));
       };
       for (int k0 = 0; k0 < nFp; k0 += 4) {
         fiter(k0, q0, SA, SB); q0 = load_r(k0 + 6);
@@ -704,15 +732,16 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       const unsigned up_base = mapa_u32(hcell(2 + min(rl, 1), 0) + c, (unsigned)max(s - 1, 0));
       const bool pol = dn_remote && !(R2_DBG(A) & 16);
       unsigned long long pvn = 0ull;                 // iteration K's cells were checked in the prologue
+      auto bneed = [&](int k) { const int pp = pofk(k) + 3; return pp % kG == 0 && pp < 2 * nFp; };
+      bool fok = !bneed(K) || test_full(gof(pofk(K) + 3));
       auto biter = [&](int k, const double (&y2)[4], BRows& cur, BRows& nxt) {
         const int i = k - 2 * rl;
         const bool active = row_ok && (unsigned)i < (unsigned)ex;
         const int iR = k - dR;
         step_bar_c(1, nFp - 1 - k);                                   // E[k+1] complete; stages/cells ready
-        if (pol) pcheck(pvn, pqb, iR + pdb);
-        {
-          const int pp = pofk(k) + 3;                                        // preload reads processing steps
-          if (pp % kG == 0 && pp < 2 * nFp) wait_full(gof(pp));             // pofk(k)+1 .. pofk(k)+3
+        if (!__all_sync(0xffffffffu, fok && (!pol || pvn != kSentinel))) {
+          if (pol) pcheck(pvn, pqb, iR + pdb);
+          if (bneed(k)) wait_full(gof(pofk(k) + 3));                // preload reads pofk(k)+1 .. pofk(k)+3
         }
         double Xb1[4], xp[4], bb4[4];
         ld4a(rl <= R - 2 ? ering(k + 1, rl + 1) : hcella(2, iR - 1), rl <= R - 2 ? kEPB : 16u, Xb1);   // (i-1, j+1) at step k+1
@@ -737,7 +766,8 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         st_cluster_if(up_push && active, up_base + (unsigned)(i * 32), x);
         const int p = pofk(k);
         if (p % kG == kG - 2) release_group(gof(p));
-        if (pol) pvn = pload(pqb, iR - 1 + pdb);        // the next iteration's cells
+        if (pol) pvn = pload_plain(pqb, iR - 1 + pdb);  // the next iteration's cells
+        fok = !bneed(k - 1) || test_full(gof(pofk(k - 1) + 3));
       };
       for (int kb0 = 0; kb0 < nFp; kb0 += 4) {
         const int k0 = K - kb0;
