@@ -63,6 +63,11 @@ template <bool F32> struct Strm {
 #ifndef NKS_R2_NS
 #define NKS_R2_NS 4
 #endif
+// ring release: 1 = named barriers (the consumers' bar.arrive of group g wakes the producer's bar.sync
+// on barrier 4 + g % NS: no spinning producer), 0 = empty mbarriers polled by the producer
+#ifndef NKS_R2_NBREL
+#define NKS_R2_NBREL 1
+#endif
 #ifndef NKS_R2_PSLEEP
 #define NKS_R2_PSLEEP 256    // producer back-off (ns) while the ring is full
 #endif
@@ -393,7 +398,19 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     for (int q = 0; q < 2 * nGr; ++q) {
       if ((R2_DBG(A) & 128) && q >= kNSW) break;   // ablation: no copy management after the first groups
       const int st = q % kNSW, use = q / kNSW;
+#if NKS_R2_NBREL
+      // Named barrier 4 + (q - NS) % NS completes when the four consumer warps have arrived for group
+      // q - NS (bar.arrive: prior shared reads performed) and this warp syncs: the warp sleeps in the
+      // barrier instead of polling.  At most NS releases are outstanding (a consumer cannot pass group
+      // q - 1 before group q is issued), so NS barrier ids never see two releases at once.
+      if (use > 0) {
+        asm volatile("bar.sync %0, %1;" ::"r"(4 + (q - kNSW) % kNSW), "n"(32 * (NCW + 1)) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads before async-proxy writes
+      }
+      (void)wait_bar;
+#else
       if (use > 0) wait_bar(empty0 + st * 8, (unsigned)((use - 1) & 1));
+#endif
       if (NKS_R2_LDGSTS || lane == 0) issue_one(q);
       __syncwarp();
     }
@@ -432,11 +449,18 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     };
     auto release_group = [&](int q) {
       __syncwarp();
-      // relaxed: the stage's shared-memory reads all completed into registers before (no fence needed)
+#if NKS_R2_NBREL
+      // whole warp (bar.arrive is .aligned); the producer syncs on the release of groups
+      // 0 .. 2 nGr - 1 - NS only (later groups have no successor in the ring), so the last NS releases
+      // are not signalled.  bar.arrive orders this warp's shared reads of the group before the refill.
+      (void)empty0;
+      if (q < 2 * nGr - kNSW) asm volatile("bar.arrive %0, %1;" ::"r"(4 + q % kNSW), "n"(32 * (NCW + 1)) : "memory");
+#else
       // release semantics: this warp's shared-memory reads of the group are ordered before the
       // producer's refill of the buffer (it acquires the empty barrier, then issues the bulk copy)
       if (lane == 0)
         asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(empty0 + (q % kNSW) * 8) : "memory");
+#endif
     };
     const unsigned full0c = smem_u32(fullb);
     // group q's bulk copy has landed (waited once per group by every consumer warp, before the first
