@@ -285,6 +285,7 @@ def test_early_divergence_rule_keeps_the_controllers_decisions():
     on = gpu_solver(shape, nsub=(4, 4), sol={"gmres_stall_cycles": 3})
     off = gpu_solver(shape, nsub=(4, 4), sol={"gmres_stall_cycles": 0})
     on.set_fields(c, eta, None)
+    off.set_fields(c, eta, None)          # same cbar0; nks_set_state needs fields set once
     on.run_adaptive(3)
     X = on.get_state()
     outcomes = []
