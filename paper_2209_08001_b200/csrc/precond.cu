@@ -8,6 +8,8 @@
 // point l = lx + 2 ly + 3 lz (the exact dependency depth of the |o|_1 <= 2 block pattern, R21;
 // i+j+k would violate the (1,-1,0)/(1,0,-1)/(0,1,-1) couplings).  Box-local arrays are stored in
 // level order ("positions") so one level is a contiguous, coalesced range.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <numeric>
 
@@ -573,6 +575,106 @@ __global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const in
   }
 }
 
+// The same sweeps with a thread-block cluster of CS CTAs per box (cluster rank r takes positions
+// p0 + r*blockDim + tid, stride CS*blockDim, of every level; the level barrier is the cluster barrier,
+// release/acquire at cluster scope).  Used when the boxes alone would leave SMs idle -- a rank's share of
+// a strong-scaled grid (config 4 on 8 GPUs: 64 boxes of 36^3 per GPU on 148 SMs).  The box vector y
+// lives in global memory and is written by the other CTAs of the cluster, so its loads bypass L1 (ld.cg).
+template <int NF, int NL, typename FT>
+__global__ void k_ras_apply_cl(SlotTables T, const int* __restrict__ gidx, const int* __restrict__ nbr,
+                               const int* __restrict__ box_lev_off, const int* __restrict__ lev_ptr,
+                               const int* __restrict__ box_pos_off, long long Ptot, long long ld, long long N,
+                               const FT* __restrict__ fac, const double* __restrict__ r, double* y,
+                               double* __restrict__ z, int variant) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = (int)cl.num_blocks();
+  const int b = blockIdx.x / CS;
+  const int t0 = (int)cl.block_rank() * blockDim.x + threadIdx.x, ts = CS * blockDim.x;
+  const int q0 = box_pos_off[b], q1 = box_pos_off[b + 1];
+  for (int pos = q0 + t0; pos < q1; pos += ts) {
+    int gi = gidx[pos];
+    const bool owned = gi >= 0;
+    if (gi < 0) gi = ~gi;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) __stcg(y + f * Ptot + pos, (variant == 2 && !owned) ? 0.0 : r[f * N + gi]);
+  }
+  cl.sync();
+  const int l0 = box_lev_off[b], l1 = box_lev_off[b + 1] - 1;
+  for (int l = l0; l < l1; ++l) {
+    const int p0 = lev_ptr[l], p1 = lev_ptr[l + 1];
+    for (int pos = p0 + t0; pos < p1; pos += ts) {
+      int kk[NL];
+#pragma unroll
+      for (int a = 0; a < NL; ++a) kk[a] = __ldg(nbr + (long long)T.lower[a] * Ptot + pos);
+      double yk[NL][NF];
+#pragma unroll
+      for (int a = 0; a < NL; ++a)
+#pragma unroll
+        for (int f = 0; f < NF; ++f) yk[a][f] = kk[a] >= 0 ? __ldcg(y + f * Ptot + kk[a]) : 0.0;
+      double acc[NF];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) acc[f] = __ldcg(y + f * Ptot + pos);
+#pragma unroll
+      for (int a = 0; a < NL; ++a) {
+        const FT* L = fac + (long long)(T.lower[a] * NF * NF) * ld + pos;
+#pragma unroll
+        for (int rr = 0; rr < NF; ++rr)
+#pragma unroll
+          for (int c = 0; c < NF; ++c)
+            acc[rr] = fma(-(double)__ldg(L + (long long)(rr * NF + c) * ld), yk[a][c], acc[rr]);
+      }
+#pragma unroll
+      for (int f = 0; f < NF; ++f) __stcg(y + f * Ptot + pos, acc[f]);
+    }
+    cl.sync();
+  }
+  for (int l = l1 - 1; l >= l0; --l) {
+    const int p0 = lev_ptr[l], p1 = lev_ptr[l + 1];
+    for (int pos = p0 + t0; pos < p1; pos += ts) {
+      int kk[NL];
+#pragma unroll
+      for (int a = 0; a < NL; ++a) kk[a] = __ldg(nbr + (long long)T.upper[a] * Ptot + pos);
+      double xk[NL][NF];
+#pragma unroll
+      for (int a = 0; a < NL; ++a)
+#pragma unroll
+        for (int f = 0; f < NF; ++f) xk[a][f] = kk[a] >= 0 ? __ldcg(y + f * Ptot + kk[a]) : 0.0;
+      double acc[NF];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) acc[f] = __ldcg(y + f * Ptot + pos);
+#pragma unroll
+      for (int a = 0; a < NL; ++a) {
+        const FT* U = fac + (long long)(T.upper[a] * NF * NF) * ld + pos;
+#pragma unroll
+        for (int rr = 0; rr < NF; ++rr)
+#pragma unroll
+          for (int c = 0; c < NF; ++c)
+            acc[rr] = fma(-(double)__ldg(U + (long long)(rr * NF + c) * ld), xk[a][c], acc[rr]);
+      }
+      const FT* D = fac + (long long)(T.diag * NF * NF) * ld + pos;
+      double xo[NF];
+#pragma unroll
+      for (int rr = 0; rr < NF; ++rr) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < NF; ++c) s = fma((double)__ldg(D + (long long)(rr * NF + c) * ld), acc[c], s);
+        xo[rr] = s;
+      }
+#pragma unroll
+      for (int f = 0; f < NF; ++f) __stcg(y + f * Ptot + pos, xo[f]);
+    }
+    cl.sync();
+  }
+  if (variant != 0) return;
+  for (int pos = q0 + t0; pos < q1; pos += ts) {
+    const int gi = gidx[pos];
+    if (gi < 0) continue;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) z[f * N + gi] = __ldcg(y + f * Ptot + pos);
+  }
+}
+
 // sum_i R_i^{deltaT} x_i: every grid point adds the solutions of the box positions covering it, in
 // increasing position order (deterministic; a periodic self-overlapping box covers a point twice)
 __global__ void k_schwarz_gather(long long N, int nf, long long Ptot, const int* __restrict__ cover_off,
@@ -624,10 +726,64 @@ void launch_fac_to_fp32(const BoxSet& B, int nf, const double* fac, float* fac32
   k_to_fp32<<<148 * 8, 256, 0, s>>>(n, fac, fac32);
 }
 
+// CTAs per box of the clustered apply: doubled while the boxes would fill at most half of the SMs, at
+// most 4 and never more than the widest level needs (NKS_RAS3D_CSMAX / NKS_RAS3D_WIDTH: build-time
+// switches for experiments).  Measured at config 4's per-GPU share (profiles/r02_ras3d_cluster.log):
+// 64 boxes of 36^3 (8 GPUs) 5.71 -> 4.54 ms with 2 CTAs per box (4: 7.67 ms); 128 boxes (4 GPUs) are
+// slower clustered (7.20 -> 9.11 ms: the cluster barrier per level costs more than the extra SMs give),
+// so they keep one CTA per box.
+#ifndef NKS_RAS3D_CSMAX
+#define NKS_RAS3D_CSMAX 4
+#endif
+static int ras_cluster_of(const BoxSet& B, int threads) {
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int cs = 1;
+#ifndef NKS_RAS3D_WIDTH
+#define NKS_RAS3D_WIDTH 1
+#endif
+  while (cs < NKS_RAS3D_CSMAX && 2LL * B.nbox * cs <= sms && (!NKS_RAS3D_WIDTH || cs * threads < B.max_level_width))
+    cs *= 2;
+  return cs;
+}
+
+template <int NF, int NL, typename FT>
+static cudaError_t launch_cl(int cs, int threads, const SlotTables& T, const BoxSet& B, long long N, const FT* fac,
+                             const double* r, double* y, double* z, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(B.nbox * cs, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_ras_apply_cl<NF, NL, FT>, T, (const int*)B.gidx, (const int*)B.nbr,
+                            (const int*)B.box_lev_off, (const int*)B.lev_ptr, (const int*)B.box_pos_off, B.P, B.ld, N,
+                            fac, r, y, z, B.variant);
+}
+
 void launch_ras_apply(const BoxSet& B, int nf, long long N, const double* fac, const float* fac32, const double* r,
                       double* y, double* z, cudaStream_t s) {
   const SlotTables T = make_tables(B, nf);
   const int threads = std::min(256, std::max(32, ((B.max_level_width + 31) / 32) * 32));
+  const int cs = ras_cluster_of(B, threads);
+  if (cs > 1) {
+    if (nf == 4) {
+      if (fac32) launch_cl<4, 6, float>(cs, threads, T, B, N, fac32, r, y, z, s);
+      else launch_cl<4, 6, double>(cs, threads, T, B, N, fac, r, y, z, s);
+    } else {
+      if (fac32) launch_cl<5, 12, float>(cs, threads, T, B, N, fac32, r, y, z, s);
+      else launch_cl<5, 12, double>(cs, threads, T, B, N, fac, r, y, z, s);
+    }
+    if (B.variant != 0) {
+      const int blocks = (int)std::min<long long>((N + 255) / 256, 148 * 8);
+      k_schwarz_gather<<<blocks, 256, 0, s>>>(N, nf, B.P, B.cover_off, B.cover_pos, y, z);
+    }
+    return;
+  }
   if (nf == 4) {
     if (fac32)
       k_ras_apply<4, 6, float><<<B.nbox, threads, 0, s>>>(T, B.gidx, B.nbr, B.box_lev_off, B.lev_ptr, B.box_pos_off,
