@@ -94,6 +94,17 @@ typedef struct {
                      /* (reading R38: cell-centred mirror ghosts; traction-free u through odd stress */
                      /* ghosts; gauge = translations + discrete rotations).  Single-GPU states with */
                      /* pc_type NONE or SPECTRAL; nks_set_fields then needs u (no FFT u^0).        */
+  int32_t yghost;    /* 0: no y split.  2..8: this state is one z x y PENCIL of a 3D grid sharded on a  */
+                     /* pz x py process grid (SURVEY 8(e), configs 4/5 "slab- then pencil-sharded"): */
+                     /* n[1] counts yghost ghost rows on each side as n[2] counts zghost (>= 2) ghost */
+                     /* planes.  Pencil states evaluate F and J.v (the config-5 sharded micro-       */
+                     /* benchmark): nks_set_fields (u given), nks_set_state, nks_get_fields,          */
+                     /* nks_eval_residual, nks_eval_jv; the NKS step itself shards by z-slabs.       */
+                     /* nks_decompose_pencil() fills a rank's pencil grid.                           */
+  int32_t y_offset;  /* yghost > 0: global y of this pencil's first own row                        */
+  int32_t ny_global; /* yghost > 0: rows of the global periodic grid                                 */
+  int32_t pz, py;    /* yghost > 0: the process grid (rank = rz * py + ry); ignored otherwise         */
+  int32_t pad_;
 } nks_grid;
 
 /* ---- communication callbacks of a z-sharded state --------------------------------
@@ -199,8 +210,19 @@ NKS_API nks_status nks_get_unique_id(uint8_t id[128]);
 NKS_API nks_status nks_decompose(const nks_grid* global, const nks_params* params, int32_t rank, int32_t nranks,
                                  nks_grid* local);
 
-/* One message of a z-slab halo exchange: kind 0 = send, 1 = receive; peer rank; offset (doubles from the
- * vector's start, field f at f * n[0]*n[1]*n[2]) and count of a contiguous run of planes. */
+/* The pencil of `rank` on a pz x py process grid (rank = rz * py + ry) for a GLOBAL periodic 3D grid --
+ * host only.  rz owns a contiguous run of z planes, ry of y rows (dealt out like nks_decompose without RAS:
+ * the first n mod p parts one longer); *local gets own extents + 2 ghost planes / rows per side (the
+ * stencils' radius), z_offset / y_offset / nz_global / ny_global / pz / py set, pc_type must be NONE.
+ * NKS_E_INVALID if the grid is not 3D or a part would own fewer than 2 planes / rows. */
+NKS_API nks_status nks_decompose_pencil(const nks_grid* global, int32_t rank, int32_t pz, int32_t py, nks_grid* local);
+
+/* One message of a halo exchange: kind 0 = send, 1 = receive of a contiguous run (`count` doubles at
+ * `offset` from the vector's start, field f at f * n[0]*n[1]*n[2]): the ghost PLANES of a slab or a pencil.
+ * kind 2 = send, 3 = receive of a pencil's y block: `count` doubles (yghost rows) at `offset` in the first
+ * own plane, repeated over every own plane with the plane stride n[0]*n[1] (packed plane after plane).  A
+ * pencil exchanges y blocks first, then whole planes (ghost rows included), so the (y, z) edge cells the
+ * stencil's (0, +-1, +-1) offsets read arrive through the second phase. */
 typedef struct {
   int32_t kind;
   int32_t peer;
@@ -209,8 +231,9 @@ typedef struct {
 } nks_halo_msg;
 
 /* The ordered halo message list the library issues (grouped ncclSend/ncclRecv, matched per peer in issue order)
- * for a slab grid from nks_decompose -- host only, no GPU.  Writes up to cap messages, returns how many the
- * exchange has (4 per field), or -1 on invalid input. */
+ * for a slab grid from nks_decompose or a pencil grid from nks_decompose_pencil (nranks = pz * py) -- host
+ * only, no GPU.  Writes up to cap messages, returns how many the exchange has (4 per field for a slab; 4 y
+ * messages then 4 plane messages per field for a pencil, y phase first), or -1 on invalid input. */
 NKS_API int32_t nks_halo_plan(const nks_grid* local, int32_t rank, int32_t nranks, int32_t nfields, nks_halo_msg* out,
                               int32_t cap);
 

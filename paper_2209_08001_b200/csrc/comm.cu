@@ -53,6 +53,59 @@ int slab_decompose(const nks_grid& global, int pc_type, int rank, int nranks, nk
   return 0;
 }
 
+// Pencil of rank r = rz * py + ry on a pz x py process grid (z x y; x stays whole): planes and rows dealt out
+// like the planes of a slab without RAS, 2 ghost planes / rows per side (the stencil radius of F and J.v).
+int pencil_decompose(const nks_grid& global, int rank, int pz, int py, nks_grid& local) {
+  if (global.dim != 3 || global.zghost != 0 || global.yghost != 0 || pz < 1 || py < 1 || rank < 0 || rank >= pz * py)
+    return 1;
+  const int rz = rank / py, ry = rank % py;
+  int z0, nzo, y0, nyo;
+  deal(global.n[2], pz, rz, z0, nzo);
+  deal(global.n[1], py, ry, y0, nyo);
+  if (nzo < 2 || nyo < 2) return 1;
+  local = global;
+  local.n[2] = nzo + 4;
+  local.n[1] = nyo + 4;
+  local.zghost = 2;
+  local.yghost = 2;
+  local.z_offset = z0;
+  local.nz_global = global.n[2];
+  local.y_offset = y0;
+  local.ny_global = global.n[1];
+  local.pz = pz;
+  local.py = py;
+  local.nsub[0] = local.nsub[1] = local.nsub[2] = 1;
+  return 0;
+}
+
+// Pencil halo plan: phase 1, per field, the y blocks of the own planes (kind 2 send / 3 receive: yg rows per
+// own plane, packed plane after plane) with the y neighbours (rz, ry -+ 1); phase 2 the z planes -- whole
+// local planes, ghost rows included, so the (y, z) edge cells arrive -- with the z neighbours (rz -+ 1, ry).
+// Per peer the messages are matched in issue order, as in the slab plan (up == down for two parts).
+void pencil_halo_plan(const nks_grid& g, int rank, int nf, std::vector<nks_halo_msg>& out) {
+  const int pz = g.pz, py = g.py, rz = rank / py, ry = rank % py;
+  const int nx = g.n[0], nyl = g.n[1], nzl = g.n[2], yg = g.yghost, zg = g.zghost;
+  const long long nxy = (long long)nx * nyl, fstride = nxy * nzl;
+  const int yup = rz * py + (ry + 1) % py, ydn = rz * py + (ry + py - 1) % py;
+  const int zup = ((rz + 1) % pz) * py + ry, zdn = ((rz + pz - 1) % pz) * py + ry;
+  const long long ycnt = (long long)yg * nx, zcnt = (long long)zg * nxy;
+  out.clear();
+  for (int f = 0; f < nf; ++f) {
+    const long long b = (long long)f * fstride + (long long)zg * nxy;           // first own plane
+    out.push_back({2, ydn, b + (long long)yg * nx, ycnt});                       // own rows lo -> ry-1's top ghosts
+    out.push_back({2, yup, b + (long long)(nyl - 2 * yg) * nx, ycnt});           // own rows hi -> ry+1's bottom ghosts
+    out.push_back({3, yup, b + (long long)(nyl - yg) * nx, ycnt});               // top ghost rows <- ry+1
+    out.push_back({3, ydn, b, ycnt});                                            // bottom ghost rows <- ry-1
+  }
+  for (int f = 0; f < nf; ++f) {
+    const long long base = (long long)f * fstride;
+    out.push_back({0, zdn, base + (long long)zg * nxy, zcnt});
+    out.push_back({0, zup, base + (long long)(nzl - 2 * zg) * nxy, zcnt});
+    out.push_back({1, zup, base + (long long)(nzl - zg) * nxy, zcnt});
+    out.push_back({1, zdn, base, zcnt});
+  }
+}
+
 // ------------------------------------------------------------------------------------------ NCCL
 struct NcclComm {
   ncclComm_t comm = nullptr;
@@ -129,6 +182,51 @@ int nccl_halo(void* c, double* vec, int nf, long long fstride, int nzl, long lon
       ncclGroupEnd();
       return 1;
     }
+  }
+  return ncclGroupEnd() == ncclSuccess ? 0 : 1;
+}
+
+// Pencil halo (plan above): y blocks are packed plane after plane into `stage` (cudaMemcpy2DAsync, one per
+// message), exchanged in one NCCL group, unpacked; then the planes go as in the slab exchange.
+int nccl_halo_pencil(void* c, const nks_grid& g, double* vec, int nf, double* stage, cudaStream_t s) {
+  NcclComm* C = (NcclComm*)c;
+  std::vector<nks_halo_msg> plan;
+  pencil_halo_plan(g, C->rank, nf, plan);
+  const long long nxy = (long long)g.n[0] * g.n[1];
+  const int nzo = g.n[2] - 2 * g.zghost;
+  const size_t pitch = (size_t)nxy * sizeof(double);
+  std::vector<double*> st(plan.size(), nullptr);
+  double* p = stage;
+  for (size_t k = 0; k < plan.size(); ++k) {
+    if (plan[k].kind < 2) continue;
+    st[k] = p;
+    p += plan[k].count * nzo;
+    if (plan[k].kind == 2 &&
+        cudaMemcpy2DAsync(st[k], plan[k].count * sizeof(double), vec + plan[k].offset, pitch, plan[k].count * sizeof(double),
+                          nzo, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return 1;
+  }
+  if (ncclGroupStart() != ncclSuccess) return 1;
+  for (size_t k = 0; k < plan.size(); ++k) {
+    const auto& m = plan[k];
+    if (m.kind < 2) continue;
+    const size_t n = (size_t)m.count * nzo;
+    const ncclResult_t r = m.kind == 2 ? ncclSend(st[k], n, ncclDouble, m.peer, C->comm, s)
+                                       : ncclRecv(st[k], n, ncclDouble, m.peer, C->comm, s);
+    if (r != ncclSuccess) { ncclGroupEnd(); return 1; }
+  }
+  if (ncclGroupEnd() != ncclSuccess) return 1;
+  for (size_t k = 0; k < plan.size(); ++k)
+    if (plan[k].kind == 3 &&
+        cudaMemcpy2DAsync(vec + plan[k].offset, pitch, st[k], plan[k].count * sizeof(double), plan[k].count * sizeof(double),
+                          nzo, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return 1;
+  if (ncclGroupStart() != ncclSuccess) return 1;
+  for (const auto& m : plan) {
+    if (m.kind > 1) continue;
+    const ncclResult_t r = m.kind == 0 ? ncclSend(vec + m.offset, (size_t)m.count, ncclDouble, m.peer, C->comm, s)
+                                       : ncclRecv(vec + m.offset, (size_t)m.count, ncclDouble, m.peer, C->comm, s);
+    if (r != ncclSuccess) { ncclGroupEnd(); return 1; }
   }
   return ncclGroupEnd() == ncclSuccess ? 0 : 1;
 }

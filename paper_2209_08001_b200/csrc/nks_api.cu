@@ -90,6 +90,9 @@ void* nccl_create(const uint8_t id[128], int rank, int nranks, std::string& err)
 void nccl_destroy(void* c);
 int nccl_halo(void* c, double* vec, int nf, long long fstride, int nzl, long long nxy, int zg, cudaStream_t s);
 int nccl_allreduce_fixed(void* c, double* buf, long long n, double* gather, cudaStream_t s);
+int pencil_decompose(const nks_grid& global, int rank, int pz, int py, nks_grid& local);
+void pencil_halo_plan(const nks_grid& g, int rank, int nf, std::vector<nks_halo_msg>& out);
+int nccl_halo_pencil(void* c, const nks_grid& g, double* vec, int nf, double* stage, cudaStream_t s);
 // init_fft.cu
 int init_displacement_fft(const DevParams& P, const double* c, double* u, void* scratch, cudaStream_t s, std::string& err);
 }  // namespace nks
@@ -151,6 +154,16 @@ const char* validate(const nks_grid* g, const nks_params* p) {
   if (g->bc == 1 && g->zghost > 0) return "Neumann boundaries: single-GPU states only";
   if (g->bc == 1 && (p->pc_type == NKS_PC_RAS_SPECTRAL || p->ilu_level != 0))
     return "Neumann boundaries: pc_type NONE, SPECTRAL or the Schwarz family with BILU(0) boxes";
+  if (g->yghost != 0) {
+    if (g->yghost < 2 || g->yghost > 8) return "yghost must be 0 or 2..8";
+    if (g->zghost < 2) return "a pencil (yghost > 0) also carries z ghost planes (zghost >= 2)";
+    if (p->pc_type != NKS_PC_NONE) return "pencil states evaluate F and J.v only (pc_type NONE)";
+    const int owny = g->n[1] - 2 * g->yghost;
+    if (owny < 2) return "a pencil must own at least 2 rows";
+    if (g->ny_global < 5 || g->y_offset < 0 || g->y_offset + owny > g->ny_global)
+      return "pencil: y_offset / ny_global do not place the own rows in the global grid";
+    if (g->pz < 1 || g->py < 1) return "pencil: pz, py >= 1";
+  }
   if (g->zghost > 0) {
     if (g->dim != 3) return "z-slab states (zghost > 0) are 3D";
     const int own = g->n[2] - 2 * g->zghost;
@@ -250,6 +263,7 @@ DevParams make_devparams(const nks_grid& g, const nks_params& p) {
   P.dim = g.dim;
   P.nx = g.n[0]; P.ny = g.n[1]; P.nz = g.n[2];
   P.zg = g.zghost;
+  P.yg = g.yghost;
   P.bc = g.bc;
   P.N = (long long)g.n[0] * g.n[1] * g.n[2];
   P.h = g.h;
@@ -343,11 +357,13 @@ void sync(nks_state* st) {
 
 // ---- z-slab communication ------------------------------------------------------------------------
 bool slab(const nks_state* st) { return st->grid.zghost > 0; }
+bool pencil(const nks_state* st) { return st->grid.yghost > 0; }
 
-// Points of the whole (global) grid: own planes of every rank.
+// Points of the whole (global) grid: own planes (and rows) of every rank.
 long long global_points(const nks_state* st) {
   if (!slab(st)) return st->N;
-  const long long nxy = (long long)st->grid.n[0] * st->grid.n[1];
+  const long long ny = pencil(st) ? (long long)st->dp.nyg : st->grid.n[1];
+  const long long nxy = (long long)st->grid.n[0] * ny;
   return st->dp.nzg > 0 ? nxy * st->dp.nzg : nxy * (st->grid.n[2] - 2 * st->grid.zghost);
 }
 
@@ -367,6 +383,10 @@ void halo(nks_state* st, double* vec, int nf) {
   if (!slab(st) || !st->comm_set) return;
   PhaseScope ps(st, PH_OTHER);   // halo exchanges are accounted under "other"
   if (st->nccl) {
+    if (pencil(st)) {       // y blocks (packed through the idle Krylov basis area), then whole planes
+      if (nccl_halo_pencil(st->nccl, st->grid, vec, nf, st->V, st->stream) != 0) throw CommError();
+      return;
+    }
     const long long nxy = (long long)st->grid.n[0] * st->grid.n[1];
     if (nccl_halo(st->nccl, vec, nf, st->N, st->grid.n[2], nxy, st->grid.zghost, st->stream) != 0) throw CommError();
     return;
@@ -1005,6 +1025,7 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, int32_t ra
   if (!workspace) return NKS_E_INVALID;
   if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks) return NKS_E_INVALID;
   if (grid->zghost == 0 && nranks != 1) return NKS_E_INVALID;     // a periodic whole-grid state is one rank
+  if (grid->yghost > 0 && nranks != grid->pz * grid->py) return NKS_E_INVALID;   // pencil: the pz x py grid
   IlukPattern Kpat;
   Layout L;
   try {
@@ -1031,6 +1052,10 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, int32_t ra
   if (grid->zghost > 0) {
     st->dp.zoff = grid->z_offset;
     st->dp.nzg = grid->nz_global;
+  }
+  if (grid->yghost > 0) {
+    st->dp.yoff = grid->y_offset;
+    st->dp.nyg = grid->ny_global;
   }
   const nks_status rc = guarded(st, [&]() -> nks_status {
     char* w = st->ws;
@@ -1166,6 +1191,7 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, int32_t ra
 
 nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, const double* u, int32_t on_device) {
   if (!st || !c || !eta) return NKS_E_INVALID;
+  if (pencil(st) && !u) return NKS_E_INVALID;        // pencil states take u (no u^0 solve)
   return guarded(st, [&]() -> nks_status {
     const long long N = st->N;
     CK(cudaMemcpyAsync(st->Xn, c, N * sizeof(double), kind_in(on_device), st->stream));
@@ -1235,6 +1261,12 @@ int32_t nks_halo_plan(const nks_grid* local, int32_t rank, int32_t nranks, int32
                       int32_t cap) {
   if (!local || local->zghost <= 0 || nranks < 1 || rank < 0 || rank >= nranks || nfields < 1) return -1;
   std::vector<nks_halo_msg> plan;
+  if (local->yghost > 0) {
+    if (local->pz < 1 || local->py < 1 || nranks != local->pz * local->py) return -1;
+    pencil_halo_plan(*local, rank, nfields, plan);
+    for (int k = 0; k < (int)plan.size() && k < cap && out; ++k) out[k] = plan[k];
+    return (int32_t)plan.size();
+  }
   const long long nxy = (long long)local->n[0] * local->n[1];
   halo_plan(rank, nranks, nfields, nxy * local->n[2], local->n[2], nxy, local->zghost, plan);
   for (int k = 0; k < (int)plan.size() && k < cap && out; ++k) out[k] = plan[k];
@@ -1244,6 +1276,14 @@ int32_t nks_halo_plan(const nks_grid* local, int32_t rank, int32_t nranks, int32
 nks_status nks_get_unique_id(uint8_t id[128]) {
   if (!id) return NKS_E_INVALID;
   return nccl_unique_id(id) == 0 ? NKS_OK : NKS_E_NCCL;
+}
+
+nks_status nks_decompose_pencil(const nks_grid* global, int32_t rank, int32_t pz, int32_t py, nks_grid* local) {
+  if (!global || !local || pz < 1 || py < 1 || pz * py > kMaxRanks) return NKS_E_INVALID;
+  nks_grid loc{};
+  if (pencil_decompose(*global, rank, pz, py, loc) != 0) return NKS_E_INVALID;
+  *local = loc;
+  return NKS_OK;
 }
 
 nks_status nks_decompose(const nks_grid* global, const nks_params* params, int32_t rank, int32_t nranks,
@@ -1312,6 +1352,7 @@ nks_status nks_get_fields(const nks_state* cst, double* c, double* eta, double* 
 
 nks_status nks_step(nks_state* st, double dt, nks_step_info* info) {
   if (!st) return NKS_E_INVALID;
+  if (pencil(st)) return NKS_E_INVALID;                   // pencil states: F and J.v only
   if (!st->have_fields) return NKS_E_STATE;
   if (slab(st) && !st->comm_set) return NKS_E_STATE;
   return guarded(st, [&]() { return step_impl(st, dt, info); });
@@ -1319,6 +1360,7 @@ nks_status nks_step(nks_state* st, double dt, nks_step_info* info) {
 
 nks_status nks_run_adaptive(nks_state* st, int32_t max_steps, double t_end, nks_step_info* per_step, int32_t* done) {
   if (!st || max_steps < 0) return NKS_E_INVALID;
+  if (pencil(st)) return NKS_E_INVALID;                   // pencil states: F and J.v only
   if (!st->have_fields) return NKS_E_STATE;
   if (slab(st) && !st->comm_set) return NKS_E_STATE;
   if (done) *done = 0;
@@ -1361,6 +1403,7 @@ nks_status nks_run_adaptive(nks_state* st, int32_t max_steps, double t_end, nks_
 
 nks_status nks_energy(nks_state* st, double parts[4], double* mass) {
   if (!st || !parts || !mass) return NKS_E_INVALID;
+  if (pencil(st)) return NKS_E_INVALID;                   // pencil states: F and J.v only
   if (!st->have_fields) return NKS_E_STATE;
   if (slab(st) && !st->comm_set) return NKS_E_STATE;
   return guarded(st, [&]() -> nks_status {
@@ -1376,6 +1419,7 @@ nks_status nks_eval_residual(nks_state* st, double dt, const double* x_b, double
     set_dt(st, dt);
     const size_t nb = st->nvec * sizeof(double);
     CK(cudaMemcpyAsync(st->Xt, x_b, nb, kind_in(on_device), st->stream));
+    if (pencil(st)) halo(st, st->Xt, st->nf);          // pencils fill their ghosts here (slabs: the caller)
     residual(st, st->Xt, st->Ft);
     CK(cudaMemcpyAsync(F, st->Ft, nb, kind_out(on_device), st->stream));
     sync(st);
@@ -1391,6 +1435,10 @@ nks_status nks_eval_jv(nks_state* st, double dt, const double* x_b, const double
     const size_t nb = st->nvec * sizeof(double);
     CK(cudaMemcpyAsync(st->Xt, x_b, nb, kind_in(on_device), st->stream));
     CK(cudaMemcpyAsync(st->W2, v, nb, kind_in(on_device), st->stream));
+    if (pencil(st)) {
+      halo(st, st->Xt, st->nf);
+      halo(st, st->W2, st->nf);
+    }
     {
       PhaseScope ps(st, PH_OTHER);
       launch_pointwise_jac(st->dp, st->Xn, st->Xt, st->jac4, st->stream);
@@ -1405,6 +1453,7 @@ nks_status nks_eval_jv(nks_state* st, double dt, const double* x_b, const double
 
 nks_status nks_pc_setup(nks_state* st, double dt, const double* x_b, int32_t on_device) {
   if (!st || !x_b || !(dt > 0)) return NKS_E_INVALID;
+  if (pencil(st)) return NKS_E_INVALID;                   // pencil states: F and J.v only
   if (!st->have_fields) return NKS_E_STATE;
   return guarded(st, [&]() -> nks_status {
     set_dt(st, dt);
@@ -1422,6 +1471,7 @@ nks_status nks_pc_setup(nks_state* st, double dt, const double* x_b, int32_t on_
 
 nks_status nks_pc_apply(nks_state* st, const double* r, double* z, int32_t on_device) {
   if (!st || !r || !z) return NKS_E_INVALID;
+  if (pencil(st)) return NKS_E_INVALID;                   // pencil states: F and J.v only
   if (st->prm.pc_type != NKS_PC_NONE && !st->pc_valid) return NKS_E_STATE;
   return guarded(st, [&]() -> nks_status {
     const size_t nb = st->nvec * sizeof(double);
@@ -1436,6 +1486,7 @@ nks_status nks_pc_apply(nks_state* st, const double* r, double* z, int32_t on_de
 nks_status nks_gmres_solve(nks_state* st, double dt, const double* x_b, const double* rhs, double* s, int32_t on_device,
                            int32_t* its) {
   if (!st || !x_b || !rhs || !s || !(dt > 0)) return NKS_E_INVALID;
+  if (pencil(st)) return NKS_E_INVALID;                   // pencil states: F and J.v only
   if (!st->have_fields) return NKS_E_STATE;
   return guarded(st, [&]() -> nks_status {
     set_dt(st, dt);

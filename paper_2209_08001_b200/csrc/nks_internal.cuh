@@ -26,6 +26,9 @@ struct DevParams {
   int zg;               // z ghost planes per side (0: periodic in z; >= 2: slab of a z-sharded grid, no z wrap)
   int zoff;             // slab: global z of the first own plane (parity classes of the gauge)
   int nzg;              // slab: global number of planes (0 when not a slab)
+  int yg;               // pencil: y ghost rows per side (0: periodic in y, no y split)
+  int yoff;             // pencil: global y of the first own row
+  int nyg;              // pencil: global number of rows
   int bc;               // 0 periodic, 1 homogeneous Neumann (mirror ghosts, reading R38)
   long long N;          // points
   double h, inv_h2, inv_2h, inv_4h2;

@@ -151,6 +151,7 @@ __global__ void k_energy(DevParams P, const double* __restrict__ X, double* __re
     const int y = (int)((i / P.nx) % P.ny);
     const int z = (int)(i / ((long long)P.nx * P.ny));
     if (z < P.zg || z >= P.nz - P.zg) continue;       // slab: own planes only
+    if (y < P.yg || y >= P.ny - P.yg) continue;       // pencil: own rows only
     const double c = c_[i], eta = e_[i];
     double e1, e2;
     local_energy(P, c, eta, e1, e2);
@@ -205,8 +206,9 @@ __global__ void k_gauge_sums(DevParams P, const double* __restrict__ X, int even
     const int y = (int)((i / P.nx) % P.ny);
     const int z = (int)(i / ((long long)P.nx * P.ny));
     if (z < P.zg || z >= P.nz - P.zg) continue;       // slab: own planes only
+    if (y < P.yg || y >= P.ny - P.yg) continue;       // pencil: own rows only
     int cls = 0, bit = 0;
-    const int co[3] = {x, y, z - P.zg + P.zoff};        // global coordinates (parity classes)
+    const int co[3] = {x, y - P.yg + P.yoff, z - P.zg + P.zoff};   // global coordinates (parity classes)
 #pragma unroll
     for (int j = 0; j < DIM; ++j)
       if (evenmask & (1 << j)) { cls |= (co[j] & 1) << bit; ++bit; }
@@ -233,7 +235,7 @@ __global__ void k_gauge_apply(DevParams P, double* __restrict__ X, int evenmask,
     const int y = (int)((i / P.nx) % P.ny);
     const int z = (int)(i / ((long long)P.nx * P.ny));
     int cls = 0, bit = 0;
-    const int co[3] = {x, y, z - P.zg + P.zoff};        // ghost planes get their (global) class too
+    const int co[3] = {x, y - P.yg + P.yoff, z - P.zg + P.zoff};   // ghost planes / rows get their (global) class too
 #pragma unroll
     for (int j = 0; j < DIM; ++j)
       if (evenmask & (1 << j)) { cls |= (co[j] & 1) << bit; ++bit; }
@@ -269,7 +271,7 @@ void launch_energy(const DevParams& P, const double* X, double* part, double* ou
 int gauge_classes(const DevParams& P, int& evenmask) {
   evenmask = 0;
   int nbits = 0;
-  const int n[3] = {P.nx, P.ny, P.nzg > 0 ? P.nzg : P.nz};
+  const int n[3] = {P.nx, P.nyg > 0 ? P.nyg : P.ny, P.nzg > 0 ? P.nzg : P.nz};
   for (int j = 0; j < P.dim; ++j)
     if (n[j] % 2 == 0) { evenmask |= 1 << j; ++nbits; }
   return 1 << nbits;
@@ -293,8 +295,7 @@ int launch_gauge_sums(const DevParams& P, const double* X, double* part, double*
 void launch_gauge_apply(const DevParams& P, double* X, const double* out, cudaStream_t s) {
   int evenmask;
   const int ncls = gauge_classes(P, evenmask);
-  const long long nown = P.N / P.nz * (P.nz - 2 * P.zg);
-  const long long nglob = P.nzg > 0 ? nown / (P.nz - 2 * P.zg) * P.nzg : P.N;
+  const long long nglob = (long long)P.nx * (P.nyg > 0 ? P.nyg : P.ny) * (P.nzg > 0 ? P.nzg : P.nz);
   const double inv_count = (double)ncls / (double)nglob;
   const int blocks = (int)std::min<long long>((P.N + 255) / 256, 148 * 16);
   if (P.dim == 2) k_gauge_apply<2><<<blocks, 256, 0, s>>>(P, X, evenmask, out, inv_count);

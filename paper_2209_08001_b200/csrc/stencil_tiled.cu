@@ -95,8 +95,9 @@ __global__ void __launch_bounds__(tj::NTF) k_jv_tiled(DevParams P, const double*
   double* sw = sa + 2 * PL;                  // [N3][RL]
 
   const long long N = P.N;
-  const int nx = P.nx, ny = P.ny, nz = P.nz, zg = P.zg;
+  const int nx = P.nx, ny = P.ny, nz = P.nz, zg = P.zg, yg = P.yg;
   const int ncz = nz - 2 * zg;                 // computed planes (all, or the slab's own planes)
+  const int ncy = ny - 2 * yg;                 // computed rows (all, or the pencil's own rows)
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int z0 = DIM == 3 ? blockIdx.z * zc : 0;
   const int z1 = DIM == 3 ? min(z0 + zc, ncz) : 1;
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(tj::NTF) k_jv_tiled(DevParams P, const double*
   for (int r = 0; r < 2; ++r) {
     const int c = tid + r * NTF;
     cell[r] = c < PL ? c : -1;
-    int gx = x0 + (c % HX) - 2, gy = y0 + (c / HX) - 2;
+    int gx = x0 + (c % HX) - 2, gy = y0 + (c / HX) - 2 + yg;   // pencil: own rows start at yg, ghost rows below
     gx = ((gx % nx) + nx) % nx;        // tiles may be wider than the grid
     gy = ((gy % ny) + ny) % ny;
     goff[r] = (long long)gy * nx + gx;
@@ -200,13 +201,13 @@ __global__ void __launch_bounds__(tj::NTF) k_jv_tiled(DevParams P, const double*
   const int hc = (ty + 2) * HX + (tx + 2);     // centre in the halo plane
   const int rc = (ty + 1) * RX + (tx + 1);     // centre in the ring
   const int x = x0 + tx, y = y0 + ty;
-  const bool inside = x < nx && y < ny && tid < NT;
+  const bool inside = x < nx && y < ncy && tid < NT;
 
   // register prefetch of the planes the NEXT iteration commits to shared memory (hides HBM latency
   // behind this iteration's arithmetic): u_x,u_y,u_z, v_c at z+2; v_eta, c^a, a11, a12 at z+1
   double R[8][2];
   double A21 = 0.0, A22 = 0.0;                   // centre a21, a22 of the plane the iteration outputs
-  const long long gc_off = (long long)min(y0 + ty, ny - 1) * nx + min(x0 + tx, nx - 1);
+  const long long gc_off = (long long)(min(y0 + ty, ncy - 1) + yg) * nx + min(x0 + tx, nx - 1);
   auto fetch = [&](int z) {
     const long long b2 = (long long)zw(z + 2) * nx * ny, b1 = (long long)zw(z + 1) * nx * ny;
     const long long b0 = (long long)zw(z) * nx * ny;
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(tj::NTF) k_jv_tiled(DevParams P, const double*
       __syncthreads();
     }
     if (inside) {
-      const long long i = ((long long)(z + zg) * ny + y) * nx + x;
+      const long long i = ((long long)(z + zg) * ny + (y + yg)) * nx + x;
       const double* C0 = sc + slot(z, NC) * PL;
       const double* E0 = se + slot(z, N3) * PL;
       const double* M0 = smo + slot(z, N3) * PL;
@@ -306,8 +307,9 @@ __global__ void __launch_bounds__(tj::NTF) k_residual_tiled(DevParams P, const d
   double* sg = sT + PL;                      // [N3][RL]       G_c
 
   const long long N = P.N;
-  const int nx = P.nx, ny = P.ny, nz = P.nz, zg = P.zg;
+  const int nx = P.nx, ny = P.ny, nz = P.nz, zg = P.zg, yg = P.yg;
   const int ncz = nz - 2 * zg;                 // computed planes (all, or the slab's own planes)
+  const int ncy = ny - 2 * yg;                 // computed rows (all, or the pencil's own rows)
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int z0 = DIM == 3 ? blockIdx.z * zc : 0;
   const int z1 = DIM == 3 ? min(z0 + zc, ncz) : 1;
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(tj::NTF) k_residual_tiled(DevParams P, const d
   for (int r = 0; r < 2; ++r) {
     const int c = tid + r * NTF;
     cell[r] = c < PL ? c : -1;
-    int gx = x0 + (c % HX) - 2, gy = y0 + (c / HX) - 2;
+    int gx = x0 + (c % HX) - 2, gy = y0 + (c / HX) - 2 + yg;
     gx = ((gx % nx) + nx) % nx;
     gy = ((gy % ny) + ny) % ny;
     goff[r] = (long long)gy * nx + gx;
@@ -372,7 +374,7 @@ __global__ void __launch_bounds__(tj::NTF) k_residual_tiled(DevParams P, const d
       const double Tb = P.K * (div * P.inv_2h - DIM * P.eps0 * (cb - P.cbar0));
       Gp[r] = gc - 0.5 * P.eps0 * (sT[k] + Tb) + gcl * 0.5 * lap;
       const int px = x0 + rx - 1, py = y0 + ry - 1;
-      if (write_eta && rx >= 1 && rx <= TX && ry >= 1 && ry <= TY && px < nx && py < ny) {
+      if (write_eta && rx >= 1 && rx <= TX && ry >= 1 && ry <= TY && px < nx && py < ncy) {
         const double ea = EA[k], eb = EB[k];
         double le = (EA[k - 1] + EB[k - 1]) + (EA[k + 1] + EB[k + 1]) + (EA[k - HX] + EB[k - HX]) +
                     (EA[k + HX] + EB[k + HX]) - 4.0 * (ea + eb);
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(tj::NTF) k_residual_tiled(DevParams P, const d
           const int m1 = tslot(z - 1, N3) * PL + k, p1 = tslot(z + 1, N3) * PL + k;
           le += (sea[m1] + seb[m1]) + (sea[p1] + seb[p1]) - 2.0 * (ea + eb);
         }
-        const long long i = ((long long)(z + zg) * ny + py) * nx + px;
+        const long long i = ((long long)(z + zg) * ny + (py + yg)) * nx + px;
         F[N + i] = (eb - ea) * P.inv_dt + ge + gel * le;
       }
     }
@@ -421,7 +423,7 @@ __global__ void __launch_bounds__(tj::NTF) k_residual_tiled(DevParams P, const d
   const int hc = (ty + 2) * HX + (tx + 2);
   const int rc = (ty + 1) * RX + (tx + 1);
   const int x = x0 + tx, y = y0 + ty;
-  const bool inside = x < nx && y < ny && tid < NT;
+  const bool inside = x < nx && y < ncy && tid < NT;
 
   // register prefetch of the next iteration's planes: u^b (3), c^b, c^a, eta^a, eta^b at z+2; T^a at z+1
   double R[8][2];
@@ -466,7 +468,7 @@ __global__ void __launch_bounds__(tj::NTF) k_residual_tiled(DevParams P, const d
       __syncthreads();
     }
     if (inside) {
-      const long long i = ((long long)(z + zg) * ny + y) * nx + x;
+      const long long i = ((long long)(z + zg) * ny + (y + yg)) * nx + x;
       const double* CA = sca + tslot(z, NC) * PL;
       const double* CB = scb + tslot(z, NC) * PL;
       const double* G0 = sg + tslot(z, N3) * RL;
@@ -511,14 +513,14 @@ void launch_residual_tiled(const DevParams& P, const double* Xa, const double* X
     else cudaFuncSetAttribute(k_residual_tiled<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (dev >= 0 && dev < 64) attr[dev][dim] = true;
   }
-  const int tiles = ((P.nx + TX - 1) / TX) * ((P.ny + TY - 1) / TY);
+  const int tiles = ((P.nx + TX - 1) / TX) * ((P.ny - 2 * P.yg + TY - 1) / TY);
   int zc = 1;
   if (dim == 3) {
     const int ncz = P.nz - 2 * P.zg;
     zc = ncz;
     while (zc > 16 && (long long)tiles * ((ncz + zc - 1) / zc) < 148 * 2 * 4) zc = (zc + 1) / 2;
   }
-  dim3 grid((P.nx + TX - 1) / TX, (P.ny + TY - 1) / TY, dim == 3 ? (P.nz - 2 * P.zg + zc - 1) / zc : 1);
+  dim3 grid((P.nx + TX - 1) / TX, (P.ny - 2 * P.yg + TY - 1) / TY, dim == 3 ? (P.nz - 2 * P.zg + zc - 1) / zc : 1);
   if (dim == 2) k_residual_tiled<2><<<grid, NTF, smem, s>>>(P, Xa, Xb, Ta, F, zc);
   else k_residual_tiled<3><<<grid, NTF, smem, s>>>(P, Xa, Xb, Ta, F, zc);
 }
@@ -543,7 +545,7 @@ void launch_jv_tiled(const DevParams& P, const double* Xa, const double* jac4, c
     else cudaFuncSetAttribute(k_jv_tiled<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (dev >= 0 && dev < 64) attr[dev][dim] = true;
   }
-  const int tiles = ((P.nx + TX - 1) / TX) * ((P.ny + TY - 1) / TY);
+  const int tiles = ((P.nx + TX - 1) / TX) * ((P.ny - 2 * P.yg + TY - 1) / TY);
   int zc = 1;
   if (dim == 3) {
     // z chunks: enough CTAs for ~4 waves of 2 CTAs/SM, chunks long enough to amortise the 4-plane prologue
@@ -551,7 +553,7 @@ void launch_jv_tiled(const DevParams& P, const double* Xa, const double* jac4, c
     zc = ncz;
     while (zc > 16 && (long long)tiles * ((ncz + zc - 1) / zc) < 148 * 2 * 4) zc = (zc + 1) / 2;
   }
-  dim3 grid((P.nx + TX - 1) / TX, (P.ny + TY - 1) / TY, dim == 3 ? (P.nz - 2 * P.zg + zc - 1) / zc : 1);
+  dim3 grid((P.nx + TX - 1) / TX, (P.ny - 2 * P.yg + TY - 1) / TY, dim == 3 ? (P.nz - 2 * P.zg + zc - 1) / zc : 1);
   if (dim == 2) k_jv_tiled<2><<<grid, NTF, smem, s>>>(P, Xa, jac4, v, out, zc);
   else k_jv_tiled<3><<<grid, NTF, smem, s>>>(P, Xa, jac4, v, out, zc);
 }

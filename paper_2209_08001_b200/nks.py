@@ -26,7 +26,8 @@ PHASES = ["residual", "jv", "ras_apply", "assemble", "factor", "gmres_vec", "red
 class Grid(C.Structure):
     _fields_ = [("dim", C.c_int32), ("n", C.c_int32 * 3), ("h", C.c_double), ("nsub", C.c_int32 * 3),
                 ("overlap", C.c_int32), ("zghost", C.c_int32), ("z_offset", C.c_int32), ("nz_global", C.c_int32),
-                ("bc", C.c_int32)]
+                ("bc", C.c_int32), ("yghost", C.c_int32), ("y_offset", C.c_int32), ("ny_global", C.c_int32),
+                ("pz", C.c_int32), ("py", C.c_int32), ("pad_", C.c_int32)]
 
 
 class Params(C.Structure):
@@ -78,6 +79,7 @@ _SIGS = {
     "nks_get_unique_id": (C.c_int, [_P]),
     "nks_decompose": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), C.c_int32, C.c_int32, C.POINTER(Grid)]),
     "nks_halo_plan": (C.c_int32, [C.POINTER(Grid), C.c_int32, C.c_int32, C.c_int32, C.POINTER(HaloMsg), C.c_int32]),
+    "nks_decompose_pencil": (C.c_int, [C.POINTER(Grid), C.c_int32, C.c_int32, C.c_int32, C.POINTER(Grid)]),
     "nks_set_fields": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
     "nks_get_fields": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
     "nks_set_state": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
@@ -159,10 +161,19 @@ def halo_plan(local: Grid, rank: int, nranks: int, nfields: int):
     lib = load_library()
     n = lib.nks_halo_plan(C.byref(local), int(rank), int(nranks), int(nfields), None, 0)
     if n < 0:
-        raise NKSError(NKS_E_INVALID, "nks_halo_plan: invalid slab")
+        raise NKSError(NKS_E_INVALID, "nks_halo_plan: invalid slab / pencil")
     buf = (HaloMsg * n)()
     lib.nks_halo_plan(C.byref(local), int(rank), int(nranks), int(nfields), buf, n)
     return [(m.kind, m.peer, m.offset, m.count) for m in buf]
+
+
+def decompose_pencil(global_grid: Grid, rank: int, pz: int, py: int) -> Grid:
+    """nks_decompose_pencil: the z x y pencil grid of `rank` = rz * py + ry on a pz x py process grid (host only)."""
+    out = Grid()
+    rc = load_library().nks_decompose_pencil(C.byref(global_grid), int(rank), int(pz), int(py), C.byref(out))
+    if rc != NKS_OK:
+        raise NKSError(rc, "nks_decompose_pencil: no valid pencil for this grid / process grid")
+    return out
 
 
 def decompose(global_grid: Grid, params: Params, rank: int, nranks: int) -> Grid:

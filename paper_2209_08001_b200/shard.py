@@ -305,3 +305,162 @@ class ShardedSolver:
         lg = decompose(make_grid(self.shape_global, self.h, (self.nsub_z, 1, 1), self.lgrid.overlap), params, r,
                        self.world)
         return int(lg.z_offset), int(lg.z_offset) + int(lg.n[2]) - 2 * int(lg.zghost)
+
+
+def run_halo_plan(vec, plan, local, rank: int, group=None):
+    """Execute the library's halo message list (nks_halo_plan: the ncclSend/ncclRecv sequence the library
+    issues) with torch.distributed point-to-point calls on a flat tensor `vec` of one local vector.
+
+    Kinds 0 / 1 send / receive `count` contiguous doubles at `offset`; kinds 2 / 3 (pencils) a y block of
+    `count` doubles per own plane, packed plane after plane.  Messages are matched per peer in issue order
+    (the k-th message between two ranks gets tag k on both sides, NCCL's rule); a pencil's y phase completes
+    before its plane phase starts.  Messages to this rank itself (a process-grid axis of length 1) pair up
+    locally in the same order."""
+    import torch
+    import torch.distributed as dist
+    nx, nyl, nzl = local.n[0], local.n[1], local.n[2]
+    nxy, zg = nx * nyl, local.zghost
+    nzo = nzl - 2 * zg
+
+    def gather(off, cnt, kind):
+        if kind < 2:
+            return vec[off:off + cnt].clone()
+        return torch.stack([vec[off + p * nxy: off + p * nxy + cnt] for p in range(nzo)]).reshape(-1).clone()
+
+    def scatter(off, cnt, kind, buf):
+        if kind < 2:
+            vec[off:off + cnt] = buf
+            return
+        b = buf.view(nzo, cnt)
+        for p in range(nzo):
+            vec[off + p * nxy: off + p * nxy + cnt] = b[p]
+
+    seq_send, seq_recv = {}, {}
+    for phase in ((2, 3), (0, 1)):
+        reqs, self_q, pending_self = [], [], []
+        for kind, peer, off, cnt in plan:
+            if kind not in phase:
+                continue
+            sending = kind in (0, 2)
+            if peer == rank:
+                (self_q if sending else pending_self).append(gather(off, cnt, kind) if sending else (off, cnt, kind))
+                continue
+            if sending:
+                tag = seq_send.get(peer, 0)
+                seq_send[peer] = tag + 1
+                reqs.append(dist.isend(gather(off, cnt, kind), peer, tag=tag, group=group))
+            else:
+                tag = seq_recv.get(peer, 0)
+                seq_recv[peer] = tag + 1
+                buf = torch.empty(cnt * (nzo if kind == 3 else 1), dtype=vec.dtype)
+                reqs.append((dist.irecv(buf, peer, tag=tag, group=group), off, cnt, kind, buf))
+        for (off, cnt, kind), buf in zip(pending_self, self_q):
+            scatter(off, cnt, kind, buf)
+        for r in reqs:
+            if isinstance(r, tuple):
+                r[0].wait()
+                scatter(r[1], r[2], r[3], r[4])
+            else:
+                r.wait()
+
+
+class PencilSolver:
+    """One z x y pencil of a 3D periodic grid per rank on a pz x py process grid (rank = rz * py + ry):
+    the residual F and the Jacobian action J.v of the library on a pencil-sharded grid (BASELINE
+    configs 4/5 "slab- then pencil-sharded"; the NKS step itself shards by z-slabs, ShardedSolver).
+
+    The library decomposes the grid (nks_decompose_pencil: planes and rows dealt out, 2 ghost planes / rows
+    per side) and fills the ghosts itself inside nks_eval_residual / nks_eval_jv: with comm="nccl" through its
+    own communicator (y blocks packed and exchanged in one NCCL group, then whole planes, so the (y, z) edge
+    cells arrive), with comm="callbacks" through this object's host callback, which runs the library's own
+    message list (nks_halo_plan) over the torch process group (host-staged; emulated ranks on one GPU)."""
+
+    def __init__(self, shape_global, model, solver, pz, py, h=0.25, group=None, device=None, comm="auto"):
+        import torch
+        from .nks import PC_NONE, Solver, decompose_pencil, halo_plan, make_grid, unique_id
+        self.torch = torch
+        self.group = group
+        self.world, self.rank = _world(group)
+        if self.world != pz * py:
+            raise ValueError("the process grid pz x py must match the group size")
+        self.shape_global = tuple(int(v) for v in shape_global)
+        self.lgrid = decompose_pencil(make_grid(self.shape_global, h), self.rank, pz, py)
+        g = self.lgrid
+        self.zg, self.yg = int(g.zghost), int(g.yghost)
+        self.z0, self.y0 = int(g.z_offset), int(g.y_offset)
+        self.local_shape = (int(g.n[2]), int(g.n[1]), int(g.n[0]))
+        self.nzo, self.nyo = self.local_shape[0] - 2 * self.zg, self.local_shape[1] - 2 * self.yg
+        if comm == "auto":
+            comm = "nccl" if (self.world == 1 or not _is_gloo(group)) else "callbacks"
+        self.comm = comm
+        self.halo_calls = 0
+        nccl_id = None
+        if comm == "nccl":
+            nccl_id = unique_id() if self.rank == 0 else None
+            if self.world > 1:
+                import torch.distributed as dist
+                box = [nccl_id]
+                src = dist.get_global_rank(group, 0) if group is not None else 0
+                dist.broadcast_object_list(box, src=src, group=group)
+                nccl_id = box[0]
+        self.solver = Solver(self.local_shape, model, solver, h=h, pc_type=PC_NONE, device=device, grid=g,
+                             rank=self.rank, nranks=self.world, nccl_id=nccl_id)
+        self.device = self.solver.device
+        self._plan = {}
+        self._halo_plan = halo_plan
+        if comm == "callbacks":
+            self.solver.set_comm(self._allreduce, self._halo)
+
+    def _allreduce(self, ptr, n, stream):
+        with self.torch.cuda.stream(self.solver.stream):
+            allreduce_fixed_order(self.solver.device_view(ptr, n), self.group)
+        return 0
+
+    def _halo(self, ptr, nf, stride, stream):
+        self.halo_calls += 1
+        if nf not in self._plan:
+            self._plan[nf] = self._halo_plan(self.lgrid, self.rank, self.world, nf)
+        v = self.solver.device_view(ptr, nf * stride)
+        self.torch.cuda.current_stream(self.device).synchronize()
+        self.solver.stream.synchronize()
+        host = v.cpu() if (self.world > 1 and _is_gloo(self.group)) else v
+        run_halo_plan(host, self._plan[nf], self.lgrid, self.rank, self.group)
+        if host is not v:
+            with self.torch.cuda.stream(self.solver.stream):
+                v.copy_(host.to(self.device))
+        return 0
+
+    def local(self, field):
+        """This rank's pencil (own planes / rows + ghosts, periodic) of a global (..., nz, ny, nx) field."""
+        nz, ny, _ = self.shape_global
+        zi = [(z % nz) for z in range(self.z0 - self.zg, self.z0 + self.nzo + self.zg)]
+        yi = [(y % ny) for y in range(self.y0 - self.yg, self.y0 + self.nyo + self.yg)]
+        a = np.asarray(field)
+        return a[..., zi, :, :][..., yi, :].copy()
+
+    def own(self, local_field):
+        """The own planes / rows of a local (..., nzl, nyl, nx) field."""
+        return local_field[..., self.zg:self.zg + self.nzo, self.yg:self.yg + self.nyo, :]
+
+    def set_fields(self, c, eta, u):
+        """Global c, eta (nz, ny, nx) and u (3, nz, ny, nx); the ghosts are refilled by the library."""
+        self.solver.set_fields(self.local(c), self.local(eta), self.local(u))
+
+    def residual(self, Xb, dt):
+        """F on the own points for a global state Xb (5, nz, ny, nx); the local ghosts are sent as NaN and
+        refilled by the library's halo exchange."""
+        loc = self.local(Xb)
+        loc[:, :self.zg] = np.nan
+        loc[:, -self.zg:] = np.nan
+        loc[:, :, :self.yg] = np.nan
+        loc[:, :, -self.yg:] = np.nan
+        return self.own(self.solver.eval_residual(loc, dt))
+
+    def jv(self, Xb, v, dt):
+        loc, lv = self.local(Xb), self.local(v)
+        for a in (loc, lv):
+            a[:, :self.zg] = np.nan
+            a[:, -self.zg:] = np.nan
+            a[:, :, :self.yg] = np.nan
+            a[:, :, -self.yg:] = np.nan
+        return self.own(self.solver.eval_jv(loc, lv, dt))

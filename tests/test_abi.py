@@ -59,7 +59,8 @@ int main(void) {
   printf("nks_params %zu\n", sizeof(nks_params));
   printf("nks_step_info %zu\n", sizeof(nks_step_info));
   F(nks_grid, h) F(nks_grid, nsub) F(nks_grid, overlap) F(nks_grid, zghost) F(nks_grid, z_offset)
-  F(nks_grid, nz_global) F(nks_grid, bc)
+  F(nks_grid, nz_global) F(nks_grid, bc) F(nks_grid, yghost) F(nks_grid, y_offset) F(nks_grid, ny_global)
+  F(nks_grid, pz) F(nks_grid, py)
   F(nks_params, S) F(nks_params, newton_rtol) F(nks_params, pc_reuse) F(nks_params, ls_alpha)
   F(nks_params, zeta) F(nks_params, xd_norm) F(nks_params, factor_fp32) F(nks_params, gmres_stall_cycles)
   F(nks_params, ilu_level) F(nks_params, u0_cg)
@@ -151,3 +152,24 @@ def test_decompose_deals_whole_box_layers(lib, nranks):
     assert z == nz
     with pytest.raises(nks.NKSError):
         nks.decompose(gg, p, 0, nsz + 1)           # fewer box layers than ranks
+
+
+@pytest.mark.parametrize("pz,py", [(1, 1), (1, 2), (2, 1), (2, 2), (3, 1), (1, 3), (2, 4)])
+def test_decompose_pencil_tiles_the_grid(lib, pz, py):
+    """nks_decompose_pencil (host only): the pencils of a pz x py process grid tile the global (z, y) range
+    exactly once, each with 2 ghost planes / rows per side (the stencils' radius) and its offsets set."""
+    g = nks.make_grid((24, 22, 16), 0.25, (1, 1, 1), 2)
+    seen = {}
+    for r in range(pz * py):
+        loc = nks.decompose_pencil(g, r, pz, py)
+        assert (loc.zghost, loc.yghost, loc.pz, loc.py) == (2, 2, pz, py)
+        assert (loc.nz_global, loc.ny_global, loc.n[0]) == (24, 22, 16)
+        nzo, nyo = loc.n[2] - 4, loc.n[1] - 4
+        assert nzo >= 2 and nyo >= 2
+        for z in range(loc.z_offset, loc.z_offset + nzo):
+            for y in range(loc.y_offset, loc.y_offset + nyo):
+                assert (z, y) not in seen
+                seen[(z, y)] = r
+    assert len(seen) == 24 * 22
+    with pytest.raises(nks.NKSError):
+        nks.decompose_pencil(g, 12, 13, 1)         # 24 planes over 13 parts: the last part owns one plane

@@ -167,3 +167,42 @@ def test_library_halo_plan_over_gloo(world):
     out = mp.Manager().dict()
     mp.spawn(_plan_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     assert all(out[r] == 0.0 for r in range(world)), dict(out)
+
+
+# ---------------------------------------------------------------------------------------- pencils (z x y)
+def _pencil_worker(rank, world, pz, py, port, out):
+    """Each rank takes its pencil from the library (nks_decompose_pencil) and runs the library's pencil halo
+    plan (y blocks, then whole planes) over gloo; every ghost cell -- the (y, z) edges included, which the
+    J.v stencil's (0, +-1, +-1) offsets read -- must equal the global periodic field."""
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        from paper_2209_08001_b200 import nks
+        from paper_2209_08001_b200.shard import run_halo_plan
+        nz, ny, nx, nf = 12, 10, 5, 5
+        lg = nks.decompose_pencil(nks.make_grid((nz, ny, nx), 0.25, (1, 1, 1), 2), rank, pz, py)
+        zg, yg, nzl, nyl = lg.zghost, lg.yghost, lg.n[2], lg.n[1]
+        g = np.random.default_rng(11).standard_normal((nf, nz, ny, nx))
+        zi = [(z % nz) for z in range(lg.z_offset - zg, lg.z_offset - zg + nzl)]
+        yi = [(y % ny) for y in range(lg.y_offset - yg, lg.y_offset - yg + nyl)]
+        want = g[:, zi][:, :, yi]
+        arr = want.copy()
+        arr[:, :zg] = np.nan
+        arr[:, -zg:] = np.nan
+        arr[:, :, :yg] = np.nan
+        arr[:, :, -yg:] = np.nan
+        vec = torch.from_numpy(arr).reshape(-1)
+        plan = nks.halo_plan(lg, rank, world, nf)
+        assert len(plan) == 8 * nf
+        assert [m[0] for m in plan[:4 * nf]] == [2, 2, 3, 3] * nf      # y phase first
+        run_halo_plan(vec, plan, lg, rank)
+        out[rank] = float(np.abs(vec.view(nf, nzl, nyl, nx).numpy() - want).max())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("pz,py", [(1, 2), (2, 1), (1, 3), (3, 1), (2, 2), (4, 1), (1, 4)])
+def test_library_pencil_halo_plan_over_gloo(pz, py):
+    world = pz * py
+    out = mp.Manager().dict()
+    mp.spawn(_pencil_worker, args=(world, pz, py, _free_port(), out), nprocs=world, join=True)
+    assert all(out[r] == 0.0 for r in range(world)), dict(out)
