@@ -366,6 +366,52 @@ def micro_sharded(shape, pg, reps=10):
     return res
 
 
+def micro_pencil(shape, pg, world, reps=10):
+    """Config 5 on z x y pencils (a pz x py process grid, the most square factorisation of the rank count):
+    F and J.v through the library's pencil state (nks_decompose_pencil; nks_eval_residual / nks_eval_jv fill
+    the ghost planes AND rows with the library's NCCL exchange: packed y blocks, then planes), the exchange
+    of every input included in the timed operator; time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2209_08001_b200.shard import PencilSolver
+    pz = max(p for p in range(1, int(world ** 0.5) + 1) if world % p == 0)
+    py = world // pz
+    ps = PencilSolver(shape, ni.model_default(), ni.solver_default(), pz, py,
+                      group=None if not dist.is_initialized() else dist.group.WORLD, comm="nccl")
+    nf, ls = 5, ps.local_shape
+    gen = torch.Generator(device="cuda").manual_seed(4321 + ps.rank)
+    c = 0.1622 + (torch.rand(ls, device="cuda", dtype=torch.float64, generator=gen) - 0.5) * 0.01
+    eta = 0.1 + (torch.rand(ls, device="cuda", dtype=torch.float64, generator=gen) - 0.5) * 0.02
+    u = torch.zeros((3,) + ls, device="cuda", dtype=torch.float64)
+    ps.solver.set_fields(c, eta, u)
+    Xb = torch.cat([c[None], eta[None], u])
+    Xb[:2] += (torch.rand((2,) + ls, device="cuda", dtype=torch.float64, generator=gen) - 0.5) * 2e-3
+    v = (torch.rand((nf,) + ls, device="cuda", dtype=torch.float64, generator=gen) - 0.5) * 2
+    del c, eta, u
+    for _ in range(2):
+        ps.solver.eval_residual(Xb, 0.01)
+        ps.solver.eval_jv(Xb, v, 0.01)
+    res = {"process_grid_pz_py": [pz, py]}
+    for key in ("residual", "jv"):
+        barrier(pg)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            if key == "residual":
+                ps.solver.eval_residual(Xb, 0.01)
+            else:
+                ps.solver.eval_jv(Xb, v, 0.01)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = max_over_ranks(pg, e0.elapsed_time(e1) / reps)
+        Ng = int(np.prod(shape))
+        res[key] = {"ms_incl_halo_exchange_and_d2d_copies": ms, "GDOF_s": nf * Ng / (ms * 1e-3) / 1e9}
+    del ps, Xb, v
+    torch.cuda.empty_cache()
+    return res
+
+
 def step_stats(per_ms):
     a = np.asarray(per_ms)
     return {"mean": float(a.mean()), "p50": float(np.percentile(a, 50)), "p90": float(np.percentile(a, 90)),
@@ -667,6 +713,10 @@ def run_gpu(args, world, rank, local, pg):
         torch.cuda.empty_cache()
         try:
             micro_sh = {"grid": [512, 512, 512], "sharding": f"z-slabs x {world}", **micro_sharded((512, 512, 512), pg)}
+            try:
+                micro_sh["pencils"] = micro_pencil((512, 512, 512), pg, world)
+            except Exception as e:            # reported, never silent
+                micro_sh["pencils"] = {"error": repr(e)[:300]}
         except Exception as e:
             micro_sh = {"error": str(e)[:200]}
     micro = {}
