@@ -68,6 +68,9 @@ template <bool F32> struct Strm {
 #ifndef NKS_R2_NBREL
 #define NKS_R2_NBREL 1
 #endif
+#ifndef NKS_R2_UNROLL
+#define NKS_R2_UNROLL 4      // steps per loop trip of the sweeps (4 or 8)
+#endif
 #ifndef NKS_R2_PSLEEP
 #define NKS_R2_PSLEEP 256    // producer back-off (ns) while the ring is full
 #endif
@@ -572,9 +575,20 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     // the same loads on 32-bit shared addresses: per-lane ring bases, one select between the ring and the
     // halo cell for the boundary lanes (no divergent branch)
     const unsigned sE = smem_u32(E), sH = smem_u32(H);
+    // exchange loads: ptxas otherwise sinks some of them below the twelve block-row preloads (register
+    // pressure), where they queue behind the preloads and the last DFMAs of the step wait on them (ncu source
+    // page); a volatile load stays in program order
+#ifndef NKS_R2_VOLX
+#define NKS_R2_VOLX 1
+#endif
     auto ld4a = [&](unsigned a, unsigned off2, double (&v)[4]) {
+#if NKS_R2_VOLX
+      asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(a) : "memory");
+      asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[2]), "=d"(v[3]) : "r"(a + off2) : "memory");
+#else
       asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(a) : "memory");
       asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[2]), "=d"(v[3]) : "r"(a + off2) : "memory");
+#endif
     };
     auto ering = [&](int k, int row) { return sE + (unsigned)(((k & 7) * 32 + row) * 16); };
     auto hcella = [&](int q, int i) { return sH + (unsigned)(q * pitch * 8 + (min(max(i, -2), ex + 1) + 2) * 32); };
@@ -637,6 +651,11 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       // will read -- sit right after the step barrier, where those loads are needed anyway.
       const bool pol = up_remote && !(R2_DBG(A) & 16);
       unsigned long long pvn = 0ull;                 // iteration 0's cells were checked in the prologue
+      // half(k+2)'s last two terms (M0[2..3] . aa4[2..3]) are finished after the next step barrier: ptxas
+      // sinks the second half of the aa4 load below the block-row preloads, and the step would otherwise
+      // end waiting for it (ncu source page); half(k+2) is first read in iteration k+1's pre(k+2)
+      double dm2 = 0.0, dm3 = 0.0, da2 = 0.0, da3 = 0.0;
+      auto finish_half = [&]() { half = fma(-dm3, da3, fma(-dm2, da2, half)); };
       auto fneed = [&](int k) { return (k + 3) % kG == 0 && k + 3 < nFp; };   // preload of k reads steps k+1..k+3
       bool fok = !fneed(0) || test_full(gof(3));
       auto fiter = [&](int k, double r2, FRows& cur, FRows& nxt) {
@@ -657,24 +676,41 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         const double a1 = dot4(cur.L5, yp, 0.0);                      // (-1,0)
         const double y = active ? a0 + a1 : 0.0;
         Est(k, y);
+        finish_half();                                                // half(k+1) complete
         const double b0 = dot4(cur.N2, Ya1, half);                    // pre(k+1): (0,-1)
         const double b1 = dot4(cur.N4, yp, 0.0);                      //           (-2,0)
-        const double c0 = dot4(cur.M0, aa4, r2);                      // half(k+2): (0,-2)
+        const double c0 = fma(-cur.M0[1], aa4[1], fma(-cur.M0[0], aa4[0], r2));   // half(k+2): (0,-2), first half
         const double c1 = dot4(cur.M1, Ya1, 0.0);                     //            (-1,-1)
         pre = b0 + b1;
         half = c0 + c1;
+        dm2 = cur.M0[2]; dm3 = cur.M0[3]; da2 = aa4[2]; da3 = aa4[3];
         if (!(R2_DBG(A) & 260)) ybuf[(size_t)k * 128] = y;
         st_cluster_if(!(R2_DBG(A) & 4) && dn_push && active, dn_base + (unsigned)(i * 32), y);
         if (k % kG == kG - 2) release_group(gof(k));   // the group's last rows are in registers now
         if (pol) pvn = pload_plain(pqf, k + 1 + pdf);  // the next iteration's cells (checked after its barrier)
         fok = !fneed(k + 1) || test_full(gof(k + 4));
       };
+#if NKS_R2_UNROLL == 8
+      // 8 steps per loop trip (nFp is a multiple of 8 with kG = 2): the exchange-ring slots k mod 8 become
+      // compile-time offsets
+      for (int k0 = 0; k0 < nFp; k0 += 8) {
+        fiter(k0, q0, SA, SB); q0 = load_r(k0 + 6);
+        fiter(k0 + 1, q1, SB, SA); q1 = load_r(k0 + 7);
+        fiter(k0 + 2, q2, SA, SB); q2 = load_r(k0 + 8);
+        fiter(k0 + 3, q3, SB, SA); q3 = load_r(k0 + 9);
+        fiter(k0 + 4, q0, SA, SB); q0 = load_r(k0 + 10);
+        fiter(k0 + 5, q1, SB, SA); q1 = load_r(k0 + 11);
+        fiter(k0 + 6, q2, SA, SB); q2 = load_r(k0 + 12);
+        fiter(k0 + 7, q3, SB, SA); q3 = load_r(k0 + 13);
+      }
+#else
       for (int k0 = 0; k0 < nFp; k0 += 4) {
         fiter(k0, q0, SA, SB); q0 = load_r(k0 + 6);
         fiter(k0 + 1, q1, SB, SA); q1 = load_r(k0 + 7);
         fiter(k0 + 2, q2, SA, SB); q2 = load_r(k0 + 8);
         fiter(k0 + 3, q3, SB, SA); q3 = load_r(k0 + 9);
       }
+#endif
     }
     const long long cf1 = clock64();
     e_bar();                          // every forward read of E is done: clear it for the backward sweep
@@ -756,6 +792,8 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       const unsigned up_base = mapa_u32(hcell(2 + min(rl, 1), 0) + c, (unsigned)max(s - 1, 0));
       const bool pol = dn_remote && !(R2_DBG(A) & 16);
       unsigned long long pvn = 0ull;                 // iteration K's cells were checked in the prologue
+      double dm2 = 0.0, dm3 = 0.0, da2 = 0.0, da3 = 0.0;   // half(k-2)'s deferred terms (see the forward sweep)
+      auto finish_half = [&]() { half = fma(-dm3, da3, fma(-dm2, da2, half)); };
       auto bneed = [&](int k) { const int pp = pofk(k) + 3; return pp % kG == 0 && pp < 2 * nFp; };
       bool fok = !bneed(K) || test_full(gof(pofk(K) + 3));
       auto biter = [&](int k, const double (&y2)[4], BRows& cur, BRows& nxt) {
@@ -776,12 +814,14 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         const double a1 = dot4(cur.U1, xp, 0.0);                      // (1,0)
         const double x = active ? a0 + a1 : 0.0;
         Est(k, x);
+        finish_half();                                                // half(k-1) complete
         const double b0 = dot4(cur.N4, Xb1, half);                    // pre(k-1): (0,1)
         const double b1 = dot4(cur.N2, xp, 0.0);                      //           (2,0)
-        const double c0 = dot4(cur.M6, bb4, ydot(cur.DM, y2));        // half(k-2): (0,2)
+        const double c0 = fma(-cur.M6[1], bb4[1], fma(-cur.M6[0], bb4[0], ydot(cur.DM, y2)));   // half(k-2): (0,2)
         const double c1 = dot4(cur.M5, Xb1, 0.0);                     //            (1,1)
         pre = b0 + b1;
         half = c0 + c1;
+        dm2 = cur.M6[2]; dm3 = cur.M6[3]; da2 = bb4[2]; da3 = bb4[3];
         {
           const int gi = gz0 + k;                  // s0x + i, wraps at most once
           const int gx = gi < 0 ? gi + A.nx : (gi >= A.nx ? gi - A.nx : gi);
@@ -793,6 +833,19 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         if (pol) pvn = pload_plain(pqb, iR - 1 + pdb);  // the next iteration's cells
         fok = !bneed(k - 1) || test_full(gof(pofk(k - 1) + 3));
       };
+#if NKS_R2_UNROLL == 8
+      for (int kb0 = 0; kb0 < nFp; kb0 += 8) {
+        const int k0 = K - kb0;
+        biter(k0, q0, SA, SB); load_y4(k0 - 6, q0);
+        biter(k0 - 1, q1, SB, SA); load_y4(k0 - 7, q1);
+        biter(k0 - 2, q2, SA, SB); load_y4(k0 - 8, q2);
+        biter(k0 - 3, q3, SB, SA); load_y4(k0 - 9, q3);
+        biter(k0 - 4, q0, SA, SB); load_y4(k0 - 10, q0);
+        biter(k0 - 5, q1, SB, SA); load_y4(k0 - 11, q1);
+        biter(k0 - 6, q2, SA, SB); load_y4(k0 - 12, q2);
+        biter(k0 - 7, q3, SB, SA); load_y4(k0 - 13, q3);
+      }
+#else
       for (int kb0 = 0; kb0 < nFp; kb0 += 4) {
         const int k0 = K - kb0;
         biter(k0, q0, SA, SB); load_y4(k0 - 6, q0);
@@ -800,6 +853,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
         biter(k0 - 2, q2, SA, SB); load_y4(k0 - 8, q2);
         biter(k0 - 3, q3, SB, SA); load_y4(k0 - 9, q3);
       }
+#endif
     }
     if (R2_PROF(A) && tid == 0) {
       long long gt1;
