@@ -97,9 +97,8 @@ typedef struct {
   int32_t yghost;    /* 0: no y split.  2..8: this state is one z x y PENCIL of a 3D grid sharded on a  */
                      /* pz x py process grid (SURVEY 8(e), configs 4/5 "slab- then pencil-sharded"): */
                      /* n[1] counts yghost ghost rows on each side as n[2] counts zghost (>= 2) ghost */
-                     /* planes.  Pencil states evaluate F and J.v (the config-5 sharded micro-       */
-                     /* benchmark): nks_set_fields (u given), nks_set_state, nks_get_fields,          */
-                     /* nks_eval_residual, nks_eval_jv; the NKS step itself shards by z-slabs.       */
+                     /* planes.  Pencil states run everything a z-slab runs (pc_type NONE or RAS with */
+                     /* BILU(0) boxes; nks_eval_residual / nks_eval_jv fill their ghosts themselves). */
                      /* nks_decompose_pencil() fills a rank's pencil grid.                           */
   int32_t y_offset;  /* yghost > 0: global y of this pencil's first own row                        */
   int32_t ny_global; /* yghost > 0: rows of the global periodic grid                                 */
@@ -211,11 +210,15 @@ NKS_API nks_status nks_decompose(const nks_grid* global, const nks_params* param
                                  nks_grid* local);
 
 /* The pencil of `rank` on a pz x py process grid (rank = rz * py + ry) for a GLOBAL periodic 3D grid --
- * host only.  rz owns a contiguous run of z planes, ry of y rows (dealt out like nks_decompose without RAS:
- * the first n mod p parts one longer); *local gets own extents + 2 ghost planes / rows per side (the
- * stencils' radius), z_offset / y_offset / nz_global / ny_global / pz / py set, pc_type must be NONE.
- * NKS_E_INVALID if the grid is not 3D or a part would own fewer than 2 planes / rows. */
-NKS_API nks_status nks_decompose_pencil(const nks_grid* global, int32_t rank, int32_t pz, int32_t py, nks_grid* local);
+ * host only.  With pc_type RAS, rz owns a contiguous run of the nsub[2] global box layers along z and ry of
+ * the nsub[1] layers along y (dealt out like nks_decompose), so every rank holds whole boxes and the
+ * iteration counts do not depend on the process grid; ghosts = max(2, overlap + 1) planes / rows per side.
+ * With pc_type NONE the planes and rows themselves are dealt out, 2 ghosts per side.  *local gets the own
+ * extents + ghosts, z_offset / y_offset / nz_global / ny_global / pz / py and its box layers.
+ * NKS_E_INVALID if the grid is not 3D, has fewer box layers than parts along an axis, or a part would own
+ * fewer than 2 planes / rows. */
+NKS_API nks_status nks_decompose_pencil(const nks_grid* global, const nks_params* params, int32_t rank, int32_t pz,
+                                        int32_t py, nks_grid* local);
 
 /* One message of a halo exchange: kind 0 = send, 1 = receive of a contiguous run (`count` doubles at
  * `offset` from the vector's start, field f at f * n[0]*n[1]*n[2]): the ghost PLANES of a slab or a pencil.

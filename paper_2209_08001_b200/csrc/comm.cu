@@ -53,28 +53,50 @@ int slab_decompose(const nks_grid& global, int pc_type, int rank, int nranks, nk
   return 0;
 }
 
-// Pencil of rank r = rz * py + ry on a pz x py process grid (z x y; x stays whole): planes and rows dealt out
-// like the planes of a slab without RAS, 2 ghost planes / rows per side (the stencil radius of F and J.v).
-int pencil_decompose(const nks_grid& global, int rank, int pz, int py, nks_grid& local) {
+// Pencil of rank r = rz * py + ry on a pz x py process grid (z x y; x stays whole).  With RAS every rank owns
+// whole layers of the global box grid along z AND y (nsub[2] layers dealt over pz, nsub[1] over py, as the
+// slab deals its z layers), so the preconditioner -- and the iteration counts -- do not depend on the process
+// grid; ghosts = max(2, overlap + 1) planes / rows per side.  Without RAS the planes and rows themselves are
+// dealt out, 2 ghosts per side (the stencil radius of F and J.v).
+int pencil_decompose(const nks_grid& global, int pc_type, int rank, int pz, int py, nks_grid& local) {
   if (global.dim != 3 || global.zghost != 0 || global.yghost != 0 || pz < 1 || py < 1 || rank < 0 || rank >= pz * py)
     return 1;
   const int rz = rank / py, ry = rank % py;
-  int z0, nzo, y0, nyo;
-  deal(global.n[2], pz, rz, z0, nzo);
-  deal(global.n[1], py, ry, y0, nyo);
-  if (nzo < 2 || nyo < 2) return 1;
+  const bool ras = pc_type != NKS_PC_NONE;
+  int z0, nzo, y0, nyo, nbz = 1, nby = 1;
+  auto layers = [&](int n, int nsub, int parts, int r, int& lo, int& own, int& nb) -> bool {
+    if (nsub < parts) return false;
+    int b0;
+    deal(nsub, parts, r, b0, nb);
+    const int base = n / nsub, rem = n % nsub;
+    auto start = [&](int b) { return b * base + std::min(b, rem); };
+    lo = start(b0);
+    own = start(b0 + nb) - lo;
+    return true;
+  };
+  if (ras) {
+    if (!layers(global.n[2], global.nsub[2], pz, rz, z0, nzo, nbz)) return 1;
+    if (!layers(global.n[1], global.nsub[1], py, ry, y0, nyo, nby)) return 1;
+  } else {
+    deal(global.n[2], pz, rz, z0, nzo);
+    deal(global.n[1], py, ry, y0, nyo);
+  }
+  const int gh = ras ? std::max(2, global.overlap + 1) : 2;
+  if (nzo < 2 || nyo < 2 || gh > 8) return 1;
   local = global;
-  local.n[2] = nzo + 4;
-  local.n[1] = nyo + 4;
-  local.zghost = 2;
-  local.yghost = 2;
+  local.n[2] = nzo + 2 * gh;
+  local.n[1] = nyo + 2 * gh;
+  local.zghost = gh;
+  local.yghost = gh;
   local.z_offset = z0;
   local.nz_global = global.n[2];
   local.y_offset = y0;
   local.ny_global = global.n[1];
   local.pz = pz;
   local.py = py;
-  local.nsub[0] = local.nsub[1] = local.nsub[2] = 1;
+  local.nsub[2] = nbz;
+  local.nsub[1] = nby;
+  if (!ras) local.nsub[0] = local.nsub[1] = local.nsub[2] = 1;
   return 0;
 }
 

@@ -90,7 +90,7 @@ void* nccl_create(const uint8_t id[128], int rank, int nranks, std::string& err)
 void nccl_destroy(void* c);
 int nccl_halo(void* c, double* vec, int nf, long long fstride, int nzl, long long nxy, int zg, cudaStream_t s);
 int nccl_allreduce_fixed(void* c, double* buf, long long n, double* gather, cudaStream_t s);
-int pencil_decompose(const nks_grid& global, int rank, int pz, int py, nks_grid& local);
+int pencil_decompose(const nks_grid& global, int pc_type, int rank, int pz, int py, nks_grid& local);
 void pencil_halo_plan(const nks_grid& g, int rank, int nf, std::vector<nks_halo_msg>& out);
 int nccl_halo_pencil(void* c, const nks_grid& g, double* vec, int nf, double* stage, cudaStream_t s);
 // init_fft.cu
@@ -121,6 +121,7 @@ struct Layout {
   size_t off_fac, off_fac32, off_ybox, off_gidx, off_nbr, off_levoff, off_levptr, off_posoff, off_geo;
   size_t off_cover_off, off_cover_pos;
   size_t off_gather;        // z-slab: [kMaxRanks][256] all-gather area of the fixed-order reductions
+  size_t off_ystage;        // pencil: packed y blocks of one halo exchange (4 per field)
   size_t off_gtab;          // level-k ILU slot tables (off, lower, upper, pair_ptr, pair_b, pair_t)
   size_t off_spec, off_pinv;  // spectral preconditioner: [nf][Nh] complex scratch, [nf*nf][Nh] inverse
   size_t off_tl;              // two-level RAS + spectral: 2 scratch vectors
@@ -157,9 +158,12 @@ const char* validate(const nks_grid* g, const nks_params* p) {
   if (g->yghost != 0) {
     if (g->yghost < 2 || g->yghost > 8) return "yghost must be 0 or 2..8";
     if (g->zghost < 2) return "a pencil (yghost > 0) also carries z ghost planes (zghost >= 2)";
-    if (p->pc_type != NKS_PC_NONE) return "pencil states evaluate F and J.v only (pc_type NONE)";
+    if (p->pc_type != NKS_PC_NONE && p->pc_type != NKS_PC_RAS_BILU0) return "pencil states: pc_type NONE or RAS";
+    if (p->pc_type != NKS_PC_NONE && p->ilu_level != 0) return "pencil states: BILU(0) boxes";
     const int owny = g->n[1] - 2 * g->yghost;
     if (owny < 2) return "a pencil must own at least 2 rows";
+    if (p->pc_type != NKS_PC_NONE && g->overlap + 1 > g->yghost) return "pencil with RAS needs yghost >= overlap + 1";
+    if (p->pc_type != NKS_PC_NONE && (g->nsub[1] < 1 || g->nsub[1] > owny)) return "pencil: nsub[1] must be in 1..own rows";
     if (g->ny_global < 5 || g->y_offset < 0 || g->y_offset + owny > g->ny_global)
       return "pencil: y_offset / ny_global do not place the own rows in the global grid";
     if (g->pz < 1 || g->py < 1) return "pencil: pz, py >= 1";
@@ -209,6 +213,8 @@ Layout make_layout(const nks_grid& g, const nks_params& p, IlukPattern* K = null
   L.off_part = o; o = align256(o + (size_t)kRedBlocks * 80 * sizeof(double));
   L.off_out = o; o = align256(o + 256 * sizeof(double));
   L.off_gather = o; o = align256(o + (g.zghost > 0 ? (size_t)kMaxRanks * 256 * sizeof(double) : 0));
+  L.off_ystage = o;
+  if (g.yghost > 0) o = align256(o + (size_t)4 * nf * g.yghost * g.n[0] * (g.n[2] - 2 * g.zghost) * sizeof(double));
   L.P = 0;
   if (p.pc_type == NKS_PC_SPECTRAL || p.pc_type == NKS_PC_RAS_SPECTRAL) {
     const long long Nh = spectral_half(g);
@@ -383,8 +389,8 @@ void halo(nks_state* st, double* vec, int nf) {
   if (!slab(st) || !st->comm_set) return;
   PhaseScope ps(st, PH_OTHER);   // halo exchanges are accounted under "other"
   if (st->nccl) {
-    if (pencil(st)) {       // y blocks (packed through the idle Krylov basis area), then whole planes
-      if (nccl_halo_pencil(st->nccl, st->grid, vec, nf, st->V, st->stream) != 0) throw CommError();
+    if (pencil(st)) {       // y blocks (packed through the pencil staging area), then whole planes
+      if (nccl_halo_pencil(st->nccl, st->grid, vec, nf, st->ystage, st->stream) != 0) throw CommError();
       return;
     }
     const long long nxy = (long long)st->grid.n[0] * st->grid.n[1];
@@ -1070,6 +1076,7 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, int32_t ra
     st->red_out = (double*)(w + L.off_out);
     st->red_cnt = (unsigned*)(st->red_out + 255);
     st->gather = (double*)(w + L.off_gather);
+    st->ystage = (double*)(w + L.off_ystage);
     if (grid->zghost > 0 && nccl_id) {     // library-owned communicator (collective over the nranks ranks)
       std::string why;
       st->nccl = nccl_create(nccl_id, rank, nranks, why);
@@ -1191,7 +1198,6 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, int32_t ra
 
 nks_status nks_set_fields(nks_state* st, const double* c, const double* eta, const double* u, int32_t on_device) {
   if (!st || !c || !eta) return NKS_E_INVALID;
-  if (pencil(st) && !u) return NKS_E_INVALID;        // pencil states take u (no u^0 solve)
   return guarded(st, [&]() -> nks_status {
     const long long N = st->N;
     CK(cudaMemcpyAsync(st->Xn, c, N * sizeof(double), kind_in(on_device), st->stream));
@@ -1278,10 +1284,13 @@ nks_status nks_get_unique_id(uint8_t id[128]) {
   return nccl_unique_id(id) == 0 ? NKS_OK : NKS_E_NCCL;
 }
 
-nks_status nks_decompose_pencil(const nks_grid* global, int32_t rank, int32_t pz, int32_t py, nks_grid* local) {
-  if (!global || !local || pz < 1 || py < 1 || pz * py > kMaxRanks) return NKS_E_INVALID;
+nks_status nks_decompose_pencil(const nks_grid* global, const nks_params* params, int32_t rank, int32_t pz, int32_t py,
+                                nks_grid* local) {
+  if (!global || !params || !local || pz < 1 || py < 1 || pz * py > kMaxRanks) return NKS_E_INVALID;
+  if (validate(global, params)) return NKS_E_INVALID;
   nks_grid loc{};
-  if (pencil_decompose(*global, rank, pz, py, loc) != 0) return NKS_E_INVALID;
+  if (pencil_decompose(*global, params->pc_type, rank, pz, py, loc) != 0) return NKS_E_INVALID;
+  if (validate(&loc, params)) return NKS_E_INVALID;
   *local = loc;
   return NKS_OK;
 }
@@ -1352,7 +1361,6 @@ nks_status nks_get_fields(const nks_state* cst, double* c, double* eta, double* 
 
 nks_status nks_step(nks_state* st, double dt, nks_step_info* info) {
   if (!st) return NKS_E_INVALID;
-  if (pencil(st)) return NKS_E_INVALID;                   // pencil states: F and J.v only
   if (!st->have_fields) return NKS_E_STATE;
   if (slab(st) && !st->comm_set) return NKS_E_STATE;
   return guarded(st, [&]() { return step_impl(st, dt, info); });
@@ -1360,7 +1368,6 @@ nks_status nks_step(nks_state* st, double dt, nks_step_info* info) {
 
 nks_status nks_run_adaptive(nks_state* st, int32_t max_steps, double t_end, nks_step_info* per_step, int32_t* done) {
   if (!st || max_steps < 0) return NKS_E_INVALID;
-  if (pencil(st)) return NKS_E_INVALID;                   // pencil states: F and J.v only
   if (!st->have_fields) return NKS_E_STATE;
   if (slab(st) && !st->comm_set) return NKS_E_STATE;
   if (done) *done = 0;
@@ -1403,7 +1410,6 @@ nks_status nks_run_adaptive(nks_state* st, int32_t max_steps, double t_end, nks_
 
 nks_status nks_energy(nks_state* st, double parts[4], double* mass) {
   if (!st || !parts || !mass) return NKS_E_INVALID;
-  if (pencil(st)) return NKS_E_INVALID;                   // pencil states: F and J.v only
   if (!st->have_fields) return NKS_E_STATE;
   if (slab(st) && !st->comm_set) return NKS_E_STATE;
   return guarded(st, [&]() -> nks_status {
@@ -1453,7 +1459,6 @@ nks_status nks_eval_jv(nks_state* st, double dt, const double* x_b, const double
 
 nks_status nks_pc_setup(nks_state* st, double dt, const double* x_b, int32_t on_device) {
   if (!st || !x_b || !(dt > 0)) return NKS_E_INVALID;
-  if (pencil(st)) return NKS_E_INVALID;                   // pencil states: F and J.v only
   if (!st->have_fields) return NKS_E_STATE;
   return guarded(st, [&]() -> nks_status {
     set_dt(st, dt);
@@ -1471,7 +1476,6 @@ nks_status nks_pc_setup(nks_state* st, double dt, const double* x_b, int32_t on_
 
 nks_status nks_pc_apply(nks_state* st, const double* r, double* z, int32_t on_device) {
   if (!st || !r || !z) return NKS_E_INVALID;
-  if (pencil(st)) return NKS_E_INVALID;                   // pencil states: F and J.v only
   if (st->prm.pc_type != NKS_PC_NONE && !st->pc_valid) return NKS_E_STATE;
   return guarded(st, [&]() -> nks_status {
     const size_t nb = st->nvec * sizeof(double);
@@ -1486,7 +1490,6 @@ nks_status nks_pc_apply(nks_state* st, const double* r, double* z, int32_t on_de
 nks_status nks_gmres_solve(nks_state* st, double dt, const double* x_b, const double* rhs, double* s, int32_t on_device,
                            int32_t* its) {
   if (!st || !x_b || !rhs || !s || !(dt > 0)) return NKS_E_INVALID;
-  if (pencil(st)) return NKS_E_INVALID;                   // pencil states: F and J.v only
   if (!st->have_fields) return NKS_E_STATE;
   return guarded(st, [&]() -> nks_status {
     set_dt(st, dt);

@@ -171,6 +171,7 @@ struct nks_state {
   bool comm_set = false;
   void* nccl = nullptr;         // library-owned NCCL communicator (comm.cu), or null (callbacks / one state)
   double* gather = nullptr;     // [kMaxRanks][256] all-gather area
+  double* ystage = nullptr;     // pencil: packed y blocks of one halo exchange
   // counters
   long long launches = 0;
   long long syncs = 0;

@@ -78,7 +78,13 @@ static void split_axis(int n, int nsub, std::vector<int>& start, std::vector<int
 // periodic neighbours' values, so no z wrap is needed (RAS needs one width-delta halo
 // of its input, assembly one of width delta+1).
 static void split_boxes(const nks_grid& g, std::vector<int> (&st)[3], std::vector<int> (&ln)[3]) {
-  for (int j = 0; j < 2; ++j) split_axis(g.n[j], g.nsub[j], st[j], ln[j]);
+  split_axis(g.n[0], g.nsub[0], st[0], ln[0]);
+  if (g.yghost > 0) {             // a pencil: the own rows, boxes addressing the ghost rows as their overlap
+    split_axis(g.n[1] - 2 * g.yghost, g.nsub[1], st[1], ln[1]);
+    for (auto& v : st[1]) v += g.yghost;
+  } else {
+    split_axis(g.n[1], g.nsub[1], st[1], ln[1]);
+  }
   if (g.zghost > 0) {
     split_axis(g.n[2] - 2 * g.zghost, g.nsub[2], st[2], ln[2]);
     for (auto& v : st[2]) v += g.zghost;

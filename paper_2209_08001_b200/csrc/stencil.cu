@@ -319,12 +319,29 @@ __global__ void k_zero_ghosts(long long nxy, int nz, int zg, int nf, long long N
   }
 }
 
+// Zero the ghost rows (y) of every plane of nf fields (pencil states).
+__global__ void k_zero_ghost_rows(int nx, int ny, int nz, int yg, int nf, long long N, double* __restrict__ v) {
+  const long long per = 2LL * yg * nx;                 // ghost cells per plane
+  const long long tot = per * nz * nf;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
+    const long long f = t / (per * nz), r = t % (per * nz);
+    const long long z = r / per, q = r % per;
+    const long long row = q / nx, x = q % nx;
+    const long long y = row < yg ? row : (ny - 2 * yg + row);
+    v[f * N + (z * ny + y) * nx + x] = 0.0;
+  }
+}
+
 void launch_zero_ghosts(const DevParams& P, int nf, double* v, cudaStream_t s) {
   if (P.zg <= 0) return;
   const long long nxy = (long long)P.nx * P.ny;
   const long long work = 2LL * P.zg * nxy * nf;
   const int blocks = (int)std::min<long long>((work + 255) / 256, 148 * 8);
   k_zero_ghosts<<<blocks, 256, 0, s>>>(nxy, P.nz, P.zg, nf, P.N, v);
+  if (P.yg > 0) {
+    const long long w2 = 2LL * P.yg * P.nx * P.nz * nf;
+    k_zero_ghost_rows<<<(int)std::min<long long>((w2 + 255) / 256, 148 * 8), 256, 0, s>>>(P.nx, P.ny, P.nz, P.yg, nf, P.N, v);
+  }
 }
 
 }  // namespace nks

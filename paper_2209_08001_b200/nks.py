@@ -79,7 +79,7 @@ _SIGS = {
     "nks_get_unique_id": (C.c_int, [_P]),
     "nks_decompose": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), C.c_int32, C.c_int32, C.POINTER(Grid)]),
     "nks_halo_plan": (C.c_int32, [C.POINTER(Grid), C.c_int32, C.c_int32, C.c_int32, C.POINTER(HaloMsg), C.c_int32]),
-    "nks_decompose_pencil": (C.c_int, [C.POINTER(Grid), C.c_int32, C.c_int32, C.c_int32, C.POINTER(Grid)]),
+    "nks_decompose_pencil": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), C.c_int32, C.c_int32, C.c_int32, C.POINTER(Grid)]),
     "nks_set_fields": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
     "nks_get_fields": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
     "nks_set_state": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
@@ -167,10 +167,12 @@ def halo_plan(local: Grid, rank: int, nranks: int, nfields: int):
     return [(m.kind, m.peer, m.offset, m.count) for m in buf]
 
 
-def decompose_pencil(global_grid: Grid, rank: int, pz: int, py: int) -> Grid:
-    """nks_decompose_pencil: the z x y pencil grid of `rank` = rz * py + ry on a pz x py process grid (host only)."""
+def decompose_pencil(global_grid: Grid, params: Params, rank: int, pz: int, py: int) -> Grid:
+    """nks_decompose_pencil: the z x y pencil grid of `rank` = rz * py + ry on a pz x py process grid (host only);
+    with RAS each rank owns whole box layers along z and y."""
     out = Grid()
-    rc = load_library().nks_decompose_pencil(C.byref(global_grid), int(rank), int(pz), int(py), C.byref(out))
+    rc = load_library().nks_decompose_pencil(C.byref(global_grid), C.byref(params), int(rank), int(pz), int(py),
+                                             C.byref(out))
     if rc != NKS_OK:
         raise NKSError(rc, "nks_decompose_pencil: no valid pencil for this grid / process grid")
     return out

@@ -365,26 +365,30 @@ def run_halo_plan(vec, plan, local, rank: int, group=None):
 
 
 class PencilSolver:
-    """One z x y pencil of a 3D periodic grid per rank on a pz x py process grid (rank = rz * py + ry):
-    the residual F and the Jacobian action J.v of the library on a pencil-sharded grid (BASELINE
-    configs 4/5 "slab- then pencil-sharded"; the NKS step itself shards by z-slabs, ShardedSolver).
+    """One z x y pencil of a 3D periodic grid per rank on a pz x py process grid (rank = rz * py + ry), for the
+    full NKS step and for F / J.v alone ("pencil z x y (2x2, 2x4) for 4 and 8 GPUs"; BASELINE
+    configs 4/5 "slab- then pencil-sharded").
 
-    The library decomposes the grid (nks_decompose_pencil: planes and rows dealt out, 2 ghost planes / rows
-    per side) and fills the ghosts itself inside nks_eval_residual / nks_eval_jv: with comm="nccl" through its
-    own communicator (y blocks packed and exchanged in one NCCL group, then whole planes, so the (y, z) edge
-    cells arrive), with comm="callbacks" through this object's host callback, which runs the library's own
-    message list (nks_halo_plan) over the torch process group (host-staged; emulated ranks on one GPU)."""
+    The library decomposes the grid (nks_decompose_pencil: with RAS every rank owns whole layers of the global
+    box grid along z AND y, so the preconditioner -- and the iteration counts -- do not depend on the process
+    grid) and fills the ghost planes and rows itself: with comm="nccl" through its own communicator (y blocks
+    packed and exchanged in one NCCL group, then whole planes, so the (y, z) edge cells arrive), with
+    comm="callbacks" through this object's host callbacks, which run the library's own message list
+    (nks_halo_plan) over the torch process group (host-staged; emulated ranks on one GPU)."""
 
-    def __init__(self, shape_global, model, solver, pz, py, h=0.25, group=None, device=None, comm="auto"):
+    def __init__(self, shape_global, model, solver, pz, py, h=0.25, nsub=(1, 1, 1), overlap=2, pc_type=None,
+                 pc_reuse=1, group=None, device=None, comm="auto"):
         import torch
-        from .nks import PC_NONE, Solver, decompose_pencil, halo_plan, make_grid, unique_id
+        from .nks import PC_NONE, Solver, decompose_pencil, halo_plan, make_grid, make_params, unique_id
         self.torch = torch
         self.group = group
         self.world, self.rank = _world(group)
         if self.world != pz * py:
             raise ValueError("the process grid pz x py must match the group size")
         self.shape_global = tuple(int(v) for v in shape_global)
-        self.lgrid = decompose_pencil(make_grid(self.shape_global, h), self.rank, pz, py)
+        self.pc_type = PC_NONE if pc_type is None else pc_type
+        params = make_params(model, solver, self.pc_type, pc_reuse)
+        self.lgrid = decompose_pencil(make_grid(self.shape_global, h, nsub, overlap), params, self.rank, pz, py)
         g = self.lgrid
         self.zg, self.yg = int(g.zghost), int(g.yghost)
         self.z0, self.y0 = int(g.z_offset), int(g.y_offset)
@@ -394,6 +398,7 @@ class PencilSolver:
             comm = "nccl" if (self.world == 1 or not _is_gloo(group)) else "callbacks"
         self.comm = comm
         self.halo_calls = 0
+        self.allreduce_calls = 0
         nccl_id = None
         if comm == "nccl":
             nccl_id = unique_id() if self.rank == 0 else None
@@ -403,8 +408,8 @@ class PencilSolver:
                 src = dist.get_global_rank(group, 0) if group is not None else 0
                 dist.broadcast_object_list(box, src=src, group=group)
                 nccl_id = box[0]
-        self.solver = Solver(self.local_shape, model, solver, h=h, pc_type=PC_NONE, device=device, grid=g,
-                             rank=self.rank, nranks=self.world, nccl_id=nccl_id)
+        self.solver = Solver(self.local_shape, model, solver, h=h, pc_type=self.pc_type, pc_reuse=pc_reuse,
+                             device=device, grid=g, rank=self.rank, nranks=self.world, nccl_id=nccl_id)
         self.device = self.solver.device
         self._plan = {}
         self._halo_plan = halo_plan
@@ -412,6 +417,7 @@ class PencilSolver:
             self.solver.set_comm(self._allreduce, self._halo)
 
     def _allreduce(self, ptr, n, stream):
+        self.allreduce_calls += 1
         with self.torch.cuda.stream(self.solver.stream):
             allreduce_fixed_order(self.solver.device_view(ptr, n), self.group)
         return 0
@@ -421,7 +427,6 @@ class PencilSolver:
         if nf not in self._plan:
             self._plan[nf] = self._halo_plan(self.lgrid, self.rank, self.world, nf)
         v = self.solver.device_view(ptr, nf * stride)
-        self.torch.cuda.current_stream(self.device).synchronize()
         self.solver.stream.synchronize()
         host = v.cpu() if (self.world > 1 and _is_gloo(self.group)) else v
         run_halo_plan(host, self._plan[nf], self.lgrid, self.rank, self.group)
@@ -442,25 +447,29 @@ class PencilSolver:
         """The own planes / rows of a local (..., nzl, nyl, nx) field."""
         return local_field[..., self.zg:self.zg + self.nzo, self.yg:self.yg + self.nyo, :]
 
-    def set_fields(self, c, eta, u):
-        """Global c, eta (nz, ny, nx) and u (3, nz, ny, nx); the ghosts are refilled by the library."""
-        self.solver.set_fields(self.local(c), self.local(eta), self.local(u))
+    def set_fields(self, c, eta, u=None):
+        """Global c, eta (nz, ny, nx) and optionally u (3, nz, ny, nx); without u the library solves u^0 by
+        conjugate gradients on the pencils (reading R13).  The ghosts are refilled by the library."""
+        self.solver.set_fields(self.local(c), self.local(eta), None if u is None else self.local(u))
+
+    def step(self, dt, raise_on_fail=True):
+        return self.solver.step(dt, raise_on_fail=raise_on_fail)
+
+    def own_state(self):
+        """(5, nzo, nyo, nx) numpy array of this rank's own points of X^n."""
+        return np.ascontiguousarray(self.own(self.solver.get_state()))
+
+    def _nan_ghosts(self, a):
+        a[:, :self.zg] = np.nan
+        a[:, -self.zg:] = np.nan
+        a[:, :, :self.yg] = np.nan
+        a[:, :, -self.yg:] = np.nan
+        return a
 
     def residual(self, Xb, dt):
         """F on the own points for a global state Xb (5, nz, ny, nx); the local ghosts are sent as NaN and
         refilled by the library's halo exchange."""
-        loc = self.local(Xb)
-        loc[:, :self.zg] = np.nan
-        loc[:, -self.zg:] = np.nan
-        loc[:, :, :self.yg] = np.nan
-        loc[:, :, -self.yg:] = np.nan
-        return self.own(self.solver.eval_residual(loc, dt))
+        return self.own(self.solver.eval_residual(self._nan_ghosts(self.local(Xb)), dt))
 
     def jv(self, Xb, v, dt):
-        loc, lv = self.local(Xb), self.local(v)
-        for a in (loc, lv):
-            a[:, :self.zg] = np.nan
-            a[:, -self.zg:] = np.nan
-            a[:, :, :self.yg] = np.nan
-            a[:, :, -self.yg:] = np.nan
-        return self.own(self.solver.eval_jv(loc, lv, dt))
+        return self.own(self.solver.eval_jv(self._nan_ghosts(self.local(Xb)), self._nan_ghosts(self.local(v)), dt))

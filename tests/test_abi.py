@@ -159,9 +159,10 @@ def test_decompose_pencil_tiles_the_grid(lib, pz, py):
     """nks_decompose_pencil (host only): the pencils of a pz x py process grid tile the global (z, y) range
     exactly once, each with 2 ghost planes / rows per side (the stencils' radius) and its offsets set."""
     g = nks.make_grid((24, 22, 16), 0.25, (1, 1, 1), 2)
+    p0 = nks.make_params(ni.model_default(), ni.solver_default(), nks.PC_NONE)
     seen = {}
     for r in range(pz * py):
-        loc = nks.decompose_pencil(g, r, pz, py)
+        loc = nks.decompose_pencil(g, p0, r, pz, py)
         assert (loc.zghost, loc.yghost, loc.pz, loc.py) == (2, 2, pz, py)
         assert (loc.nz_global, loc.ny_global, loc.n[0]) == (24, 22, 16)
         nzo, nyo = loc.n[2] - 4, loc.n[1] - 4
@@ -172,4 +173,25 @@ def test_decompose_pencil_tiles_the_grid(lib, pz, py):
                 seen[(z, y)] = r
     assert len(seen) == 24 * 22
     with pytest.raises(nks.NKSError):
-        nks.decompose_pencil(g, 12, 13, 1)         # 24 planes over 13 parts: the last part owns one plane
+        nks.decompose_pencil(g, p0, 12, 13, 1)     # 24 planes over 13 parts: the last part owns one plane
+
+
+@pytest.mark.parametrize("pz,py", [(1, 1), (2, 2), (1, 4), (4, 2)])
+def test_decompose_pencil_deals_whole_box_layers(lib, pz, py):
+    """With RAS each pencil owns whole layers of the global box grid along z and y (so the preconditioner and
+    the iteration counts do not depend on the process grid) and overlap + 1 ghosts per side."""
+    nz, ny, nsz, nsy = 24, 20, 4, 8
+    g = nks.make_grid((nz, ny, 12), 0.25, (nsz, nsy, 2), 2)
+    p = nks.make_params(ni.model_default(), ni.solver_default(), nks.PC_RAS_BILU0)
+    zstarts = {b * (nz // nsz) for b in range(nsz + 1)}
+    ystarts = {b * (ny // nsy) + min(b, ny % nsy) for b in range(nsy + 1)}
+    tot_z, tot_y = {}, {}
+    for r in range(pz * py):
+        loc = nks.decompose_pencil(g, p, r, pz, py)
+        assert loc.zghost == loc.yghost == 3
+        nzo, nyo = loc.n[2] - 6, loc.n[1] - 6
+        assert loc.z_offset in zstarts and loc.z_offset + nzo in zstarts
+        assert loc.y_offset in ystarts and loc.y_offset + nyo in ystarts
+        tot_z[r // py] = loc.nsub[2]
+        tot_y[r % py] = loc.nsub[1]
+    assert sum(tot_z.values()) == nsz and sum(tot_y.values()) == nsy

@@ -179,7 +179,9 @@ def _pencil_worker(rank, world, pz, py, port, out):
         from paper_2209_08001_b200 import nks
         from paper_2209_08001_b200.shard import run_halo_plan
         nz, ny, nx, nf = 12, 10, 5, 5
-        lg = nks.decompose_pencil(nks.make_grid((nz, ny, nx), 0.25, (1, 1, 1), 2), rank, pz, py)
+        import nks_inputs as ni
+        p0 = nks.make_params(ni.model_default(), ni.solver_default(), nks.PC_NONE)
+        lg = nks.decompose_pencil(nks.make_grid((nz, ny, nx), 0.25, (1, 1, 1), 2), p0, rank, pz, py)
         zg, yg, nzl, nyl = lg.zghost, lg.yghost, lg.n[2], lg.n[1]
         g = np.random.default_rng(11).standard_normal((nf, nz, ny, nx))
         zi = [(z % nz) for z in range(lg.z_offset - zg, lg.z_offset - zg + nzl)]
