@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="3D sharded runs: strong (a fixed grid split over N ranks) or weak (128^3 per rank)")
+    ap.add_argument("--decomp", default="slab", choices=["slab", "pencil"],
+                    help="sharded 3D runs: z-slabs (default) or z x y pencils on the most square pz x py grid")
     ap.add_argument("--sharded", action="store_true",
                     help="3D configs: run the z-slab sharded NKS step (ShardedSolver, NCCL halos/allreduces); "
                          "implied for 3D configs at N > 1")
@@ -241,7 +243,7 @@ def bench_solver(cfg):
     return sol
 
 
-def config_dict(cfg, ngpus, sharded=False):
+def config_dict(cfg, ngpus, sharded=False, decomp="slab"):
     d = len(cfg["shape"])
     return {"workload": f"config {2 if cfg['name'] == '2d_512' else cfg['name']}: {cfg['name']} "
                         f"{'x'.join(map(str, cfg['shape']))} periodic, adaptive dt (P:596-607), "
@@ -249,7 +251,9 @@ def config_dict(cfg, ngpus, sharded=False):
             "grid": list(cfg["shape"]), "dof": (2 + d) * int(np.prod(cfg["shape"])),
             "nsub": list(cfg["nsub"]), "overlap": cfg["overlap"], "newton_rtol": 1e-11, "gmres_rtol": 1e-10,
             "init": "c=0.1622+U(-0.005,0.005), eta=0.1+U(-0.01,0.01), seed 0, u0=FFT equilibrium",
-            "parallelism": (f"z-slabs x {ngpus} (sharded NKS step, NCCL halo exchange + allreduce)" if sharded
+            "parallelism": ((f"z x y pencils {'x'.join(map(str, pencil_grid(ngpus)))} (sharded NKS step, NCCL halo "
+                             f"exchange + allreduce)" if decomp == "pencil" else
+                             f"z-slabs x {ngpus} (sharded NKS step, NCCL halo exchange + allreduce)") if sharded
                             else ("replicas" if ngpus > 1 else "1 GPU")),
             "l2": l2_note(cfg)}
 
@@ -452,13 +456,28 @@ def run_variant(args, cfg, model, sol, c, eta, pg, pc_type):
     return out
 
 
-def run_sharded_point(args, cfg, model, sol, pg, steps, warmup):
-    """Config 3 through the z-slab sharded path (ShardedSolver: library decomposition, library-owned NCCL
-    communicator) with the ranks of pg (one rank here): W + K adaptive steps, max-over-ranks time."""
+def pencil_grid(world):
+    """The most square pz x py factorisation of the rank count (pz <= py)."""
+    pz = max(p for p in range(1, int(world ** 0.5) + 1) if world % p == 0)
+    return pz, world // pz
+
+
+def run_sharded_point(args, cfg, model, sol, pg, steps, warmup, decomp="slab"):
+    """Config 3 through the sharded path (library decomposition into z-slabs -- ShardedSolver -- or z x y
+    pencils -- PencilSolver --, library-owned NCCL communicator) with the ranks of pg (one rank here): W + K
+    adaptive steps, max-over-ranks time."""
     import torch
-    from paper_2209_08001_b200.shard import ShardedSolver
+    from paper_2209_08001_b200 import PC_RAS_BILU0
+    from paper_2209_08001_b200.shard import PencilSolver, ShardedSolver
     c, eta = ni.initial_fields(cfg["shape"], 0)
-    sh = ShardedSolver(cfg["shape"], model, sol, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"], pc_reuse=1)
+    if decomp == "pencil":
+        import torch.distributed as dist
+        pz, py = pencil_grid(dist.get_world_size() if dist.is_initialized() else 1)
+        sh = PencilSolver(cfg["shape"], model, sol, pz, py, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"],
+                          pc_type=PC_RAS_BILU0, pc_reuse=1, comm="nccl")
+        sh.run_adaptive = sh.solver.run_adaptive
+    else:
+        sh = ShardedSolver(cfg["shape"], model, sol, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"], pc_reuse=1)
     sh.set_fields(c, eta)
     for _ in range(warmup):
         sh.run_adaptive(1)
@@ -508,9 +527,15 @@ def run_gpu(args, world, rank, local, pg):
     sharded = d == 3 and (world > 1 or args.sharded)
     c, eta = ni.initial_fields(shape, 0)
     if sharded:
-        # one z-slab per rank; the library calls back for halo exchanges and fixed-order allreduces
-        from paper_2209_08001_b200.shard import ShardedSolver
-        sh = ShardedSolver(shape, model, sol, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"], pc_reuse=1)
+        # one z-slab (or z x y pencil, --decomp pencil) per rank; the library exchanges halos and reduces
+        from paper_2209_08001_b200 import PC_RAS_BILU0
+        from paper_2209_08001_b200.shard import PencilSolver, ShardedSolver
+        if args.decomp == "pencil":
+            pz, py = pencil_grid(world)
+            sh = PencilSolver(shape, model, sol, pz, py, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"],
+                              pc_type=PC_RAS_BILU0, pc_reuse=1)
+        else:
+            sh = ShardedSolver(shape, model, sol, h=cfg["h"], nsub=cfg["nsub"], overlap=cfg["overlap"], pc_reuse=1)
         sh.set_fields(c, eta)
         g = sh.solver
     else:
@@ -624,6 +649,11 @@ def run_gpu(args, world, rank, local, pg):
         g = None
         try:
             extra["config3_sharded_1rank"] = run_sharded_point(args, ni.CONFIGS[3], model, sol, pg, steps=2, warmup=1)
+            try:       # the pencil-sharded step at one rank (NCCL self-exchange along z and y), one step
+                extra["config3_pencil_1rank"] = run_sharded_point(args, ni.CONFIGS[3], model, sol, pg, steps=1,
+                                                                  warmup=0, decomp="pencil")
+            except Exception as e:
+                extra["config3_pencil_1rank"] = {"error": str(e)[:300]}
         except Exception as e:
             extra["config3_sharded_1rank"] = {"error": str(e)[:300]}
         torch.cuda.empty_cache()
@@ -754,7 +784,7 @@ def run_gpu(args, world, rank, local, pg):
     roof["traffic"] = traffic
 
     if rank == 0:
-        conf = config_dict(cfg, world, sharded)
+        conf = config_dict(cfg, world, sharded, args.decomp)
         conf["gmres_stall_cycles"] = sol["gmres_stall_cycles"]
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
