@@ -250,7 +250,8 @@ def config_dict(cfg, ngpus, sharded=False, decomp="slab"):
                         f"RAS {'x'.join(map(str, cfg['nsub']))} boxes delta={cfg['overlap']} BILU(0), GMRES(30)",
             "grid": list(cfg["shape"]), "dof": (2 + d) * int(np.prod(cfg["shape"])),
             "nsub": list(cfg["nsub"]), "overlap": cfg["overlap"], "newton_rtol": 1e-11, "gmres_rtol": 1e-10,
-            "init": "c=0.1622+U(-0.005,0.005), eta=0.1+U(-0.01,0.01), seed 0, u0=FFT equilibrium",
+            "init": "c=0.1622+U(-0.005,0.005), eta=0.1+U(-0.01,0.01), seed 0, " +
+                    ("u0 = conjugate gradients on the elastic block (sharded)" if sharded else "u0=FFT equilibrium"),
             "parallelism": ((f"z x y pencils {'x'.join(map(str, pencil_grid(ngpus)))} (sharded NKS step, NCCL halo "
                              f"exchange + allreduce)" if decomp == "pencil" else
                              f"z-slabs x {ngpus} (sharded NKS step, NCCL halo exchange + allreduce)") if sharded
