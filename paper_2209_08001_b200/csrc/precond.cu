@@ -486,8 +486,22 @@ __global__ void k_bilu0(SlotTables T, const int* __restrict__ nbr, const int* __
 // NL = number of lower (= upper) slots: 6 in 2D, 12 in 3D; the slot loops are unrolled so that every
 // neighbour index and neighbour vector of a point is requested before the first one is used (two
 // dependent memory latencies per wavefront level instead of 2*NL).
+// NKS_RAS3D_SPLIT: the NL neighbour blocks of a point are taken in chunks of NL / SPLIT (fewer live
+// registers: 3D with one chunk holds 12 x 5 neighbour values and needs 168 registers, so only 3 CTAs of
+// 128 threads fit an SM and config 3's 512 boxes run in two rounds)
+#ifndef NKS_RAS3D_SPLIT
+#define NKS_RAS3D_SPLIT 1
+#endif
+#ifndef NKS_RAS3D_LB
+#define NKS_RAS3D_LB 0       // > 0: __launch_bounds__(256, LB) (2 caps the registers at 128)
+#endif
+#if NKS_RAS3D_LB > 0
+#define NKS_RAS3D_BOUNDS __launch_bounds__(256, NKS_RAS3D_LB)
+#else
+#define NKS_RAS3D_BOUNDS
+#endif
 template <int NF, int NL, typename FT>
-__global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const int* __restrict__ nbr,
+__global__ void NKS_RAS3D_BOUNDS k_ras_apply(SlotTables T, const int* __restrict__ gidx, const int* __restrict__ nbr,
                             const int* __restrict__ box_lev_off, const int* __restrict__ lev_ptr,
                             const int* __restrict__ box_pos_off, long long Ptot, long long ld, long long N,
                             const FT* __restrict__ fac, const double* __restrict__ r, double* y,
@@ -508,25 +522,29 @@ __global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const in
   for (int l = l0; l < l1; ++l) {
     const int p0 = lev_ptr[l], p1 = lev_ptr[l + 1];
     for (int pos = p0 + threadIdx.x; pos < p1; pos += blockDim.x) {
-      int kk[NL];
-#pragma unroll
-      for (int a = 0; a < NL; ++a) kk[a] = __ldg(nbr + (long long)T.lower[a] * Ptot + pos);
-      double yk[NL][NF];
-#pragma unroll
-      for (int a = 0; a < NL; ++a)
-#pragma unroll
-        for (int f = 0; f < NF; ++f) yk[a][f] = kk[a] >= 0 ? y[f * Ptot + kk[a]] : 0.0;
+      constexpr int CH = NL / NKS_RAS3D_SPLIT;
       double acc[NF];
 #pragma unroll
       for (int f = 0; f < NF; ++f) acc[f] = y[f * Ptot + pos];
 #pragma unroll
-      for (int a = 0; a < NL; ++a) {
-        const FT* L = fac + (long long)(T.lower[a] * NF * NF) * ld + pos;
+      for (int h = 0; h < NKS_RAS3D_SPLIT; ++h) {
+        int kk[CH];
 #pragma unroll
-        for (int rr = 0; rr < NF; ++rr)
+        for (int a = 0; a < CH; ++a) kk[a] = __ldg(nbr + (long long)T.lower[h * CH + a] * Ptot + pos);
+        double yk[CH][NF];
 #pragma unroll
-          for (int c = 0; c < NF; ++c)
-            acc[rr] = fma(-(double)__ldg(L + (long long)(rr * NF + c) * ld), yk[a][c], acc[rr]);
+        for (int a = 0; a < CH; ++a)
+#pragma unroll
+          for (int f = 0; f < NF; ++f) yk[a][f] = kk[a] >= 0 ? y[f * Ptot + kk[a]] : 0.0;
+#pragma unroll
+        for (int a = 0; a < CH; ++a) {
+          const FT* L = fac + (long long)(T.lower[h * CH + a] * NF * NF) * ld + pos;
+#pragma unroll
+          for (int rr = 0; rr < NF; ++rr)
+#pragma unroll
+            for (int c = 0; c < NF; ++c)
+              acc[rr] = fma(-(double)__ldg(L + (long long)(rr * NF + c) * ld), yk[a][c], acc[rr]);
+        }
       }
 #pragma unroll
       for (int f = 0; f < NF; ++f) y[f * Ptot + pos] = acc[f];
@@ -537,25 +555,29 @@ __global__ void k_ras_apply(SlotTables T, const int* __restrict__ gidx, const in
   for (int l = l1 - 1; l >= l0; --l) {
     const int p0 = lev_ptr[l], p1 = lev_ptr[l + 1];
     for (int pos = p0 + threadIdx.x; pos < p1; pos += blockDim.x) {
-      int kk[NL];
-#pragma unroll
-      for (int a = 0; a < NL; ++a) kk[a] = __ldg(nbr + (long long)T.upper[a] * Ptot + pos);
-      double xk[NL][NF];
-#pragma unroll
-      for (int a = 0; a < NL; ++a)
-#pragma unroll
-        for (int f = 0; f < NF; ++f) xk[a][f] = kk[a] >= 0 ? y[f * Ptot + kk[a]] : 0.0;
+      constexpr int CH = NL / NKS_RAS3D_SPLIT;
       double acc[NF];
 #pragma unroll
       for (int f = 0; f < NF; ++f) acc[f] = y[f * Ptot + pos];
 #pragma unroll
-      for (int a = 0; a < NL; ++a) {
-        const FT* U = fac + (long long)(T.upper[a] * NF * NF) * ld + pos;
+      for (int h = 0; h < NKS_RAS3D_SPLIT; ++h) {
+        int kk[CH];
 #pragma unroll
-        for (int rr = 0; rr < NF; ++rr)
+        for (int a = 0; a < CH; ++a) kk[a] = __ldg(nbr + (long long)T.upper[h * CH + a] * Ptot + pos);
+        double xk[CH][NF];
 #pragma unroll
-          for (int c = 0; c < NF; ++c)
-            acc[rr] = fma(-(double)__ldg(U + (long long)(rr * NF + c) * ld), xk[a][c], acc[rr]);
+        for (int a = 0; a < CH; ++a)
+#pragma unroll
+          for (int f = 0; f < NF; ++f) xk[a][f] = kk[a] >= 0 ? y[f * Ptot + kk[a]] : 0.0;
+#pragma unroll
+        for (int a = 0; a < CH; ++a) {
+          const FT* U = fac + (long long)(T.upper[h * CH + a] * NF * NF) * ld + pos;
+#pragma unroll
+          for (int rr = 0; rr < NF; ++rr)
+#pragma unroll
+            for (int c = 0; c < NF; ++c)
+              acc[rr] = fma(-(double)__ldg(U + (long long)(rr * NF + c) * ld), xk[a][c], acc[rr]);
+        }
       }
       const FT* D = fac + (long long)(T.diag * NF * NF) * ld + pos;
       double xo[NF];
