@@ -629,6 +629,16 @@ def run_gpu(args, world, rank, local, pg):
         nsteps = 2 * (ex + 2 * (ey - 1))
         roof["critical_path_steps"] = nsteps
         roof["ns_per_wavefront_step"] = per_launch_ms[dom] * 1e6 / nsteps
+        # minimum latency of one wavefront step: step barrier 22.6 + exchange LDS 29.1 + 4 dependent DFMA
+        # x 8.3 + DADD 8.3 + exchange store ~20 cycles (probes: profiles/r01_bar_probe2.txt,
+        # profiles/r01_fp64_peak_probe.txt); the apply cannot beat nsteps x that at the measured SM clock
+        min_cyc = 22.6 + 29.1 + 4 * 8.3 + 8.3 + 20.0
+        sm_mhz = clocks.get("sm_mhz") or 1965.0
+        lat_ms = nsteps * min_cyc / (sm_mhz * 1e3)
+        roof["latency_roofline"] = {"min_step_cycles": min_cyc, "sm_mhz": sm_mhz, "bound_ms": lat_ms,
+                                    "frac": lat_ms / per_launch_ms[dom],
+                                    "note": "critical-path steps x minimum step latency (barrier, exchange load, "
+                                            "4-deep DFMA chain, add, exchange store)"}
 
     # ---- the same workload with the B200-native spectral preconditioner (not the configured one-level RAS;
     # DESIGN.md section 9): its own adaptive trajectory from the same seeded state, W + K steps

@@ -1,6 +1,6 @@
 # round-2 session-3 final measurements: GPU tests, smoke, bench, ncu launch list + RAS apply capture, config-3 phases
 cd $GRAFT_REPO_ROOT
-TAG=${1:-r2f3}
+TAG=${1:-r2f4}
 timeout 1700 python -m pytest tests -m gpu -q -rf > gpurun_out/${TAG}_pytest_gpu.log 2>&1
 echo "pytest rc $?" >> gpurun_out/${TAG}_pytest_gpu.log
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
