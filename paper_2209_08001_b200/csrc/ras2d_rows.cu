@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     // reuses the buffer of group q - kNSW once all four consumer warps have released it
     for (int q = 0; q < 2 * nGr; ++q) {
       if ((R2_DBG(A) & 128) && q >= kNSW) break;   // ablation: no copy management after the first groups
-      const int st = q % kNSW, use = q / kNSW;
+      const int use = q / kNSW;
 #if NKS_R2_NBREL
       // Named barrier 4 + (q - NS) % NS completes when the four consumer warps have arrived for group
       // q - NS (bar.arrive: prior shared reads performed) and this warp syncs: the warp sleeps in the
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       }
       (void)wait_bar;
 #else
-      if (use > 0) wait_bar(empty0 + st * 8, (unsigned)((use - 1) & 1));
+      if (use > 0) wait_bar(empty0 + (q % kNSW) * 8, (unsigned)((use - 1) & 1));
 #endif
       if (NKS_R2_LDGSTS || lane == 0) issue_one(q);
       __syncwarp();
