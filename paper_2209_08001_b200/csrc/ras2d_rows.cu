@@ -565,13 +565,21 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     // E holds components (0,1) and (2,3) in two planes [8][32][2] 512 doubles apart, so a lane's two
     // 16-byte loads of a neighbour's 4-vector hit consecutive 16-byte slots (4 wavefronts per warp
     // load instead of 8 with the interleaved [8][32][4] layout); halo cells keep 4 contiguous doubles
-    auto Erow = [&](int k, int row) -> const double* { return E + ((k & 7) * 32 + row) * 2; };
-    constexpr int kEP = 512;          // plane offset of components (2,3)
+    // exchange ring depth: step k's values are written in iteration k and read in iterations k+1, k+2
+    // (backward: k-1, k-2), and every warp passes the step barrier of k+1 only after all wrote step k, so
+    // 4 slots suffice; with the 4-step unroll the slot of every unrolled iteration is then a compile-time
+    // constant (one add from a per-lane base instead of the ring arithmetic)
+#ifndef NKS_R2_ESLOTS
+#define NKS_R2_ESLOTS 4
+#endif
+    constexpr int kES = NKS_R2_ESLOTS;
+    auto Erow = [&](int k, int row) -> const double* { return E + ((k & (kES - 1)) * 32 + row) * 2; };
+    constexpr int kEP = kES * 64;     // plane offset of components (2,3)
     auto ld4s = [&](const double* p, int off2, double (&v)[4]) {
       const double2 a = *reinterpret_cast<const double2*>(p), b = *reinterpret_cast<const double2*>(p + off2);
       v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
     };
-    auto Est = [&](int k, double val) { E[(c >> 1) * kEP + ((k & 7) * 32 + rl) * 2 + (c & 1)] = val; };
+    auto Est = [&](int k, double val) { E[(c >> 1) * kEP + ((k & (kES - 1)) * 32 + rl) * 2 + (c & 1)] = val; };
     // the same loads on 32-bit shared addresses: per-lane ring bases, one select between the ring and the
     // halo cell for the boundary lanes (no divergent branch)
     const unsigned sE = smem_u32(E), sH = smem_u32(H);
@@ -590,7 +598,7 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
       asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[2]), "=d"(v[3]) : "r"(a + off2) : "memory");
 #endif
     };
-    auto ering = [&](int k, int row) { return sE + (unsigned)(((k & 7) * 32 + row) * 16); };
+    auto ering = [&](int k, int row) { return sE + (unsigned)(((k & (kES - 1)) * 32 + row) * 16); };
     auto hcella = [&](int q, int i) { return sH + (unsigned)(q * pitch * 8 + (min(max(i, -2), ex + 1) + 2) * 32); };
     constexpr unsigned kEPB = kEP * 8;    // plane offset in bytes
     long long t_bar = 0, t_stage = 0, t_poll = 0;
