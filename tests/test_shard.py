@@ -208,3 +208,26 @@ def test_library_pencil_halo_plan_over_gloo(pz, py):
     out = mp.Manager().dict()
     mp.spawn(_pencil_worker, args=(world, pz, py, _free_port(), out), nprocs=world, join=True)
     assert all(out[r] == 0.0 for r in range(world)), dict(out)
+
+
+def test_pencil_plan_single_rank_is_the_periodic_copy():
+    """One rank (pz = py = 1, no process group): every message of the library's pencil plan goes to this rank
+    itself and the executor pairs them locally -- the ghosts become the periodic images (RAS ghost width 3)."""
+    import nks_inputs as ni
+    from paper_2209_08001_b200 import nks
+    from paper_2209_08001_b200.shard import run_halo_plan
+    nz, ny, nx, nf = 12, 10, 6, 5
+    p = nks.make_params(ni.model_default(), ni.solver_default(), nks.PC_RAS_BILU0)
+    lg = nks.decompose_pencil(nks.make_grid((nz, ny, nx), 0.25, (2, 2, 1), 2), p, 0, 1, 1)
+    assert lg.zghost == lg.yghost == 3
+    zg, yg, nzl, nyl = lg.zghost, lg.yghost, lg.n[2], lg.n[1]
+    g = np.random.default_rng(5).standard_normal((nf, nz, ny, nx))
+    want = g[:, [(z - zg) % nz for z in range(nzl)]][:, :, [(y - yg) % ny for y in range(nyl)]]
+    arr = want.copy()
+    arr[:, :zg] = np.nan
+    arr[:, -zg:] = np.nan
+    arr[:, :, :yg] = np.nan
+    arr[:, :, -yg:] = np.nan
+    vec = torch.from_numpy(arr).reshape(-1)
+    run_halo_plan(vec, nks.halo_plan(lg, 0, 1, nf), lg, 0)
+    assert np.array_equal(vec.view(nf, nzl, nyl, nx).numpy(), want)
