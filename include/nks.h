@@ -169,6 +169,11 @@ typedef struct {
                                      /* FFT solve on periodic whole-grid states, conjugate gradients */
                                      /* on the elastic block otherwise (z-slabs: no whole-grid FFT;  */
                                      /* Neumann); 1 = conjugate gradients always.                    */
+  int32_t ras_cta_per_box;           /* level-synchronous RAS apply (3D; 2D boxes the pipelined apply */
+                                     /* does not take): 0 = auto (a cluster of 2 CTAs per box when   */
+                                     /* the boxes fill at most half the SMs), 1 = one CTA per box,   */
+                                     /* 2 or 4 = a cluster of that many CTAs per box.  Same results  */
+                                     /* bit for bit; only the work split over SMs changes.          */
 } nks_params;
 
 typedef struct {

@@ -187,6 +187,8 @@ const char* validate(const nks_grid* g, const nks_params* p) {
   }
   if (!(p->kappa > 0) || !(p->theta >= 0)) return "kappa must be > 0, theta >= 0";
   if (p->ilu_level < -1 || p->ilu_level > 8) return "ilu_level must be -1 (exact LU) or 0..8";
+  if (p->ras_cta_per_box != 0 && p->ras_cta_per_box != 1 && p->ras_cta_per_box != 2 && p->ras_cta_per_box != 4)
+    return "ras_cta_per_box must be 0 (auto), 1, 2 or 4";
   if (p->ilu_level != 0 && p->factor_fp32) return "factor_fp32 is available for ILU(0) only";
   if (p->pc_type == NKS_PC_RAS_SPECTRAL && p->ilu_level != 0) return "the two-level preconditioner uses BILU(0) boxes";
   return nullptr;
@@ -1150,6 +1152,7 @@ nks_status nks_create(const nks_grid* grid, const nks_params* params, int32_t ra
       CK(cudaMemcpyAsync(B.box_pos_off, H.box_pos_off.data(), H.box_pos_off.size() * sizeof(int), cudaMemcpyHostToDevice,
                          st->stream));
       B.variant = params->pc_type == NKS_PC_AS_BILU0 ? 1 : (params->pc_type == NKS_PC_RRAS_BILU0 ? 2 : 0);
+      B.cta_per_box = params->ras_cta_per_box;
       std::vector<int> cov_off, cov_pos;
       if (B.variant != 0) {        // CSR of the box positions covering every grid point, increasing position
         const long long Np = st->N;

@@ -61,6 +61,7 @@ struct BoxSet {
   int* cover_off = nullptr;     // AS / RRAS: [N+1] CSR of the box positions covering each grid point
   int* cover_pos = nullptr;     // [P] positions, increasing (fixed summation order)
   int variant = 0;              // 0 RAS, 1 AS, 2 RRAS
+  int cta_per_box = 0;          // level-synchronous apply: 0 auto, 1, 2, 4 (nks_params.ras_cta_per_box)
   // host copies
   std::vector<int> h_box_lev_off, h_box_pos_off;
   // slot tables (host, copied into kernel params)

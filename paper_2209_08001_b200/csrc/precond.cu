@@ -764,6 +764,7 @@ void launch_fac_to_fp32(const BoxSet& B, int nf, const double* fac, float* fac32
 #define NKS_RAS3D_CSMAX 4
 #endif
 static int ras_cluster_of(const BoxSet& B, int threads) {
+  if (B.cta_per_box > 0) return B.cta_per_box;      // nks_params.ras_cta_per_box (forced)
   int sms = 148;
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

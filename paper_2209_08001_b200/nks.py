@@ -44,6 +44,7 @@ class Params(C.Structure):
         ("zeta", C.c_double), ("dt_min", C.c_double), ("dt_max", C.c_double), ("dt_init", C.c_double),
         ("dt_floor_factor", C.c_double), ("xd_norm", C.c_int32), ("factor_fp32", C.c_int32),
         ("gmres_stall_cycles", C.c_int32), ("ilu_level", C.c_int32), ("u0_cg", C.c_int32),
+        ("ras_cta_per_box", C.c_int32),
     ]
 
 
@@ -206,6 +207,7 @@ def make_params(model: dict, solver: dict, pc_type=PC_RAS_BILU0, pc_reuse=1) -> 
     p.gmres_stall_cycles = int(solver.get("gmres_stall_cycles", 0))
     p.ilu_level = int(solver.get("ilu_level", 0))
     p.u0_cg = int(solver.get("u0_cg", 0))
+    p.ras_cta_per_box = int(solver.get("ras_cta_per_box", 0))
     return p
 
 

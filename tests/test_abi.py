@@ -63,7 +63,7 @@ int main(void) {
   F(nks_grid, pz) F(nks_grid, py)
   F(nks_params, S) F(nks_params, newton_rtol) F(nks_params, pc_reuse) F(nks_params, ls_alpha)
   F(nks_params, zeta) F(nks_params, xd_norm) F(nks_params, factor_fp32) F(nks_params, gmres_stall_cycles)
-  F(nks_params, ilu_level) F(nks_params, u0_cg)
+  F(nks_params, ilu_level) F(nks_params, u0_cg) F(nks_params, ras_cta_per_box)
   F(nks_step_info, dt) F(nks_step_info, energy_parts) F(nks_step_info, mass) F(nks_step_info, xd)
   return 0;
 }

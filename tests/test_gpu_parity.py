@@ -142,6 +142,32 @@ def test_ras_bilu0_apply_parity(shape, nsub, delta):
     assert max(errs) < 1e-10, errs
 
 
+@pytest.mark.parametrize("variant", ["ras", "as"])
+def test_ras3d_cluster_apply_parity(variant):
+    """The 3D level-synchronous apply split over a cluster of 2 or 4 CTAs per box (precond.cu k_ras_apply_cl;
+    nks_params.ras_cta_per_box forces it, auto picks it only for a strong-scaled rank's few boxes): against the
+    oracle, and bit for bit equal to one CTA per box (same per-point summation order)."""
+    from paper_2209_08001_b200 import PC_AS_BILU0, PC_RAS_BILU0
+    shape, nsub, delta = (8, 10, 12), (1, 2, 2), 2
+    nf = 5
+    Xa, Xb = states(shape)
+    dt = 0.3
+    r = ni.random_direction(nf, shape, 13)
+    pc_type = PC_RAS_BILU0 if variant == "ras" else PC_AS_BILU0
+    out = {}
+    for cta in (1, 2, 4):
+        g = gpu_solver(shape, nsub=nsub, overlap=delta, pc_type=pc_type, sol={"ras_cta_per_box": cta})
+        g.set_fields(Xa[0], Xa[1], Xa[2:])
+        g.pc_setup(Xb, dt)
+        out[cta] = g.pc_apply(r).cpu().numpy()
+    J = jacobian.assemble(oracle_model(3), Xa, Xb, dt)
+    zo = pc.RAS(J, shape, nf, tuple(reversed(nsub)), delta, variant=variant).apply(r)
+    for cta in (1, 2, 4):
+        assert max(field_rel_err(out[cta], zo)) < 1e-10, cta
+    np.testing.assert_array_equal(out[2], out[1])
+    np.testing.assert_array_equal(out[4], out[1])
+
+
 @pytest.mark.parametrize("shape,nsub,delta", [((96, 80), (3, 2), 2), ((70, 130), (1, 2), 1), ((256, 40), (2, 1), 2)])
 def test_ras2d_apply_parity(shape, nsub, delta):
     """The 2D RAS apply (ras2d_rows.cu: one lane per row, four component warps, a cluster of stripes per
