@@ -337,14 +337,12 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
   // [klo(q), klo(q) + kG); one extra dummy group lets the consumer look one group past the end
   auto klo = [&](int q) { return q < nGr ? q * kG : nFp - kG * (q - nGr + 1); };
 
-  // Step barrier: the 4 consumer warps meet once per step (barrier 1, 128 threads); the producer is
-  // not on it (round 2: taking it off cut the step from ~840 to ... cycles).  Old comment kept for the
-  // history of the gatekeeper design:
-  // threads).  Before arriving for step p the producer has made the factor groups the consumers will
-  // read during step p resident (mbarrier waits) and has seen the halo cells they will read written
-  // (sentinel polls), so the consumers themselves never wait on an mbarrier or poll: their loop is
-  // the exchange barrier, a few shared loads and the DFMA chains.  Barrier 3 (128) orders the E reset
-  // between the sweeps.
+  // Step barrier: the 4 consumer warps meet once per step (named barrier 1, 128 threads).  The producer
+  // is not on it: each consumer warp waits on a group's full mbarrier itself (probed one step early) and
+  // polls the neighbour's halo cells itself (one step ahead), and releases ring buffers with bar.arrive on
+  // barrier 4 + g mod NS, on which the producer sleeps.  (Until round 2 the producer was a gatekeeper on
+  // every step barrier -- it checked copies and halo cells before arriving -- and arrived last: the step
+  // took ~840 cycles, now ~690.)  Barrier 3 (128) orders the E reset between sweeps.
   auto gof = [&](int p) { return p / kG; };   // group of processing step p (forward k = p, backward k = 2 nFp - 1 - p)
 
   if (w == NCW) {
@@ -482,8 +480,9 @@ __global__ void __launch_bounds__(160, 1) k_apply(Args A) {
     };
     // Halo polls, one step ahead: lanes 0-3 / 4-7 / 8-31 watch component lane & 3 of the three halo
     // cells the NEXT iteration reads (forward: (1,k+1) (0,k+2) (1,k); backward: (2,iR-1) (2,iR)
-    // (3,iR-2)).  The volatile load is issued early in an iteration and checked at its end, so its
-    // latency is off the step chain; the stripe pipeline settles one step further behind its neighbour.
+    // (3,iR-2)).  A plain load at the end of an iteration, checked by one vote after the next step
+    // barrier (slow path: volatile re-reads), so its latency is off the step chain; the stripe pipeline
+    // settles one step further behind its neighbour.
     const int pwhich = min(lane >> 2, 2);
     const int pqf = pwhich == 1 ? 0 : 1, pdf = pwhich == 0 ? 1 : (pwhich == 1 ? 2 : 0);
     const int pqb = pwhich == 2 ? 3 : 2, pdb = pwhich == 0 ? -1 : (pwhich == 1 ? 0 : -2);
