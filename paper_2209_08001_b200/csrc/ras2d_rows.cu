@@ -7,8 +7,9 @@
 // above] and (i,j-2).  Lane rl owns box row j = r0 + rl and processes point i = k - 2 rl at step k,
 // so every step of the CTA is one wavefront t = 2 r0 + k.  Warp c computes output component c of
 // every row (a quarter of the arithmetic per step: 24 DFMA and 12 16-byte loads of its block rows);
-// the four warps exchange each step's 4-vectors through a shared ring E (two planes [8][32][2]) with one named
-// barrier per step (two in the backward sweep, whose inverted diagonal block mixes components).
+// the four warps exchange each step's 4-vectors through a shared ring E (two planes [4][32][2]) with one named
+// barrier per step (the inverted diagonal block is folded into the upper blocks at pack time, so the
+// backward sweep has the same shape).
 // Only the two lag-1 blocks are on the loop-carried chain: iteration k finishes step k with them and
 // accumulates the four older-neighbour blocks of step k+1 (software pipeline).
 //
@@ -23,8 +24,9 @@
 // SM; tools/bulk_probe.cu), so one copy per step would cap the step rate.  The factors are therefore
 // repacked once per factorisation into a COMPACT per-stripe stream -- the active rows of step 0, then
 // of step 1, ... ([row][plane], blocks row-major, row pitch = 16 mod 128 bytes) -- and the producer
-// moves one group of 4 steps per bulk copy into a 2-deep ring; off[k] (rows before step k) is a
-// small host-built table.  r is gathered with a register prefetch 4 steps ahead; the forward result
+// moves one group of kG = 2 steps per bulk copy into a ring of NS = 4 buffers, off the consumers' step
+// barrier (they wait on each group's full mbarrier and release buffers through named barriers); off[k]
+// (rows before step k) is a small host-built table.  r is gathered with a register prefetch 4 steps ahead; the forward result
 // y goes to a per-step scratch the backward sweep prefetches back; x goes straight to z at the box's
 // owned points (R_i^{0T}).  Source factor layout (precond.cu): plane p = slot*16 + row*4 + col,
 // position-minor with leading dimension ld; slots 0..5 lower, 6 diagonal (inverted), 7..12 upper.
