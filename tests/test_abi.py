@@ -195,3 +195,30 @@ def test_decompose_pencil_deals_whole_box_layers(lib, pz, py):
         tot_z[r // py] = loc.nsub[2]
         tot_y[r % py] = loc.nsub[1]
     assert sum(tot_z.values()) == nsz and sum(tot_y.values()) == nsy
+
+
+def test_decompose_pencil_rejects_bad_requests(lib):
+    """Host-only validation of pencil requests: more parts than box layers along an axis, a 2D grid, a
+    preconditioner a pencil does not support (AS needs a reverse halo exchange)."""
+    g = nks.make_grid((24, 20, 12), 0.25, (4, 2, 2), 2)
+    ras = nks.make_params(ni.model_default(), ni.solver_default(), nks.PC_RAS_BILU0)
+    with pytest.raises(nks.NKSError):
+        nks.decompose_pencil(g, ras, 0, 1, 3)              # 2 box layers along y over 3 parts
+    with pytest.raises(nks.NKSError):
+        nks.decompose_pencil(g, ras, 0, 5, 1)              # 4 box layers along z over 5 parts
+    with pytest.raises(nks.NKSError):
+        nks.decompose_pencil(nks.make_grid((16, 16), 0.25, (2, 2), 2), ras, 0, 1, 1)
+    as_ = nks.make_params(ni.model_default(), ni.solver_default(), nks.PC_AS_BILU0)
+    with pytest.raises(nks.NKSError):
+        nks.decompose_pencil(g, as_, 0, 2, 2)
+    loc = nks.decompose_pencil(g, ras, 3, 2, 2)             # rank 3 = (rz 1, ry 1)
+    assert (loc.z_offset, loc.y_offset) == (12, 10)
+
+
+def test_bench_pencil_grid_is_the_most_square_factorisation():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    assert [bench.pencil_grid(n) for n in (1, 2, 3, 4, 6, 8, 9, 16)] == \
+        [(1, 1), (1, 2), (1, 3), (2, 2), (2, 3), (2, 4), (3, 3), (4, 4)]
